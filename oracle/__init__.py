@@ -1,0 +1,253 @@
+"""CPU fp64 oracle for RCholeskyQR (Balabanov, arXiv 2210.09953, Algorithm 2).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  It shares no code with
+``paper_2210_09953_b200`` (the CUDA product path) and never imports it.
+
+The arithmetic lives in ``oracle/oracle.c`` (plain C, fp64, -ffp-contract=off); this module is
+ctypes marshalling plus the stability *metrics* the paper defines (PAPER.md:773, 797:
+cond(Q), ||I - (Theta Q)^T Theta Q||, column residuals), written with numpy/LAPACK.
+
+Parity status of each oracle function ("Oracle pins"):
+  philox4x32_10      pinned: Random123 known-answer vectors + ATen's independent Philox
+  ln32 / sincos2pi32 pinned: exhaustive 2^24-input comparison against fp64 libm
+  gauss4 / theta     pinned: moments, KS test vs N(0,1), E||Theta x||^2 = ||x||^2
+  sparse_col         pinned: structural invariants (one row per block, +-1/sqrt(zeta)), chi^2
+  sketch             pinned: exact rational Theta X on tiny inputs, n=1 closed form, linearity,
+                     partition invariance
+  householder        pinned: SPEC examples, LAPACK QR (sign-normalised), mpmath 50-digit QR
+  forward_subst      pinned: SPEC examples, R = I, scipy solve_triangular, Higham Thm 8.5 bound
+  factor             pinned: cond(Q) = cond(Theta U) identity, eq:main1 residual, metamorphic
+                     power-of-two scaling (bitwise)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+OK, E_INVALID, E_SHAPE, E_NONFINITE, E_SINGULAR, E_NOMEM = 0, 1, 2, 3, 4, 7
+GAUSSIAN, SPARSE_SIGN = 0, 1
+F64, F32 = 0, 1
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c into liboracle.so (gcc, -O2 -fopenmp -ffp-contract=off, no fast-math)."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        tmp = _LIB_PATH + ".tmp%d" % os.getpid()
+        cmd = ["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-fopenmp", "-ffp-contract=off",
+               "-fno-fast-math", "-Wall", "-o", tmp, _SRC, "-lm"]
+        subprocess.check_call(cmd)
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def _L():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            lib = ctypes.CDLL(_LIB_PATH)
+            P, I64, I32, U64, U32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_uint64, ctypes.c_uint32
+            lib.oracle_philox4x32_10.argtypes = [P, P, P]
+            lib.oracle_ln32.argtypes = [ctypes.c_float]
+            lib.oracle_ln32.restype = ctypes.c_float
+            lib.oracle_ln32_batch.argtypes = [P, P, I64]
+            lib.oracle_sincos2pi32_batch.argtypes = [P, P, P, I64]
+            lib.oracle_gauss4.argtypes = [U64, U64, U32, P]
+            lib.oracle_theta_gauss.argtypes = [U64, I32, U64, I32]
+            lib.oracle_theta_gauss.restype = ctypes.c_double
+            lib.oracle_theta_gauss_z.argtypes = [U64, I32, I64, I64, P]
+            lib.oracle_theta_sparse.argtypes = [U64, I32, I32, I64, I64, P, P]
+            lib.oracle_sketch.argtypes = [P, I32, I64, I32, I64, I64, I32, I32, I32, U64, P]
+            lib.oracle_sketch.restype = I32
+            lib.oracle_householder.argtypes = [P, I32, I32, P, P]
+            lib.oracle_householder.restype = I32
+            lib.oracle_forward_subst.argtypes = [P, I32, I64, I32, I64, P, P, I64]
+            lib.oracle_forward_subst.restype = I32
+            lib.oracle_factor.argtypes = [P, I32, I64, I32, I64, I64, I32, I32, I32, U64, P, I64, P, P, P]
+            lib.oracle_factor.restype = I32
+            lib.oracle_num_threads.restype = I32
+            lib.oracle_sketch_entry.argtypes = [P, I64, I64, I32, I32, I32, U64, I32]
+            lib.oracle_sketch_entry.restype = ctypes.c_double
+            _lib = lib
+    return _lib
+
+
+def _ptr(a):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+def _dtype_code(X):
+    if X.dtype == np.float64:
+        return F64
+    if X.dtype == np.float32:
+        return F32
+    raise TypeError("X must be float64 or float32")
+
+
+def num_threads() -> int:
+    return int(_L().oracle_num_threads())
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        super().__init__(f"oracle {where}: status {status}")
+        self.status = status
+
+
+# ---------------------------------------------------------------- Theta (reading A1-A4)
+def philox4x32_10(ctr, key) -> np.ndarray:
+    c = np.ascontiguousarray(ctr, dtype=np.uint32)
+    k = np.ascontiguousarray(key, dtype=np.uint32)
+    out = np.zeros(4, dtype=np.uint32)
+    _L().oracle_philox4x32_10(_ptr(c), _ptr(k), _ptr(out))
+    return out
+
+
+def ln32(a) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.float32)
+    out = np.empty_like(a)
+    _L().oracle_ln32_batch(_ptr(a), _ptr(out), a.size)
+    return out
+
+
+def sincos2pi32(b):
+    b = np.ascontiguousarray(b, dtype=np.float32)
+    s = np.empty_like(b)
+    c = np.empty_like(b)
+    _L().oracle_sincos2pi32_batch(_ptr(b), _ptr(s), _ptr(c), b.size)
+    return s, c
+
+
+def gauss4(seed: int, i: int, q: int) -> np.ndarray:
+    z = np.zeros(4, dtype=np.float32)
+    _L().oracle_gauss4(seed, i, q, _ptr(z))
+    return z
+
+
+def theta_gauss_z(seed: int, k: int, m: int, row_offset: int = 0) -> np.ndarray:
+    """Unscaled N(0,1) fp32 draws z_ri, shape (k, m), columns = global rows row_offset..+m."""
+    Z = np.empty((k, m), dtype=np.float32)
+    _L().oracle_theta_gauss_z(seed, k, row_offset, m, _ptr(Z))
+    return Z
+
+
+def theta_sparse(seed: int, k: int, zeta: int, m: int, row_offset: int = 0):
+    """Sparse-sign columns: rows (m, zeta) int32 and signs (m, zeta) int8."""
+    rows = np.empty((m, zeta), dtype=np.int32)
+    signs = np.empty((m, zeta), dtype=np.int8)
+    _L().oracle_theta_sparse(seed, k, zeta, row_offset, m, _ptr(rows), _ptr(signs))
+    return rows, signs
+
+
+def theta_dense(seed: int, k: int, m: int, sketch: int = GAUSSIAN, zeta: int = 8,
+                row_offset: int = 0) -> np.ndarray:
+    """Explicit fp64 Theta (k x m) -- for tiny test inputs only."""
+    if sketch == GAUSSIAN:
+        Z = theta_gauss_z(seed, k, m, row_offset).astype(np.float64)
+        return Z * (1.0 / np.sqrt(np.float64(k)))
+    rows, signs = theta_sparse(seed, k, zeta, m, row_offset)
+    T = np.zeros((k, m), dtype=np.float64)
+    v = 1.0 / np.sqrt(np.float64(zeta))
+    for i in range(m):
+        for t in range(zeta):
+            T[rows[i, t], i] = v if signs[i, t] > 0 else -v
+    return T
+
+
+# ---------------------------------------------------------------- Algorithm 2 steps
+def sketch(X: np.ndarray, k: int, sketch: int = GAUSSIAN, zeta: int = 8, seed: int = 0,
+           row_offset: int = 0) -> np.ndarray:
+    """Step 1, P = Theta X."""
+    X = np.ascontiguousarray(X)
+    m, n = X.shape
+    P = np.empty((k, n), dtype=np.float64)
+    st = _L().oracle_sketch(_ptr(X), _dtype_code(X), m, n, n, row_offset, k, sketch, zeta, seed, _ptr(P))
+    if st != OK:
+        raise OracleError(st, "sketch")
+    return P
+
+
+def sketch_entry(x_col: np.ndarray, r: int, k: int, sketch: int = GAUSSIAN, zeta: int = 8, seed: int = 0,
+                 row_offset: int = 0) -> float:
+    """P_rj = sum_i Theta_ri x_ij for one column x (fp64) -- sampled full-size sketch checks."""
+    x = np.ascontiguousarray(x_col, dtype=np.float64)
+    return float(_L().oracle_sketch_entry(_ptr(x), x.size, row_offset, k, sketch, zeta, seed, r))
+
+
+def householder(P: np.ndarray, want_S: bool = True):
+    """Step 2, [R, S] = QR(P) by Householder; diag(R) >= 0.
+
+    Returns (R, S, status); status E_SINGULAR is returned, not raised."""
+    P = np.ascontiguousarray(P, dtype=np.float64)
+    k, n = P.shape
+    R = np.empty((n, n), dtype=np.float64)
+    S = np.empty((k, n), dtype=np.float64) if want_S else None
+    st = _L().oracle_householder(_ptr(P), k, n, _ptr(R), _ptr(S))
+    if st not in (OK, E_SINGULAR):
+        raise OracleError(st, "householder")
+    return R, S, st
+
+
+def forward_subst(X: np.ndarray, R: np.ndarray) -> np.ndarray:
+    """Step 3, Q = X R^{-1} by row-wise forward substitution."""
+    X = np.ascontiguousarray(X)
+    R = np.ascontiguousarray(R, dtype=np.float64)
+    m, n = X.shape
+    Q = np.empty_like(X)
+    st = _L().oracle_forward_subst(_ptr(X), _dtype_code(X), m, n, n, _ptr(R), _ptr(Q), n)
+    if st != OK:
+        raise OracleError(st, "forward_subst")
+    return Q
+
+
+def factor(X: np.ndarray, k: int, sketch: int = GAUSSIAN, zeta: int = 8, seed: int = 0,
+           row_offset: int = 0, want_S: bool = True) -> dict:
+    """Whole Algorithm 2: returns dict(Q, R, P, S)."""
+    X = np.ascontiguousarray(X)
+    m, n = X.shape
+    Q = np.empty_like(X)
+    R = np.empty((n, n), dtype=np.float64)
+    P = np.empty((k, n), dtype=np.float64)
+    S = np.empty((k, n), dtype=np.float64) if want_S else None
+    st = _L().oracle_factor(_ptr(X), _dtype_code(X), m, n, n, row_offset, k, sketch, zeta, seed,
+                            _ptr(Q), n, _ptr(R), _ptr(P), _ptr(S))
+    if st != OK:
+        raise OracleError(st, "factor")
+    return {"Q": Q, "R": R, "P": P, "S": S}
+
+
+# ---------------------------------------------------------------- metrics
+def orth_defect(S: np.ndarray) -> float:
+    """||I - S^T S||_2 (fp64)."""
+    S = np.asarray(S, dtype=np.float64)
+    G = S.T @ S
+    return float(np.linalg.norm(np.eye(G.shape[0]) - G, 2))
+
+
+def cond(A: np.ndarray) -> float:
+    s = np.linalg.svd(np.asarray(A, dtype=np.float64), compute_uv=False)
+    return float(s[0] / s[-1]) if s[-1] > 0 else float("inf")
+
+
+def cond_from_gram(G: np.ndarray) -> float:
+    """cond(Q) from its fp64 Gram matrix Q^T Q (valid while cond(Q)^2 u << 1)."""
+    w = np.linalg.eigvalsh(np.asarray(G, dtype=np.float64))
+    return float(np.sqrt(w[-1] / w[0])) if w[0] > 0 else float("inf")
+
+
+def col_residual(X: np.ndarray, Q: np.ndarray, R: np.ndarray) -> float:
+    """max_j ||X_j - (Q R)_j|| / ||X_j||  (eq:main1)."""
+    Xd = np.asarray(X, dtype=np.float64)
+    E = Xd - np.asarray(Q, dtype=np.float64) @ R
+    return float(np.max(np.linalg.norm(E, axis=0) / np.linalg.norm(Xd, axis=0)))

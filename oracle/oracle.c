@@ -1,0 +1,466 @@
+/*
+ * oracle.c -- plain, slow, obviously-correct CPU fp64 oracle for the direct randomized
+ * Cholesky QR (RCholeskyQR, Algorithm 2 of Balabanov, arXiv 2210.09953).
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  The product path
+ * (paper_2210_09953_b200/) never imports, links or executes anything under oracle/, and
+ * this file shares no code, header, table or constant generator with it.
+ *
+ * What it computes (alg:RCQR):
+ *     1. P <- Theta X   oracle_sketch
+ *     2. [R, S] <- QR(P)   oracle_householder  (Householder)
+ *     3. Q <- X R^{-1}   oracle_forward_subst (forward substitution,
+ *                                                 PAPER.md:178, row-wise)
+ * Theta is defined normatively in DESIGN.md section "Theta specification" (readings A1-A4):
+ * Philox4x32-10 keyed by (seed, global row i, block q, domain), Box-Muller in fp32 with
+ * fixed polynomials, scaled by fl64(1/sqrt(k)) (Gaussian, "scaled by a factor
+ * sqrt(1/k)"), or an OSNAP-style sparse-sign map (BASELINE.json C4; reading A3).
+ *
+ * Precision: every step of the method is fp64 (PAPER.md:83, 406 -- minor operations in
+ * higher precision; reading A7: step 3 in fp64 rounded once to Q's dtype).  The only fp32
+ * arithmetic is inside the normative definition of Theta (the normal transform), which is
+ * written with explicit fmaf and compiled with -ffp-contract=off.
+ *
+ * Layouts: X (m x n, leading dim ldx), Q (m x n, ldq), P (k x n), R (n x n), S (k x n) are
+ * all ROW-MAJOR.  dtype 0 = fp64, 1 = fp32 for X and Q.
+ *
+ * Sketch accuracy (reading A15): the paper performs "random projections and low-dimensional
+ * operations" with a unit roundoff u_f lower than u (u_f = O(u/(mn)) for the
+ * sketch).  The oracle therefore evaluates every sketch sum with the compensated
+ * dot product Dot2 (Ogita, Rump, Oishi, SIAM J. Sci. Comput. 26(6), 2005: TwoProduct by fma +
+ * TwoSum), i.e. as if in twice the working precision, so that it is a reference for P rather
+ * than one more fp64 summation order.
+ *
+ * Determinism: the sketch sums fixed 65536-row blocks (independent of thread count) and adds
+ * the block partials in block order; Householder is serial; substitution is per row.
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+enum { OR_OK = 0, OR_E_INVALID = 1, OR_E_SHAPE = 2, OR_E_NONFINITE = 3, OR_E_SINGULAR = 4,
+       OR_E_NOMEM = 7 };
+enum { OR_GAUSSIAN = 0, OR_SPARSE_SIGN = 1 };
+#define OR_SKETCH_BLOCK 65536
+
+/* ------------------------------------------------------------------------------------------
+ * Philox4x32-10 (Salmon et al., SC'11; the generator BASELINE.json's north star names).
+ * One round: (hi0,lo0) = M0*c0, (hi1,lo1) = M1*c2;
+ *            c' = (hi1 ^ c1 ^ k0, lo1, hi0 ^ c3 ^ k1, lo0);   key bumped by (W0, W1) between
+ * rounds.  10 rounds.
+ * ---------------------------------------------------------------------------------------- */
+void oracle_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+    const uint32_t M0 = 0xD2511F53u, M1 = 0xCD9E8D57u, W0 = 0x9E3779B9u, W1 = 0xBB67AE85u;
+    uint32_t c[4] = {ctr_in[0], ctr_in[1], ctr_in[2], ctr_in[3]};
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int round = 0; round < 10; ++round) {
+        if (round > 0) { k0 += W0; k1 += W1; }
+        uint64_t p0 = (uint64_t)M0 * c[0];
+        uint64_t p1 = (uint64_t)M1 * c[2];
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c[1] ^ k0, n1 = lo1, n2 = hi0 ^ c[3] ^ k1, n3 = lo0;
+        c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+    }
+    out[0] = c[0]; out[1] = c[1]; out[2] = c[2]; out[3] = c[3];
+}
+
+/* Counter layout (reading A2): ctr = (lo32(i), hi32(i), q, domain), key = (lo32(seed), hi32(seed)). */
+static void philox_for(uint64_t seed, uint64_t i, uint32_t q, uint32_t domain, uint32_t out[4]) {
+    uint32_t ctr[4] = {(uint32_t)i, (uint32_t)(i >> 32), q, domain};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    oracle_philox4x32_10(ctr, key, out);
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Normative fp32 normal transform (reading A1).  All operations are single correctly-rounded
+ * IEEE fp32 operations in the order written.
+ * ---------------------------------------------------------------------------------------- */
+static float u32_as_f32(uint32_t u) { float f; memcpy(&f, &u, 4); return f; }
+static uint32_t f32_as_u32(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
+
+/* natural log for a in [2^-24, 1]: a = 2^e f, f in [sqrt(1/2), sqrt(2)); t = (f-1)/(f+1);
+ * ln f = 2t + t^3 (2/3 + t^2 (2/5 + t^2 (2/7 + t^2 2/9)))  (atanh series);
+ * ln a = e*ln2_hi + (e*ln2_lo + ln f). */
+float oracle_ln32(float a) {
+    uint32_t bits = f32_as_u32(a);
+    int e = (int)(bits >> 23) - 127;
+    float f = u32_as_f32((bits & 0x007FFFFFu) | 0x3F800000u);
+    if (f > 0x1.6a09e6p+0f) { f = f * 0.5f; e = e + 1; }
+    float num = f - 1.0f;
+    float den = f + 1.0f;
+    float t = num / den;
+    float t2 = t * t;
+    float p = 0x1.c71c72p-3f;                 /* fl32(2/9) */
+    p = fmaf(p, t2, 0x1.24924ap-2f);          /* fl32(2/7) */
+    p = fmaf(p, t2, 0x1.99999ap-2f);          /* fl32(2/5) */
+    p = fmaf(p, t2, 0x1.555556p-1f);          /* fl32(2/3) */
+    float t3 = t * t2;
+    float lnf = fmaf(t3, p, 2.0f * t);
+    float ef = (float)e;
+    float r = fmaf(ef, 0x1.7f7d1cp-20f, lnf); /* ln2_lo */
+    r = fmaf(ef, 0x1.62e4p-1f, r);            /* ln2_hi (16 significant bits: e*ln2_hi exact) */
+    return r;
+}
+
+/* sin(2 pi b), cos(2 pi b) for b in [0,1): x = 4b, n = floor(x + 1/2), r = x - n in [-1/2,1/2),
+ * angle = n*pi/2 + (pi/2) r; Taylor polynomials of sin/cos((pi/2) r). */
+void oracle_sincos2pi32(float b, float* s_out, float* c_out) {
+    float x = 4.0f * b;
+    float nf = floorf(x + 0.5f);
+    float r = x - nf;
+    int n = ((int)nf) & 3;
+    float r2 = r * r;
+    float ps = 0x1.507834p-13f;
+    ps = fmaf(ps, r2, -0x1.32d2ccp-8f);
+    ps = fmaf(ps, r2, 0x1.466bc6p-4f);
+    ps = fmaf(ps, r2, -0x1.4abbcep-1f);
+    ps = fmaf(ps, r2, 0x1.921fb6p+0f);
+    float s = ps * r;
+    float pc = -0x1.a6d1f2p-16f;
+    pc = fmaf(pc, r2, 0x1.e1f506p-11f);
+    pc = fmaf(pc, r2, -0x1.55d3c8p-6f);
+    pc = fmaf(pc, r2, 0x1.03c1f0p-2f);
+    pc = fmaf(pc, r2, -0x1.3bd3ccp+0f);
+    float c = fmaf(pc, r2, 1.0f);
+    float so, co;
+    switch (n) {
+        case 0: so = s; co = c; break;
+        case 1: so = c; co = -s; break;
+        case 2: so = -s; co = -c; break;
+        default: so = -c; co = s; break;
+    }
+    *s_out = so; *c_out = co;
+}
+
+/* Four N(0,1) draws z[0..3] for Theta rows 4q..4q+3 at global X-row i (domain 1). */
+void oracle_gauss4(uint64_t seed, uint64_t i, uint32_t q, float z[4]) {
+    uint32_t w[4];
+    philox_for(seed, i, q, 1u, w);
+    for (int p = 0; p < 2; ++p) {
+        uint32_t wa = w[2 * p], wb = w[2 * p + 1];
+        float ua = (float)((wa >> 8) + 1u) * 0x1p-24f;   /* (0, 1] */
+        float ub = (float)(wb >> 8) * 0x1p-24f;          /* [0, 1) */
+        float rho = sqrtf(-2.0f * oracle_ln32(ua));
+        float s, c;
+        oracle_sincos2pi32(ub, &s, &c);
+        z[2 * p] = rho * c;
+        z[2 * p + 1] = rho * s;
+    }
+}
+
+/* Gaussian Theta entry (fp64): Theta_ri = (double) z_ri * fl64(1/sqrt(k)). */
+double oracle_theta_gauss(uint64_t seed, int k, uint64_t i, int r) {
+    float z[4];
+    oracle_gauss4(seed, i, (uint32_t)(r / 4), z);
+    double sk = 1.0 / sqrt((double)k);
+    return (double)z[r % 4] * sk;
+}
+
+/* Sparse-sign column i of Theta (reading A3): zeta blocks of beta = k/zeta rows; half-word t of
+ * Philox call (i, q = t/8, domain 2) picks row t*beta + ((h & 0x7FFF) * beta >> 15) and sign
+ * (h >> 15) ? -1 : +1.  Value +-1/sqrt(zeta). */
+void oracle_sparse_col(uint64_t seed, int k, int zeta, uint64_t i, int32_t* rows, int8_t* signs) {
+    int beta = k / zeta;
+    uint32_t w[4];
+    for (int t = 0; t < zeta; ++t) {
+        if (t % 8 == 0) philox_for(seed, i, (uint32_t)(t / 8), 2u, w);
+        uint32_t word = w[(t % 8) / 2];
+        uint32_t h = (t % 2 == 0) ? (word & 0xFFFFu) : (word >> 16);
+        rows[t] = t * beta + (int32_t)(((h & 0x7FFFu) * (uint32_t)beta) >> 15);
+        signs[t] = (h >> 15) ? (int8_t)-1 : (int8_t)1;
+    }
+}
+
+/* ---------------- batch helpers for the tests ---------------- */
+void oracle_ln32_batch(const float* a, float* out, int64_t n) {
+    for (int64_t t = 0; t < n; ++t) out[t] = oracle_ln32(a[t]);
+}
+void oracle_sincos2pi32_batch(const float* b, float* s, float* c, int64_t n) {
+    for (int64_t t = 0; t < n; ++t) oracle_sincos2pi32(b[t], &s[t], &c[t]);
+}
+/* Z: k x m row-major, Z[r*m + (i-row_offset)] = z_ri (unscaled N(0,1) draw, fp32). */
+void oracle_theta_gauss_z(uint64_t seed, int k, int64_t row_offset, int64_t m, float* Z) {
+    #pragma omp parallel for schedule(static)
+    for (int64_t ii = 0; ii < m; ++ii) {
+        float z[4];
+        for (int q = 0; q < (k + 3) / 4; ++q) {
+            oracle_gauss4(seed, (uint64_t)(row_offset + ii), (uint32_t)q, z);
+            for (int t = 0; t < 4 && 4 * q + t < k; ++t) Z[(int64_t)(4 * q + t) * m + ii] = z[t];
+        }
+    }
+}
+/* rows/signs: m x zeta row-major. */
+void oracle_theta_sparse(uint64_t seed, int k, int zeta, int64_t row_offset, int64_t m,
+                         int32_t* rows, int8_t* signs) {
+    #pragma omp parallel for schedule(static)
+    for (int64_t ii = 0; ii < m; ++ii)
+        oracle_sparse_col(seed, k, zeta, (uint64_t)(row_offset + ii), rows + ii * zeta,
+                          signs + ii * zeta);
+}
+
+static double load_x(const void* X, int dtype, int64_t idx) {
+    return dtype == 0 ? ((const double*)X)[idx] : (double)((const float*)X)[idx];
+}
+
+/* Dot2 accumulator (Ogita-Rump-Oishi 2005, Alg. 5.3): s + c carries the sum of a*b terms.
+ * TwoProduct: p = fl(a b), e = fma(a, b, -p) exact.  TwoSum: t = s + p, z = t - s,
+ * err = (s - (t - z)) + (p - z) exact. */
+static void dot2_add(double* s, double* c, double a, double b) {
+    double p = a * b;
+    double e = fma(a, b, -p);
+    double t = *s + p;
+    double z = t - *s;
+    double err = (*s - (t - z)) + (p - z);
+    *s = t;
+    *c += err + e;
+}
+static void sum2_add(double* s, double* c, double v) {
+    double t = *s + v;
+    double z = t - *s;
+    double err = (*s - (t - z)) + (v - z);
+    *s = t;
+    *c += err;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Step 1: P = Theta X.  P_rj = sum_i Theta_ri x_ij, fp64, i ascending inside
+ * fixed 65536-row blocks, block partials added in block order.  Theta is keyed by the GLOBAL
+ * row index row_offset + i (so a row-partitioned X gives the same Theta for any partition).
+ * ---------------------------------------------------------------------------------------- */
+int oracle_sketch(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset,
+                  int k, int sketch, int zeta, uint64_t seed, double* P) {
+    if (!P || (m > 0 && !X) || n < 1 || k < 1 || ldx < n || m < 0) return OR_E_INVALID;
+    if (sketch == OR_SPARSE_SIGN && (zeta < 1 || zeta > k || k % zeta != 0)) return OR_E_SHAPE;
+    int64_t nb = (m + OR_SKETCH_BLOCK - 1) / OR_SKETCH_BLOCK;
+    size_t kn = (size_t)k * n;
+    double* part = (double*)calloc((size_t)(nb > 0 ? nb : 1) * kn, sizeof(double));
+    double* comp = (double*)calloc((size_t)(nb > 0 ? nb : 1) * kn, sizeof(double));
+    if (!part || !comp) { free(part); free(comp); return OR_E_NOMEM; }
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t b = 0; b < nb; ++b) {
+        double* Pb = part + (size_t)b * kn;
+        double* Cb = comp + (size_t)b * kn;
+        double* th = (double*)malloc(sizeof(double) * (size_t)k);
+        int32_t* rows = (int32_t*)malloc(sizeof(int32_t) * (size_t)(zeta > 0 ? zeta : 1));
+        int8_t* sg = (int8_t*)malloc((size_t)(zeta > 0 ? zeta : 1));
+        double sk = 1.0 / sqrt((double)k);
+        double sz = zeta > 0 ? 1.0 / sqrt((double)zeta) : 0.0;
+        int64_t i0 = b * OR_SKETCH_BLOCK, i1 = i0 + OR_SKETCH_BLOCK < m ? i0 + OR_SKETCH_BLOCK : m;
+        for (int64_t i = i0; i < i1; ++i) {
+            uint64_t gi = (uint64_t)(row_offset + i);
+            if (sketch == OR_GAUSSIAN) {
+                float z[4];
+                for (int q = 0; q < (k + 3) / 4; ++q) {
+                    oracle_gauss4(seed, gi, (uint32_t)q, z);
+                    for (int t = 0; t < 4 && 4 * q + t < k; ++t) th[4 * q + t] = (double)z[t] * sk;
+                }
+                for (int r = 0; r < k; ++r) {
+                    double* prow = Pb + (size_t)r * n;
+                    double* crow = Cb + (size_t)r * n;
+                    for (int j = 0; j < n; ++j) dot2_add(&prow[j], &crow[j], th[r], load_x(X, dtype, i * ldx + j));
+                }
+            } else {
+                oracle_sparse_col(seed, k, zeta, gi, rows, sg);
+                for (int t = 0; t < zeta; ++t) {
+                    double theta = sg[t] > 0 ? sz : -sz;
+                    double* prow = Pb + (size_t)rows[t] * n;
+                    double* crow = Cb + (size_t)rows[t] * n;
+                    for (int j = 0; j < n; ++j) dot2_add(&prow[j], &crow[j], theta, load_x(X, dtype, i * ldx + j));
+                }
+            }
+        }
+        free(th); free(rows); free(sg);
+    }
+    for (size_t t = 0; t < kn; ++t) {
+        double s = 0.0, c = 0.0;
+        for (int64_t b = 0; b < nb; ++b) {
+            sum2_add(&s, &c, part[(size_t)b * kn + t]);
+            c += comp[(size_t)b * kn + t];
+        }
+        P[t] = s + c;
+    }
+    free(part);
+    free(comp);
+    for (size_t t = 0; t < kn; ++t)
+        if (!isfinite(P[t])) return OR_E_NONFINITE;
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Step 2: [R, S] = QR(P), unblocked textbook Householder.
+ * For j = 0..n-1 on the working copy A (= P):
+ *   alpha = ||A[j:,j]||_2; v = A[j:,j]; v_0 += sign(v_0) alpha  (sign(0) = +1);
+ *   H_j = I - v v^T / (alpha |v_0|);  A[j:, l] -= v (v^T A[j:, l]) / (alpha |v_0|), l > j;
+ *   R_jj = -sign(x_0) alpha, R_jl = A[j, l].
+ * Sign convention (reading A5): rows of R with R_jj < 0 are negated (and the matching columns
+ * of S), so diag(R) >= 0.  S = H_0 ... H_{n-1} [I_n; 0] (Alg. 2's S).
+ * Returns OR_E_SINGULAR if some R_jj == 0 or is non-finite (reading A6).
+ * ---------------------------------------------------------------------------------------- */
+int oracle_householder(const double* P, int k, int n, double* R, double* S) {
+    if (!P || !R || n < 1 || k < n) return k < n ? OR_E_SHAPE : OR_E_INVALID;
+    double* A = (double*)malloc(sizeof(double) * (size_t)k * n);      /* column-major copy */
+    double* V = (double*)calloc((size_t)k * n, sizeof(double));       /* reflectors, col-major */
+    double* tau = (double*)calloc((size_t)n, sizeof(double));         /* 1/(alpha |v0|) or 0 */
+    if (!A || !V || !tau) { free(A); free(V); free(tau); return OR_E_NOMEM; }
+    for (int i = 0; i < k; ++i)
+        for (int j = 0; j < n; ++j) A[(size_t)j * k + i] = P[(size_t)i * n + j];
+    memset(R, 0, sizeof(double) * (size_t)n * n);
+    int status = OR_OK;
+    for (int j = 0; j < n; ++j) {
+        double* a = A + (size_t)j * k;
+        double ss = 0.0;
+        for (int i = j; i < k; ++i) ss += a[i] * a[i];
+        double alpha = sqrt(ss);
+        double* v = V + (size_t)j * k;
+        if (alpha == 0.0) {               /* zero column: no reflector, R_jj = 0 */
+            tau[j] = 0.0;
+            R[(size_t)j * n + j] = 0.0;
+            for (int l = j + 1; l < n; ++l) R[(size_t)j * n + l] = A[(size_t)l * k + j];
+            status = OR_E_SINGULAR;
+            continue;
+        }
+        double sgn = a[j] >= 0.0 ? 1.0 : -1.0;
+        for (int i = j; i < k; ++i) v[i] = a[i];
+        v[j] = a[j] + sgn * alpha;
+        double beta = 1.0 / (alpha * fabs(v[j]));
+        tau[j] = beta;
+        for (int l = j + 1; l < n; ++l) {
+            double* c = A + (size_t)l * k;
+            double w = 0.0;
+            for (int i = j; i < k; ++i) w += v[i] * c[i];
+            w *= beta;
+            for (int i = j; i < k; ++i) c[i] -= v[i] * w;
+        }
+        R[(size_t)j * n + j] = -sgn * alpha;
+        for (int l = j + 1; l < n; ++l) R[(size_t)j * n + l] = A[(size_t)l * k + j];
+    }
+    /* S = H_0 H_1 ... H_{n-1} E, E = [I_n; 0], applied right-to-left. */
+    if (S) {
+        double* E = (double*)calloc((size_t)k * n, sizeof(double));   /* column-major k x n */
+        if (!E) { free(A); free(V); free(tau); return OR_E_NOMEM; }
+        for (int j = 0; j < n; ++j) E[(size_t)j * k + j] = 1.0;
+        for (int j = n - 1; j >= 0; --j) {
+            if (tau[j] == 0.0) continue;
+            const double* v = V + (size_t)j * k;
+            for (int l = 0; l < n; ++l) {
+                double* c = E + (size_t)l * k;
+                double w = 0.0;
+                for (int i = j; i < k; ++i) w += v[i] * c[i];
+                w *= tau[j];
+                for (int i = j; i < k; ++i) c[i] -= v[i] * w;
+            }
+        }
+        for (int i = 0; i < k; ++i)
+            for (int j = 0; j < n; ++j) S[(size_t)i * n + j] = E[(size_t)j * k + i];
+        free(E);
+    }
+    for (int j = 0; j < n; ++j) {
+        double d = R[(size_t)j * n + j];
+        if (d < 0.0) {
+            for (int l = j; l < n; ++l) R[(size_t)j * n + l] = -R[(size_t)j * n + l];
+            if (S) for (int i = 0; i < k; ++i) S[(size_t)i * n + j] = -S[(size_t)i * n + j];
+        }
+        d = R[(size_t)j * n + j];
+        if (d == 0.0 || !isfinite(d)) status = OR_E_SINGULAR;
+    }
+    free(A); free(V); free(tau);
+    return status;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Step 3: Q = X R^{-1} by forward substitution, row by row:
+ *   q_ij = (x_ij - sum_{l<j, ascending} q_il R_lj) / R_jj  in fp64, rounded once to Q's dtype.
+ * ---------------------------------------------------------------------------------------- */
+int oracle_forward_subst(const void* X, int dtype, int64_t m, int n, int64_t ldx,
+                         const double* R, void* Q, int64_t ldq) {
+    if (!R || (m > 0 && (!X || !Q)) || n < 1 || ldx < n || ldq < n || m < 0) return OR_E_INVALID;
+    for (int j = 0; j < n; ++j) {
+        double d = R[(size_t)j * n + j];
+        if (d == 0.0 || !isfinite(d)) return OR_E_SINGULAR;
+    }
+    #pragma omp parallel
+    {
+        double* q = (double*)malloc(sizeof(double) * (size_t)n);
+        #pragma omp for schedule(static)
+        for (int64_t i = 0; i < m; ++i) {
+            for (int j = 0; j < n; ++j) {
+                double s = load_x(X, dtype, i * ldx + j);
+                for (int l = 0; l < j; ++l) s -= q[l] * R[(size_t)l * n + j];
+                q[j] = s / R[(size_t)j * n + j];
+            }
+            if (dtype == 0) {
+                for (int j = 0; j < n; ++j) ((double*)Q)[i * ldq + j] = q[j];
+            } else {
+                for (int j = 0; j < n; ++j) ((float*)Q)[i * ldq + j] = (float)q[j];
+            }
+        }
+        free(q);
+    }
+    return OR_OK;
+}
+
+/* Whole Algorithm 2 on one row block (single process).  P (k x n) and S (k x n) optional. */
+int oracle_factor(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset,
+                  int k, int sketch, int zeta, uint64_t seed, void* Q, int64_t ldq, double* R,
+                  double* P_out, double* S_out) {
+    if (k < n) return OR_E_SHAPE;
+    double* P = P_out ? P_out : (double*)malloc(sizeof(double) * (size_t)k * n);
+    if (!P) return OR_E_NOMEM;
+    int st = oracle_sketch(X, dtype, m, n, ldx, row_offset, k, sketch, zeta, seed, P);
+    if (st == OR_OK) st = oracle_householder(P, k, n, R, S_out);
+    if (st == OR_OK) st = oracle_forward_subst(X, dtype, m, n, ldx, R, Q, ldq);
+    if (!P_out) free(P);
+    return st;
+}
+
+/* One sketch entry P_rj = sum_i Theta_ri x_i for a single column x (m fp64 values), in the same
+ * fixed-block order as oracle_sketch -- used to check sampled entries of full-size sketches. */
+double oracle_sketch_entry(const double* x, int64_t m, int64_t row_offset, int k, int sketch, int zeta,
+                           uint64_t seed, int r) {
+    int64_t nb = (m + OR_SKETCH_BLOCK - 1) / OR_SKETCH_BLOCK;
+    double* part = (double*)calloc((size_t)(nb > 0 ? 2 * nb : 2), sizeof(double));
+    if (!part) return NAN;
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t b = 0; b < nb; ++b) {
+        int32_t rows[64];
+        int8_t sg[64];
+        double acc = 0.0, cmp = 0.0;
+        double sk = 1.0 / sqrt((double)k), sz = zeta > 0 ? 1.0 / sqrt((double)zeta) : 0.0;
+        int64_t i0 = b * OR_SKETCH_BLOCK, i1 = i0 + OR_SKETCH_BLOCK < m ? i0 + OR_SKETCH_BLOCK : m;
+        for (int64_t i = i0; i < i1; ++i) {
+            uint64_t gi = (uint64_t)(row_offset + i);
+            if (sketch == OR_GAUSSIAN) {
+                float z[4];
+                oracle_gauss4(seed, gi, (uint32_t)(r / 4), z);
+                dot2_add(&acc, &cmp, (double)z[r % 4] * sk, x[i]);
+            } else {
+                oracle_sparse_col(seed, k, zeta, gi, rows, sg);
+                for (int t = 0; t < zeta && t < 64; ++t)
+                    if (rows[t] == r) dot2_add(&acc, &cmp, sg[t] > 0 ? sz : -sz, x[i]);
+            }
+        }
+        part[2 * b] = acc;
+        part[2 * b + 1] = cmp;
+    }
+    double s = 0.0, c = 0.0;
+    for (int64_t b = 0; b < nb; ++b) {
+        sum2_add(&s, &c, part[2 * b]);
+        c += part[2 * b + 1];
+    }
+    free(part);
+    return s + c;
+}
+
+int oracle_num_threads(void) {
+#ifdef _OPENMP
+    return omp_get_max_threads();
+#else
+    return 1;
+#endif
+}
