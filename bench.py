@@ -1,0 +1,345 @@
+#!/usr/bin/env python
+"""Benchmark: RandCholQR factor throughput (GB/s of X, rows/s) on B200 (BASELINE.json metric).
+
+One step = one whole Algorithm 2 factorization (sketch + reduce [+ all-reduce] + Householder QR +
+R^-1 + tall solve) of the workload's X, inputs resident in HBM.  Default workload at N=1 is
+BASELINE.json configs[1] (C2: m=2^20, n=100, k=200, Gaussian, fp32 X, cond 1e5).  With N GPUs
+(torchrun, one process per GPU) each rank factors its own C2-sized row block of a (N*2^20) x 100
+X with one NCCL all-reduce of the 200 x 100 sketch ("weak" scaling); --config C3/C4/C5 instead
+row-partitions the full BASELINE matrix ("strong").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+DMMA_PEAK_TFLOPS = 37.2   # derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz
+L2_BYTES = 126 * 2**20
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """SM clocks + throttle reasons sampled with NVML during the timed region."""
+
+    def __init__(self, dev_index: int):
+        self.samples, self.reasons, self._stop = [], set(), threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(dev_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # noqa: BLE001
+            self._nv = None
+
+    def _run(self):
+        nv = self._nv
+        names = {
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for k, bit in names.items():
+                    if r & bit:
+                        self.reasons.add(k)
+            except Exception:  # noqa: BLE001
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self._nv:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._nv:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _workload(cfg_name: str, ws: int, rank: int):
+    cfg = synth.config(cfg_name)
+    if cfg_name in ("C1", "C2"):           # single-GPU configs: weak scaling, one C2 block per rank
+        m_local, m_global, ro, scaling = cfg["m"], cfg["m"] * ws, rank * cfg["m"], "weak"
+    else:                                  # BASELINE multi-GPU configs: row-partition the full X
+        m_global = cfg["m"]
+        base, rem = divmod(m_global, ws)
+        m_local = base + (1 if rank < rem else 0)
+        ro = rank * base + min(rank, rem)
+        scaling = "strong"
+    return cfg, m_local, m_global, ro, scaling
+
+
+def _cpu_sample_rate(X_dev, cfg, target_s: float):
+    """Time the oracle (as it stands, all host cores) on a bounded leading sample of X."""
+    import oracle
+    so = oracle.GAUSSIAN if cfg["sketch"] == "gaussian" else oracle.SPARSE_SIGN
+    m = X_dev.shape[0]
+    rows = min(m, 4096)
+    while True:
+        Xs = X_dev[:rows].cpu().numpy()
+        t0 = time.perf_counter()
+        oracle.factor(Xs, cfg["k"], sketch=so, zeta=cfg["nnz"], want_S=False)
+        dt = time.perf_counter() - t0
+        if dt >= target_s * 0.5 or rows >= m:
+            return rows, dt, oracle.num_threads()
+        rows = min(m, int(rows * max(2.0, 0.8 * target_s / max(dt, 1e-3))))
+
+
+def run_reference(args):
+    """--impl reference: the CPU fp64 oracle timed as it stands (this tier's reference arm)."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return 0
+    import numpy as np
+    import oracle
+    cfg = synth.config(args.config)
+    so = oracle.GAUSSIAN if cfg["sketch"] == "gaussian" else oracle.SPARSE_SIGN
+    s_x = 8 if cfg["dtype"] == "f64" else 4
+    per_step_s = max(1.0, 150.0 / (args.steps + args.warmup))
+    # calibrate a sample size on the leading rows of the workload's X
+    rows = 4096
+    while True:
+        X = synth.make_X(rows, cfg["n"], cfg["log10_cond"], cfg["dtype"])
+        t0 = time.perf_counter()
+        oracle.factor(X, cfg["k"], sketch=so, zeta=cfg["nnz"], want_S=False)
+        dt = time.perf_counter() - t0
+        if dt >= 0.5 * per_step_s or rows >= cfg["m"]:
+            break
+        rows = min(cfg["m"], int(rows * max(2.0, 0.8 * per_step_s / max(dt, 1e-3))))
+    X = synth.make_X(rows, cfg["n"], cfg["log10_cond"], cfg["dtype"])
+    for _ in range(args.warmup):
+        oracle.factor(X, cfg["k"], sketch=so, zeta=cfg["nnz"], want_S=False)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.factor(X, cfg["k"], sketch=so, zeta=cfg["nnz"], want_S=False)
+    el = time.perf_counter() - t0
+    ms = el / args.steps * 1e3
+    gbs = rows * cfg["n"] * s_x / (ms * 1e-3) / 1e9
+    cores = oracle.num_threads()
+    sample = f"{rows} leading rows of {args.config} (m={cfg['m']}) per step, oracle.factor fp64 C/OpenMP"
+    line = {"metric": "RandCholQR factor throughput (GB/s of X)", "value": gbs, "unit": "GB/s",
+            "impl": "reference", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "rows_per_s": rows / (ms * 1e-3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "m": rows, "n": cfg["n"], "k": cfg["k"], "sketch": cfg["sketch"],
+                       "x_dtype": cfg["dtype"]},
+            "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2210_09953_b200 as rcq
+
+    ws, rank, local = _dist()
+    if ws != args.gpus and "WORLD_SIZE" in os.environ:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={ws}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    comm = None
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        obj = [rcq.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        comm = rcq.comm_create(obj[0], ws, rank, local)
+
+    cfg, m_local, m_global, ro, scaling = _workload(args.config, ws, rank)
+    n, k, dt = cfg["n"], cfg["k"], cfg["dtype"]
+    s_x = 8 if dt == "f64" else 4
+    # each rank generates exactly its own rows of the global X (reproducible per row range)
+    X = synth.make_X_torch(m_local, n, cfg["log10_cond"], dt, seed=synth.X_SEED, device=dev, row_start=ro)
+    plan = rcq.RCholQR(n=n, k=k, dtype=X.dtype, sketch=cfg["sketch"], nnz_per_col=cfg["nnz"], seed=synth.THETA_SEED,
+                       device=local, comm=comm)
+    Q = torch.empty_like(X)
+    R = torch.empty((n, n), dtype=torch.float64, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        plan.factor(X, row_offset=ro, Q=Q, R=R, stream=stream, sync=False)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    st = plan.query_status()
+    if st != rcq.OK:
+        raise rcq.RCholQRError(st, "warm-up factor")
+
+    # ---- timed region (device events on the launching stream; inputs > L2, no flush needed)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    ms_local = e0.elapsed_time(e1) / args.steps
+    st = plan.query_status()
+    if st != rcq.OK:
+        raise rcq.RCholQRError(st, "timed factor")
+    t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+
+    # ---- per-kernel times (library-recorded CUDA events on the same stream), separate pass
+    plan.set_timing(True)
+    per = {}
+    for _ in range(max(3, min(args.steps, 20))):
+        step()
+        plan.query_status()
+        for kk, v in plan.last_timings().items():
+            per.setdefault(kk, []).append(v)
+    plan.set_timing(False)
+    per_ms = {kk: statistics.median(v) for kk, v in per.items()}
+
+    # ---- end-to-end through the public API with host buffers (H2D + D2H inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        Xh = X.cpu().pin_memory()
+        Qh = torch.empty_like(Xh).pin_memory()
+        Rh = torch.empty((n, n), dtype=torch.float64).pin_memory()
+        plan.factor_host(Xh, row_offset=ro, Q_host=Qh, R_host=Rh, stream=stream)
+        ke = max(2, min(args.steps, 10))
+        barrier()
+        h0, h1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        h0.record(stream)
+        for _ in range(ke):
+            plan.factor_host(Xh, row_offset=ro, Q_host=Qh, R_host=Rh, stream=stream)
+        h1.record(stream)
+        barrier()
+        te = torch.tensor([h0.elapsed_time(h1) / ke], dtype=torch.float64, device=dev)
+        if ws > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_ms = float(te.item())
+        e2e = {"value": m_global * n * s_x / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": m_local * n * s_x, "d2h_bytes_per_step": m_local * n * s_x + n * n * 8}
+        del Xh, Qh
+
+    # ---- roofline of the dominant kernel (the Gaussian sketch: FP64 DMMA-bound)
+    gbs = m_global * n * s_x / (ms * 1e-3) / 1e9
+    peaks = _peaks()
+    hbm = peaks.get("hbm_gbs", 6545.0)
+    if cfg["sketch"] == "gaussian":
+        flops = 2.0 * k * m_local * n
+        ach = flops / (per_ms["sketch"] * 1e-3) / 1e12
+        roof = {"kernel": "sketch_gauss_kernel", "bound": "tensor", "achieved": ach, "peak": DMMA_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
+                "peak_source": "derived FP64 DMMA peak (148 SM x 64 FMA/clk x 2 x 1.965 GHz); "
+                               "microbenchmark 37.0 (profiles/peaks_r1.jsonl)",
+                "algorithmic": f"2*k*m*n = {flops:.4g} flop per launch", "traffic": None}
+    else:
+        byts = m_local * n * s_x
+        ach = byts / (per_ms["sketch"] * 1e-3) / 1e9
+        roof = {"kernel": "sketch_sparse_kernel", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                "frac": ach / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                "algorithmic": f"m*n*s_x = {byts:.4g} B per launch", "traffic": None}
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            tr = json.load(f).get(args.config)
+            if tr:
+                roof["traffic"] = tr
+    except OSError:
+        pass
+    # north-star roofline for the whole factorization
+    t_hbm = 3.0 * m_local * n * s_x / (hbm * 1e9)
+    t_flop = m_local * n * n / (DMMA_PEAK_TFLOPS * 1e12)
+    ns = {"t_hbm_ms": t_hbm * 1e3, "t_solve_fp64_ms": t_flop * 1e3, "roofline_ms": max(t_hbm, t_flop) * 1e3,
+          "frac": max(t_hbm, t_flop) * 1e3 / ms,
+          "sketch_inclusive_roofline_ms": max(t_hbm, (m_local * n * n + 2.0 * k * m_local * n) /
+                                               (DMMA_PEAK_TFLOPS * 1e12)) * 1e3}
+
+    line = {"metric": "RandCholQR factor throughput (GB/s of X)", "value": gbs, "unit": "GB/s",
+            "rows_per_s": m_global / (ms * 1e-3), "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": args.config, "m_global": m_global, "m_local": m_local, "n": n, "k": k,
+                       "sketch": cfg["sketch"], "x_dtype": dt, "cond": 10.0 ** cfg["log10_cond"],
+                       "parallelism": f"row-partition x{ws}, 1 all-reduce",
+                       "l2": f"inputs larger than L2 (X = {m_local * n * s_x / 2**20:.0f} MiB > 126 MiB), no flush"},
+            "per_kernel_ms": per_ms, "roofline": roof, "northstar_roofline": ns,
+            "gpu_launches": plan.launches_per_factor(m_local) * args.steps,
+            "clocks": clk.summary(), "e2e": e2e}
+
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        rows, dt_s, cores = _cpu_sample_rate(X, cfg, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": rows * n * s_x / dt_s / 1e9, "unit": "GB/s", "cores": cores,
+                                "kind": "oracle", "seconds": dt_s,
+                                "sample": f"oracle.factor on the leading {rows} rows of the same X"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if comm is not None:
+        rcq.comm_destroy(comm)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,154 @@
+/*
+ * rcholqr.h -- C ABI of the B200 (sm_100a) direct randomized Cholesky QR library.
+ *
+ * Method: RCholeskyQR, Algorithm 2 of O. Balabanov, "Randomized Cholesky QR factorizations",
+ * arXiv 2210.09953:
+ *     1. P <- Theta X  sketch, fp64 accumulation
+ *     2. [R, S] <- QR(P)  fp64 Householder
+ *     3. Q <- X R^{-1}  tall triangular solve
+ * Multi-GPU ("only one global synchronization", reduction operator = addition):
+ * X is row-partitioned, each rank sketches its rows with Theta keyed by the GLOBAL row index,
+ * one in-place NCCL all-reduce (sum) of the k x n sketch, R computed redundantly on every rank,
+ * Q solved locally.
+ *
+ * Conventions (all entry points):
+ *   - C linkage, no exceptions cross the boundary; every call returns an rcholqr_status.
+ *   - Matrices are ROW-MAJOR with an explicit leading dimension (elements, >= number of columns).
+ *     X and Q: m_local x n in the plan's dtype; P, S: k x n fp64; R: n x n fp64 upper triangular
+ *     (zeros below the diagonal), diag(R) >= 0 (reading A5).
+ *   - Pointers passed to rcholqr_factor / _sketch / _small_qr / _tri_solve / _theta_export are
+ *     CUDA DEVICE pointers on the plan's device, owned by the caller; the library never frees
+ *     them.  rcholqr_factor_host takes HOST pointers (pinned memory recommended) and performs the
+ *     host<->device copies itself.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Work is
+ *     stream-ordered; functions documented "synchronous" block the host until the stream has
+ *     drained and return a definitive numerical status.
+ *   - Q must not alias X.  S may be NULL (not requested).
+ *   - A plan is not thread-safe; distinct plans are independent.
+ *
+ * Theta (readings A1-A4): Philox4x32-10, key = (lo32(seed),
+ * hi32(seed)), counter = (lo32(i), hi32(i), q, domain), i = global X row.  Gaussian: entries
+ * z/sqrt(k), z from a fixed fp32 Box-Muller transform ("i.i.d. Gaussian ...
+ * scaled by sqrt(1/k)").  Sparse-sign: nnz_per_col nonzeros +-1/sqrt(nnz_per_col) per column,
+ * one per block of k/nnz_per_col rows (BASELINE.json config 4; OSNAP block construction).
+ */
+#ifndef RCHOLQR_H
+#define RCHOLQR_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RCHOLQR_VERSION 100  /* 1.0.0 */
+
+typedef struct rcholqr_plan_s* rcholqr_plan;
+
+typedef enum { RCHOLQR_F64 = 0, RCHOLQR_F32 = 1 } rcholqr_dtype;          /* dtype of X and Q */
+typedef enum { RCHOLQR_GAUSSIAN = 0, RCHOLQR_SPARSE_SIGN = 1 } rcholqr_sketch_kind;
+
+typedef enum {
+  RCHOLQR_OK = 0,
+  RCHOLQR_E_INVALID = 1,   /* null pointer, bad enum, ld < n, Q aliases X, m_local < 0        */
+  RCHOLQR_E_SHAPE = 2,     /* n < 1, k < n, sparse: nnz < 1 or k % nnz != 0                    */
+  RCHOLQR_E_NONFINITE = 3, /* the (reduced) sketch P contains NaN/Inf (non-finite X / overflow) */
+  RCHOLQR_E_SINGULAR = 4,  /* some R_jj == 0 or non-finite: X not numerically full rank
+                              (eq:condstab); Q is left unwritten              */
+  RCHOLQR_E_CUDA = 5,      /* a CUDA runtime call or kernel launch failed                       */
+  RCHOLQR_E_NCCL = 6,      /* NCCL unavailable or a collective failed                           */
+  RCHOLQR_E_NOMEM = 7      /* device or host allocation failed                                   */
+} rcholqr_status;
+
+typedef struct {
+  int32_t n;            /* columns of X (>= 1)                                                  */
+  int32_t k;            /* sketch rows (>= n); k = 2n is the paper's choice  */
+  int32_t dtype;        /* rcholqr_dtype of X and Q                                             */
+  int32_t sketch;       /* rcholqr_sketch_kind                                                    */
+  int32_t nnz_per_col;  /* sparse-sign nonzeros per column of Theta (ignored for Gaussian)      */
+  int32_t device;       /* CUDA device ordinal the plan lives on                                */
+  uint64_t seed;        /* Theta seed                                                            */
+  void* nccl_comm;      /* communicator from rcholqr_comm_create, or NULL for a single GPU.
+                           Referenced, not owned.                                                */
+} rcholqr_desc;
+
+/* Create a plan: validates the descriptor, allocates the workspace (per-CTA sketch partials,
+ * P, R^{-1}, QR scratch, status word) on desc->device.  *out is NULL on failure. */
+rcholqr_status rcholqr_create(const rcholqr_desc* desc, rcholqr_plan* out);
+
+/* Free the plan and its workspace (NULL is a no-op). */
+rcholqr_status rcholqr_destroy(rcholqr_plan plan);
+
+/* Whole Algorithm 2 on this rank's row block, SYNCHRONOUS.
+ *   X        [device] m_local x n, leading dim ldx, rows row_offset .. row_offset+m_local-1 of
+ *            the global X (row_offset keys Theta; 0 on a single GPU).  m_local may be 0.
+ *   Q        [device] m_local x n output, leading dim ldq, X's dtype (computed in fp64, rounded
+ *            once -- reading A7).  Not written if the status is E_SINGULAR / E_NONFINITE.
+ *   R        [device] n x n fp64 output (identical bits on every rank).
+ *   S        [device] k x n fp64 output or NULL (Alg. 2's orthonormal sketch of Q).
+ * With a communicator every rank must call this (collective). */
+rcholqr_status rcholqr_factor(rcholqr_plan plan, const void* X, int64_t m_local, int64_t row_offset,
+                              int64_t ldx, void* Q, int64_t ldq, double* R, double* S, void* stream);
+
+/* Same as rcholqr_factor but ASYNCHRONOUS: only argument/launch errors are reported; the
+ * numerical status (E_NONFINITE / E_SINGULAR) is fetched later with rcholqr_query_status. */
+rcholqr_status rcholqr_factor_async(rcholqr_plan plan, const void* X, int64_t m_local,
+                                    int64_t row_offset, int64_t ldx, void* Q, int64_t ldq,
+                                    double* R, double* S, void* stream);
+
+/* Synchronize `stream` and return the numerical status of the last factor/sketch/QR call. */
+rcholqr_status rcholqr_query_status(rcholqr_plan plan, void* stream);
+
+/* End-to-end call with HOST buffers (X_host read, Q_host/R_host/S_host written): copies X to a
+ * plan-owned device buffer, factors, copies Q, R (and S) back.  SYNCHRONOUS. */
+rcholqr_status rcholqr_factor_host(rcholqr_plan plan, const void* X_host, int64_t m_local,
+                                   int64_t row_offset, int64_t ldx, void* Q_host, int64_t ldq,
+                                   double* R_host, double* S_host, void* stream);
+
+/* ---- step-level entry points (same kernels as rcholqr_factor; used by the parity tests) ---- */
+
+/* Step 1 (+ the all-reduce when the plan has a communicator): P = Theta X, k x n fp64 row-major
+ * [device].  SYNCHRONOUS; returns E_NONFINITE if P has NaN/Inf. */
+rcholqr_status rcholqr_sketch(rcholqr_plan plan, const void* X, int64_t m_local, int64_t row_offset,
+                              int64_t ldx, double* P, void* stream);
+
+/* Step 2: Householder QR of the k x n fp64 matrix P [device] -> R [device] (n x n), S [device]
+ * (k x n) or NULL.  SYNCHRONOUS; returns E_SINGULAR on a zero/non-finite pivot (R still written). */
+rcholqr_status rcholqr_small_qr(rcholqr_plan plan, const double* P, double* R, double* S,
+                                void* stream);
+
+/* Step 3: Q = X R^{-1} [device] for a given upper-triangular R [device].  SYNCHRONOUS. */
+rcholqr_status rcholqr_tri_solve(rcholqr_plan plan, const void* X, int64_t m_local, int64_t ldx,
+                                 const double* R, void* Q, int64_t ldq, void* stream);
+
+/* Test export of Theta for global rows row_offset .. row_offset+m-1 [device buffers]:
+ *   Gaussian:    Z (k x m fp32, row-major) = the unscaled N(0,1) draws z_ri (Theta = z/sqrt(k)).
+ *   Sparse-sign: rows (m x nnz int32) and signs (m x nnz int8). Unused outputs may be NULL.
+ * SYNCHRONOUS. */
+rcholqr_status rcholqr_theta_export(uint64_t seed, int32_t k, int32_t sketch, int32_t nnz_per_col,
+                                    int64_t row_offset, int64_t m, float* Z, int32_t* rows,
+                                    int8_t* signs, void* stream);
+
+/* ---- multi-GPU: library-owned NCCL communicator (NCCL is loaded on first use) ---- */
+
+/* Write a 128-byte ncclUniqueId (call on rank 0, broadcast it with torch.distributed). */
+rcholqr_status rcholqr_comm_unique_id(uint8_t id_out[128]);
+/* ncclCommInitRank on `device`; *comm receives an opaque ncclComm_t. Collective over nranks. */
+rcholqr_status rcholqr_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank,
+                                   int32_t device, void** comm);
+rcholqr_status rcholqr_comm_destroy(void* comm);
+
+/* ---- introspection ---- */
+const char* rcholqr_strerror(rcholqr_status s);
+int32_t rcholqr_version(void);
+/* Number of kernels rcholqr_factor_async launches per call for this plan and m_local. */
+int32_t rcholqr_launches_per_factor(rcholqr_plan plan, int64_t m_local);
+/* Per-step device times (ms) of the last factor call when timing is enabled:
+ * out[0] sketch, out[1] partial reduce, out[2] all-reduce, out[3] small QR, out[4] tri prep,
+ * out[5] tall solve.  Enable with rcholqr_set_timing(plan, 1) (adds events, no host syncs). */
+rcholqr_status rcholqr_set_timing(rcholqr_plan plan, int32_t enable);
+rcholqr_status rcholqr_last_timings(rcholqr_plan plan, float out_ms[6]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RCHOLQR_H */

@@ -1,0 +1,289 @@
+"""B200-native direct randomized Cholesky QR (RCholeskyQR, Balabanov arXiv 2210.09953, Alg. 2).
+
+Thin Python binding of the C ABI declared in ``include/rcholqr.h`` (argument marshalling only --
+every step of the factorization runs in the CUDA kernels of ``lib/librcholqr.so``).  PyTorch is
+used for device memory, streams and process groups.  There is no CPU fallback: importing works
+anywhere, but any call that needs the library raises if it is missing or no GPU is present.
+
+    plan = RCholQR(n=100, k=200, dtype=torch.float32, sketch="gaussian", seed=0)
+    Q, R, _ = plan.factor(X)            # X: (m, n) CUDA tensor, row-major
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+from typing import Optional, Tuple
+
+__all__ = ["RCholQR", "RCholQRError", "load_library", "library_path", "theta_export",
+           "comm_unique_id", "comm_create", "comm_destroy", "strerror", "version",
+           "OK", "E_INVALID", "E_SHAPE", "E_NONFINITE", "E_SINGULAR", "E_CUDA", "E_NCCL", "E_NOMEM",
+           "GAUSSIAN", "SPARSE_SIGN"]
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_PKG, "lib", "librcholqr.so")
+_lock = threading.Lock()
+_lib = None
+
+OK, E_INVALID, E_SHAPE, E_NONFINITE, E_SINGULAR, E_CUDA, E_NCCL, E_NOMEM = range(8)
+GAUSSIAN, SPARSE_SIGN = 0, 1
+F64, F32 = 0, 1
+
+# exported symbols (checked by tests/test_abi.py against include/rcholqr.h)
+SYMBOLS = ["rcholqr_create", "rcholqr_destroy", "rcholqr_factor", "rcholqr_factor_async",
+           "rcholqr_query_status", "rcholqr_factor_host", "rcholqr_sketch", "rcholqr_small_qr",
+           "rcholqr_tri_solve", "rcholqr_theta_export", "rcholqr_comm_unique_id",
+           "rcholqr_comm_create", "rcholqr_comm_destroy", "rcholqr_strerror", "rcholqr_version",
+           "rcholqr_launches_per_factor", "rcholqr_set_timing", "rcholqr_last_timings"]
+
+
+class _Desc(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("k", ctypes.c_int32), ("dtype", ctypes.c_int32),
+                ("sketch", ctypes.c_int32), ("nnz_per_col", ctypes.c_int32), ("device", ctypes.c_int32),
+                ("seed", ctypes.c_uint64), ("nccl_comm", ctypes.c_void_p)]
+
+
+class RCholQRError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        super().__init__(f"{where}: {strerror(status)} (status {status})")
+        self.status = status
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def load_library():
+    """Load lib/librcholqr.so (built by ``__graft_entry__.build()`` / ``python -m
+    paper_2210_09953_b200.build``).  Raises if it is missing -- there is no fallback."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(_LIB_PATH):
+            raise RuntimeError(f"CUDA library not built: {_LIB_PATH} (run python -m paper_2210_09953_b200.build)")
+        lib = ctypes.CDLL(_LIB_PATH)
+        V, I32, I64, U64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
+        sig = {
+            "rcholqr_create": ([ctypes.POINTER(_Desc), ctypes.POINTER(V)], I32),
+            "rcholqr_destroy": ([V], I32),
+            "rcholqr_factor": ([V, V, I64, I64, I64, V, I64, V, V, V], I32),
+            "rcholqr_factor_async": ([V, V, I64, I64, I64, V, I64, V, V, V], I32),
+            "rcholqr_query_status": ([V, V], I32),
+            "rcholqr_factor_host": ([V, V, I64, I64, I64, V, I64, V, V, V], I32),
+            "rcholqr_sketch": ([V, V, I64, I64, I64, V, V], I32),
+            "rcholqr_small_qr": ([V, V, V, V, V], I32),
+            "rcholqr_tri_solve": ([V, V, I64, I64, V, V, I64, V], I32),
+            "rcholqr_theta_export": ([U64, I32, I32, I32, I64, I64, V, V, V, V], I32),
+            "rcholqr_comm_unique_id": ([V], I32),
+            "rcholqr_comm_create": ([V, I32, I32, I32, ctypes.POINTER(V)], I32),
+            "rcholqr_comm_destroy": ([V], I32),
+            "rcholqr_strerror": ([I32], ctypes.c_char_p),
+            "rcholqr_version": ([], I32),
+            "rcholqr_launches_per_factor": ([V, I64], I32),
+            "rcholqr_set_timing": ([V, I32], I32),
+            "rcholqr_last_timings": ([V, V], I32),
+        }
+        for name, (argt, rest) in sig.items():
+            f = getattr(lib, name)
+            f.argtypes, f.restype = argt, rest
+        _lib = lib
+        return lib
+
+
+def strerror(status: int) -> str:
+    try:
+        return load_library().rcholqr_strerror(status).decode()
+    except Exception:  # noqa: BLE001 - message only
+        return f"status {status}"
+
+
+def version() -> int:
+    return int(load_library().rcholqr_version())
+
+
+def _check(st: int, where: str):
+    if st != OK:
+        raise RCholQRError(st, where)
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    torch = _torch()
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t) -> ctypes.c_void_p:
+    return ctypes.c_void_p(0 if t is None else t.data_ptr())
+
+
+class RCholQR:
+    """A plan (``rcholqr_create``) for m x n matrices X with fixed n, k, dtype, sketch and seed."""
+
+    def __init__(self, n: int, k: int, dtype=None, sketch: str = "gaussian", nnz_per_col: int = 8,
+                 seed: int = 0, device: int = 0, comm: Optional[int] = None):
+        torch = _torch()
+        if not torch.cuda.is_available():
+            raise RuntimeError("RCholQR needs a CUDA device (no CPU fallback)")
+        dtype = torch.float64 if dtype is None else dtype
+        if dtype not in (torch.float64, torch.float32):
+            raise TypeError("dtype must be torch.float64 or torch.float32")
+        self.n, self.k, self.dtype, self.seed, self.device = int(n), int(k), dtype, int(seed), int(device)
+        self.sketch_kind = {"gaussian": GAUSSIAN, "sparse": SPARSE_SIGN, "sparse_sign": SPARSE_SIGN}[sketch]
+        self.nnz_per_col = int(nnz_per_col)
+        self._lib = load_library()
+        d = _Desc(self.n, self.k, F64 if dtype == torch.float64 else F32, self.sketch_kind, self.nnz_per_col,
+                  self.device, self.seed, ctypes.c_void_p(comm or 0))
+        h = ctypes.c_void_p()
+        _check(self._lib.rcholqr_create(ctypes.byref(d), ctypes.byref(h)), "rcholqr_create")
+        self._h = h
+
+    # -- lifecycle
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            self._lib.rcholqr_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    # -- helpers
+    def _dev(self):
+        return _torch().device("cuda", self.device)
+
+    def _check_x(self, X):
+        torch = _torch()
+        if not (X.is_cuda and X.dtype == self.dtype and X.dim() == 2 and X.shape[1] == self.n):
+            raise ValueError(f"X must be a CUDA {self.dtype} tensor of shape (m, {self.n})")
+        if X.stride(1) != 1:
+            raise ValueError("X must be row-major (stride(1) == 1)")
+        return X.shape[0], max(X.stride(0), self.n) if X.shape[0] > 1 else self.n
+
+    # -- Algorithm 2
+    def factor(self, X, row_offset: int = 0, want_S: bool = False, Q=None, R=None, S=None,
+               stream=None, sync: bool = True) -> Tuple:
+        """Q, R (and S) of X.  ``sync=False`` uses rcholqr_factor_async (status via query_status)."""
+        torch = _torch()
+        m, ldx = self._check_x(X)
+        Q = torch.empty((m, self.n), dtype=self.dtype, device=X.device) if Q is None else Q
+        R = torch.empty((self.n, self.n), dtype=torch.float64, device=X.device) if R is None else R
+        if want_S and S is None:
+            S = torch.empty((self.k, self.n), dtype=torch.float64, device=X.device)
+        fn = self._lib.rcholqr_factor if sync else self._lib.rcholqr_factor_async
+        st = fn(self._h, _ptr(X), m, row_offset, ldx, _ptr(Q), Q.stride(0) if m > 1 else self.n, _ptr(R),
+                _ptr(S), _stream_ptr(stream))
+        _check(st, "rcholqr_factor")
+        return Q, R, S
+
+    def query_status(self, stream=None) -> int:
+        return int(self._lib.rcholqr_query_status(self._h, _stream_ptr(stream)))
+
+    def factor_host(self, X_host, row_offset: int = 0, want_S: bool = False, Q_host=None, R_host=None,
+                    S_host=None, stream=None):
+        """End-to-end call with host (preferably pinned) CPU tensors; copies are inside the call."""
+        torch = _torch()
+        if X_host.is_cuda or X_host.dtype != self.dtype or X_host.shape[1] != self.n or X_host.stride(1) != 1:
+            raise ValueError("X_host must be a row-major CPU tensor of the plan's dtype")
+        m = X_host.shape[0]
+        Q_host = torch.empty((m, self.n), dtype=self.dtype, pin_memory=True) if Q_host is None else Q_host
+        R_host = torch.empty((self.n, self.n), dtype=torch.float64, pin_memory=True) if R_host is None else R_host
+        if want_S and S_host is None:
+            S_host = torch.empty((self.k, self.n), dtype=torch.float64, pin_memory=True)
+        st = self._lib.rcholqr_factor_host(self._h, _ptr(X_host), m, row_offset, max(X_host.stride(0), self.n),
+                                           _ptr(Q_host), self.n, _ptr(R_host), _ptr(S_host), _stream_ptr(stream))
+        _check(st, "rcholqr_factor_host")
+        return Q_host, R_host, S_host
+
+    # -- step-level entry points
+    def sketch(self, X, row_offset: int = 0, P=None, stream=None):
+        torch = _torch()
+        m, ldx = self._check_x(X)
+        P = torch.empty((self.k, self.n), dtype=torch.float64, device=X.device) if P is None else P
+        _check(self._lib.rcholqr_sketch(self._h, _ptr(X), m, row_offset, ldx, _ptr(P), _stream_ptr(stream)),
+               "rcholqr_sketch")
+        return P
+
+    def small_qr(self, P, want_S: bool = True, stream=None):
+        """Returns (R, S, status) -- E_SINGULAR is returned, not raised (R is still written)."""
+        torch = _torch()
+        P = P.contiguous()
+        R = torch.empty((self.n, self.n), dtype=torch.float64, device=P.device)
+        S = torch.empty((self.k, self.n), dtype=torch.float64, device=P.device) if want_S else None
+        st = self._lib.rcholqr_small_qr(self._h, _ptr(P), _ptr(R), _ptr(S), _stream_ptr(stream))
+        if st not in (OK, E_SINGULAR):
+            _check(st, "rcholqr_small_qr")
+        return R, S, int(st)
+
+    def tri_solve(self, X, R, Q=None, stream=None):
+        torch = _torch()
+        m, ldx = self._check_x(X)
+        R = R.contiguous()
+        Q = torch.empty((m, self.n), dtype=self.dtype, device=X.device) if Q is None else Q
+        _check(self._lib.rcholqr_tri_solve(self._h, _ptr(X), m, ldx, _ptr(R), _ptr(Q), self.n,
+                                           _stream_ptr(stream)), "rcholqr_tri_solve")
+        return Q
+
+    # -- introspection
+    def launches_per_factor(self, m: int) -> int:
+        return int(self._lib.rcholqr_launches_per_factor(self._h, m))
+
+    def set_timing(self, enable: bool = True):
+        _check(self._lib.rcholqr_set_timing(self._h, int(enable)), "rcholqr_set_timing")
+
+    def last_timings(self) -> dict:
+        out = (ctypes.c_float * 6)()
+        _check(self._lib.rcholqr_last_timings(self._h, out), "rcholqr_last_timings")
+        keys = ["sketch", "reduce", "allreduce", "small_qr", "tri_prep", "solve"]
+        return {k: float(v) for k, v in zip(keys, out)}
+
+
+def theta_export(seed: int, k: int, m: int, sketch: str = "gaussian", nnz_per_col: int = 8,
+                 row_offset: int = 0, device: int = 0, stream=None):
+    """GPU-generated Theta for global rows row_offset..+m (test export, rcholqr_theta_export).
+
+    Gaussian -> Z (k, m) float32 unscaled draws; sparse -> (rows (m, nnz) int32, signs (m, nnz) int8)."""
+    torch = _torch()
+    lib = load_library()
+    dev = torch.device("cuda", device)
+    if sketch == "gaussian":
+        Z = torch.empty((k, m), dtype=torch.float32, device=dev)
+        _check(lib.rcholqr_theta_export(seed, k, GAUSSIAN, 0, row_offset, m, _ptr(Z), None, None,
+                                        _stream_ptr(stream)), "rcholqr_theta_export")
+        return Z
+    rows = torch.empty((m, nnz_per_col), dtype=torch.int32, device=dev)
+    signs = torch.empty((m, nnz_per_col), dtype=torch.int8, device=dev)
+    _check(lib.rcholqr_theta_export(seed, k, SPARSE_SIGN, nnz_per_col, row_offset, m, None, _ptr(rows),
+                                    _ptr(signs), _stream_ptr(stream)), "rcholqr_theta_export")
+    return rows, signs
+
+
+def comm_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(load_library().rcholqr_comm_unique_id(buf), "rcholqr_comm_unique_id")
+    return bytes(buf)
+
+
+def comm_create(uid: bytes, nranks: int, rank: int, device: int) -> int:
+    buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+    out = ctypes.c_void_p()
+    _check(load_library().rcholqr_comm_create(buf, nranks, rank, device, ctypes.byref(out)), "rcholqr_comm_create")
+    return int(out.value)
+
+
+def comm_destroy(comm: int):
+    _check(load_library().rcholqr_comm_destroy(ctypes.c_void_p(comm)), "rcholqr_comm_destroy")

@@ -1,0 +1,422 @@
+// api.cu -- C ABI (include/rcholqr.h): plan/workspace management, argument validation, the launch
+// sequence of Algorithm 2 and the multi-GPU all-reduce.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include "internal.cuh"
+#include "rcholqr.h"
+
+using namespace rcq;
+
+// ---------------------------------------------------------------------------------------------
+// NCCL, loaded lazily (a single-GPU plan never touches it).
+namespace {
+struct NcclApi {
+  bool tried = false, ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+};
+NcclApi g_nccl;
+std::mutex g_nccl_mu;
+
+bool nccl_load() {
+  std::lock_guard<std::mutex> lk(g_nccl_mu);
+  if (g_nccl.tried) return g_nccl.ok;
+  g_nccl.tried = true;
+  const char* env = getenv("RCHOLQR_NCCL_LIB");
+  void* h = nullptr;
+  if (env) h = dlopen(env, RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return false;
+  g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+  g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+  g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
+  g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+  g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.CommDestroy;
+  return g_nccl.ok;
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+struct rcholqr_plan_s {
+  rcholqr_desc d;
+  int sms = 0;
+  size_t smem_optin = 0;
+  SketchLaunch sk{};
+  TrsmLaunch tr{};
+  int qr_kind = 0;
+  double* part = nullptr;   // [splits][k][n] per-CTA sketch partials
+  double* P = nullptr;      // [k][n] reduced sketch
+  double* W = nullptr;      // [n][n] R^{-1}
+  double* Awork = nullptr;  // [n][k] column-major Householder workspace (reflectors)
+  double* diag = nullptr;   // [n] raw pivots (sign before normalisation)
+  double* tau = nullptr;    // [n] reflector scalings
+  double* Rtmp = nullptr;   // [n][n] R when the caller does not want one
+  int* status_d = nullptr;
+  int* status_h = nullptr;  // pinned
+  // factor_host staging
+  void* xbuf = nullptr; void* qbuf = nullptr; size_t xq_bytes = 0;
+  double* rbuf = nullptr; double* sbuf = nullptr;
+  bool timing = false;
+  cudaEvent_t ev[7] = {};
+  float last_ms[6] = {0, 0, 0, 0, 0, 0};
+  bool have_timing = false;
+};
+
+namespace {
+size_t esize(int dtype) { return dtype == RCHOLQR_F64 ? 8 : 4; }
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+rcholqr_status cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return RCHOLQR_OK;
+  if (e == cudaErrorMemoryAllocation) return RCHOLQR_E_NOMEM;
+  return RCHOLQR_E_CUDA;
+}
+#define CU(x)                                        \
+  do {                                               \
+    cudaError_t _e = (x);                            \
+    if (_e != cudaSuccess) return cuda_status(_e);   \
+  } while (0)
+
+rcholqr_status validate_desc(const rcholqr_desc* d) {
+  if (!d) return RCHOLQR_E_INVALID;
+  if (d->dtype != RCHOLQR_F64 && d->dtype != RCHOLQR_F32) return RCHOLQR_E_INVALID;
+  if (d->sketch != RCHOLQR_GAUSSIAN && d->sketch != RCHOLQR_SPARSE_SIGN) return RCHOLQR_E_INVALID;
+  if (d->n < 1 || d->k < d->n) return RCHOLQR_E_SHAPE;
+  if (d->sketch == RCHOLQR_SPARSE_SIGN &&
+      (d->nnz_per_col < 1 || d->nnz_per_col > d->k || d->k % d->nnz_per_col != 0))
+    return RCHOLQR_E_SHAPE;
+  if ((int64_t)d->k * d->n > (int64_t)1 << 28) return RCHOLQR_E_SHAPE;
+  return RCHOLQR_OK;
+}
+
+bool overlaps(const void* a, size_t abytes, const void* b, size_t bbytes) {
+  const char* pa = (const char*)a;
+  const char* pb = (const char*)b;
+  return pa < pb + bbytes && pb < pa + abytes;
+}
+
+size_t span_bytes(int64_t rows, int64_t ld, int n, size_t es) {
+  return rows <= 0 ? 0 : (size_t)((rows - 1) * ld + n) * es;
+}
+
+rcholqr_status status_from_word(int w) {
+  if (w & kStNonfinite) return RCHOLQR_E_NONFINITE;
+  if (w & kStSingular) return RCHOLQR_E_SINGULAR;
+  return RCHOLQR_OK;
+}
+
+rcholqr_status check_factor_args(rcholqr_plan p, const void* X, int64_t m, int64_t ro, int64_t ldx,
+                                 const void* Q, int64_t ldq) {
+  if (!p) return RCHOLQR_E_INVALID;
+  const int n = p->d.n;
+  if (m < 0 || ro < 0 || ldx < n || ldq < n) return RCHOLQR_E_INVALID;
+  if (m > 0 && (!X || !Q)) return RCHOLQR_E_INVALID;
+  const size_t es = esize(p->d.dtype);
+  if (m > 0 && overlaps(X, span_bytes(m, ldx, n, es), Q, span_bytes(m, ldq, n, es))) return RCHOLQR_E_INVALID;
+  return RCHOLQR_OK;
+}
+
+rcholqr_status do_sketch(rcholqr_plan p, const void* X, int64_t m, int64_t ro, int64_t ldx, double* P,
+                         cudaStream_t st) {
+  const auto& d = p->d;
+  if (m > 0) {
+    if (p->timing) cudaEventRecord(p->ev[0], st);
+    CU(launch_sketch(p->sk, X, d.dtype, m, d.n, ldx, ro, d.k, d.nnz_per_col, d.seed, p->part, P, p->status_d, st,
+                     p->timing ? p->ev[1] : nullptr));
+  } else {
+    if (p->timing) { cudaEventRecord(p->ev[0], st); cudaEventRecord(p->ev[1], st); }
+    CU(cudaMemsetAsync(P, 0, sizeof(double) * (size_t)d.k * d.n, st));
+  }
+  if (p->timing) cudaEventRecord(p->ev[2], st);
+  if (d.nccl_comm) {
+    if (!nccl_load()) return RCHOLQR_E_NCCL;
+    ncclResult_t r = g_nccl.AllReduce(P, P, (size_t)d.k * d.n, ncclFloat64, ncclSum, (ncclComm_t)d.nccl_comm, st);
+    if (r != ncclSuccess) return RCHOLQR_E_NCCL;
+  }
+  if (p->timing) cudaEventRecord(p->ev[3], st);
+  return RCHOLQR_OK;
+}
+
+rcholqr_status read_status(rcholqr_plan p, cudaStream_t st) {
+  CU(cudaMemcpyAsync(p->status_h, p->status_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (p->timing) {
+    const int pairs[6][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {4, 5}, {5, 6}};
+    for (int t = 0; t < 6; ++t) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, p->ev[pairs[t][0]], p->ev[pairs[t][1]]) != cudaSuccess) ms = -1.f;
+      p->last_ms[t] = ms;
+    }
+    p->have_timing = true;
+  }
+  return status_from_word(*p->status_h);
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------------------------
+extern "C" {
+
+int32_t rcholqr_version(void) { return RCHOLQR_VERSION; }
+
+const char* rcholqr_strerror(rcholqr_status s) {
+  switch (s) {
+    case RCHOLQR_OK: return "ok";
+    case RCHOLQR_E_INVALID: return "invalid argument";
+    case RCHOLQR_E_SHAPE: return "invalid shape (need n >= 1, k >= n, sparse: k % nnz == 0)";
+    case RCHOLQR_E_NONFINITE: return "sketch contains NaN/Inf";
+    case RCHOLQR_E_SINGULAR: return "R has a zero or non-finite pivot (X not numerically full rank)";
+    case RCHOLQR_E_CUDA: return "CUDA error";
+    case RCHOLQR_E_NCCL: return "NCCL unavailable or collective failed";
+    case RCHOLQR_E_NOMEM: return "out of memory";
+  }
+  return "unknown status";
+}
+
+rcholqr_status rcholqr_create(const rcholqr_desc* desc, rcholqr_plan* out) {
+  if (!out) return RCHOLQR_E_INVALID;
+  *out = nullptr;
+  rcholqr_status vs = validate_desc(desc);
+  if (vs != RCHOLQR_OK) return vs;
+  int ndev = 0;
+  CU(cudaGetDeviceCount(&ndev));
+  if (desc->device < 0 || desc->device >= ndev) return RCHOLQR_E_INVALID;
+  DeviceGuard dg(desc->device);
+  rcholqr_plan p = new (std::nothrow) rcholqr_plan_s();
+  if (!p) return RCHOLQR_E_NOMEM;
+  p->d = *desc;
+  cudaDeviceProp prop;
+  cudaError_t e = cudaGetDeviceProperties(&prop, desc->device);
+  if (e != cudaSuccess) { delete p; return cuda_status(e); }
+  p->sms = prop.multiProcessorCount;
+  p->smem_optin = prop.sharedMemPerBlockOptin;
+  const int k = desc->k, n = desc->n;
+  p->sk = plan_sketch(k, n, desc->dtype, desc->sketch, desc->nnz_per_col, p->sms, p->smem_optin);
+  p->tr = plan_trsm(n, desc->dtype, p->smem_optin);
+  p->qr_kind = plan_qr(k, n, p->smem_optin);
+  const size_t kn = (size_t)k * n, nn = (size_t)n * n;
+  bool okalloc = cudaMalloc(&p->part, sizeof(double) * kn * p->sk.splits) == cudaSuccess &&
+                 cudaMalloc(&p->P, sizeof(double) * kn) == cudaSuccess &&
+                 cudaMalloc(&p->W, sizeof(double) * nn) == cudaSuccess &&
+                 cudaMalloc(&p->Awork, sizeof(double) * kn) == cudaSuccess &&
+                 cudaMalloc(&p->diag, sizeof(double) * n) == cudaSuccess &&
+                 cudaMalloc(&p->tau, sizeof(double) * n) == cudaSuccess &&
+                 cudaMalloc(&p->Rtmp, sizeof(double) * nn) == cudaSuccess &&
+                 cudaMalloc(&p->status_d, sizeof(int)) == cudaSuccess &&
+                 cudaMallocHost(&p->status_h, sizeof(int)) == cudaSuccess;
+  if (okalloc) {
+    for (int t = 0; t < 7 && okalloc; ++t) okalloc = cudaEventCreate(&p->ev[t]) == cudaSuccess;
+  }
+  if (!okalloc) {
+    cudaGetLastError();
+    rcholqr_destroy(p);
+    return RCHOLQR_E_NOMEM;
+  }
+  cudaMemset(p->status_d, 0, sizeof(int));
+  *p->status_h = 0;
+  *out = p;
+  return RCHOLQR_OK;
+}
+
+rcholqr_status rcholqr_destroy(rcholqr_plan p) {
+  if (!p) return RCHOLQR_OK;
+  DeviceGuard dg(p->d.device);
+  cudaFree(p->part); cudaFree(p->P); cudaFree(p->W); cudaFree(p->Awork); cudaFree(p->diag); cudaFree(p->tau);
+  cudaFree(p->Rtmp); cudaFree(p->status_d);
+  if (p->status_h) cudaFreeHost(p->status_h);
+  cudaFree(p->xbuf); cudaFree(p->qbuf); cudaFree(p->rbuf); cudaFree(p->sbuf);
+  for (int t = 0; t < 7; ++t)
+    if (p->ev[t]) cudaEventDestroy(p->ev[t]);
+  delete p;
+  return RCHOLQR_OK;
+}
+
+rcholqr_status rcholqr_factor_async(rcholqr_plan p, const void* X, int64_t m, int64_t ro, int64_t ldx, void* Q,
+                                    int64_t ldq, double* R, double* S, void* stream) {
+  rcholqr_status a = check_factor_args(p, X, m, ro, ldx, Q, ldq);
+  if (a != RCHOLQR_OK) return a;
+  DeviceGuard dg(p->d.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int k = p->d.k, n = p->d.n;
+  double* Rout = R ? R : p->Rtmp;
+  CU(cudaMemsetAsync(p->status_d, 0, sizeof(int), st));
+  rcholqr_status s = do_sketch(p, X, m, ro, ldx, p->P, st);
+  if (s != RCHOLQR_OK) return s;
+  CU(launch_qr(p->qr_kind, p->P, k, n, Rout, p->Awork, p->diag, p->tau, p->status_d, st));
+  if (S) CU(launch_form_s(p->Awork, p->tau, p->diag, k, n, S, p->status_d, st));
+  if (p->timing) cudaEventRecord(p->ev[4], st);
+  CU(launch_tri_inverse(Rout, n, p->W, p->status_d, st));
+  if (p->timing) cudaEventRecord(p->ev[5], st);
+  if (m > 0) CU(launch_trsm(p->tr, X, p->d.dtype, m, n, ldx, p->W, Q, ldq, p->status_d, st));
+  if (p->timing) cudaEventRecord(p->ev[6], st);
+  return RCHOLQR_OK;
+}
+
+rcholqr_status rcholqr_query_status(rcholqr_plan p, void* stream) {
+  if (!p) return RCHOLQR_E_INVALID;
+  DeviceGuard dg(p->d.device);
+  return read_status(p, (cudaStream_t)stream);
+}
+
+rcholqr_status rcholqr_factor(rcholqr_plan p, const void* X, int64_t m, int64_t ro, int64_t ldx, void* Q,
+                              int64_t ldq, double* R, double* S, void* stream) {
+  rcholqr_status s = rcholqr_factor_async(p, X, m, ro, ldx, Q, ldq, R, S, stream);
+  if (s != RCHOLQR_OK) return s;
+  return rcholqr_query_status(p, stream);
+}
+
+rcholqr_status rcholqr_factor_host(rcholqr_plan p, const void* Xh, int64_t m, int64_t ro, int64_t ldx, void* Qh,
+                                   int64_t ldq, double* Rh, double* Sh, void* stream) {
+  if (!p || !Rh) return RCHOLQR_E_INVALID;
+  const int n = p->d.n, k = p->d.k;
+  if (m < 0 || ldx < n || ldq < n || (m > 0 && (!Xh || !Qh))) return RCHOLQR_E_INVALID;
+  DeviceGuard dg(p->d.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t es = esize(p->d.dtype);
+  const size_t need = (size_t)std::max<int64_t>(m, 1) * n * es;
+  if (need > p->xq_bytes) {
+    cudaFree(p->xbuf); cudaFree(p->qbuf);
+    p->xbuf = p->qbuf = nullptr; p->xq_bytes = 0;
+    CU(cudaMalloc(&p->xbuf, need));
+    CU(cudaMalloc(&p->qbuf, need));
+    p->xq_bytes = need;
+  }
+  if (!p->rbuf) CU(cudaMalloc(&p->rbuf, sizeof(double) * (size_t)n * n));
+  if (Sh && !p->sbuf) CU(cudaMalloc(&p->sbuf, sizeof(double) * (size_t)k * n));
+  if (m > 0) CU(cudaMemcpy2DAsync(p->xbuf, n * es, Xh, ldx * es, n * es, m, cudaMemcpyHostToDevice, st));
+  rcholqr_status s = rcholqr_factor_async(p, p->xbuf, m, ro, n, p->qbuf, n, p->rbuf, Sh ? p->sbuf : nullptr, st);
+  if (s != RCHOLQR_OK) return s;
+  if (m > 0) CU(cudaMemcpy2DAsync(Qh, ldq * es, p->qbuf, n * es, n * es, m, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(Rh, p->rbuf, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToHost, st));
+  if (Sh) CU(cudaMemcpyAsync(Sh, p->sbuf, sizeof(double) * (size_t)k * n, cudaMemcpyDeviceToHost, st));
+  return read_status(p, st);
+}
+
+rcholqr_status rcholqr_sketch(rcholqr_plan p, const void* X, int64_t m, int64_t ro, int64_t ldx, double* P,
+                              void* stream) {
+  if (!p || !P || m < 0 || ro < 0 || ldx < p->d.n || (m > 0 && !X)) return RCHOLQR_E_INVALID;
+  DeviceGuard dg(p->d.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  CU(cudaMemsetAsync(p->status_d, 0, sizeof(int), st));
+  rcholqr_status s = do_sketch(p, X, m, ro, ldx, P, st);
+  if (s != RCHOLQR_OK) return s;
+  const bool t = p->timing;
+  p->timing = false;
+  s = read_status(p, st);
+  p->timing = t;
+  return s;
+}
+
+rcholqr_status rcholqr_small_qr(rcholqr_plan p, const double* P, double* R, double* S, void* stream) {
+  if (!p || !P || !R) return RCHOLQR_E_INVALID;
+  DeviceGuard dg(p->d.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int k = p->d.k, n = p->d.n;
+  CU(cudaMemsetAsync(p->status_d, 0, sizeof(int), st));
+  CU(launch_qr(p->qr_kind, P, k, n, R, p->Awork, p->diag, p->tau, p->status_d, st));
+  if (S) CU(launch_form_s(p->Awork, p->tau, p->diag, k, n, S, p->status_d, st));
+  const bool t = p->timing;
+  p->timing = false;
+  rcholqr_status s = read_status(p, st);
+  p->timing = t;
+  return s;
+}
+
+rcholqr_status rcholqr_tri_solve(rcholqr_plan p, const void* X, int64_t m, int64_t ldx, const double* R, void* Q,
+                                 int64_t ldq, void* stream) {
+  rcholqr_status a = check_factor_args(p, X, m, 0, ldx, Q, ldq);
+  if (a != RCHOLQR_OK) return a;
+  if (!R) return RCHOLQR_E_INVALID;
+  DeviceGuard dg(p->d.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = p->d.n;
+  CU(cudaMemsetAsync(p->status_d, 0, sizeof(int), st));
+  CU(launch_check_diag(R, n, p->status_d, st));
+  CU(launch_tri_inverse(R, n, p->W, p->status_d, st));
+  if (m > 0) CU(launch_trsm(p->tr, X, p->d.dtype, m, n, ldx, p->W, Q, ldq, p->status_d, st));
+  const bool t = p->timing;
+  p->timing = false;
+  rcholqr_status s = read_status(p, st);
+  p->timing = t;
+  return s;
+}
+
+rcholqr_status rcholqr_theta_export(uint64_t seed, int32_t k, int32_t sketch, int32_t zeta, int64_t ro, int64_t m,
+                                    float* Z, int32_t* rows, int8_t* signs, void* stream) {
+  if (k < 1 || m < 0 || ro < 0) return RCHOLQR_E_INVALID;
+  if (sketch != RCHOLQR_GAUSSIAN && sketch != RCHOLQR_SPARSE_SIGN) return RCHOLQR_E_INVALID;
+  if (sketch == RCHOLQR_SPARSE_SIGN && (zeta < 1 || zeta > k || k % zeta != 0)) return RCHOLQR_E_SHAPE;
+  cudaStream_t st = (cudaStream_t)stream;
+  CU(launch_theta_export(seed, k, sketch, zeta, ro, m, Z, rows, signs, st));
+  CU(cudaStreamSynchronize(st));
+  return RCHOLQR_OK;
+}
+
+rcholqr_status rcholqr_comm_unique_id(uint8_t id_out[128]) {
+  if (!id_out) return RCHOLQR_E_INVALID;
+  if (!nccl_load()) return RCHOLQR_E_NCCL;
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId must be 128 bytes");
+  ncclUniqueId id;
+  if (g_nccl.GetUniqueId(&id) != ncclSuccess) return RCHOLQR_E_NCCL;
+  memcpy(id_out, &id, 128);
+  return RCHOLQR_OK;
+}
+
+rcholqr_status rcholqr_comm_create(const uint8_t id[128], int32_t nranks, int32_t rank, int32_t device, void** comm) {
+  if (!id || !comm || nranks < 1 || rank < 0 || rank >= nranks) return RCHOLQR_E_INVALID;
+  *comm = nullptr;
+  if (!nccl_load()) return RCHOLQR_E_NCCL;
+  DeviceGuard dg(device);
+  ncclUniqueId uid;
+  memcpy(&uid, id, 128);
+  ncclComm_t c = nullptr;
+  if (g_nccl.CommInitRank(&c, nranks, uid, rank) != ncclSuccess) return RCHOLQR_E_NCCL;
+  *comm = (void*)c;
+  return RCHOLQR_OK;
+}
+
+rcholqr_status rcholqr_comm_destroy(void* comm) {
+  if (!comm) return RCHOLQR_OK;
+  if (!nccl_load()) return RCHOLQR_E_NCCL;
+  return g_nccl.CommDestroy((ncclComm_t)comm) == ncclSuccess ? RCHOLQR_OK : RCHOLQR_E_NCCL;
+}
+
+int32_t rcholqr_launches_per_factor(rcholqr_plan p, int64_t m) {
+  if (!p) return -1;
+  // sketch (+ reduce) | QR | tri-inverse | tall solve   (memsets and the all-reduce are not ours)
+  return (m > 0 ? 2 : 0) + 1 + 1 + (m > 0 ? 1 : 0);
+}
+
+rcholqr_status rcholqr_set_timing(rcholqr_plan p, int32_t enable) {
+  if (!p) return RCHOLQR_E_INVALID;
+  p->timing = enable != 0;
+  return RCHOLQR_OK;
+}
+
+rcholqr_status rcholqr_last_timings(rcholqr_plan p, float out_ms[6]) {
+  if (!p || !out_ms) return RCHOLQR_E_INVALID;
+  for (int t = 0; t < 6; ++t) out_ms[t] = p->have_timing ? p->last_ms[t] : -1.f;
+  return RCHOLQR_OK;
+}
+
+}  // extern "C"

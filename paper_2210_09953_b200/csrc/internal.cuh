@@ -1,0 +1,58 @@
+// internal.cuh -- plan layout and launch interfaces shared by the library's translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstddef>
+#include <cstdint>
+#include "rcholqr.h"
+
+namespace rcq {
+
+// Status bits written by kernels into the plan's device status word (0 = OK).
+enum : int { kStNonfinite = 1, kStSingular = 2 };
+
+// One FP64 tensor-core MMA: D(16x8) += A(16x4) B(4x8)  (DMMA on sm_100a; tcgen05 has no f64 kind).
+// Fragments (PTX ISA, mma.m16n8k4 .f64): g = lane/4, t = lane%4;
+//   A: a0 = A[g][t], a1 = A[g+8][t];  B: b0 = B[t][g];  D: d0,d1 = D[g][2t..2t+1], d2,d3 = D[g+8][..].
+__device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1, double b) {
+  asm("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};"
+      : "+d"(d[0]), "+d"(d[1]), "+d"(d[2]), "+d"(d[3])
+      : "d"(a0), "d"(a1), "d"(b));
+}
+
+// ---- launch configurations chosen at plan creation ----
+enum SketchKind : int { kSketchG64x32 = 0, kSketchG128x64 = 1, kSketchG112x104 = 2, kSketchG208x56 = 3,
+                        kSketchG128x128 = 4, kSketchSparse = 10 };
+enum TrsmKind : int { kTrsm64x24 = 0, kTrsm128x64 = 1, kTrsm128x112 = 2, kTrsm128x128 = 3 };
+enum QrKind : int { kQrSmem = 0, kQrGlobal = 1 };
+
+struct SketchLaunch {
+  int kind;
+  int KT, NT, threads;   // tile of P per CTA (sparse: NT = columns per CTA, KT = k)
+  int tiles_k, tiles_n, splits;
+  size_t smem;
+};
+struct TrsmLaunch {
+  int kind;
+  int TM, NT, threads, tiles_n;
+  size_t smem;
+};
+
+// Host-side launchers (defined in sketch.cu / qr.cu / trsm.cu).
+SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms, size_t smem_optin);
+cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
+                          int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* P,
+                          int* status, cudaStream_t st, cudaEvent_t ev_mid);
+TrsmLaunch plan_trsm(int n, int dtype, size_t smem_optin);
+cudaError_t launch_tri_inverse(const double* R, int n, double* W, int* status, cudaStream_t st);
+cudaError_t launch_trsm(const TrsmLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
+                        const double* W, void* Q, int64_t ldq, const int* status, cudaStream_t st);
+int plan_qr(int k, int n, size_t smem_optin);
+cudaError_t launch_qr(int kind, const double* P, int k, int n, double* R, double* Awork, double* diag,
+                      double* tau, int* status, cudaStream_t st);
+cudaError_t launch_form_s(const double* Awork, const double* tau, const double* diag, int k, int n,
+                          double* S, const int* status, cudaStream_t st);
+cudaError_t launch_theta_export(uint64_t seed, int k, int sketch, int zeta, int64_t row_offset, int64_t m,
+                                float* Z, int32_t* rows, int8_t* signs, cudaStream_t st);
+cudaError_t launch_check_diag(const double* R, int n, int* status, cudaStream_t st);
+
+}  // namespace rcq

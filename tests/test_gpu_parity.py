@@ -1,0 +1,336 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bars:
+  * Theta: bit-exact (Gaussian draws and sparse (row, sign) lists).
+  * P (sketch): ||P_gpu - P_oracle||_F <= 1e-12 ||P_oracle||_F (the oracle's P is compensated,
+    so this measures the GPU's own fp64 accumulation error; expected ~1e-15).
+  * R: relative Frobenius <= 1e-10 (fp64 X) / 1e-4 (fp32 X) vs the oracle (north star); on an
+    identical P the QR kernels agree to 1e-13.
+  * Q: ||Q_gpu - Q_oracle||_F / ||Q_oracle||_F <= 10 u kappa (+ 2^-24 for fp32 storage): both
+    carry the u*kappa forward error of the solve (eq:stab3).
+  * ||I - (Theta Q)^T (Theta Q)||_2 <= max(tol, 10 * oracle's), tol = 1e-12 / 1e-5 (reading A12).
+  * eq:main1 column residual <= 2.1 u n (fp64).
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2210_09953_b200 as rcq
+import synth
+
+pytestmark = pytest.mark.gpu
+U64 = 2.0**-53
+U32 = 2.0**-24
+
+
+def _t(a, dev="cuda"):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+
+
+def _np(t):
+    return t.detach().cpu().numpy()
+
+
+def _rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def _plan(n, k, dt, sketch="gaussian", nnz=8, seed=0):
+    return rcq.RCholQR(n=n, k=k, dtype=torch.float64 if dt == "f64" else torch.float32, sketch=sketch,
+                       nnz_per_col=nnz, seed=seed)
+
+
+# ---------------------------------------------------------------------------------- Theta
+@pytest.mark.parametrize("seed,k,ro,m", [(0, 40, 0, 10_000), (0, 200, 0, 4097), (123456789, 2048, 2**40 + 7, 3000),
+                                         (2**64 - 1, 13, 5, 1000)])
+def test_theta_gaussian_bit_exact(cuda, seed, k, ro, m):
+    Zg = _np(rcq.theta_export(seed, k, m, row_offset=ro))
+    Zo = oracle.theta_gauss_z(seed, k, m, row_offset=ro)
+    assert np.array_equal(Zg.view(np.uint32), Zo.view(np.uint32))
+
+
+@pytest.mark.parametrize("seed,k,nnz,ro,m", [(0, 128, 8, 0, 100_000), (7, 96, 12, 2**33, 5000), (1, 40, 4, 3, 777)])
+def test_theta_sparse_bit_exact(cuda, seed, k, nnz, ro, m):
+    rg, sg = rcq.theta_export(seed, k, m, sketch="sparse", nnz_per_col=nnz, row_offset=ro)
+    ro_, so_ = oracle.theta_sparse(seed, k, nnz, m, row_offset=ro)
+    assert np.array_equal(_np(rg), ro_) and np.array_equal(_np(sg), so_)
+
+
+# ---------------------------------------------------------------------------------- sketch
+SKETCH_CASES = [
+    # m, n, k, dtype, sketch, log10 cond  (cover every kernel tile config + ragged tails)
+    (10_000, 20, 40, "f64", "gaussian", 3),      # C1 (64x32 tile)
+    (70_001, 100, 200, "f32", "gaussian", 5),    # C2 shape, ragged (112x104 tile)
+    (33, 64, 128, "f64", "gaussian", 2),         # 128x64 tile, m < one chunk + 1
+    (5_003, 256, 512, "f64", "gaussian", 10),    # C3 shape (128x128 tiles)
+    (1_000, 130, 260, "f32", "gaussian", 3),     # ragged n and k over 128x128 tiles
+    (1, 8, 16, "f64", "gaussian", 0),            # single row
+    (100_003, 64, 128, "f32", "sparse", 4),      # C4 shape
+    (2_000, 300, 600, "f64", "sparse", 3),       # sparse with column tiling
+]
+
+
+@pytest.mark.parametrize("m,n,k,dt,sk,c", SKETCH_CASES)
+def test_sketch_parity(cuda, m, n, k, dt, sk, c):
+    X = synth.make_X(m, n, c, dt)
+    plan = _plan(n, k, dt, sk)
+    Pg = _np(plan.sketch(_t(X)))
+    Po = oracle.sketch(X, k, sketch=oracle.GAUSSIAN if sk == "gaussian" else oracle.SPARSE_SIGN, zeta=8)
+    assert _rel(Pg, Po) <= 1e-12, _rel(Pg, Po)
+
+
+def test_sketch_ld_and_row_offset(cuda):
+    X = synth.make_X(5000, 40, 3.0)
+    wide = np.zeros((5000, 57))
+    wide[:, 3:43] = X
+    Xt = _t(wide)[:, 3:43]                       # ldx = 57
+    plan = _plan(40, 80, "f64")
+    Pg = _np(plan.sketch(Xt, row_offset=2**35 + 11))
+    Po = oracle.sketch(X, 80, row_offset=2**35 + 11)
+    assert _rel(Pg, Po) <= 1e-12
+
+
+def test_sketch_partition_emulation(cuda):
+    # one GPU emulating G ranks: Theta keyed by the GLOBAL row => sum of block sketches == sketch
+    X = synth.make_X(100_000, 32, 4.0)
+    plan = _plan(32, 64, "f64")
+    Xt = _t(X)
+    full = _np(plan.sketch(Xt))
+    bounds = [0, 12_345, 50_000, 77_777, 100_000]
+    parts = sum(_np(plan.sketch(Xt[a:b], row_offset=a)) for a, b in zip(bounds[:-1], bounds[1:]))
+    assert _rel(parts, full) <= 1e-14
+
+
+def test_sketch_deterministic(cuda):
+    X = _t(synth.make_X(200_000, 100, 5.0, "f32"))
+    plan = _plan(100, 200, "f32")
+    a, b = _np(plan.sketch(X)), _np(plan.sketch(X))
+    assert np.array_equal(a, b)
+
+
+# ---------------------------------------------------------------------------------- small QR
+@pytest.mark.parametrize("k,n", [(40, 20), (200, 100), (128, 64), (512, 256), (300, 150), (2, 1)])
+def test_small_qr_parity(cuda, k, n):
+    rng = np.random.default_rng(k + n)
+    P = rng.standard_normal((k, n)) @ np.diag(10.0 ** -np.linspace(0, 8, n))
+    plan = _plan(n, k, "f64")
+    Rg, Sg, st = plan.small_qr(_t(P), want_S=True)
+    Ro, So, sto = oracle.householder(P)
+    assert st == sto == rcq.OK
+    Rg, Sg = _np(Rg), _np(Sg)
+    assert _rel(Rg, Ro) <= 1e-13
+    assert np.all(np.diag(Rg) > 0) and np.all(np.tril(Rg, -1) == 0)
+    assert np.linalg.norm(Sg.T @ Sg - np.eye(n)) <= 50 * n * U64
+    assert np.linalg.norm(P - Sg @ Rg) <= 50 * n * U64 * np.linalg.norm(P)
+
+
+def test_small_qr_spec_example(cuda):
+    plan = _plan(1, 2, "f64")
+    R, S, st = plan.small_qr(_t(np.array([[3.0], [4.0]])))
+    assert st == rcq.OK and abs(_np(R)[0, 0] - 5.0) < 1e-15 and np.allclose(_np(S)[:, 0], [0.6, 0.8], atol=1e-16)
+
+
+def test_small_qr_singular(cuda):
+    P = np.zeros((8, 4))
+    P[:, 0] = 1.0
+    P[:, 2:] = np.arange(16).reshape(8, 2)
+    plan = _plan(4, 8, "f64")
+    R, _, st = plan.small_qr(_t(P), want_S=False)
+    assert st == rcq.E_SINGULAR and _np(R)[1, 1] == 0.0
+
+
+# ---------------------------------------------------------------------------------- tall solve
+@pytest.mark.parametrize("m,n,dt,c", [(10_000, 20, "f64", 3), (50_001, 100, "f32", 5), (20_000, 64, "f32", 4),
+                                      (3_001, 256, "f64", 10), (1_000, 1024, "f64", 12), (5, 130, "f64", 3)])
+def test_tri_solve_parity(cuda, m, n, dt, c):
+    X = synth.make_X(max(m, n), n, c, dt)
+    Ro, _, _ = oracle.householder(oracle.sketch(X, 2 * n))
+    X = X[:m]
+    plan = _plan(n, 2 * n, dt)
+    Qg = _np(plan.tri_solve(_t(X), _t(Ro)))
+    Qo = oracle.forward_subst(X, Ro)
+    u = U64 if dt == "f64" else U32
+    assert _rel(Qg, Qo) <= 10 * U64 * 10**c + (2 * U32 if dt == "f32" else 0)
+    if dt == "f64":
+        assert oracle.col_residual(X, Qg, Ro) <= 2.1 * u * n
+
+
+def test_tri_solve_spec_example_and_identity(cuda):
+    plan = _plan(2, 4, "f64")
+    Q = _np(plan.tri_solve(_t(np.array([[2.0, 1.0]])), _t(np.array([[2.0, 1.0], [0.0, 1.0]]))))
+    assert np.array_equal(Q, [[1.0, 0.0]])
+    X = np.random.default_rng(0).standard_normal((777, 2))
+    assert np.array_equal(_np(plan.tri_solve(_t(X), _t(np.eye(2)))), X)
+
+
+def test_tri_solve_singular(cuda):
+    plan = _plan(3, 6, "f64")
+    R = np.eye(3)
+    R[2, 2] = 0.0
+    with pytest.raises(rcq.RCholQRError) as e:
+        plan.tri_solve(_t(np.ones((10, 3))), _t(R))
+    assert e.value.status == rcq.E_SINGULAR
+
+
+# ---------------------------------------------------------------------------------- end to end
+E2E = [
+    # name, m, n, k, dtype, sketch, log10 cond
+    ("C1", 10_000, 20, 40, "f64", "gaussian", 3),
+    ("C2-reduced", 262_144, 100, 200, "f32", "gaussian", 5),
+    ("C3-reduced", 65_536, 256, 512, "f64", "gaussian", 10),
+    ("C4-reduced", 262_144, 64, 128, "f32", "sparse", 4),
+    ("C5-reduced", 12_288, 1024, 2048, "f64", "gaussian", 12),
+]
+
+
+def _check_e2e(X, k, sk, c, Qg, Rg, plan, dt):
+    n = X.shape[1]
+    so = oracle.GAUSSIAN if sk == "gaussian" else oracle.SPARSE_SIGN
+    out = oracle.factor(X, k, sketch=so, zeta=8, want_S=False)
+    Qo, Ro = out["Q"], out["R"]
+    tolR = 1e-10 if dt == "f64" else 1e-4
+    assert _rel(Rg, Ro) <= tolR, _rel(Rg, Ro)
+    assert _rel(Qg, Qo) <= 10 * U64 * 10**c + (2 * U32 if dt == "f32" else 0), _rel(Qg, Qo)
+    # sketched orthonormality (eq:sketchedcond) with the oracle's Theta applied to both Q's
+    dg = oracle.orth_defect(oracle.sketch(Qg, k, sketch=so, zeta=8))
+    do = oracle.orth_defect(oracle.sketch(Qo, k, sketch=so, zeta=8))
+    tol = 1e-12 if dt == "f64" else 1e-5
+    assert dg <= max(tol, 10 * do), (dg, do)
+    if dt == "f64":
+        assert oracle.col_residual(X, Qg, Rg) <= 2.1 * U64 * n
+    cg, co = oracle.cond(Qg), oracle.cond(Qo)
+    assert abs(cg / co - 1) <= 1e-6 + 10 * U64 * 10**c + (4 * U32 if dt == "f32" else 0)
+    return dg, do
+
+
+@pytest.mark.parametrize("name,m,n,k,dt,sk,c", E2E)
+def test_factor_parity(cuda, name, m, n, k, dt, sk, c):
+    X = synth.make_X(m, n, c, dt)
+    plan = _plan(n, k, dt, sk)
+    Q, R, S = plan.factor(_t(X), want_S=True)
+    Qg, Rg, Sg = _np(Q), _np(R), _np(S)
+    _check_e2e(X, k, sk, c, Qg, Rg, plan, dt)
+    assert np.linalg.norm(Sg.T @ Sg - np.eye(n)) <= 50 * n * U64
+    # determinism: a second call is bit-identical
+    Q2, R2, _ = plan.factor(_t(X))
+    assert torch.equal(Q2, Q) and torch.equal(R2, R)
+
+
+def test_factor_C2_full_size(cuda):
+    cfg = synth.config("C2")
+    X = synth.make_X(cfg["m"], cfg["n"], cfg["log10_cond"], cfg["dtype"])
+    plan = _plan(cfg["n"], cfg["k"], cfg["dtype"])
+    Q, R, _ = plan.factor(_t(X))
+    _check_e2e(X, cfg["k"], "gaussian", cfg["log10_cond"], _np(Q), _np(R), plan, "f32")
+
+
+def test_factor_host_matches_device(cuda):
+    X = synth.make_X(50_000, 100, 5.0, "f32")
+    plan = _plan(100, 200, "f32")
+    Qd, Rd, _ = plan.factor(_t(X))
+    Xh = torch.from_numpy(X).pin_memory()
+    Qh, Rh, _ = plan.factor_host(Xh)
+    assert np.array_equal(_np(Qd), Qh.numpy()) and np.array_equal(_np(Rd), Rh.numpy())
+
+
+def test_factor_nccl_single_rank_comm(cuda):
+    # the collective path with a 1-rank NCCL communicator (all-reduce = identity) is bit-identical
+    X = _t(synth.make_X(30_000, 20, 3.0))
+    uid = rcq.comm_unique_id()
+    comm = rcq.comm_create(uid, 1, 0, 0)
+    try:
+        a = rcq.RCholQR(n=20, k=40, comm=comm)
+        b = rcq.RCholQR(n=20, k=40)
+        Qa, Ra, _ = a.factor(X)
+        Qb, Rb, _ = b.factor(X)
+        assert torch.equal(Qa, Qb) and torch.equal(Ra, Rb)
+        a.close()
+    finally:
+        rcq.comm_destroy(comm)
+
+
+# ---------------------------------------------------------------------------------- edge cases
+def test_factor_nonfinite_and_singular(cuda):
+    plan = _plan(10, 20, "f64")
+    X = synth.make_X(1000, 10, 2.0)
+    Xn = X.copy()
+    Xn[500, 3] = np.nan
+    Q = torch.full((1000, 10), 7.0, dtype=torch.float64, device="cuda")
+    with pytest.raises(rcq.RCholQRError) as e:
+        plan.factor(_t(Xn), Q=Q)
+    assert e.value.status == rcq.E_NONFINITE and bool((Q == 7.0).all())
+    Xz = X.copy()
+    Xz[:, 4] = 0.0
+    with pytest.raises(rcq.RCholQRError) as e:
+        plan.factor(_t(Xz), Q=Q)
+    assert e.value.status == rcq.E_SINGULAR and bool((Q == 7.0).all())
+    with pytest.raises(rcq.RCholQRError) as e:   # m = 0: P = 0, R singular
+        plan.factor(torch.empty((0, 10), dtype=torch.float64, device="cuda"))
+    assert e.value.status == rcq.E_SINGULAR
+
+
+def test_factor_invalid_args(cuda):
+    plan = _plan(10, 20, "f64")
+    X = _t(synth.make_X(100, 10, 1.0))
+    with pytest.raises(rcq.RCholQRError) as e:
+        plan.factor(X, Q=X)                       # Q aliases X
+    assert e.value.status == rcq.E_INVALID
+    with pytest.raises(rcq.RCholQRError) as e:
+        plan.factor(X, row_offset=-1)
+    assert e.value.status == rcq.E_INVALID
+    with pytest.raises(ValueError):
+        plan.factor(X.float())
+
+
+@pytest.mark.parametrize("m", [10, 31, 32, 33, 127, 129, 4097])
+def test_factor_ragged_m(cuda, m):
+    n, k = 8, 16
+    X = synth.make_X(m, n, 2.0)
+    plan = _plan(n, k, "f64")
+    Q, R, _ = plan.factor(_t(X))
+    out = oracle.factor(X, k, want_S=False)
+    assert _rel(_np(R), out["R"]) <= 1e-12 and _rel(_np(Q), out["Q"]) <= 1e-12
+
+
+# ---------------------------------------------------------------------------------- full size, sampled
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["C3", "C4", "C5"])
+def test_full_size_sampled(cuda, name):
+    """BASELINE.json full sizes in the bench's launch configuration; checked on sampled outputs
+    the oracle computes one by one (sketch entries, rows of Q) and on the exact QR of the GPU's P."""
+    cfg = synth.config(name)
+    m, n, k, dt = cfg["m"], cfg["n"], cfg["k"], cfg["dtype"]
+    sk = cfg["sketch"]
+    so = oracle.GAUSSIAN if sk == "gaussian" else oracle.SPARSE_SIGN
+    X = synth.make_X_torch(m, n, cfg["log10_cond"], dt)
+    plan = _plan(n, k, dt, sk)
+    Q, R, _ = plan.factor(X)
+    P = plan.sketch(X)                          # same kernels, deterministic
+    R2, _, st = plan.small_qr(P, want_S=False)
+    assert st == rcq.OK and torch.equal(R2, R)
+    Pn, Rn = _np(P), _np(R)
+    rng = np.random.default_rng(0)
+    cols = rng.choice(n, 3, replace=False)
+    for j in cols:
+        xj = _np(X[:, j].double())
+        for r in rng.choice(k, 2, replace=False):
+            ref = oracle.sketch_entry(xj, int(r), k, sketch=so, zeta=8)
+            assert abs(Pn[r, j] - ref) <= 1e-12 * np.linalg.norm(Pn[:, j]), (r, j, Pn[r, j], ref)
+        del xj
+    Ro, _, _ = oracle.householder(Pn, want_S=False)
+    assert _rel(Rn, Ro) <= 1e-13
+    rows = np.concatenate([[0, m - 1], rng.choice(m, 62, replace=False)])
+    Xs = _np(X[torch.from_numpy(rows).cuda()])
+    Qs = oracle.forward_subst(Xs, Ro)
+    assert _rel(_np(Q[torch.from_numpy(rows).cuda()]), Qs) <= 10 * U64 * 10**cfg["log10_cond"] + (2 * U32 if dt == "f32" else 0)
+    # sketched orthonormality at full size: A12 (fp64 defect ~ 2 u kappa; bound with margin 10x)
+    d = oracle.orth_defect(_np(plan.sketch(Q)))
+    tol = 1e-12 if dt == "f64" else 1e-5
+    assert d <= max(tol, 20 * U64 * 10**cfg["log10_cond"]), d
+    # cond(Q) from the fp64 Gram (reading A11: Marchenko-Pastur ~5.83 for k = 2n; <= 8)
+    Qd = Q.double()
+    G = _np(Qd.T @ Qd)
+    assert oracle.cond_from_gram(G) <= 8.0
