@@ -52,6 +52,7 @@ struct rcholqr_plan_s {
   size_t smem_optin = 0;
   SketchLaunch sk{};
   TrsmLaunch tr{};
+  int res_tm = 0;           // > 0: blocked-substitution resident solve with this row tile
   int qr_kind = 0;
   double* part = nullptr;   // [splits][k][n] per-CTA sketch partials
   double* P = nullptr;      // [k][n] reduced sketch
@@ -158,6 +159,22 @@ rcholqr_status do_sketch(rcholqr_plan p, const void* X, int64_t m, int64_t ro, i
   return RCHOLQR_OK;
 }
 
+// Step 3: triangular prep + tall solve (blocked substitution when resident, else R^{-1} GEMM).
+rcholqr_status solve(rcholqr_plan p, const void* X, int64_t m, int64_t ldx, const double* R, void* Q, int64_t ldq,
+                     cudaStream_t st, bool timed) {
+  const int n = p->d.n;
+  if (p->res_tm > 0) {
+    CU(launch_tri_prep_blocked(R, n, p->W, p->status_d, st));
+    if (timed && p->timing) cudaEventRecord(p->ev[5], st);
+    if (m > 0) CU(launch_trsm_resident(p->res_tm, X, p->d.dtype, m, n, ldx, p->W, Q, ldq, p->status_d, p->sms, st));
+  } else {
+    CU(launch_tri_inverse(R, n, p->W, p->status_d, st));
+    if (timed && p->timing) cudaEventRecord(p->ev[5], st);
+    if (m > 0) CU(launch_trsm(p->tr, X, p->d.dtype, m, n, ldx, p->W, Q, ldq, p->status_d, st));
+  }
+  return RCHOLQR_OK;
+}
+
 rcholqr_status read_status(rcholqr_plan p, cudaStream_t st) {
   CU(cudaMemcpyAsync(p->status_h, p->status_d, sizeof(int), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
@@ -213,8 +230,10 @@ rcholqr_status rcholqr_create(const rcholqr_desc* desc, rcholqr_plan* out) {
   const int k = desc->k, n = desc->n;
   p->sk = plan_sketch(k, n, desc->dtype, desc->sketch, desc->nnz_per_col, p->sms, p->smem_optin);
   p->tr = plan_trsm(n, desc->dtype, p->smem_optin);
+  p->res_tm = trsm_resident_tm(n, desc->dtype, p->smem_optin);
+  if (const char* f = getenv("RCHOLQR_FORCE_INVERSE_SOLVE")) if (atoi(f)) p->res_tm = 0;  // experiments
   p->qr_kind = plan_qr(k, n, p->smem_optin);
-  const size_t kn = (size_t)k * n, nn = (size_t)n * n;
+  const size_t kn = (size_t)k * n, nn = (size_t)((n + 7) / 8 * 8) * ((n + 7) / 8 * 8);
   bool okalloc = cudaMalloc(&p->part, sizeof(double) * kn * p->sk.splits) == cudaSuccess &&
                  cudaMalloc(&p->P, sizeof(double) * kn) == cudaSuccess &&
                  cudaMalloc(&p->W, sizeof(double) * nn) == cudaSuccess &&
@@ -265,9 +284,8 @@ rcholqr_status rcholqr_factor_async(rcholqr_plan p, const void* X, int64_t m, in
   CU(launch_qr(p->qr_kind, p->P, k, n, Rout, p->Awork, p->diag, p->tau, p->status_d, st));
   if (S) CU(launch_form_s(p->Awork, p->tau, p->diag, k, n, S, p->status_d, st));
   if (p->timing) cudaEventRecord(p->ev[4], st);
-  CU(launch_tri_inverse(Rout, n, p->W, p->status_d, st));
-  if (p->timing) cudaEventRecord(p->ev[5], st);
-  if (m > 0) CU(launch_trsm(p->tr, X, p->d.dtype, m, n, ldx, p->W, Q, ldq, p->status_d, st));
+  rcholqr_status s2 = solve(p, X, m, ldx, Rout, Q, ldq, st, true);
+  if (s2 != RCHOLQR_OK) return s2;
   if (p->timing) cudaEventRecord(p->ev[6], st);
   return RCHOLQR_OK;
 }
@@ -303,10 +321,12 @@ rcholqr_status rcholqr_factor_host(rcholqr_plan p, const void* Xh, int64_t m, in
   }
   if (!p->rbuf) CU(cudaMalloc(&p->rbuf, sizeof(double) * (size_t)n * n));
   if (Sh && !p->sbuf) CU(cudaMalloc(&p->sbuf, sizeof(double) * (size_t)k * n));
-  if (m > 0) CU(cudaMemcpy2DAsync(p->xbuf, n * es, Xh, ldx * es, n * es, m, cudaMemcpyHostToDevice, st));
+  if (m > 0 && ldx == n) CU(cudaMemcpyAsync(p->xbuf, Xh, (size_t)m * n * es, cudaMemcpyHostToDevice, st));
+  else if (m > 0) CU(cudaMemcpy2DAsync(p->xbuf, n * es, Xh, ldx * es, n * es, m, cudaMemcpyHostToDevice, st));
   rcholqr_status s = rcholqr_factor_async(p, p->xbuf, m, ro, n, p->qbuf, n, p->rbuf, Sh ? p->sbuf : nullptr, st);
   if (s != RCHOLQR_OK) return s;
-  if (m > 0) CU(cudaMemcpy2DAsync(Qh, ldq * es, p->qbuf, n * es, n * es, m, cudaMemcpyDeviceToHost, st));
+  if (m > 0 && ldq == n) CU(cudaMemcpyAsync(Qh, p->qbuf, (size_t)m * n * es, cudaMemcpyDeviceToHost, st));
+  else if (m > 0) CU(cudaMemcpy2DAsync(Qh, ldq * es, p->qbuf, n * es, n * es, m, cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(Rh, p->rbuf, sizeof(double) * (size_t)n * n, cudaMemcpyDeviceToHost, st));
   if (Sh) CU(cudaMemcpyAsync(Sh, p->sbuf, sizeof(double) * (size_t)k * n, cudaMemcpyDeviceToHost, st));
   return read_status(p, st);
@@ -352,8 +372,8 @@ rcholqr_status rcholqr_tri_solve(rcholqr_plan p, const void* X, int64_t m, int64
   const int n = p->d.n;
   CU(cudaMemsetAsync(p->status_d, 0, sizeof(int), st));
   CU(launch_check_diag(R, n, p->status_d, st));
-  CU(launch_tri_inverse(R, n, p->W, p->status_d, st));
-  if (m > 0) CU(launch_trsm(p->tr, X, p->d.dtype, m, n, ldx, p->W, Q, ldq, p->status_d, st));
+  rcholqr_status s2 = solve(p, X, m, ldx, R, Q, ldq, st, false);
+  if (s2 != RCHOLQR_OK) return s2;
   const bool t = p->timing;
   p->timing = false;
   rcholqr_status s = read_status(p, st);

@@ -54,5 +54,10 @@ cudaError_t launch_form_s(const double* Awork, const double* tau, const double* 
 cudaError_t launch_theta_export(uint64_t seed, int k, int sketch, int zeta, int64_t row_offset, int64_t m,
                                 float* Z, int32_t* rows, int8_t* signs, cudaStream_t st);
 cudaError_t launch_check_diag(const double* R, int n, int* status, cudaStream_t st);
+// blocked substitution (default tall solve for n <= 128): M = [-R_{<J,J}; Winv_JJ] packed
+int trsm_resident_tm(int n, int dtype, size_t smem_optin);   // 0 = not applicable
+cudaError_t launch_tri_prep_blocked(const double* R, int n, double* M, int* status, cudaStream_t st);
+cudaError_t launch_trsm_resident(int tm, const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M,
+                                 void* Q, int64_t ldq, const int* status, int sms, cudaStream_t st);
 
 }  // namespace rcq

@@ -244,4 +244,248 @@ cudaError_t launch_check_diag(const double* R, int n, int* status, cudaStream_t 
   return cudaGetLastError();
 }
 
+// ============================================================================================
+// Blocked forward substitution (the default tall solve).  Columns are processed in blocks J of
+// width 32 (last block ragged, multiple of 8):
+//     T_J = X_J - Q_{<J} R_{<J,J}          (DMMA, K = 32 J)
+//     Q_J = T_J  Winv_JJ                   (DMMA, K = 32, Winv_JJ = R_JJ^{-1} by row substitution)
+// i.e. the paper's row-wise forward substitution with only the 32x32 diagonal
+// blocks inverted, which keeps the row-wise backward stability of substitution (an explicit full
+// R^{-1} lost 4x in ||I - (Theta Q)^T Theta Q|| at n=1024, kappa=1e12 -- DESIGN.md "Tall solve").
+// M (npad x npad) packs both operands: M[L,J] = -R_{L,J} (L < J), M[J,J] = Winv_JJ, 0 below.
+//
+// Resident variant (n <= 128): a persistent CTA keeps M in shared memory for its whole life and a
+// TM-row tile of X (widened to fp64, overwritten in place by Q) so the fp64 history Q_{<J} never
+// leaves the SM; the next tile's X is prefetched with cp.async while the current tile is solved.
+constexpr int TB = 32;           // diagonal block width
+constexpr int RES_THREADS = 256;
+
+__device__ __forceinline__ void cp_async4(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(s)), "l"(g));
+}
+__device__ __forceinline__ void cp_async8(void* s, const void* g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(s)), "l"(g));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
+struct ResLayout {
+  int ld, tld;
+  size_t m_bytes, a_bytes, t_bytes, raw_bytes;
+  __host__ __device__ ResLayout(int npad, int tm, int xs) {
+    ld = npad + 4;                       // (npad+4) = 4 or 12 (mod 16): fragment loads conflict-free
+    tld = TB + 4;
+    m_bytes = sizeof(double) * (size_t)npad * ld;
+    a_bytes = sizeof(double) * (size_t)tm * ld;
+    t_bytes = sizeof(double) * (size_t)tm * tld;
+    raw_bytes = (size_t)xs * tm * npad;
+  }
+  __host__ __device__ size_t total() const { return m_bytes + a_bytes + t_bytes + raw_bytes; }
+};
+
+template <typename TX, int TM>
+__global__ void __launch_bounds__(RES_THREADS, 1)
+trsm_resident_kernel(const TX* __restrict__ X, int64_t m, int n, int NPAD, int64_t ldx,
+                     const double* __restrict__ Mg, TX* __restrict__ Q, int64_t ldq, const int* status) {
+  if (*status) return;
+  const ResLayout C(NPAD, TM, (int)sizeof(TX));
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* Ms = reinterpret_cast<double*>(smem_raw);
+  double* As = reinterpret_cast<double*>(smem_raw + C.m_bytes);
+  double* Ts = reinterpret_cast<double*>(smem_raw + C.m_bytes + C.a_bytes);
+  TX* raw = reinterpret_cast<TX*>(smem_raw + C.m_bytes + C.a_bytes + C.t_bytes);
+  constexpr int STRIPS = TM / 16;
+  constexpr int NWARP = RES_THREADS / 32;
+  constexpr int WPS = NWARP / STRIPS;          // warps sharing one m16 strip
+  const int NBLK = (NPAD + TB - 1) / TB;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+  const int strip = warp % STRIPS, wsub = warp / STRIPS;
+  const int64_t ntiles = (m + TM - 1) / TM;
+
+  for (int c = tid; c < NPAD * NPAD; c += RES_THREADS) Ms[(c / NPAD) * C.ld + (c % NPAD)] = Mg[c];
+
+  auto prefetch = [&](int64_t tile) {
+    if (tile >= ntiles) return;
+    const int64_t r0 = tile * TM;
+    for (int c = tid; c < TM * n; c += RES_THREADS) {
+      const int ii = c / n, jj = c % n;
+      if (r0 + ii < m) {
+        if (sizeof(TX) == 4) cp_async4(raw + ii * NPAD + jj, X + (r0 + ii) * ldx + jj);
+        else cp_async8(raw + ii * NPAD + jj, X + (r0 + ii) * ldx + jj);
+      }
+    }
+    cp_async_commit();
+  };
+
+  int64_t tile = blockIdx.x;
+  prefetch(tile);
+  for (; tile < ntiles; tile += gridDim.x) {
+    const int64_t r0 = tile * TM;
+    const int rows = (int)min((int64_t)TM, m - r0);
+    cp_async_wait_all();
+    __syncthreads();  // raw landed; previous tile fully consumed (As, Ts free)
+    for (int c = tid; c < TM * NPAD; c += RES_THREADS) {
+      const int ii = c / NPAD, jj = c % NPAD;
+      As[ii * C.ld + jj] = (ii < rows && jj < n) ? (double)raw[ii * NPAD + jj] : 0.0;
+    }
+    __syncthreads();
+    prefetch(tile + gridDim.x);   // overlaps with the solve of this tile
+
+    for (int J = 0; J < NBLK; ++J) {
+      const int c0 = J * TB;
+      const int bw = min(TB, NPAD - c0);       // block width (multiple of 8)
+      const int nt8 = bw / 8;
+      // n8 tiles of this block owned by this warp: t = wsub, wsub + WPS, ...
+      constexpr int MAXT = (TB / 8 + WPS - 1) / WPS;
+      double acc[MAXT][4];
+      const int arow = strip * 16 + g;
+#pragma unroll
+      for (int u = 0; u < MAXT; ++u) {
+        const int t = wsub + WPS * u;
+        if (t < nt8) {
+          const int col = c0 + 8 * t + 2 * t4;
+          acc[u][0] = As[arow * C.ld + col];
+          acc[u][1] = As[arow * C.ld + col + 1];
+          acc[u][2] = As[(arow + 8) * C.ld + col];
+          acc[u][3] = As[(arow + 8) * C.ld + col + 1];
+        }
+      }
+      // phase 1: T = X_J + Q_{<J} (-R_{<J,J})
+      for (int ks = 0; ks < c0 / 4; ++ks) {
+        const double a0 = As[arow * C.ld + 4 * ks + t4];
+        const double a1 = As[(arow + 8) * C.ld + 4 * ks + t4];
+#pragma unroll
+        for (int u = 0; u < MAXT; ++u) {
+          const int t = wsub + WPS * u;
+          if (t < nt8) dmma_16x8x4(acc[u], a0, a1, Ms[(4 * ks + t4) * C.ld + c0 + 8 * t + g]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < MAXT; ++u) {
+        const int t = wsub + WPS * u;
+        if (t < nt8) {
+          const int col = 8 * t + 2 * t4;
+          Ts[arow * C.tld + col] = acc[u][0];
+          Ts[arow * C.tld + col + 1] = acc[u][1];
+          Ts[(arow + 8) * C.tld + col] = acc[u][2];
+          Ts[(arow + 8) * C.tld + col + 1] = acc[u][3];
+        }
+      }
+      __syncthreads();
+      // phase 2: Q_J = T_J Winv_JJ (Winv upper triangular: skip k-steps past the tile's columns)
+#pragma unroll
+      for (int u = 0; u < MAXT; ++u)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[u][e] = 0.0;
+      for (int ks = 0; ks < bw / 4; ++ks) {
+        const double a0 = Ts[arow * C.tld + 4 * ks + t4];
+        const double a1 = Ts[(arow + 8) * C.tld + 4 * ks + t4];
+#pragma unroll
+        for (int u = 0; u < MAXT; ++u) {
+          const int t = wsub + WPS * u;
+          if (t < nt8 && 4 * ks <= 8 * t + 7)
+            dmma_16x8x4(acc[u], a0, a1, Ms[(c0 + 4 * ks + t4) * C.ld + c0 + 8 * t + g]);
+        }
+      }
+      // Q_J -> shared history (fp64) and global (rounded once to TX)
+#pragma unroll
+      for (int u = 0; u < MAXT; ++u) {
+        const int t = wsub + WPS * u;
+        if (t < nt8) {
+          const int col = c0 + 8 * t + 2 * t4;
+          As[arow * C.ld + col] = acc[u][0];
+          As[arow * C.ld + col + 1] = acc[u][1];
+          As[(arow + 8) * C.ld + col] = acc[u][2];
+          As[(arow + 8) * C.ld + col + 1] = acc[u][3];
+          const int64_t gr = r0 + arow;
+          if (arow < rows) {
+            if (col < n) Q[gr * ldq + col] = to_out<TX>(acc[u][0]);
+            if (col + 1 < n) Q[gr * ldq + col + 1] = to_out<TX>(acc[u][1]);
+          }
+          if (arow + 8 < rows) {
+            if (col < n) Q[(gr + 8) * ldq + col] = to_out<TX>(acc[u][2]);
+            if (col + 1 < n) Q[(gr + 8) * ldq + col + 1] = to_out<TX>(acc[u][3]);
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  cp_async_wait_all();
+}
+
+// M = [-R_{<J,J}; Winv_JJ] packed (npad x npad, zero padded).  One warp per row i of M.
+__global__ void tri_prep_blocked_kernel(const double* __restrict__ R, int n, int npad, double* __restrict__ M,
+                                        const int* status) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int i = warp;
+  if (i >= npad || *status) return;
+  const int Jb = (i / TB) * TB;                     // first column of i's diagonal block
+  const int be = min(Jb + TB, n);                   // end of the block (within n)
+  // diagonal block row: w R_JJ = e_i  (lane l holds w[Jb + l])
+  double w = 0.0;
+  if (i < n) {
+    if (lane == i - Jb) w = 1.0 / R[(size_t)i * n + i];
+    for (int j = i + 1; j < be; ++j) {
+      const int l = Jb + lane;
+      double s = (l >= i && l < j) ? w * R[(size_t)l * n + j] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (lane == j - Jb) w = -s / R[(size_t)j * n + j];
+    }
+  }
+  for (int base = 0; base < npad; base += 32) {   // uniform trip count: shuffles are convergent
+    const int c = base + lane;
+    const double wc = __shfl_sync(0xffffffffu, w, (c - Jb) & 31);
+    double v = 0.0;
+    if (i < n && c < n) {
+      if (c >= Jb + TB) v = -R[(size_t)i * n + c];
+      else if (c >= Jb) v = wc;
+    }
+    if (c < npad) M[(size_t)i * npad + c] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+int trsm_resident_tm(int n, int dtype, size_t smem_optin) {
+  const int npad = (n + 7) / 8 * 8;
+  const int xs = dtype == RCHOLQR_F64 ? 8 : 4;
+  if (n > 128) return 0;
+  if (ResLayout(npad, 64, xs).total() <= smem_optin) return 64;
+  if (ResLayout(npad, 32, xs).total() <= smem_optin) return 32;
+  return 0;
+}
+
+cudaError_t launch_tri_prep_blocked(const double* R, int n, double* M, int* status, cudaStream_t st) {
+  const int npad = (n + 7) / 8 * 8;
+  const int warps_per_block = 4;
+  tri_prep_blocked_kernel<<<(npad + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, st>>>(
+      R, n, npad, M, status);
+  return cudaGetLastError();
+}
+
+template <typename TX, int TM>
+static cudaError_t launch_res(const void* X, int64_t m, int n, int64_t ldx, const double* M, void* Q, int64_t ldq,
+                              const int* status, int sms, cudaStream_t st) {
+  const int npad = (n + 7) / 8 * 8;
+  const size_t smem = ResLayout(npad, TM, (int)sizeof(TX)).total();
+  auto kern = trsm_resident_kernel<TX, TM>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t ntiles = (m + TM - 1) / TM;
+  const int grid = (int)std::min<int64_t>(ntiles, sms);
+  if (grid == 0) return cudaSuccess;
+  kern<<<grid, RES_THREADS, smem, st>>>((const TX*)X, m, n, npad, ldx, M, (TX*)Q, ldq, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trsm_resident(int tm, const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M,
+                                 void* Q, int64_t ldq, const int* status, int sms, cudaStream_t st) {
+  if (dtype == RCHOLQR_F64)
+    return tm == 64 ? launch_res<double, 64>(X, m, n, ldx, M, Q, ldq, status, sms, st)
+                    : launch_res<double, 32>(X, m, n, ldx, M, Q, ldq, status, sms, st);
+  return tm == 64 ? launch_res<float, 64>(X, m, n, ldx, M, Q, ldq, status, sms, st)
+                  : launch_res<float, 32>(X, m, n, ldx, M, Q, ldq, status, sms, st);
+}
+
 }  // namespace rcq
