@@ -10,7 +10,7 @@ cond(Q), ||I - (Theta Q)^T Theta Q||, column residuals), written with numpy/LAPA
 
 Parity status of each oracle function ("Oracle pins"):
   philox4x32_10      pinned: Random123 known-answer vectors + ATen's independent Philox
-  ln32 / sincos2pi32 pinned: exhaustive 2^24-input comparison against fp64 libm
+  ln32 / sincos2pi_j pinned: exhaustive 2^23-input comparison against fp64 libm
   gauss4 / theta     pinned: moments, KS test vs N(0,1), E||Theta x||^2 = ||x||^2
   sparse_col         pinned: structural invariants (one row per block, +-1/sqrt(zeta)), chi^2
   sketch             pinned: exact rational Theta X on tiny inputs, n=1 closed form, linearity,
@@ -62,7 +62,7 @@ def _L():
             lib.oracle_ln32.argtypes = [ctypes.c_float]
             lib.oracle_ln32.restype = ctypes.c_float
             lib.oracle_ln32_batch.argtypes = [P, P, I64]
-            lib.oracle_sincos2pi32_batch.argtypes = [P, P, P, I64]
+            lib.oracle_sincos2pi_j_batch.argtypes = [P, P, P, I64]
             lib.oracle_gauss4.argtypes = [U64, U64, U32, P]
             lib.oracle_theta_gauss.argtypes = [U64, I32, U64, I32]
             lib.oracle_theta_gauss.restype = ctypes.c_double
@@ -121,11 +121,12 @@ def ln32(a) -> np.ndarray:
     return out
 
 
-def sincos2pi32(b):
-    b = np.ascontiguousarray(b, dtype=np.float32)
-    s = np.empty_like(b)
-    c = np.empty_like(b)
-    _L().oracle_sincos2pi32_batch(_ptr(b), _ptr(s), _ptr(c), b.size)
+def sincos2pi_j(j):
+    """sin, cos of 2 pi j 2^-23 for integer j in [0, 2^23) (fp32, normative transform)."""
+    j = np.ascontiguousarray(j, dtype=np.uint32)
+    s = np.empty(j.shape, dtype=np.float32)
+    c = np.empty(j.shape, dtype=np.float32)
+    _L().oracle_sincos2pi_j_batch(_ptr(j), _ptr(s), _ptr(c), j.size)
     return s, c
 
 

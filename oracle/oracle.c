@@ -84,37 +84,43 @@ static void philox_for(uint64_t seed, uint64_t i, uint32_t q, uint32_t domain, u
 static float u32_as_f32(uint32_t u) { float f; memcpy(&f, &u, 4); return f; }
 static uint32_t f32_as_u32(float f) { uint32_t u; memcpy(&u, &f, 4); return u; }
 
-/* natural log for a in [2^-24, 1]: a = 2^e f, f in [sqrt(1/2), sqrt(2)); t = (f-1)/(f+1);
- * ln f = 2t + t^3 (2/3 + t^2 (2/5 + t^2 (2/7 + t^2 2/9)))  (atanh series);
- * ln a = e*ln2_hi + (e*ln2_lo + ln f). */
+/* float(e) for a small integer e without a conversion instruction: 0x4B400000 is 1.5 * 2^23. */
+static float small_int_to_f32(int e) { return u32_as_f32((uint32_t)(0x4B400000 + e)) - 12582912.0f; }
+
+/* natural log for a in [2^-23, 1] (reading A1): a = 2^e f with f in [sqrt(1/2), sqrt(2)),
+ * s = f - 1 (exact), ln f = s P(s) with P the degree-9 polynomial below (Chebyshev fit of
+ * ln(1+s)/s on [sqrt(1/2)-1, sqrt(2)-1], coefficients rounded to fp32), Horner with fmaf;
+ * ln a = e*ln2_hi + (e*ln2_lo + ln f).  No division. */
 float oracle_ln32(float a) {
     uint32_t bits = f32_as_u32(a);
     int e = (int)(bits >> 23) - 127;
     float f = u32_as_f32((bits & 0x007FFFFFu) | 0x3F800000u);
     if (f > 0x1.6a09e6p+0f) { f = f * 0.5f; e = e + 1; }
-    float num = f - 1.0f;
-    float den = f + 1.0f;
-    float t = num / den;
-    float t2 = t * t;
-    float p = 0x1.c71c72p-3f;                 /* fl32(2/9) */
-    p = fmaf(p, t2, 0x1.24924ap-2f);          /* fl32(2/7) */
-    p = fmaf(p, t2, 0x1.99999ap-2f);          /* fl32(2/5) */
-    p = fmaf(p, t2, 0x1.555556p-1f);          /* fl32(2/3) */
-    float t3 = t * t2;
-    float lnf = fmaf(t3, p, 2.0f * t);
-    float ef = (float)e;
+    float s = f - 1.0f;
+    float p = -0x1.31335cp-4f;
+    p = fmaf(p, s, 0x1.064786p-3f);
+    p = fmaf(p, s, -0x1.0fb036p-3f);
+    p = fmaf(p, s, 0x1.22cf10p-3f);
+    p = fmaf(p, s, -0x1.5423b0p-3f);
+    p = fmaf(p, s, 0x1.999e86p-3f);
+    p = fmaf(p, s, -0x1.000424p-2f);
+    p = fmaf(p, s, 0x1.55555ep-2f);
+    p = fmaf(p, s, -0x1.fffff8p-2f);
+    p = fmaf(p, s, 1.0f);
+    float lnf = s * p;
+    float ef = small_int_to_f32(e);
     float r = fmaf(ef, 0x1.7f7d1cp-20f, lnf); /* ln2_lo */
     r = fmaf(ef, 0x1.62e4p-1f, r);            /* ln2_hi (16 significant bits: e*ln2_hi exact) */
     return r;
 }
 
-/* sin(2 pi b), cos(2 pi b) for b in [0,1): x = 4b, n = floor(x + 1/2), r = x - n in [-1/2,1/2),
- * angle = n*pi/2 + (pi/2) r; Taylor polynomials of sin/cos((pi/2) r). */
-void oracle_sincos2pi32(float b, float* s_out, float* c_out) {
-    float x = 4.0f * b;
-    float nf = floorf(x + 0.5f);
-    float r = x - nf;
-    int n = ((int)nf) & 3;
+/* sin(2 pi b), cos(2 pi b) for b = j 2^-23, j in [0, 2^23) (reading A1): quadrant
+ * n = (j + 2^20) >> 21, remainder ri = j - n 2^21 in [-2^20, 2^20), r = ri 2^-21 in [-1/2, 1/2)
+ * (exact); angle = n pi/2 + (pi/2) r; Taylor polynomials of sin/cos((pi/2) r) with fmaf. */
+void oracle_sincos2pi_j(uint32_t j, float* s_out, float* c_out) {
+    uint32_t n = (j + (1u << 20)) >> 21;
+    int ri = (int)j - (int)(n << 21);
+    float r = small_int_to_f32(ri) * 0x1p-21f;
     float r2 = r * r;
     float ps = 0x1.507834p-13f;
     ps = fmaf(ps, r2, -0x1.32d2ccp-8f);
@@ -129,7 +135,7 @@ void oracle_sincos2pi32(float b, float* s_out, float* c_out) {
     pc = fmaf(pc, r2, -0x1.3bd3ccp+0f);
     float c = fmaf(pc, r2, 1.0f);
     float so, co;
-    switch (n) {
+    switch (n & 3u) {
         case 0: so = s; co = c; break;
         case 1: so = c; co = -s; break;
         case 2: so = -s; co = -c; break;
@@ -138,17 +144,18 @@ void oracle_sincos2pi32(float b, float* s_out, float* c_out) {
     *s_out = so; *c_out = co;
 }
 
-/* Four N(0,1) draws z[0..3] for Theta rows 4q..4q+3 at global X-row i (domain 1). */
+/* Four N(0,1) draws z[0..3] for Theta rows 4q..4q+3 at global X-row i (domain 1): Box-Muller on
+ * the word pairs (w0, w1) and (w2, w3) with 23-bit uniforms ua = 2 - (1 + ja 2^-23) in (0, 1]
+ * (ja = wa >> 9) and angle index jb = wb >> 9. */
 void oracle_gauss4(uint64_t seed, uint64_t i, uint32_t q, float z[4]) {
     uint32_t w[4];
     philox_for(seed, i, q, 1u, w);
     for (int p = 0; p < 2; ++p) {
-        uint32_t wa = w[2 * p], wb = w[2 * p + 1];
-        float ua = (float)((wa >> 8) + 1u) * 0x1p-24f;   /* (0, 1] */
-        float ub = (float)(wb >> 8) * 0x1p-24f;          /* [0, 1) */
+        uint32_t ja = w[2 * p] >> 9, jb = w[2 * p + 1] >> 9;
+        float ua = 2.0f - u32_as_f32(0x3F800000u | ja);   /* exact: 1 - ja 2^-23 */
         float rho = sqrtf(-2.0f * oracle_ln32(ua));
         float s, c;
-        oracle_sincos2pi32(ub, &s, &c);
+        oracle_sincos2pi_j(jb, &s, &c);
         z[2 * p] = rho * c;
         z[2 * p + 1] = rho * s;
     }
@@ -181,8 +188,8 @@ void oracle_sparse_col(uint64_t seed, int k, int zeta, uint64_t i, int32_t* rows
 void oracle_ln32_batch(const float* a, float* out, int64_t n) {
     for (int64_t t = 0; t < n; ++t) out[t] = oracle_ln32(a[t]);
 }
-void oracle_sincos2pi32_batch(const float* b, float* s, float* c, int64_t n) {
-    for (int64_t t = 0; t < n; ++t) oracle_sincos2pi32(b[t], &s[t], &c[t]);
+void oracle_sincos2pi_j_batch(const uint32_t* j, float* s, float* c, int64_t n) {
+    for (int64_t t = 0; t < n; ++t) oracle_sincos2pi_j(j[t], &s[t], &c[t]);
 }
 /* Z: k x m row-major, Z[r*m + (i-row_offset)] = z_ri (unscaled N(0,1) draw, fp32). */
 void oracle_theta_gauss_z(uint64_t seed, int k, int64_t row_offset, int64_t m, float* Z) {

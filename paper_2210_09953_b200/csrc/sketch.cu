@@ -1,13 +1,14 @@
 // sketch.cu -- step 1 of RCholeskyQR: P = Theta X, fp64 accumulation.
 //
 // Gaussian Theta: a GEMM with M = k (Theta rows), N = n, K = m (rows of X).  Each CTA owns a
-// KT x NT tile of P and a contiguous range of X rows ("split"); per 32-row chunk it
-//   * generates the KT x 32 Theta tile in registers (Philox4x32-10 + Box-Muller, theta.cuh) and
-//     parks it in shared memory as fp64 (exact: Theta's draws are fp32),
-//   * stages the 32 x NT X tile (coalesced loads, fp32 -> fp64 exact widening),
-//   * runs DMMA m16n8k4 (FP64 tensor core) with register-resident accumulators,
-// double-buffered so the next chunk's generation and loads overlap this chunk's MMAs.  X is read
-// from HBM once per (tile_k) -- exactly once when one tile covers P (C1, C2).  Per-CTA partials
+// KT x NT tile of P and a contiguous range of X rows ("split"), and is warp-specialised:
+//   * 8 producer warps, per 32-row stage, generate the KT x 32 Theta tile in registers
+//     (Philox4x32-10 + Box-Muller, theta.cuh), park it in shared memory as fp64 (exact: the draws
+//     are fp32) and stage the 32 x NT X tile (coalesced loads, exact fp32 -> fp64 widening);
+//   * 8 MMA warps consume the stages with DMMA m16n8k4 (the FP64 tensor core) into register
+//     accumulators, the CTA's m16n8 output tiles split evenly so every SMSP's DMMA pipe is loaded
+//     alike; a 3-stage ring (named-barrier FULL/EMPTY handshake) overlaps generation with MMA.
+// X is read from HBM once per tile_k (C2: twice from L2-adjacent CTAs).  Per-CTA partials
 // go to a workspace and are summed in a fixed order (deterministic, bitwise reproducible), then
 // scaled once by fl(1/sqrt(k)) (reading A4).
 //
@@ -23,28 +24,67 @@
 
 namespace rcq {
 
-constexpr int KC = 32;  // X rows per pipeline chunk
+constexpr int KC = 32;             // X rows per pipeline stage
+constexpr int SK_MMA_WARPS = 16;   // 4 per SMSP; output tiles split so every SMSP's DMMA pipe is loaded alike
+constexpr int SK_PROD_WARPS = 8;   // Theta generation + X prefetch (2 per SMSP, 2 Philox chains each)
+constexpr int SK_THREADS = 32 * (SK_MMA_WARPS + SK_PROD_WARPS);
+constexpr size_t SK_SMEM_BUDGET = 200 * 1024;
 
-template <int WM, int WN, int MW, int NW>
+__device__ __forceinline__ void cp_async_zfill4(void* s, const void* g, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"((unsigned)__cvta_generic_to_shared(s)), "l"(g),
+               "r"(valid ? 4 : 0));
+}
+__device__ __forceinline__ void cp_async_zfill8(void* s, const void* g, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"((unsigned)__cvta_generic_to_shared(s)), "l"(g),
+               "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_async_commit_grp() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// Tile of P per CTA: MS m16 strips (Theta rows) x NS n8 tiles (X columns).
+template <typename TX, int MS, int NS>
 struct GCfg {
-  static constexpr int KT = 16 * MW * WM;
-  static constexpr int NT = 8 * NW * WN;
-  static constexpr int THREADS = 32 * WM * WN;
-  static constexpr int TS_LD = KC + 4;  // 36 doubles = 72 words: A-fragment loads conflict-free
-  static constexpr int XS_LD = NT + 4;  // NT+4 = 4 or 12 (mod 16): B-fragment loads conflict-free
-  static constexpr size_t SMEM = sizeof(double) * (2 * (size_t)KT * TS_LD + 2 * (size_t)KC * XS_LD);
-  static constexpr int XREG = (KC * NT + THREADS - 1) / THREADS;
+  static constexpr int KT = 16 * MS;
+  static constexpr int NT = 8 * NS;
+  static constexpr int UNITS = MS * NS;                                   // m16n8 output tiles
+  static constexpr int UMAX = (UNITS + SK_MMA_WARPS - 1) / SK_MMA_WARPS;   // per MMA warp
+  static constexpr int TS_LD = KC + 4;  // fp64 Theta: 36 doubles, A-fragment loads conflict-free
+  // X stage keeps X's own dtype (cp.async): B-fragment loads (4 rows x 8 cols) conflict-free when the
+  // row stride is 8 or 24 words (mod 32) for fp32, 4 or 12 doubles (mod 16) for fp64.
+  static constexpr int XS_LD = sizeof(TX) == 4 ? NT + ((40 - NT % 32) % 32 == 32 ? 0 : (40 - NT % 32) % 32)
+                                               : NT + 4;
+  static constexpr size_t T_BYTES = sizeof(double) * (size_t)KT * TS_LD;
+  static constexpr size_t X_BYTES = (sizeof(TX) * (size_t)KC * XS_LD + 15) / 16 * 16;
+  static constexpr size_t STAGE = T_BYTES + X_BYTES;
+  static constexpr int STAGES = (int)(SK_SMEM_BUDGET / STAGE) < 6 ? (int)(SK_SMEM_BUDGET / STAGE) : 6;  // barrier ids <= 13
+  static constexpr size_t SMEM = STAGE * STAGES;
+  static_assert(STAGES >= 2, "sketch tile too large for the stage ring");
 };
 
-template <typename TX, int WM, int WN, int MW, int NW>
-__global__ void __launch_bounds__(32 * WM * WN, 1)
+__device__ __forceinline__ void named_sync(int id, int count) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+__device__ __forceinline__ void named_arrive(int id, int count) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(count) : "memory");
+}
+
+// Warp-specialised Gaussian sketch.  Producer warps fill a STAGES-deep ring of (Theta tile fp64,
+// X tile in X's dtype) stages: the X tile of chunk c+1 is requested with cp.async (no register
+// staging) before Theta of chunk c is generated, so HBM latency hides behind the generator.  MMA
+// warps consume the stages with DMMA into register accumulators.  FULL(s) / EMPTY(s) are named
+// barriers (ids 1..2*STAGES).  The CTA's m16n8 output tiles are split contiguously over the 16 MMA
+// warps, so each SMSP (warps w, w+4, w+8, w+12) carries the same DMMA load to within one tile.
+template <typename TX, int MS, int NS>
+__global__ void __launch_bounds__(SK_THREADS, 1)
 sketch_gauss_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                     uint64_t seed, int tiles_k, int tiles_n, int64_t rows_per_split,
                     double* __restrict__ part) {
-  using C = GCfg<WM, WN, MW, NW>;
-  extern __shared__ __align__(16) double smem[];
-  double* Ts = smem;                              // [2][KT][TS_LD]  Theta tile (row r, X-row i)
-  double* Xs = smem + 2 * C::KT * C::TS_LD;       // [2][KC][XS_LD]  X tile (X-row i, column j)
+  using C = GCfg<TX, MS, NS>;
+  constexpr int S = C::STAGES;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  auto Tst = [&](int s) { return reinterpret_cast<double*>(smem_raw + (size_t)s * C::STAGE); };
+  auto Xst = [&](int s) { return reinterpret_cast<TX*>(smem_raw + (size_t)s * C::STAGE + C::T_BYTES); };
 
   const int tiles = tiles_k * tiles_n;
   const int tile = blockIdx.x % tiles, split = blockIdx.x / tiles;
@@ -53,103 +93,120 @@ sketch_gauss_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int
   const int64_t i_begin = (int64_t)split * rows_per_split;
   const int64_t i_end = min(m, i_begin + rows_per_split);
   const int nchunks = i_end > i_begin ? (int)((i_end - i_begin + KC - 1) / KC) : 0;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
-  const int wm = warp % WM, wn = warp / WM;
-
-  double acc[MW][NW][4];
+  if (warp >= SK_MMA_WARPS) {
+    // ------------------------------------------------------------------ producers
+    const int ptid = tid - 32 * SK_MMA_WARPS;
+    constexpr int PT = 32 * SK_PROD_WARPS;
+    auto issue_x = [&](int ch) {   // cp.async the X tile of chunk ch into its stage (zero-filled tails)
+      const int64_t i0 = i_begin + (int64_t)ch * KC;
+      TX* Xb = Xst(ch % S);
+      for (int c = ptid; c < KC * C::NT; c += PT) {
+        const int ii = c / C::NT, jj = c % C::NT;
+        const bool ok = i0 + ii < i_end && n0 + jj < n;
+        const TX* src = ok ? X + (i0 + ii) * ldx + n0 + jj : X;
+        if (sizeof(TX) == 4) cp_async_zfill4(Xb + ii * C::XS_LD + jj, src, ok);
+        else cp_async_zfill8(Xb + ii * C::XS_LD + jj, src, ok);
+      }
+      cp_async_commit_grp();
+    };
+    if (nchunks > 0) issue_x(0);
+    for (int ch = 0; ch < nchunks; ++ch) {
+      const int s = ch % S;
+      // stage of chunk ch+1 must be free before its X is requested
+      if (ch + 1 < nchunks) {
+        if (ch + 1 >= S) named_sync(1 + S + (ch + 1) % S, SK_THREADS);   // EMPTY(stage of ch+1)
+        issue_x(ch + 1);
+      } else {
+        cp_async_commit_grp();   // keep one group per iteration so wait_group(1) stays uniform
+      }
+      const int64_t i0 = i_begin + (int64_t)ch * KC;
+      double* T = Tst(s);
+      constexpr int NGEN = (C::KT / 4) * KC;
+      for (int c = ptid; c < NGEN; c += 2 * PT) {
 #pragma unroll
-  for (int a = 0; a < MW; ++a)
-#pragma unroll
-    for (int b = 0; b < NW; ++b)
-#pragma unroll
-      for (int c = 0; c < 4; ++c) acc[a][b][c] = 0.0;
-
-  // Theta tile for X rows i0 .. i0+KC-1: one Philox call -> 4 consecutive Theta rows.
-  auto gen_theta = [&](int buf, int64_t i0) {
-    double* T = Ts + buf * C::KT * C::TS_LD;
-    for (int c = tid; c < (C::KT / 4) * KC; c += C::THREADS) {
-      const int qq = c / KC, ii = c % KC;
-      const int rb = r0 + 4 * qq;
-      float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (i0 + ii < i_end && rb < k) z = gauss4(seed, (uint64_t)(row_offset + i0 + ii), (uint32_t)(rb >> 2));
-      double* Tc = T + (4 * qq) * C::TS_LD + ii;
-      Tc[0 * C::TS_LD] = (rb + 0 < k) ? (double)z.x : 0.0;
-      Tc[1 * C::TS_LD] = (rb + 1 < k) ? (double)z.y : 0.0;
-      Tc[2 * C::TS_LD] = (rb + 2 < k) ? (double)z.z : 0.0;
-      Tc[3 * C::TS_LD] = (rb + 3 < k) ? (double)z.w : 0.0;
+        for (int v = 0; v < 2; ++v) {          // two independent Philox/Box-Muller chains (ILP 2)
+          const int cc = c + v * PT;
+          if (cc < NGEN) {
+            const int qq = cc / KC, ii = cc % KC;
+            const int rb = r0 + 4 * qq;
+            float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (i0 + ii < i_end && rb < k) z = gauss4(seed, (uint64_t)(row_offset + i0 + ii), (uint32_t)(rb >> 2));
+            double* Tc = T + (4 * qq) * C::TS_LD + ii;
+            Tc[0 * C::TS_LD] = (rb + 0 < k) ? (double)z.x : 0.0;
+            Tc[1 * C::TS_LD] = (rb + 1 < k) ? (double)z.y : 0.0;
+            Tc[2 * C::TS_LD] = (rb + 2 < k) ? (double)z.z : 0.0;
+            Tc[3 * C::TS_LD] = (rb + 3 < k) ? (double)z.w : 0.0;
+          }
+        }
+      }
+      cp_async_wait_1();                        // this thread's copies for chunk ch have landed
+      named_arrive(1 + s, SK_THREADS);          // FULL(s): Theta + X of chunk ch visible to MMA warps
     }
-  };
-  TX xr[C::XREG];
-  auto load_x = [&](int64_t i0) {
-#pragma unroll
-    for (int u = 0; u < C::XREG; ++u) {
-      const int c = tid + u * C::THREADS;
-      const int ii = c / C::NT, jj = c % C::NT;
-      TX v = TX(0);
-      if (c < KC * C::NT && i0 + ii < i_end && n0 + jj < n) v = __ldcs(X + (i0 + ii) * ldx + n0 + jj);
-      xr[u] = v;
-    }
-  };
-  auto store_x = [&](int buf) {
-    double* Xb = Xs + buf * KC * C::XS_LD;
-#pragma unroll
-    for (int u = 0; u < C::XREG; ++u) {
-      const int c = tid + u * C::THREADS;
-      if (c < KC * C::NT) Xb[(c / C::NT) * C::XS_LD + (c % C::NT)] = (double)xr[u];
-    }
-  };
-
-  if (nchunks > 0) {
-    load_x(i_begin);
-    gen_theta(0, i_begin);
-    store_x(0);
+    cp_async_wait_0();
+    return;
   }
-  __syncthreads();
+
+  // -------------------------------------------------------------------- MMA warps
+  const int g = lane >> 2, t4 = lane & 3;
+  const int u_begin = (warp * C::UNITS) / SK_MMA_WARPS;
+  const int u_end = ((warp + 1) * C::UNITS) / SK_MMA_WARPS;
+  const int nun = u_end - u_begin;
+  const int sA = u_begin / NS, tA = u_begin % NS;
+  const int nA = min(nun, NS - tA);                 // units in strip sA; the rest are in sA + 1
+  static_assert(C::UMAX <= NS + 1, "a warp's units must span at most two strips");
+  double acc[C::UMAX][4];
+#pragma unroll
+  for (int u = 0; u < C::UMAX; ++u)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[u][e] = 0.0;
+  int bcol[C::UMAX];                                // B-fragment column offset of each unit
+#pragma unroll
+  for (int u = 0; u < C::UMAX; ++u) bcol[u] = ((u < nA) ? tA + u : u - nA) * 8 + g;
+  const int rowA = sA * 16 + g, rowB = min(sA + 1, MS - 1) * 16 + g;
+
   for (int ch = 0; ch < nchunks; ++ch) {
-    const int buf = ch & 1;
-    const bool more = ch + 1 < nchunks;
-    const int64_t inext = i_begin + (int64_t)(ch + 1) * KC;
-    if (more) load_x(inext);
-    if (more) gen_theta(buf ^ 1, inext);
-    const double* T = Ts + buf * C::KT * C::TS_LD;
-    const double* Xb = Xs + buf * KC * C::XS_LD;
-#pragma unroll
+    const int s = ch % S;
+    named_sync(1 + s, SK_THREADS);                                         // FULL(s)
+    const double* T = Tst(s);
+    const TX* Xb = Xst(s);
+#pragma unroll 2
     for (int ks = 0; ks < KC / 4; ++ks) {
-      double a0[MW], a1[MW];
+      const double* Tk = T + 4 * ks + t4;
+      const double aA0 = Tk[rowA * C::TS_LD], aA1 = Tk[(rowA + 8) * C::TS_LD];
+      const double aB0 = Tk[rowB * C::TS_LD], aB1 = Tk[(rowB + 8) * C::TS_LD];
+      const TX* xrow = Xb + (4 * ks + t4) * C::XS_LD;
+      double b[C::UMAX];
 #pragma unroll
-      for (int mw = 0; mw < MW; ++mw) {
-        const int row = (wm * MW + mw) * 16 + g;
-        a0[mw] = T[row * C::TS_LD + 4 * ks + t4];
-        a1[mw] = T[(row + 8) * C::TS_LD + 4 * ks + t4];
-      }
+      for (int u = 0; u < C::UMAX; ++u) b[u] = (u < nun) ? (double)xrow[bcol[u]] : 0.0;
 #pragma unroll
-      for (int nw = 0; nw < NW; ++nw) {
-        const double b = Xb[(4 * ks + t4) * C::XS_LD + (wn * NW + nw) * 8 + g];
-#pragma unroll
-        for (int mw = 0; mw < MW; ++mw) dmma_16x8x4(acc[mw][nw], a0[mw], a1[mw], b);
+      for (int u = 0; u < C::UMAX; ++u) {
+        if (u < nun) {
+          const bool inA = u < nA;
+          dmma_16x8x4(acc[u], inA ? aA0 : aB0, inA ? aA1 : aB1, b[u]);
+        }
       }
     }
-    if (more) store_x(buf ^ 1);
-    __syncthreads();
+    if (ch + S < nchunks) named_arrive(1 + S + s, SK_THREADS);            // EMPTY(s)
   }
 
   double* Pp = part + (size_t)split * (size_t)k * n;
 #pragma unroll
-  for (int mw = 0; mw < MW; ++mw)
-#pragma unroll
-    for (int nw = 0; nw < NW; ++nw) {
-      const int row = r0 + (wm * MW + mw) * 16 + g;
-      const int col = n0 + (wn * NW + nw) * 8 + 2 * t4;
+  for (int u = 0; u < C::UMAX; ++u) {
+    if (u < nun) {
+      const int row = r0 + ((u < nA) ? sA : sA + 1) * 16 + g;
+      const int col = n0 + (bcol[u] - g) + 2 * t4;
       if (row < k) {
-        if (col < n) Pp[(size_t)row * n + col] = acc[mw][nw][0];
-        if (col + 1 < n) Pp[(size_t)row * n + col + 1] = acc[mw][nw][1];
+        if (col < n) Pp[(size_t)row * n + col] = acc[u][0];
+        if (col + 1 < n) Pp[(size_t)row * n + col + 1] = acc[u][1];
       }
       if (row + 8 < k) {
-        if (col < n) Pp[(size_t)(row + 8) * n + col] = acc[mw][nw][2];
-        if (col + 1 < n) Pp[(size_t)(row + 8) * n + col + 1] = acc[mw][nw][3];
+        if (col < n) Pp[(size_t)(row + 8) * n + col] = acc[u][2];
+        if (col + 1 < n) Pp[(size_t)(row + 8) * n + col + 1] = acc[u][3];
       }
     }
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -255,12 +312,12 @@ __global__ void theta_sparse_export_kernel(uint64_t seed, int k, int zeta, int64
 
 // ---------------------------------------------------------------------------------------------
 // Host side.
-template <int WM, int WN, int MW, int NW>
-static void fill_gauss(SketchLaunch& L, int kind, int k, int n) {
-  using C = GCfg<WM, WN, MW, NW>;
-  L.kind = kind; L.KT = C::KT; L.NT = C::NT; L.threads = C::THREADS; L.smem = C::SMEM;
-  L.tiles_k = (k + C::KT - 1) / C::KT;
-  L.tiles_n = (n + C::NT - 1) / C::NT;
+template <int MS, int NS>
+static void fill_gauss(SketchLaunch& L, int kind, int k, int n, int dtype) {
+  L.kind = kind; L.KT = 16 * MS; L.NT = 8 * NS; L.threads = SK_THREADS;
+  L.smem = dtype == RCHOLQR_F64 ? GCfg<double, MS, NS>::SMEM : GCfg<float, MS, NS>::SMEM;
+  L.tiles_k = (k + L.KT - 1) / L.KT;
+  L.tiles_n = (n + L.NT - 1) / L.NT;
 }
 
 // Choose the number of row splits so tiles*splits fills whole waves of one CTA per SM.
@@ -280,7 +337,6 @@ static int choose_splits(int tiles, int sms) {
 
 SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms, size_t smem_optin) {
   SketchLaunch L{};
-  (void)dtype;
   if (sketch == RCHOLQR_SPARSE_SIGN) {
     L.kind = kSketchSparse;
     L.threads = SPARSE_THREADS;
@@ -298,23 +354,21 @@ SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms,
     return L;
   }
   // Gaussian: pick the tile minimising padded work (tiles * KT * NT), ties -> larger tile.
-  constexpr int NC = 5;
+  constexpr int NC = 4;
   SketchLaunch cand[NC];
-  fill_gauss<4, 1, 1, 4>(cand[0], kSketchG64x32, k, n);
-  fill_gauss<8, 1, 1, 8>(cand[1], kSketchG128x64, k, n);
-  fill_gauss<7, 1, 1, 13>(cand[2], kSketchG112x104, k, n);
-  fill_gauss<13, 1, 1, 7>(cand[3], kSketchG208x56, k, n);
-  fill_gauss<4, 4, 2, 4>(cand[4], kSketchG128x128, k, n);
+  fill_gauss<3, 3>(cand[0], kSketchG48x24, k, n, dtype);
+  fill_gauss<8, 8>(cand[1], kSketchG128x64, k, n, dtype);
+  fill_gauss<7, 13>(cand[2], kSketchG112x104, k, n, dtype);
+  fill_gauss<4, 8>(cand[3], kSketchG64x64, k, n, dtype);
   int best = NC - 1;
   double best_cost = 1e300;
   const char* force = getenv("RCHOLQR_SKETCH_KIND");  // experiments only
   for (int c = 0; c < NC; ++c) {
     if (force && atoi(force) != cand[c].kind) continue;
     if (cand[c].smem > smem_optin) continue;
-    // padded MMA work + a per-tile Theta regeneration/X re-read penalty
+    // padded MMA work + a per-tile Theta regeneration / X re-read penalty
     const double padded = (double)cand[c].tiles_k * cand[c].KT * cand[c].tiles_n * cand[c].NT;
-    const double cost = padded * (1.0 + 0.05 * (cand[c].tiles_n - 1) + 0.02 * (cand[c].tiles_k - 1)) /
-                        (cand[c].threads >= 256 ? 1.0 : 1.15);
+    const double cost = padded * (1.0 + 0.05 * (cand[c].tiles_n - 1) + 0.02 * (cand[c].tiles_k - 1));
     if (cost < best_cost) { best_cost = cost; best = c; }
   }
   L = cand[best];
@@ -322,14 +376,14 @@ SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms,
   return L;
 }
 
-template <typename TX, int WM, int WN, int MW, int NW>
+template <typename TX, int MS, int NS>
 static cudaError_t launch_g(const SketchLaunch& L, const void* X, int64_t m, int n, int64_t ldx, int64_t ro,
                             int k, uint64_t seed, int64_t rps, double* part, cudaStream_t st) {
-  auto kern = sketch_gauss_kernel<TX, WM, WN, MW, NW>;
+  auto kern = sketch_gauss_kernel<TX, MS, NS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
   if (e != cudaSuccess) return e;
-  kern<<<L.tiles_k * L.tiles_n * L.splits, L.threads, L.smem, st>>>((const TX*)X, m, n, ldx, ro, k, seed,
-                                                                    L.tiles_k, L.tiles_n, rps, part);
+  kern<<<L.tiles_k * L.tiles_n * L.splits, SK_THREADS, L.smem, st>>>((const TX*)X, m, n, ldx, ro, k, seed,
+                                                                     L.tiles_k, L.tiles_n, rps, part);
   return cudaGetLastError();
 }
 
@@ -338,11 +392,10 @@ static cudaError_t launch_gauss_typed(const SketchLaunch& L, const void* X, int6
                                       int64_t ro, int k, uint64_t seed, int64_t rps, double* part,
                                       cudaStream_t st) {
   switch (L.kind) {
-    case kSketchG64x32: return launch_g<TX, 4, 1, 1, 4>(L, X, m, n, ldx, ro, k, seed, rps, part, st);
-    case kSketchG128x64: return launch_g<TX, 8, 1, 1, 8>(L, X, m, n, ldx, ro, k, seed, rps, part, st);
-    case kSketchG112x104: return launch_g<TX, 7, 1, 1, 13>(L, X, m, n, ldx, ro, k, seed, rps, part, st);
-    case kSketchG208x56: return launch_g<TX, 13, 1, 1, 7>(L, X, m, n, ldx, ro, k, seed, rps, part, st);
-    default: return launch_g<TX, 4, 4, 2, 4>(L, X, m, n, ldx, ro, k, seed, rps, part, st);
+    case kSketchG48x24: return launch_g<TX, 3, 3>(L, X, m, n, ldx, ro, k, seed, rps, part, st);
+    case kSketchG128x64: return launch_g<TX, 8, 8>(L, X, m, n, ldx, ro, k, seed, rps, part, st);
+    case kSketchG112x104: return launch_g<TX, 7, 13>(L, X, m, n, ldx, ro, k, seed, rps, part, st);
+    default: return launch_g<TX, 4, 8>(L, X, m, n, ldx, ro, k, seed, rps, part, st);
   }
 }
 

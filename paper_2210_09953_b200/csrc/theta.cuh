@@ -31,30 +31,39 @@ __device__ __forceinline__ uint4 philox_at(uint64_t seed, uint64_t i, uint32_t q
                        (uint32_t)(seed >> 32));
 }
 
-// ln(a), a in [2^-24, 1]: a = 2^e f, f in [sqrt(1/2), sqrt(2)); t = (f-1)/(f+1);
-// ln f = 2t + t^3 (2/3 + t^2 (2/5 + t^2 (2/7 + t^2 * 2/9))); ln a = e ln2_hi + (e ln2_lo + ln f).
+// Exact small-integer -> fp32 without an I2F: 0x4B400000 is 1.5 * 2^23.
+__device__ __forceinline__ float small_int_f32(int e) {
+  return __fsub_rn(__int_as_float(0x4B400000 + e), 12582912.0f);
+}
+
+// ln(a), a in [2^-23, 1]: a = 2^e f, f in [sqrt(1/2), sqrt(2)), s = f - 1;
+// ln f = s P(s), P degree 9 (A1 coefficients); ln a = e ln2_hi + (e ln2_lo + ln f).
 __device__ __forceinline__ float ln_unit(float a) {
   const uint32_t bits = __float_as_uint(a);
   int e = (int)(bits >> 23) - 127;
   float f = __uint_as_float((bits & 0x007FFFFFu) | 0x3F800000u);
   if (f > 0x1.6a09e6p+0f) { f = __fmul_rn(f, 0.5f); e += 1; }
-  const float t = __fdiv_rn(__fsub_rn(f, 1.0f), __fadd_rn(f, 1.0f));
-  const float t2 = __fmul_rn(t, t);
-  float p = 0x1.c71c72p-3f;
-  p = __fmaf_rn(p, t2, 0x1.24924ap-2f);
-  p = __fmaf_rn(p, t2, 0x1.99999ap-2f);
-  p = __fmaf_rn(p, t2, 0x1.555556p-1f);
-  const float lnf = __fmaf_rn(__fmul_rn(t, t2), p, __fmul_rn(2.0f, t));
-  const float ef = (float)e;  // exact: |e| <= 24
+  const float s = __fsub_rn(f, 1.0f);
+  float p = -0x1.31335cp-4f;
+  p = __fmaf_rn(p, s, 0x1.064786p-3f);
+  p = __fmaf_rn(p, s, -0x1.0fb036p-3f);
+  p = __fmaf_rn(p, s, 0x1.22cf10p-3f);
+  p = __fmaf_rn(p, s, -0x1.5423b0p-3f);
+  p = __fmaf_rn(p, s, 0x1.999e86p-3f);
+  p = __fmaf_rn(p, s, -0x1.000424p-2f);
+  p = __fmaf_rn(p, s, 0x1.55555ep-2f);
+  p = __fmaf_rn(p, s, -0x1.fffff8p-2f);
+  p = __fmaf_rn(p, s, 1.0f);
+  const float lnf = __fmul_rn(s, p);
+  const float ef = small_int_f32(e);
   return __fmaf_rn(ef, 0x1.62e4p-1f, __fmaf_rn(ef, 0x1.7f7d1cp-20f, lnf));
 }
 
-// sin/cos(2 pi b), b in [0,1): x = 4b, n = floor(x + 1/2), r = x - n; angle = n pi/2 + (pi/2) r.
-__device__ __forceinline__ void sincos_2pi(float b, float& so, float& co) {
-  const float x = __fmul_rn(4.0f, b);
-  const float nf = floorf(__fadd_rn(x, 0.5f));
-  const float r = __fsub_rn(x, nf);
-  const int n = ((int)nf) & 3;
+// sin/cos(2 pi j 2^-23): n = (j + 2^20) >> 21, ri = j - n 2^21, r = ri 2^-21; angle = n pi/2 + (pi/2) r.
+__device__ __forceinline__ void sincos_2pi_j(uint32_t j, float& so, float& co) {
+  const uint32_t n = (j + (1u << 20)) >> 21;
+  const int ri = (int)j - (int)(n << 21);
+  const float r = __fmul_rn(small_int_f32(ri), 0x1p-21f);
   const float r2 = __fmul_rn(r, r);
   float ps = 0x1.507834p-13f;
   ps = __fmaf_rn(ps, r2, -0x1.32d2ccp-8f);
@@ -68,17 +77,19 @@ __device__ __forceinline__ void sincos_2pi(float b, float& so, float& co) {
   pc = __fmaf_rn(pc, r2, 0x1.03c1f0p-2f);
   pc = __fmaf_rn(pc, r2, -0x1.3bd3ccp+0f);
   const float c = __fmaf_rn(pc, r2, 1.0f);
-  so = (n == 0) ? s : (n == 1) ? c : (n == 2) ? -s : -c;
-  co = (n == 0) ? c : (n == 1) ? -s : (n == 2) ? -c : s;
+  const uint32_t q = n & 3u;
+  const float sa = (q & 1u) ? c : s;      // |sin| source
+  const float ca = (q & 1u) ? s : c;      // |cos| source
+  so = (q >= 2u) ? -sa : sa;
+  co = (q == 1u || q == 2u) ? -ca : ca;
 }
 
-// Box-Muller on one Philox word pair: z_a = rho cos, z_b = rho sin.
+// Box-Muller on one Philox word pair: ua = 2 - (1 + ja 2^-23) in (0, 1], angle index jb.
 __device__ __forceinline__ void box_muller(uint32_t wa, uint32_t wb, float& za, float& zb) {
-  const float ua = __fmul_rn(__uint2float_rn((wa >> 8) + 1u), 0x1p-24f);  // (0, 1]
-  const float ub = __fmul_rn(__uint2float_rn(wb >> 8), 0x1p-24f);         // [0, 1)
+  const float ua = __fsub_rn(2.0f, __uint_as_float(0x3F800000u | (wa >> 9)));
   const float rho = __fsqrt_rn(__fmul_rn(-2.0f, ln_unit(ua)));
   float s, c;
-  sincos_2pi(ub, s, c);
+  sincos_2pi_j(wb >> 9, s, c);
   za = __fmul_rn(rho, c);
   zb = __fmul_rn(rho, s);
 }

@@ -64,41 +64,42 @@ def test_philox_matches_aten(aten_philox):
 
 
 def test_ln32_exhaustive_vs_libm():
-    # every uniform the transform can see: a = j 2^-24, j = 1..2^24 (reading A1)
-    a = (np.arange(1, 2**24 + 1, dtype=np.float64) * 2.0**-24).astype(np.float32)
+    # every uniform the transform can see: a = 1 - j 2^-23, j = 0..2^23-1 (reading A1)
+    a = (1.0 - np.arange(0, 2**23, dtype=np.float64) * 2.0**-23).astype(np.float32)
     got = oracle.ln32(a).astype(np.float64)
     ref = np.log(a.astype(np.float64))
     ulp = np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64)
     ulp[ref == 0] = np.spacing(np.float32(0))
     err = np.abs(got - ref) / ulp
-    assert err.max() <= 2.0, err.max()      # measured 1.68 ulp
-    assert got[-1] == 0.0                    # ln(1) = 0 exactly
-    assert np.all(np.diff(got) >= 0)         # monotone
+    assert err.max() <= 2.0, err.max()      # measured 1.5 ulp
+    assert got[0] == 0.0                     # ln(1) = 0 exactly
+    assert np.all(np.diff(got) <= 0)         # monotone (a decreasing)
 
 
-def test_sincos2pi32_exhaustive_vs_libm():
-    b = (np.arange(0, 2**24, dtype=np.float64) * 2.0**-24).astype(np.float32)
-    s, c = oracle.sincos2pi32(b)
-    ang = 2.0 * np.pi * b.astype(np.float64)
+def test_sincos2pi_j_exhaustive_vs_libm():
+    j = np.arange(0, 2**23, dtype=np.uint32)
+    s, c = oracle.sincos2pi_j(j)
+    ang = 2.0 * np.pi * j.astype(np.float64) * 2.0**-23
     es = np.abs(s - np.sin(ang))
     ec = np.abs(c - np.cos(ang))
     assert es.max() <= 1.6 * 2.0**-24 and ec.max() <= 1.6 * 2.0**-24, (es.max(), ec.max())
     # exact special angles
     assert s[0] == 0.0 and c[0] == 1.0
-    q = 2**22  # b = 1/4, 1/2, 3/4
+    q = 2**21  # j 2^-23 = 1/4, 1/2, 3/4
     assert (s[q], c[q]) == (1.0, 0.0) and (s[2 * q], c[2 * q]) == (0.0, -1.0) and (s[3 * q], c[3 * q]) == (-1.0, 0.0)
     assert np.all(np.abs(s.astype(np.float64) ** 2 + c.astype(np.float64) ** 2 - 1) < 4e-7)
 
 
 def test_gauss4_box_muller_definition():
-    # z = sqrt(-2 ln ua) (cos 2 pi ub, sin 2 pi ub) with the spec's uniforms, checked in fp64.
-    for (seed, i, q) in [(0, 0, 0), (0, 12345, 7), (2**63 + 5, 2**40 + 3, 99)]:
+    # z = sqrt(-2 ln ua) (cos 2 pi ub, sin 2 pi ub), ua = 1 - (wa >> 9) 2^-23, ub = (wb >> 9) 2^-23,
+    # checked against fp64 libm.
+    for (seed, i, q) in [(0, 0, 0), (0, 12345, 7), (2**63 + 5, 2**40 + 3, 99), (17, 2**32 + 1, 2**20)]:
         z = oracle.gauss4(seed, i, q).astype(np.float64)
         ctr = [i & 0xFFFFFFFF, i >> 32, q, 1]
         w = oracle.philox4x32_10(ctr, [seed & 0xFFFFFFFF, seed >> 32]).astype(np.uint64)
         for p in range(2):
-            ua = ((w[2 * p] >> 8) + 1) * 2.0**-24
-            ub = (w[2 * p + 1] >> 8) * 2.0**-24
+            ua = 1.0 - (w[2 * p] >> 9) * 2.0**-23
+            ub = (w[2 * p + 1] >> 9) * 2.0**-23
             rho = np.sqrt(-2.0 * np.log(ua))
             assert abs(z[2 * p] - rho * np.cos(2 * np.pi * ub)) <= 8e-7 * max(1.0, rho)
             assert abs(z[2 * p + 1] - rho * np.sin(2 * np.pi * ub)) <= 8e-7 * max(1.0, rho)
