@@ -53,12 +53,17 @@ struct rcholqr_plan_s {
   SketchLaunch sk{};
   TrsmLaunch tr{};
   int res_tm = 0;           // > 0: blocked-substitution resident solve with this row tile
+  int warp_solve = 0;       // > 0: warp-independent blocked substitution with this many warps/CTA
+  int stream_tb = 0;        // > 0: streamed blocked substitution (fp64, n > 128) with this block width
+  double* tbuf = nullptr;   // [m_local][stream_tb] T_J workspace of the streamed solve
+  size_t tbuf_elems = 0;
   int qr_kind = 0;
-  double* part = nullptr;   // [splits][k][n] per-CTA sketch partials
+  double* part = nullptr;   // [splits][k][n] per-CTA sketch partials (running sums)
+  double* partc = nullptr;  // [splits][k][n] their TwoSum compensations (Gaussian sketch)
   double* P = nullptr;      // [k][n] reduced sketch
   double* W = nullptr;      // [n][n] R^{-1}
   double* Awork = nullptr;  // [n][k] column-major Householder workspace (reflectors)
-  double* diag = nullptr;   // [n] raw pivots (sign before normalisation)
+  double* diag = nullptr;   // [2n] raw pivots (sign before normalisation), then reflector heads v0
   double* tau = nullptr;    // [n] reflector scalings
   double* Rtmp = nullptr;   // [n][n] R when the caller does not want one
   int* status_d = nullptr;
@@ -143,7 +148,7 @@ rcholqr_status do_sketch(rcholqr_plan p, const void* X, int64_t m, int64_t ro, i
   const auto& d = p->d;
   if (m > 0) {
     if (p->timing) cudaEventRecord(p->ev[0], st);
-    CU(launch_sketch(p->sk, X, d.dtype, m, d.n, ldx, ro, d.k, d.nnz_per_col, d.seed, p->part, P, p->status_d, st,
+    CU(launch_sketch(p->sk, X, d.dtype, m, d.n, ldx, ro, d.k, d.nnz_per_col, d.seed, p->part, p->partc, P, p->status_d, st,
                      p->timing ? p->ev[1] : nullptr));
   } else {
     if (p->timing) { cudaEventRecord(p->ev[0], st); cudaEventRecord(p->ev[1], st); }
@@ -163,7 +168,35 @@ rcholqr_status do_sketch(rcholqr_plan p, const void* X, int64_t m, int64_t ro, i
 rcholqr_status solve(rcholqr_plan p, const void* X, int64_t m, int64_t ldx, const double* R, void* Q, int64_t ldq,
                      cudaStream_t st, bool timed) {
   const int n = p->d.n;
-  if (p->res_tm > 0) {
+  if (p->stream_tb > 0) {
+    // blocked substitution by column blocks of width tb, each = 2 fp64 DMMA GEMM launches
+    const int tb = p->stream_tb, npad = (n + 7) / 8 * 8;
+    CU(launch_tri_prep_blocked(R, n, p->W, p->status_d, st, tb, npad));
+    if (timed && p->timing) cudaEventRecord(p->ev[5], st);
+    if (m > 0) {
+      const size_t need = (size_t)m * tb;
+      if (need > p->tbuf_elems) {
+        cudaFree(p->tbuf);
+        p->tbuf = nullptr; p->tbuf_elems = 0;
+        CU(cudaMalloc(&p->tbuf, sizeof(double) * need));
+        p->tbuf_elems = need;
+      }
+      const double* Xd = (const double*)X;
+      double* Qd = (double*)Q;
+      for (int Jb = 0; Jb < n; Jb += tb) {
+        const int bw = std::min(tb, n - Jb);
+        // T_J = X_J + Q_{<J} (-R_{<J,J})
+        CU(launch_gemm_f64(Qd, ldq, p->W + Jb, npad, Xd + Jb, ldx, p->tbuf, tb, m, bw, Jb, false, p->status_d, st));
+        // Q_J = T_J Winv_JJ
+        CU(launch_gemm_f64(p->tbuf, tb, p->W + (size_t)Jb * npad + Jb, npad, nullptr, 0, Qd + Jb, ldq, m, bw, bw, true,
+                           p->status_d, st));
+      }
+    }
+  } else if (p->warp_solve > 0) {
+    CU(launch_tri_prep_blocked(R, n, p->W, p->status_d, st));
+    if (timed && p->timing) cudaEventRecord(p->ev[5], st);
+    if (m > 0) CU(launch_trsm_warp(p->warp_solve, X, p->d.dtype, m, n, ldx, p->W, Q, ldq, p->status_d, p->sms, st));
+  } else if (p->res_tm > 0) {
     CU(launch_tri_prep_blocked(R, n, p->W, p->status_d, st));
     if (timed && p->timing) cudaEventRecord(p->ev[5], st);
     if (m > 0) CU(launch_trsm_resident(p->res_tm, X, p->d.dtype, m, n, ldx, p->W, Q, ldq, p->status_d, p->sms, st));
@@ -231,14 +264,21 @@ rcholqr_status rcholqr_create(const rcholqr_desc* desc, rcholqr_plan* out) {
   p->sk = plan_sketch(k, n, desc->dtype, desc->sketch, desc->nnz_per_col, p->sms, p->smem_optin);
   p->tr = plan_trsm(n, desc->dtype, p->smem_optin);
   p->res_tm = trsm_resident_tm(n, desc->dtype, p->smem_optin);
-  if (const char* f = getenv("RCHOLQR_FORCE_INVERSE_SOLVE")) if (atoi(f)) p->res_tm = 0;  // experiments
+  p->warp_solve = trsm_warp_count(n, p->smem_optin);
+  if (p->warp_solve == 0 && p->res_tm == 0 && desc->dtype == RCHOLQR_F64) p->stream_tb = n < 512 ? 64 : 128;
+  if (const char* f = getenv("RCHOLQR_SOLVE")) {  // experiments: 0 = inverse GEMM, 1 = CTA-resident, 2 = warp
+    const int v = atoi(f);
+    if (v != 2) p->warp_solve = 0;
+    if (v == 0) { p->res_tm = 0; p->stream_tb = 0; }
+  }
   p->qr_kind = plan_qr(k, n, p->smem_optin);
   const size_t kn = (size_t)k * n, nn = (size_t)((n + 7) / 8 * 8) * ((n + 7) / 8 * 8);
   bool okalloc = cudaMalloc(&p->part, sizeof(double) * kn * p->sk.splits) == cudaSuccess &&
+                 cudaMalloc(&p->partc, sizeof(double) * kn * p->sk.splits) == cudaSuccess &&
                  cudaMalloc(&p->P, sizeof(double) * kn) == cudaSuccess &&
                  cudaMalloc(&p->W, sizeof(double) * nn) == cudaSuccess &&
                  cudaMalloc(&p->Awork, sizeof(double) * kn) == cudaSuccess &&
-                 cudaMalloc(&p->diag, sizeof(double) * n) == cudaSuccess &&
+                 cudaMalloc(&p->diag, sizeof(double) * 2 * n) == cudaSuccess &&
                  cudaMalloc(&p->tau, sizeof(double) * n) == cudaSuccess &&
                  cudaMalloc(&p->Rtmp, sizeof(double) * nn) == cudaSuccess &&
                  cudaMalloc(&p->status_d, sizeof(int)) == cudaSuccess &&
@@ -260,10 +300,10 @@ rcholqr_status rcholqr_create(const rcholqr_desc* desc, rcholqr_plan* out) {
 rcholqr_status rcholqr_destroy(rcholqr_plan p) {
   if (!p) return RCHOLQR_OK;
   DeviceGuard dg(p->d.device);
-  cudaFree(p->part); cudaFree(p->P); cudaFree(p->W); cudaFree(p->Awork); cudaFree(p->diag); cudaFree(p->tau);
+  cudaFree(p->part); cudaFree(p->partc); cudaFree(p->P); cudaFree(p->W); cudaFree(p->Awork); cudaFree(p->diag); cudaFree(p->tau);
   cudaFree(p->Rtmp); cudaFree(p->status_d);
   if (p->status_h) cudaFreeHost(p->status_h);
-  cudaFree(p->xbuf); cudaFree(p->qbuf); cudaFree(p->rbuf); cudaFree(p->sbuf);
+  cudaFree(p->xbuf); cudaFree(p->qbuf); cudaFree(p->rbuf); cudaFree(p->sbuf); cudaFree(p->tbuf);
   for (int t = 0; t < 7; ++t)
     if (p->ev[t]) cudaEventDestroy(p->ev[t]);
   delete p;
@@ -424,7 +464,8 @@ rcholqr_status rcholqr_comm_destroy(void* comm) {
 int32_t rcholqr_launches_per_factor(rcholqr_plan p, int64_t m) {
   if (!p) return -1;
   // sketch (+ reduce) | QR | tri-inverse | tall solve   (memsets and the all-reduce are not ours)
-  return (m > 0 ? 2 : 0) + 1 + 1 + (m > 0 ? 1 : 0);
+  const int solve_launches = p->stream_tb > 0 ? 2 * ((p->d.n + p->stream_tb - 1) / p->stream_tb) : 1;
+  return (m > 0 ? 2 : 0) + 1 + 1 + (m > 0 ? solve_launches : 0);
 }
 
 rcholqr_status rcholqr_set_timing(rcholqr_plan p, int32_t enable) {

@@ -40,7 +40,7 @@ struct TrsmLaunch {
 // Host-side launchers (defined in sketch.cu / qr.cu / trsm.cu).
 SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms, size_t smem_optin);
 cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
-                          int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* P,
+                          int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* partc, double* P,
                           int* status, cudaStream_t st, cudaEvent_t ev_mid);
 TrsmLaunch plan_trsm(int n, int dtype, size_t smem_optin);
 cudaError_t launch_tri_inverse(const double* R, int n, double* W, int* status, cudaStream_t st);
@@ -56,7 +56,15 @@ cudaError_t launch_theta_export(uint64_t seed, int k, int sketch, int zeta, int6
 cudaError_t launch_check_diag(const double* R, int n, int* status, cudaStream_t st);
 // blocked substitution (default tall solve for n <= 128): M = [-R_{<J,J}; Winv_JJ] packed
 int trsm_resident_tm(int n, int dtype, size_t smem_optin);   // 0 = not applicable
-cudaError_t launch_tri_prep_blocked(const double* R, int n, double* M, int* status, cudaStream_t st);
+int trsm_warp_count(int n, size_t smem_optin);                 // 0 = not applicable
+cudaError_t launch_trsm_warp(int warps, const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M,
+                             void* Q, int64_t ldq, const int* status, int sms, cudaStream_t st);
+cudaError_t launch_tri_prep_blocked(const double* R, int n, double* M, int* status, cudaStream_t st, int tb = 32,
+                                    int npad = 0);
+// fp64 DMMA GEMM C = C0 + A B (gemm.cu), used by the streamed blocked solve (n > 128, fp64 X)
+cudaError_t launch_gemm_f64(const double* A, int64_t lda, const double* B, int64_t ldb, const double* C0,
+                            int64_t ldc0, double* C, int64_t ldc, int64_t m, int N, int K, bool tri_b,
+                            const int* status, cudaStream_t st);
 cudaError_t launch_trsm_resident(int tm, const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M,
                                  void* Q, int64_t ldq, const int* status, int sms, cudaStream_t st);
 

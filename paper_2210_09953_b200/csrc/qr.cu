@@ -3,11 +3,12 @@
 //
 // One CTA (1024 threads) factors the k x n fp64 sketch.  The working copy A lives column-major in
 // shared memory when it fits (k*n*8 <= ~200 KB: configs C1, C2, C4) and in a global workspace
-// (L2-resident) otherwise.  For column j:
-//   warp 0:   alpha = ||A[j:,j]||, v = A[j:,j] + sign(a_jj) alpha e_j, beta = 1/(alpha |v_0|),
-//             R_jj = -sign(a_jj) alpha                                   (one CTA barrier)
-//   all warps: each trailing column l > j (round-robin over warps) gets
-//             A[j:,l] -= v * beta * (v^T A[j:,l])   (warp-shuffle dot product)   (one barrier)
+// (L2-resident) otherwise.  For column j (one CTA barrier per column):
+//   every warp: alpha = ||A[j:,j]||, v = A[j:,j] + sign(a_jj) alpha e_j, beta = 1/(alpha |v_0|),
+//               R_jj = -sign(a_jj) alpha   (from the look-ahead norm of the previous step)
+//   all warps:  each trailing column l > j (dealt cyclically) gets
+//               A[j:,l] -= v * beta * (v^T A[j:,l])   (warp-shuffle dot product); the owner of
+//               column j+1 then computes ||A[j+1:,j+1]||^2 for the next step.
 // Then diag(R) >= 0 by negating rows (reading A5) and a zero/non-finite pivot raises the
 // singular flag (reading A6).  The reflectors (v, beta) stay in the workspace so that S (Alg. 2's
 // orthonormal sketch) can be formed on request: S = H_0 ... H_{n-1} [I_n; 0], one warp
@@ -26,14 +27,19 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// A: column-major working copy with leading dimension lda (= k).
+// A: column-major working copy with leading dimension lda (= k).  One barrier per column:
+// every warp derives (alpha_j, v0, beta) redundantly from ||A[j:,j]||^2, which the owner of
+// column j (columns are dealt cyclically to warps) computed at the end of step j-1 right after
+// updating that column ("look-ahead"); the reflector's head v0 is kept in diag_v[] instead of
+// being written into A[j][j], so no warp races the others for it.
+template <bool use_smem>   // compile-time, so A's accesses are LDS/STS (not generic LD/ST)
 __global__ void __launch_bounds__(QR_THREADS, 1)
 householder_kernel(const double* __restrict__ P, int k, int n, double* __restrict__ R,
                    double* __restrict__ Aglob, double* __restrict__ diag_out, double* __restrict__ tau_out,
-                   int* status, int use_smem) {
+                   int* status) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ double sh_beta, sh_rjj;
   __shared__ int sh_flag;
+  __shared__ double sh_norm2[2];     // ping-pong: ||A[j:,j]||^2 for the current / next column
   double* A = use_smem ? smem : Aglob;
   const int lda = k;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, nwarps = QR_THREADS / 32;
@@ -51,38 +57,42 @@ householder_kernel(const double* __restrict__ P, int k, int n, double* __restric
     if (tid == 0) atomicOr(status, kStNonfinite);
     return;
   }
+  if (warp == 0) {   // ||A[:,0]||^2
+    double ss = 0.0;
+    for (int i = lane; i < k; i += 32) ss += A[i] * A[i];
+    ss = warp_sum(ss);
+    if (lane == 0) sh_norm2[0] = ss;
+  }
+  __syncthreads();
   for (int j = 0; j < n; ++j) {
-    double* a = A + (size_t)j * lda;
-    if (warp == 0) {
-      double ss = 0.0;
-      for (int i = j + lane; i < k; i += 32) ss += a[i] * a[i];
-      ss = warp_sum(ss);
-      if (lane == 0) {
-        const double alpha = sqrt(ss);
-        const double x0 = a[j];
-        const double sgn = x0 >= 0.0 ? 1.0 : -1.0;
-        if (alpha == 0.0) {
-          sh_beta = 0.0;
-          sh_rjj = 0.0;
-        } else {
-          const double v0 = x0 + sgn * alpha;
-          a[j] = v0;
-          sh_beta = 1.0 / (alpha * fabs(v0));
-          sh_rjj = -sgn * alpha;
-        }
-        tau_out[j] = sh_beta;
-        diag_out[j] = sh_rjj;
-      }
+    const double* a = A + (size_t)j * lda;
+    const double alpha = sqrt(sh_norm2[j & 1]);
+    const double x0 = a[j];
+    const double sgn = x0 >= 0.0 ? 1.0 : -1.0;
+    const double v0 = x0 + sgn * alpha;
+    const double beta = alpha == 0.0 ? 0.0 : 1.0 / (alpha * fabs(v0));
+    if (tid == 0) {
+      tau_out[j] = beta;
+      diag_out[j] = alpha == 0.0 ? 0.0 : -sgn * alpha;
+      diag_out[n + j] = v0;           // reflector head (v = [v0; A[j+1:, j]])
     }
-    __syncthreads();
-    const double beta = sh_beta;
-    if (beta != 0.0) {
-      for (int l = j + 1 + warp; l < n; l += nwarps) {
-        double* c = A + (size_t)l * lda;
-        double w = 0.0;
-        for (int i = j + lane; i < k; i += 32) w += a[i] * c[i];
+    // trailing columns l > j, dealt cyclically: warp w owns l = w, w + nwarps, ...
+    int l = j + 1 + ((warp - (j + 1)) % nwarps + nwarps) % nwarps;
+    for (; l < n; l += nwarps) {
+      double* c = A + (size_t)l * lda;
+      if (beta != 0.0) {
+        double w = (lane == 0) ? v0 * c[j] : 0.0;
+        for (int i = j + 1 + lane; i < k; i += 32) w += a[i] * c[i];
         w = warp_sum(w) * beta;
-        for (int i = j + lane; i < k; i += 32) c[i] -= a[i] * w;
+        if (lane == 0) c[j] -= v0 * w;
+        for (int i = j + 1 + lane; i < k; i += 32) c[i] -= a[i] * w;
+      }
+      if (l == j + 1) {              // look-ahead: norm of the next pivot column below row j+1
+        __syncwarp();
+        double ss = 0.0;
+        for (int i = j + 1 + lane; i < k; i += 32) ss += c[i] * c[i];
+        ss = warp_sum(ss);
+        if (lane == 0) sh_norm2[(j + 1) & 1] = ss;
       }
     }
     __syncthreads();
@@ -97,8 +107,11 @@ householder_kernel(const double* __restrict__ P, int k, int n, double* __restric
     else if (l > j) v = A[(size_t)l * lda + j];
     R[c] = sg * v;
   }
-  if (use_smem) {  // keep the reflectors for S formation
-    for (int64_t c = tid; c < (int64_t)k * n; c += QR_THREADS) Aglob[c] = A[c];
+  // keep the reflectors (column-major, head v0 on the diagonal) for S formation
+  for (int64_t c = tid; c < (int64_t)k * n; c += QR_THREADS) {
+    const int j = (int)(c / lda), i = (int)(c % lda);
+    if (i == j) Aglob[c] = diag_out[n + j];
+    else if (use_smem) Aglob[c] = A[c];
   }
   if (tid < 32) {
     int bad = 0;
@@ -145,10 +158,14 @@ int plan_qr(int k, int n, size_t smem_optin) {
 
 cudaError_t launch_qr(int kind, const double* P, int k, int n, double* R, double* Awork, double* diag,
                       double* tau, int* status, cudaStream_t st) {
-  const size_t smem = kind == kQrSmem ? sizeof(double) * (size_t)k * n : 0;
-  cudaError_t e = cudaFuncSetAttribute(householder_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  householder_kernel<<<1, QR_THREADS, smem, st>>>(P, k, n, R, Awork, diag, tau, status, kind == kQrSmem);
+  if (kind == kQrSmem) {
+    const size_t smem = sizeof(double) * (size_t)k * n;
+    cudaError_t e = cudaFuncSetAttribute(householder_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    householder_kernel<true><<<1, QR_THREADS, smem, st>>>(P, k, n, R, Awork, diag, tau, status);
+  } else {
+    householder_kernel<false><<<1, QR_THREADS, 0, st>>>(P, k, n, R, Awork, diag, tau, status);
+  }
   return cudaGetLastError();
 }
 

@@ -26,7 +26,7 @@ namespace rcq {
 
 constexpr int KC = 32;             // X rows per pipeline stage
 constexpr int SK_MMA_WARPS = 16;   // 4 per SMSP; output tiles split so every SMSP's DMMA pipe is loaded alike
-constexpr int SK_PROD_WARPS = 8;   // Theta generation + X prefetch (2 per SMSP, 2 Philox chains each)
+constexpr int SK_PROD_WARPS = 4;   // Theta generation + X prefetch (1 per SMSP, 2 Philox chains each)
 constexpr int SK_THREADS = 32 * (SK_MMA_WARPS + SK_PROD_WARPS);
 constexpr size_t SK_SMEM_BUDGET = 200 * 1024;
 
@@ -42,13 +42,20 @@ __device__ __forceinline__ void cp_async_commit_grp() { asm volatile("cp.async.c
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
+// Per-MMA-warp work: a contiguous run of n8 tiles inside ONE m16 strip (so the A fragment is
+// shared by all of the warp's MMAs), chosen on the host so the four SMSPs (warps w = s mod 4)
+// carry the same number of m16n8 tiles to within one piece (plan_warps()).
+struct WarpPlan {
+  int8_t strip[SK_MMA_WARPS], t0[SK_MMA_WARPS], cnt[SK_MMA_WARPS];
+};
+
 // Tile of P per CTA: MS m16 strips (Theta rows) x NS n8 tiles (X columns).
 template <typename TX, int MS, int NS>
 struct GCfg {
   static constexpr int KT = 16 * MS;
   static constexpr int NT = 8 * NS;
   static constexpr int UNITS = MS * NS;                                   // m16n8 output tiles
-  static constexpr int UMAX = (UNITS + SK_MMA_WARPS - 1) / SK_MMA_WARPS;   // per MMA warp
+  static constexpr int UMAX = (UNITS + SK_MMA_WARPS - 1) / SK_MMA_WARPS + 1;   // per MMA warp (plan slack)
   static constexpr int TS_LD = KC + 4;  // fp64 Theta: 36 doubles, A-fragment loads conflict-free
   // X stage keeps X's own dtype (cp.async): B-fragment loads (4 rows x 8 cols) conflict-free when the
   // row stride is 8 or 24 words (mod 32) for fp32, 4 or 12 doubles (mod 16) for fp64.
@@ -79,7 +86,7 @@ template <typename TX, int MS, int NS>
 __global__ void __launch_bounds__(SK_THREADS, 1)
 sketch_gauss_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                     uint64_t seed, int tiles_k, int tiles_n, int64_t rows_per_split,
-                    double* __restrict__ part) {
+                    double* __restrict__ part, double* __restrict__ partc, const WarpPlan plan) {
   using C = GCfg<TX, MS, NS>;
   constexpr int S = C::STAGES;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -150,63 +157,73 @@ sketch_gauss_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int
 
   // -------------------------------------------------------------------- MMA warps
   const int g = lane >> 2, t4 = lane & 3;
-  const int u_begin = (warp * C::UNITS) / SK_MMA_WARPS;
-  const int u_end = ((warp + 1) * C::UNITS) / SK_MMA_WARPS;
-  const int nun = u_end - u_begin;
-  const int sA = u_begin / NS, tA = u_begin % NS;
-  const int nA = min(nun, NS - tA);                 // units in strip sA; the rest are in sA + 1
-  static_assert(C::UMAX <= NS + 1, "a warp's units must span at most two strips");
+  const int wstrip = plan.strip[warp], wt0 = plan.t0[warp], nun = plan.cnt[warp];
   double acc[C::UMAX][4];
 #pragma unroll
   for (int u = 0; u < C::UMAX; ++u)
 #pragma unroll
     for (int e = 0; e < 4; ++e) acc[u][e] = 0.0;
-  int bcol[C::UMAX];                                // B-fragment column offset of each unit
+  const int arow = wstrip * 16 + g;
+  const int bcol0 = wt0 * 8 + g;
+
+  // Compensated two-level accumulation (the paper's "random projections in higher precision",
+  // PAPER.md:83, 406, 423): the DMMA chain covers SEG chunks only, then is folded with TwoSum into
+  // this CTA's private (sum, compensation) partial in global memory.
+  double* Pp = part + (size_t)split * (size_t)k * n;
+  double* Pc = partc + (size_t)split * (size_t)k * n;
+  bool first_flush = true;
+  const int frow = r0 + wstrip * 16 + g;
+  const bool rok0 = frow < k, rok1 = frow + 8 < k;
+  auto fold = [&](double* __restrict__ ps, double* __restrict__ pc, double a, bool first) {
+    if (first) {
+      *ps = a;
+      *pc = 0.0;
+    } else {
+      const double sold = *ps;
+      const double snew = sold + a;                               // TwoSum(sold, a)
+      const double bb = snew - sold;
+      *ps = snew;
+      *pc += (sold - (snew - bb)) + (a - bb);
+    }
+  };
+  auto flush = [&]() {
 #pragma unroll
-  for (int u = 0; u < C::UMAX; ++u) bcol[u] = ((u < nA) ? tA + u : u - nA) * 8 + g;
-  const int rowA = sA * 16 + g, rowB = min(sA + 1, MS - 1) * 16 + g;
+    for (int u = 0; u < C::UMAX; ++u) {
+      if (u < nun) {
+        const int col = n0 + (wt0 + u) * 8 + 2 * t4;
+        const size_t i0 = (size_t)frow * n + col, i1 = i0 + (size_t)8 * n;
+        const bool c0 = col < n, c1 = col + 1 < n;
+        if (rok0 && c0) fold(Pp + i0, Pc + i0, acc[u][0], first_flush);
+        if (rok0 && c1) fold(Pp + i0 + 1, Pc + i0 + 1, acc[u][1], first_flush);
+        if (rok1 && c0) fold(Pp + i1, Pc + i1, acc[u][2], first_flush);
+        if (rok1 && c1) fold(Pp + i1 + 1, Pc + i1 + 1, acc[u][3], first_flush);
+        acc[u][0] = acc[u][1] = acc[u][2] = acc[u][3] = 0.0;
+      }
+    }
+    first_flush = false;
+  };
+  constexpr int SEG = 8;   // chunks (256 rows) per DMMA accumulation chain
 
   for (int ch = 0; ch < nchunks; ++ch) {
     const int s = ch % S;
     named_sync(1 + s, SK_THREADS);                                         // FULL(s)
-    const double* T = Tst(s);
-    const TX* Xb = Xst(s);
+    const double* Tk = Tst(s) + arow * C::TS_LD + t4;
+    const TX* Xk = Xst(s) + t4 * C::XS_LD + bcol0;
 #pragma unroll 2
     for (int ks = 0; ks < KC / 4; ++ks) {
-      const double* Tk = T + 4 * ks + t4;
-      const double aA0 = Tk[rowA * C::TS_LD], aA1 = Tk[(rowA + 8) * C::TS_LD];
-      const double aB0 = Tk[rowB * C::TS_LD], aB1 = Tk[(rowB + 8) * C::TS_LD];
-      const TX* xrow = Xb + (4 * ks + t4) * C::XS_LD;
-      double b[C::UMAX];
+      const double a0 = Tk[4 * ks], a1 = Tk[8 * C::TS_LD + 4 * ks];
+      const TX* xrow = Xk + 4 * ks * C::XS_LD;
+      TX braw[C::UMAX];
 #pragma unroll
-      for (int u = 0; u < C::UMAX; ++u) b[u] = (u < nun) ? (double)xrow[bcol[u]] : 0.0;
+      for (int u = 0; u < C::UMAX; ++u) braw[u] = (u < nun) ? xrow[8 * u] : TX(0);
 #pragma unroll
-      for (int u = 0; u < C::UMAX; ++u) {
-        if (u < nun) {
-          const bool inA = u < nA;
-          dmma_16x8x4(acc[u], inA ? aA0 : aB0, inA ? aA1 : aB1, b[u]);
-        }
-      }
+      for (int u = 0; u < C::UMAX; ++u)
+        if (u < nun) dmma_16x8x4(acc[u], a0, a1, (double)braw[u]);
     }
     if (ch + S < nchunks) named_arrive(1 + S + s, SK_THREADS);            // EMPTY(s)
+    if ((ch + 1) % SEG == 0) flush();
   }
-
-  double* Pp = part + (size_t)split * (size_t)k * n;
-#pragma unroll
-  for (int u = 0; u < C::UMAX; ++u) {
-    if (u < nun) {
-      const int row = r0 + ((u < nA) ? sA : sA + 1) * 16 + g;
-      const int col = n0 + (bcol[u] - g) + 2 * t4;
-      if (row < k) {
-        if (col < n) Pp[(size_t)row * n + col] = acc[u][0];
-        if (col + 1 < n) Pp[(size_t)row * n + col + 1] = acc[u][1];
-      }
-      if (row + 8 < k) {
-        if (col < n) Pp[(size_t)(row + 8) * n + col] = acc[u][2];
-        if (col + 1 < n) Pp[(size_t)(row + 8) * n + col + 1] = acc[u][3];
-      }
-    }
-  }
+  if (first_flush || nchunks % SEG != 0) flush();   // the tail segment (or zeros for an empty split)
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -272,13 +289,20 @@ sketch_sparse_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, in
 }
 
 // Fixed-order sum of the per-split partials, one scaling, non-finite detection.
-__global__ void sketch_reduce_kernel(const double* __restrict__ part, int splits, int64_t kn, double scale,
-                                     double* __restrict__ P, int* status) {
+__global__ void sketch_reduce_kernel(const double* __restrict__ part, const double* __restrict__ partc, int splits,
+                                     int64_t kn, double scale, double* __restrict__ P, int* status) {
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < kn;
        idx += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0;
-    for (int sp = 0; sp < splits; ++sp) s += part[(size_t)sp * kn + idx];
-    s *= scale;
+    double s = 0.0, c = 0.0;                    // compensated (TwoSum) sum over the splits
+    for (int sp = 0; sp < splits; ++sp) {
+      const double v = part[(size_t)sp * kn + idx];
+      const double t = s + v;
+      const double bb = t - s;
+      c += (s - (t - bb)) + (v - bb);
+      s = t;
+      if (partc) c += partc[(size_t)sp * kn + idx];
+    }
+    s = (s + c) * scale;
     P[idx] = s;
     if (!isfinite(s)) atomicOr(status, kStNonfinite);
   }
@@ -318,6 +342,54 @@ static void fill_gauss(SketchLaunch& L, int kind, int k, int n, int dtype) {
   L.smem = dtype == RCHOLQR_F64 ? GCfg<double, MS, NS>::SMEM : GCfg<float, MS, NS>::SMEM;
   L.tiles_k = (k + L.KT - 1) / L.KT;
   L.tiles_n = (n + L.NT - 1) / L.NT;
+}
+
+// Split the MS x NS m16n8 tiles into <= SK_MMA_WARPS single-strip pieces and deal them to the four
+// SMSPs (warp w runs on SMSP w % 4) longest-first, so the per-SMSP DMMA loads are balanced.
+static WarpPlan plan_warps(int MS, int NS) {
+  WarpPlan P{};
+  int pieces_per_strip[64];
+  for (int s = 0; s < MS; ++s) pieces_per_strip[s] = 1;
+  int npieces = MS;
+  // repeatedly split the strip whose pieces are largest while warps remain
+  while (true) {
+    int best = -1, bestsz = 0;
+    for (int s = 0; s < MS; ++s) {
+      const int sz = (NS + pieces_per_strip[s] - 1) / pieces_per_strip[s];
+      if (sz > bestsz && pieces_per_strip[s] < NS) { bestsz = sz; best = s; }
+    }
+    if (best < 0 || npieces + 1 > SK_MMA_WARPS) break;
+    pieces_per_strip[best]++;
+    npieces++;
+  }
+  struct Piece { int strip, t0, cnt; };
+  Piece pc[SK_MMA_WARPS];
+  int np = 0;
+  for (int s = 0; s < MS; ++s) {
+    const int p = pieces_per_strip[s];
+    int t = 0;
+    for (int q = 0; q < p; ++q) {
+      const int c = NS / p + (q < NS % p ? 1 : 0);
+      pc[np++] = {s, t, c};
+      t += c;
+    }
+  }
+  // longest-first onto the least-loaded SMSP that still has a free warp slot
+  for (int i = 0; i < np; ++i)
+    for (int j = i + 1; j < np; ++j)
+      if (pc[j].cnt > pc[i].cnt) { Piece tmp = pc[i]; pc[i] = pc[j]; pc[j] = tmp; }
+  int load[4] = {0, 0, 0, 0}, used[4] = {0, 0, 0, 0};
+  for (int w = 0; w < SK_MMA_WARPS; ++w) { P.strip[w] = 0; P.t0[w] = 0; P.cnt[w] = 0; }
+  for (int i = 0; i < np; ++i) {
+    int best = -1;
+    for (int sm = 0; sm < 4; ++sm)
+      if (used[sm] < SK_MMA_WARPS / 4 && (best < 0 || load[sm] < load[best])) best = sm;
+    const int w = best + 4 * used[best];
+    used[best]++;
+    load[best] += pc[i].cnt;
+    P.strip[w] = (int8_t)pc[i].strip; P.t0[w] = (int8_t)pc[i].t0; P.cnt[w] = (int8_t)pc[i].cnt;
+  }
+  return P;
 }
 
 // Choose the number of row splits so tiles*splits fills whole waves of one CTA per SM.
@@ -378,29 +450,33 @@ SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms,
 
 template <typename TX, int MS, int NS>
 static cudaError_t launch_g(const SketchLaunch& L, const void* X, int64_t m, int n, int64_t ldx, int64_t ro,
-                            int k, uint64_t seed, int64_t rps, double* part, cudaStream_t st) {
+                            int k, uint64_t seed, int64_t rps, double* part, double* partc, cudaStream_t st) {
   auto kern = sketch_gauss_kernel<TX, MS, NS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
   if (e != cudaSuccess) return e;
+  static_assert(sizeof(WarpPlan) == 3 * SK_MMA_WARPS, "plan layout");
+  const WarpPlan plan = plan_warps(MS, NS);
+  for (int w = 0; w < SK_MMA_WARPS; ++w)
+    if (plan.cnt[w] > GCfg<TX, MS, NS>::UMAX) return cudaErrorInvalidConfiguration;
   kern<<<L.tiles_k * L.tiles_n * L.splits, SK_THREADS, L.smem, st>>>((const TX*)X, m, n, ldx, ro, k, seed,
-                                                                     L.tiles_k, L.tiles_n, rps, part);
+                                                                     L.tiles_k, L.tiles_n, rps, part, partc, plan);
   return cudaGetLastError();
 }
 
 template <typename TX>
 static cudaError_t launch_gauss_typed(const SketchLaunch& L, const void* X, int64_t m, int n, int64_t ldx,
-                                      int64_t ro, int k, uint64_t seed, int64_t rps, double* part,
+                                      int64_t ro, int k, uint64_t seed, int64_t rps, double* part, double* partc,
                                       cudaStream_t st) {
   switch (L.kind) {
-    case kSketchG48x24: return launch_g<TX, 3, 3>(L, X, m, n, ldx, ro, k, seed, rps, part, st);
-    case kSketchG128x64: return launch_g<TX, 8, 8>(L, X, m, n, ldx, ro, k, seed, rps, part, st);
-    case kSketchG112x104: return launch_g<TX, 7, 13>(L, X, m, n, ldx, ro, k, seed, rps, part, st);
-    default: return launch_g<TX, 4, 8>(L, X, m, n, ldx, ro, k, seed, rps, part, st);
+    case kSketchG48x24: return launch_g<TX, 3, 3>(L, X, m, n, ldx, ro, k, seed, rps, part, partc, st);
+    case kSketchG128x64: return launch_g<TX, 8, 8>(L, X, m, n, ldx, ro, k, seed, rps, part, partc, st);
+    case kSketchG112x104: return launch_g<TX, 7, 13>(L, X, m, n, ldx, ro, k, seed, rps, part, partc, st);
+    default: return launch_g<TX, 4, 8>(L, X, m, n, ldx, ro, k, seed, rps, part, partc, st);
   }
 }
 
 cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
-                          int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* P,
+                          int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* partc, double* P,
                           int* status, cudaStream_t st, cudaEvent_t ev_mid) {
   cudaError_t e;
   const int64_t per = (m + L.splits - 1) / L.splits;
@@ -420,8 +496,8 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
     scale = 1.0 / std::sqrt((double)zeta);
   } else {
     const int64_t rps = std::max<int64_t>(KC, ((per + KC - 1) / KC) * KC);
-    e = dtype == RCHOLQR_F64 ? launch_gauss_typed<double>(L, X, m, n, ldx, row_offset, k, seed, rps, part, st)
-                             : launch_gauss_typed<float>(L, X, m, n, ldx, row_offset, k, seed, rps, part, st);
+    e = dtype == RCHOLQR_F64 ? launch_gauss_typed<double>(L, X, m, n, ldx, row_offset, k, seed, rps, part, partc, st)
+                             : launch_gauss_typed<float>(L, X, m, n, ldx, row_offset, k, seed, rps, part, partc, st);
     scale = 1.0 / std::sqrt((double)k);
   }
   if (e != cudaSuccess) return e;
@@ -429,7 +505,8 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
   const int64_t kn = (int64_t)k * n;
   const int threads = 256;
   const int blocks = (int)std::min<int64_t>((kn + threads - 1) / threads, 4096);
-  sketch_reduce_kernel<<<blocks, threads, 0, st>>>(part, L.splits, kn, scale, P, status);
+  sketch_reduce_kernel<<<blocks, threads, 0, st>>>(part, L.kind == kSketchSparse ? nullptr : partc, L.splits, kn,
+                                                   scale, P, status);
   return cudaGetLastError();
 }
 

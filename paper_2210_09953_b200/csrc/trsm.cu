@@ -414,32 +414,157 @@ trsm_resident_kernel(const TX* __restrict__ X, int64_t m, int n, int NPAD, int64
   cp_async_wait_all();
 }
 
-// M = [-R_{<J,J}; Winv_JJ] packed (npad x npad, zero padded).  One warp per row i of M.
-__global__ void tri_prep_blocked_kernel(const double* __restrict__ R, int n, int npad, double* __restrict__ M,
+// Warp-independent variant (default for n <= 128): every warp owns whole 16-row tiles and runs the
+// blocked substitution on them alone -- no CTA barrier after the one-time load of M -- with its
+// fp64 Q history in a private 16-row shared-memory slab.  The X values of block J+1 are
+// prefetched into registers while block J is solved.
+template <typename TX>
+__device__ __forceinline__ void load_x_frag(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64_t r0, int c,
+                                            int g, TX (&v)[4]) {
+  const int64_t ra = r0 + g, rb = r0 + g + 8;
+  v[0] = (ra < m && c < n) ? __ldcs(X + ra * ldx + c) : TX(0);
+  v[1] = (ra < m && c + 1 < n) ? __ldcs(X + ra * ldx + c + 1) : TX(0);
+  v[2] = (rb < m && c < n) ? __ldcs(X + rb * ldx + c) : TX(0);
+  v[3] = (rb < m && c + 1 < n) ? __ldcs(X + rb * ldx + c + 1) : TX(0);
+}
+
+template <typename TX, int WARPS>
+__global__ void __launch_bounds__(32 * WARPS, 1)
+trsm_warp_kernel(const TX* __restrict__ X, int64_t m, int n, int NPAD, int64_t ldx, const double* __restrict__ Mg,
+                 TX* __restrict__ Q, int64_t ldq, const int* status) {
+  if (*status) return;
+  extern __shared__ __align__(16) double smem_w[];
+  const int LD = NPAD + 4;                       // = 4 or 12 (mod 16) doubles: fragment loads conflict-free
+  double* Ms = smem_w;                            // [NPAD][LD]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  double* Aw = smem_w + (size_t)NPAD * LD + (size_t)warp * 16 * LD;   // this warp's [16][LD] slab
+  for (int c = threadIdx.x; c < NPAD * NPAD; c += 32 * WARPS) Ms[(c / NPAD) * LD + (c % NPAD)] = Mg[c];
+  __syncthreads();
+  const int NBLK = (NPAD + TB - 1) / TB;
+  const int64_t ntiles = (m + 15) / 16;
+  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp, nw = (int64_t)gridDim.x * WARPS;
+  TX xn[TB / 8][4];                               // prefetched X fragments of the next block
+  auto prefetch = [&](int64_t tile, int J) {
+    const int c0 = J * TB;
+#pragma unroll
+    for (int u = 0; u < TB / 8; ++u) load_x_frag(X, m, n, ldx, tile * 16, c0 + 8 * u + 2 * t4, g, xn[u]);
+  };
+  if (gw < ntiles) prefetch(gw, 0);
+  for (int64_t tile = gw; tile < ntiles; tile += nw) {
+    const int64_t r0 = tile * 16;
+    for (int J = 0; J < NBLK; ++J) {
+      const int c0 = J * TB;
+      const int nt8 = min(TB, NPAD - c0) / 8;
+      double acc[TB / 8][4];
+#pragma unroll
+      for (int u = 0; u < TB / 8; ++u)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[u][e] = (double)xn[u][e];
+      // prefetch the next block (or the next tile's first block)
+      if (J + 1 < NBLK) prefetch(tile, J + 1);
+      else if (tile + nw < ntiles) prefetch(tile + nw, 0);
+      // phase 1: T_J = X_J + Q_{<J} (-R_{<J,J})
+      const double* arow = Aw + g * LD + t4;
+      for (int ks = 0; ks < c0 / 4; ++ks) {
+        const double a0 = arow[4 * ks], a1 = arow[8 * LD + 4 * ks];
+        const double* mrow = Ms + (4 * ks + t4) * LD + c0 + g;
+#pragma unroll
+        for (int u = 0; u < TB / 8; ++u)
+          if (u < nt8) dmma_16x8x4(acc[u], a0, a1, mrow[8 * u]);
+      }
+#pragma unroll
+      for (int u = 0; u < TB / 8; ++u) {
+        if (u < nt8) {
+          double* tp = Aw + g * LD + c0 + 8 * u + 2 * t4;
+          tp[0] = acc[u][0]; tp[1] = acc[u][1]; tp[8 * LD] = acc[u][2]; tp[8 * LD + 1] = acc[u][3];
+        }
+      }
+      __syncwarp();
+      // phase 2: Q_J = T_J Winv_JJ (upper triangular: skip k-steps past each 8-column tile)
+#pragma unroll
+      for (int u = 0; u < TB / 8; ++u)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[u][e] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < TB / 4; ++ks) {
+        if (4 * ks < 8 * nt8) {
+          const double a0 = arow[c0 + 4 * ks], a1 = arow[8 * LD + c0 + 4 * ks];
+          const double* mrow = Ms + (c0 + 4 * ks + t4) * LD + c0 + g;
+#pragma unroll
+          for (int u = 0; u < TB / 8; ++u)
+            if (u < nt8 && 4 * ks <= 8 * u + 7) dmma_16x8x4(acc[u], a0, a1, mrow[8 * u]);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < TB / 8; ++u) {
+        if (u < nt8) {
+          const int col = c0 + 8 * u + 2 * t4;
+          double* tp = Aw + g * LD + col;
+          tp[0] = acc[u][0]; tp[1] = acc[u][1]; tp[8 * LD] = acc[u][2]; tp[8 * LD + 1] = acc[u][3];
+          const int64_t ra = r0 + g, rb = r0 + g + 8;
+          if (ra < m) {
+            if (col < n) Q[ra * ldq + col] = to_out<TX>(acc[u][0]);
+            if (col + 1 < n) Q[ra * ldq + col + 1] = to_out<TX>(acc[u][1]);
+          }
+          if (rb < m) {
+            if (col < n) Q[rb * ldq + col] = to_out<TX>(acc[u][2]);
+            if (col + 1 < n) Q[rb * ldq + col + 1] = to_out<TX>(acc[u][3]);
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// M = [-R_{<J,J}; Winv_JJ] packed (npad x npad, zero padded), diagonal blocks of width tb
+// (32 for the resident solves, 64/128 for the streamed one; tb <= 128).  One warp per row i of M:
+// the row of Winv_JJ solves w R_JJ = e_i by forward substitution, lane l holding w[Jb + l + 32 t].
+__global__ void tri_prep_blocked_kernel(const double* __restrict__ R, int n, int npad, int tb, double* __restrict__ M,
                                         const int* status) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int i = warp;
   if (i >= npad || *status) return;
-  const int Jb = (i / TB) * TB;                     // first column of i's diagonal block
-  const int be = min(Jb + TB, n);                   // end of the block (within n)
-  // diagonal block row: w R_JJ = e_i  (lane l holds w[Jb + l])
-  double w = 0.0;
+  const int Jb = (i / tb) * tb;                     // first column of i's diagonal block
+  const int be = min(Jb + tb, n);                   // end of the block (within n)
+  double w[4] = {0.0, 0.0, 0.0, 0.0};               // w[t] = Winv row entry at column Jb + lane + 32 t
   if (i < n) {
-    if (lane == i - Jb) w = 1.0 / R[(size_t)i * n + i];
+    if (lane == (i - Jb) % 32) {
+      const double v = 1.0 / R[(size_t)i * n + i];
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+        if (t == (i - Jb) / 32) w[t] = v;
+    }
     for (int j = i + 1; j < be; ++j) {
-      const int l = Jb + lane;
-      double s = (l >= i && l < j) ? w * R[(size_t)l * n + j] : 0.0;
+      double s = 0.0;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int l = Jb + lane + 32 * t;
+        if (l >= i && l < j) s += w[t] * R[(size_t)l * n + j];
+      }
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == j - Jb) w = -s / R[(size_t)j * n + j];
+      if (lane == (j - Jb) % 32) {
+        const double v = -s / R[(size_t)j * n + j];
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (t == (j - Jb) / 32) w[t] = v;
+      }
     }
   }
   for (int base = 0; base < npad; base += 32) {   // uniform trip count: shuffles are convergent
     const int c = base + lane;
-    const double wc = __shfl_sync(0xffffffffu, w, (c - Jb) & 31);
+    const int tsel = (base - Jb) >= 0 ? (base - Jb) / 32 : 0;   // same for all lanes of this chunk
+    double wc = 0.0;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      const double vv = __shfl_sync(0xffffffffu, w[t], lane);
+      if (t == tsel) wc = vv;
+    }
     double v = 0.0;
     if (i < n && c < n) {
-      if (c >= Jb + TB) v = -R[(size_t)i * n + c];
+      if (c >= Jb + tb) v = -R[(size_t)i * n + c];
       else if (c >= Jb) v = wc;
     }
     if (c < npad) M[(size_t)i * npad + c] = v;
@@ -447,6 +572,40 @@ __global__ void tri_prep_blocked_kernel(const double* __restrict__ R, int n, int
 }
 
 // ---------------------------------------------------------------------------------------------
+static size_t warp_smem(int npad, int warps) { return sizeof(double) * (size_t)(npad + 4) * (npad + 16 * warps); }
+
+int trsm_warp_count(int n, size_t smem_optin) {
+  const int npad = (n + 7) / 8 * 8;
+  if (n > 128) return 0;
+  if (warp_smem(npad, 8) <= smem_optin) return 8;
+  if (warp_smem(npad, 4) <= smem_optin) return 4;
+  return 0;
+}
+
+template <typename TX, int WARPS>
+static cudaError_t launch_w(const void* X, int64_t m, int n, int64_t ldx, const double* M, void* Q, int64_t ldq,
+                            const int* status, int sms, cudaStream_t st) {
+  const int npad = (n + 7) / 8 * 8;
+  const size_t smem = warp_smem(npad, WARPS);
+  auto kern = trsm_warp_kernel<TX, WARPS>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t ntiles = (m + 15) / 16;
+  const int grid = (int)std::min<int64_t>((ntiles + WARPS - 1) / WARPS, sms);
+  if (grid == 0) return cudaSuccess;
+  kern<<<grid, 32 * WARPS, smem, st>>>((const TX*)X, m, n, npad, ldx, M, (TX*)Q, ldq, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_trsm_warp(int warps, const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M,
+                             void* Q, int64_t ldq, const int* status, int sms, cudaStream_t st) {
+  if (dtype == RCHOLQR_F64)
+    return warps == 8 ? launch_w<double, 8>(X, m, n, ldx, M, Q, ldq, status, sms, st)
+                      : launch_w<double, 4>(X, m, n, ldx, M, Q, ldq, status, sms, st);
+  return warps == 8 ? launch_w<float, 8>(X, m, n, ldx, M, Q, ldq, status, sms, st)
+                    : launch_w<float, 4>(X, m, n, ldx, M, Q, ldq, status, sms, st);
+}
+
 int trsm_resident_tm(int n, int dtype, size_t smem_optin) {
   const int npad = (n + 7) / 8 * 8;
   const int xs = dtype == RCHOLQR_F64 ? 8 : 4;
@@ -456,11 +615,12 @@ int trsm_resident_tm(int n, int dtype, size_t smem_optin) {
   return 0;
 }
 
-cudaError_t launch_tri_prep_blocked(const double* R, int n, double* M, int* status, cudaStream_t st) {
-  const int npad = (n + 7) / 8 * 8;
+cudaError_t launch_tri_prep_blocked(const double* R, int n, double* M, int* status, cudaStream_t st, int tb,
+                                    int npad) {
+  if (npad <= 0) npad = (n + 7) / 8 * 8;
   const int warps_per_block = 4;
   tri_prep_blocked_kernel<<<(npad + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, st>>>(
-      R, n, npad, M, status);
+      R, n, npad, tb, M, status);
   return cudaGetLastError();
 }
 
