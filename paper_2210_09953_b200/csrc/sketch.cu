@@ -86,7 +86,7 @@ template <typename TX, int MS, int NS>
 __global__ void __launch_bounds__(SK_THREADS, 1)
 sketch_gauss_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                     uint64_t seed, int tiles_k, int tiles_n, int64_t rows_per_split,
-                    double* __restrict__ part, double* __restrict__ partc, const WarpPlan plan) {
+                    double* __restrict__ part, double* __restrict__ partc, const WarpPlan plan, int seg_chunks) {
   using C = GCfg<TX, MS, NS>;
   constexpr int S = C::STAGES;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -169,23 +169,12 @@ sketch_gauss_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int
   // Compensated two-level accumulation (the paper's "random projections in higher precision",
   // PAPER.md:83, 406, 423): the DMMA chain covers SEG chunks only, then is folded with TwoSum into
   // this CTA's private (sum, compensation) partial in global memory.
-  double* Pp = part + (size_t)split * (size_t)k * n;
-  double* Pc = partc + (size_t)split * (size_t)k * n;
+  double* __restrict__ Pp = part + (size_t)split * (size_t)k * n;
+  double* __restrict__ Pc = partc + (size_t)split * (size_t)k * n;
   bool first_flush = true;
   const int frow = r0 + wstrip * 16 + g;
   const bool rok0 = frow < k, rok1 = frow + 8 < k;
-  auto fold = [&](double* __restrict__ ps, double* __restrict__ pc, double a, bool first) {
-    if (first) {
-      *ps = a;
-      *pc = 0.0;
-    } else {
-      const double sold = *ps;
-      const double snew = sold + a;                               // TwoSum(sold, a)
-      const double bb = snew - sold;
-      *ps = snew;
-      *pc += (sold - (snew - bb)) + (a - bb);
-    }
-  };
+  // per unit: issue the 8 loads first (no store in between), then the TwoSums, then the stores
   auto flush = [&]() {
 #pragma unroll
     for (int u = 0; u < C::UMAX; ++u) {
@@ -193,16 +182,34 @@ sketch_gauss_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int
         const int col = n0 + (wt0 + u) * 8 + 2 * t4;
         const size_t i0 = (size_t)frow * n + col, i1 = i0 + (size_t)8 * n;
         const bool c0 = col < n, c1 = col + 1 < n;
-        if (rok0 && c0) fold(Pp + i0, Pc + i0, acc[u][0], first_flush);
-        if (rok0 && c1) fold(Pp + i0 + 1, Pc + i0 + 1, acc[u][1], first_flush);
-        if (rok1 && c0) fold(Pp + i1, Pc + i1, acc[u][2], first_flush);
-        if (rok1 && c1) fold(Pp + i1 + 1, Pc + i1 + 1, acc[u][3], first_flush);
-        acc[u][0] = acc[u][1] = acc[u][2] = acc[u][3] = 0.0;
+        const bool ok[4] = {rok0 && c0, rok0 && c1, rok1 && c0, rok1 && c1};
+        const size_t ix[4] = {i0, i0 + 1, i1, i1 + 1};
+        double so[4], co[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          so[e] = (ok[e] && !first_flush) ? __ldcg(Pp + ix[e]) : 0.0;
+          co[e] = (ok[e] && !first_flush) ? __ldcg(Pc + ix[e]) : 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const double av = acc[u][e];
+          const double snew = so[e] + av;                              // TwoSum(so, av)
+          const double bb = snew - so[e];
+          co[e] += (so[e] - (snew - bb)) + (av - bb);
+          so[e] = snew;
+          acc[u][e] = 0.0;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (ok[e]) { __stcg(Pp + ix[e], so[e]); __stcg(Pc + ix[e], co[e]); }
       }
     }
     first_flush = false;
   };
-  constexpr int SEG = 8;   // chunks (256 rows) per DMMA accumulation chain
+  // fp64 X (working precision u = 2^-53) needs the sketch at u_f << u: compensated folds every SEG
+  // chunks.  fp32 X (u = 2^-24): a plain fp64 DMMA chain is already u_f ~ 1e-13 << u, so one fold.
+  constexpr bool kComp = sizeof(TX) == 8;
+  const int SEG = seg_chunks;   // chunks per DMMA accumulation chain (default 16 = 512 rows)
 
   for (int ch = 0; ch < nchunks; ++ch) {
     const int s = ch % S;
@@ -221,9 +228,11 @@ sketch_gauss_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int
         if (u < nun) dmma_16x8x4(acc[u], a0, a1, (double)braw[u]);
     }
     if (ch + S < nchunks) named_arrive(1 + S + s, SK_THREADS);            // EMPTY(s)
-    if ((ch + 1) % SEG == 0) flush();
+    if constexpr (kComp) {
+      if ((ch + 1) % SEG == 0) flush();
+    }
   }
-  if (first_flush || nchunks % SEG != 0) flush();   // the tail segment (or zeros for an empty split)
+  if (first_flush || !kComp || nchunks % SEG != 0) flush();   // tail segment (or the only one)
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -344,6 +353,17 @@ static void fill_gauss(SketchLaunch& L, int kind, int k, int n, int dtype) {
   L.tiles_n = (n + L.NT - 1) / L.NT;
 }
 
+// Chunks of KC rows per DMMA accumulation chain before a compensated fold (DESIGN.md "Sketch
+// accuracy"); RCHOLQR_SEG overrides it for experiments.
+static int seg_chunks() {
+  static int v = [] {
+    const char* e = getenv("RCHOLQR_SEG");
+    const int x = e ? atoi(e) : 16;
+    return x > 0 ? x : 16;
+  }();
+  return v;
+}
+
 // Split the MS x NS m16n8 tiles into <= SK_MMA_WARPS single-strip pieces and deal them to the four
 // SMSPs (warp w runs on SMSP w % 4) longest-first, so the per-SMSP DMMA loads are balanced.
 static WarpPlan plan_warps(int MS, int NS) {
@@ -459,7 +479,8 @@ static cudaError_t launch_g(const SketchLaunch& L, const void* X, int64_t m, int
   for (int w = 0; w < SK_MMA_WARPS; ++w)
     if (plan.cnt[w] > GCfg<TX, MS, NS>::UMAX) return cudaErrorInvalidConfiguration;
   kern<<<L.tiles_k * L.tiles_n * L.splits, SK_THREADS, L.smem, st>>>((const TX*)X, m, n, ldx, ro, k, seed,
-                                                                     L.tiles_k, L.tiles_n, rps, part, partc, plan);
+                                                                     L.tiles_k, L.tiles_n, rps, part, partc, plan,
+                                                                     seg_chunks());
   return cudaGetLastError();
 }
 
