@@ -96,14 +96,14 @@ def _dist():
 
 
 def _workload(cfg_name: str, ws: int, rank: int):
+    from paper_2210_09953_b200.partition import row_block, weak_block
     cfg = synth.config(cfg_name)
     if cfg_name in ("C1", "C2"):           # single-GPU configs: weak scaling, one C2 block per rank
-        m_local, m_global, ro, scaling = cfg["m"], cfg["m"] * ws, rank * cfg["m"], "weak"
+        ro, m_local, m_global = weak_block(cfg["m"], ws, rank)
+        scaling = "weak"
     else:                                  # BASELINE multi-GPU configs: row-partition the full X
         m_global = cfg["m"]
-        base, rem = divmod(m_global, ws)
-        m_local = base + (1 if rank < rem else 0)
-        ro = rank * base + min(rank, rem)
+        ro, m_local = row_block(m_global, ws, rank)
         scaling = "strong"
     return cfg, m_local, m_global, ro, scaling
 
