@@ -15,6 +15,7 @@
 // per column of S.
 #include <cuda_runtime.h>
 #include <algorithm>
+#include <utility>
 #include "internal.cuh"
 
 namespace rcq {
@@ -124,6 +125,197 @@ householder_kernel(const double* __restrict__ P, int k, int n, double* __restric
   }
 }
 
+// (beta, v0, raw R_jj) of a pivot column from ||A[j:,j]||^2 and A[j][j].
+__device__ __forceinline__ void pivot_params(double ss, double x0, double* par) {
+  const double alpha = sqrt(ss);
+  const double sgn = x0 >= 0.0 ? 1.0 : -1.0;
+  const double v0 = x0 + sgn * alpha;
+  par[0] = alpha == 0.0 ? 0.0 : 1.0 / (alpha * fabs(v0));   // beta
+  par[1] = v0;
+  par[2] = alpha == 0.0 ? 0.0 : -sgn * alpha;               // raw R_jj
+}
+
+// Register-resident variant (k <= 32*RPL, n <= 16*CPW; configs C1, C2, C4): 16 warps own the
+// columns cyclically (column l -> warp l % 16, slot l / 16) and lane L holds rows L, L+32, ... of
+// every owned column in registers.  Per column j only the Householder vector v_j (k doubles) goes
+// through shared memory: the owner of column j+1 updates that column first, computes its norm,
+// publishes (beta, v0, R_jj) and v_{j+1}, then all warps update their other columns two at a time
+// (two dot products and reductions in flight).  One barrier per column; rows above the pivot need no
+// predicate because v_j is zero there.
+constexpr int QR_REG_WARPS = 16;
+
+// Pivot column j sits in slot C (compile time) of warp j % 16: norm below row j, pivot parameters,
+// v_j into shared memory (and the reflector into the global workspace for S).
+template <int CPW, int RPL, int C>
+__device__ __forceinline__ void qr_publish(const double (&col)[CPW][RPL], int j, int k, int n, int lane,
+                                           double (*vbuf)[32 * RPL], double (*sh_par)[3], double* Aglob,
+                                           double* diag_out, double* tau_out) {
+  double ss = 0.0, x0 = 0.0;
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) {
+    const int i = r * 32 + lane;
+    const double v = col[C][r];
+    ss = fma(i >= j ? v : 0.0, v, ss);
+    x0 = (i == j) ? v : x0;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    x0 += __shfl_xor_sync(0xffffffffu, x0, o);
+  }
+  double par[3];
+  pivot_params(ss, x0, par);
+  if (lane == 0) {
+    sh_par[j & 1][0] = par[0]; sh_par[j & 1][1] = par[1]; sh_par[j & 1][2] = par[2];
+    tau_out[j] = par[0]; diag_out[j] = par[2]; diag_out[n + j] = par[1];
+  }
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) {
+    const int i = r * 32 + lane;
+    const double v = i < j ? 0.0 : (i == j ? par[1] : col[C][r]);
+    vbuf[j & 1][i] = v;
+    if (i < k) Aglob[(size_t)j * k + i] = v;            // reflector (head v0 on the diagonal)
+  }
+}
+
+// A[:, slot C] -= v (beta v^T A[:, slot C]) for this warp's column in slot C (v = vbuf, zero above j).
+template <int CPW, int RPL, int C>
+__device__ __forceinline__ void qr_update1(double (&col)[CPW][RPL], const double* vr, double beta) {
+  double w = 0.0;
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) w = fma(vr[32 * r], col[C][r], w);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) w += __shfl_xor_sync(0xffffffffu, w, o);
+  w *= beta;
+#pragma unroll
+  for (int r = 0; r < RPL; ++r) col[C][r] = fma(-vr[32 * r], w, col[C][r]);
+}
+
+// Register-resident variant (k <= 32*RPL, n <= 16*CPW; configs C1, C2, C4): 16 warps own the
+// columns cyclically (column l -> warp l % 16, slot l / 16) and lane L holds rows L, L+32, ... of
+// every owned column in registers.  Per column j only the Householder vector v_j (k doubles) goes
+// through shared memory: the owner of column j+1 updates that column first and publishes pivot
+// j+1, then every warp updates its remaining live columns with all dot products and reductions in
+// flight together.  One barrier per column.  The column loop is unrolled over slots so every slot
+// index is a compile-time constant (no dynamic register-array indexing).
+template <int CPW, int RPL>
+__global__ void __launch_bounds__(32 * QR_REG_WARPS, 1)
+householder_reg_kernel(const double* __restrict__ P, int k, int n, double* __restrict__ R,
+                       double* __restrict__ Aglob, double* __restrict__ diag_out, double* __restrict__ tau_out,
+                       int* status) {
+  __shared__ double vbuf[2][32 * RPL];
+  __shared__ double sh_par[2][3];
+  __shared__ int sh_flag;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) sh_flag = 0;
+  __syncthreads();
+  double col[CPW][RPL];
+  int bad = 0;
+#pragma unroll
+  for (int c = 0; c < CPW; ++c) {
+    const int l = warp + QR_REG_WARPS * c;
+#pragma unroll
+    for (int r = 0; r < RPL; ++r) {
+      const int i = r * 32 + lane;
+      double v = 0.0;
+      if (l < n && i < k) v = P[(size_t)i * n + l];
+      if (!isfinite(v)) bad = 1;
+      col[c][r] = v;
+    }
+  }
+  if (__syncthreads_or(bad)) {
+    for (int c = tid; c < n * n; c += 32 * QR_REG_WARPS) R[c] = 0.0;
+    if (tid == 0) atomicOr(status, kStNonfinite);
+    return;
+  }
+  if (warp == 0) qr_publish<CPW, RPL, 0>(col, 0, k, n, lane, vbuf, sh_par, Aglob, diag_out, tau_out);
+  __syncthreads();
+  auto step = [&](auto CC, int jj) {            // column j = 16*C + jj (owner: warp jj, slot C)
+    constexpr int C = decltype(CC)::value;
+    const int j = QR_REG_WARPS * C + jj;
+    if (j >= n) return;
+    const double beta = sh_par[j & 1][0];
+    const double* vr = vbuf[j & 1] + lane;
+    const int jn = j + 1;
+    // owner of column j+1: warp jj+1 slot C, or warp 0 slot C+1 when jj == 15
+    if (jn < n) {
+      if (jj + 1 < QR_REG_WARPS) {
+        if (warp == jj + 1) {
+          if (beta != 0.0) qr_update1<CPW, RPL, C>(col, vr, beta);
+          qr_publish<CPW, RPL, C>(col, jn, k, n, lane, vbuf, sh_par, Aglob, diag_out, tau_out);
+        }
+      } else if constexpr (C + 1 < CPW) {
+        if (warp == 0) {
+          if (beta != 0.0) qr_update1<CPW, RPL, C + 1>(col, vr, beta);
+          qr_publish<CPW, RPL, C + 1>(col, jn, k, n, lane, vbuf, sh_par, Aglob, diag_out, tau_out);
+        }
+      }
+    }
+    // every other live owned column l > j+1: all dots, one interleaved reduction, all axpys
+    if (beta != 0.0) {
+      double w[CPW];
+#pragma unroll
+      for (int c = 0; c < CPW; ++c) w[c] = 0.0;
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const double v = vr[32 * r];
+#pragma unroll
+        for (int c = C; c < CPW; ++c) w[c] = fma(v, col[c][r], w[c]);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int c = C; c < CPW; ++c) w[c] += __shfl_xor_sync(0xffffffffu, w[c], o);
+#pragma unroll
+      for (int c = C; c < CPW; ++c) {
+        const int l = warp + QR_REG_WARPS * c;
+        w[c] = (l > jn && l < n) ? w[c] * beta : 0.0;
+      }
+#pragma unroll
+      for (int r = 0; r < RPL; ++r) {
+        const double v = vr[32 * r];
+#pragma unroll
+        for (int c = C; c < CPW; ++c) col[c][r] = fma(-v, w[c], col[c][r]);
+      }
+    }
+    // row j of R (raw; signs fixed at the end): A[j][l] for the owned columns l > j
+    if (lane == (j & 31)) {
+#pragma unroll
+      for (int c = C; c < CPW; ++c) {
+        const int l = warp + QR_REG_WARPS * c;
+        if (l > j && l < n) {
+#pragma unroll
+          for (int r = 0; r < RPL; ++r)
+            if (r == (j >> 5)) R[(size_t)j * n + l] = col[c][r];
+        }
+      }
+    }
+    __syncthreads();
+  };
+  [&]<int... Cs>(std::integer_sequence<int, Cs...>) {
+    (([&] {
+       for (int jj = 0; jj < QR_REG_WARPS; ++jj) step(std::integral_constant<int, Cs>{}, jj);
+     }()), ...);
+  }(std::make_integer_sequence<int, CPW>{});
+  for (int c = tid; c < n * n; c += 32 * QR_REG_WARPS) {
+    const int j = c / n, l = c % n;
+    const double d = diag_out[j];
+    const double sg = d < 0.0 ? -1.0 : 1.0;
+    if (l < j) R[c] = 0.0;
+    else if (l == j) R[c] = sg * d;
+    else R[c] = sg * R[c];
+  }
+  if (tid < 32) {
+    int b2 = 0;
+    for (int j = lane; j < n; j += 32) {
+      const double d = diag_out[j];
+      if (d == 0.0 || !isfinite(d)) b2 = 1;
+    }
+    b2 = __any_sync(0xffffffffu, b2);
+    if (lane == 0 && b2) atomicOr(status, kStSingular);
+  }
+}
+
 // S = H_0 ... H_{n-1} [I_n; 0], then column l negated where diag_l < 0.  One warp per column;
 // the column lives in a shared-memory buffer of k doubles per warp.
 constexpr int FS_WARPS = 4;
@@ -158,7 +350,11 @@ int plan_qr(int k, int n, size_t smem_optin) {
 
 cudaError_t launch_qr(int kind, const double* P, int k, int n, double* R, double* Awork, double* diag,
                       double* tau, int* status, cudaStream_t st) {
-  if (kind == kQrSmem) {
+  if (k <= 32 * 4 && n <= QR_REG_WARPS * 4) {
+    householder_reg_kernel<4, 4><<<1, 32 * QR_REG_WARPS, 0, st>>>(P, k, n, R, Awork, diag, tau, status);
+  } else if (k <= 32 * 7 && n <= QR_REG_WARPS * 7) {
+    householder_reg_kernel<7, 7><<<1, 32 * QR_REG_WARPS, 0, st>>>(P, k, n, R, Awork, diag, tau, status);
+  } else if (kind == kQrSmem) {
     const size_t smem = sizeof(double) * (size_t)k * n;
     cudaError_t e = cudaFuncSetAttribute(householder_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
