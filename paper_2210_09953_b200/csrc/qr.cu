@@ -142,11 +142,10 @@ __device__ __forceinline__ void pivot_params(double ss, double x0, double* par) 
 // publishes (beta, v0, R_jj) and v_{j+1}, then all warps update their other columns two at a time
 // (two dot products and reductions in flight).  One barrier per column; rows above the pivot need no
 // predicate because v_j is zero there.
-constexpr int QR_REG_WARPS = 16;
 
 // Pivot column j sits in slot C (compile time) of warp j % 16: norm below row j, pivot parameters,
 // v_j into shared memory (and the reflector into the global workspace for S).
-template <int CPW, int RPL, int C>
+template <int CPW, int RPL, int C, int NW>
 __device__ __forceinline__ void qr_publish(const double (&col)[CPW][RPL], int j, int k, int n, int lane,
                                            double (*vbuf)[32 * RPL], double (*sh_par)[3], double* Aglob,
                                            double* diag_out, double* tau_out) {
@@ -198,8 +197,8 @@ __device__ __forceinline__ void qr_update1(double (&col)[CPW][RPL], const double
 // j+1, then every warp updates its remaining live columns with all dot products and reductions in
 // flight together.  One barrier per column.  The column loop is unrolled over slots so every slot
 // index is a compile-time constant (no dynamic register-array indexing).
-template <int CPW, int RPL>
-__global__ void __launch_bounds__(32 * QR_REG_WARPS, 1)
+template <int CPW, int RPL, int NW>
+__global__ void __launch_bounds__(32 * NW, 1)
 householder_reg_kernel(const double* __restrict__ P, int k, int n, double* __restrict__ R,
                        double* __restrict__ Aglob, double* __restrict__ diag_out, double* __restrict__ tau_out,
                        int* status) {
@@ -213,7 +212,7 @@ householder_reg_kernel(const double* __restrict__ P, int k, int n, double* __res
   int bad = 0;
 #pragma unroll
   for (int c = 0; c < CPW; ++c) {
-    const int l = warp + QR_REG_WARPS * c;
+    const int l = warp + NW * c;
 #pragma unroll
     for (int r = 0; r < RPL; ++r) {
       const int i = r * 32 + lane;
@@ -224,30 +223,30 @@ householder_reg_kernel(const double* __restrict__ P, int k, int n, double* __res
     }
   }
   if (__syncthreads_or(bad)) {
-    for (int c = tid; c < n * n; c += 32 * QR_REG_WARPS) R[c] = 0.0;
+    for (int c = tid; c < n * n; c += 32 * NW) R[c] = 0.0;
     if (tid == 0) atomicOr(status, kStNonfinite);
     return;
   }
-  if (warp == 0) qr_publish<CPW, RPL, 0>(col, 0, k, n, lane, vbuf, sh_par, Aglob, diag_out, tau_out);
+  if (warp == 0) qr_publish<CPW, RPL, 0, NW>(col, 0, k, n, lane, vbuf, sh_par, Aglob, diag_out, tau_out);
   __syncthreads();
   auto step = [&](auto CC, int jj) {            // column j = 16*C + jj (owner: warp jj, slot C)
     constexpr int C = decltype(CC)::value;
-    const int j = QR_REG_WARPS * C + jj;
+    const int j = NW * C + jj;
     if (j >= n) return;
     const double beta = sh_par[j & 1][0];
     const double* vr = vbuf[j & 1] + lane;
     const int jn = j + 1;
     // owner of column j+1: warp jj+1 slot C, or warp 0 slot C+1 when jj == 15
     if (jn < n) {
-      if (jj + 1 < QR_REG_WARPS) {
+      if (jj + 1 < NW) {
         if (warp == jj + 1) {
           if (beta != 0.0) qr_update1<CPW, RPL, C>(col, vr, beta);
-          qr_publish<CPW, RPL, C>(col, jn, k, n, lane, vbuf, sh_par, Aglob, diag_out, tau_out);
+          qr_publish<CPW, RPL, C, NW>(col, jn, k, n, lane, vbuf, sh_par, Aglob, diag_out, tau_out);
         }
       } else if constexpr (C + 1 < CPW) {
         if (warp == 0) {
           if (beta != 0.0) qr_update1<CPW, RPL, C + 1>(col, vr, beta);
-          qr_publish<CPW, RPL, C + 1>(col, jn, k, n, lane, vbuf, sh_par, Aglob, diag_out, tau_out);
+          qr_publish<CPW, RPL, C + 1, NW>(col, jn, k, n, lane, vbuf, sh_par, Aglob, diag_out, tau_out);
         }
       }
     }
@@ -268,7 +267,7 @@ householder_reg_kernel(const double* __restrict__ P, int k, int n, double* __res
         for (int c = C; c < CPW; ++c) w[c] += __shfl_xor_sync(0xffffffffu, w[c], o);
 #pragma unroll
       for (int c = C; c < CPW; ++c) {
-        const int l = warp + QR_REG_WARPS * c;
+        const int l = warp + NW * c;
         w[c] = (l > jn && l < n) ? w[c] * beta : 0.0;
       }
 #pragma unroll
@@ -282,7 +281,7 @@ householder_reg_kernel(const double* __restrict__ P, int k, int n, double* __res
     if (lane == (j & 31)) {
 #pragma unroll
       for (int c = C; c < CPW; ++c) {
-        const int l = warp + QR_REG_WARPS * c;
+        const int l = warp + NW * c;
         if (l > j && l < n) {
 #pragma unroll
           for (int r = 0; r < RPL; ++r)
@@ -294,10 +293,10 @@ householder_reg_kernel(const double* __restrict__ P, int k, int n, double* __res
   };
   [&]<int... Cs>(std::integer_sequence<int, Cs...>) {
     (([&] {
-       for (int jj = 0; jj < QR_REG_WARPS; ++jj) step(std::integral_constant<int, Cs>{}, jj);
+       for (int jj = 0; jj < NW; ++jj) step(std::integral_constant<int, Cs>{}, jj);
      }()), ...);
   }(std::make_integer_sequence<int, CPW>{});
-  for (int c = tid; c < n * n; c += 32 * QR_REG_WARPS) {
+  for (int c = tid; c < n * n; c += 32 * NW) {
     const int j = c / n, l = c % n;
     const double d = diag_out[j];
     const double sg = d < 0.0 ? -1.0 : 1.0;
@@ -350,10 +349,10 @@ int plan_qr(int k, int n, size_t smem_optin) {
 
 cudaError_t launch_qr(int kind, const double* P, int k, int n, double* R, double* Awork, double* diag,
                       double* tau, int* status, cudaStream_t st) {
-  if (k <= 32 * 4 && n <= QR_REG_WARPS * 4) {
-    householder_reg_kernel<4, 4><<<1, 32 * QR_REG_WARPS, 0, st>>>(P, k, n, R, Awork, diag, tau, status);
-  } else if (k <= 32 * 7 && n <= QR_REG_WARPS * 7) {
-    householder_reg_kernel<7, 7><<<1, 32 * QR_REG_WARPS, 0, st>>>(P, k, n, R, Awork, diag, tau, status);
+  if (k <= 32 * 4 && n <= 16 * 4) {
+    householder_reg_kernel<4, 4, 16><<<1, 32 * 16, 0, st>>>(P, k, n, R, Awork, diag, tau, status);
+  } else if (k <= 32 * 7 && n <= 16 * 7) {
+    householder_reg_kernel<7, 7, 16><<<1, 32 * 16, 0, st>>>(P, k, n, R, Awork, diag, tau, status);
   } else if (kind == kQrSmem) {
     const size_t smem = sizeof(double) * (size_t)k * n;
     cudaError_t e = cudaFuncSetAttribute(householder_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
