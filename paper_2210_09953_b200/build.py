@@ -40,7 +40,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     nvcc = os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "bin", "nvcc")
     tmp = LIB + ".tmp%d" % os.getpid()
-    cmd = [nvcc, "-O3", "-std=c++17", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
+    cmd = [nvcc, "-O3", "-std=c++20", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
            "-I" + os.path.join(ROOT, "include"), "-I" + _nccl_include(),
            "-o", tmp, *SRCS, "-ldl"]
     if verbose:
