@@ -10,6 +10,7 @@
 //           X is widened to fp64 on the way into shared memory; Q is rounded once to X's dtype.
 #include <cuda_runtime.h>
 #include <algorithm>
+#include <cstdlib>
 #include "internal.cuh"
 
 namespace rcq {
@@ -465,12 +466,25 @@ trsm_warp_kernel(const TX* __restrict__ X, int64_t m, int n, int NPAD, int64_t l
       else if (tile + nw < ntiles) prefetch(tile + nw, 0);
       // phase 1: T_J = X_J + Q_{<J} (-R_{<J,J})
       const double* arow = Aw + g * LD + t4;
-      for (int ks = 0; ks < c0 / 4; ++ks) {
-        const double a0 = arow[4 * ks], a1 = arow[8 * LD + 4 * ks];
-        const double* mrow = Ms + (4 * ks + t4) * LD + c0 + g;
+      if (nt8 == TB / 8) {             // full-width block: no per-MMA predicates (no WARPSYNC)
+#pragma unroll 4
+        for (int ks = 0; ks < c0 / 4; ++ks) {
+          const double a0 = arow[4 * ks], a1 = arow[8 * LD + 4 * ks];
+          const double* mrow = Ms + (4 * ks + t4) * LD + c0 + g;
+          double b[TB / 8];
 #pragma unroll
-        for (int u = 0; u < TB / 8; ++u)
-          if (u < nt8) dmma_16x8x4(acc[u], a0, a1, mrow[8 * u]);
+          for (int u = 0; u < TB / 8; ++u) b[u] = mrow[8 * u];
+#pragma unroll
+          for (int u = 0; u < TB / 8; ++u) dmma_16x8x4(acc[u], a0, a1, b[u]);
+        }
+      } else {
+        for (int ks = 0; ks < c0 / 4; ++ks) {
+          const double a0 = arow[4 * ks], a1 = arow[8 * LD + 4 * ks];
+          const double* mrow = Ms + (4 * ks + t4) * LD + c0 + g;
+#pragma unroll
+          for (int u = 0; u < TB / 8; ++u)
+            if (u < nt8) dmma_16x8x4(acc[u], a0, a1, mrow[8 * u]);
+        }
       }
 #pragma unroll
       for (int u = 0; u < TB / 8; ++u) {
@@ -514,6 +528,118 @@ trsm_warp_kernel(const TX* __restrict__ X, int64_t m, int n, int NPAD, int64_t l
         }
       }
       __syncwarp();
+    }
+  }
+}
+
+// Warp-pair variant: two warps share one 16-row tile (each owns half of the 8-column MMA tiles of a
+// block), so 16 warps run with the same shared-memory slabs as 8 -- twice the warps per SMSP to
+// hide DMMA/shared-memory latency.  The pair synchronises with a 64-thread named barrier.
+__device__ __forceinline__ void pair_sync(int id) { asm volatile("bar.sync %0, 64;\n" ::"r"(id) : "memory"); }
+
+template <typename TX, int PAIRS>
+__global__ void __launch_bounds__(64 * PAIRS, 1)
+trsm_pair_kernel(const TX* __restrict__ X, int64_t m, int n, int NPAD, int64_t ldx, const double* __restrict__ Mg,
+                 TX* __restrict__ Q, int64_t ldq, const int* status) {
+  if (*status) return;
+  extern __shared__ __align__(16) double smem_w[];
+  const int LD = NPAD + 4;
+  double* Ms = smem_w;                            // [NPAD][LD]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  const int pair = warp >> 1, h = warp & 1;
+  double* Aw = smem_w + (size_t)NPAD * LD + (size_t)pair * 16 * LD;   // the pair's [16][LD] slab
+  for (int c = threadIdx.x; c < NPAD * NPAD; c += 64 * PAIRS) Ms[(c / NPAD) * LD + (c % NPAD)] = Mg[c];
+  __syncthreads();
+  const int NBLK = (NPAD + TB - 1) / TB;
+  const int64_t ntiles = (m + 15) / 16;
+  const int64_t gp = (int64_t)blockIdx.x * PAIRS + pair, np = (int64_t)gridDim.x * PAIRS;
+  constexpr int HU = TB / 16;                     // 8-column MMA tiles per warp per block (2)
+  TX xn[HU][4];
+  auto prefetch = [&](int64_t tile, int J) {
+#pragma unroll
+    for (int v = 0; v < HU; ++v)
+      load_x_frag(X, m, n, ldx, tile * 16, J * TB + 8 * (HU * h + v) + 2 * t4, g, xn[v]);
+  };
+  if (gp < ntiles) prefetch(gp, 0);
+  const double* arow = Aw + g * LD + t4;
+  for (int64_t tile = gp; tile < ntiles; tile += np) {
+    const int64_t r0 = tile * 16;
+    for (int J = 0; J < NBLK; ++J) {
+      const int c0 = J * TB;
+      const int nt8 = min(TB, NPAD - c0) / 8;
+      double acc[HU][4];
+#pragma unroll
+      for (int v = 0; v < HU; ++v)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[v][e] = (double)xn[v][e];
+      if (J + 1 < NBLK) prefetch(tile, J + 1);
+      else if (tile + np < ntiles) prefetch(tile + np, 0);
+      const int u0 = HU * h;                      // this warp's first 8-column tile of the block
+      const bool full = nt8 == TB / 8;
+      // phase 1: T_J = X_J + Q_{<J} (-R_{<J,J}) for this warp's tiles
+      if (full) {
+#pragma unroll 4
+        for (int ks = 0; ks < c0 / 4; ++ks) {
+          const double a0 = arow[4 * ks], a1 = arow[8 * LD + 4 * ks];
+          const double* mrow = Ms + (4 * ks + t4) * LD + c0 + 8 * u0 + g;
+          const double b0 = mrow[0], b1 = mrow[8];
+          dmma_16x8x4(acc[0], a0, a1, b0);
+          dmma_16x8x4(acc[1], a0, a1, b1);
+        }
+      } else {
+        for (int ks = 0; ks < c0 / 4; ++ks) {
+          const double a0 = arow[4 * ks], a1 = arow[8 * LD + 4 * ks];
+          const double* mrow = Ms + (4 * ks + t4) * LD + c0 + g;
+#pragma unroll
+          for (int v = 0; v < HU; ++v)
+            if (u0 + v < nt8) dmma_16x8x4(acc[v], a0, a1, mrow[8 * (u0 + v)]);
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < HU; ++v) {
+        if (u0 + v < nt8) {
+          double* tp = Aw + g * LD + c0 + 8 * (u0 + v) + 2 * t4;
+          tp[0] = acc[v][0]; tp[1] = acc[v][1]; tp[8 * LD] = acc[v][2]; tp[8 * LD + 1] = acc[v][3];
+        }
+      }
+      pair_sync(1 + pair);                        // all of T_J visible to both warps
+      // phase 2: Q_J = T_J Winv_JJ (upper triangular: skip k-steps past each 8-column tile)
+#pragma unroll
+      for (int v = 0; v < HU; ++v)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[v][e] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < TB / 4; ++ks) {
+        if (4 * ks < 8 * nt8 && 4 * ks <= 8 * (u0 + HU - 1) + 7) {
+          const double a0 = arow[c0 + 4 * ks], a1 = arow[8 * LD + c0 + 4 * ks];
+          const double* mrow = Ms + (c0 + 4 * ks + t4) * LD + c0 + g;
+#pragma unroll
+          for (int v = 0; v < HU; ++v) {
+            const int u = u0 + v;
+            if (u < nt8 && 4 * ks <= 8 * u + 7) dmma_16x8x4(acc[v], a0, a1, mrow[8 * u]);
+          }
+        }
+      }
+      pair_sync(1 + pair);                        // both warps done reading T_J
+#pragma unroll
+      for (int v = 0; v < HU; ++v) {
+        const int u = u0 + v;
+        if (u < nt8) {
+          const int col = c0 + 8 * u + 2 * t4;
+          double* tp = Aw + g * LD + col;
+          tp[0] = acc[v][0]; tp[1] = acc[v][1]; tp[8 * LD] = acc[v][2]; tp[8 * LD + 1] = acc[v][3];
+          const int64_t ra = r0 + g, rb = r0 + g + 8;
+          if (ra < m) {
+            if (col < n) Q[ra * ldq + col] = to_out<TX>(acc[v][0]);
+            if (col + 1 < n) Q[ra * ldq + col + 1] = to_out<TX>(acc[v][1]);
+          }
+          if (rb < m) {
+            if (col < n) Q[rb * ldq + col] = to_out<TX>(acc[v][2]);
+            if (col + 1 < n) Q[rb * ldq + col + 1] = to_out<TX>(acc[v][3]);
+          }
+        }
+      }
+      pair_sync(1 + pair);                        // Q_J history visible before the next block
     }
   }
 }
@@ -577,6 +703,8 @@ static size_t warp_smem(int npad, int warps) { return sizeof(double) * (size_t)(
 int trsm_warp_count(int n, size_t smem_optin) {
   const int npad = (n + 7) / 8 * 8;
   if (n > 128) return 0;
+  const char* f = getenv("RCHOLQR_SOLVE_WARPS");  // experiments: 8 = one warp per tile
+  if (!(f && atoi(f) == 8) && warp_smem(npad, 8) <= smem_optin) return 16;   // 8 warp pairs
   if (warp_smem(npad, 8) <= smem_optin) return 8;
   if (warp_smem(npad, 4) <= smem_optin) return 4;
   return 0;
@@ -597,8 +725,26 @@ static cudaError_t launch_w(const void* X, int64_t m, int n, int64_t ldx, const 
   return cudaGetLastError();
 }
 
+template <typename TX, int PAIRS>
+static cudaError_t launch_p(const void* X, int64_t m, int n, int64_t ldx, const double* M, void* Q, int64_t ldq,
+                            const int* status, int sms, cudaStream_t st) {
+  const int npad = (n + 7) / 8 * 8;
+  const size_t smem = warp_smem(npad, PAIRS);
+  auto kern = trsm_pair_kernel<TX, PAIRS>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  const int64_t ntiles = (m + 15) / 16;
+  const int grid = (int)std::min<int64_t>((ntiles + PAIRS - 1) / PAIRS, sms);
+  if (grid == 0) return cudaSuccess;
+  kern<<<grid, 64 * PAIRS, smem, st>>>((const TX*)X, m, n, npad, ldx, M, (TX*)Q, ldq, status);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_trsm_warp(int warps, const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M,
                              void* Q, int64_t ldq, const int* status, int sms, cudaStream_t st) {
+  if (warps == 16)
+    return dtype == RCHOLQR_F64 ? launch_p<double, 8>(X, m, n, ldx, M, Q, ldq, status, sms, st)
+                                : launch_p<float, 8>(X, m, n, ldx, M, Q, ldq, status, sms, st);
   if (dtype == RCHOLQR_F64)
     return warps == 8 ? launch_w<double, 8>(X, m, n, ldx, M, Q, ldq, status, sms, st)
                       : launch_w<double, 4>(X, m, n, ldx, M, Q, ldq, status, sms, st);
