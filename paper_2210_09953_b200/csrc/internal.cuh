@@ -21,7 +21,7 @@ __device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1
 
 // ---- launch configurations chosen at plan creation ----
 enum SketchKind : int { kSketchG48x24 = 0, kSketchG128x64 = 1, kSketchG112x104 = 2, kSketchG64x64 = 3,
-                        kSketchSparse = 10 };
+                        kSketchSparse = 10, kSketchSparseReg = 11 };
 enum TrsmKind : int { kTrsm64x24 = 0, kTrsm128x64 = 1, kTrsm128x112 = 2, kTrsm128x128 = 3 };
 enum QrKind : int { kQrSmem = 0, kQrGlobal = 1 };
 

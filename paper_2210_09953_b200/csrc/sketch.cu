@@ -297,6 +297,119 @@ sketch_sparse_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, in
   }
 }
 
+// Register-resident sparse-sign sketch (zeta <= 8, beta = k/zeta <= 16, n <= 64): warp t owns Theta
+// block t, i.e. the beta x n tile P[t*beta .. t*beta+beta-1, :] in registers (lane L: columns
+// L, L+32).  For every X row the block's target row h is warp-uniform, so a uniform switch adds
+// the (sign-flipped) row into acc[h] -- no shared-memory read-modify-write chain.  X chunks are
+// widened to fp64 once in shared memory (shared by the zeta warps); the next chunk is prefetched
+// into registers while the current one is consumed.
+constexpr int SPR_KC = 32;       // rows per chunk (= warp size: one ballot per target row)
+constexpr int SPR_STAGES = 4;    // cp.async ring depth (raw X chunks in flight per CTA)
+constexpr int SPR_THREADS = 256;
+template <typename TX, int BETA, int CPL>
+__global__ void __launch_bounds__(SPR_THREADS)
+sketch_sparse_reg_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
+                         int zeta, uint64_t seed, int64_t rows_per_split, double* __restrict__ part) {
+  constexpr int NC = 32 * CPL;
+  extern __shared__ __align__(16) unsigned char spr_smem[];
+  double (*Xs)[NC] = reinterpret_cast<double (*)[NC]>(spr_smem);                        // [KC][NC] fp64
+  TX (*Xraw)[SPR_KC][NC] = reinterpret_cast<TX (*)[SPR_KC][NC]>(spr_smem + sizeof(double) * SPR_KC * NC);
+  uint8_t (*sel)[SPR_KC][8] = reinterpret_cast<uint8_t (*)[SPR_KC][8]>(
+      spr_smem + sizeof(double) * SPR_KC * NC + sizeof(TX) * SPR_STAGES * SPR_KC * NC);
+  const int split = blockIdx.x;
+  const int64_t i_begin = (int64_t)split * rows_per_split;
+  const int64_t i_end = min(m, i_begin + rows_per_split);
+  const int nchunks = i_end > i_begin ? (int)((i_end - i_begin + SPR_KC - 1) / SPR_KC) : 0;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  double acc[BETA][CPL];
+#pragma unroll
+  for (int r = 0; r < BETA; ++r)
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) acc[r][c] = 0.0;
+  auto issue = [&](int ch) {      // cp.async chunk ch (zero-filled tails) + its row selections
+    const int st = ch % SPR_STAGES;
+    const int64_t i0 = i_begin + (int64_t)ch * SPR_KC;
+    const int rows_here = (int)min((int64_t)SPR_KC, i_end - i0);
+    const TX* xbase = X + i0 * ldx;
+#pragma unroll
+    for (int u = 0; u < SPR_KC * NC / SPR_THREADS; ++u) {
+      const int cidx = tid + u * SPR_THREADS;
+      const int ii = cidx / NC, jj = cidx % NC;              // NC is a power of two
+      const bool ok = ii < rows_here && jj < n;
+      const TX* src = ok ? xbase + (int64_t)ii * ldx + jj : X;
+      if (sizeof(TX) == 4) cp_async_zfill4(&Xraw[st][ii][jj], src, ok);
+      else cp_async_zfill8(&Xraw[st][ii][jj], src, ok);
+    }
+    cp_async_commit_grp();
+    if (tid < SPR_KC) {
+      uint32_t w0 = 0xFFFFFFFFu, w1 = 0xFFFFFFFFu;   // 0xFF = "no row" (tail)
+      if (i0 + tid < i_end) {
+        const uint4 w = philox_at(seed, (uint64_t)(row_offset + i0 + tid), 0u, kDomainSparse);
+        const int beta = k / zeta;
+        w0 = w1 = 0u;
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          uint32_t code = 0xFFu;
+          if (t < zeta) {
+            const uint32_t hw = sparse_halfword(w, t);
+            code = (uint32_t)(sparse_row(hw, t, beta) - t * beta) | ((hw >> 15) << 4);
+          }
+          if (t < 4) w0 |= code << (8 * t); else w1 |= code << (8 * (t - 4));
+        }
+      }
+      *reinterpret_cast<uint32_t*>(&sel[st][tid][0]) = w0;
+      *reinterpret_cast<uint32_t*>(&sel[st][tid][4]) = w1;
+    }
+  };
+#pragma unroll 1
+  for (int c = 0; c < SPR_STAGES - 1; ++c) {
+    if (c < nchunks) issue(c);
+    else cp_async_commit_grp();
+  }
+  for (int ch = 0; ch < nchunks; ++ch) {
+    const int st = ch % SPR_STAGES;
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(SPR_STAGES - 2) : "memory");
+    __syncthreads();   // chunk ch landed for everyone; Xs free (previous chunk consumed)
+#pragma unroll
+    for (int u = 0; u < SPR_KC * NC / SPR_THREADS; ++u) {
+      const int cidx = tid + u * SPR_THREADS;
+      Xs[cidx / NC][cidx % NC] = (double)Xraw[st][cidx / NC][cidx % NC];
+    }
+    __syncthreads();
+    if (ch + SPR_STAGES - 1 < nchunks) issue(ch + SPR_STAGES - 1);
+    else cp_async_commit_grp();
+    if (warp < zeta) {
+      // bucket the chunk's 32 rows by target row h (lane = row): one ballot per h, then the rows of
+      // bucket h are added into the statically indexed acc[h] (no indirect branch)
+      const uint32_t mycode = sel[st][lane][warp];
+      const uint32_t negmask = __ballot_sync(0xffffffffu, (mycode & 16u) != 0);
+#pragma unroll
+      for (int r = 0; r < BETA; ++r) {
+        uint32_t mask = __ballot_sync(0xffffffffu, (mycode & 0xEFu) == (uint32_t)r);
+        while (mask) {
+          const int ii = __ffs(mask) - 1;
+          mask &= mask - 1;
+          const double sg = ((negmask >> ii) & 1u) ? -1.0 : 1.0;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) acc[r][c] = fma(Xs[ii][lane + 32 * c], sg, acc[r][c]);
+        }
+      }
+    }
+  }
+  cp_async_wait_0();
+  if (warp < zeta) {
+    const int beta = k / zeta;
+    double* Pp = part + (size_t)split * (size_t)k * n;
+#pragma unroll
+    for (int r = 0; r < BETA; ++r)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        const int col = lane + 32 * c;
+        if (r < beta && col < n) Pp[(size_t)(warp * beta + r) * n + col] = acc[r][c];
+      }
+  }
+}
+
 // Fixed-order sum of the per-split partials, one scaling, non-finite detection.
 __global__ void sketch_reduce_kernel(const double* __restrict__ part, const double* __restrict__ partc, int splits,
                                      int64_t kn, double scale, double* __restrict__ P, int* status) {
@@ -429,6 +542,13 @@ static int choose_splits(int tiles, int sms) {
 
 SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms, size_t smem_optin) {
   SketchLaunch L{};
+  if (sketch == RCHOLQR_SPARSE_SIGN && zeta <= 8 && k / zeta <= 16 && n <= 64 && !getenv("RCHOLQR_SPARSE_SMEM")) {
+    L.kind = kSketchSparseReg;
+    L.threads = SPR_THREADS;
+    L.KT = k; L.NT = n; L.tiles_k = 1; L.tiles_n = 1; L.smem = 0;
+    L.splits = choose_splits(1, 2 * sms);
+    return L;
+  }
   if (sketch == RCHOLQR_SPARSE_SIGN) {
     L.kind = kSketchSparse;
     L.threads = SPARSE_THREADS;
@@ -502,7 +622,27 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
   cudaError_t e;
   const int64_t per = (m + L.splits - 1) / L.splits;
   double scale;
-  if (L.kind == kSketchSparse) {
+  if (L.kind == kSketchSparseReg) {
+    const int64_t rps = std::max<int64_t>(SPR_KC, ((per + SPR_KC - 1) / SPR_KC) * SPR_KC);
+    const int beta = k / zeta;
+    auto launch = [&](auto* tag) -> cudaError_t {
+      using TX = std::remove_pointer_t<decltype(tag)>;
+      auto go = [&](auto kern, int cpl) -> cudaError_t {
+        const size_t sm = (sizeof(double) + sizeof(TX) * SPR_STAGES) * SPR_KC * 32 * cpl + SPR_STAGES * SPR_KC * 8;
+        cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        if (e2 != cudaSuccess) return e2;
+        kern<<<L.splits, SPR_THREADS, sm, st>>>((const TX*)X, m, n, ldx, row_offset, k, zeta, seed, rps, part);
+        return cudaSuccess;
+      };
+      cudaError_t e2;
+      if (beta <= 8) e2 = n <= 32 ? go(sketch_sparse_reg_kernel<TX, 8, 1>, 1) : go(sketch_sparse_reg_kernel<TX, 8, 2>, 2);
+      else e2 = n <= 32 ? go(sketch_sparse_reg_kernel<TX, 16, 1>, 1) : go(sketch_sparse_reg_kernel<TX, 16, 2>, 2);
+      if (e2 != cudaSuccess) return e2;
+      return cudaGetLastError();
+    };
+    e = dtype == RCHOLQR_F64 ? launch((double*)nullptr) : launch((float*)nullptr);
+    scale = 1.0 / std::sqrt((double)zeta);
+  } else if (L.kind == kSketchSparse) {
     const int64_t rps = std::max<int64_t>(KCS, ((per + KCS - 1) / KCS) * KCS);
     auto launch = [&](auto* tag) -> cudaError_t {
       using TX = std::remove_pointer_t<decltype(tag)>;
@@ -526,7 +666,7 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
   const int64_t kn = (int64_t)k * n;
   const int threads = 256;
   const int blocks = (int)std::min<int64_t>((kn + threads - 1) / threads, 4096);
-  sketch_reduce_kernel<<<blocks, threads, 0, st>>>(part, L.kind == kSketchSparse ? nullptr : partc, L.splits, kn,
+  sketch_reduce_kernel<<<blocks, threads, 0, st>>>(part, (L.kind == kSketchSparse || L.kind == kSketchSparseReg) ? nullptr : partc, L.splits, kn,
                                                    scale, P, status);
   return cudaGetLastError();
 }
