@@ -21,7 +21,14 @@ __device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1
 
 // ---- launch configurations chosen at plan creation ----
 enum SketchKind : int { kSketchG48x24 = 0, kSketchG128x64 = 1, kSketchG112x104 = 2, kSketchG64x64 = 3,
-                        kSketchSparse = 10, kSketchSparseReg = 11 };
+                        kSketchSparse = 10, kSketchSparseReg = 11, kSketchSparseTC = 12 };
+// tcgen05 int8 sparse sketch (sketch_tc.cu): exact int32 accumulation bound on rows per CTA
+constexpr int64_t kSparseTcMaxRows = 8 * 1024 * 1024;
+bool sparse_tc_applicable(int k, int n, int zeta);
+bool sparse_tc_aligned(const void* X, int dtype, int n, int64_t ldx);
+cudaError_t launch_sparse_tc(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
+                             int zeta, uint64_t seed, int splits, int64_t rows_per_split, double* part, int* overflow,
+                             cudaStream_t st);
 enum TrsmKind : int { kTrsm64x24 = 0, kTrsm128x64 = 1, kTrsm128x112 = 2, kTrsm128x128 = 3 };
 enum QrKind : int { kQrSmem = 0, kQrGlobal = 1 };
 

@@ -309,7 +309,10 @@ constexpr int SPR_THREADS = 256;
 template <typename TX, int BETA, int CPL>
 __global__ void __launch_bounds__(SPR_THREADS)
 sketch_sparse_reg_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
-                         int zeta, uint64_t seed, int64_t rows_per_split, double* __restrict__ part) {
+                         int zeta, uint64_t seed, int64_t rows_per_split, double* __restrict__ part,
+                         const int* __restrict__ guard) {
+  // guard != null: recompute only if the tensor-core sketch (sketch_tc.cu) flagged a headroom overflow
+  if (guard && *guard == 0) return;
   constexpr int NC = 32 * CPL;
   extern __shared__ __align__(16) unsigned char spr_smem[];
   double (*Xs)[NC] = reinterpret_cast<double (*)[NC]>(spr_smem);                        // [KC][NC] fp64
@@ -547,6 +550,11 @@ SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms,
     L.threads = SPR_THREADS;
     L.KT = k; L.NT = n; L.tiles_k = 1; L.tiles_n = 1; L.smem = 0;
     L.splits = choose_splits(1, 2 * sms);
+    // tcgen05 int8 path (sketch_tc.cu) with the register kernel as its guarded fallback
+    if (sparse_tc_applicable(k, n, zeta) && !getenv("RCHOLQR_SPARSE_CUDA_CORE")) {
+      L.kind = kSketchSparseTC;
+      L.splits = sms;
+    }
     return L;
   }
   if (sketch == RCHOLQR_SPARSE_SIGN) {
@@ -622,16 +630,29 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
   cudaError_t e;
   const int64_t per = (m + L.splits - 1) / L.splits;
   double scale;
-  if (L.kind == kSketchSparseReg) {
+  if (L.kind == kSketchSparseReg || L.kind == kSketchSparseTC) {
     const int64_t rps = std::max<int64_t>(SPR_KC, ((per + SPR_KC - 1) / SPR_KC) * SPR_KC);
     const int beta = k / zeta;
+    // tensor-core path: the (unused for sparse) compensation buffer's first word is the overflow
+    // flag; the register kernel below then runs only if the flag is raised.  int32 accumulators
+    // are exact while rows_per_split * 255 < 2^31.
+    const int* guard = nullptr;
+    if (L.kind == kSketchSparseTC && rps <= kSparseTcMaxRows && sparse_tc_aligned(X, dtype, n, ldx)) {
+      int* flag = reinterpret_cast<int*>(partc);
+      e = cudaMemsetAsync(flag, 0, sizeof(int), st);
+      if (e != cudaSuccess) return e;
+      e = launch_sparse_tc(X, dtype, m, n, ldx, row_offset, k, zeta, seed, L.splits, rps, part, flag, st);
+      if (e != cudaSuccess) return e;
+      guard = flag;
+    }
     auto launch = [&](auto* tag) -> cudaError_t {
       using TX = std::remove_pointer_t<decltype(tag)>;
       auto go = [&](auto kern, int cpl) -> cudaError_t {
         const size_t sm = (sizeof(double) + sizeof(TX) * SPR_STAGES) * SPR_KC * 32 * cpl + SPR_STAGES * SPR_KC * 8;
         cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         if (e2 != cudaSuccess) return e2;
-        kern<<<L.splits, SPR_THREADS, sm, st>>>((const TX*)X, m, n, ldx, row_offset, k, zeta, seed, rps, part);
+        kern<<<L.splits, SPR_THREADS, sm, st>>>((const TX*)X, m, n, ldx, row_offset, k, zeta, seed, rps, part,
+                                                guard);
         return cudaSuccess;
       };
       cudaError_t e2;
@@ -666,7 +687,8 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
   const int64_t kn = (int64_t)k * n;
   const int threads = 256;
   const int blocks = (int)std::min<int64_t>((kn + threads - 1) / threads, 4096);
-  sketch_reduce_kernel<<<blocks, threads, 0, st>>>(part, (L.kind == kSketchSparse || L.kind == kSketchSparseReg) ? nullptr : partc, L.splits, kn,
+  const bool sparse = L.kind == kSketchSparse || L.kind == kSketchSparseReg || L.kind == kSketchSparseTC;
+  sketch_reduce_kernel<<<blocks, threads, 0, st>>>(part, sparse ? nullptr : partc, L.splits, kn,
                                                    scale, P, status);
   return cudaGetLastError();
 }

@@ -82,6 +82,55 @@ def test_sketch_parity(cuda, m, n, k, dt, sk, c):
     assert _rel(Pg, Po) <= 1e-12, _rel(Pg, Po)
 
 
+SPARSE_TC_CASES = [
+    # m, n, k, dtype, nnz, ldx (None = contiguous): the tcgen05 int8 sparse sketch (sketch_tc.cu)
+    (100_003, 64, 128, "f64", 8, None),          # C4 shape, fp64 X: 8 digit planes
+    (50_001, 20, 40, "f32", 4, None),            # n < 64, k < 128
+    (30_000, 50, 256, "f64", 8, None),           # two Theta row tiles
+    (20_000, 60, 120, "f32", 8, 68),             # strided rows (one bulk copy per row)
+    (20_000, 61, 122, "f32", 2, 63),             # unaligned rows -> CUDA-core kernel
+    (65, 64, 128, "f32", 8, None),               # fewer rows than CTAs, one ragged stage
+]
+
+
+@pytest.mark.parametrize("m,n,k,dt,nnz,ldx", SPARSE_TC_CASES)
+def test_sketch_sparse_tc_parity(cuda, m, n, k, dt, nnz, ldx):
+    X = synth.make_X(m, n, 4.0, dt)
+    Xt = _t(X)
+    if ldx is not None:
+        wide = torch.zeros((m, ldx), dtype=Xt.dtype, device="cuda")
+        wide[:, :n] = Xt
+        Xt = wide[:, :n]
+    plan = _plan(n, k, dt, "sparse", nnz=nnz, seed=11)
+    Pg = _np(plan.sketch(Xt, row_offset=977))
+    Po = oracle.sketch(X, k, sketch=oracle.SPARSE_SIGN, zeta=nnz, seed=11, row_offset=977)
+    assert _rel(Pg, Po) <= 1e-12, _rel(Pg, Po)
+
+
+@pytest.mark.parametrize("dt,case", [("f32", "spike"), ("f64", "spike"), ("f32", "zero_head")])
+def test_sketch_sparse_tc_headroom_overflow(cuda, dt, case):
+    # rows far above each CTA's first-stage column scale, or a column that is zero in every CTA's
+    # first stage, must trigger the guarded CUDA-core recomputation; the result still matches.
+    m, n, k = 300_000, 64, 128
+    X = synth.make_X(m, n, 2.0, dt)
+    if case == "spike":
+        X[1000::4099, :] *= 1e6
+    else:
+        X[np.arange(m) % 2048 < 64, 5] = 0.0
+    plan = _plan(n, k, dt, "sparse", nnz=8)
+    Pg = _np(plan.sketch(_t(X)))
+    Po = oracle.sketch(X, k, sketch=oracle.SPARSE_SIGN, zeta=8)
+    assert _rel(Pg, Po) <= 1e-12, _rel(Pg, Po)
+
+
+def test_sketch_sparse_tc_matches_cuda_core(cuda, monkeypatch):
+    X = _t(synth.make_X(400_000, 64, 5.0, "f32"))
+    a = _np(_plan(64, 128, "f32", "sparse").sketch(X))
+    monkeypatch.setenv("RCHOLQR_SPARSE_CUDA_CORE", "1")
+    b = _np(_plan(64, 128, "f32", "sparse").sketch(X))
+    assert _rel(a, b) <= 1e-13, _rel(a, b)
+
+
 def test_sketch_ld_and_row_offset(cuda):
     X = synth.make_X(5000, 40, 3.0)
     wide = np.zeros((5000, 57))
