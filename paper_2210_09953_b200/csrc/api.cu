@@ -67,6 +67,7 @@ struct rcholqr_plan_s {
   double* tau = nullptr;    // [n] reflector scalings
   double* Rtmp = nullptr;   // [n][n] R when the caller does not want one
   int* status_d = nullptr;
+  int* flag_d = nullptr;    // tensor-core sketch overflow flag (selects the guarded fallback kernel)
   int* status_h = nullptr;  // pinned
   // factor_host staging
   void* xbuf = nullptr; void* qbuf = nullptr; size_t xq_bytes = 0;
@@ -95,6 +96,7 @@ struct DeviceGuard {
 
 rcholqr_status cuda_status(cudaError_t e) {
   if (e == cudaSuccess) return RCHOLQR_OK;
+  if (getenv("RCHOLQR_DEBUG")) fprintf(stderr, "rcholqr: CUDA error: %s\n", cudaGetErrorString(e));
   if (e == cudaErrorMemoryAllocation) return RCHOLQR_E_NOMEM;
   return RCHOLQR_E_CUDA;
 }
@@ -148,7 +150,7 @@ rcholqr_status do_sketch(rcholqr_plan p, const void* X, int64_t m, int64_t ro, i
   const auto& d = p->d;
   if (m > 0) {
     if (p->timing) cudaEventRecord(p->ev[0], st);
-    CU(launch_sketch(p->sk, X, d.dtype, m, d.n, ldx, ro, d.k, d.nnz_per_col, d.seed, p->part, p->partc, P, p->status_d, st,
+    CU(launch_sketch(p->sk, X, d.dtype, m, d.n, ldx, ro, d.k, d.nnz_per_col, d.seed, p->part, p->partc, P, p->status_d, p->flag_d, st,
                      p->timing ? p->ev[1] : nullptr));
   } else {
     if (p->timing) { cudaEventRecord(p->ev[0], st); cudaEventRecord(p->ev[1], st); }
@@ -273,8 +275,9 @@ rcholqr_status rcholqr_create(const rcholqr_desc* desc, rcholqr_plan* out) {
   }
   p->qr_kind = plan_qr(k, n, p->smem_optin);
   const size_t kn = (size_t)k * n, nn = (size_t)((n + 7) / 8 * 8) * ((n + 7) / 8 * 8);
-  bool okalloc = cudaMalloc(&p->part, sizeof(double) * kn * p->sk.splits) == cudaSuccess &&
-                 cudaMalloc(&p->partc, sizeof(double) * kn * p->sk.splits) == cudaSuccess &&
+  bool okalloc = cudaMalloc(&p->part, sizeof(double) * kn * p->sk.max_splits()) == cudaSuccess &&
+                 cudaMalloc(&p->partc, sizeof(double) * kn * p->sk.max_splits()) == cudaSuccess &&
+                 cudaMalloc(&p->flag_d, sizeof(int)) == cudaSuccess &&
                  cudaMalloc(&p->P, sizeof(double) * kn) == cudaSuccess &&
                  cudaMalloc(&p->W, sizeof(double) * nn) == cudaSuccess &&
                  cudaMalloc(&p->Awork, sizeof(double) * kn) == cudaSuccess &&
@@ -301,7 +304,7 @@ rcholqr_status rcholqr_destroy(rcholqr_plan p) {
   if (!p) return RCHOLQR_OK;
   DeviceGuard dg(p->d.device);
   cudaFree(p->part); cudaFree(p->partc); cudaFree(p->P); cudaFree(p->W); cudaFree(p->Awork); cudaFree(p->diag); cudaFree(p->tau);
-  cudaFree(p->Rtmp); cudaFree(p->status_d);
+  cudaFree(p->Rtmp); cudaFree(p->status_d); cudaFree(p->flag_d);
   if (p->status_h) cudaFreeHost(p->status_h);
   cudaFree(p->xbuf); cudaFree(p->qbuf); cudaFree(p->rbuf); cudaFree(p->sbuf); cudaFree(p->tbuf);
   for (int t = 0; t < 7; ++t)

@@ -37,7 +37,15 @@ struct SketchLaunch {
   int KT, NT, threads;   // tile of P per CTA (sparse: NT = columns per CTA, KT = k)
   int tiles_k, tiles_n, splits;
   size_t smem;
+  // Gaussian: tcgen05 digit sketch (sketch_gtc.cu) in front of the DMMA kernel described above
+  int tc = 0, tc_tiles_k = 0, tc_tiles_n = 0, tc_splits = 0;
+  int max_splits() const { return tc && tc_splits > splits ? tc_splits : splits; }
 };
+int gauss_tc_kt(int dtype);   // Theta rows per tcgen05 Gaussian-sketch tile (X columns per tile: 128)
+bool gauss_tc_aligned(const void* X, int dtype, int n, int64_t ldx);
+cudaError_t launch_gauss_tc(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
+                            uint64_t seed, int tiles_k, int tiles_n, int splits, int64_t rows_per_split,
+                            double* part, double* partc, int* overflow, cudaStream_t st);
 struct TrsmLaunch {
   int kind;
   int TM, NT, threads, tiles_n;
@@ -48,7 +56,7 @@ struct TrsmLaunch {
 SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms, size_t smem_optin);
 cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
                           int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* partc, double* P,
-                          int* status, cudaStream_t st, cudaEvent_t ev_mid);
+                          int* status, int* flag, cudaStream_t st, cudaEvent_t ev_mid);
 TrsmLaunch plan_trsm(int n, int dtype, size_t smem_optin);
 cudaError_t launch_tri_inverse(const double* R, int n, double* W, int* status, cudaStream_t st);
 cudaError_t launch_trsm(const TrsmLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,

@@ -86,7 +86,10 @@ template <typename TX, int MS, int NS>
 __global__ void __launch_bounds__(SK_THREADS, 1)
 sketch_gauss_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                     uint64_t seed, int tiles_k, int tiles_n, int64_t rows_per_split,
-                    double* __restrict__ part, double* __restrict__ partc, const WarpPlan plan, int seg_chunks) {
+                    double* __restrict__ part, double* __restrict__ partc, const WarpPlan plan, int seg_chunks,
+                    const int* __restrict__ guard) {
+  // guard != null: recompute only if the tensor-core sketch (sketch_gtc.cu) flagged a headroom overflow
+  if (guard && *guard == 0) return;
   using C = GCfg<TX, MS, NS>;
   constexpr int S = C::STAGES;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -593,12 +596,22 @@ SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms,
   }
   L = cand[best];
   L.splits = choose_splits(L.tiles_k * L.tiles_n, sms);
+  L.tc = 0;
+  // tcgen05 int8 digit sketch (sketch_gtc.cu), the DMMA kernel above as its guarded fallback
+  if (!getenv("RCHOLQR_GAUSS_DMMA")) {
+    const int kt = gauss_tc_kt(dtype);
+    L.tc = 1;
+    L.tc_tiles_k = (k + kt - 1) / kt;
+    L.tc_tiles_n = (n + 127) / 128;
+    L.tc_splits = choose_splits(L.tc_tiles_k * L.tc_tiles_n, sms);
+  }
   return L;
 }
 
 template <typename TX, int MS, int NS>
 static cudaError_t launch_g(const SketchLaunch& L, const void* X, int64_t m, int n, int64_t ldx, int64_t ro,
-                            int k, uint64_t seed, int64_t rps, double* part, double* partc, cudaStream_t st) {
+                            int k, uint64_t seed, int64_t rps, double* part, double* partc, cudaStream_t st,
+                            const int* guard) {
   auto kern = sketch_gauss_kernel<TX, MS, NS>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
   if (e != cudaSuccess) return e;
@@ -608,37 +621,36 @@ static cudaError_t launch_g(const SketchLaunch& L, const void* X, int64_t m, int
     if (plan.cnt[w] > GCfg<TX, MS, NS>::UMAX) return cudaErrorInvalidConfiguration;
   kern<<<L.tiles_k * L.tiles_n * L.splits, SK_THREADS, L.smem, st>>>((const TX*)X, m, n, ldx, ro, k, seed,
                                                                      L.tiles_k, L.tiles_n, rps, part, partc, plan,
-                                                                     seg_chunks());
+                                                                     seg_chunks(), guard);
   return cudaGetLastError();
 }
 
 template <typename TX>
 static cudaError_t launch_gauss_typed(const SketchLaunch& L, const void* X, int64_t m, int n, int64_t ldx,
                                       int64_t ro, int k, uint64_t seed, int64_t rps, double* part, double* partc,
-                                      cudaStream_t st) {
+                                      cudaStream_t st, const int* guard) {
   switch (L.kind) {
-    case kSketchG48x24: return launch_g<TX, 3, 3>(L, X, m, n, ldx, ro, k, seed, rps, part, partc, st);
-    case kSketchG128x64: return launch_g<TX, 8, 8>(L, X, m, n, ldx, ro, k, seed, rps, part, partc, st);
-    case kSketchG112x104: return launch_g<TX, 7, 13>(L, X, m, n, ldx, ro, k, seed, rps, part, partc, st);
-    default: return launch_g<TX, 4, 8>(L, X, m, n, ldx, ro, k, seed, rps, part, partc, st);
+    case kSketchG48x24: return launch_g<TX, 3, 3>(L, X, m, n, ldx, ro, k, seed, rps, part, partc, st, guard);
+    case kSketchG128x64: return launch_g<TX, 8, 8>(L, X, m, n, ldx, ro, k, seed, rps, part, partc, st, guard);
+    case kSketchG112x104: return launch_g<TX, 7, 13>(L, X, m, n, ldx, ro, k, seed, rps, part, partc, st, guard);
+    default: return launch_g<TX, 4, 8>(L, X, m, n, ldx, ro, k, seed, rps, part, partc, st, guard);
   }
 }
 
 cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
                           int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* partc, double* P,
-                          int* status, cudaStream_t st, cudaEvent_t ev_mid) {
+                          int* status, int* flag, cudaStream_t st, cudaEvent_t ev_mid) {
   cudaError_t e;
   const int64_t per = (m + L.splits - 1) / L.splits;
   double scale;
+  int reduce_splits = L.splits;
   if (L.kind == kSketchSparseReg || L.kind == kSketchSparseTC) {
     const int64_t rps = std::max<int64_t>(SPR_KC, ((per + SPR_KC - 1) / SPR_KC) * SPR_KC);
     const int beta = k / zeta;
-    // tensor-core path: the (unused for sparse) compensation buffer's first word is the overflow
-    // flag; the register kernel below then runs only if the flag is raised.  int32 accumulators
-    // are exact while rows_per_split * 255 < 2^31.
+    // tensor-core path first; the register kernel below then runs only if it raised the overflow
+    // flag.  int32 accumulators are exact while rows_per_split * 255 < 2^31.
     const int* guard = nullptr;
     if (L.kind == kSketchSparseTC && rps <= kSparseTcMaxRows && sparse_tc_aligned(X, dtype, n, ldx)) {
-      int* flag = reinterpret_cast<int*>(partc);
       e = cudaMemsetAsync(flag, 0, sizeof(int), st);
       if (e != cudaSuccess) return e;
       e = launch_sparse_tc(X, dtype, m, n, ldx, row_offset, k, zeta, seed, L.splits, rps, part, flag, st);
@@ -677,10 +689,30 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
     e = dtype == RCHOLQR_F64 ? launch((double*)nullptr) : launch((float*)nullptr);
     scale = 1.0 / std::sqrt((double)zeta);
   } else {
-    const int64_t rps = std::max<int64_t>(KC, ((per + KC - 1) / KC) * KC);
-    e = dtype == RCHOLQR_F64 ? launch_gauss_typed<double>(L, X, m, n, ldx, row_offset, k, seed, rps, part, partc, st)
-                             : launch_gauss_typed<float>(L, X, m, n, ldx, row_offset, k, seed, rps, part, partc, st);
+    int splits = L.splits;
+    const int* guard = nullptr;
+    const bool tc = L.tc && gauss_tc_aligned(X, dtype, n, ldx);
+    if (tc) {
+      splits = L.tc_splits;
+      const int64_t tper = (m + splits - 1) / splits;
+      const int64_t trps = std::max<int64_t>(KC, ((tper + KC - 1) / KC) * KC);
+      e = cudaMemsetAsync(flag, 0, sizeof(int), st);
+      if (e != cudaSuccess) return e;
+      e = launch_gauss_tc(X, dtype, m, n, ldx, row_offset, k, seed, L.tc_tiles_k, L.tc_tiles_n, splits, trps, part,
+                          partc, flag, st);
+      if (e == cudaSuccess) guard = flag;                     // else: the DMMA kernel computes the sketch
+      else if (e != cudaErrorNotSupported) return e;
+    }
+    // DMMA kernel: the path itself, or the overflow fallback of the tensor-core kernel (same splits)
+    SketchLaunch Lg = L;
+    Lg.splits = splits;
+    const int64_t gper = (m + splits - 1) / splits;
+    const int64_t rps = std::max<int64_t>(KC, ((gper + KC - 1) / KC) * KC);
+    e = dtype == RCHOLQR_F64
+            ? launch_gauss_typed<double>(Lg, X, m, n, ldx, row_offset, k, seed, rps, part, partc, st, guard)
+            : launch_gauss_typed<float>(Lg, X, m, n, ldx, row_offset, k, seed, rps, part, partc, st, guard);
     scale = 1.0 / std::sqrt((double)k);
+    reduce_splits = splits;
   }
   if (e != cudaSuccess) return e;
   if (ev_mid) cudaEventRecord(ev_mid, st);
@@ -688,7 +720,7 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
   const int threads = 256;
   const int blocks = (int)std::min<int64_t>((kn + threads - 1) / threads, 4096);
   const bool sparse = L.kind == kSketchSparse || L.kind == kSketchSparseReg || L.kind == kSketchSparseTC;
-  sketch_reduce_kernel<<<blocks, threads, 0, st>>>(part, sparse ? nullptr : partc, L.splits, kn,
+  sketch_reduce_kernel<<<blocks, threads, 0, st>>>(part, sparse ? nullptr : partc, reduce_splits, kn,
                                                    scale, P, status);
   return cudaGetLastError();
 }

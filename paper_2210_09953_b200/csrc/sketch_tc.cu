@@ -25,60 +25,11 @@
 #include <cstdlib>
 #include <type_traits>
 #include "internal.cuh"
+#include "tcgen05.cuh"
 #include "theta.cuh"
 
 namespace rcq {
 
-namespace tc {
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
-// UMMA shared-memory descriptor: canonical K-major, SWIZZLE_NONE, descriptor version 1 (sm_100).
-__device__ __forceinline__ uint64_t desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
-         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46);
-}
-// kind::i8 instruction descriptor: D s32, A/B signedness, K-major A and B, N, M.
-__host__ __device__ constexpr uint32_t idesc_i8(int M, int N, bool a_signed, bool b_signed) {
-  return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | ((b_signed ? 1u : 0u) << 10) | ((uint32_t)(N >> 3) << 17) |
-         ((uint32_t)(M >> 4) << 24);
-}
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t accum) {
-  asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
-               ::"r"(tmem_d), "l"(da), "l"(db), "r"(idesc), "r"(accum));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("{\n.reg .b64 st;\nmbarrier.arrive.expect_tx.shared::cta.b64 st, [%0], %1;\n}\n"
-               ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
-                 : "=r"(done) : "r"(smem_u32(b)), "r"(parity) : "memory");
-  }
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n"
-               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void commit(uint64_t* b) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void ld16(uint32_t taddr, uint32_t (&v)[16]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
-               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-                 "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-               : "r"(taddr));
-}
-__device__ __forceinline__ void named_bar(int id, int count) {
-  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(count) : "memory");
-}
-}  // namespace tc
 
 constexpr int STC_M = 128;        // Theta rows per CTA (MMA M = TMEM lanes)
 constexpr int STC_N = 64;         // X columns per CTA (MMA N)
@@ -138,19 +89,6 @@ struct StcCfg {
   static __device__ __forceinline__ int tcol(int t) { return t < PG ? Fm::ONES + t * STC_N : TBASE1 + (t - PG) * STC_N; }
 };
 
-// byte offset of int8 element (row r, k) in a K-major SWIZZLE_NONE core-matrix tile of R rows:
-// 8x16-byte core matrices, LBO (next 16 k) = (R/8)*128 bytes, SBO (next 8 rows) = 128 bytes.
-// (8 (r >> 3) + (r & 7) = r, so the row term is simply 16 r.)
-__device__ __forceinline__ int cm_off(int r, int k, int R) { return (k >> 4) * R * 16 + r * 16 + (k & 15); }
-
-// 4x4 byte transpose: W[b] = byte b of (a, b, c, d) packed in that order.
-__device__ __forceinline__ void transpose4(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t (&W)[4]) {
-  const uint32_t x0 = __byte_perm(a, b, 0x5140), x1 = __byte_perm(a, b, 0x7362);
-  const uint32_t y0 = __byte_perm(c, d, 0x5140), y1 = __byte_perm(c, d, 0x7362);
-  W[0] = __byte_perm(x0, y0, 0x5410); W[1] = __byte_perm(x0, y0, 0x7632);
-  W[2] = __byte_perm(x1, y1, 0x5410); W[3] = __byte_perm(x1, y1, 0x7632);
-}
-
 // Per-(CTA, column) scale: e = (exponent bound of the first stage's max |x|) + 4 bits of headroom.
 struct ColParam {
   double s;          // fp32: 2^(175 - e) (applied to x 2^-128); fp64: 2^(31 - e)
@@ -183,8 +121,6 @@ __device__ __forceinline__ ColParam col_param(uint32_t maxbits) {
   }
   return p;
 }
-
-constexpr double kMagic = 6755399441055744.0;               // 1.5 * 2^52: ulp 1
 
 // fp32: (hi, lo) words of t = RN(x 2^(47-e) + 1.5 2^52 + 2^47)
 __device__ __forceinline__ void split_words(float x, const ColParam& p, uint32_t& hi, uint32_t& lo) {

@@ -21,9 +21,9 @@ __host__ __device__ constexpr uint32_t make_idesc_i8(int M, int N, bool a_signed
 }
 
 template <int N>
-__global__ void probe(const int8_t* A, const int8_t* B, int32_t* D, int a_signed, int b_signed) {
+__global__ void probe(const int8_t* A, const int8_t* B, int32_t* D, int a_signed, int b_signed, int dcol, int sbo_a) {
   constexpr int M = 128, K = 64;
-  __shared__ __align__(1024) int8_t As[M * K];
+  __shared__ __align__(1024) int8_t As[M * K * 2];
   __shared__ __align__(1024) int8_t Bs[N * K];
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) uint64_t mbar;
@@ -31,7 +31,7 @@ __global__ void probe(const int8_t* A, const int8_t* B, int32_t* D, int a_signed
   // canonical K-major: byte (r, k) at ((k/16) * (R/8) + r/8) * 128 + (r%8) * 16 + k%16
   for (int c = tid; c < M * K; c += blockDim.x) {
     const int r = c / K, k = c % K;
-    As[((k / 16) * (M / 8) + r / 8) * 128 + (r % 8) * 16 + (k % 16)] = A[c];
+    As[(k / 16) * (M / 8) * sbo_a + (r / 8) * sbo_a + (r % 8) * 16 + (k % 16)] = A[c];
   }
   for (int c = tid; c < N * K; c += blockDim.x) {
     const int r = c / K, k = c % K;
@@ -43,7 +43,7 @@ __global__ void probe(const int8_t* A, const int8_t* B, int32_t* D, int a_signed
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)), "r"(N < 32 ? 32 : N));
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)), "r"(512));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -53,12 +53,12 @@ __global__ void probe(const int8_t* A, const int8_t* B, int32_t* D, int a_signed
   if (tid == 0) {
     const uint32_t idesc = make_idesc_i8(M, N, a_signed, b_signed);
     for (int ks = 0; ks < K / 32; ++ks) {
-      const uint64_t da = make_desc(smem_u32(As) + ks * 2 * (M / 8) * 128, (M / 8) * 128, 128);
+      const uint64_t da = make_desc(smem_u32(As) + ks * 2 * (M / 8) * sbo_a, (M / 8) * sbo_a, sbo_a);
       const uint64_t db = make_desc(smem_u32(Bs) + ks * 2 * (N / 8) * 128, (N / 8) * 128, 128);
       const uint32_t acc = ks > 0;
       asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
-                   ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(acc));
+                   ::"r"(tmem + dcol), "l"(da), "l"(db), "r"(idesc), "r"(acc));
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(&mbar)));
   }
@@ -74,7 +74,7 @@ __global__ void probe(const int8_t* A, const int8_t* B, int32_t* D, int a_signed
   // warp w reads TMEM lanes 32w..32w+31 (rows), N columns
   for (int c0 = 0; c0 < N; c0 += 16) {
     uint32_t v[16];
-    const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + c0;
+    const uint32_t taddr = tmem + ((uint32_t)(32 * warp) << 16) + c0 + dcol;
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
                    "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
@@ -84,20 +84,21 @@ __global__ void probe(const int8_t* A, const int8_t* B, int32_t* D, int a_signed
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
-  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(N < 32 ? 32 : N));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(512));
 }
 
-int main() {
-  constexpr int M = 128, N = 64, K = 64;
+template <int N>
+int check(int dcol, int sbo_a) {
+  constexpr int M = 128, K = 64;
   int8_t *A, *B; int32_t* D;
   cudaMallocManaged(&A, M * K); cudaMallocManaged(&B, N * K); cudaMallocManaged(&D, M * N * 4);
-  srand(1);
+  srand(1 + dcol);
   int bad = 0;
   for (int mode = 0; mode < 4; ++mode) {
     const int as = mode & 1, bs = (mode >> 1) & 1;
     for (int i = 0; i < M * K; ++i) A[i] = (int8_t)(as ? (rand() % 256 - 128) : (rand() % 256));
     for (int i = 0; i < N * K; ++i) B[i] = (int8_t)(bs ? (rand() % 256 - 128) : (rand() % 256));
-    probe<N><<<1, 128>>>(A, B, D, as, bs);
+    probe<N><<<1, 128>>>(A, B, D, as, bs, dcol, sbo_a);
     cudaError_t e = cudaDeviceSynchronize();
     if (e != cudaSuccess) { printf("CUDA error %s\n", cudaGetErrorString(e)); return 1; }
     int nb = 0;
@@ -109,11 +110,22 @@ int main() {
           const long b = bs ? (long)(int8_t)B[c * K + k] : (long)(uint8_t)B[c * K + k];
           s += a * b;
         }
-        if (s != D[r * N + c]) { if (nb < 3) printf("mode %d mismatch r %d c %d: %ld vs %d\n", mode, r, c, s, D[r * N + c]); ++nb; }
+        if (s != D[r * N + c]) ++nb;
       }
-    printf("{\"mode_a_signed\":%d,\"b_signed\":%d,\"mismatches\":%d}\n", as, bs, nb);
     bad += nb;
   }
+  printf("{\"N\":%d,\"dcol\":%d,\"sbo_a\":%d,\"mismatches\":%d}\n", N, dcol, sbo_a, bad);
+  cudaFree(A); cudaFree(B); cudaFree(D);
+  return bad;
+}
+
+int main() {
+  int bad = 0;
+  bad += check<64>(0, 128);
+  bad += check<240>(40, 128);
+  bad += check<240>(200, 144);
+  bad += check<256>(96, 144);
+  bad += check<192>(8, 144);
   printf(bad ? "FAIL\n" : "PASS\n");
   return bad ? 1 : 0;
 }

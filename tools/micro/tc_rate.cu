@@ -16,10 +16,10 @@ __host__ __device__ constexpr uint32_t idesc(int kind, int M, int N) {
 }
 
 template <int KIND, int N>
-__global__ void rate(int iters, int G, long long* out) {
+__global__ void rate(int iters, int G, long long* out, int sbo_b) {
   constexpr int M = 128;
   __shared__ __align__(1024) uint8_t As[M * 32 * 2];
-  __shared__ __align__(1024) uint8_t Bs[256 * 32 * 2];
+  __shared__ __align__(1024) uint8_t Bs[256 * 32 * 2 + 4096];
   __shared__ uint32_t tmem_base;
   __shared__ __align__(8) uint64_t mbar;
   const int tid = threadIdx.x, warp = tid >> 5;
@@ -41,7 +41,7 @@ __global__ void rate(int iters, int G, long long* out) {
   if (tid == 0) {
     const uint32_t id = idesc(KIND, M, N);
     const uint64_t da = make_desc(smem_u32(As), (M / 8) * 128, 128);
-    const uint64_t db = make_desc(smem_u32(Bs), (N / 8) * 128, 128);
+    const uint64_t db = make_desc(smem_u32(Bs), (N / 8) * sbo_b, sbo_b);
     uint32_t phase = 0;
     const long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
@@ -69,13 +69,13 @@ __global__ void rate(int iters, int G, long long* out) {
 }
 
 template <int KIND, int N>
-void run(int G) {
+void run(int G, int sbo_b = 128) {
   long long* out;
   cudaMallocManaged(&out, 148 * sizeof(long long));
   const int iters = 2000;
-  rate<KIND, N><<<148, 128>>>(iters, G, out);
+  rate<KIND, N><<<148, 128>>>(iters, G, out, sbo_b);
   cudaDeviceSynchronize();
-  rate<KIND, N><<<148, 128>>>(iters, G, out);
+  rate<KIND, N><<<148, 128>>>(iters, G, out, sbo_b);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return; }
   double s = 0;
@@ -83,15 +83,13 @@ void run(int G) {
   s /= 148;
   const double per = s / ((double)iters * G);
   const double macs = 128.0 * N * (KIND == 0 ? 32 : 16);
-  printf("{\"kind\":\"%s\",\"N\":%d,\"G\":%d,\"cyc_per_mma\":%.1f,\"mac_per_cyc\":%.0f}\n", KIND == 0 ? "i8" : "f16", N, G,
+  printf("{\"sbo_b\":%d,\"kind\":\"%s\",\"N\":%d,\"G\":%d,\"cyc_per_mma\":%.1f,\"mac_per_cyc\":%.0f}\n", sbo_b, KIND == 0 ? "i8" : "f16", N, G,
          per, macs / per);
   cudaFree(out);
 }
 
 int main() {
-  for (int G : {1, 4, 12, 48}) {
-    run<0, 64>(G); run<0, 128>(G); run<0, 256>(G);
-    run<1, 64>(G); run<1, 256>(G);
-  }
+  for (int sbo : {128, 144, 160, 256}) { run<0, 240>(48, sbo); run<0, 192>(48, sbo); }
+  run<0, 64>(48); run<0, 256>(48);
   return 0;
 }
