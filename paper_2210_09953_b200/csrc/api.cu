@@ -55,6 +55,8 @@ struct rcholqr_plan_s {
   int res_tm = 0;           // > 0: blocked-substitution resident solve with this row tile
   int warp_solve = 0;       // > 0: warp-independent blocked substitution with this many warps/CTA
   int stream_tb = 0;        // > 0: streamed blocked substitution (fp64, n > 128) with this block width
+  bool solve_tc = false;    // fp32 X, n <= 64: tcgen05 digit solve Q = X R^{-1} (solve_tc.cu)
+  void* qws = nullptr;      // its W-digit workspace
   double* tbuf = nullptr;   // [m_local][stream_tb] T_J workspace of the streamed solve
   size_t tbuf_elems = 0;
   int qr_kind = 0;
@@ -170,6 +172,14 @@ rcholqr_status do_sketch(rcholqr_plan p, const void* X, int64_t m, int64_t ro, i
 rcholqr_status solve(rcholqr_plan p, const void* X, int64_t m, int64_t ldx, const double* R, void* Q, int64_t ldq,
                      cudaStream_t st, bool timed) {
   const int n = p->d.n;
+  if (p->solve_tc && m > 0 && solve_tc_supported(X, m, ldx, Q, ldq)) {
+    CU(launch_tri_inverse(R, n, p->W, p->status_d, st));
+    if (timed && p->timing) cudaEventRecord(p->ev[5], st);
+    const cudaError_t e = launch_solve_tc(p->W, n, (const float*)X, m, ldx, (float*)Q, ldq, p->qws, p->status_d,
+                                          p->sms, st);
+    if (e == cudaSuccess) return RCHOLQR_OK;
+    if (e != cudaErrorNotSupported) return cuda_status(e);
+  }
   if (p->stream_tb > 0) {
     // blocked substitution by column blocks of width tb, each = 2 fp64 DMMA GEMM launches
     const int tb = p->stream_tb, npad = (n + 7) / 8 * 8;
@@ -273,11 +283,13 @@ rcholqr_status rcholqr_create(const rcholqr_desc* desc, rcholqr_plan* out) {
     if (v != 2) p->warp_solve = 0;
     if (v == 0) { p->res_tm = 0; p->stream_tb = 0; }
   }
+  p->solve_tc = solve_tc_applicable(desc->dtype, n);
   p->qr_kind = plan_qr(k, n, p->smem_optin);
   const size_t kn = (size_t)k * n, nn = (size_t)((n + 7) / 8 * 8) * ((n + 7) / 8 * 8);
   bool okalloc = cudaMalloc(&p->part, sizeof(double) * kn * p->sk.max_splits()) == cudaSuccess &&
                  cudaMalloc(&p->partc, sizeof(double) * kn * p->sk.max_splits()) == cudaSuccess &&
                  cudaMalloc(&p->flag_d, sizeof(int)) == cudaSuccess &&
+                 cudaMalloc(&p->qws, solve_tc_workspace()) == cudaSuccess &&
                  cudaMalloc(&p->P, sizeof(double) * kn) == cudaSuccess &&
                  cudaMalloc(&p->W, sizeof(double) * nn) == cudaSuccess &&
                  cudaMalloc(&p->Awork, sizeof(double) * kn) == cudaSuccess &&
@@ -304,7 +316,7 @@ rcholqr_status rcholqr_destroy(rcholqr_plan p) {
   if (!p) return RCHOLQR_OK;
   DeviceGuard dg(p->d.device);
   cudaFree(p->part); cudaFree(p->partc); cudaFree(p->P); cudaFree(p->W); cudaFree(p->Awork); cudaFree(p->diag); cudaFree(p->tau);
-  cudaFree(p->Rtmp); cudaFree(p->status_d); cudaFree(p->flag_d);
+  cudaFree(p->Rtmp); cudaFree(p->status_d); cudaFree(p->flag_d); cudaFree(p->qws);
   if (p->status_h) cudaFreeHost(p->status_h);
   cudaFree(p->xbuf); cudaFree(p->qbuf); cudaFree(p->rbuf); cudaFree(p->sbuf); cudaFree(p->tbuf);
   for (int t = 0; t < 7; ++t)

@@ -80,6 +80,12 @@ cudaError_t launch_tri_prep_blocked(const double* R, int n, double* M, int* stat
 cudaError_t launch_gemm_f64(const double* A, int64_t lda, const double* B, int64_t ldb, const double* C0,
                             int64_t ldc0, double* C, int64_t ldc, int64_t m, int N, int K, bool tri_b,
                             const int* status, cudaStream_t st);
+// tcgen05 int8 digit solve for fp32 X, n <= 64 (solve_tc.cu): Q = X fl64(R^{-1})
+bool solve_tc_applicable(int dtype, int n);
+bool solve_tc_supported(const void* X, int64_t m, int64_t ldx, const void* Q, int64_t ldq);
+size_t solve_tc_workspace();
+cudaError_t launch_solve_tc(const double* Winv, int n, const float* X, int64_t m, int64_t ldx, float* Q, int64_t ldq,
+                            void* ws, const int* status, int sms, cudaStream_t st);
 cudaError_t launch_trsm_resident(int tm, const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M,
                                  void* Q, int64_t ldq, const int* status, int sms, cudaStream_t st);
 

@@ -1,0 +1,390 @@
+// solve_tc.cu -- tall solve Q = X R^{-1} (Alg. 2 step 3) for fp32 X with n <= 64 on the
+// 5th-generation tensor core (tcgen05 kind::i8), the B200 form of the paper's dominant step
+// ("mainly determined by the computation of X R^{-1} ... m n^2 flops").
+//
+// For fp32 X the solve is computed as Q = X W with W = fl64(R^{-1}) (tri_inverse_kernel, fp64) and
+// the product evaluated EXACTLY in integer digits (reading A16: the forward error of
+// X W vs row-wise substitution is <= kappa u_64 << u_32, far below the single rounding of Q to
+// fp32 that both carry):
+//   * X row i:    F_x = round(x 2^(46 - e_i)), e_i = exponent bound of the row's max |x|,
+//                 6 signed base-256 digits (d_0 most significant);
+//   * W column j: F_w = round(w 2^(54 - e_j)), 7 signed digits (prepared once per solve);
+//   * Q_ij = 2^(e_i - 46 + e_j - 54) sum_L acc_L 256^(11 - L), acc_L = sum_{a + b = L} xd_a . wd_b,
+//     levels L <= 6 kept.
+// Accuracy: the solve amplifies a relative perturbation of x_i or of W by up to kappa(R) sqrt(n),
+// so both are carried to ~2^-46 of their row / column scale and the dropped levels are < 2^-56
+// of |x_i| |w_j| n: all far below the 2^-24 of the final rounding of Q to fp32 for kappa <= 1e6.
+// Each int8 MMA has M = 128 X rows and N = (7 - a) * 32 stacked W digit planes of one 32-column
+// group, writing levels a..6 at once into int32 TMEM (accumulate flag off for the first MMA of a
+// tile initialises every level).  TMEM holds two 224-column level buffers, so the drain warps
+// (fp64 combine, fp32 Q stores) of one group overlap the MMAs of the next.
+//
+// Roles (persistent CTAs, 18 warps): warp 0 lane 0 issues tcgen05.mma; warp 1 lane 0 stages the W
+// digits (cp.async.bulk) and the X tiles (one 2D TMA box of 128 rows x K+4 columns per tile);
+// warps 2..9 drain TMEM in two sets of four (set d drains level buffer d, one lane quadrant per
+// warp) and write Q through swizzled shared memory with TMA stores; warps 10..17 split X into
+// digit planes.
+#include <cuda_runtime.h>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <algorithm>
+#include "internal.cuh"
+#include "tcgen05.cuh"
+
+namespace rcq {
+
+constexpr int QT_M = 128;       // X rows per tile (MMA M = TMEM lanes)
+constexpr int QT_G = 32;        // output columns per TMEM level group
+constexpr int QT_DA = 6;        // X digits
+constexpr int QT_DB = 7;        // W digits
+constexpr int QT_LEV = 7;       // levels kept (a + b <= 6)
+constexpr int QT_NB = QT_DB * QT_G;             // stacked W digit rows of one group (224)
+constexpr int QT_KMAX = 64;
+constexpr int QT_DIG = 2, QT_RAW = 2;
+constexpr int QT_DWARPS = 8;    // digit warps 10..17
+constexpr int QT_RWARPS = 8;    // drain warps 2..9: two sets of four (one per TMEM level buffer)
+constexpr int QT_THREADS = 32 * (2 + QT_RWARPS + QT_DWARPS);
+constexpr int QT_A_TILE = QT_M * QT_KMAX;       // one X digit plane (128 x 64 B)
+constexpr int QT_RS_MAX = QT_KMAX + 4;          // raw X row pitch (floats): K + 4 -> conflict-free LDS.128
+constexpr int QT_RAW_STAGE = QT_M * QT_RS_MAX * 4;
+constexpr int QT_W_BYTES = 2 * QT_NB * QT_KMAX;  // two groups (n <= 64)
+constexpr int QT_QS_BYTES = QT_RWARPS * 32 * QT_G * 4;  // Q staging: one 32-row x 32-col fp32 tile per drain warp (128B-swizzled)
+constexpr size_t QT_SMEM = (size_t)QT_W_BYTES + (size_t)QT_DIG * QT_DA * QT_A_TILE + (size_t)QT_RAW * QT_RAW_STAGE + QT_QS_BYTES + 2048;
+static_assert(QT_SMEM <= 232448, "shared memory");
+static_assert(2 * QT_LEV * QT_G <= 512, "two TMEM level buffers");
+
+// ---------------------------------------------------------------------------------------------
+// W digit prep: column scales e_j and the signed digit planes, laid out per group g as the B
+// operand tile [6 * 32 rows (row = b * 32 + jj) x K bytes], K-major SWIZZLE_NONE core matrices.
+__global__ void solve_tc_prep_kernel(const double* __restrict__ W, int n, int kpad, int8_t* __restrict__ wdig,
+                                     int* __restrict__ wexp, const int* status) {
+  if (*status) return;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int groups = (n + QT_G - 1) / QT_G;
+  if (j >= groups * QT_G) return;
+  const int g = j / QT_G, jj = j % QT_G;
+  int8_t* tile = wdig + (size_t)g * QT_NB * kpad;
+  double mx = 0.0;
+  if (j < n)
+    for (int l = 0; l < n; ++l) mx = fmax(mx, fabs(W[(size_t)l * n + j]));
+  int e = 0;
+  if (mx > 0.0) { frexp(mx, &e); }                     // mx < 2^e
+  wexp[j] = e;
+  for (int l = 0; l < kpad; ++l) {
+    long long F = (j < n && l < n) ? llrint(ldexp(W[(size_t)l * n + j], 54 - e)) : 0;   // |F| <= 2^54
+    int d[QT_DB];
+    for (int b = QT_DB - 1; b >= 1; --b) {             // balanced base-256 digits, exact
+      const long long r = ((F + 128) & 255) - 128;
+      d[b] = (int)r;
+      F = (F - r) >> 8;
+    }
+    d[0] = (int)F;                                     // |d0| <= 65
+    for (int b = 0; b < QT_DB; ++b) tile[(l >> 4) * QT_NB * 16 + (b * QT_G + jj) * 16 + (l & 15)] = (int8_t)d[b];
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(QT_THREADS, 1)
+solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap qmap,
+                const int8_t* __restrict__ wdig, const int* __restrict__ wexp,
+                int64_t m, int n, int kpad, float* __restrict__ Q, int64_t ldq, const int* status, int dbg) {
+  if (*status) return;                                 // singular R: Q is not written
+  extern __shared__ __align__(1024) unsigned char sm[];
+  unsigned char* wsm = sm;                                                   // W digits, all groups
+  unsigned char* abase = sm + QT_W_BYTES;                                     // [DIG][DA][A_TILE]
+  float* raw_base = reinterpret_cast<float*>(abase + (size_t)QT_DIG * QT_DA * QT_A_TILE);   // [RAW][128][kpad]
+  unsigned char* qstage = reinterpret_cast<unsigned char*>(raw_base) + (size_t)QT_RAW * QT_RAW_STAGE;   // [4][32 rows][128 B]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(qstage + QT_QS_BYTES);
+  uint64_t* dfull = bars;                   // [DIG] X digits of a tile ready
+  uint64_t* dempty = dfull + QT_DIG;        // [DIG] tile fully drained (slot + row scales free)
+  uint64_t* rfull = dempty + QT_DIG;        // [RAW]
+  uint64_t* rempty = rfull + QT_RAW;        // [RAW]
+  uint64_t* tready = rempty + QT_RAW;       // [2] level buffer written (commit)
+  uint64_t* tfree = tready + 2;             // [2] level buffer drained
+  uint64_t* wbar = tfree + 2;               // W digits staged
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wbar + 1);
+  int* rexp = reinterpret_cast<int*>(tmem_slot + 4);                          // [DIG][128]
+  double* wsc = reinterpret_cast<double*>(rexp + QT_DIG * QT_M);             // [64] 2^(e_j - 60): column scale x 2^-(46+54-40)
+
+  const int groups = (n + QT_G - 1) / QT_G;
+  const int64_t ntiles = (m + QT_M - 1) / QT_M;
+  const int my_tiles = blockIdx.x < ntiles ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int lg_n = kpad / 16;                                                 // 16-column groups per row
+  const int ksteps = kpad / 32;
+
+  if (tid == 0) {
+    for (int s = 0; s < QT_DIG; ++s) { tc::mbar_init(&dfull[s], QT_DWARPS); tc::mbar_init(&dempty[s], QT_RWARPS); }
+    for (int s = 0; s < QT_RAW; ++s) { tc::mbar_init(&rfull[s], 1); tc::mbar_init(&rempty[s], QT_DWARPS); }
+    for (int b = 0; b < 2; ++b) { tc::mbar_init(&tready[b], 1); tc::mbar_init(&tfree[b], 4); }
+    tc::mbar_init(wbar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (tid < groups * QT_G) wsc[tid] = ldexp(1.0, wexp[tid] - 60);
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(tc::smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- MMA issuer (lane 0)
+    tc::mbar_wait(wbar, 0u);
+    for (int tt = 0; tt < my_tiles; ++tt) {
+      const int s = tt % QT_DIG;
+      tc::mbar_wait(&dfull[s], (uint32_t)((tt / QT_DIG) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      for (int g = 0; g < groups; ++g) {
+        const int use = tt * groups + g, buf = use & 1, u = use >> 1;
+        if (u > 0) tc::mbar_wait(&tfree[buf], (uint32_t)((u - 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        if (lane == 0 && !(dbg & 1)) {
+          const uint32_t sa = tc::smem_u32(abase + (size_t)s * QT_DA * QT_A_TILE);
+          const uint32_t sb = tc::smem_u32(wsm + (size_t)g * QT_NB * kpad);
+          for (int ks = 0; ks < ksteps; ++ks) {
+#pragma unroll
+            for (int a = 0; a < QT_DA; ++a) {
+              const uint64_t da = tc::desc(sa + a * QT_A_TILE + ks * 2 * (QT_M * 16), QT_M * 16, 128);
+              const uint64_t db = tc::desc(sb + ks * 2 * (QT_NB * 16), QT_NB * 16, 128);
+              const uint32_t idesc = tc::idesc_i8(QT_M, (QT_DB - a) * QT_G, true, true);
+              tc::mma_i8(tmem + buf * (QT_LEV * QT_G) + a * QT_G, da, db, idesc, (ks > 0 || a > 0) ? 1u : 0u);
+            }
+          }
+        }
+        if (lane == 0) tc::commit(&tready[buf]);
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- loader (lane 0)
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&xmap) : "memory");
+      const uint32_t wbytes = (uint32_t)(groups * QT_NB * kpad);
+      tc::mbar_arrive_tx(wbar, wbytes);
+      tc::bulk_g2s(wsm, wdig, wbytes, wbar);
+    }
+    __syncwarp();
+    for (int tt = 0; tt < my_tiles; ++tt) {
+      const int s = tt % QT_RAW;
+      if (tt >= QT_RAW) tc::mbar_wait(&rempty[s], (uint32_t)(((tt / QT_RAW) - 1) & 1));
+      if (lane == 0) {
+        const int64_t row0 = (blockIdx.x + (int64_t)tt * gridDim.x) * QT_M;
+        if (dbg & 8) tc::mbar_arrive(&rfull[s]);
+        else {
+          tc::mbar_arrive_tx(&rfull[s], (uint32_t)(QT_M * (kpad + 4) * 4));
+          tc::tma_load_2d(raw_base + (size_t)s * QT_M * QT_RS_MAX, &xmap, 0, (int)row0, &rfull[s]);
+        }
+      }
+      __syncwarp();
+    }
+  } else if (warp < 2 + QT_RWARPS) {
+    // ---------------------------------------------------------------- drain (set = buffer, lane quadrant)
+    const int dset = (warp - 2) >> 2, dq = warp & 3, row_l = dq * 32 + lane;
+    const uint32_t lb = tmem + ((uint32_t)(dq * 32) << 16);
+    for (int tt = 0; tt < my_tiles; ++tt) {
+      const int s = tt % QT_DIG;
+      for (int g = 0; g < groups; ++g) {
+        const int use = tt * groups + g, buf = use & 1, u = use >> 1;
+        if (buf != dset) continue;
+        tc::mbar_wait(&tready[buf], (uint32_t)(u & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        // Levels are exact int32 with |acc_L| < 2^23 (<= 6 pairs x 64 terms x 2^14), so adjacent
+        // levels pair exactly in int32 (acc_L 256 + acc_{L+1} < 2^31): four values per output,
+        // each converted to fp64 by the 2^52 magic constant (LOP3 + DADD, no I2F), then combined
+        // by three DFMAs -- the fewest issue slots per output of the variants tried.
+        static_assert(QT_LEV == 7, "pairing below assumes 7 levels");
+        double v[QT_G];
+        const uint32_t lv = lb + buf * (QT_LEV * QT_G);
+        if (dbg & 4) {
+#pragma unroll
+          for (int c = 0; c < QT_G; ++c) v[c] = 0.0;
+        } else
+#pragma unroll
+        for (int h = 0; h < QT_G / 8; ++h) {
+          uint32_t p[4][8];
+#pragma unroll
+          for (int pp = 0; pp < 3; ++pp) {
+            uint32_t hi8[8], lo8[8];
+            tc::ld8(lv + (2 * pp) * QT_G + h * 8, hi8);
+            tc::ld8(lv + (2 * pp + 1) * QT_G + h * 8, lo8);
+            tc::wait_ld();
+#pragma unroll
+            for (int c = 0; c < 8; ++c) p[pp][c] = hi8[c] * 256u + lo8[c];
+          }
+          tc::ld8(lv + 6 * QT_G + h * 8, p[3]);
+          tc::wait_ld();
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            double f[4];
+#pragma unroll
+            for (int pp = 0; pp < 4; ++pp)
+              f[pp] = __hiloint2double(0x43300000, (int)(p[pp][c] ^ 0x80000000u)) - 4503601774854144.0;   // 2^52 + 2^31
+            v[h * 8 + c] = fma(f[0], 0x1p40, fma(f[1], 0x1p24, fma(f[2], 256.0, f[3])));
+          }
+        }
+        asm volatile("tcgen05.fence::before_thread_sync;\n");
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tfree[buf]);       // TMEM buffer free; the stores below need no TMEM
+        {
+          // stage this warp's 32 rows x 32 columns (fp32) in shared memory with the 128-byte swizzle
+          // (16-byte chunk c of row r at chunk c ^ (r & 7): conflict-free STS.128), then one 2D TMA
+          // store writes them; TMA clips rows >= m and columns >= n.
+          const double si = __hiloint2double((rexp[s * QT_M + row_l] + 1023) << 20, 0);   // 2^e_i
+          unsigned char* qs = qstage + (warp - 2) * (32 * QT_G * 4);
+          if (lane == 0) tc::bulk_wait_read0();              // previous store finished reading the tile
+          __syncwarp();
+#pragma unroll
+          for (int c = 0; c < QT_G; c += 4) {
+            float o4[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {   // exact power-of-two scale 2^(e_i - 46 + e_j - 54 + 40)
+              o4[q] = __double2float_rn(v[c + q] * si * wsc[g * QT_G + c + q]);   // v carries 256^(6-L)
+            }
+            *reinterpret_cast<float4*>(qs + lane * 128 + (((c >> 2) ^ (lane & 7)) << 4)) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+          }
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          __syncwarp();
+          if (lane == 0) {
+            tc::tma_store_2d(&qmap, qs, g * QT_G, (int)((blockIdx.x + (int64_t)tt * gridDim.x) * QT_M + dq * 32));
+            tc::bulk_commit();
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&dempty[s]);          // slot (X digits + row scales) free
+    }
+  } else {
+    // ---------------------------------------------------------------- X digit planes
+    const int dt = tid - 32 * (2 + QT_RWARPS);
+    for (int tt = 0; tt < my_tiles; ++tt) {
+      const int s = tt % QT_DIG, sr = tt % QT_RAW;
+      if (tt >= QT_DIG) tc::mbar_wait(&dempty[s], (uint32_t)(((tt / QT_DIG) - 1) & 1));
+      tc::mbar_wait(&rfull[sr], (uint32_t)((tt / QT_RAW) & 1));
+      const float* raw = raw_base + (size_t)sr * QT_M * QT_RS_MAX;
+      unsigned char* at = abase + (size_t)s * QT_DA * QT_A_TILE;
+      const int rs = kpad + 4, rpw = 32 / lg_n;            // raw row pitch; rows per warp pass
+      for (int task = dt; task < ((dbg & 2) ? 0 : QT_M * lg_n); task += 32 * QT_DWARPS) {
+        // lane -> (column group lg, row): consecutive lanes take consecutive rows of one column
+        // group, so with the (K + 4)-float pitch every 8-lane phase of an LDS.128 hits 8 distinct
+        // 16-byte bank groups, and the digit STS.128 of a phase are contiguous.
+        const int w = task >> 5, l = task & 31;
+        const int lg = l / rpw, i = w * rpw + (l % rpw);
+        float x[16];
+#pragma unroll
+        for (int c = 0; c < 16; c += 4) {
+          const float4 f = *reinterpret_cast<const float4*>(raw + i * rs + lg * 16 + c);
+          x[c] = f.x; x[c + 1] = f.y; x[c + 2] = f.z; x[c + 3] = f.w;
+        }
+        uint32_t mx = 0u;
+#pragma unroll
+        for (int c = 0; c < 16; ++c) mx = max(mx, __float_as_uint(x[c]) & 0x7FFFFFFFu);
+        for (int o = rpw; o < 32; o <<= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        // e_i: smallest e with max |x| < 2^e (finite input assumed: the sketch rejected NaN/Inf)
+        const int e = mx == 0u ? 0 : (mx < 0x00800000u ? -126 : (int)(mx >> 23) - 126);
+        const double sx = ldexp(1.0, 128 + 46 - e);
+        if (lg == 0) rexp[s * QT_M + i] = e;
+        uint32_t W[QT_DA][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t hw[4], lw[4];
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint32_t ub = __float_as_uint(x[q * 4 + kk]);
+            const uint32_t h = ((uint32_t)((int32_t)ub >> 3) & 0x8FFFFFFFu) | 0x30000000u;   // x 2^-128
+            const double t = fma(__hiloint2double((int)h, (int)(ub << 29)), sx, kMagic + (double)0x8080808080ull);
+            hw[kk] = (uint32_t)__double2hiint(t);                                              // F + C, 48 bits
+            lw[kk] = (uint32_t)__double2loint(t);
+          }
+          uint32_t H[4], L[4];
+          transpose4(hw[0], hw[1], hw[2], hw[3], H);
+          transpose4(lw[0], lw[1], lw[2], lw[3], L);
+          W[0][q] = H[1]; W[1][q] = H[0] ^ 0x80808080u;
+          W[2][q] = L[3] ^ 0x80808080u; W[3][q] = L[2] ^ 0x80808080u;
+          W[4][q] = L[1] ^ 0x80808080u; W[5][q] = L[0] ^ 0x80808080u;
+        }
+#pragma unroll
+        for (int a = 0; a < QT_DA; ++a)
+          *reinterpret_cast<uint4*>(at + a * QT_A_TILE + lg * (QT_M * 16) + i * 16) =
+              make_uint4(W[a][0], W[a][1], W[a][2], W[a][3]);
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) { tc::mbar_arrive(&dfull[s]); tc::mbar_arrive(&rempty[sr]); }
+    }
+  }
+  if (warp >= 2 && warp < 2 + QT_RWARPS && lane == 0) tc::bulk_wait0();   // Q stores complete before exit
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
+bool solve_tc_applicable(int dtype, int n) { return dtype == RCHOLQR_F32 && n >= 1 && n <= QT_KMAX && !getenv("RCHOLQR_SOLVE_DMMA"); }
+
+bool solve_tc_supported(const void* X, int64_t m, int64_t ldx, const void* Q, int64_t ldq) {
+  return m <= INT32_MAX && ((uintptr_t)X % 16) == 0 && ((size_t)ldx * 4) % 16 == 0 &&   // TMA base / pitch
+         ((uintptr_t)Q % 16) == 0 && ((size_t)ldq * 4) % 16 == 0;
+}
+
+size_t solve_tc_workspace() { return (size_t)2 * QT_NB * QT_KMAX + sizeof(int) * 2 * QT_G; }
+
+using EncodeTiledFn2 = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// W = R^{-1} already in Winv (n x n fp64).  ws: workspace of solve_tc_workspace(n) bytes.
+cudaError_t launch_solve_tc(const double* Winv, int n, const float* X, int64_t m, int64_t ldx, float* Q, int64_t ldq,
+                            void* ws, const int* status, int sms, cudaStream_t st) {
+  if (m == 0) return cudaSuccess;
+  if (!solve_tc_supported(X, m, ldx, Q, ldq)) return cudaErrorNotSupported;
+  static EncodeTiledFn2 enc = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn2>(p);
+  }();
+  if (!enc) return cudaErrorNotSupported;
+  const int kpad = n <= 32 ? 32 : 64;
+  const int groups = (n + QT_G - 1) / QT_G;
+  int8_t* wdig = reinterpret_cast<int8_t*>(ws);
+  int* wexp = reinterpret_cast<int*>(wdig + (size_t)2 * QT_NB * QT_KMAX);
+  solve_tc_prep_kernel<<<1, groups * QT_G, 0, st>>>(Winv, n, kpad, wdig, wexp, status);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)m};
+  const cuuint64_t strides[1] = {(cuuint64_t)ldx * 4};
+  const cuuint32_t box[2] = {(cuuint32_t)kpad + 4, QT_M}, estr[2] = {1, 1};   // + 4 zero-filled pad columns
+  if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides, box, estr,
+          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  CUtensorMap qmapd;
+  const cuuint64_t qdims[2] = {(cuuint64_t)n, (cuuint64_t)m};
+  const cuuint64_t qstrides[1] = {(cuuint64_t)ldq * 4};
+  const cuuint32_t qbox[2] = {QT_G, 32};
+  if (enc(&qmapd, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Q, qdims, qstrides, qbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  e = cudaFuncSetAttribute(solve_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QT_SMEM);
+  if (e != cudaSuccess) return e;
+  const int64_t ntiles = (m + QT_M - 1) / QT_M;
+  const int grid = (int)std::min<int64_t>(ntiles, sms);
+  static const int dbg = getenv("RCHOLQR_QTC_DEBUG") ? atoi(getenv("RCHOLQR_QTC_DEBUG")) : 0;   // ablations only
+  if (getenv("RCHOLQR_DEBUG")) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, solve_tc_kernel);
+    fprintf(stderr, "solve_tc: regs %d maxthreads %d smem_dyn %zu static %zu threads %d\n", fa.numRegs,
+            fa.maxThreadsPerBlock, (size_t)QT_SMEM, fa.sharedSizeBytes, QT_THREADS);
+  }
+  solve_tc_kernel<<<grid, QT_THREADS, QT_SMEM, st>>>(map, qmapd, wdig, wexp, m, n, kpad, Q, ldq, status, dbg);
+  return cudaGetLastError();
+}
+
+}  // namespace rcq

@@ -207,6 +207,46 @@ def test_tri_solve_parity(cuda, m, n, dt, c):
         assert oracle.col_residual(X, Qg, Ro) <= 2.1 * u * n
 
 
+SOLVE_TC_CASES = [
+    # m, n, log10 cond, ldx (None = contiguous): fp32 X, n <= 64 -> tcgen05 digit solve (solve_tc.cu)
+    (100_003, 64, 4, None),      # C4 shape, ragged last 128-row tile
+    (1_000, 20, 3, None),        # one 32-column group, K padded to 32
+    (70_000, 48, 5, None),       # second group partial
+    (300, 33, 2, None),          # n just above one group
+    (1, 64, 1, None),            # single row
+    (40_000, 64, 4, 68),         # strided rows (TMA pitch)
+    (20_000, 61, 3, 63),         # unaligned pitch -> CUDA-core path
+]
+
+
+@pytest.mark.parametrize("m,n,c,ldx", SOLVE_TC_CASES)
+def test_tri_solve_tc_parity(cuda, m, n, c, ldx):
+    X = synth.make_X(max(m, n), n, c, "f32")
+    Ro, _, _ = oracle.householder(oracle.sketch(X, 2 * n))
+    X = X[:m]
+    Xt = _t(X)
+    if ldx is not None:
+        wide = torch.zeros((m, ldx), dtype=torch.float32, device="cuda")
+        wide[:, :n] = Xt
+        Xt = wide[:, :n]
+    plan = _plan(n, 2 * n, "f32")
+    Qg = _np(plan.tri_solve(Xt, _t(Ro)))
+    Qo = oracle.forward_subst(X, Ro)
+    assert _rel(Qg, Qo) <= 10 * U64 * 10**c + 2 * U32, _rel(Qg, Qo)
+    # row-wise: each row agrees to a couple of fp32 ulps of its own norm (exact digit products)
+    err = np.abs(Qg.astype(np.float64) - Qo.astype(np.float64)).max(axis=1)
+    assert np.all(err <= 4 * U32 * np.abs(Qo.astype(np.float64)).max(axis=1) + 1e-30)
+
+
+def test_tri_solve_tc_matches_dmma(cuda, monkeypatch):
+    X = synth.make_X(200_000, 64, 4.0, "f32")
+    Ro, _, _ = oracle.householder(oracle.sketch(X[:20_000], 128))
+    a = _np(_plan(64, 128, "f32").tri_solve(_t(X), _t(Ro)))
+    monkeypatch.setenv("RCHOLQR_SOLVE_DMMA", "1")
+    b = _np(_plan(64, 128, "f32").tri_solve(_t(X), _t(Ro)))
+    assert _rel(a, b) <= 4 * U32, _rel(a, b)
+
+
 def test_tri_solve_spec_example_and_identity(cuda):
     plan = _plan(2, 4, "f64")
     Q = _np(plan.tri_solve(_t(np.array([[2.0, 1.0]])), _t(np.array([[2.0, 1.0], [0.0, 1.0]]))))

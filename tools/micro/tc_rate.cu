@@ -16,7 +16,7 @@ __host__ __device__ constexpr uint32_t idesc(int kind, int M, int N) {
 }
 
 template <int KIND, int N>
-__global__ void rate(int iters, int G, long long* out, int sbo_b) {
+__global__ void rate(int iters, int G, long long* out, int sbo_b, int nreg, int shift) {
   constexpr int M = 128;
   __shared__ __align__(1024) uint8_t As[M * 32 * 2];
   __shared__ __align__(1024) uint8_t Bs[256 * 32 * 2 + 4096];
@@ -49,10 +49,10 @@ __global__ void rate(int iters, int G, long long* out, int sbo_b) {
         const uint32_t acc = 1;
         if (KIND == 0)
           asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n"
-                       ::"r"(tmem + (g % (512 / N > 4 ? 4 : 512 / N)) * N), "l"(da), "l"(db), "r"(id), "r"(acc));
+                       ::"r"(tmem + (g & (nreg - 1)) * shift), "l"(da), "l"(db), "r"(id), "r"(acc));
         else
           asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\ntcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n"
-                       ::"r"(tmem + (g % (512 / N > 4 ? 4 : 512 / N)) * N), "l"(da), "l"(db), "r"(id), "r"(acc));
+                       ::"r"(tmem + (g & (nreg - 1)) * shift), "l"(da), "l"(db), "r"(id), "r"(acc));
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(smem_u32(&mbar)));
       uint32_t done = 0;
@@ -69,13 +69,13 @@ __global__ void rate(int iters, int G, long long* out, int sbo_b) {
 }
 
 template <int KIND, int N>
-void run(int G, int sbo_b = 128) {
+void run(int G, int sbo_b = 128, int nreg = 4, int shift = N) {
   long long* out;
   cudaMallocManaged(&out, 148 * sizeof(long long));
   const int iters = 2000;
-  rate<KIND, N><<<148, 128>>>(iters, G, out, sbo_b);
+  rate<KIND, N><<<148, 128>>>(iters, G, out, sbo_b, nreg, shift);
   cudaDeviceSynchronize();
-  rate<KIND, N><<<148, 128>>>(iters, G, out, sbo_b);
+  rate<KIND, N><<<148, 128>>>(iters, G, out, sbo_b, nreg, shift);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return; }
   double s = 0;
@@ -83,13 +83,16 @@ void run(int G, int sbo_b = 128) {
   s /= 148;
   const double per = s / ((double)iters * G);
   const double macs = 128.0 * N * (KIND == 0 ? 32 : 16);
-  printf("{\"sbo_b\":%d,\"kind\":\"%s\",\"N\":%d,\"G\":%d,\"cyc_per_mma\":%.1f,\"mac_per_cyc\":%.0f}\n", sbo_b, KIND == 0 ? "i8" : "f16", N, G,
+  printf("{\"nreg\":%d,\"shift\":%d,\"sbo_b\":%d,\"kind\":\"%s\",\"N\":%d,\"G\":%d,\"cyc_per_mma\":%.1f,\"mac_per_cyc\":%.0f}\n", nreg, shift, sbo_b, KIND == 0 ? "i8" : "f16", N, G,
          per, macs / per);
   cudaFree(out);
 }
 
 int main() {
-  for (int sbo : {128, 144, 160, 256}) { run<0, 240>(48, sbo); run<0, 192>(48, sbo); }
-  run<0, 64>(48); run<0, 256>(48);
+  // independent D regions vs one shared accumulator vs overlapping (level-stacked) regions
+  run<0, 224>(48, 128, 2, 224); run<0, 224>(48, 128, 1, 0); run<0, 224>(48, 128, 8, 32);
+  run<0, 128>(48, 128, 4, 128); run<0, 128>(48, 128, 1, 0); run<0, 128>(48, 128, 4, 32);
+  run<0, 64>(48, 128, 4, 64); run<0, 64>(48, 128, 1, 0);
+  run<0, 256>(48, 128, 2, 256); run<0, 256>(48, 128, 1, 0);
   return 0;
 }
