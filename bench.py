@@ -263,31 +263,55 @@ def run(args):
                "h2d_bytes_per_step": m_local * n * s_x, "d2h_bytes_per_step": m_local * n * s_x + n * n * 8}
         del Xh, Qh
 
-    # ---- roofline of the dominant kernel (the Gaussian sketch: FP64 DMMA-bound)
+    # ---- rooflines: every heavy kernel against its own bound, algorithmic
+    # work per launch / its library-event time on the launching stream; "roofline" = the dominant one.
     gbs = m_global * n * s_x / (ms * 1e-3) / 1e9
     peaks = _peaks()
     hbm = peaks.get("hbm_gbs", 6545.0)
+    roofs = {}
     if cfg["sketch"] == "gaussian":
+        # exact int8 digit-product sketch (sketch_gtc.cu); its algorithmic work is the method's 2kmn
+        # fp64 flops, so it is measured against the FP64 tensor (DMMA) peak it replaces.
         flops = 2.0 * k * m_local * n
         ach = flops / (per_ms["sketch"] * 1e-3) / 1e12
-        roof = {"kernel": "sketch_gauss_kernel", "bound": "tensor", "achieved": ach, "peak": DMMA_PEAK_TFLOPS,
-                "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
-                "peak_source": "derived FP64 DMMA peak (148 SM x 64 FMA/clk x 2 x 1.965 GHz); "
-                               "microbenchmark 37.0 (profiles/peaks_r1.jsonl)",
-                "algorithmic": f"2*k*m*n = {flops:.4g} flop per launch", "traffic": None}
+        roofs["sketch"] = {"kernel": "sketch_gauss_tc_kernel", "bound": "tensor", "achieved": ach,
+                           "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
+                           "peak_source": "FP64 DMMA peak 37.2 TF (148 SM x 64 FMA/clk x 2 x 1.965 GHz; "
+                                          "microbenchmark 37.0, profiles/peaks_r1.jsonl): fp64-equivalent view "
+                                          "of the exact int8 digit emulation",
+                           "algorithmic": f"2*k*m*n = {flops:.4g} flop per launch", "traffic": None}
     else:
         byts = m_local * n * s_x
         ach = byts / (per_ms["sketch"] * 1e-3) / 1e9
-        roof = {"kernel": "sketch_sparse_kernel", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                "frac": ach / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-                "algorithmic": f"m*n*s_x = {byts:.4g} B per launch", "traffic": None}
-    try:
+        roofs["sketch"] = {"kernel": "sketch_sparse_tc_kernel", "bound": "hbm", "achieved": ach, "peak": hbm,
+                           "unit": "GB/s", "frac": ach / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                           "algorithmic": f"m*n*s_x = {byts:.4g} B per launch (one read of X)", "traffic": None}
+    if dt == "f32" and n <= 64:
+        byts = 2.0 * m_local * n * s_x
+        ach = byts / (per_ms["solve"] * 1e-3) / 1e9
+        roofs["solve"] = {"kernel": "solve_tc_kernel", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                          "frac": ach / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                          "algorithmic": f"2*m*n*s_x = {byts:.4g} B per launch (read X, write Q)", "traffic": None}
+    else:
+        flops = float(m_local) * n * n
+        ach = flops / (per_ms["solve"] * 1e-3) / 1e12
+        roofs["solve"] = {"kernel": "blocked substitution (fp64 DMMA)", "bound": "tensor", "achieved": ach,
+                          "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
+                          "peak_source": "FP64 DMMA peak 37.2 TF", "algorithmic": f"m*n^2 = {flops:.4g} flop per solve",
+                          "traffic": None}
+    try:   # DRAM bytes per launch from one `ncu --set full` capture of the same workload (tools/ncu_traffic.py)
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            tr = json.load(f).get(args.config)
-            if tr:
-                roof["traffic"] = tr
+            tr = json.load(f).get(args.config) or {}
     except OSError:
-        pass
+        tr = {}
+    for r_ in roofs.values():
+        tb = tr.get(r_["kernel"])
+        if tb is not None and ws == 1:
+            r_["traffic"] = tb
+            r_["traffic_source"] = "ncu --set full: dram__bytes_read.sum + dram__bytes_write.sum per launch"
+    dom = max(("sketch", "solve"), key=lambda kk: per_ms.get(kk, 0.0))
+    roof = dict(roofs[dom])
+    roof["share_of_step"] = per_ms.get(dom, 0.0) / ms
     # north-star roofline for the whole factorization
     t_hbm = 3.0 * m_local * n * s_x / (hbm * 1e9)
     t_flop = m_local * n * n / (DMMA_PEAK_TFLOPS * 1e12)
@@ -304,7 +328,7 @@ def run(args):
                        "sketch": cfg["sketch"], "x_dtype": dt, "cond": 10.0 ** cfg["log10_cond"],
                        "parallelism": f"row-partition x{ws}, 1 all-reduce",
                        "l2": f"inputs larger than L2 (X = {m_local * n * s_x / 2**20:.0f} MiB > 126 MiB), no flush"},
-            "per_kernel_ms": per_ms, "roofline": roof, "northstar_roofline": ns,
+            "per_kernel_ms": per_ms, "roofline": roof, "kernel_rooflines": roofs, "northstar_roofline": ns,
             "gpu_launches": plan.launches_per_factor(m_local) * args.steps,
             "clocks": clk.summary(), "e2e": e2e}
 

@@ -478,9 +478,17 @@ rcholqr_status rcholqr_comm_destroy(void* comm) {
 
 int32_t rcholqr_launches_per_factor(rcholqr_plan p, int64_t m) {
   if (!p) return -1;
-  // sketch (+ reduce) | QR | tri-inverse | tall solve   (memsets and the all-reduce are not ours)
-  const int solve_launches = p->stream_tb > 0 ? 2 * ((p->d.n + p->stream_tb - 1) / p->stream_tb) : 1;
-  return (m > 0 ? 2 : 0) + 1 + 1 + (m > 0 ? solve_launches : 0);
+  // Our kernels per factor (without S), assuming 16-byte aligned X/Q so the tensor-core paths run;
+  // memsets and the NCCL all-reduce are not counted.
+  //   sketch: [tcgen05 sketch +] the CUDA-core kernel (its guarded fallback, exits at once) + reduce
+  //   QR: 1 | triangular prep (blocked prep or R^{-1}): 1 | solve: tcgen05 (W-digit prep + solve) = 2,
+  //   streamed fp64 GEMMs = 2 per column block, else 1.
+  const bool tc_sketch = p->sk.kind == kSketchSparseTC || (p->sk.kind < kSketchSparse && p->sk.tc);
+  const int sketch_launches = (tc_sketch ? 2 : 1) + 1;
+  int solve_launches = 1;
+  if (p->solve_tc) solve_launches = 2;
+  else if (p->stream_tb > 0) solve_launches = 2 * ((p->d.n + p->stream_tb - 1) / p->stream_tb);
+  return (m > 0 ? sketch_launches : 0) + 1 + 1 + (m > 0 ? solve_launches : 0);
 }
 
 rcholqr_status rcholqr_set_timing(rcholqr_plan p, int32_t enable) {
