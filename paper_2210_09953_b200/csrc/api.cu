@@ -56,6 +56,8 @@ struct rcholqr_plan_s {
   int warp_solve = 0;       // > 0: warp-independent blocked substitution with this many warps/CTA
   int stream_tb = 0;        // > 0: streamed blocked substitution (fp64, n > 128) with this block width
   bool solve_tc = false;    // fp32 X, n <= 64: tcgen05 digit solve Q = X R^{-1} (solve_tc.cu)
+  void* xdig = nullptr;     // pre-split X digit planes of the tcgen05 Gaussian sketch (grown on demand)
+  size_t xdig_bytes = 0;
   void* qws = nullptr;      // its W-digit workspace
   double* tbuf = nullptr;   // [m_local][stream_tb] T_J workspace of the streamed solve
   size_t tbuf_elems = 0;
@@ -152,7 +154,17 @@ rcholqr_status do_sketch(rcholqr_plan p, const void* X, int64_t m, int64_t ro, i
   const auto& d = p->d;
   if (m > 0) {
     if (p->timing) cudaEventRecord(p->ev[0], st);
-    CU(launch_sketch(p->sk, X, d.dtype, m, d.n, ldx, ro, d.k, d.nnz_per_col, d.seed, p->part, p->partc, P, p->status_d, p->flag_d, st,
+    if (p->sk.tc && p->sk.kind < kSketchSparse) {   // grow the pre-split digit workspace (capped)
+      const size_t need = gauss_tcp_workspace(m, d.n, d.dtype, p->sk.tc_splits);
+      if (need <= kXdigCapBytes && need > p->xdig_bytes) {
+        cudaFree(p->xdig);
+        p->xdig = nullptr; p->xdig_bytes = 0;
+        if (cudaMalloc(&p->xdig, need) == cudaSuccess) p->xdig_bytes = need;
+        else cudaGetLastError();   // not enough memory: the in-kernel split is used instead
+      }
+    }
+    CU(launch_sketch(p->sk, X, d.dtype, m, d.n, ldx, ro, d.k, d.nnz_per_col, d.seed, p->part, p->partc, P, p->status_d, p->flag_d,
+                     p->xdig, p->xdig_bytes, st,
                      p->timing ? p->ev[1] : nullptr));
   } else {
     if (p->timing) { cudaEventRecord(p->ev[0], st); cudaEventRecord(p->ev[1], st); }
@@ -316,7 +328,7 @@ rcholqr_status rcholqr_destroy(rcholqr_plan p) {
   if (!p) return RCHOLQR_OK;
   DeviceGuard dg(p->d.device);
   cudaFree(p->part); cudaFree(p->partc); cudaFree(p->P); cudaFree(p->W); cudaFree(p->Awork); cudaFree(p->diag); cudaFree(p->tau);
-  cudaFree(p->Rtmp); cudaFree(p->status_d); cudaFree(p->flag_d); cudaFree(p->qws);
+  cudaFree(p->Rtmp); cudaFree(p->status_d); cudaFree(p->flag_d); cudaFree(p->qws); cudaFree(p->xdig);
   if (p->status_h) cudaFreeHost(p->status_h);
   cudaFree(p->xbuf); cudaFree(p->qbuf); cudaFree(p->rbuf); cudaFree(p->sbuf); cudaFree(p->tbuf);
   for (int t = 0; t < 7; ++t)
@@ -484,7 +496,10 @@ int32_t rcholqr_launches_per_factor(rcholqr_plan p, int64_t m) {
   //   QR: 1 | triangular prep (blocked prep or R^{-1}): 1 | solve: tcgen05 (W-digit prep + solve) = 2,
   //   streamed fp64 GEMMs = 2 per column block, else 1.
   const bool tc_sketch = p->sk.kind == kSketchSparseTC || (p->sk.kind < kSketchSparse && p->sk.tc);
-  const int sketch_launches = (tc_sketch ? 2 : 1) + 1;
+  int sketch_launches = (tc_sketch ? 2 : 1) + 1;
+  if (tc_sketch && p->sk.kind < kSketchSparse &&
+      gauss_tcp_workspace(m, p->d.n, p->d.dtype, p->sk.tc_splits) <= kXdigCapBytes)
+    sketch_launches += 2;   // pre-split: column maxima + digit planes
   int solve_launches = 1;
   if (p->solve_tc) solve_launches = 2;
   else if (p->stream_tb > 0) solve_launches = 2 * ((p->d.n + p->stream_tb - 1) / p->stream_tb);

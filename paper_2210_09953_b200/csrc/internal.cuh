@@ -46,6 +46,12 @@ bool gauss_tc_aligned(const void* X, int dtype, int n, int64_t ldx);
 cudaError_t launch_gauss_tc(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                             uint64_t seed, int tiles_k, int tiles_n, int splits, int64_t rows_per_split,
                             double* part, double* partc, int* overflow, cudaStream_t st);
+// pre-split variant: X digit planes written once to a workspace of gauss_tcp_workspace() bytes
+size_t gauss_tcp_workspace(int64_t m, int n, int dtype, int splits);
+cudaError_t launch_gauss_tcp(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
+                             uint64_t seed, int tiles_k, int tiles_n, int splits, int64_t rows_per_split,
+                             double* part, double* partc, int* overflow, void* ws, cudaStream_t st);
+constexpr size_t kXdigCapBytes = (size_t)4 << 30;   // largest pre-split digit workspace a plan allocates
 struct TrsmLaunch {
   int kind;
   int TM, NT, threads, tiles_n;
@@ -56,7 +62,7 @@ struct TrsmLaunch {
 SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms, size_t smem_optin);
 cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
                           int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* partc, double* P,
-                          int* status, int* flag, cudaStream_t st, cudaEvent_t ev_mid);
+                          int* status, int* flag, void* xdig, size_t xdig_bytes, cudaStream_t st, cudaEvent_t ev_mid);
 TrsmLaunch plan_trsm(int n, int dtype, size_t smem_optin);
 cudaError_t launch_tri_inverse(const double* R, int n, double* W, int* status, cudaStream_t st);
 cudaError_t launch_trsm(const TrsmLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,

@@ -639,7 +639,7 @@ static cudaError_t launch_gauss_typed(const SketchLaunch& L, const void* X, int6
 
 cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
                           int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* partc, double* P,
-                          int* status, int* flag, cudaStream_t st, cudaEvent_t ev_mid) {
+                          int* status, int* flag, void* xdig, size_t xdig_bytes, cudaStream_t st, cudaEvent_t ev_mid) {
   cudaError_t e;
   const int64_t per = (m + L.splits - 1) / L.splits;
   double scale;
@@ -698,8 +698,12 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
       const int64_t trps = std::max<int64_t>(KC, ((tper + KC - 1) / KC) * KC);
       e = cudaMemsetAsync(flag, 0, sizeof(int), st);
       if (e != cudaSuccess) return e;
-      e = launch_gauss_tc(X, dtype, m, n, ldx, row_offset, k, seed, L.tc_tiles_k, L.tc_tiles_n, splits, trps, part,
-                          partc, flag, st);
+      if (xdig && gauss_tcp_workspace(m, n, dtype, splits) <= xdig_bytes && !getenv("RCHOLQR_GAUSS_NO_PRESPLIT"))
+        e = launch_gauss_tcp(X, dtype, m, n, ldx, row_offset, k, seed, L.tc_tiles_k, L.tc_tiles_n, splits, trps, part,
+                             partc, flag, xdig, st);
+      else
+        e = launch_gauss_tc(X, dtype, m, n, ldx, row_offset, k, seed, L.tc_tiles_k, L.tc_tiles_n, splits, trps, part,
+                            partc, flag, st);
       if (e == cudaSuccess) guard = flag;                     // else: the DMMA kernel computes the sketch
       else if (e != cudaErrorNotSupported) return e;
     }

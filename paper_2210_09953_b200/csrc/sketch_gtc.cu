@@ -27,6 +27,7 @@
 // Theta (Philox + Box-Muller) and its digit tiles in two groups of three warps that alternate
 // stages; warps 8..15 split X into digit planes (warps 8..11 also drain TMEM).
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 #include <type_traits>
@@ -418,6 +419,320 @@ sketch_gauss_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int 
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
+// =============================================================================================
+// Pre-split variant (fp32/fp64 X when the digit buffer fits): X is split into its digit planes ONCE
+// by xdig_split_kernel, in exactly the shared-memory tile layout of the sketch (one contiguous
+// DX x 4 KB block per (split, 32-row stage, 128-column tile)), so the sketch kernel receives each
+// stage with a single bulk copy and all of its producer warps generate Theta.  Column scales are
+// per (split, column), from the split's first 32 rows (the same heuristic and overflow guard).
+constexpr int GP_TWARPS = 12;                     // Theta warps 2..13: four groups of three
+constexpr int GP_THREADS = 32 * (2 + GP_TWARPS);
+constexpr int GP_GROUPS = 4;
+static_assert(GT_DRAIN % GP_GROUPS == 0, "drain stages belong to group 0");
+
+template <typename TX>
+struct GpCfg {
+  using G = GtCfg<TX>;
+  static constexpr int A_BYTES = G::DX * 4096;                        // DX planes of 128 x 32 B
+  static constexpr int DIG_STAGE = A_BYTES + G::B_BYTES;
+  static constexpr int STAGES = (232448 - 2048) / DIG_STAGE < 6 ? (232448 - 2048) / DIG_STAGE : 6;
+  static constexpr size_t SMEM = (size_t)STAGES * DIG_STAGE + 2048;
+  static_assert(SMEM <= 232448 && STAGES >= 3, "shared memory");
+};
+
+// per (split, column): max |x| high bits over the split's first 32 rows (tile-padded columns)
+template <typename TX>
+__global__ void xdig_maxbits_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64_t rows_per_split,
+                                    int npad, uint32_t* __restrict__ maxbits) {
+  const int split = blockIdx.x;
+  const int64_t i0 = (int64_t)split * rows_per_split;
+  const int rows = (int)max((int64_t)0, min((int64_t)GT_KC, min(m, i0 + rows_per_split) - i0));
+  for (int j = threadIdx.x; j < npad; j += blockDim.x) {
+    uint32_t mx = 0u;
+    if (j < n)
+      for (int ii = 0; ii < rows; ++ii) mx = max(mx, gt_habs(X[(i0 + ii) * ldx + j]));
+    maxbits[(size_t)split * npad + j] = mx;
+  }
+}
+
+// unit u = ((split * stages + stage) * tiles_n + tn): DX digit planes of 128 columns x 32 rows
+template <typename TX>
+__global__ void __launch_bounds__(256)
+xdig_split_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64_t rows_per_split, int stages,
+                  int tiles_n, int64_t units, const uint32_t* __restrict__ maxbits, unsigned char* __restrict__ dig,
+                  int* overflow) {
+  constexpr int DX = GtFmt<TX>::DX;
+  const int j = threadIdx.x & (GT_M - 1), kg = threadIdx.x >> 7;
+  const int npad = tiles_n * GT_M;
+  uint32_t amax = 0u;
+  bool bad = false;
+  for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
+    const int tn = (int)(u % tiles_n);
+    const int64_t st_g = u / tiles_n;
+    const int split = (int)(st_g / stages), stage = (int)(st_g % stages);
+    const int64_t i_begin = (int64_t)split * rows_per_split, i_end = min(m, i_begin + rows_per_split);
+    const int64_t i0 = i_begin + (int64_t)stage * GT_KC;
+    const int col = tn * GT_M + j;
+    const GtCol cp = gt_col<TX>(maxbits[(size_t)split * npad + col]);
+    uint32_t Wd[DX][4];
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+      uint32_t hw[4], lw[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int64_t i = i0 + kg * 16 + qq * 4 + kk;
+        const TX x = (col < n && i < i_end) ? X[i * ldx + col] : (TX)0;
+        if (col < n) { amax = max(amax, gt_habs(x) >= cp.lim ? 0xFFFFFFFFu : 0u); bad |= cp.bad; }
+        gt_split(x, cp.s, hw[kk], lw[kk]);
+      }
+      uint32_t W[DX];
+      gt_digits<DX>(hw, lw, W);
+#pragma unroll
+      for (int b = 0; b < DX; ++b) Wd[b][qq] = W[b];
+    }
+    unsigned char* blk = dig + (size_t)u * (DX * 4096);
+#pragma unroll
+    for (int b = 0; b < DX; ++b)
+      *reinterpret_cast<uint4*>(blk + b * 4096 + cm_off(j, kg * 16, GT_M)) = make_uint4(Wd[b][0], Wd[b][1], Wd[b][2], Wd[b][3]);
+  }
+  if (amax || bad) atomicOr(overflow, 1);
+}
+
+template <typename TX>
+__global__ void __launch_bounds__(GP_THREADS, 1)
+sketch_gauss_tcp_kernel(const unsigned char* __restrict__ dig, const uint32_t* __restrict__ maxbits, int64_t m, int n,
+                        int64_t row_offset, int k, uint64_t seed, int tiles_k, int tiles_n, int64_t rows_per_split,
+                        int stages_per_split, double* __restrict__ part, double* __restrict__ partc) {
+  using C = GtCfg<TX>;
+  using P = GpCfg<TX>;
+  using F = GtFmt<TX>;
+  constexpr int DX = C::DX, KT = C::KT, LEV = C::LEV, S = P::STAGES;
+  extern __shared__ __align__(1024) unsigned char sm[];
+  uint64_t* dfull = reinterpret_cast<uint64_t*>(sm + (size_t)S * P::DIG_STAGE);
+  uint64_t* dempty = dfull + S;
+  uint64_t* drainbar = dempty + S;
+  uint64_t* drained = drainbar + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(drained + 1);
+
+  const int tiles = tiles_k * tiles_n;
+  const int tile = blockIdx.x % tiles, split = blockIdx.x / tiles;
+  const int tk = tile % tiles_k, tn = tile / tiles_k;
+  const int r0 = tk * KT, n0 = tn * GT_M;
+  const int ncols = min(GT_M, n - n0), nrows = min(KT, k - r0);
+  const int64_t i_begin = (int64_t)split * rows_per_split;
+  const int64_t i_end = min(m, i_begin + rows_per_split);
+  const int nstages = i_end > i_begin ? (int)((i_end - i_begin + GT_KC - 1) / GT_KC) : 0;
+  const int ndrains = (nstages + GT_DRAIN - 1) / GT_DRAIN;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      tc::mbar_init(&dfull[s], GP_TWARPS / GP_GROUPS + 1);   // the stage's Theta group + the loader (tx)
+      tc::mbar_init(&dempty[s], 1);
+    }
+    tc::mbar_init(drainbar, 1);
+    tc::mbar_init(drained, 4);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(tc::smem_u32(tmem_slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+  const uint32_t tmem = *tmem_slot;
+  if (warp < 4) {
+    const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
+    for (int c8 = 0; c8 < LEV * KT / 8; ++c8) tc::st8_zero(lb + c8 * 8);
+    tc::wait_st();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n");
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- MMA issuer (lane 0)
+    constexpr uint32_t idesc = tc::idesc_i8(GT_M, C::NB, true, true);
+    for (int c = 0; c < nstages; ++c) {
+      const int s = c % S;
+      if (c > 0 && c % GT_DRAIN == 0) tc::mbar_wait(drained, (uint32_t)((c / GT_DRAIN - 1) & 1));
+      tc::mbar_wait(&dfull[s], (uint32_t)((c / S) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      if (lane == 0) {
+        const uint32_t sa = tc::smem_u32(sm + (size_t)s * P::DIG_STAGE);
+        const uint64_t db = tc::desc(sa + P::A_BYTES, C::B_LBO, GT_BSBO);
+#pragma unroll
+        for (int b = 0; b < DX; ++b)
+          tc::mma_i8(tmem + b * KT, tc::desc(sa + b * 4096, (GT_M / 8) * 128, 128), db, idesc, 1u);
+        tc::commit(&dempty[s]);
+        if ((c + 1) % GT_DRAIN == 0 || c == nstages - 1) tc::commit(drainbar);
+      }
+      __syncwarp();
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- digit loader (lane 0)
+    for (int c = 0; c < nstages; ++c) {
+      const int s = c % S;
+      if (c >= S) tc::mbar_wait(&dempty[s], (uint32_t)(((c / S) - 1) & 1));
+      if (lane == 0) {
+        const size_t u = ((size_t)split * stages_per_split + c) * tiles_n + tn;
+        tc::mbar_arrive_tx(&dfull[s], (uint32_t)P::A_BYTES);
+        tc::bulk_g2s(sm + (size_t)s * P::DIG_STAGE, dig + u * P::A_BYTES, (uint32_t)P::A_BYTES, &dfull[s]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---------------------------------------------------------------- Theta digits (+ drains: warps 2..5)
+    const int tw = warp - 2, grp = tw / (GP_TWARPS / GP_GROUPS);
+    const int t = (tw % (GP_TWARPS / GP_GROUPS)) * 32 + lane;
+    const bool active = t < C::TASKS_Z;
+    const int q = t % (KT / 4), kq = t / (KT / 4);
+    const uint32_t qg = (uint32_t)((r0 >> 2) + q);
+    const bool drainer = warp < 6;
+    const int dq = warp & 3;
+    auto drain = [&](int d) {
+      tc::mbar_wait(drainbar, (uint32_t)(d & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;\n");
+      const int jj = dq * 32 + lane;
+      const uint32_t lb = tmem + ((uint32_t)(dq * 32) << 16);
+      double* Ps = part + (size_t)split * (size_t)k * n;
+      double* Pc = partc + (size_t)split * (size_t)k * n;
+      const int ej = gt_col<TX>(maxbits[(size_t)split * tiles_n * GT_M + n0 + jj]).e;
+#pragma unroll 1
+      for (int r8 = 0; r8 < KT / 8; ++r8) {
+        double v[8];
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) v[rr] = 0.0;
+#pragma unroll
+        for (int L = LEV - 1; L >= 0; --L) {
+          uint32_t a8[8];
+          tc::ld8(lb + L * KT + r8 * 8, a8);
+          tc::wait_ld();
+          const double w = ldexp(1.0, 8 * (LEV - 1 - L));
+#pragma unroll
+          for (int rr = 0; rr < 8; ++rr) v[rr] = fma((double)(int32_t)a8[rr], w, v[rr]);
+        }
+        if (jj < ncols) {
+#pragma unroll
+          for (int rr = 0; rr < 8; ++rr) {
+            const int r = r8 * 8 + rr;
+            if (r < nrows) {
+              const double val = ldexp(v[rr], ej - 44 - F::FB);
+              const size_t o = (size_t)(r0 + r) * n + n0 + jj;
+              if (d == 0) { Ps[o] = val; Pc[o] = 0.0; }
+              else {
+                const double a0 = Ps[o], sum = a0 + val, bb = sum - a0;
+                Pc[o] += (a0 - (sum - bb)) + (val - bb);
+                Ps[o] = sum;
+              }
+            }
+          }
+        }
+      }
+      if (d + 1 < ndrains) {
+        for (int c8 = 0; c8 < LEV * KT / 8; ++c8) tc::st8_zero(lb + c8 * 8);
+        tc::wait_st();
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n");
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(drained);
+    };
+    int boff[4];
+#pragma unroll
+    for (int rr = 0; rr < 4; ++rr) boff[rr] = b_off<TX>(4 * q + rr, 4 * kq);
+    int next_drain = 1;                                   // drain d is due before stage (d + 1) * GT_DRAIN
+    for (int c = grp; c < nstages; c += GP_GROUPS) {
+      const int s = c % S;
+      if (drainer)
+        while (next_drain * GT_DRAIN <= c) { drain(next_drain - 1); ++next_drain; }
+      uint32_t W[4][GT_DZ];
+      if (active) {
+        const uint64_t gi = (uint64_t)(row_offset + i_begin + (int64_t)c * GT_KC + 4 * kq);
+        float z[4][4];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const float4 g = gauss4(seed, gi + kk, qg);
+          z[kk][0] = g.x; z[kk][1] = g.y; z[kk][2] = g.z; z[kk][3] = g.w;
+        }
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+          uint32_t hw[4], lw[4];
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) gt_split(z[kk][rr], 0x1p172, hw[kk], lw[kk]);
+          gt_digits<GT_DZ>(hw, lw, W[rr]);
+        }
+      }
+      if (c >= S) tc::mbar_wait(&dempty[s], (uint32_t)(((c / S) - 1) & 1));
+      if (active) {
+        unsigned char* st = sm + (size_t)s * P::DIG_STAGE + P::A_BYTES;
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr)
+#pragma unroll
+          for (int a = 0; a < GT_DZ; ++a)
+            *reinterpret_cast<uint32_t*>(st + boff[rr] + (a * KT >> 3) * GT_BSBO) = W[rr][a];
+      }
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&dfull[s]);
+    }
+    if (drainer) {
+      while (next_drain <= ndrains) { drain(next_drain - 1); ++next_drain; }
+      if (ndrains == 0) {
+        const int jj = dq * 32 + lane;
+        if (jj < ncols)
+          for (int r = 0; r < nrows; ++r) {
+            part[(size_t)split * k * n + (size_t)(r0 + r) * n + n0 + jj] = 0.0;
+            partc[(size_t)split * k * n + (size_t)(r0 + r) * n + n0 + jj] = 0.0;
+          }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
+}
+
+// bytes of the pre-split digit workspace (digit blocks + per-(split, column) maxima)
+size_t gauss_tcp_workspace(int64_t m, int n, int dtype, int splits) {
+  const int dx = dtype == RCHOLQR_F64 ? GtFmt<double>::DX : GtFmt<float>::DX;
+  const int tiles_n = (n + GT_M - 1) / GT_M;
+  const int64_t per = (m + splits - 1) / splits;
+  const int64_t rps = std::max<int64_t>(GT_KC, ((per + GT_KC - 1) / GT_KC) * GT_KC);
+  const int64_t stages = rps / GT_KC;
+  return (size_t)splits * stages * tiles_n * dx * 4096 + (size_t)splits * tiles_n * GT_M * 4;
+}
+
+template <typename TX>
+static cudaError_t launch_gtcp(const TX* X, int64_t m, int n, int64_t ldx, int64_t ro, int k, uint64_t seed,
+                               int tiles_k, int tiles_n, int splits, int64_t rps, double* part, double* partc,
+                               int* overflow, void* ws, cudaStream_t st) {
+  constexpr int DX = GtFmt<TX>::DX;
+  const int stages = (int)(rps / GT_KC);
+  const int64_t units = (int64_t)splits * stages * tiles_n;
+  unsigned char* dig = reinterpret_cast<unsigned char*>(ws);
+  uint32_t* maxbits = reinterpret_cast<uint32_t*>(dig + (size_t)units * DX * 4096);
+  xdig_maxbits_kernel<TX><<<splits, 256, 0, st>>>(X, m, n, ldx, rps, tiles_n * GT_M, maxbits);
+  xdig_split_kernel<TX><<<(int)std::min<int64_t>(units, 148 * 8), 256, 0, st>>>(X, m, n, ldx, rps, stages, tiles_n,
+                                                                                 units, maxbits, dig, overflow);
+  auto kern = sketch_gauss_tcp_kernel<TX>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GpCfg<TX>::SMEM);
+  if (e != cudaSuccess) return e;
+  kern<<<tiles_k * tiles_n * splits, GP_THREADS, GpCfg<TX>::SMEM, st>>>(dig, maxbits, m, n, ro, k, seed, tiles_k,
+                                                                         tiles_n, rps, stages, part, partc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gauss_tcp(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
+                             uint64_t seed, int tiles_k, int tiles_n, int splits, int64_t rows_per_split,
+                             double* part, double* partc, int* overflow, void* ws, cudaStream_t st) {
+  if (dtype == RCHOLQR_F64)
+    return launch_gtcp((const double*)X, m, n, ldx, row_offset, k, seed, tiles_k, tiles_n, splits, rows_per_split,
+                       part, partc, overflow, ws, st);
+  return launch_gtcp((const float*)X, m, n, ldx, row_offset, k, seed, tiles_k, tiles_n, splits, rows_per_split, part,
+                     partc, overflow, ws, st);
 }
 
 int gauss_tc_kt(int dtype) { return dtype == RCHOLQR_F64 ? GtFmt<double>::KT : GtFmt<float>::KT; }
