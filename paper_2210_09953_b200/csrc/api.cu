@@ -62,6 +62,7 @@ struct rcholqr_plan_s {
   double* tbuf = nullptr;   // [m_local][stream_tb] T_J workspace of the streamed solve
   size_t tbuf_elems = 0;
   int qr_kind = 0;
+  double* qr_ws = nullptr;   // blocked Householder workspace (kQrBlocked)
   double* part = nullptr;   // [splits][k][n] per-CTA sketch partials (running sums)
   double* partc = nullptr;  // [splits][k][n] their TwoSum compensations (Gaussian sketch)
   double* P = nullptr;      // [k][n] reduced sketch
@@ -302,6 +303,7 @@ rcholqr_status rcholqr_create(const rcholqr_desc* desc, rcholqr_plan* out) {
                  cudaMalloc(&p->partc, sizeof(double) * kn * p->sk.max_splits()) == cudaSuccess &&
                  cudaMalloc(&p->flag_d, sizeof(int)) == cudaSuccess &&
                  cudaMalloc(&p->qws, solve_tc_workspace()) == cudaSuccess &&
+                 (p->qr_kind != kQrBlocked || cudaMalloc(&p->qr_ws, qr_blocked_workspace(k, n)) == cudaSuccess) &&
                  cudaMalloc(&p->P, sizeof(double) * kn) == cudaSuccess &&
                  cudaMalloc(&p->W, sizeof(double) * nn) == cudaSuccess &&
                  cudaMalloc(&p->Awork, sizeof(double) * kn) == cudaSuccess &&
@@ -328,7 +330,7 @@ rcholqr_status rcholqr_destroy(rcholqr_plan p) {
   if (!p) return RCHOLQR_OK;
   DeviceGuard dg(p->d.device);
   cudaFree(p->part); cudaFree(p->partc); cudaFree(p->P); cudaFree(p->W); cudaFree(p->Awork); cudaFree(p->diag); cudaFree(p->tau);
-  cudaFree(p->Rtmp); cudaFree(p->status_d); cudaFree(p->flag_d); cudaFree(p->qws); cudaFree(p->xdig);
+  cudaFree(p->Rtmp); cudaFree(p->status_d); cudaFree(p->flag_d); cudaFree(p->qws); cudaFree(p->xdig); cudaFree(p->qr_ws);
   if (p->status_h) cudaFreeHost(p->status_h);
   cudaFree(p->xbuf); cudaFree(p->qbuf); cudaFree(p->rbuf); cudaFree(p->sbuf); cudaFree(p->tbuf);
   for (int t = 0; t < 7; ++t)
@@ -348,7 +350,7 @@ rcholqr_status rcholqr_factor_async(rcholqr_plan p, const void* X, int64_t m, in
   CU(cudaMemsetAsync(p->status_d, 0, sizeof(int), st));
   rcholqr_status s = do_sketch(p, X, m, ro, ldx, p->P, st);
   if (s != RCHOLQR_OK) return s;
-  CU(launch_qr(p->qr_kind, p->P, k, n, Rout, p->Awork, p->diag, p->tau, p->status_d, st));
+  CU(launch_qr(p->qr_kind, p->P, k, n, Rout, p->Awork, p->diag, p->tau, p->qr_ws, p->status_d, st));
   if (S) CU(launch_form_s(p->Awork, p->tau, p->diag, k, n, S, p->status_d, st));
   if (p->timing) cudaEventRecord(p->ev[4], st);
   rcholqr_status s2 = solve(p, X, m, ldx, Rout, Q, ldq, st, true);
@@ -420,7 +422,7 @@ rcholqr_status rcholqr_small_qr(rcholqr_plan p, const double* P, double* R, doub
   cudaStream_t st = (cudaStream_t)stream;
   const int k = p->d.k, n = p->d.n;
   CU(cudaMemsetAsync(p->status_d, 0, sizeof(int), st));
-  CU(launch_qr(p->qr_kind, P, k, n, R, p->Awork, p->diag, p->tau, p->status_d, st));
+  CU(launch_qr(p->qr_kind, P, k, n, R, p->Awork, p->diag, p->tau, p->qr_ws, p->status_d, st));
   if (S) CU(launch_form_s(p->Awork, p->tau, p->diag, k, n, S, p->status_d, st));
   const bool t = p->timing;
   p->timing = false;
@@ -503,7 +505,12 @@ int32_t rcholqr_launches_per_factor(rcholqr_plan p, int64_t m) {
   int solve_launches = 1;
   if (p->solve_tc) solve_launches = 2;
   else if (p->stream_tb > 0) solve_launches = 2 * ((p->d.n + p->stream_tb - 1) / p->stream_tb);
-  return (m > 0 ? sketch_launches : 0) + 1 + 1 + (m > 0 ? solve_launches : 0);
+  int qr_launches = 1;
+  if (p->qr_kind == kQrBlocked) {   // copy + per panel (panel kernel + 3 GEMMs, the last panel 1) + finalize
+    const int panels = (p->d.n + 31) / 32;
+    qr_launches = 2 + panels + 3 * (panels - 1);
+  }
+  return (m > 0 ? sketch_launches : 0) + qr_launches + 1 + (m > 0 ? solve_launches : 0);
 }
 
 rcholqr_status rcholqr_set_timing(rcholqr_plan p, int32_t enable) {

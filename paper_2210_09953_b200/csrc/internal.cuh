@@ -30,7 +30,7 @@ cudaError_t launch_sparse_tc(const void* X, int dtype, int64_t m, int n, int64_t
                              int zeta, uint64_t seed, int splits, int64_t rows_per_split, double* part, int* overflow,
                              cudaStream_t st);
 enum TrsmKind : int { kTrsm64x24 = 0, kTrsm128x64 = 1, kTrsm128x112 = 2, kTrsm128x128 = 3 };
-enum QrKind : int { kQrSmem = 0, kQrGlobal = 1 };
+enum QrKind : int { kQrSmem = 0, kQrGlobal = 1, kQrBlocked = 2 };
 
 struct SketchLaunch {
   int kind;
@@ -69,7 +69,11 @@ cudaError_t launch_trsm(const TrsmLaunch& L, const void* X, int dtype, int64_t m
                         const double* W, void* Q, int64_t ldq, const int* status, cudaStream_t st);
 int plan_qr(int k, int n, size_t smem_optin);
 cudaError_t launch_qr(int kind, const double* P, int k, int n, double* R, double* Awork, double* diag,
-                      double* tau, int* status, cudaStream_t st);
+                      double* tau, double* qr_ws, int* status, cudaStream_t st);
+// blocked Householder (qr_blocked.cu) for sketches the single-CTA kernels do not fit
+size_t qr_blocked_workspace(int k, int n);
+cudaError_t launch_qr_blocked(const double* P, int k, int n, double* R, double* A, double* diag, double* tau,
+                              double* ws, int* status, cudaStream_t st);
 cudaError_t launch_form_s(const double* Awork, const double* tau, const double* diag, int k, int n,
                           double* S, const int* status, cudaStream_t st);
 cudaError_t launch_theta_export(uint64_t seed, int k, int sketch, int zeta, int64_t row_offset, int64_t m,

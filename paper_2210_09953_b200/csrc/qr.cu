@@ -15,6 +15,7 @@
 // per column of S.
 #include <cuda_runtime.h>
 #include <algorithm>
+#include <cstdlib>
 #include <utility>
 #include "internal.cuh"
 
@@ -344,11 +345,13 @@ form_s_kernel(const double* __restrict__ A, const double* __restrict__ tau, cons
 
 int plan_qr(int k, int n, size_t smem_optin) {
   const size_t need = sizeof(double) * (size_t)k * n;
-  return need + 1024 <= std::min<size_t>(smem_optin, 220 * 1024) ? kQrSmem : kQrGlobal;
+  if (need + 1024 <= std::min<size_t>(smem_optin, 220 * 1024)) return kQrSmem;
+  return getenv("RCHOLQR_QR_UNBLOCKED") ? kQrGlobal : kQrBlocked;
 }
 
 cudaError_t launch_qr(int kind, const double* P, int k, int n, double* R, double* Awork, double* diag,
-                      double* tau, int* status, cudaStream_t st) {
+                      double* tau, double* qr_ws, int* status, cudaStream_t st) {
+  if (kind == kQrBlocked && qr_ws) return launch_qr_blocked(P, k, n, R, Awork, diag, tau, qr_ws, status, st);
   if (k <= 32 * 4 && n <= 16 * 4) {
     householder_reg_kernel<4, 4, 16><<<1, 32 * 16, 0, st>>>(P, k, n, R, Awork, diag, tau, status);
   } else if (k <= 32 * 7 && n <= 16 * 7) {
