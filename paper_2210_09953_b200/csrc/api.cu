@@ -156,8 +156,8 @@ rcholqr_status do_sketch(rcholqr_plan p, const void* X, int64_t m, int64_t ro, i
   if (m > 0) {
     if (p->timing) cudaEventRecord(p->ev[0], st);
     if (p->sk.tc && p->sk.kind < kSketchSparse) {   // grow the pre-split digit workspace (capped)
-      const size_t need = gauss_tcp_workspace(m, d.n, d.dtype, p->sk.tc_splits);
-      if (need <= kXdigCapBytes && need > p->xdig_bytes) {
+      const size_t need = gauss_tcp_chunk_workspace(m, d.n, d.dtype, p->sk.tc_splits);
+      if (need > p->xdig_bytes) {
         cudaFree(p->xdig);
         p->xdig = nullptr; p->xdig_bytes = 0;
         if (cudaMalloc(&p->xdig, need) == cudaSuccess) p->xdig_bytes = need;
@@ -499,9 +499,13 @@ int32_t rcholqr_launches_per_factor(rcholqr_plan p, int64_t m) {
   //   streamed fp64 GEMMs = 2 per column block, else 1.
   const bool tc_sketch = p->sk.kind == kSketchSparseTC || (p->sk.kind < kSketchSparse && p->sk.tc);
   int sketch_launches = (tc_sketch ? 2 : 1) + 1;
-  if (tc_sketch && p->sk.kind < kSketchSparse &&
-      gauss_tcp_workspace(m, p->d.n, p->d.dtype, p->sk.tc_splits) <= kXdigCapBytes)
-    sketch_launches += 2;   // pre-split: column maxima + digit planes
+  if (tc_sketch && p->sk.kind < kSketchSparse && m > 0) {   // pre-split: (column maxima + digit planes + sketch) per chunk
+    const size_t cap = gauss_tcp_chunk_workspace(m, p->d.n, p->d.dtype, p->sk.tc_splits);
+    int64_t chunk = m;
+    while (chunk > 32 && gauss_tcp_workspace(chunk, p->d.n, p->d.dtype, p->sk.tc_splits) > cap) chunk = (chunk + 1) / 2;
+    const int64_t chunks = (m + chunk - 1) / chunk;
+    sketch_launches += (int)(3 * chunks - 1);
+  }
   int solve_launches = 1;
   if (p->solve_tc) solve_launches = 2;
   else if (p->stream_tb > 0) solve_launches = 2 * ((p->d.n + p->stream_tb - 1) / p->stream_tb);

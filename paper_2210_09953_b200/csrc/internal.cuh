@@ -48,9 +48,10 @@ cudaError_t launch_gauss_tc(const void* X, int dtype, int64_t m, int n, int64_t 
                             double* part, double* partc, int* overflow, cudaStream_t st);
 // pre-split variant: X digit planes written once to a workspace of gauss_tcp_workspace() bytes
 size_t gauss_tcp_workspace(int64_t m, int n, int dtype, int splits);
+size_t gauss_tcp_chunk_workspace(int64_t m, int n, int dtype, int splits);   // capped at kXdigCapBytes
 cudaError_t launch_gauss_tcp(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
-                             uint64_t seed, int tiles_k, int tiles_n, int splits, int64_t rows_per_split,
-                             double* part, double* partc, int* overflow, void* ws, cudaStream_t st);
+                             uint64_t seed, int tiles_k, int tiles_n, int splits, double* part, double* partc,
+                             int* overflow, void* ws, size_t ws_bytes, cudaStream_t st);
 constexpr size_t kXdigCapBytes = (size_t)4 << 30;   // largest pre-split digit workspace a plan allocates
 struct TrsmLaunch {
   int kind;

@@ -698,10 +698,11 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
       const int64_t trps = std::max<int64_t>(KC, ((tper + KC - 1) / KC) * KC);
       e = cudaMemsetAsync(flag, 0, sizeof(int), st);
       if (e != cudaSuccess) return e;
-      if (xdig && gauss_tcp_workspace(m, n, dtype, splits) <= xdig_bytes && !getenv("RCHOLQR_GAUSS_NO_PRESPLIT"))
-        e = launch_gauss_tcp(X, dtype, m, n, ldx, row_offset, k, seed, L.tc_tiles_k, L.tc_tiles_n, splits, trps, part,
-                             partc, flag, xdig, st);
-      else
+      e = cudaErrorNotSupported;
+      if (xdig && !getenv("RCHOLQR_GAUSS_NO_PRESPLIT"))    // pre-split digits (row chunks that fit the workspace)
+        e = launch_gauss_tcp(X, dtype, m, n, ldx, row_offset, k, seed, L.tc_tiles_k, L.tc_tiles_n, splits, part,
+                             partc, flag, xdig, xdig_bytes, st);
+      if (e == cudaErrorNotSupported)
         e = launch_gauss_tc(X, dtype, m, n, ldx, row_offset, k, seed, L.tc_tiles_k, L.tc_tiles_n, splits, trps, part,
                             partc, flag, st);
       if (e == cudaSuccess) guard = flag;                     // else: the DMMA kernel computes the sketch

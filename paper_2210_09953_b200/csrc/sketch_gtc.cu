@@ -504,7 +504,7 @@ template <typename TX>
 __global__ void __launch_bounds__(GP_THREADS, 1)
 sketch_gauss_tcp_kernel(const unsigned char* __restrict__ dig, const uint32_t* __restrict__ maxbits, int64_t m, int n,
                         int64_t row_offset, int k, uint64_t seed, int tiles_k, int tiles_n, int64_t rows_per_split,
-                        int stages_per_split, double* __restrict__ part, double* __restrict__ partc) {
+                        int stages_per_split, double* __restrict__ part, double* __restrict__ partc, int accumulate) {
   using C = GtCfg<TX>;
   using P = GpCfg<TX>;
   using F = GtFmt<TX>;
@@ -622,8 +622,8 @@ sketch_gauss_tcp_kernel(const unsigned char* __restrict__ dig, const uint32_t* _
             if (r < nrows) {
               const double val = ldexp(v[rr], ej - 44 - F::FB);
               const size_t o = (size_t)(r0 + r) * n + n0 + jj;
-              if (d == 0) { Ps[o] = val; Pc[o] = 0.0; }
-              else {
+              if (d == 0 && !accumulate) { Ps[o] = val; Pc[o] = 0.0; }
+              else {                                   // TwoSum into the running (sum, compensation)
                 const double a0 = Ps[o], sum = a0 + val, bb = sum - a0;
                 Pc[o] += (a0 - (sum - bb)) + (val - bb);
                 Ps[o] = sum;
@@ -680,7 +680,7 @@ sketch_gauss_tcp_kernel(const unsigned char* __restrict__ dig, const uint32_t* _
     }
     if (drainer) {
       while (next_drain <= ndrains) { drain(next_drain - 1); ++next_drain; }
-      if (ndrains == 0) {
+      if (ndrains == 0 && !accumulate) {
         const int jj = dq * 32 + lane;
         if (jj < ncols)
           for (int r = 0; r < nrows; ++r) {
@@ -708,7 +708,7 @@ size_t gauss_tcp_workspace(int64_t m, int n, int dtype, int splits) {
 template <typename TX>
 static cudaError_t launch_gtcp(const TX* X, int64_t m, int n, int64_t ldx, int64_t ro, int k, uint64_t seed,
                                int tiles_k, int tiles_n, int splits, int64_t rps, double* part, double* partc,
-                               int* overflow, void* ws, cudaStream_t st) {
+                               int* overflow, void* ws, int accumulate, cudaStream_t st) {
   constexpr int DX = GtFmt<TX>::DX;
   const int stages = (int)(rps / GT_KC);
   const int64_t units = (int64_t)splits * stages * tiles_n;
@@ -721,18 +721,41 @@ static cudaError_t launch_gtcp(const TX* X, int64_t m, int n, int64_t ldx, int64
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GpCfg<TX>::SMEM);
   if (e != cudaSuccess) return e;
   kern<<<tiles_k * tiles_n * splits, GP_THREADS, GpCfg<TX>::SMEM, st>>>(dig, maxbits, m, n, ro, k, seed, tiles_k,
-                                                                         tiles_n, rps, stages, part, partc);
+                                                                         tiles_n, rps, stages, part, partc, accumulate);
   return cudaGetLastError();
 }
 
+// Rows are processed in chunks whose digit workspace fits ws_bytes; every chunk after the first adds
+// into the per-split partials (TwoSum), so the result is the sketch of all m rows.
 cudaError_t launch_gauss_tcp(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
-                             uint64_t seed, int tiles_k, int tiles_n, int splits, int64_t rows_per_split,
-                             double* part, double* partc, int* overflow, void* ws, cudaStream_t st) {
-  if (dtype == RCHOLQR_F64)
-    return launch_gtcp((const double*)X, m, n, ldx, row_offset, k, seed, tiles_k, tiles_n, splits, rows_per_split,
-                       part, partc, overflow, ws, st);
-  return launch_gtcp((const float*)X, m, n, ldx, row_offset, k, seed, tiles_k, tiles_n, splits, rows_per_split, part,
-                     partc, overflow, ws, st);
+                             uint64_t seed, int tiles_k, int tiles_n, int splits, double* part, double* partc,
+                             int* overflow, void* ws, size_t ws_bytes, cudaStream_t st) {
+  const size_t es = dtype == RCHOLQR_F64 ? 8 : 4;
+  int64_t chunk = m;
+  while (chunk > GT_KC && gauss_tcp_workspace(chunk, n, dtype, splits) > ws_bytes) chunk = (chunk + 1) / 2;
+  if (gauss_tcp_workspace(chunk, n, dtype, splits) > ws_bytes) return cudaErrorNotSupported;
+  for (int64_t c0 = 0; c0 < m; c0 += chunk) {
+    const int64_t mc = std::min(chunk, m - c0);
+    const int64_t per = (mc + splits - 1) / splits;
+    const int64_t rps = std::max<int64_t>(GT_KC, ((per + GT_KC - 1) / GT_KC) * GT_KC);
+    const char* Xc = reinterpret_cast<const char*>(X) + (size_t)c0 * ldx * es;
+    cudaError_t e = dtype == RCHOLQR_F64
+                        ? launch_gtcp((const double*)Xc, mc, n, ldx, row_offset + c0, k, seed, tiles_k, tiles_n, splits,
+                                      rps, part, partc, overflow, ws, c0 > 0, st)
+                        : launch_gtcp((const float*)Xc, mc, n, ldx, row_offset + c0, k, seed, tiles_k, tiles_n, splits,
+                                      rps, part, partc, overflow, ws, c0 > 0, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+// chunk rows the plan sizes its workspace for (at most kXdigCapBytes)
+size_t gauss_tcp_chunk_workspace(int64_t m, int n, int dtype, int splits) {
+  size_t cap = kXdigCapBytes;
+  if (const char* e = getenv("RCHOLQR_XDIG_CAP_MB")) cap = (size_t)atoll(e) << 20;   // tests: force chunking
+  int64_t chunk = m;
+  while (chunk > GT_KC && gauss_tcp_workspace(chunk, n, dtype, splits) > cap) chunk = (chunk + 1) / 2;
+  return gauss_tcp_workspace(chunk, n, dtype, splits);
 }
 
 int gauss_tc_kt(int dtype) { return dtype == RCHOLQR_F64 ? GtFmt<double>::KT : GtFmt<float>::KT; }

@@ -131,6 +131,19 @@ def test_sketch_sparse_tc_matches_cuda_core(cuda, monkeypatch):
     assert _rel(a, b) <= 1e-13, _rel(a, b)
 
 
+@pytest.mark.parametrize("dt,n,k", [("f64", 256, 512), ("f32", 100, 200)])
+def test_sketch_gauss_chunked_presplit(cuda, monkeypatch, dt, n, k):
+    # tiny digit-workspace cap: the tcgen05 Gaussian sketch runs in many row chunks that add into
+    # the same per-split partials; the result must still match the oracle (and the unchunked run)
+    X = synth.make_X(40_001, n, 6.0, dt)
+    Po = oracle.sketch(X, k, row_offset=12345)
+    full = _np(_plan(n, k, dt).sketch(_t(X), row_offset=12345))
+    monkeypatch.setenv("RCHOLQR_XDIG_CAP_MB", "2")
+    chunked = _np(_plan(n, k, dt).sketch(_t(X), row_offset=12345))
+    assert _rel(chunked, Po) <= 1e-12, _rel(chunked, Po)
+    assert _rel(full, Po) <= 1e-12, _rel(full, Po)
+
+
 def test_sketch_ld_and_row_offset(cuda):
     X = synth.make_X(5000, 40, 3.0)
     wide = np.zeros((5000, 57))
