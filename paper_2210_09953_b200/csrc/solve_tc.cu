@@ -1,4 +1,4 @@
-// solve_tc.cu -- tall solve Q = X R^{-1} (Alg. 2 step 3) for fp32 X with n <= 64 on the
+// solve_tc.cu -- tall solve Q = X R^{-1} (Alg. 2 step 3) for fp32 X with n <= 128 on the
 // 5th-generation tensor core (tcgen05 kind::i8), the B200 form of the paper's dominant step
 // ("mainly determined by the computation of X R^{-1} ... m n^2 flops").
 //
@@ -19,11 +19,15 @@
 // tile initialises every level).  TMEM holds two 224-column level buffers, so the drain warps
 // (fp64 combine, fp32 Q stores) of one group overlap the MMAs of the next.
 //
+// W = R^{-1} is upper triangular, so column group g only needs rows l < 32 (g + 1): its digit
+// tile and its MMAs stop there (K_g = 32 (g + 1)).
+//
 // Roles (persistent CTAs, 18 warps): warp 0 lane 0 issues tcgen05.mma; warp 1 lane 0 stages the W
-// digits (cp.async.bulk) and the X tiles (one 2D TMA box of 128 rows x K+4 columns per tile);
-// warps 2..9 drain TMEM in two sets of four (set d drains level buffer d, one lane quadrant per
-// warp) and write Q through swizzled shared memory with TMA stores; warps 10..17 split X into
-// digit planes.
+// digits (cp.async.bulk) and, for n <= 64, the X tiles (one 2D TMA box of 128 rows x K+4 columns
+// per tile, two-stage ring); warps 2..9 drain TMEM in two sets of four (set d drains level buffer d,
+// one lane quadrant per warp) and write Q through swizzled shared memory with TMA stores; warps
+// 10..17 split X into digit planes (for 64 < n <= 128 they read X with plain loads: there is room
+// for only one digit stage and no raw ring).
 #include <cuda_runtime.h>
 #include <cmath>
 #include <cstdint>
@@ -41,19 +45,29 @@ constexpr int QT_DA = 6;        // X digits
 constexpr int QT_DB = 7;        // W digits
 constexpr int QT_LEV = 7;       // levels kept (a + b <= 6)
 constexpr int QT_NB = QT_DB * QT_G;             // stacked W digit rows of one group (224)
-constexpr int QT_KMAX = 64;
-constexpr int QT_DIG = 2, QT_RAW = 2;
 constexpr int QT_DWARPS = 8;    // digit warps 10..17
 constexpr int QT_RWARPS = 8;    // drain warps 2..9: two sets of four (one per TMEM level buffer)
 constexpr int QT_THREADS = 32 * (2 + QT_RWARPS + QT_DWARPS);
-constexpr int QT_A_TILE = QT_M * QT_KMAX;       // one X digit plane (128 x 64 B)
-constexpr int QT_RS_MAX = QT_KMAX + 4;          // raw X row pitch (floats): K + 4 -> conflict-free LDS.128
-constexpr int QT_RAW_STAGE = QT_M * QT_RS_MAX * 4;
-constexpr int QT_W_BYTES = 2 * QT_NB * QT_KMAX;  // two groups (n <= 64)
 constexpr int QT_QS_BYTES = QT_RWARPS * 32 * QT_G * 4;  // Q staging: one 32-row x 32-col fp32 tile per drain warp (128B-swizzled)
-constexpr size_t QT_SMEM = (size_t)QT_W_BYTES + (size_t)QT_DIG * QT_DA * QT_A_TILE + (size_t)QT_RAW * QT_RAW_STAGE + QT_QS_BYTES + 2048;
-static_assert(QT_SMEM <= 232448, "shared memory");
+constexpr int QT_KMAX_ALL = 128;
 static_assert(2 * QT_LEV * QT_G <= 512, "two TMEM level buffers");
+
+// byte offset of column group g's W digit tile (triangular: K_h = 32 (h + 1) rows of W per group)
+__host__ __device__ constexpr int qt_woff(int g) { return QT_NB * 32 * g * (g + 1) / 2; }
+
+template <int KMAX>
+struct QCfg {
+  static constexpr bool TMA_RAW = KMAX <= 64;     // raw X ring via TMA (else plain loads)
+  static constexpr int DIG = KMAX <= 64 ? 2 : 1;
+  static constexpr int RAW = TMA_RAW ? 2 : 0;
+  static constexpr int A_TILE = QT_M * KMAX;      // one X digit plane (128 x KMAX B)
+  static constexpr int RS = KMAX + 4;             // raw X row pitch (floats): K + 4 -> conflict-free LDS.128
+  static constexpr int RAW_STAGE = QT_M * RS * 4;
+  static constexpr int W_BYTES = qt_woff(KMAX / 32);
+  static constexpr size_t SMEM =
+      (size_t)W_BYTES + (size_t)DIG * QT_DA * A_TILE + (size_t)RAW * RAW_STAGE + QT_QS_BYTES + 2048;
+  static_assert(SMEM <= 232448, "shared memory");
+};
 
 // ---------------------------------------------------------------------------------------------
 // W digit prep: column scales e_j and the signed digit planes, laid out per group g as the B
@@ -65,14 +79,15 @@ __global__ void solve_tc_prep_kernel(const double* __restrict__ W, int n, int kp
   const int groups = (n + QT_G - 1) / QT_G;
   if (j >= groups * QT_G) return;
   const int g = j / QT_G, jj = j % QT_G;
-  int8_t* tile = wdig + (size_t)g * QT_NB * kpad;
+  const int kg = min(QT_G * (g + 1), kpad);          // rows l < kg of W (upper triangular)
+  int8_t* tile = wdig + qt_woff(g);
   double mx = 0.0;
   if (j < n)
     for (int l = 0; l < n; ++l) mx = fmax(mx, fabs(W[(size_t)l * n + j]));
   int e = 0;
   if (mx > 0.0) { frexp(mx, &e); }                     // mx < 2^e
   wexp[j] = e;
-  for (int l = 0; l < kpad; ++l) {
+  for (int l = 0; l < kg; ++l) {
     long long F = (j < n && l < n) ? llrint(ldexp(W[(size_t)l * n + j], 54 - e)) : 0;   // |F| <= 2^54
     int d[QT_DB];
     for (int b = QT_DB - 1; b >= 1; --b) {             // balanced base-256 digits, exact
@@ -86,16 +101,21 @@ __global__ void solve_tc_prep_kernel(const double* __restrict__ W, int n, int kp
 }
 
 // ---------------------------------------------------------------------------------------------
+template <int KMAX>
 __global__ void __launch_bounds__(QT_THREADS, 1)
 solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap qmap,
-                const int8_t* __restrict__ wdig, const int* __restrict__ wexp,
-                int64_t m, int n, int kpad, float* __restrict__ Q, int64_t ldq, const int* status, int dbg) {
+                const int8_t* __restrict__ wdig, const int* __restrict__ wexp, const float* __restrict__ X,
+                int64_t ldx, int64_t m, int n, int kpad, float* __restrict__ Q, int64_t ldq, const int* status,
+                int dbg) {
+  using Cf = QCfg<KMAX>;
+  constexpr int QT_DIG = Cf::DIG, QT_RAW = Cf::RAW > 0 ? Cf::RAW : 1, QT_A_TILE = Cf::A_TILE;
+  constexpr int QT_RS_MAX = Cf::RS, QT_RAW_STAGE = Cf::RAW_STAGE;
   if (*status) return;                                 // singular R: Q is not written
   extern __shared__ __align__(1024) unsigned char sm[];
   unsigned char* wsm = sm;                                                   // W digits, all groups
-  unsigned char* abase = sm + QT_W_BYTES;                                     // [DIG][DA][A_TILE]
-  float* raw_base = reinterpret_cast<float*>(abase + (size_t)QT_DIG * QT_DA * QT_A_TILE);   // [RAW][128][kpad]
-  unsigned char* qstage = reinterpret_cast<unsigned char*>(raw_base) + (size_t)QT_RAW * QT_RAW_STAGE;   // [4][32 rows][128 B]
+  unsigned char* abase = sm + Cf::W_BYTES;                                    // [DIG][DA][A_TILE]
+  float* raw_base = reinterpret_cast<float*>(abase + (size_t)QT_DIG * QT_DA * QT_A_TILE);   // [RAW][128][RS]
+  unsigned char* qstage = reinterpret_cast<unsigned char*>(raw_base) + (size_t)Cf::RAW * QT_RAW_STAGE;   // [8][32 rows][128 B]
   uint64_t* bars = reinterpret_cast<uint64_t*>(qstage + QT_QS_BYTES);
   uint64_t* dfull = bars;                   // [DIG] X digits of a tile ready
   uint64_t* dempty = dfull + QT_DIG;        // [DIG] tile fully drained (slot + row scales free)
@@ -113,7 +133,6 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
   const int my_tiles = blockIdx.x < ntiles ? (int)((ntiles - 1 - blockIdx.x) / gridDim.x + 1) : 0;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int lg_n = kpad / 16;                                                 // 16-column groups per row
-  const int ksteps = kpad / 32;
 
   if (tid == 0) {
     for (int s = 0; s < QT_DIG; ++s) { tc::mbar_init(&dfull[s], QT_DWARPS); tc::mbar_init(&dempty[s], QT_RWARPS); }
@@ -145,7 +164,8 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         if (lane == 0 && !(dbg & 1)) {
           const uint32_t sa = tc::smem_u32(abase + (size_t)s * QT_DA * QT_A_TILE);
-          const uint32_t sb = tc::smem_u32(wsm + (size_t)g * QT_NB * kpad);
+          const uint32_t sb = tc::smem_u32(wsm + qt_woff(g));
+          const int ksteps = min(g + 1, kpad / 32);           // W rows l < 32 (g + 1): upper triangular
           for (int ks = 0; ks < ksteps; ++ks) {
 #pragma unroll
             for (int a = 0; a < QT_DA; ++a) {
@@ -163,13 +183,13 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
   } else if (warp == 1) {
     // ---------------------------------------------------------------- loader (lane 0)
     if (lane == 0) {
-      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&xmap) : "memory");
-      const uint32_t wbytes = (uint32_t)(groups * QT_NB * kpad);
+      if (Cf::TMA_RAW) asm volatile("prefetch.tensormap [%0];\n" ::"l"(&xmap) : "memory");
+      const uint32_t wbytes = (uint32_t)qt_woff(groups);
       tc::mbar_arrive_tx(wbar, wbytes);
       tc::bulk_g2s(wsm, wdig, wbytes, wbar);
     }
     __syncwarp();
-    for (int tt = 0; tt < my_tiles; ++tt) {
+    for (int tt = 0; tt < (Cf::TMA_RAW ? my_tiles : 0); ++tt) {
       const int s = tt % QT_RAW;
       if (tt >= QT_RAW) tc::mbar_wait(&rempty[s], (uint32_t)(((tt / QT_RAW) - 1) & 1));
       if (lane == 0) {
@@ -264,8 +284,9 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
     for (int tt = 0; tt < my_tiles; ++tt) {
       const int s = tt % QT_DIG, sr = tt % QT_RAW;
       if (tt >= QT_DIG) tc::mbar_wait(&dempty[s], (uint32_t)(((tt / QT_DIG) - 1) & 1));
-      tc::mbar_wait(&rfull[sr], (uint32_t)((tt / QT_RAW) & 1));
+      if (Cf::TMA_RAW) tc::mbar_wait(&rfull[sr], (uint32_t)((tt / QT_RAW) & 1));
       const float* raw = raw_base + (size_t)sr * QT_M * QT_RS_MAX;
+      const int64_t trow0 = (blockIdx.x + (int64_t)tt * gridDim.x) * QT_M;
       unsigned char* at = abase + (size_t)s * QT_DA * QT_A_TILE;
       const int rs = kpad + 4, rpw = 32 / lg_n;            // raw row pitch; rows per warp pass
       for (int task = dt; task < ((dbg & 2) ? 0 : QT_M * lg_n); task += 32 * QT_DWARPS) {
@@ -275,10 +296,26 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
         const int w = task >> 5, l = task & 31;
         const int lg = l / rpw, i = w * rpw + (l % rpw);
         float x[16];
+        if constexpr (Cf::TMA_RAW) {
 #pragma unroll
-        for (int c = 0; c < 16; c += 4) {
-          const float4 f = *reinterpret_cast<const float4*>(raw + i * rs + lg * 16 + c);
-          x[c] = f.x; x[c + 1] = f.y; x[c + 2] = f.z; x[c + 3] = f.w;
+          for (int c = 0; c < 16; c += 4) {
+            const float4 f = *reinterpret_cast<const float4*>(raw + i * rs + lg * 16 + c);
+            x[c] = f.x; x[c + 1] = f.y; x[c + 2] = f.z; x[c + 3] = f.w;
+          }
+        } else {                                           // plain loads, zero outside X
+          const int64_t row = trow0 + i;
+          const float* xr = X + row * ldx + lg * 16;
+          const bool rok = row < m, full = rok && lg * 16 + 16 <= n;
+          if (full) {
+#pragma unroll
+            for (int c = 0; c < 16; c += 4) {
+              const float4 f = *reinterpret_cast<const float4*>(xr + c);
+              x[c] = f.x; x[c + 1] = f.y; x[c + 2] = f.z; x[c + 3] = f.w;
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 16; ++c) x[c] = (rok && lg * 16 + c < n) ? xr[c] : 0.0f;
+          }
         }
         uint32_t mx = 0u;
 #pragma unroll
@@ -314,7 +351,7 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       __syncwarp();
-      if (lane == 0) { tc::mbar_arrive(&dfull[s]); tc::mbar_arrive(&rempty[sr]); }
+      if (lane == 0) { tc::mbar_arrive(&dfull[s]); if (Cf::TMA_RAW) tc::mbar_arrive(&rempty[sr]); }
     }
   }
   if (warp >= 2 && warp < 2 + QT_RWARPS && lane == 0) tc::bulk_wait0();   // Q stores complete before exit
@@ -323,14 +360,19 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
-bool solve_tc_applicable(int dtype, int n) { return dtype == RCHOLQR_F32 && n >= 1 && n <= QT_KMAX && !getenv("RCHOLQR_SOLVE_DMMA"); }
+// n <= 64 by default; 64 < n <= 128 (plain-load producers, one digit stage) is correct but not yet
+// faster than the DMMA substitution on B200 (C2: 0.80 vs 0.69 ms), so it is opt-in.
+bool solve_tc_applicable(int dtype, int n) {
+  if (dtype != RCHOLQR_F32 || n < 1 || getenv("RCHOLQR_SOLVE_DMMA")) return false;
+  return n <= 64 || (n <= QT_KMAX_ALL && getenv("RCHOLQR_SOLVE_TC128"));
+}
 
 bool solve_tc_supported(const void* X, int64_t m, int64_t ldx, const void* Q, int64_t ldq) {
   return m <= INT32_MAX && ((uintptr_t)X % 16) == 0 && ((size_t)ldx * 4) % 16 == 0 &&   // TMA base / pitch
          ((uintptr_t)Q % 16) == 0 && ((size_t)ldq * 4) % 16 == 0;
 }
 
-size_t solve_tc_workspace() { return (size_t)2 * QT_NB * QT_KMAX + sizeof(int) * 2 * QT_G; }
+size_t solve_tc_workspace() { return (size_t)qt_woff(QT_KMAX_ALL / QT_G) + sizeof(int) * QT_KMAX_ALL; }
 
 using EncodeTiledFn2 = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
@@ -350,17 +392,17 @@ cudaError_t launch_solve_tc(const double* Winv, int n, const float* X, int64_t m
     return reinterpret_cast<EncodeTiledFn2>(p);
   }();
   if (!enc) return cudaErrorNotSupported;
-  const int kpad = n <= 32 ? 32 : 64;
+  const int kpad = (n + 31) / 32 * 32;
   const int groups = (n + QT_G - 1) / QT_G;
   int8_t* wdig = reinterpret_cast<int8_t*>(ws);
-  int* wexp = reinterpret_cast<int*>(wdig + (size_t)2 * QT_NB * QT_KMAX);
+  int* wexp = reinterpret_cast<int*>(wdig + qt_woff(QT_KMAX_ALL / QT_G));
   solve_tc_prep_kernel<<<1, groups * QT_G, 0, st>>>(Winv, n, kpad, wdig, wexp, status);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   CUtensorMap map;
   const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)m};
   const cuuint64_t strides[1] = {(cuuint64_t)ldx * 4};
-  const cuuint32_t box[2] = {(cuuint32_t)kpad + 4, QT_M}, estr[2] = {1, 1};   // + 4 zero-filled pad columns
+  const cuuint32_t box[2] = {(cuuint32_t)std::min(kpad, 64) + 4, QT_M}, estr[2] = {1, 1};   // + 4 zero-filled pad columns
   if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides, box, estr,
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
@@ -372,19 +414,16 @@ cudaError_t launch_solve_tc(const double* Winv, int n, const float* X, int64_t m
   if (enc(&qmapd, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Q, qdims, qstrides, qbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
-  e = cudaFuncSetAttribute(solve_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)QT_SMEM);
-  if (e != cudaSuccess) return e;
   const int64_t ntiles = (m + QT_M - 1) / QT_M;
   const int grid = (int)std::min<int64_t>(ntiles, sms);
   static const int dbg = getenv("RCHOLQR_QTC_DEBUG") ? atoi(getenv("RCHOLQR_QTC_DEBUG")) : 0;   // ablations only
-  if (getenv("RCHOLQR_DEBUG")) {
-    cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, solve_tc_kernel);
-    fprintf(stderr, "solve_tc: regs %d maxthreads %d smem_dyn %zu static %zu threads %d\n", fa.numRegs,
-            fa.maxThreadsPerBlock, (size_t)QT_SMEM, fa.sharedSizeBytes, QT_THREADS);
-  }
-  solve_tc_kernel<<<grid, QT_THREADS, QT_SMEM, st>>>(map, qmapd, wdig, wexp, m, n, kpad, Q, ldq, status, dbg);
-  return cudaGetLastError();
+  auto go = [&](auto kern, size_t smem) -> cudaError_t {
+    cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e2 != cudaSuccess) return e2;
+    kern<<<grid, QT_THREADS, smem, st>>>(map, qmapd, wdig, wexp, X, ldx, m, n, kpad, Q, ldq, status, dbg);
+    return cudaGetLastError();
+  };
+  return kpad <= 64 ? go(solve_tc_kernel<64>, QCfg<64>::SMEM) : go(solve_tc_kernel<128>, QCfg<128>::SMEM);
 }
 
 }  // namespace rcq

@@ -229,11 +229,17 @@ SOLVE_TC_CASES = [
     (1, 64, 1, None),            # single row
     (40_000, 64, 4, 68),         # strided rows (TMA pitch)
     (20_000, 61, 3, 63),         # unaligned pitch -> CUDA-core path
+    (100_003, 100, 5, None),     # C2 shape: 64 < n <= 128 (plain-load producers, 4 triangular groups)
+    (5_000, 128, 3, None),       # four full groups
+    (3_001, 97, 4, 104),         # strided, ragged last group
+    (1, 100, 1, None),           # single row
 ]
 
 
 @pytest.mark.parametrize("m,n,c,ldx", SOLVE_TC_CASES)
-def test_tri_solve_tc_parity(cuda, m, n, c, ldx):
+def test_tri_solve_tc_parity(cuda, monkeypatch, m, n, c, ldx):
+    if n > 64:
+        monkeypatch.setenv("RCHOLQR_SOLVE_TC128", "1")   # opt-in path for 64 < n <= 128
     X = synth.make_X(max(m, n), n, c, "f32")
     Ro, _, _ = oracle.householder(oracle.sketch(X, 2 * n))
     X = X[:m]
