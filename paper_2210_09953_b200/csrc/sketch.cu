@@ -142,7 +142,7 @@ sketch_gauss_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int
             const int qq = cc / KC, ii = cc % KC;
             const int rb = r0 + 4 * qq;
             float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (i0 + ii < i_end && rb < k) z = gauss4(seed, (uint64_t)(row_offset + i0 + ii), (uint32_t)(rb >> 2));
+            if (i0 + ii < i_end && rb < k) z = gauss4_x2(seed, (uint64_t)(row_offset + i0 + ii), (uint32_t)(rb >> 2));
             double* Tc = T + (4 * qq) * C::TS_LD + ii;
             Tc[0 * C::TS_LD] = (rb + 0 < k) ? (double)z.x : 0.0;
             Tc[1 * C::TS_LD] = (rb + 1 < k) ? (double)z.y : 0.0;
@@ -443,7 +443,7 @@ __global__ void theta_gauss_export_kernel(uint64_t seed, int k, int64_t row_offs
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < m * nq; c += (int64_t)gridDim.x * blockDim.x) {
     const int64_t i = c % m;
     const int q = (int)(c / m);
-    const float4 z = gauss4(seed, (uint64_t)(row_offset + i), (uint32_t)q);
+    const float4 z = gauss4_x2(seed, (uint64_t)(row_offset + i), (uint32_t)q);
     const float zz[4] = {z.x, z.y, z.z, z.w};
     for (int u = 0; u < 4 && 4 * q + u < k; ++u) Z[(int64_t)(4 * q + u) * m + i] = zz[u];
   }

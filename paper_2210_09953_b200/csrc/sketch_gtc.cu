@@ -264,7 +264,7 @@ sketch_gauss_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int 
         float z[4][4];
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          const float4 g = gauss4(seed, gi + kk, qg);
+          const float4 g = gauss4_x2(seed, gi + kk, qg);
           z[kk][0] = g.x; z[kk][1] = g.y; z[kk][2] = g.z; z[kk][3] = g.w;
         }
 #pragma unroll
@@ -654,7 +654,7 @@ sketch_gauss_tcp_kernel(const unsigned char* __restrict__ dig, const uint32_t* _
         float z[4][4];
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          const float4 g = gauss4(seed, gi + kk, qg);
+          const float4 g = gauss4_x2(seed, gi + kk, qg);
           z[kk][0] = g.x; z[kk][1] = g.y; z[kk][2] = g.z; z[kk][3] = g.w;
         }
 #pragma unroll

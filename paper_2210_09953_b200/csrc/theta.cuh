@@ -103,6 +103,75 @@ __device__ __forceinline__ float4 gauss4(uint64_t seed, uint64_t i, uint32_t q) 
   return z;
 }
 
+// The same four draws with the two Box-Muller pairs evaluated in packed FP32x2 arithmetic (sm_100
+// FADD2/FMUL2/FFMA2): every lane of a packed op is one correctly rounded IEEE op, applied in the
+// same order as above, so the result is bit-identical to gauss4 (the exported-Theta tests check it)
+// while the polynomial work costs half the instructions.  Lane 0 = pair (w.x, w.y), lane 1 =
+// pair (w.z, w.w); subtraction a - b is written a + (-b) (identical rounding).
+__device__ __forceinline__ float2 f2(float a) { return make_float2(a, a); }
+
+__device__ __forceinline__ float2 ln_unit_x2(float2 a) {
+  const uint32_t b0 = __float_as_uint(a.x), b1 = __float_as_uint(a.y);
+  int e0 = (int)(b0 >> 23) - 127, e1 = (int)(b1 >> 23) - 127;
+  float f0 = __uint_as_float((b0 & 0x007FFFFFu) | 0x3F800000u);
+  float f1 = __uint_as_float((b1 & 0x007FFFFFu) | 0x3F800000u);
+  if (f0 > 0x1.6a09e6p+0f) { f0 = __fmul_rn(f0, 0.5f); e0 += 1; }
+  if (f1 > 0x1.6a09e6p+0f) { f1 = __fmul_rn(f1, 0.5f); e1 += 1; }
+  const float2 s = __fadd2_rn(make_float2(f0, f1), f2(-1.0f));
+  float2 p = f2(-0x1.31335cp-4f);
+  p = __ffma2_rn(p, s, f2(0x1.064786p-3f));
+  p = __ffma2_rn(p, s, f2(-0x1.0fb036p-3f));
+  p = __ffma2_rn(p, s, f2(0x1.22cf10p-3f));
+  p = __ffma2_rn(p, s, f2(-0x1.5423b0p-3f));
+  p = __ffma2_rn(p, s, f2(0x1.999e86p-3f));
+  p = __ffma2_rn(p, s, f2(-0x1.000424p-2f));
+  p = __ffma2_rn(p, s, f2(0x1.55555ep-2f));
+  p = __ffma2_rn(p, s, f2(-0x1.fffff8p-2f));
+  p = __ffma2_rn(p, s, f2(1.0f));
+  const float2 lnf = __fmul2_rn(s, p);
+  const float2 ef = __fadd2_rn(make_float2(__int_as_float(0x4B400000 + e0), __int_as_float(0x4B400000 + e1)),
+                               f2(-12582912.0f));
+  return __ffma2_rn(ef, f2(0x1.62e4p-1f), __ffma2_rn(ef, f2(0x1.7f7d1cp-20f), lnf));
+}
+
+__device__ __forceinline__ void sincos_2pi_j_x2(uint32_t j0, uint32_t j1, float2& so, float2& co) {
+  const uint32_t n0 = (j0 + (1u << 20)) >> 21, n1 = (j1 + (1u << 20)) >> 21;
+  const int r0 = (int)j0 - (int)(n0 << 21), r1 = (int)j1 - (int)(n1 << 21);
+  const float2 ri = __fadd2_rn(make_float2(__int_as_float(0x4B400000 + r0), __int_as_float(0x4B400000 + r1)),
+                               f2(-12582912.0f));
+  const float2 r = __fmul2_rn(ri, f2(0x1p-21f));
+  const float2 r2 = __fmul2_rn(r, r);
+  float2 ps = f2(0x1.507834p-13f);
+  ps = __ffma2_rn(ps, r2, f2(-0x1.32d2ccp-8f));
+  ps = __ffma2_rn(ps, r2, f2(0x1.466bc6p-4f));
+  ps = __ffma2_rn(ps, r2, f2(-0x1.4abbcep-1f));
+  ps = __ffma2_rn(ps, r2, f2(0x1.921fb6p+0f));
+  const float2 s = __fmul2_rn(ps, r);
+  float2 pc = f2(-0x1.a6d1f2p-16f);
+  pc = __ffma2_rn(pc, r2, f2(0x1.e1f506p-11f));
+  pc = __ffma2_rn(pc, r2, f2(-0x1.55d3c8p-6f));
+  pc = __ffma2_rn(pc, r2, f2(0x1.03c1f0p-2f));
+  pc = __ffma2_rn(pc, r2, f2(-0x1.3bd3ccp+0f));
+  const float2 c = __ffma2_rn(pc, r2, f2(1.0f));
+  const uint32_t q0 = n0 & 3u, q1 = n1 & 3u;
+  const float sa0 = (q0 & 1u) ? c.x : s.x, ca0 = (q0 & 1u) ? s.x : c.x;
+  const float sa1 = (q1 & 1u) ? c.y : s.y, ca1 = (q1 & 1u) ? s.y : c.y;
+  so = make_float2((q0 >= 2u) ? -sa0 : sa0, (q1 >= 2u) ? -sa1 : sa1);
+  co = make_float2((q0 == 1u || q0 == 2u) ? -ca0 : ca0, (q1 == 1u || q1 == 2u) ? -ca1 : ca1);
+}
+
+__device__ __forceinline__ float4 gauss4_x2(uint64_t seed, uint64_t i, uint32_t q) {
+  const uint4 w = philox_at(seed, i, q, kDomainGauss);
+  const float2 ua = __fadd2_rn(f2(2.0f), make_float2(-__uint_as_float(0x3F800000u | (w.x >> 9)),
+                                                      -__uint_as_float(0x3F800000u | (w.z >> 9))));
+  const float2 m2 = __fmul2_rn(f2(-2.0f), ln_unit_x2(ua));
+  const float2 rho = make_float2(__fsqrt_rn(m2.x), __fsqrt_rn(m2.y));
+  float2 sn, cs;
+  sincos_2pi_j_x2(w.y >> 9, w.w >> 9, sn, cs);
+  const float2 zc = __fmul2_rn(rho, cs), zs = __fmul2_rn(rho, sn);
+  return make_float4(zc.x, zs.x, zc.y, zs.y);
+}
+
 // Sparse-sign column (A3): half-word t of Philox(i, t/8, domain 2) selects row t*beta +
 // ((h & 0x7FFF) * beta >> 15) inside block t and sign (h >> 15 ? -1 : +1).
 __device__ __forceinline__ uint32_t sparse_halfword(const uint4& w, int t) {
