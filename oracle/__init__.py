@@ -77,6 +77,13 @@ def _L():
             lib.oracle_factor.argtypes = [P, I32, I64, I32, I64, I64, I32, I32, I32, U64, P, I64, P, P, P]
             lib.oracle_factor.restype = I32
             lib.oracle_num_threads.restype = I32
+            lib.oracle_gram.argtypes = [P, I32, I64, I32, I64, P]
+            lib.oracle_gram.restype = I32
+            lib.oracle_cholesky.argtypes = [P, I32, P]
+            lib.oracle_cholesky.restype = I32
+            lib.oracle_trmm_upper.argtypes = [P, P, I32, P]
+            lib.oracle_factor2.argtypes = [P, I32, I64, I32, I64, I64, I32, I32, I32, U64, P, I64, P, P, P]
+            lib.oracle_factor2.restype = I32
             lib.oracle_sketch_entry.argtypes = [P, I64, I64, I32, I32, I32, U64, I32]
             lib.oracle_sketch_entry.restype = ctypes.c_double
             _lib = lib
@@ -226,6 +233,52 @@ def factor(X: np.ndarray, k: int, sketch: int = GAUSSIAN, zeta: int = 8, seed: i
     if st != OK:
         raise OracleError(st, "factor")
     return {"Q": Q, "R": R, "P": P, "S": S}
+
+
+def gram(Q: np.ndarray) -> np.ndarray:
+    """A = Q^T Q, compensated (Alg. 3 step 2)."""
+    Q = np.ascontiguousarray(Q)
+    m, n = Q.shape
+    A = np.empty((n, n), dtype=np.float64)
+    st = _L().oracle_gram(_ptr(Q), _dtype_code(Q), m, n, n, _ptr(A))
+    if st != OK:
+        raise OracleError(st, "gram")
+    return A
+
+
+def cholesky(A: np.ndarray):
+    """R' upper triangular with A = R'^T R' (Alg. 3 step 3); returns (R', status)."""
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    n = A.shape[0]
+    Rp = np.empty((n, n), dtype=np.float64)
+    st = _L().oracle_cholesky(_ptr(A), n, _ptr(Rp))
+    if st not in (OK, E_SINGULAR):
+        raise OracleError(st, "cholesky")
+    return Rp, st
+
+
+def trmm_upper(U: np.ndarray, V: np.ndarray) -> np.ndarray:
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    V = np.ascontiguousarray(V, dtype=np.float64)
+    out = np.empty_like(U)
+    _L().oracle_trmm_upper(_ptr(U), _ptr(V), U.shape[0], _ptr(out))
+    return out
+
+
+def factor2(X: np.ndarray, k: int, sketch: int = GAUSSIAN, zeta: int = 8, seed: int = 0,
+            row_offset: int = 0) -> dict:
+    """Whole Algorithm 3 (RCholeskyQR2): dict(Q, R, Q1, Rp) with Q = Q1 Rp^{-1}."""
+    X = np.ascontiguousarray(X)
+    m, n = X.shape
+    Q = np.empty_like(X)
+    Q1 = np.empty_like(X)
+    R = np.empty((n, n), dtype=np.float64)
+    Rp = np.empty((n, n), dtype=np.float64)
+    st = _L().oracle_factor2(_ptr(X), _dtype_code(X), m, n, n, row_offset, k, sketch, zeta, seed,
+                             _ptr(Q), n, _ptr(R), _ptr(Q1), _ptr(Rp))
+    if st != OK:
+        raise OracleError(st, "factor2")
+    return {"Q": Q, "R": R, "Q1": Q1, "Rp": Rp}
 
 
 # ---------------------------------------------------------------- metrics (PAPER.md:773, 797)

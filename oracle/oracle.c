@@ -7,7 +7,7 @@
  * (paper_2210_09953_b200/) never imports, links or executes anything under oracle/, and
  * this file shares no code, header, table or constant generator with it.
  *
- * What it computes (alg:RCQR):
+ * What it computes (alg:RCQR; and alg:RCQR2, below):
  *     1. P <- Theta X   oracle_sketch
  *     2. [R, S] <- QR(P)   oracle_householder  (Householder)
  *     3. Q <- X R^{-1}   oracle_forward_subst (forward substitution,
@@ -423,6 +423,100 @@ int oracle_factor(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64
     if (st == OR_OK) st = oracle_householder(P, k, n, R, S_out);
     if (st == OR_OK) st = oracle_forward_subst(X, dtype, m, n, ldx, R, Q, ldq);
     if (!P_out) free(P);
+    return st;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Algorithm 3, RCholeskyQR2 (alg:RCQR2):
+ *   1. [Q, S, R] <- RCholeskyQR(X, Theta)          (oracle_factor)
+ *   2. A <- Q^T Q                                   (oracle_gram)
+ *   3. R' <- chol(A), R <- R' R                     (oracle_cholesky, oracle_trmm_upper)
+ *   4. Q <- Q R'^{-1}                               (oracle_forward_subst with R')
+ * Implicit form: return Q (step 1) and R' instead of step 4's product.
+ * ---------------------------------------------------------------------------------------- */
+
+/* A = Q^T Q (n x n, both triangles), each entry a compensated Dot2 sum over the rows in fixed
+ * 65536-row blocks whose partials are added in block order (same accuracy policy as the sketch,
+ * reading A15: "low-dimensional operations" in higher precision). */
+int oracle_gram(const void* Q, int dtype, int64_t m, int n, int64_t ldq, double* A) {
+    if (!A || n < 1 || ldq < n || m < 0 || (m > 0 && !Q)) return OR_E_INVALID;
+    int64_t nb = (m + OR_SKETCH_BLOCK - 1) / OR_SKETCH_BLOCK;
+    if (nb == 0) nb = 1;
+    size_t nn = (size_t)n * n;
+    double* part = (double*)calloc((size_t)nb * nn * 2, sizeof(double));
+    if (!part) return OR_E_NOMEM;
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t b = 0; b < nb; ++b) {
+        double* ps = part + (size_t)b * nn * 2;
+        double* pc = ps + nn;
+        int64_t i0 = b * OR_SKETCH_BLOCK, i1 = i0 + OR_SKETCH_BLOCK < m ? i0 + OR_SKETCH_BLOCK : m;
+        for (int64_t r = i0; r < i1; ++r)
+            for (int i = 0; i < n; ++i) {
+                double qi = load_x(Q, dtype, r * ldq + i);
+                for (int j = i; j < n; ++j)
+                    dot2_add(&ps[(size_t)i * n + j], &pc[(size_t)i * n + j], qi, load_x(Q, dtype, r * ldq + j));
+            }
+    }
+    for (int i = 0; i < n; ++i)
+        for (int j = i; j < n; ++j) {
+            double s = 0.0, c = 0.0;
+            for (int64_t b = 0; b < nb; ++b) {
+                sum2_add(&s, &c, part[(size_t)b * nn * 2 + (size_t)i * n + j]);
+                c += part[(size_t)b * nn * 2 + nn + (size_t)i * n + j];
+            }
+            A[(size_t)i * n + j] = A[(size_t)j * n + i] = s + c;
+        }
+    free(part);
+    return OR_OK;
+}
+
+/* R' upper triangular with A = R'^T R' (textbook Cholesky, row by row, "chol"):
+ *   r_ii = sqrt(a_ii - sum_{l<i} r_li^2),  r_ij = (a_ij - sum_{l<i} r_li r_lj) / r_ii  (j > i).
+ * A non-positive or non-finite pivot returns OR_E_SINGULAR (A not numerically positive definite). */
+int oracle_cholesky(const double* A, int n, double* Rp) {
+    if (!A || !Rp || n < 1) return OR_E_INVALID;
+    for (size_t c = 0; c < (size_t)n * n; ++c) Rp[c] = 0.0;
+    for (int i = 0; i < n; ++i) {
+        double d = A[(size_t)i * n + i];
+        for (int l = 0; l < i; ++l) d -= Rp[(size_t)l * n + i] * Rp[(size_t)l * n + i];
+        if (!(d > 0.0) || !isfinite(d)) return OR_E_SINGULAR;
+        double rii = sqrt(d);
+        Rp[(size_t)i * n + i] = rii;
+        for (int j = i + 1; j < n; ++j) {
+            double s = A[(size_t)i * n + j];
+            for (int l = 0; l < i; ++l) s -= Rp[(size_t)l * n + i] * Rp[(size_t)l * n + j];
+            Rp[(size_t)i * n + j] = s / rii;
+        }
+    }
+    return OR_OK;
+}
+
+/* out = U V for upper triangular U, V (n x n): out_ij = sum_{l=i..j} u_il v_lj. */
+void oracle_trmm_upper(const double* U, const double* V, int n, double* out) {
+    for (int i = 0; i < n; ++i)
+        for (int j = 0; j < n; ++j) {
+            double s = 0.0;
+            for (int l = i; l <= j; ++l) s += U[(size_t)i * n + l] * V[(size_t)l * n + j];
+            out[(size_t)i * n + j] = j >= i ? s : 0.0;
+        }
+}
+
+/* Whole Algorithm 3.  Q1 (RCholeskyQR's Q, same dtype as X) and R' (n x n) are outputs too
+ * (the implicit-Q form of PAPER.md:206); Q = Q1 R'^{-1} (explicit form), R = R' R1. */
+int oracle_factor2(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset,
+                   int k, int sketch, int zeta, uint64_t seed, void* Q, int64_t ldq, double* R,
+                   void* Q1, double* Rp) {
+    if (!Q1 || !Rp || !R || !Q) return OR_E_INVALID;
+    double* R1 = (double*)malloc(sizeof(double) * (size_t)n * n);
+    double* A = (double*)malloc(sizeof(double) * (size_t)n * n);
+    if (!R1 || !A) { free(R1); free(A); return OR_E_NOMEM; }
+    int st = oracle_factor(X, dtype, m, n, ldx, row_offset, k, sketch, zeta, seed, Q1, n, R1, NULL, NULL);
+    if (st == OR_OK) st = oracle_gram(Q1, dtype, m, n, n, A);
+    if (st == OR_OK) st = oracle_cholesky(A, n, Rp);
+    if (st == OR_OK) oracle_trmm_upper(Rp, R1, n, R);
+    if (st == OR_OK) st = oracle_forward_subst(Q1, dtype, m, n, n, Rp, Q, ldq);
+    free(R1);
+    free(A);
     return st;
 }
 
