@@ -108,16 +108,18 @@ def _workload(cfg_name: str, ws: int, rank: int):
     return cfg, m_local, m_global, ro, scaling
 
 
-def _cpu_sample_rate(X_dev, cfg, target_s: float):
+def _cpu_sample_rate(X_dev, cfg, target_s: float, algo: str = "rcholqr"):
     """Time the oracle (as it stands, all host cores) on a bounded leading sample of X."""
     import oracle
     so = oracle.GAUSSIAN if cfg["sketch"] == "gaussian" else oracle.SPARSE_SIGN
+    run = (lambda A: oracle.factor2(A, cfg["k"], sketch=so, zeta=cfg["nnz"])) if algo == "rcholqr2" else \
+        (lambda A: oracle.factor(A, cfg["k"], sketch=so, zeta=cfg["nnz"], want_S=False))
     m = X_dev.shape[0]
     rows = min(m, 4096)
     while True:
         Xs = X_dev[:rows].cpu().numpy()
         t0 = time.perf_counter()
-        oracle.factor(Xs, cfg["k"], sketch=so, zeta=cfg["nnz"], want_S=False)
+        run(Xs)
         dt = time.perf_counter() - t0
         if dt >= target_s * 0.5 or rows >= m:
             return rows, dt, oracle.num_threads()
@@ -197,8 +199,13 @@ def run(args):
     R = torch.empty((n, n), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream()
 
+    Rp = torch.empty((n, n), dtype=torch.float64, device=dev)
+
     def step():
-        plan.factor(X, row_offset=ro, Q=Q, R=R, stream=stream, sync=False)
+        if args.algo == "rcholqr2":   # Alg. 3: synchronous (status read inside the call)
+            plan.factor2(X, row_offset=ro, Q=Q, R=R, Rprime=Rp, stream=stream)
+        else:
+            plan.factor(X, row_offset=ro, Q=Q, R=R, stream=stream, sync=False)
 
     def barrier():
         if ws > 1:
@@ -242,7 +249,7 @@ def run(args):
 
     # ---- end-to-end through the public API with host buffers (H2D + D2H inside the timed region)
     e2e = None
-    if not args.no_e2e:
+    if not args.no_e2e and args.algo == "rcholqr":
         Xh = X.cpu().pin_memory()
         Qh = torch.empty_like(Xh).pin_memory()
         Rh = torch.empty((n, n), dtype=torch.float64).pin_memory()
@@ -332,11 +339,24 @@ def run(args):
             "gpu_launches": plan.launches_per_factor(m_local) * args.steps,
             "clocks": clk.summary(), "e2e": e2e}
 
+    if args.algo == "rcholqr2":
+        # Alg. 3 = Alg. 2 + Gram (reads Q1) + Cholesky + second solve (reads Q1, writes Q): 6 passes
+        # over an m x n matrix and 2 m n^2 (solves) + m n^2 (Gram, both triangles) fp64 flops
+        t_hbm2 = 6.0 * m_local * n * s_x / (hbm * 1e9)
+        t_flop2 = 3.0 * m_local * n * n / (DMMA_PEAK_TFLOPS * 1e12)
+        line["metric"] = "RandCholQR2 factor throughput (GB/s of X)"
+        line["config"]["algo"] = "rcholqr2 (Alg. 3, explicit Q)"
+        line["northstar_roofline"] = {"t_hbm_ms": t_hbm2 * 1e3, "t_fp64_ms": t_flop2 * 1e3,
+                                      "roofline_ms": max(t_hbm2, t_flop2) * 1e3,
+                                      "frac": max(t_hbm2, t_flop2) * 1e3 / ms,
+                                      "note": "Alg. 3 accounting: 6 passes over m x n, 3 m n^2 fp64 flops"}
+        line["gpu_launches"] = (plan.launches_per_factor(m_local) + 4 + 2) * args.steps
+        line["e2e"] = None   # the host-buffer entry point is Alg. 2's
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        rows, dt_s, cores = _cpu_sample_rate(X, cfg, args.cpu_seconds)
+        rows, dt_s, cores = _cpu_sample_rate(X, cfg, args.cpu_seconds, args.algo)
         line["cpu_baseline"] = {"value": rows * n * s_x / dt_s / 1e9, "unit": "GB/s", "cores": cores,
                                 "kind": "oracle", "seconds": dt_s,
-                                "sample": f"oracle.factor on the leading {rows} rows of the same X"}
+                                "sample": f"oracle.{'factor2' if args.algo == 'rcholqr2' else 'factor'} on the leading {rows} rows of the same X"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     plan.close()
@@ -357,6 +377,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--algo", default="rcholqr", choices=["rcholqr", "rcholqr2"],
+                    help="Alg. 2 (default, the north star) or Alg. 3 RCholeskyQR2 (orthonormal Q)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -104,6 +104,21 @@ rcholqr_status rcholqr_factor_host(rcholqr_plan plan, const void* X_host, int64_
                                    int64_t row_offset, int64_t ldx, void* Q_host, int64_t ldq,
                                    double* R_host, double* S_host, void* stream);
 
+/* RCholeskyQR2 (Alg. 3, alg:RCQR2): RCholeskyQR (Alg. 2) followed by one
+ * CholeskyQR pass, A = Q1^T Q1 (all-reduced over the communicator), R' = chol(A), R = R' R1,
+ * Q = Q1 R'^{-1} -- an orthonormal Q factor (to O(n u)) and the QR factor R of X.
+ *   X, m_local, row_offset, ldx, Q, ldq, stream: as for rcholqr_factor.
+ *   R        [device] n x n fp64 output: R' R1 (upper triangular, positive diagonal).
+ *   Rprime   [device] n x n fp64 output or NULL: R' (A = R'^T R').
+ *   implicit 0: Q receives the explicit orthonormal factor Q1 R'^{-1} (a plan-owned m_local x n
+ *              buffer holds Q1); nonzero: Q receives Q1 and Rprime (then required) R' -- the
+ *              implicit form of PAPER.md:206 (products with Q as (Y Q1) R'^{-1}, Q1 (R'^{-1} Y)).
+ * Status: as rcholqr_factor; E_SINGULAR also if A is not numerically positive definite.
+ * SYNCHRONOUS.  With a communicator every rank must call this (collective; two all-reduces). */
+rcholqr_status rcholqr_factor2(rcholqr_plan plan, const void* X, int64_t m_local, int64_t row_offset,
+                               int64_t ldx, void* Q, int64_t ldq, double* R, double* Rprime, int32_t implicit,
+                               void* stream);
+
 /* ---- step-level entry points (same kernels as rcholqr_factor; used by the parity tests) ---- */
 
 /* Step 1 (+ the all-reduce when the plan has a communicator): P = Theta X, k x n fp64 row-major

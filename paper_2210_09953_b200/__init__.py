@@ -34,7 +34,7 @@ SYMBOLS = ["rcholqr_create", "rcholqr_destroy", "rcholqr_factor", "rcholqr_facto
            "rcholqr_query_status", "rcholqr_factor_host", "rcholqr_sketch", "rcholqr_small_qr",
            "rcholqr_tri_solve", "rcholqr_theta_export", "rcholqr_comm_unique_id",
            "rcholqr_comm_create", "rcholqr_comm_destroy", "rcholqr_strerror", "rcholqr_version",
-           "rcholqr_launches_per_factor", "rcholqr_set_timing", "rcholqr_last_timings"]
+           "rcholqr_launches_per_factor", "rcholqr_set_timing", "rcholqr_last_timings", "rcholqr_factor2"]
 
 
 class _Desc(ctypes.Structure):
@@ -71,6 +71,7 @@ def load_library():
             "rcholqr_factor_async": ([V, V, I64, I64, I64, V, I64, V, V, V], I32),
             "rcholqr_query_status": ([V, V], I32),
             "rcholqr_factor_host": ([V, V, I64, I64, I64, V, I64, V, V, V], I32),
+            "rcholqr_factor2": ([V, V, I64, I64, I64, V, I64, V, V, I32, V], I32),
             "rcholqr_sketch": ([V, V, I64, I64, I64, V, V], I32),
             "rcholqr_small_qr": ([V, V, V, V, V], I32),
             "rcholqr_tri_solve": ([V, V, I64, I64, V, V, I64, V], I32),
@@ -189,6 +190,21 @@ class RCholQR:
                 _ptr(S), _stream_ptr(stream))
         _check(st, "rcholqr_factor")
         return Q, R, S
+
+    def factor2(self, X, row_offset: int = 0, Q=None, R=None, Rprime=None, implicit: bool = False,
+                stream=None) -> Tuple:
+        """RCholeskyQR2 (Alg. 3): Q (orthonormal; with ``implicit`` RCholeskyQR's Q1), R, R'."""
+        torch = _torch()
+        m, ldx = self._check_x(X)
+        Q = torch.empty((m, self.n), dtype=self.dtype, device=X.device) if Q is None else Q
+        R = torch.empty((self.n, self.n), dtype=torch.float64, device=X.device) if R is None else R
+        if Rprime is None:
+            Rprime = torch.empty((self.n, self.n), dtype=torch.float64, device=X.device)
+        st = self._lib.rcholqr_factor2(self._h, _ptr(X), m, row_offset, ldx, _ptr(Q),
+                                       Q.stride(0) if m > 1 else self.n, _ptr(R), _ptr(Rprime), int(bool(implicit)),
+                                       _stream_ptr(stream))
+        _check(st, "rcholqr_factor2")
+        return Q, R, Rprime
 
     def query_status(self, stream=None) -> int:
         return int(self._lib.rcholqr_query_status(self._h, _stream_ptr(stream)))

@@ -57,6 +57,10 @@ struct rcholqr_plan_s {
   int stream_tb = 0;        // > 0: streamed blocked substitution (fp64, n > 128) with this block width
   bool solve_tc = false;    // fp32 X, n <= 64: tcgen05 digit solve Q = X R^{-1} (solve_tc.cu)
   void* xdig = nullptr;     // pre-split X digit planes of the tcgen05 Gaussian sketch (grown on demand)
+  // RCholeskyQR2 (rcqr2.cu): Gram partials, A, Cholesky work, R', R1, and Q1 (grown on demand)
+  int gram_splits = 0;
+  double* gpart = nullptr; double* gA = nullptr; double* gW = nullptr; double* gRp = nullptr; double* gR1 = nullptr;
+  void* q1buf = nullptr; size_t q1_bytes = 0;
   size_t xdig_bytes = 0;
   void* qws = nullptr;      // its W-digit workspace
   double* tbuf = nullptr;   // [m_local][stream_tb] T_J workspace of the streamed solve
@@ -331,6 +335,7 @@ rcholqr_status rcholqr_destroy(rcholqr_plan p) {
   DeviceGuard dg(p->d.device);
   cudaFree(p->part); cudaFree(p->partc); cudaFree(p->P); cudaFree(p->W); cudaFree(p->Awork); cudaFree(p->diag); cudaFree(p->tau);
   cudaFree(p->Rtmp); cudaFree(p->status_d); cudaFree(p->flag_d); cudaFree(p->qws); cudaFree(p->xdig); cudaFree(p->qr_ws);
+  cudaFree(p->gpart); cudaFree(p->gA); cudaFree(p->gW); cudaFree(p->gRp); cudaFree(p->gR1); cudaFree(p->q1buf);
   if (p->status_h) cudaFreeHost(p->status_h);
   cudaFree(p->xbuf); cudaFree(p->qbuf); cudaFree(p->rbuf); cudaFree(p->sbuf); cudaFree(p->tbuf);
   for (int t = 0; t < 7; ++t)
@@ -357,6 +362,61 @@ rcholqr_status rcholqr_factor_async(rcholqr_plan p, const void* X, int64_t m, in
   if (s2 != RCHOLQR_OK) return s2;
   if (p->timing) cudaEventRecord(p->ev[6], st);
   return RCHOLQR_OK;
+}
+
+rcholqr_status rcholqr_factor2(rcholqr_plan p, const void* X, int64_t m, int64_t ro, int64_t ldx, void* Q,
+                               int64_t ldq, double* R, double* Rprime, int32_t implicit, void* stream) {
+  rcholqr_status a = check_factor_args(p, X, m, ro, ldx, Q, ldq);
+  if (a != RCHOLQR_OK) return a;
+  if (!R || (implicit && !Rprime)) return RCHOLQR_E_INVALID;
+  DeviceGuard dg(p->d.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = p->d.n;
+  const size_t nn = (size_t)n * n, es = esize(p->d.dtype);
+  if (!p->gA) {   // Gram workspace, allocated on first use
+    p->gram_splits = gram_splits(n, p->sms);
+    bool ok = cudaMalloc(&p->gpart, sizeof(double) * nn * p->gram_splits) == cudaSuccess &&
+              cudaMalloc(&p->gA, sizeof(double) * nn) == cudaSuccess &&
+              cudaMalloc(&p->gW, sizeof(double) * nn) == cudaSuccess &&
+              cudaMalloc(&p->gRp, sizeof(double) * nn) == cudaSuccess &&
+              cudaMalloc(&p->gR1, sizeof(double) * nn) == cudaSuccess;
+    if (!ok) { cudaGetLastError(); return RCHOLQR_E_NOMEM; }
+  }
+  // Q1: the caller's Q (implicit form) or a plan-owned buffer (explicit form; Q must not alias it)
+  void* Q1 = Q;
+  int64_t ldq1 = ldq;
+  if (!implicit && m > 0) {
+    const size_t need = (size_t)m * n * es;
+    if (need > p->q1_bytes) {
+      cudaFree(p->q1buf);
+      p->q1buf = nullptr; p->q1_bytes = 0;
+      CU(cudaMalloc(&p->q1buf, need));
+      p->q1_bytes = need;
+    }
+    Q1 = p->q1buf;
+    ldq1 = n;
+  }
+  // 1. RCholeskyQR (Alg. 2): Q1, R1
+  rcholqr_status s = rcholqr_factor_async(p, X, m, ro, ldx, Q1, ldq1, p->gR1, nullptr, stream);
+  if (s != RCHOLQR_OK) return s;
+  // 2. A = Q1^T Q1 (+ all-reduce)
+  if (m > 0) CU(launch_gram(Q1, p->d.dtype, m, n, ldq1, p->gram_splits, p->gpart, p->gA, p->status_d, st));
+  else CU(cudaMemsetAsync(p->gA, 0, sizeof(double) * nn, st));
+  if (p->d.nccl_comm) {
+    if (!nccl_load()) return RCHOLQR_E_NCCL;
+    if (g_nccl.AllReduce(p->gA, p->gA, nn, ncclFloat64, ncclSum, (ncclComm_t)p->d.nccl_comm, st) != ncclSuccess)
+      return RCHOLQR_E_NCCL;
+  }
+  // 3. R' = chol(A), R = R' R1
+  double* Rp = Rprime ? Rprime : p->gRp;
+  CU(launch_cholesky(p->gA, n, p->gW, Rp, p->status_d, st));
+  CU(launch_trmm_upper(Rp, p->gR1, n, R, p->status_d, st));
+  // 4. Q = Q1 R'^{-1} (explicit form)
+  if (!implicit) {
+    rcholqr_status s2 = solve(p, Q1, m, ldq1, Rp, Q, ldq, st, false);
+    if (s2 != RCHOLQR_OK) return s2;
+  }
+  return read_status(p, st);
 }
 
 rcholqr_status rcholqr_query_status(rcholqr_plan p, void* stream) {

@@ -97,6 +97,15 @@ bool solve_tc_supported(const void* X, int64_t m, int64_t ldx, const void* Q, in
 size_t solve_tc_workspace();
 cudaError_t launch_solve_tc(const double* Winv, int n, const float* X, int64_t m, int64_t ldx, float* Q, int64_t ldq,
                             void* ws, const int* status, int sms, cudaStream_t st);
+// RCholeskyQR2 (rcqr2.cu): Gram A = Q^T Q, Cholesky R', R' R
+cudaError_t launch_reduce(const double* part, int splits, int64_t kn, double scale, double* P, int* status,
+                          cudaStream_t st);
+int gram_splits(int n, int sms);
+cudaError_t launch_gram(const void* Q, int dtype, int64_t m, int n, int64_t ldq, int splits, double* part, double* A,
+                        int* status, cudaStream_t st);
+cudaError_t launch_cholesky(const double* A, int n, double* W, double* Rp, int* status, cudaStream_t st);
+cudaError_t launch_trmm_upper(const double* U, const double* V, int n, double* out, const int* status,
+                              cudaStream_t st);
 cudaError_t launch_trsm_resident(int tm, const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M,
                                  void* Q, int64_t ldq, const int* status, int sms, cudaStream_t st);
 

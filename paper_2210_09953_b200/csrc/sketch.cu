@@ -730,6 +730,15 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
   return cudaGetLastError();
 }
 
+// fixed-order compensated sum of per-split partials (also the Gram reduction of rcqr2.cu)
+cudaError_t launch_reduce(const double* part, int splits, int64_t kn, double scale, double* P, int* status,
+                          cudaStream_t st) {
+  const int threads = 256;
+  const int blocks = (int)std::min<int64_t>((kn + threads - 1) / threads, 4096);
+  sketch_reduce_kernel<<<blocks, threads, 0, st>>>(part, nullptr, splits, kn, scale, P, status);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_theta_export(uint64_t seed, int k, int sketch, int zeta, int64_t row_offset, int64_t m,
                                 float* Z, int32_t* rows, int8_t* signs, cudaStream_t st) {
   if (m == 0) return cudaSuccess;
