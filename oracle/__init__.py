@@ -84,6 +84,10 @@ def _L():
             lib.oracle_trmm_upper.argtypes = [P, P, I32, P]
             lib.oracle_factor2.argtypes = [P, I32, I64, I32, I64, I64, I32, I32, I32, U64, P, I64, P, P, P]
             lib.oracle_factor2.restype = I32
+            lib.oracle_extract.argtypes = [P, I32, I64, I32, I64, I64, I32, I32, U64, P]
+            lib.oracle_extract.restype = I32
+            lib.oracle_factor_reduced.argtypes = [P, I32, I64, I32, I64, I64, I32, I32, I32, U64, I32, P, P, P, P]
+            lib.oracle_factor_reduced.restype = I32
             lib.oracle_sketch_entry.argtypes = [P, I64, I64, I32, I32, I32, U64, I32]
             lib.oracle_sketch_entry.restype = ctypes.c_double
             _lib = lib
@@ -279,6 +283,38 @@ def factor2(X: np.ndarray, k: int, sketch: int = GAUSSIAN, zeta: int = 8, seed: 
     if st != OK:
         raise OracleError(st, "factor2")
     return {"Q": Q, "R": R, "Q1": Q1, "Rp": Rp}
+
+
+def extractor_row0(k: int, sketch: int = GAUSSIAN) -> int:
+    """First Gaussian-stream row of the Alg. 5 extractor L (reading A20): k after a Gaussian Theta, else 0."""
+    return k if sketch == GAUSSIAN else 0
+
+
+def extract(X: np.ndarray, l0: int, l: int, seed: int = 0, row_offset: int = 0) -> np.ndarray:
+    """Y = L X with L_ji = z(seed, i, l0 + j) / sqrt(l) (Alg. 5 step 1)."""
+    X = np.ascontiguousarray(X)
+    m, n = X.shape
+    Y = np.empty((l, n), dtype=np.float64)
+    st = _L().oracle_extract(_ptr(X), _dtype_code(X), m, n, n, row_offset, l0, l, seed, _ptr(Y))
+    if st != OK:
+        raise OracleError(st, "extract")
+    return Y
+
+
+def factor_reduced(X: np.ndarray, k: int, l: int, sketch: int = GAUSSIAN, zeta: int = 8, seed: int = 0,
+                   row_offset: int = 0, want_S: bool = True) -> dict:
+    """Whole Algorithm 5 (reduced RCholeskyQR): dict(Z, R, Y, S), Z = Y R^{-1} = L Q."""
+    X = np.ascontiguousarray(X)
+    m, n = X.shape
+    Z = np.empty((l, n), dtype=np.float64)
+    Y = np.empty((l, n), dtype=np.float64)
+    R = np.empty((n, n), dtype=np.float64)
+    S = np.empty((k, n), dtype=np.float64) if want_S else None
+    st = _L().oracle_factor_reduced(_ptr(X), _dtype_code(X), m, n, n, row_offset, k, sketch, zeta, seed, l,
+                                    _ptr(Z), _ptr(R), _ptr(Y), _ptr(S))
+    if st != OK:
+        raise OracleError(st, "factor_reduced")
+    return {"Z": Z, "R": R, "Y": Y, "S": S}
 
 
 # ---------------------------------------------------------------- metrics (PAPER.md:773, 797)

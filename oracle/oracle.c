@@ -7,7 +7,8 @@
  * (paper_2210_09953_b200/) never imports, links or executes anything under oracle/, and
  * this file shares no code, header, table or constant generator with it.
  *
- * What it computes (alg:RCQR; and alg:RCQR2, below):
+ * What it computes (alg:RCQR; alg:RCQR2, and alg:oneRCQR,
+ * PAPER.md:263-276, below):
  *     1. P <- Theta X   oracle_sketch
  *     2. [R, S] <- QR(P)   oracle_householder  (Householder)
  *     3. Q <- X R^{-1}   oracle_forward_subst (forward substitution,
@@ -517,6 +518,80 @@ int oracle_factor2(const void* X, int dtype, int64_t m, int n, int64_t ldx, int6
     if (st == OR_OK) st = oracle_forward_subst(Q1, dtype, m, n, n, Rp, Q, ldq);
     free(R1);
     free(A);
+    return st;
+}
+
+/* ------------------------------------------------------------------------------------------
+ * Algorithm 5, reduced RCholeskyQR (alg:oneRCQR):
+ *   1. P <- Theta X,  Y <- L X          (oracle_sketch, oracle_extract; one pass over X on the GPU)
+ *   2. [S, R] <- QR(P)                   (oracle_householder)
+ *   3. Z <- Y R^{-1}                     (oracle_forward_subst on the l x n matrix Y, fp64)
+ * The extractor L (l x m, "possibly randomized ... possibly provided as a function handle",
+ * PAPER.md:266-270) is a Gaussian OSE drawn from the SAME normative Gaussian stream as Theta
+ * (reading A20): L_ji = z(seed, i, row l0 + j) * fl64(1/sqrt(l)), with l0 = k when Theta is
+ * Gaussian (L continues Theta's rows, so [Theta; L] is one (k + l)-row draw) and l0 = 0 when
+ * Theta is sparse-sign (domain 2; the Gaussian stream is then unused by Theta).
+ * ---------------------------------------------------------------------------------------- */
+
+/* Y = L X (l x n): Y_jc = sum_i L_ji x_ic with the Dot2 fixed-block policy of oracle_sketch. */
+int oracle_extract(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset,
+                   int l0, int l, uint64_t seed, double* Y) {
+    if (!Y || (m > 0 && !X) || n < 1 || l < 1 || l0 < 0 || ldx < n || m < 0) return OR_E_INVALID;
+    int64_t nb = (m + OR_SKETCH_BLOCK - 1) / OR_SKETCH_BLOCK;
+    size_t ln = (size_t)l * n;
+    double* part = (double*)calloc((size_t)(nb > 0 ? nb : 1) * ln * 2, sizeof(double));
+    if (!part) return OR_E_NOMEM;
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t b = 0; b < nb; ++b) {
+        double* Yb = part + (size_t)b * ln * 2;
+        double* Cb = Yb + ln;
+        double* lr = (double*)malloc(sizeof(double) * (size_t)l);
+        double sl = 1.0 / sqrt((double)l);
+        int64_t i0 = b * OR_SKETCH_BLOCK, i1 = i0 + OR_SKETCH_BLOCK < m ? i0 + OR_SKETCH_BLOCK : m;
+        for (int64_t i = i0; i < i1; ++i) {
+            uint64_t gi = (uint64_t)(row_offset + i);
+            for (int j = 0; j < l; ++j) {
+                float z[4];
+                int r = l0 + j;
+                oracle_gauss4(seed, gi, (uint32_t)(r / 4), z);
+                lr[j] = (double)z[r % 4] * sl;
+            }
+            for (int j = 0; j < l; ++j)
+                for (int c = 0; c < n; ++c)
+                    dot2_add(&Yb[(size_t)j * n + c], &Cb[(size_t)j * n + c], lr[j], load_x(X, dtype, i * ldx + c));
+        }
+        free(lr);
+    }
+    for (size_t t = 0; t < ln; ++t) {
+        double s = 0.0, c = 0.0;
+        for (int64_t b = 0; b < nb; ++b) {
+            sum2_add(&s, &c, part[(size_t)b * ln * 2 + t]);
+            c += part[(size_t)b * ln * 2 + ln + t];
+        }
+        Y[t] = s + c;
+    }
+    free(part);
+    for (size_t t = 0; t < ln; ++t)
+        if (!isfinite(Y[t])) return OR_E_NONFINITE;
+    return OR_OK;
+}
+
+/* Whole Algorithm 5.  Z (l x n fp64) and R (n x n) are outputs; Y (l x n) and S (k x n) optional. */
+int oracle_factor_reduced(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset,
+                          int k, int sketch, int zeta, uint64_t seed, int l, double* Z, double* R,
+                          double* Y_out, double* S_out) {
+    if (!Z || !R || l < 1) return OR_E_INVALID;
+    if (k < n) return OR_E_SHAPE;
+    double* P = (double*)malloc(sizeof(double) * (size_t)k * n);
+    double* Y = Y_out ? Y_out : (double*)malloc(sizeof(double) * (size_t)l * n);
+    if (!P || !Y) { free(P); if (!Y_out) free(Y); return OR_E_NOMEM; }
+    int l0 = sketch == OR_GAUSSIAN ? k : 0;
+    int st = oracle_sketch(X, dtype, m, n, ldx, row_offset, k, sketch, zeta, seed, P);
+    if (st == OR_OK) st = oracle_extract(X, dtype, m, n, ldx, row_offset, l0, l, seed, Y);
+    if (st == OR_OK) st = oracle_householder(P, k, n, R, S_out);
+    if (st == OR_OK) st = oracle_forward_subst(Y, 0, l, n, n, R, Z, n);
+    free(P);
+    if (!Y_out) free(Y);
     return st;
 }
 
