@@ -108,12 +108,16 @@ def _workload(cfg_name: str, ws: int, rank: int):
     return cfg, m_local, m_global, ro, scaling
 
 
-def _cpu_sample_rate(X_dev, cfg, target_s: float, algo: str = "rcholqr"):
+def _cpu_sample_rate(X_dev, cfg, target_s: float, algo: str = "rcholqr", l: int = 0):
     """Time the oracle (as it stands, all host cores) on a bounded leading sample of X."""
     import oracle
     so = oracle.GAUSSIAN if cfg["sketch"] == "gaussian" else oracle.SPARSE_SIGN
-    run = (lambda A: oracle.factor2(A, cfg["k"], sketch=so, zeta=cfg["nnz"])) if algo == "rcholqr2" else \
-        (lambda A: oracle.factor(A, cfg["k"], sketch=so, zeta=cfg["nnz"], want_S=False))
+    if algo == "rcholqr2":
+        run = lambda A: oracle.factor2(A, cfg["k"], sketch=so, zeta=cfg["nnz"])  # noqa: E731
+    elif algo == "rcholqr_reduced":
+        run = lambda A: oracle.factor_reduced(A, cfg["k"], l, sketch=so, zeta=cfg["nnz"], want_S=False)  # noqa: E731
+    else:
+        run = lambda A: oracle.factor(A, cfg["k"], sketch=so, zeta=cfg["nnz"], want_S=False)  # noqa: E731
     m = X_dev.shape[0]
     rows = min(m, 4096)
     while True:
@@ -200,10 +204,14 @@ def run(args):
     stream = torch.cuda.current_stream()
 
     Rp = torch.empty((n, n), dtype=torch.float64, device=dev)
+    l_red = args.l or k                     # Alg. 5: rows of the extractor L (default: as many as Theta)
+    Z = torch.empty((l_red, n), dtype=torch.float64, device=dev) if args.algo == "rcholqr_reduced" else None
 
     def step():
         if args.algo == "rcholqr2":   # Alg. 3: synchronous (status read inside the call)
             plan.factor2(X, row_offset=ro, Q=Q, R=R, Rprime=Rp, stream=stream)
+        elif args.algo == "rcholqr_reduced":   # Alg. 5: synchronous
+            plan.factor_reduced(X, l_red, row_offset=ro, Z=Z, R=R, stream=stream)
         else:
             plan.factor(X, row_offset=ro, Q=Q, R=R, stream=stream, sync=False)
 
@@ -276,24 +284,39 @@ def run(args):
     peaks = _peaks()
     hbm = peaks.get("hbm_gbs", 6545.0)
     roofs = {}
+    reduced = args.algo == "rcholqr_reduced"
+    k_sk = k + l_red if reduced else k      # Alg. 5 with a Gaussian Theta: one (k + l)-row sketch
     if cfg["sketch"] == "gaussian":
         # exact int8 digit-product sketch (sketch_gtc.cu); its algorithmic work is the method's 2kmn
         # fp64 flops, so it is measured against the FP64 tensor (DMMA) peak it replaces.
-        flops = 2.0 * k * m_local * n
+        flops = 2.0 * k_sk * m_local * n
         ach = flops / (per_ms["sketch"] * 1e-3) / 1e12
         roofs["sketch"] = {"kernel": "sketch_gauss_tc_kernel", "bound": "tensor", "achieved": ach,
                            "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
                            "peak_source": "FP64 DMMA peak 37.2 TF (148 SM x 64 FMA/clk x 2 x 1.965 GHz; "
                                           "microbenchmark 37.0, profiles/peaks_r1.jsonl): fp64-equivalent view "
                                           "of the exact int8 digit emulation",
-                           "algorithmic": f"2*k*m*n = {flops:.4g} flop per launch", "traffic": None}
+                           "algorithmic": f"2*{'(k+l)' if reduced else 'k'}*m*n = {flops:.4g} flop per launch",
+                           "traffic": None}
+    elif reduced:
+        # sparse Theta: P by the sparse tcgen05 sketch (one HBM pass), then Y = L X by the Gaussian
+        # one; the Gaussian extract's 2 l m n fp64-equivalent flops dominate both passes' time
+        flops = 2.0 * l_red * m_local * n
+        ach = flops / (per_ms["sketch"] * 1e-3) / 1e12
+        roofs["sketch"] = {"kernel": "sketch_gauss_tc_kernel", "bound": "tensor", "achieved": ach,
+                           "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
+                           "peak_source": "FP64 DMMA peak 37.2 TF (fp64-equivalent view of the exact int8 digits)",
+                           "algorithmic": f"2*l*m*n = {flops:.4g} flop (Gaussian extract; the time includes "
+                                          "the sparse sketch pass)", "traffic": None}
     else:
         byts = m_local * n * s_x
         ach = byts / (per_ms["sketch"] * 1e-3) / 1e9
         roofs["sketch"] = {"kernel": "sketch_sparse_tc_kernel", "bound": "hbm", "achieved": ach, "peak": hbm,
                            "unit": "GB/s", "frac": ach / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                            "algorithmic": f"m*n*s_x = {byts:.4g} B per launch (one read of X)", "traffic": None}
-    if dt == "f32" and n <= 64:
+    if reduced:
+        pass                                 # step 3 is the tiny l x n substitution (rowsub_kernel)
+    elif dt == "f32" and n <= 64:
         byts = 2.0 * m_local * n * s_x
         ach = byts / (per_ms["solve"] * 1e-3) / 1e9
         roofs["solve"] = {"kernel": "solve_tc_kernel", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
@@ -316,7 +339,7 @@ def run(args):
         if tb is not None and ws == 1:
             r_["traffic"] = tb
             r_["traffic_source"] = "ncu --set full: dram__bytes_read.sum + dram__bytes_write.sum per launch"
-    dom = max(("sketch", "solve"), key=lambda kk: per_ms.get(kk, 0.0))
+    dom = max(roofs, key=lambda kk: per_ms.get(kk, 0.0))
     roof = dict(roofs[dom])
     roof["share_of_step"] = per_ms.get(dom, 0.0) / ms
     # north-star roofline for the whole factorization
@@ -352,11 +375,28 @@ def run(args):
                                       "note": "Alg. 3 accounting: 6 passes over m x n, 3 m n^2 fp64 flops"}
         line["gpu_launches"] = (plan.launches_per_factor(m_local) + 4 + 2) * args.steps
         line["e2e"] = None   # the host-buffer entry point is Alg. 2's
+    if reduced:
+        # Alg. 5 reads X once: max(one pass at HBM, the (k + l)-row sketch's 2 (k + l) m n fp64 flops)
+        t_hbm5 = 1.0 * m_local * n * s_x / (hbm * 1e9)
+        t_flop5 = 2.0 * (k_sk if cfg["sketch"] == "gaussian" else l_red) * m_local * n / (DMMA_PEAK_TFLOPS * 1e12)
+        if cfg["sketch"] != "gaussian":
+            t_hbm5 *= 2.0            # sparse Theta: P and Y are two passes over X
+        line["metric"] = "Reduced RandCholQR throughput (GB/s of X)"
+        line["config"]["algo"] = f"rcholqr_reduced (Alg. 5, Gaussian extractor l = {l_red})"
+        line["config"]["l"] = l_red
+        line["northstar_roofline"] = {"t_hbm_ms": t_hbm5 * 1e3, "t_fp64_ms": t_flop5 * 1e3,
+                                      "roofline_ms": max(t_hbm5, t_flop5) * 1e3,
+                                      "frac": max(t_hbm5, t_flop5) * 1e3 / ms,
+                                      "note": "Alg. 5 accounting: 1 pass over X, 2 (k+l) m n fp64-equivalent flops"}
+        # Alg. 2's launches minus its solve (prep + solve) plus the Z substitution
+        line["gpu_launches"] = (plan.launches_per_factor(m_local) - 1) * args.steps
+        line["e2e"] = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        rows, dt_s, cores = _cpu_sample_rate(X, cfg, args.cpu_seconds, args.algo)
+        rows, dt_s, cores = _cpu_sample_rate(X, cfg, args.cpu_seconds, args.algo, l_red)
+        fn = {"rcholqr2": "factor2", "rcholqr_reduced": "factor_reduced"}.get(args.algo, "factor")
         line["cpu_baseline"] = {"value": rows * n * s_x / dt_s / 1e9, "unit": "GB/s", "cores": cores,
                                 "kind": "oracle", "seconds": dt_s,
-                                "sample": f"oracle.{'factor2' if args.algo == 'rcholqr2' else 'factor'} on the leading {rows} rows of the same X"}
+                                "sample": f"oracle.{fn} on the leading {rows} rows of the same X"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     plan.close()
@@ -377,8 +417,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--algo", default="rcholqr", choices=["rcholqr", "rcholqr2"],
-                    help="Alg. 2 (default, the north star) or Alg. 3 RCholeskyQR2 (orthonormal Q)")
+    ap.add_argument("--algo", default="rcholqr", choices=["rcholqr", "rcholqr2", "rcholqr_reduced"],
+                    help="Alg. 2 (default, the north star), Alg. 3 RCholeskyQR2 (orthonormal Q) or Alg. 5 "
+                         "reduced RCholeskyQR (Z = L Q)")
+    ap.add_argument("--l", type=int, default=0, help="Alg. 5: rows of the extractor L (default k)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -119,6 +119,24 @@ rcholqr_status rcholqr_factor2(rcholqr_plan plan, const void* X, int64_t m_local
                                int64_t ldx, void* Q, int64_t ldq, double* R, double* Rprime, int32_t implicit,
                                void* stream);
 
+/* Reduced RCholeskyQR (Alg. 5, alg:oneRCQR): the extract Z = L Q of the Q factor
+ * without forming Q -- P = Theta X and Y = L X in step 1, [S, R] = QR(P), Z = Y R^{-1}.
+ * L (l x m) is a Gaussian extractor from the normative Gaussian stream (reading A20):
+ * L_ji = z(seed, global row i, l0 + j) / sqrt(l), l0 = k for a Gaussian plan (then [Theta; L] is
+ * one (k + l)-row sketch and X is read ONCE), l0 = 0 for a sparse-sign plan (a second pass).
+ *   X, m_local, row_offset, ldx, stream: as for rcholqr_factor.
+ *   l  rows of L (>= 1; (k + l) n <= 2^28).
+ *   Z  [device] l x n fp64 row-major output (required).
+ *   R  [device] n x n fp64 output or NULL;  S [device] k x n fp64 or NULL (Alg. 5's S);
+ *   Y  [device] l x n fp64 or NULL: the extract L X (after the all-reduce).
+ * Status: E_INVALID (arguments), E_SHAPE, E_NONFINITE (P or Y), E_SINGULAR (Z not written).
+ * Memory: the plan grows an (k + l) x n sketch workspace on the first call with a new l.
+ * SYNCHRONOUS.  With a communicator every rank must call this (one all-reduce of [P; Y]); Z is
+ * computed redundantly and is identical on every rank. */
+rcholqr_status rcholqr_factor_reduced(rcholqr_plan plan, const void* X, int64_t m_local, int64_t row_offset,
+                                      int64_t ldx, int32_t l, double* Z, double* R, double* S, double* Y,
+                                      void* stream);
+
 /* ---- step-level entry points (same kernels as rcholqr_factor; used by the parity tests) ---- */
 
 /* Step 1 (+ the all-reduce when the plan has a communicator): P = Theta X, k x n fp64 row-major

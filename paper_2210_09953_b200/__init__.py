@@ -34,7 +34,8 @@ SYMBOLS = ["rcholqr_create", "rcholqr_destroy", "rcholqr_factor", "rcholqr_facto
            "rcholqr_query_status", "rcholqr_factor_host", "rcholqr_sketch", "rcholqr_small_qr",
            "rcholqr_tri_solve", "rcholqr_theta_export", "rcholqr_comm_unique_id",
            "rcholqr_comm_create", "rcholqr_comm_destroy", "rcholqr_strerror", "rcholqr_version",
-           "rcholqr_launches_per_factor", "rcholqr_set_timing", "rcholqr_last_timings", "rcholqr_factor2"]
+           "rcholqr_launches_per_factor", "rcholqr_set_timing", "rcholqr_last_timings", "rcholqr_factor2",
+           "rcholqr_factor_reduced"]
 
 
 class _Desc(ctypes.Structure):
@@ -72,6 +73,7 @@ def load_library():
             "rcholqr_query_status": ([V, V], I32),
             "rcholqr_factor_host": ([V, V, I64, I64, I64, V, I64, V, V, V], I32),
             "rcholqr_factor2": ([V, V, I64, I64, I64, V, I64, V, V, I32, V], I32),
+            "rcholqr_factor_reduced": ([V, V, I64, I64, I64, I32, V, V, V, V, V], I32),
             "rcholqr_sketch": ([V, V, I64, I64, I64, V, V], I32),
             "rcholqr_small_qr": ([V, V, V, V, V], I32),
             "rcholqr_tri_solve": ([V, V, I64, I64, V, V, I64, V], I32),
@@ -205,6 +207,23 @@ class RCholQR:
                                        _stream_ptr(stream))
         _check(st, "rcholqr_factor2")
         return Q, R, Rprime
+
+    def factor_reduced(self, X, l: int, row_offset: int = 0, want_S: bool = False, want_Y: bool = False, Z=None,
+                       R=None, S=None, Y=None, stream=None) -> Tuple:
+        """Reduced RCholeskyQR (Alg. 5): Z = L Q (l x n) without forming Q; returns (Z, R, S, Y)."""
+        torch = _torch()
+        m, ldx = self._check_x(X)
+        f64 = dict(dtype=torch.float64, device=X.device)
+        Z = torch.empty((l, self.n), **f64) if Z is None else Z
+        R = torch.empty((self.n, self.n), **f64) if R is None else R
+        if want_S and S is None:
+            S = torch.empty((self.k, self.n), **f64)
+        if want_Y and Y is None:
+            Y = torch.empty((l, self.n), **f64)
+        st = self._lib.rcholqr_factor_reduced(self._h, _ptr(X), m, row_offset, ldx, int(l), _ptr(Z), _ptr(R),
+                                              _ptr(S), _ptr(Y), _stream_ptr(stream))
+        _check(st, "rcholqr_factor_reduced")
+        return Z, R, S, Y
 
     def query_status(self, stream=None) -> int:
         return int(self._lib.rcholqr_query_status(self._h, _stream_ptr(stream)))

@@ -61,6 +61,10 @@ struct rcholqr_plan_s {
   int gram_splits = 0;
   double* gpart = nullptr; double* gA = nullptr; double* gW = nullptr; double* gRp = nullptr; double* gR1 = nullptr;
   void* q1buf = nullptr; size_t q1_bytes = 0;
+  // reduced RCholeskyQR (Alg. 5): the (k + l)-row sketch [P; Y] and its partials (grown on demand)
+  int red_l = 0;
+  SketchLaunch red_sk{};
+  double* red_part = nullptr; double* red_partc = nullptr; double* red_P = nullptr;
   size_t xdig_bytes = 0;
   void* qws = nullptr;      // its W-digit workspace
   double* tbuf = nullptr;   // [m_local][stream_tb] T_J workspace of the streamed solve
@@ -154,13 +158,20 @@ rcholqr_status check_factor_args(rcholqr_plan p, const void* X, int64_t m, int64
   return RCHOLQR_OK;
 }
 
+// Step 1 (+ the all-reduce).  By default the plan's k-row sketch; Alg. 5 passes its own launch `L` of
+// `k` rows (partials part/partc), with rows >= k_first scaled as extractor rows, and may defer the
+// all-reduce (allreduce = false) to sum [P; Y] at once.
 rcholqr_status do_sketch(rcholqr_plan p, const void* X, int64_t m, int64_t ro, int64_t ldx, double* P,
-                         cudaStream_t st) {
+                         cudaStream_t st, const SketchLaunch* Lp = nullptr, int k = 0, double* part = nullptr,
+                         double* partc = nullptr, int k_first = 0, bool allreduce = true) {
   const auto& d = p->d;
+  const SketchLaunch& L = Lp ? *Lp : p->sk;
+  if (!Lp) { k = d.k; part = p->part; partc = p->partc; }
+  const bool timed = p->timing && allreduce;
   if (m > 0) {
-    if (p->timing) cudaEventRecord(p->ev[0], st);
-    if (p->sk.tc && p->sk.kind < kSketchSparse) {   // grow the pre-split digit workspace (capped)
-      const size_t need = gauss_tcp_chunk_workspace(m, d.n, d.dtype, p->sk.tc_splits);
+    if (timed) cudaEventRecord(p->ev[0], st);
+    if (L.tc && L.kind < kSketchSparse) {   // grow the pre-split digit workspace (capped)
+      const size_t need = gauss_tcp_chunk_workspace(m, d.n, d.dtype, L.tc_splits);
       if (need > p->xdig_bytes) {
         cudaFree(p->xdig);
         p->xdig = nullptr; p->xdig_bytes = 0;
@@ -168,20 +179,19 @@ rcholqr_status do_sketch(rcholqr_plan p, const void* X, int64_t m, int64_t ro, i
         else cudaGetLastError();   // not enough memory: the in-kernel split is used instead
       }
     }
-    CU(launch_sketch(p->sk, X, d.dtype, m, d.n, ldx, ro, d.k, d.nnz_per_col, d.seed, p->part, p->partc, P, p->status_d, p->flag_d,
-                     p->xdig, p->xdig_bytes, st,
-                     p->timing ? p->ev[1] : nullptr));
+    CU(launch_sketch(L, X, d.dtype, m, d.n, ldx, ro, k, d.nnz_per_col, d.seed, part, partc, P, p->status_d, p->flag_d,
+                     p->xdig, p->xdig_bytes, st, timed ? p->ev[1] : nullptr, k_first));
   } else {
-    if (p->timing) { cudaEventRecord(p->ev[0], st); cudaEventRecord(p->ev[1], st); }
-    CU(cudaMemsetAsync(P, 0, sizeof(double) * (size_t)d.k * d.n, st));
+    if (timed) { cudaEventRecord(p->ev[0], st); cudaEventRecord(p->ev[1], st); }
+    CU(cudaMemsetAsync(P, 0, sizeof(double) * (size_t)k * d.n, st));
   }
-  if (p->timing) cudaEventRecord(p->ev[2], st);
-  if (d.nccl_comm) {
+  if (timed) cudaEventRecord(p->ev[2], st);
+  if (d.nccl_comm && allreduce) {
     if (!nccl_load()) return RCHOLQR_E_NCCL;
-    ncclResult_t r = g_nccl.AllReduce(P, P, (size_t)d.k * d.n, ncclFloat64, ncclSum, (ncclComm_t)d.nccl_comm, st);
+    ncclResult_t r = g_nccl.AllReduce(P, P, (size_t)k * d.n, ncclFloat64, ncclSum, (ncclComm_t)d.nccl_comm, st);
     if (r != ncclSuccess) return RCHOLQR_E_NCCL;
   }
-  if (p->timing) cudaEventRecord(p->ev[3], st);
+  if (timed) cudaEventRecord(p->ev[3], st);
   return RCHOLQR_OK;
 }
 
@@ -336,6 +346,7 @@ rcholqr_status rcholqr_destroy(rcholqr_plan p) {
   cudaFree(p->part); cudaFree(p->partc); cudaFree(p->P); cudaFree(p->W); cudaFree(p->Awork); cudaFree(p->diag); cudaFree(p->tau);
   cudaFree(p->Rtmp); cudaFree(p->status_d); cudaFree(p->flag_d); cudaFree(p->qws); cudaFree(p->xdig); cudaFree(p->qr_ws);
   cudaFree(p->gpart); cudaFree(p->gA); cudaFree(p->gW); cudaFree(p->gRp); cudaFree(p->gR1); cudaFree(p->q1buf);
+  cudaFree(p->red_part); cudaFree(p->red_partc); cudaFree(p->red_P);
   if (p->status_h) cudaFreeHost(p->status_h);
   cudaFree(p->xbuf); cudaFree(p->qbuf); cudaFree(p->rbuf); cudaFree(p->sbuf); cudaFree(p->tbuf);
   for (int t = 0; t < 7; ++t)
@@ -417,6 +428,67 @@ rcholqr_status rcholqr_factor2(rcholqr_plan p, const void* X, int64_t m, int64_t
     if (s2 != RCHOLQR_OK) return s2;
   }
   return read_status(p, st);
+}
+
+rcholqr_status rcholqr_factor_reduced(rcholqr_plan p, const void* X, int64_t m, int64_t ro, int64_t ldx, int32_t l,
+                                      double* Z, double* R, double* S, double* Y, void* stream) {
+  if (!p || !Z || l < 1 || m < 0 || ro < 0 || ldx < p->d.n || (m > 0 && !X)) return RCHOLQR_E_INVALID;
+  const int k = p->d.k, n = p->d.n;
+  const bool gauss = p->d.sketch == RCHOLQR_GAUSSIAN;
+  if ((int64_t)(k + (int64_t)l) * n > (int64_t)1 << 28) return RCHOLQR_E_SHAPE;
+  DeviceGuard dg(p->d.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (p->red_l != l) {   // the (k + l)-row launch (Gaussian Theta) or the l-row extractor launch (sparse Theta)
+    cudaFree(p->red_part); cudaFree(p->red_partc); cudaFree(p->red_P);
+    p->red_part = p->red_partc = p->red_P = nullptr;
+    p->red_l = 0;
+    p->red_sk = plan_sketch(gauss ? k + l : l, n, p->d.dtype, RCHOLQR_GAUSSIAN, p->d.nnz_per_col, p->sms, p->smem_optin);
+    const size_t rows = gauss ? (size_t)(k + l) : (size_t)l;
+    const size_t elems = rows * n * p->red_sk.max_splits();
+    bool ok = cudaMalloc(&p->red_part, sizeof(double) * elems) == cudaSuccess &&
+              cudaMalloc(&p->red_partc, sizeof(double) * elems) == cudaSuccess &&
+              cudaMalloc(&p->red_P, sizeof(double) * (size_t)(k + l) * n) == cudaSuccess;
+    if (!ok) { cudaGetLastError(); return RCHOLQR_E_NOMEM; }
+    p->red_l = l;
+  }
+  double* P = p->red_P;
+  double* Yd = p->red_P + (size_t)k * n;
+  double* Rout = R ? R : p->Rtmp;
+  CU(cudaMemsetAsync(p->status_d, 0, sizeof(int), st));
+  // 1. P = Theta X, Y = L X: one (k + l)-row pass for a Gaussian Theta, else the sparse sketch and the
+  //    l-row Gaussian extract; one all-reduce of [P; Y] either way
+  rcholqr_status s;
+  const bool t = p->timing;
+  if (gauss) {   // (library events as for rcholqr_factor: sketch | reduce | all-reduce | QR | - | Z)
+    s = do_sketch(p, X, m, ro, ldx, P, st, &p->red_sk, k + l, p->red_part, p->red_partc, k, true);
+  } else {       // events: both passes (sparse P, Gaussian Y, their reductions) | - | all-reduce
+    if (t) cudaEventRecord(p->ev[0], st);
+    p->timing = false;
+    s = do_sketch(p, X, m, ro, ldx, P, st, &p->sk, k, p->part, p->partc, 0, false);
+    if (s == RCHOLQR_OK) s = do_sketch(p, X, m, ro, ldx, Yd, st, &p->red_sk, l, p->red_part, p->red_partc, 0, false);
+    p->timing = t;
+    if (t) { cudaEventRecord(p->ev[1], st); cudaEventRecord(p->ev[2], st); }
+    if (s == RCHOLQR_OK && p->d.nccl_comm) {
+      if (!nccl_load()) s = RCHOLQR_E_NCCL;
+      else if (g_nccl.AllReduce(P, P, (size_t)(k + l) * n, ncclFloat64, ncclSum, (ncclComm_t)p->d.nccl_comm, st) !=
+               ncclSuccess)
+        s = RCHOLQR_E_NCCL;
+    }
+    if (t) cudaEventRecord(p->ev[3], st);
+  }
+  if (s != RCHOLQR_OK) { p->timing = t; return s; }
+  // 2. [S, R] = QR(P)
+  cudaError_t e = launch_qr(p->qr_kind, P, k, n, Rout, p->Awork, p->diag, p->tau, p->qr_ws, p->status_d, st);
+  if (e == cudaSuccess && S) e = launch_form_s(p->Awork, p->tau, p->diag, k, n, S, p->status_d, st);
+  if (p->timing) { cudaEventRecord(p->ev[4], st); cudaEventRecord(p->ev[5], st); }
+  // 3. Z = Y R^{-1}
+  if (e == cudaSuccess) e = launch_rowsub(Yd, l, n, Rout, Z, p->status_d, st);
+  if (p->timing) cudaEventRecord(p->ev[6], st);
+  if (e == cudaSuccess && Y) e = cudaMemcpyAsync(Y, Yd, sizeof(double) * (size_t)l * n, cudaMemcpyDeviceToDevice, st);
+  if (e != cudaSuccess) { p->timing = t; return cuda_status(e); }
+  rcholqr_status r = read_status(p, st);
+  p->timing = t;
+  return r;
 }
 
 rcholqr_status rcholqr_query_status(rcholqr_plan p, void* stream) {

@@ -63,7 +63,8 @@ struct TrsmLaunch {
 SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms, size_t smem_optin);
 cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
                           int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* partc, double* P,
-                          int* status, int* flag, void* xdig, size_t xdig_bytes, cudaStream_t st, cudaEvent_t ev_mid);
+                          int* status, int* flag, void* xdig, size_t xdig_bytes, cudaStream_t st, cudaEvent_t ev_mid,
+                          int k_first = 0);
 TrsmLaunch plan_trsm(int n, int dtype, size_t smem_optin);
 cudaError_t launch_tri_inverse(const double* R, int n, double* W, int* status, cudaStream_t st);
 cudaError_t launch_trsm(const TrsmLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
@@ -106,6 +107,9 @@ cudaError_t launch_gram(const void* Q, int dtype, int64_t m, int n, int64_t ldq,
 cudaError_t launch_cholesky(const double* A, int n, double* W, double* Rp, int* status, cudaStream_t st);
 cudaError_t launch_trmm_upper(const double* U, const double* V, int n, double* out, const int* status,
                               cudaStream_t st);
+// reduced RCholeskyQR (reduced.cu): Z = Y R^{-1} for the small l x n extract Y, row-wise substitution
+cudaError_t launch_rowsub(const double* Y, int64_t l, int n, const double* R, double* Z, const int* status,
+                          cudaStream_t st);
 cudaError_t launch_trsm_resident(int tm, const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M,
                                  void* Q, int64_t ldq, const int* status, int sms, cudaStream_t st);
 

@@ -417,8 +417,11 @@ sketch_sparse_reg_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx
 }
 
 // Fixed-order sum of the per-split partials, one scaling, non-finite detection.
+// Entries idx < kn_first are scaled by `scale`, the rest by `scale2` (the (k + l)-row sketch of Alg. 5:
+// Theta rows by 1/sqrt(k), extractor rows by 1/sqrt(l)).
 __global__ void sketch_reduce_kernel(const double* __restrict__ part, const double* __restrict__ partc, int splits,
-                                     int64_t kn, double scale, double* __restrict__ P, int* status) {
+                                     int64_t kn, double scale, int64_t kn_first, double scale2,
+                                     double* __restrict__ P, int* status) {
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < kn;
        idx += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0, c = 0.0;                    // compensated (TwoSum) sum over the splits
@@ -430,7 +433,7 @@ __global__ void sketch_reduce_kernel(const double* __restrict__ part, const doub
       s = t;
       if (partc) c += partc[(size_t)sp * kn + idx];
     }
-    s = (s + c) * scale;
+    s = (s + c) * (idx < kn_first ? scale : scale2);
     P[idx] = s;
     if (!isfinite(s)) atomicOr(status, kStNonfinite);
   }
@@ -639,7 +642,8 @@ static cudaError_t launch_gauss_typed(const SketchLaunch& L, const void* X, int6
 
 cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
                           int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* partc, double* P,
-                          int* status, int* flag, void* xdig, size_t xdig_bytes, cudaStream_t st, cudaEvent_t ev_mid) {
+                          int* status, int* flag, void* xdig, size_t xdig_bytes, cudaStream_t st, cudaEvent_t ev_mid,
+                          int k_first) {
   cudaError_t e;
   const int64_t per = (m + L.splits - 1) / L.splits;
   double scale;
@@ -725,8 +729,14 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
   const int threads = 256;
   const int blocks = (int)std::min<int64_t>((kn + threads - 1) / threads, 4096);
   const bool sparse = L.kind == kSketchSparse || L.kind == kSketchSparseReg || L.kind == kSketchSparseTC;
-  sketch_reduce_kernel<<<blocks, threads, 0, st>>>(part, sparse ? nullptr : partc, reduce_splits, kn,
-                                                   scale, P, status);
+  // Gaussian rows >= k_first (Alg. 5's extractor rows) take 1/sqrt(k - k_first) instead of 1/sqrt(k)
+  double scale2 = scale;
+  if (!sparse && k_first > 0 && k_first < k) {
+    scale = 1.0 / std::sqrt((double)k_first);
+    scale2 = 1.0 / std::sqrt((double)(k - k_first));
+  }
+  sketch_reduce_kernel<<<blocks, threads, 0, st>>>(part, sparse ? nullptr : partc, reduce_splits, kn, scale,
+                                                   (int64_t)std::min(std::max(k_first, 0), k) * n, scale2, P, status);
   return cudaGetLastError();
 }
 
@@ -735,7 +745,7 @@ cudaError_t launch_reduce(const double* part, int splits, int64_t kn, double sca
                           cudaStream_t st) {
   const int threads = 256;
   const int blocks = (int)std::min<int64_t>((kn + threads - 1) / threads, 4096);
-  sketch_reduce_kernel<<<blocks, threads, 0, st>>>(part, nullptr, splits, kn, scale, P, status);
+  sketch_reduce_kernel<<<blocks, threads, 0, st>>>(part, nullptr, splits, kn, scale, kn, scale, P, status);
   return cudaGetLastError();
 }
 
