@@ -88,6 +88,13 @@ def _L():
             lib.oracle_extract.restype = I32
             lib.oracle_factor_reduced.argtypes = [P, I32, I64, I32, I64, I64, I32, I32, I32, U64, I32, P, P, P, P]
             lib.oracle_factor_reduced.restype = I32
+            lib.oracle_colnorms.argtypes = [P, I32, I64, I32, I64, P]
+            lib.oracle_colnorms.restype = I32
+            lib.oracle_rrqr.argtypes = [P, I32, I32, ctypes.c_double, ctypes.c_double, I32, P, P, P, P, P]
+            lib.oracle_rrqr.restype = I32
+            lib.oracle_factor_rr.argtypes = [P, I32, I64, I32, I64, I64, I32, I32, I32, U64, ctypes.c_double,
+                                             ctypes.c_double, I32, P, I64, P, P, P, P, P, P]
+            lib.oracle_factor_rr.restype = I32
             lib.oracle_sketch_entry.argtypes = [P, I64, I64, I32, I32, I32, U64, I32]
             lib.oracle_sketch_entry.restype = ctypes.c_double
             _lib = lib
@@ -315,6 +322,56 @@ def factor_reduced(X: np.ndarray, k: int, l: int, sketch: int = GAUSSIAN, zeta: 
     if st != OK:
         raise OracleError(st, "factor_reduced")
     return {"Z": Z, "R": R, "Y": Y, "S": S}
+
+
+def colnorms(X: np.ndarray) -> np.ndarray:
+    """D = diag(||X(:, j)||_2), compensated (Alg. 7 normalisation)."""
+    X = np.ascontiguousarray(X)
+    m, n = X.shape
+    d = np.empty(n, dtype=np.float64)
+    st = _L().oracle_colnorms(_ptr(X), _dtype_code(X), m, n, n, _ptr(d))
+    if st != OK:
+        raise OracleError(st, "colnorms")
+    return d
+
+
+def rrqr(P: np.ndarray, tau: float, f: float = 1.5, rank_fixed: int = 0, want_S: bool = False) -> dict:
+    """Strong RRQR of P (Alg. 7 steps 2-3, reading A21): dict(perm, R (n x n of P[:, perm]), rank, swaps, S)."""
+    P = np.ascontiguousarray(P, dtype=np.float64)
+    k, n = P.shape
+    perm = np.empty(n, dtype=np.int32)
+    R = np.empty((n, n), dtype=np.float64)
+    S = np.empty((k, n), dtype=np.float64) if want_S else None
+    rank = ctypes.c_int(0)
+    swaps = ctypes.c_int(0)
+    st = _L().oracle_rrqr(_ptr(P), k, n, float(tau), float(f), int(rank_fixed), _ptr(perm), _ptr(R), _ptr(S),
+                          ctypes.byref(rank), ctypes.byref(swaps))
+    if st not in (OK, E_SINGULAR):
+        raise OracleError(st, "rrqr")
+    return {"perm": perm, "R": R, "rank": rank.value, "swaps": swaps.value, "S": S, "status": st}
+
+
+def factor_rr(X: np.ndarray, k: int, tau: float, f: float = 1.5, rank_fixed: int = 0, sketch: int = GAUSSIAN,
+              zeta: int = 8, seed: int = 0, row_offset: int = 0, want_S: bool = False) -> dict:
+    """Whole Algorithm 7 (RRRCholeskyQR): dict(Q (m x r), R (r x n), perm, rank, D, S, swaps)
+    with X[:, perm] ~= Q R."""
+    X = np.ascontiguousarray(X)
+    m, n = X.shape
+    Q = np.zeros_like(X)
+    R = np.empty((n, n), dtype=np.float64)
+    perm = np.empty(n, dtype=np.int32)
+    D = np.empty(n, dtype=np.float64)
+    S = np.empty((k, n), dtype=np.float64) if want_S else None
+    rank = ctypes.c_int(0)
+    swaps = ctypes.c_int(0)
+    st = _L().oracle_factor_rr(_ptr(X), _dtype_code(X), m, n, n, row_offset, k, sketch, zeta, seed, float(tau),
+                               float(f), int(rank_fixed), _ptr(Q), n, _ptr(R), _ptr(perm), ctypes.byref(rank),
+                               _ptr(D), _ptr(S), ctypes.byref(swaps))
+    if st != OK:
+        raise OracleError(st, "factor_rr")
+    r = rank.value
+    return {"Q": Q[:, :r].copy(), "R": R[:r].copy(), "perm": perm, "rank": r, "D": D,
+            "S": None if S is None else S[:, :r].copy(), "swaps": swaps.value}
 
 
 # ---------------------------------------------------------------- metrics (PAPER.md:773, 797)

@@ -595,6 +595,258 @@ int oracle_factor_reduced(const void* X, int dtype, int64_t m, int n, int64_t ld
     return st;
 }
 
+/* ------------------------------------------------------------------------------------------
+ * Algorithm 7, rank-revealing RCholeskyQR (alg:RRRCholeskyQR), with the column
+ * normalisation of PAPER.md:350:
+ *   1. P <- Theta X, D = diag(||X(:,j)||_2) in the same pass; P <- P D^{-1}
+ *   2. [S, R, Pi] <- RRQR(P): strong rank-revealing QR (Gu & Eisenstat 1996, f = 1.5; PAPER.md:652,
+ *      778), reading A21: Businger-Golub column pivoting picks Pi, then -- for the rank r of step 3 --
+ *      Gu-Eisenstat swaps of a leading column i and a trailing column r + j while
+ *      rho_ij = sqrt((R11^{-1} R12)_ij^2 + (gamma_j(R22) / omega_i(R11))^2) > f.
+ *   3. r = min r such that ||R(r+1:n, r+1:n)||_F <= tau ||R||_2
+ *   4. Q <- (X Pi(:, 1:r)) R(1:r, 1:r)^{-1}  (with R already post-processed R <- R Pi^T D Pi)
+ *   5. R <- R(1:r, :)
+ * ---------------------------------------------------------------------------------------- */
+
+/* d_j = ||X(:, j)||_2: compensated sums of squares (Dot2) in the fixed 65536-row blocks. */
+int oracle_colnorms(const void* X, int dtype, int64_t m, int n, int64_t ldx, double* d) {
+    if (!d || n < 1 || ldx < n || m < 0 || (m > 0 && !X)) return OR_E_INVALID;
+    int64_t nb = (m + OR_SKETCH_BLOCK - 1) / OR_SKETCH_BLOCK;
+    if (nb == 0) nb = 1;
+    double* part = (double*)calloc((size_t)nb * n * 2, sizeof(double));
+    if (!part) return OR_E_NOMEM;
+    #pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t b = 0; b < nb; ++b) {
+        double* ps = part + (size_t)b * n * 2;
+        double* pc = ps + n;
+        int64_t i0 = b * OR_SKETCH_BLOCK, i1 = i0 + OR_SKETCH_BLOCK < m ? i0 + OR_SKETCH_BLOCK : m;
+        for (int64_t i = i0; i < i1; ++i)
+            for (int j = 0; j < n; ++j) {
+                double x = load_x(X, dtype, i * ldx + j);
+                dot2_add(&ps[j], &pc[j], x, x);
+            }
+    }
+    for (int j = 0; j < n; ++j) {
+        double s = 0.0, c = 0.0;
+        for (int64_t b = 0; b < nb; ++b) {
+            sum2_add(&s, &c, part[(size_t)b * n * 2 + j]);
+            c += part[(size_t)b * n * 2 + n + j];
+        }
+        d[j] = sqrt(s + c);
+    }
+    free(part);
+    for (int j = 0; j < n; ++j)
+        if (!isfinite(d[j])) return OR_E_NONFINITE;
+    return OR_OK;
+}
+
+/* Businger-Golub QR with column pivoting of the k x n matrix P (k >= n): at step j the pivot is the
+ * first trailing column of largest 2-norm over rows j..k-1 (norms recomputed, not downdated); the
+ * reflectors are those of oracle_householder.  Only the permutation is returned (perm[j] = original
+ * column in position j); R is recomputed by oracle_householder on P(:, perm), which performs the
+ * same operations. */
+static int qrcp_perm(const double* P, int k, int n, int* perm) {
+    double* A = (double*)malloc(sizeof(double) * (size_t)k * n);   /* column-major working copy */
+    if (!A) return OR_E_NOMEM;
+    for (int i = 0; i < k; ++i)
+        for (int j = 0; j < n; ++j) A[(size_t)j * k + i] = P[(size_t)i * n + j];
+    for (int j = 0; j < n; ++j) perm[j] = j;
+    for (int j = 0; j < n; ++j) {
+        int best = j;
+        double bn = -1.0;
+        for (int l = j; l < n; ++l) {
+            double ss = 0.0;
+            for (int i = j; i < k; ++i) ss += A[(size_t)l * k + i] * A[(size_t)l * k + i];
+            if (ss > bn) { bn = ss; best = l; }
+        }
+        if (best != j) {
+            for (int i = 0; i < k; ++i) {
+                double t = A[(size_t)j * k + i];
+                A[(size_t)j * k + i] = A[(size_t)best * k + i];
+                A[(size_t)best * k + i] = t;
+            }
+            int t = perm[j]; perm[j] = perm[best]; perm[best] = t;
+        }
+        double* a = A + (size_t)j * k;
+        double alpha = sqrt(bn);
+        if (alpha == 0.0) break;                       /* the trailing columns are all zero */
+        double v0 = a[j] + (a[j] >= 0.0 ? alpha : -alpha);
+        double scale = 1.0 / (alpha * fabs(v0));
+        for (int l = j + 1; l < n; ++l) {
+            double* c = A + (size_t)l * k;
+            double dot = v0 * c[j];
+            for (int i = j + 1; i < k; ++i) dot += a[i] * c[i];
+            double t = dot * scale;
+            c[j] -= t * v0;
+            for (int i = j + 1; i < k; ++i) c[i] -= t * a[i];
+        }
+        a[j] = a[j] >= 0.0 ? -alpha : alpha;
+        for (int i = j + 1; i < k; ++i) a[i] = 0.0;
+    }
+    free(A);
+    return OR_OK;
+}
+
+/* ||R||_2 of the n x n upper triangular R (reading A21): 64 power iterations on R^T R from the
+ * all-ones vector, sigma = ||R x|| for the final unit x. */
+static double norm2_upper(const double* R, int n) {
+    double* x = (double*)malloc(sizeof(double) * (size_t)n);
+    double* y = (double*)malloc(sizeof(double) * (size_t)n);
+    for (int j = 0; j < n; ++j) x[j] = 1.0 / sqrt((double)n);
+    double sigma = 0.0;
+    for (int it = 0; it <= 64; ++it) {
+        for (int i = 0; i < n; ++i) {                  /* y = R x */
+            double s = 0.0;
+            for (int j = i; j < n; ++j) s += R[(size_t)i * n + j] * x[j];
+            y[i] = s;
+        }
+        double ny = 0.0;
+        for (int i = 0; i < n; ++i) ny += y[i] * y[i];
+        sigma = sqrt(ny);
+        if (it == 64 || sigma == 0.0) break;
+        for (int j = 0; j < n; ++j) {                  /* x = R^T y / ||R^T y|| */
+            double s = 0.0;
+            for (int i = 0; i <= j; ++i) s += R[(size_t)i * n + j] * y[i];
+            x[j] = s;
+        }
+        double nx = 0.0;
+        for (int j = 0; j < n; ++j) nx += x[j] * x[j];
+        nx = sqrt(nx);
+        if (nx == 0.0) break;
+        for (int j = 0; j < n; ++j) x[j] /= nx;
+    }
+    free(x); free(y);
+    return sigma;
+}
+
+/* Step 3: min r with ||R(r:n, r:n)||_F <= tau ||R||_2 (0-based r = number of kept columns). */
+static int rank_rule(const double* R, int n, double tau) {
+    double thr = tau * norm2_upper(R, n);
+    /* t_r^2 = sum_{i >= r, j >= i} R_ij^2, accumulated from the bottom-right corner */
+    double t2 = 0.0;
+    int r = n;
+    for (int j = n - 1; j >= 0; --j) {               /* t_j^2 = t_{j+1}^2 + row j of the trailing block */
+        double row = 0.0;
+        for (int l = j; l < n; ++l) row += R[(size_t)j * n + l] * R[(size_t)j * n + l];
+        t2 += row;
+        if (sqrt(t2) <= thr) r = j;
+        else break;
+    }
+    return r;
+}
+
+/* Strong-RRQR check at rank r for the upper triangular R (n x n): returns max rho_ij^2 and its (i, j)
+ * (j counted from r), rho_ij^2 = (R11^{-1} R12)_ij^2 + (gamma_j(R22) / omega_i(R11))^2 with
+ * omega_i = 1 / ||row i of R11^{-1}||, gamma_j = ||column j of R22||. */
+static double strong_rho(const double* R, int n, int r, int* bi, int* bj) {
+    double* W = (double*)calloc((size_t)r * r, sizeof(double));   /* R11^{-1}, upper */
+    for (int j = 0; j < r; ++j) {                                  /* column j: R11 w = e_j */
+        for (int i = j; i >= 0; --i) {
+            double s = i == j ? 1.0 : 0.0;
+            for (int l = i + 1; l <= j; ++l) s -= R[(size_t)i * n + l] * W[(size_t)l * r + j];
+            W[(size_t)i * r + j] = s / R[(size_t)i * n + i];
+        }
+    }
+    double best = -1.0;
+    *bi = 0; *bj = 0;
+    for (int i = 0; i < r; ++i) {
+        double wi2 = 0.0;                                          /* 1 / omega_i^2 */
+        for (int l = i; l < r; ++l) wi2 += W[(size_t)i * r + l] * W[(size_t)i * r + l];
+        for (int j = 0; j < n - r; ++j) {
+            double a = 0.0;                                        /* (R11^{-1} R12)_ij */
+            for (int l = i; l < r; ++l) a += W[(size_t)i * r + l] * R[(size_t)l * n + r + j];
+            double g2 = 0.0;                                       /* gamma_j^2 */
+            for (int l = r; l <= r + j; ++l) g2 += R[(size_t)l * n + r + j] * R[(size_t)l * n + r + j];
+            double rho2 = a * a + g2 * wi2;
+            if (rho2 > best) { best = rho2; *bi = i; *bj = j; }
+        }
+    }
+    free(W);
+    return best;
+}
+
+/* RRQR of the k x n matrix P (step 2 + step 3).  Outputs perm (n), R (n x n, of P(:, perm), diag >= 0),
+ * S (k x n, optional), *rank, *swaps.  rank_fixed > 0 replaces the tau rule (fixed-rank strong RRQR). */
+int oracle_rrqr(const double* P, int k, int n, double tau, double f, int rank_fixed, int* perm, double* R,
+                double* S, int* rank, int* swaps) {
+    if (!P || !perm || !R || !rank || n < 1) return OR_E_INVALID;
+    if (k < n) return OR_E_SHAPE;
+    double* Pp = (double*)malloc(sizeof(double) * (size_t)k * n);
+    if (!Pp) return OR_E_NOMEM;
+    int st = qrcp_perm(P, k, n, perm);
+    int nsw = 0, r = 0;
+    for (int pass = 0; st == OR_OK; ++pass) {
+        for (int i = 0; i < k; ++i)
+            for (int j = 0; j < n; ++j) Pp[(size_t)i * n + j] = P[(size_t)i * n + perm[j]];
+        st = oracle_householder(Pp, k, n, R, S);
+        if (st == OR_E_SINGULAR) st = OR_OK;          /* zero pivots are expected beyond the rank */
+        if (st != OR_OK) break;
+        if (pass == 0) r = rank_fixed > 0 ? (rank_fixed < n ? rank_fixed : n) : rank_rule(R, n, tau);
+        if (r == 0 || r == n || pass >= 64) break;
+        int bi, bj;
+        if (strong_rho(R, n, r, &bi, &bj) <= f * f) break;
+        int t = perm[bi]; perm[bi] = perm[r + bj]; perm[r + bj] = t;
+        ++nsw;
+    }
+    free(Pp);
+    *rank = r;
+    if (swaps) *swaps = nsw;
+    if (st == OR_OK && r == 0) st = OR_E_SINGULAR;
+    return st;
+}
+
+/* Whole Algorithm 7.  Outputs: Q (m x r, ldq >= n columns available), R (n x n buffer: rows 0..r-1 hold
+ * R(1:r, :) Pi^T D Pi, the rest zero), perm (n), *rank, D (n, optional), S (k x n buffer, optional: the
+ * first r columns are Alg. 7's S), *swaps. */
+int oracle_factor_rr(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
+                     int sketch, int zeta, uint64_t seed, double tau, double f, int rank_fixed, void* Q,
+                     int64_t ldq, double* R, int* perm, int* rank, double* D_out, double* S, int* swaps) {
+    if (!R || !perm || !rank || !Q) return OR_E_INVALID;
+    if (k < n) return OR_E_SHAPE;
+    double* P = (double*)malloc(sizeof(double) * (size_t)k * n);
+    double* D = D_out ? D_out : (double*)malloc(sizeof(double) * (size_t)n);
+    if (!P || !D) { free(P); if (!D_out) free(D); return OR_E_NOMEM; }
+    int st = oracle_sketch(X, dtype, m, n, ldx, row_offset, k, sketch, zeta, seed, P);
+    if (st == OR_OK) st = oracle_colnorms(X, dtype, m, n, ldx, D);
+    if (st == OR_OK)                                   /* P <- P D^{-1} (zero columns stay zero) */
+        for (int i = 0; i < k; ++i)
+            for (int j = 0; j < n; ++j) P[(size_t)i * n + j] = D[j] > 0.0 ? P[(size_t)i * n + j] / D[j] : 0.0;
+    int r = 0;
+    if (st == OR_OK) st = oracle_rrqr(P, k, n, tau, f, rank_fixed, perm, R, S, &r, swaps);
+    *rank = r;
+    if (st == OR_OK) {
+        /* R <- R(1:r, :) Pi^T D Pi: column l of the permuted R is scaled by d_{perm[l]} */
+        for (int i = 0; i < n; ++i)
+            for (int l = 0; l < n; ++l) R[(size_t)i * n + l] = i < r ? R[(size_t)i * n + l] * D[perm[l]] : 0.0;
+        /* Q <- (X Pi(:, 1:r)) R(1:r, 1:r)^{-1} by forward substitution */
+        size_t es = dtype == 0 ? 8 : 4;
+        void* Xr = malloc(es * (size_t)(m > 0 ? m : 1) * r);
+        double* R11 = (double*)malloc(sizeof(double) * (size_t)r * r);
+        if (!Xr || !R11) st = OR_E_NOMEM;
+        else {
+            for (int64_t i = 0; i < m; ++i)
+                for (int j = 0; j < r; ++j) {
+                    if (dtype == 0) ((double*)Xr)[i * r + j] = ((const double*)X)[i * ldx + perm[j]];
+                    else ((float*)Xr)[i * r + j] = ((const float*)X)[i * ldx + perm[j]];
+                }
+            for (int i = 0; i < r; ++i)
+                for (int j = 0; j < r; ++j) R11[(size_t)i * r + j] = R[(size_t)i * n + j];
+            void* Qr = malloc(es * (size_t)(m > 0 ? m : 1) * r);
+            if (!Qr) st = OR_E_NOMEM;
+            else {
+                st = oracle_forward_subst(Xr, dtype, m, r, r, R11, Qr, r);
+                for (int64_t i = 0; st == OR_OK && i < m; ++i)
+                    memcpy((char*)Q + (size_t)i * ldq * es, (char*)Qr + (size_t)i * r * es, es * (size_t)r);
+                free(Qr);
+            }
+        }
+        free(Xr); free(R11);
+    }
+    free(P);
+    if (!D_out) free(D);
+    return st;
+}
+
 /* One sketch entry P_rj = sum_i Theta_ri x_i for a single column x (m fp64 values), in the same
  * fixed-block order as oracle_sketch -- used to check sampled entries of full-size sketches. */
 double oracle_sketch_entry(const double* x, int64_t m, int64_t row_offset, int k, int sketch, int zeta,

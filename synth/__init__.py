@@ -47,6 +47,22 @@ def make_X(m: int, n: int, log10_cond: float, dtype: str = "f64", seed: int = X_
     return np.ascontiguousarray(X if dtype == "f64" else X.astype(np.float32))
 
 
+def make_X_lowrank(m: int, n: int, rank: int, log10_cond: float = 2.0, noise: float = 0.0, dtype: str = "f64",
+                   seed: int = X_SEED) -> np.ndarray:
+    """Numerically rank-deficient X for Alg. 7 (PAPER.md:856's third experiment, simplified):
+    X = (G diag(sigma) ) B with G m x rank Gaussian, sigma graded over 10^log10_cond and B a rank x n
+    Gaussian, plus noise * (an independent Gaussian m x n) / sqrt(m); columns carry norms of varying
+    size (column j scaled by 2^(j mod 5 - 2)) so the normalisation D of PAPER.md:350 matters."""
+    rng = np.random.Generator(np.random.PCG64([seed, 7]))
+    G = rng.standard_normal((m, rank))
+    B = rng.standard_normal((rank, n))
+    X = (G * sigma(rank, log10_cond)[None, :]) @ B
+    if noise:
+        X = X + noise * rng.standard_normal((m, n)) * np.linalg.norm(X) / np.sqrt(m * n)
+    X = X * (2.0 ** (np.arange(n) % 5 - 2))[None, :]
+    return np.ascontiguousarray(X if dtype == "f64" else X.astype(np.float32))
+
+
 CHUNK_ROWS = 1 << 18
 
 
