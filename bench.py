@@ -108,12 +108,14 @@ def _workload(cfg_name: str, ws: int, rank: int):
     return cfg, m_local, m_global, ro, scaling
 
 
-def _cpu_sample_rate(X_dev, cfg, target_s: float, algo: str = "rcholqr", l: int = 0):
+def _cpu_sample_rate(X_dev, cfg, target_s: float, algo: str = "rcholqr", l: int = 0, tau: float = 0.0):
     """Time the oracle (as it stands, all host cores) on a bounded leading sample of X."""
     import oracle
     so = oracle.GAUSSIAN if cfg["sketch"] == "gaussian" else oracle.SPARSE_SIGN
     if algo == "rcholqr2":
         run = lambda A: oracle.factor2(A, cfg["k"], sketch=so, zeta=cfg["nnz"])  # noqa: E731
+    elif algo == "rcholqr_rr":
+        run = lambda A: oracle.factor_rr(A, cfg["k"], tau, sketch=so, zeta=cfg["nnz"])  # noqa: E731
     elif algo == "rcholqr_reduced":
         run = lambda A: oracle.factor_reduced(A, cfg["k"], l, sketch=so, zeta=cfg["nnz"], want_S=False)  # noqa: E731
     else:
@@ -207,8 +209,14 @@ def run(args):
     l_red = args.l or k                     # Alg. 5: rows of the extractor L (default: as many as Theta)
     Z = torch.empty((l_red, n), dtype=torch.float64, device=dev) if args.algo == "rcholqr_reduced" else None
 
+    # Alg. 7: the paper's truncation tolerances (4e-15 in fp64; 2e-7 in fp32)
+    tau_rr = args.tau if args.tau > 0 else (4e-15 if dt == "f64" else 2e-7)
+    rr_last = {}
+
     def step():
-        if args.algo == "rcholqr2":   # Alg. 3: synchronous (status read inside the call)
+        if args.algo == "rcholqr_rr":   # Alg. 7: synchronous (rank and swap decisions on the host)
+            rr_last.update(plan.factor_rr(X, tau_rr, row_offset=ro, Q=Q, R=R, stream=stream))
+        elif args.algo == "rcholqr2":   # Alg. 3: synchronous (status read inside the call)
             plan.factor2(X, row_offset=ro, Q=Q, R=R, Rprime=Rp, stream=stream)
         elif args.algo == "rcholqr_reduced":   # Alg. 5: synchronous
             plan.factor_reduced(X, l_red, row_offset=ro, Z=Z, R=R, stream=stream)
@@ -285,6 +293,8 @@ def run(args):
     hbm = peaks.get("hbm_gbs", 6545.0)
     roofs = {}
     reduced = args.algo == "rcholqr_reduced"
+    rr = args.algo == "rcholqr_rr"
+    r_rr = rr_last.get("rank", n)
     k_sk = k + l_red if reduced else k      # Alg. 5 with a Gaussian Theta: one (k + l)-row sketch
     if cfg["sketch"] == "gaussian":
         # exact int8 digit-product sketch (sketch_gtc.cu); its algorithmic work is the method's 2kmn
@@ -316,6 +326,27 @@ def run(args):
                            "algorithmic": f"m*n*s_x = {byts:.4g} B per launch (one read of X)", "traffic": None}
     if reduced:
         pass                                 # step 3 is the tiny l x n substitution (rowsub_kernel)
+    elif rr:
+        # Alg. 7: column norms (one read of X), gather of the r kept columns, solve with r columns
+        byts = m_local * n * s_x
+        ach = byts / (per_ms["reduce"] * 1e-3) / 1e9
+        roofs["colnorms"] = {"kernel": "colsq_kernel", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                             "frac": ach / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                             "algorithmic": f"m*n*s_x = {byts:.4g} B (one read of X)", "traffic": None}
+        byts = 2.0 * m_local * r_rr * s_x
+        ach = byts / (per_ms["tri_prep"] * 1e-3) / 1e9
+        roofs["gather"] = {"kernel": "gather_x_kernel", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                           "frac": ach / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                           "algorithmic": f"2*m*r*s_x = {byts:.4g} B (read r columns, write them packed)",
+                           "traffic": None}
+        flops = float(m_local) * r_rr * r_rr
+        ach = flops / (per_ms["solve"] * 1e-3) / 1e12
+        roofs["solve"] = {"kernel": "blocked substitution (fp64 DMMA), r columns", "bound": "tensor", "achieved": ach,
+                          "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
+                          "peak_source": "FP64 DMMA peak 37.2 TF", "algorithmic": f"m*r^2 = {flops:.4g} flop",
+                          "traffic": None}
+        per_ms = {"sketch": per_ms["sketch"], "colnorms": per_ms["reduce"], "allreduce": per_ms["allreduce"],
+                  "rrqr": per_ms["small_qr"], "gather": per_ms["tri_prep"], "solve": per_ms["solve"]}
     elif dt == "f32" and n <= 64:
         byts = 2.0 * m_local * n * s_x
         ach = byts / (per_ms["solve"] * 1e-3) / 1e9
@@ -391,9 +422,26 @@ def run(args):
         # Alg. 2's launches minus its solve (prep + solve) plus the Z substitution
         line["gpu_launches"] = (plan.launches_per_factor(m_local) - 1) * args.steps
         line["e2e"] = None
+    if rr:
+        # Alg. 7 passes: sketch + column norms (2 reads of X), gather (r/n read + write), solve (r/n read + write)
+        t_hbm7 = (2.0 + 4.0 * r_rr / n) * m_local * n * s_x / (hbm * 1e9)
+        t_flop7 = float(m_local) * r_rr * r_rr / (DMMA_PEAK_TFLOPS * 1e12)
+        line["metric"] = "RRRCholQR factor throughput (GB/s of X)"
+        line["config"]["algo"] = f"rcholqr_rr (Alg. 7, tau = {tau_rr:g}, f = 1.5)"
+        line["config"]["rank"] = r_rr
+        line["config"]["swaps"] = rr_last.get("swaps")
+        line["northstar_roofline"] = {"t_hbm_ms": t_hbm7 * 1e3, "t_fp64_ms": t_flop7 * 1e3,
+                                      "roofline_ms": max(t_hbm7, t_flop7) * 1e3,
+                                      "frac": max(t_hbm7, t_flop7) * 1e3 / ms,
+                                      "note": "Alg. 7 accounting: (2 + 4 r/n) passes over m x n, m r^2 fp64 flops"}
+        # sketch launches + colsq (2) + normalize + qrcp + gather + QR + rank + strong + finalize + gather_x
+        # + check_diag + solve
+        line["gpu_launches"] = (plan.launches_per_factor(m_local) + 10) * args.steps
+        line["e2e"] = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
-        rows, dt_s, cores = _cpu_sample_rate(X, cfg, args.cpu_seconds, args.algo, l_red)
-        fn = {"rcholqr2": "factor2", "rcholqr_reduced": "factor_reduced"}.get(args.algo, "factor")
+        rows, dt_s, cores = _cpu_sample_rate(X, cfg, args.cpu_seconds, args.algo, l_red, tau_rr)
+        fn = {"rcholqr2": "factor2", "rcholqr_reduced": "factor_reduced", "rcholqr_rr": "factor_rr"}.get(args.algo,
+                                                                                                       "factor")
         line["cpu_baseline"] = {"value": rows * n * s_x / dt_s / 1e9, "unit": "GB/s", "cores": cores,
                                 "kind": "oracle", "seconds": dt_s,
                                 "sample": f"oracle.{fn} on the leading {rows} rows of the same X"}
@@ -417,10 +465,12 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--algo", default="rcholqr", choices=["rcholqr", "rcholqr2", "rcholqr_reduced"],
+    ap.add_argument("--algo", default="rcholqr", choices=["rcholqr", "rcholqr2", "rcholqr_reduced", "rcholqr_rr"],
                     help="Alg. 2 (default, the north star), Alg. 3 RCholeskyQR2 (orthonormal Q) or Alg. 5 "
                          "reduced RCholeskyQR (Z = L Q)")
     ap.add_argument("--l", type=int, default=0, help="Alg. 5: rows of the extractor L (default k)")
+    ap.add_argument("--tau", type=float, default=0.0,
+                    help="Alg. 7: truncation tolerance (default: the paper's 4e-15 fp64 / 2e-7 fp32)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

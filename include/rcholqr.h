@@ -137,6 +137,31 @@ rcholqr_status rcholqr_factor_reduced(rcholqr_plan plan, const void* X, int64_t 
                                       int64_t ldx, int32_t l, double* Z, double* R, double* S, double* Y,
                                       void* stream);
 
+/* Rank-revealing RCholeskyQR (Alg. 7, alg:RRRCholeskyQR; reading A21):
+ * X Pi ~= Q R with Q (m x r) well conditioned and R (r x n) upper trapezoidal, for numerically
+ * rank-deficient X.  P = Theta X and D = diag(||X(:, j)||) in step 1 (one all-reduce of both),
+ * P <- P D^{-1}, strong RRQR of P (column pivoting + Gu-Eisenstat swaps with parameter f),
+ * r = min r with ||R(r+1:n, r+1:n)||_F <= tau ||R||_2, Q = (X Pi(:, 1:r)) R(1:r, 1:r)^{-1},
+ * R <- R(1:r, :) Pi^T D Pi.
+ *   X, m_local, row_offset, ldx, stream: as for rcholqr_factor.
+ *   tau         truncation tolerance (>= 0; the paper uses ~1e-15 in fp64, ~1e-7 in fp32).
+ *   f           strong-RRQR parameter (> 1; the paper's 1.5).
+ *   rank_fixed  0: r from tau; > 0: r = min(rank_fixed, n) (fixed-rank strong RRQR).
+ *   Q     [device] m_local x n buffer (ldq >= n); columns 0..r-1 receive Q (X's dtype), the rest untouched.
+ *   R     [device] n x n fp64 (row-major, ld n): rows 0..r-1 = R(1:r, :) in permuted column order, rows
+ *         r..n-1 zero.
+ *   perm  [device] n int32: Pi as perm[j] = original column in position j.
+ *   D     [device] n fp64 column norms or NULL;  S [device] k x n fp64 or NULL (columns 0..r-1 = S).
+ *   rank_out, swaps_out [host] int32: r and the number of Gu-Eisenstat swaps (swaps_out may be NULL).
+ * Status: E_INVALID (arguments, f <= 1, tau < 0), E_NONFINITE, E_SINGULAR if r = 0 (X = 0).
+ * Memory: the plan allocates an O(k n) workspace on first use and an m_local x r gather buffer.
+ * SYNCHRONOUS (the rank and each swap decision are read on the host).  With a communicator every
+ * rank must call this (one all-reduce); Pi, r and R are identical on every rank. */
+rcholqr_status rcholqr_factor_rr(rcholqr_plan plan, const void* X, int64_t m_local, int64_t row_offset,
+                                 int64_t ldx, double tau, double f, int32_t rank_fixed, void* Q, int64_t ldq,
+                                 double* R, int32_t* perm, double* D, double* S, int32_t* rank_out,
+                                 int32_t* swaps_out, void* stream);
+
 /* ---- step-level entry points (same kernels as rcholqr_factor; used by the parity tests) ---- */
 
 /* Step 1 (+ the all-reduce when the plan has a communicator): P = Theta X, k x n fp64 row-major

@@ -6,8 +6,10 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <mutex>
+#include <vector>
 #include "internal.cuh"
 #include "rcholqr.h"
 
@@ -46,16 +48,23 @@ bool nccl_load() {
 }  // namespace
 
 // ---------------------------------------------------------------------------------------------
+// Which tall-solve kernels serve n columns of dtype (the plan's n, or Alg. 7's rank r).
+struct SolvePlan {
+  TrsmLaunch tr{};
+  int res_tm = 0, warp_solve = 0, stream_tb = 0;
+  bool solve_tc = false;
+};
+
 struct rcholqr_plan_s {
   rcholqr_desc d;
   int sms = 0;
   size_t smem_optin = 0;
   SketchLaunch sk{};
-  TrsmLaunch tr{};
-  int res_tm = 0;           // > 0: blocked-substitution resident solve with this row tile
-  int warp_solve = 0;       // > 0: warp-independent blocked substitution with this many warps/CTA
-  int stream_tb = 0;        // > 0: streamed blocked substitution (fp64, n > 128) with this block width
-  bool solve_tc = false;    // fp32 X, n <= 64: tcgen05 digit solve Q = X R^{-1} (solve_tc.cu)
+  // tall-solve kernels for n columns: TrsmLaunch tr (R^{-1} GEMM); res_tm > 0: blocked-substitution
+  // resident solve with this row tile; warp_solve > 0: warp-independent blocked substitution with this
+  // many warps/CTA; stream_tb > 0: streamed blocked substitution (fp64, n > 128) with this block width;
+  // solve_tc: fp32 X, n <= 64, tcgen05 digit solve Q = X R^{-1} (solve_tc.cu)
+  SolvePlan sp{};
   void* xdig = nullptr;     // pre-split X digit planes of the tcgen05 Gaussian sketch (grown on demand)
   // RCholeskyQR2 (rcqr2.cu): Gram partials, A, Cholesky work, R', R1, and Q1 (grown on demand)
   int gram_splits = 0;
@@ -65,6 +74,13 @@ struct rcholqr_plan_s {
   int red_l = 0;
   SketchLaunch red_sk{};
   double* red_part = nullptr; double* red_partc = nullptr; double* red_P = nullptr;
+  // rank-revealing RCholeskyQR (Alg. 7), allocated on first use: [P; colsq] (k + 1) x n, P D^{-1},
+  // the pivoting workspace, P(:, perm), R, R11^{-1}, the compact R11, d, column partials, scalars
+  double* rr_buf = nullptr; double* rr_Pn = nullptr; double* rr_A = nullptr; double* rr_Pg = nullptr;
+  double* rr_R = nullptr; double* rr_W = nullptr; double* rr_R11 = nullptr; double* rr_d = nullptr;
+  double* rr_cpart = nullptr; double* rr_sd = nullptr; int* rr_si = nullptr; int* rr_perm = nullptr;
+  int* rr_qst = nullptr; int rr_splits = 0;
+  void* rr_xr = nullptr; size_t rr_xr_bytes = 0;
   size_t xdig_bytes = 0;
   void* qws = nullptr;      // its W-digit workspace
   double* tbuf = nullptr;   // [m_local][stream_tb] T_J workspace of the streamed solve
@@ -195,11 +211,30 @@ rcholqr_status do_sketch(rcholqr_plan p, const void* X, int64_t m, int64_t ro, i
   return RCHOLQR_OK;
 }
 
-// Step 3: triangular prep + tall solve (blocked substitution when resident, else R^{-1} GEMM).
+SolvePlan plan_solve(int n, int dtype, size_t smem_optin) {
+  SolvePlan s;
+  s.tr = plan_trsm(n, dtype, smem_optin);
+  s.res_tm = trsm_resident_tm(n, dtype, smem_optin);
+  s.warp_solve = trsm_warp_count(n, smem_optin);
+  if (s.warp_solve == 0 && s.res_tm == 0 && dtype == RCHOLQR_F64) s.stream_tb = n < 512 ? 64 : 128;
+  if (const char* f = getenv("RCHOLQR_SOLVE")) {  // experiments: 0 = inverse GEMM, 1 = CTA-resident, 2 = warp
+    const int v = atoi(f);
+    if (v != 2) s.warp_solve = 0;
+    if (v == 0) { s.res_tm = 0; s.stream_tb = 0; }
+  }
+  s.solve_tc = solve_tc_applicable(dtype, n);
+  return s;
+}
+
+// Step 3: triangular prep + tall solve (blocked substitution when resident, else R^{-1} GEMM).  `n_cols`
+// > 0 solves with that many columns (R n_cols x n_cols) instead of the plan's n.
 rcholqr_status solve(rcholqr_plan p, const void* X, int64_t m, int64_t ldx, const double* R, void* Q, int64_t ldq,
-                     cudaStream_t st, bool timed) {
-  const int n = p->d.n;
-  if (p->solve_tc && m > 0 && solve_tc_supported(X, m, ldx, Q, ldq)) {
+                     cudaStream_t st, bool timed, int n_cols = 0) {
+  const int n = n_cols > 0 ? n_cols : p->d.n;
+  SolvePlan sp_own;
+  if (n_cols > 0) sp_own = plan_solve(n, p->d.dtype, p->smem_optin);
+  const SolvePlan& sp = n_cols > 0 ? sp_own : p->sp;
+  if (sp.solve_tc && m > 0 && solve_tc_supported(X, m, ldx, Q, ldq)) {
     CU(launch_tri_inverse(R, n, p->W, p->status_d, st));
     if (timed && p->timing) cudaEventRecord(p->ev[5], st);
     const cudaError_t e = launch_solve_tc(p->W, n, (const float*)X, m, ldx, (float*)Q, ldq, p->qws, p->status_d,
@@ -207,9 +242,9 @@ rcholqr_status solve(rcholqr_plan p, const void* X, int64_t m, int64_t ldx, cons
     if (e == cudaSuccess) return RCHOLQR_OK;
     if (e != cudaErrorNotSupported) return cuda_status(e);
   }
-  if (p->stream_tb > 0) {
+  if (sp.stream_tb > 0) {
     // blocked substitution by column blocks of width tb, each = 2 fp64 DMMA GEMM launches
-    const int tb = p->stream_tb, npad = (n + 7) / 8 * 8;
+    const int tb = sp.stream_tb, npad = (n + 7) / 8 * 8;
     CU(launch_tri_prep_blocked(R, n, p->W, p->status_d, st, tb, npad));
     if (timed && p->timing) cudaEventRecord(p->ev[5], st);
     if (m > 0) {
@@ -231,18 +266,18 @@ rcholqr_status solve(rcholqr_plan p, const void* X, int64_t m, int64_t ldx, cons
                            p->status_d, st));
       }
     }
-  } else if (p->warp_solve > 0) {
+  } else if (sp.warp_solve > 0) {
     CU(launch_tri_prep_blocked(R, n, p->W, p->status_d, st));
     if (timed && p->timing) cudaEventRecord(p->ev[5], st);
-    if (m > 0) CU(launch_trsm_warp(p->warp_solve, X, p->d.dtype, m, n, ldx, p->W, Q, ldq, p->status_d, p->sms, st));
-  } else if (p->res_tm > 0) {
+    if (m > 0) CU(launch_trsm_warp(sp.warp_solve, X, p->d.dtype, m, n, ldx, p->W, Q, ldq, p->status_d, p->sms, st));
+  } else if (sp.res_tm > 0) {
     CU(launch_tri_prep_blocked(R, n, p->W, p->status_d, st));
     if (timed && p->timing) cudaEventRecord(p->ev[5], st);
-    if (m > 0) CU(launch_trsm_resident(p->res_tm, X, p->d.dtype, m, n, ldx, p->W, Q, ldq, p->status_d, p->sms, st));
+    if (m > 0) CU(launch_trsm_resident(sp.res_tm, X, p->d.dtype, m, n, ldx, p->W, Q, ldq, p->status_d, p->sms, st));
   } else {
     CU(launch_tri_inverse(R, n, p->W, p->status_d, st));
     if (timed && p->timing) cudaEventRecord(p->ev[5], st);
-    if (m > 0) CU(launch_trsm(p->tr, X, p->d.dtype, m, n, ldx, p->W, Q, ldq, p->status_d, st));
+    if (m > 0) CU(launch_trsm(sp.tr, X, p->d.dtype, m, n, ldx, p->W, Q, ldq, p->status_d, st));
   }
   return RCHOLQR_OK;
 }
@@ -301,16 +336,7 @@ rcholqr_status rcholqr_create(const rcholqr_desc* desc, rcholqr_plan* out) {
   p->smem_optin = prop.sharedMemPerBlockOptin;
   const int k = desc->k, n = desc->n;
   p->sk = plan_sketch(k, n, desc->dtype, desc->sketch, desc->nnz_per_col, p->sms, p->smem_optin);
-  p->tr = plan_trsm(n, desc->dtype, p->smem_optin);
-  p->res_tm = trsm_resident_tm(n, desc->dtype, p->smem_optin);
-  p->warp_solve = trsm_warp_count(n, p->smem_optin);
-  if (p->warp_solve == 0 && p->res_tm == 0 && desc->dtype == RCHOLQR_F64) p->stream_tb = n < 512 ? 64 : 128;
-  if (const char* f = getenv("RCHOLQR_SOLVE")) {  // experiments: 0 = inverse GEMM, 1 = CTA-resident, 2 = warp
-    const int v = atoi(f);
-    if (v != 2) p->warp_solve = 0;
-    if (v == 0) { p->res_tm = 0; p->stream_tb = 0; }
-  }
-  p->solve_tc = solve_tc_applicable(desc->dtype, n);
+  p->sp = plan_solve(n, desc->dtype, p->smem_optin);
   p->qr_kind = plan_qr(k, n, p->smem_optin);
   const size_t kn = (size_t)k * n, nn = (size_t)((n + 7) / 8 * 8) * ((n + 7) / 8 * 8);
   bool okalloc = cudaMalloc(&p->part, sizeof(double) * kn * p->sk.max_splits()) == cudaSuccess &&
@@ -347,6 +373,9 @@ rcholqr_status rcholqr_destroy(rcholqr_plan p) {
   cudaFree(p->Rtmp); cudaFree(p->status_d); cudaFree(p->flag_d); cudaFree(p->qws); cudaFree(p->xdig); cudaFree(p->qr_ws);
   cudaFree(p->gpart); cudaFree(p->gA); cudaFree(p->gW); cudaFree(p->gRp); cudaFree(p->gR1); cudaFree(p->q1buf);
   cudaFree(p->red_part); cudaFree(p->red_partc); cudaFree(p->red_P);
+  cudaFree(p->rr_buf); cudaFree(p->rr_Pn); cudaFree(p->rr_A); cudaFree(p->rr_Pg); cudaFree(p->rr_R); cudaFree(p->rr_W);
+  cudaFree(p->rr_R11); cudaFree(p->rr_d); cudaFree(p->rr_cpart); cudaFree(p->rr_sd); cudaFree(p->rr_si);
+  cudaFree(p->rr_perm); cudaFree(p->rr_qst); cudaFree(p->rr_xr);
   if (p->status_h) cudaFreeHost(p->status_h);
   cudaFree(p->xbuf); cudaFree(p->qbuf); cudaFree(p->rbuf); cudaFree(p->sbuf); cudaFree(p->tbuf);
   for (int t = 0; t < 7; ++t)
@@ -440,6 +469,9 @@ rcholqr_status rcholqr_factor_reduced(rcholqr_plan p, const void* X, int64_t m, 
   cudaStream_t st = (cudaStream_t)stream;
   if (p->red_l != l) {   // the (k + l)-row launch (Gaussian Theta) or the l-row extractor launch (sparse Theta)
     cudaFree(p->red_part); cudaFree(p->red_partc); cudaFree(p->red_P);
+  cudaFree(p->rr_buf); cudaFree(p->rr_Pn); cudaFree(p->rr_A); cudaFree(p->rr_Pg); cudaFree(p->rr_R); cudaFree(p->rr_W);
+  cudaFree(p->rr_R11); cudaFree(p->rr_d); cudaFree(p->rr_cpart); cudaFree(p->rr_sd); cudaFree(p->rr_si);
+  cudaFree(p->rr_perm); cudaFree(p->rr_qst); cudaFree(p->rr_xr);
     p->red_part = p->red_partc = p->red_P = nullptr;
     p->red_l = 0;
     p->red_sk = plan_sketch(gauss ? k + l : l, n, p->d.dtype, RCHOLQR_GAUSSIAN, p->d.nnz_per_col, p->sms, p->smem_optin);
@@ -489,6 +521,118 @@ rcholqr_status rcholqr_factor_reduced(rcholqr_plan p, const void* X, int64_t m, 
   rcholqr_status r = read_status(p, st);
   p->timing = t;
   return r;
+}
+
+rcholqr_status rcholqr_factor_rr(rcholqr_plan p, const void* X, int64_t m, int64_t ro, int64_t ldx, double tau,
+                                 double f, int32_t rank_fixed, void* Q, int64_t ldq, double* R, int32_t* perm,
+                                 double* D, double* S, int32_t* rank_out, int32_t* swaps_out, void* stream) {
+  rcholqr_status a = check_factor_args(p, X, m, ro, ldx, Q, ldq);
+  if (a != RCHOLQR_OK) return a;
+  if (!R || !perm || !rank_out || !(f > 1.0) || !(tau >= 0.0) || !std::isfinite(tau) || rank_fixed < 0)
+    return RCHOLQR_E_INVALID;
+  const int k = p->d.k, n = p->d.n;
+  const size_t kn = (size_t)k * n, nn = (size_t)n * n, es = esize(p->d.dtype);
+  DeviceGuard dg(p->d.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!p->rr_buf) {
+    p->rr_splits = colsq_splits(n, p->sms);
+    bool ok = cudaMalloc(&p->rr_buf, sizeof(double) * (kn + n)) == cudaSuccess &&
+              cudaMalloc(&p->rr_Pn, sizeof(double) * kn) == cudaSuccess &&
+              cudaMalloc(&p->rr_A, sizeof(double) * kn) == cudaSuccess &&
+              cudaMalloc(&p->rr_Pg, sizeof(double) * kn) == cudaSuccess &&
+              cudaMalloc(&p->rr_R, sizeof(double) * nn) == cudaSuccess &&
+              cudaMalloc(&p->rr_W, sizeof(double) * nn) == cudaSuccess &&
+              cudaMalloc(&p->rr_R11, sizeof(double) * nn) == cudaSuccess &&
+              cudaMalloc(&p->rr_d, sizeof(double) * n) == cudaSuccess &&
+              cudaMalloc(&p->rr_cpart, sizeof(double) * n * p->rr_splits) == cudaSuccess &&
+              cudaMalloc(&p->rr_sd, sizeof(double) * 2) == cudaSuccess &&
+              cudaMalloc(&p->rr_si, sizeof(int) * 2) == cudaSuccess &&
+              cudaMalloc(&p->rr_perm, sizeof(int) * n) == cudaSuccess &&
+              cudaMalloc(&p->rr_qst, sizeof(int)) == cudaSuccess;
+    if (!ok) { cudaGetLastError(); return RCHOLQR_E_NOMEM; }
+  }
+  const bool t = p->timing;
+  p->timing = false;
+  struct Restore { rcholqr_plan p; bool t; ~Restore() { p->timing = t; } } restore{p, t};
+  CU(cudaMemsetAsync(p->status_d, 0, sizeof(int), st));
+  // library events: sketch | column norms | all-reduce | RRQR (incl. host decisions) | gather | solve
+  if (t) cudaEventRecord(p->ev[0], st);
+  // 1. P = Theta X and the column sums of squares, all-reduced together as [P; colsq]
+  rcholqr_status s = do_sketch(p, X, m, ro, ldx, p->rr_buf, st, nullptr, 0, nullptr, nullptr, 0, false);
+  if (s != RCHOLQR_OK) return s;
+  if (t) cudaEventRecord(p->ev[1], st);
+  if (m > 0) CU(launch_colsq(X, p->d.dtype, m, n, ldx, p->rr_splits, p->rr_cpart, p->rr_buf + kn, p->status_d, st));
+  else CU(cudaMemsetAsync(p->rr_buf + kn, 0, sizeof(double) * n, st));
+  if (t) cudaEventRecord(p->ev[2], st);
+  if (p->d.nccl_comm) {
+    if (!nccl_load()) return RCHOLQR_E_NCCL;
+    if (g_nccl.AllReduce(p->rr_buf, p->rr_buf, kn + n, ncclFloat64, ncclSum, (ncclComm_t)p->d.nccl_comm, st) !=
+        ncclSuccess)
+      return RCHOLQR_E_NCCL;
+  }
+  if (t) cudaEventRecord(p->ev[3], st);
+  // (a non-finite P is caught by the final status read: every later kernel honours the status word)
+  // P <- P D^{-1}; column pivoting picks Pi
+  CU(launch_rr_normalize(p->rr_buf, k, n, p->rr_Pn, p->rr_d, st));
+  CU(launch_qrcp(p->rr_Pn, k, n, p->rr_A, p->rr_perm, st));
+  std::vector<int> hperm(n);
+  // 2.-3. R of P(:, Pi) (the Householder kernels of Alg. 2), the rank rule, Gu-Eisenstat swaps
+  int r = 0, swaps = 0;
+  for (int pass = 0;; ++pass) {
+    CU(launch_rr_gather(p->rr_Pn, k, n, p->rr_perm, p->rr_Pg, st));
+    CU(cudaMemsetAsync(p->rr_qst, 0, sizeof(int), st));   // zero pivots beyond the rank are expected
+    CU(launch_qr(p->qr_kind, p->rr_Pg, k, n, p->rr_R, p->Awork, p->diag, p->tau, p->qr_ws, p->rr_qst, st));
+    if (pass == 0) {   // one host round trip: the permutation and the rank
+      CU(launch_rank(p->rr_R, n, tau, rank_fixed, p->rr_si, p->rr_sd, st));
+      CU(cudaMemcpyAsync(hperm.data(), p->rr_perm, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+      CU(cudaMemcpyAsync(&r, p->rr_si, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+    }
+    if (r == 0 || r == n || pass >= 64) break;
+    double rho2 = 0.0;
+    int flat = 0;
+    CU(launch_strong(p->rr_R, n, r, p->rr_W, p->rr_sd + 1, p->rr_si + 1, st));
+    CU(cudaMemcpyAsync(&rho2, p->rr_sd + 1, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(&flat, p->rr_si + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    if (!(rho2 > f * f) || flat < 0 || flat >= r * (n - r)) break;
+    const int bi = flat / (n - r), bj = flat % (n - r);
+    std::swap(hperm[bi], hperm[r + bj]);
+    CU(cudaMemcpyAsync(p->rr_perm, hperm.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+    ++swaps;
+  }
+  *rank_out = r;
+  if (swaps_out) *swaps_out = swaps;
+  CU(cudaMemcpyAsync(perm, p->rr_perm, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
+  if (D) CU(cudaMemcpyAsync(D, p->rr_d, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  if (S) CU(launch_form_s(p->Awork, p->tau, p->diag, k, n, S, p->rr_qst, st));
+  if (r == 0) {
+    CU(cudaMemsetAsync(R, 0, sizeof(double) * nn, st));
+    CU(cudaStreamSynchronize(st));
+    return RCHOLQR_E_SINGULAR;
+  }
+  // R <- R(1:r, :) Pi^T D Pi;  4. Q = (X Pi(:, 1:r)) R11^{-1}
+  CU(launch_rr_finalize(p->rr_R, n, r, p->rr_d, p->rr_perm, R, p->rr_R11, st));
+  if (t) cudaEventRecord(p->ev[4], st);
+  if (m > 0) {
+    const size_t need = (size_t)m * r * es;
+    if (need > p->rr_xr_bytes) {
+      cudaFree(p->rr_xr);
+      p->rr_xr = nullptr; p->rr_xr_bytes = 0;
+      CU(cudaMalloc(&p->rr_xr, need));
+      p->rr_xr_bytes = need;
+    }
+    CU(launch_gather_x(X, p->d.dtype, m, ldx, p->rr_perm, r, p->rr_xr, p->sms, st));
+    if (t) cudaEventRecord(p->ev[5], st);
+    CU(launch_check_diag(p->rr_R11, r, p->status_d, st));
+    s = solve(p, p->rr_xr, m, r, p->rr_R11, Q, ldq, st, false, r);
+    if (s != RCHOLQR_OK) return s;
+  } else if (t) {
+    cudaEventRecord(p->ev[5], st);
+  }
+  if (t) cudaEventRecord(p->ev[6], st);
+  p->timing = t;
+  return read_status(p, st);
 }
 
 rcholqr_status rcholqr_query_status(rcholqr_plan p, void* stream) {
@@ -639,8 +783,8 @@ int32_t rcholqr_launches_per_factor(rcholqr_plan p, int64_t m) {
     sketch_launches += (int)(3 * chunks - 1);
   }
   int solve_launches = 1;
-  if (p->solve_tc) solve_launches = 2;
-  else if (p->stream_tb > 0) solve_launches = 2 * ((p->d.n + p->stream_tb - 1) / p->stream_tb);
+  if (p->sp.solve_tc) solve_launches = 2;
+  else if (p->sp.stream_tb > 0) solve_launches = 2 * ((p->d.n + p->sp.stream_tb - 1) / p->sp.stream_tb);
   int qr_launches = 1;
   if (p->qr_kind == kQrBlocked) {   // copy + per panel (panel kernel + 3 GEMMs, the last panel 1) + finalize
     const int panels = (p->d.n + 31) / 32;

@@ -110,6 +110,19 @@ cudaError_t launch_trmm_upper(const double* U, const double* V, int n, double* o
 // reduced RCholeskyQR (reduced.cu): Z = Y R^{-1} for the small l x n extract Y, row-wise substitution
 cudaError_t launch_rowsub(const double* Y, int64_t l, int n, const double* R, double* Z, const int* status,
                           cudaStream_t st);
+// rank-revealing RCholeskyQR (rrqr.cu)
+int colsq_splits(int n, int sms);
+cudaError_t launch_colsq(const void* X, int dtype, int64_t m, int n, int64_t ldx, int splits, double* part,
+                         double* out, int* status, cudaStream_t st);
+cudaError_t launch_rr_normalize(const double* buf, int k, int n, double* Pn, double* d, cudaStream_t st);
+cudaError_t launch_qrcp(const double* Pn, int k, int n, double* A, int* perm, cudaStream_t st);
+cudaError_t launch_rr_gather(const double* Pn, int k, int n, const int* perm, double* Pg, cudaStream_t st);
+cudaError_t launch_rank(const double* R, int n, double tau, int rank_fixed, int* rank, double* sigma, cudaStream_t st);
+cudaError_t launch_strong(const double* R, int n, int r, double* W, double* out_v, int* out_i, cudaStream_t st);
+cudaError_t launch_rr_finalize(const double* Rf, int n, int r, const double* d, const int* perm, double* Rout,
+                               double* R11, cudaStream_t st);
+cudaError_t launch_gather_x(const void* X, int dtype, int64_t m, int64_t ldx, const int* perm, int r, void* Xr,
+                            int sms, cudaStream_t st);
 cudaError_t launch_trsm_resident(int tm, const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M,
                                  void* Q, int64_t ldq, const int* status, int sms, cudaStream_t st);
 
