@@ -36,7 +36,7 @@ _lock = threading.Lock()
 _lib = None
 
 OK, E_INVALID, E_SHAPE, E_NONFINITE, E_SINGULAR, E_NOMEM = 0, 1, 2, 3, 4, 7
-GAUSSIAN, SPARSE_SIGN = 0, 1
+GAUSSIAN, SPARSE_SIGN, RADEMACHER = 0, 1, 2
 F64, F32 = 0, 1
 
 
@@ -68,6 +68,9 @@ def _L():
             lib.oracle_theta_gauss.restype = ctypes.c_double
             lib.oracle_theta_gauss_z.argtypes = [U64, I32, I64, I64, P]
             lib.oracle_theta_sparse.argtypes = [U64, I32, I32, I64, I64, P, P]
+            lib.oracle_theta_rademacher.argtypes = [U64, I32, I64, I64, P]
+            lib.oracle_rademacher_sign.argtypes = [U64, U64, I32]
+            lib.oracle_rademacher_sign.restype = I32
             lib.oracle_sketch.argtypes = [P, I32, I64, I32, I64, I64, I32, I32, I32, U64, P]
             lib.oracle_sketch.restype = I32
             lib.oracle_householder.argtypes = [P, I32, I32, P, P]
@@ -169,12 +172,21 @@ def theta_sparse(seed: int, k: int, zeta: int, m: int, row_offset: int = 0):
     return rows, signs
 
 
+def theta_rademacher(seed: int, k: int, m: int, row_offset: int = 0) -> np.ndarray:
+    """Rademacher signs (k, m) int8 (unscaled; Theta = signs / sqrt(k), reading A22)."""
+    S = np.empty((k, m), dtype=np.int8)
+    _L().oracle_theta_rademacher(seed, k, row_offset, m, _ptr(S))
+    return S
+
+
 def theta_dense(seed: int, k: int, m: int, sketch: int = GAUSSIAN, zeta: int = 8,
                 row_offset: int = 0) -> np.ndarray:
     """Explicit fp64 Theta (k x m) -- for tiny test inputs only."""
     if sketch == GAUSSIAN:
         Z = theta_gauss_z(seed, k, m, row_offset).astype(np.float64)
         return Z * (1.0 / np.sqrt(np.float64(k)))
+    if sketch == RADEMACHER:
+        return theta_rademacher(seed, k, m, row_offset).astype(np.float64) * (1.0 / np.sqrt(np.float64(k)))
     rows, signs = theta_sparse(seed, k, zeta, m, row_offset)
     T = np.zeros((k, m), dtype=np.float64)
     v = 1.0 / np.sqrt(np.float64(zeta))

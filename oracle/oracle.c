@@ -46,7 +46,7 @@
 
 enum { OR_OK = 0, OR_E_INVALID = 1, OR_E_SHAPE = 2, OR_E_NONFINITE = 3, OR_E_SINGULAR = 4,
        OR_E_NOMEM = 7 };
-enum { OR_GAUSSIAN = 0, OR_SPARSE_SIGN = 1 };
+enum { OR_GAUSSIAN = 0, OR_SPARSE_SIGN = 1, OR_RADEMACHER = 2 };
 #define OR_SKETCH_BLOCK 65536
 
 /* ------------------------------------------------------------------------------------------
@@ -185,6 +185,16 @@ void oracle_sparse_col(uint64_t seed, int k, int zeta, uint64_t i, int32_t* rows
     }
 }
 
+/* Rademacher Theta (reading A22): Theta_ri = s_ri fl64(1/sqrt(k)) with
+ * s_ri = +1 if bit (r mod 32) of word ((r mod 128) / 32) of Philox(ctr = (i, q = r / 128, domain 5))
+ * is 0, else -1 -- one Philox call gives the signs of 128 consecutive sketch rows. */
+int oracle_rademacher_sign(uint64_t seed, uint64_t i, int r) {
+    uint32_t w[4];
+    philox_for(seed, i, (uint32_t)(r / 128), 5u, w);
+    uint32_t word = w[(r % 128) / 32];
+    return ((word >> (r % 32)) & 1u) ? -1 : 1;
+}
+
 /* ---------------- batch helpers for the tests ---------------- */
 void oracle_ln32_batch(const float* a, float* out, int64_t n) {
     for (int64_t t = 0; t < n; ++t) out[t] = oracle_ln32(a[t]);
@@ -202,6 +212,13 @@ void oracle_theta_gauss_z(uint64_t seed, int k, int64_t row_offset, int64_t m, f
             for (int t = 0; t < 4 && 4 * q + t < k; ++t) Z[(int64_t)(4 * q + t) * m + ii] = z[t];
         }
     }
+}
+/* S: k x m row-major int8 signs of the Rademacher Theta (unscaled). */
+void oracle_theta_rademacher(uint64_t seed, int k, int64_t row_offset, int64_t m, int8_t* S) {
+    #pragma omp parallel for schedule(static)
+    for (int64_t ii = 0; ii < m; ++ii)
+        for (int r = 0; r < k; ++r)
+            S[(int64_t)r * m + ii] = (int8_t)oracle_rademacher_sign(seed, (uint64_t)(row_offset + ii), r);
 }
 /* rows/signs: m x zeta row-major. */
 void oracle_theta_sparse(uint64_t seed, int k, int zeta, int64_t row_offset, int64_t m,
@@ -262,11 +279,15 @@ int oracle_sketch(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64
         int64_t i0 = b * OR_SKETCH_BLOCK, i1 = i0 + OR_SKETCH_BLOCK < m ? i0 + OR_SKETCH_BLOCK : m;
         for (int64_t i = i0; i < i1; ++i) {
             uint64_t gi = (uint64_t)(row_offset + i);
-            if (sketch == OR_GAUSSIAN) {
-                float z[4];
-                for (int q = 0; q < (k + 3) / 4; ++q) {
-                    oracle_gauss4(seed, gi, (uint32_t)q, z);
-                    for (int t = 0; t < 4 && 4 * q + t < k; ++t) th[4 * q + t] = (double)z[t] * sk;
+            if (sketch == OR_GAUSSIAN || sketch == OR_RADEMACHER) {
+                if (sketch == OR_GAUSSIAN) {
+                    float z[4];
+                    for (int q = 0; q < (k + 3) / 4; ++q) {
+                        oracle_gauss4(seed, gi, (uint32_t)q, z);
+                        for (int t = 0; t < 4 && 4 * q + t < k; ++t) th[4 * q + t] = (double)z[t] * sk;
+                    }
+                } else {
+                    for (int r = 0; r < k; ++r) th[r] = oracle_rademacher_sign(seed, gi, r) > 0 ? sk : -sk;
                 }
                 for (int r = 0; r < k; ++r) {
                     double* prow = Pb + (size_t)r * n;
@@ -867,6 +888,8 @@ double oracle_sketch_entry(const double* x, int64_t m, int64_t row_offset, int k
                 float z[4];
                 oracle_gauss4(seed, gi, (uint32_t)(r / 4), z);
                 dot2_add(&acc, &cmp, (double)z[r % 4] * sk, x[i]);
+            } else if (sketch == OR_RADEMACHER) {
+                dot2_add(&acc, &cmp, oracle_rademacher_sign(seed, gi, r) > 0 ? sk : -sk, x[i]);
             } else {
                 oracle_sparse_col(seed, k, zeta, gi, rows, sg);
                 for (int t = 0; t < zeta && t < 64; ++t)
