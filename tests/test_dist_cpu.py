@@ -79,3 +79,82 @@ def test_partition_helpers():
     assert weak_block(100, 4, 3) == (300, 100, 400)
     with pytest.raises(ValueError):
         row_block(5, 2, 2)
+
+
+def _worker_alg(rank, world, port, algo, m, n, k, out_q):
+    """Alg. 5 / Alg. 7 / Alg. 3 on 2 ranks: one all-reduce of the stacked small matrices each needs
+    ([P; Y], [P; D^2]; Alg. 3 adds the Gram all-reduce), everything after it redundant per rank."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        if algo == "rr":
+            X = synth.make_X_lowrank(m, n, n - 4, 2.0, 1e-13)
+        else:
+            X = synth.make_X(m, n, 5.0, "f64")
+        ro, ml = row_block(m, world, rank)
+        Xl = X[ro:ro + ml]
+        P = oracle.sketch(Xl, k, row_offset=ro)
+        if algo == "reduced":
+            l = 9
+            Y = oracle.extract(Xl, oracle.extractor_row0(k), l, row_offset=ro)
+            buf = torch.from_numpy(np.concatenate([P, Y]))
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM)
+            P, Y = buf.numpy()[:k], buf.numpy()[k:]
+            R, _, _ = oracle.householder(P, want_S=False)
+            out = {"R": R, "Z": oracle.forward_subst(Y, R)}
+        elif algo == "rr":
+            d2 = np.sum(Xl.astype(np.float64) ** 2, axis=0)
+            buf = torch.from_numpy(np.concatenate([P, d2[None, :]]))
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM)
+            P, D = buf.numpy()[:k], np.sqrt(buf.numpy()[k])
+            rq = oracle.rrqr(P / D[None, :], 1e-9)
+            r, perm = rq["rank"], rq["perm"]
+            Rf = rq["R"][:r] * D[perm][None, :]
+            out = {"rank": r, "perm": perm, "R": Rf,
+                   "Q": oracle.forward_subst(np.ascontiguousarray(Xl[:, perm[:r]]), Rf[:, :r].copy())}
+        else:   # rcqr2
+            Pt = torch.from_numpy(P)
+            dist.all_reduce(Pt, op=dist.ReduceOp.SUM)
+            R1, _, _ = oracle.householder(Pt.numpy(), want_S=False)
+            Q1 = oracle.forward_subst(Xl, R1)
+            A = torch.from_numpy(oracle.gram(Q1))
+            dist.all_reduce(A, op=dist.ReduceOp.SUM)            # the second all-reduce of Alg. 3
+            Rp, _ = oracle.cholesky(A.numpy())
+            out = {"R": oracle.trmm_upper(Rp, R1), "Q": oracle.forward_subst(Q1, Rp)}
+        out_q.put((rank, out))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("algo", ["reduced", "rr", "rcqr2"])
+def test_two_rank_variants_equal_single(algo):
+    m, n, k, world = 70_001, 12, 24, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_alg, args=(r, world, port, algo, m, n, k, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    a, b = res[0], res[1]
+    assert np.array_equal(a["R"], b["R"])                       # redundant small steps agree bitwise
+    if algo == "reduced":
+        full = oracle.factor_reduced(synth.make_X(m, n, 5.0, "f64"), k, 9, want_S=False)
+        assert np.array_equal(a["Z"], b["Z"])
+        assert np.linalg.norm(a["Z"] - full["Z"]) <= 1e-10 * np.linalg.norm(full["Z"])
+        assert np.linalg.norm(a["R"] - full["R"]) <= 1e-13 * np.linalg.norm(full["R"])
+    elif algo == "rr":
+        full = oracle.factor_rr(synth.make_X_lowrank(m, n, n - 4, 2.0, 1e-13), k, 1e-9)
+        assert a["rank"] == b["rank"] == full["rank"] == n - 4
+        assert np.array_equal(a["perm"][: a["rank"]], full["perm"][: full["rank"]])
+        Q = np.concatenate([a["Q"], b["Q"]])
+        assert np.linalg.norm(Q - full["Q"]) <= 1e-10 * np.linalg.norm(full["Q"])
+    else:
+        full = oracle.factor2(synth.make_X(m, n, 5.0, "f64"), k)
+        assert np.linalg.norm(a["R"] - full["R"]) <= 1e-12 * np.linalg.norm(full["R"])
+        Q = np.concatenate([a["Q"], b["Q"]])
+        assert np.linalg.norm(Q.T @ Q - np.eye(n), 2) <= 1e-13
