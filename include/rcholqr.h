@@ -31,6 +31,8 @@
  * z/sqrt(k), z from a fixed fp32 Box-Muller transform ("i.i.d. Gaussian ...
  * scaled by sqrt(1/k)").  Sparse-sign: nnz_per_col nonzeros +-1/sqrt(nnz_per_col) per column,
  * one per block of k/nnz_per_col rows (BASELINE.json config 4; OSNAP block construction).
+ * Rademacher (reading A22): +-1/sqrt(k), sign = bit (r mod 32) of word ((r mod 128)/32) of the
+ * Philox call (i, r/128, domain 5).
  */
 #ifndef RCHOLQR_H
 #define RCHOLQR_H
@@ -45,7 +47,7 @@ extern "C" {
 typedef struct rcholqr_plan_s* rcholqr_plan;
 
 typedef enum { RCHOLQR_F64 = 0, RCHOLQR_F32 = 1 } rcholqr_dtype;          /* dtype of X and Q */
-typedef enum { RCHOLQR_GAUSSIAN = 0, RCHOLQR_SPARSE_SIGN = 1 } rcholqr_sketch_kind;
+typedef enum { RCHOLQR_GAUSSIAN = 0, RCHOLQR_SPARSE_SIGN = 1, RCHOLQR_RADEMACHER = 2 } rcholqr_sketch_kind;
 
 typedef enum {
   RCHOLQR_OK = 0,
@@ -64,7 +66,7 @@ typedef struct {
   int32_t k;            /* sketch rows (>= n); k = 2n is the paper's choice  */
   int32_t dtype;        /* rcholqr_dtype of X and Q                                             */
   int32_t sketch;       /* rcholqr_sketch_kind                                                    */
-  int32_t nnz_per_col;  /* sparse-sign nonzeros per column of Theta (ignored for Gaussian)      */
+  int32_t nnz_per_col;  /* sparse-sign nonzeros per column of Theta (ignored otherwise)        */
   int32_t device;       /* CUDA device ordinal the plan lives on                                */
   uint64_t seed;        /* Theta seed                                                            */
   void* nccl_comm;      /* communicator from rcholqr_comm_create, or NULL for a single GPU.

@@ -138,7 +138,8 @@ rcholqr_status cuda_status(cudaError_t e) {
 rcholqr_status validate_desc(const rcholqr_desc* d) {
   if (!d) return RCHOLQR_E_INVALID;
   if (d->dtype != RCHOLQR_F64 && d->dtype != RCHOLQR_F32) return RCHOLQR_E_INVALID;
-  if (d->sketch != RCHOLQR_GAUSSIAN && d->sketch != RCHOLQR_SPARSE_SIGN) return RCHOLQR_E_INVALID;
+  if (d->sketch != RCHOLQR_GAUSSIAN && d->sketch != RCHOLQR_SPARSE_SIGN && d->sketch != RCHOLQR_RADEMACHER)
+    return RCHOLQR_E_INVALID;
   if (d->n < 1 || d->k < d->n) return RCHOLQR_E_SHAPE;
   if (d->sketch == RCHOLQR_SPARSE_SIGN &&
       (d->nnz_per_col < 1 || d->nnz_per_col > d->k || d->k % d->nnz_per_col != 0))
@@ -729,7 +730,8 @@ rcholqr_status rcholqr_tri_solve(rcholqr_plan p, const void* X, int64_t m, int64
 rcholqr_status rcholqr_theta_export(uint64_t seed, int32_t k, int32_t sketch, int32_t zeta, int64_t ro, int64_t m,
                                     float* Z, int32_t* rows, int8_t* signs, void* stream) {
   if (k < 1 || m < 0 || ro < 0) return RCHOLQR_E_INVALID;
-  if (sketch != RCHOLQR_GAUSSIAN && sketch != RCHOLQR_SPARSE_SIGN) return RCHOLQR_E_INVALID;
+  if (sketch != RCHOLQR_GAUSSIAN && sketch != RCHOLQR_SPARSE_SIGN && sketch != RCHOLQR_RADEMACHER)
+    return RCHOLQR_E_INVALID;
   if (sketch == RCHOLQR_SPARSE_SIGN && (zeta < 1 || zeta > k || k % zeta != 0)) return RCHOLQR_E_SHAPE;
   cudaStream_t st = (cudaStream_t)stream;
   CU(launch_theta_export(seed, k, sketch, zeta, ro, m, Z, rows, signs, st));
@@ -773,9 +775,9 @@ int32_t rcholqr_launches_per_factor(rcholqr_plan p, int64_t m) {
   //   sketch: [tcgen05 sketch +] the CUDA-core kernel (its guarded fallback, exits at once) + reduce
   //   QR: 1 | triangular prep (blocked prep or R^{-1}): 1 | solve: tcgen05 (W-digit prep + solve) = 2,
   //   streamed fp64 GEMMs = 2 per column block, else 1.
-  const bool tc_sketch = p->sk.kind == kSketchSparseTC || (p->sk.kind < kSketchSparse && p->sk.tc);
+  const bool tc_sketch = p->sk.kind == kSketchSparseTC || (p->sk.kind < kSketchSparse && (p->sk.tc || p->sk.rad_tc));
   int sketch_launches = (tc_sketch ? 2 : 1) + 1;
-  if (tc_sketch && p->sk.kind < kSketchSparse && m > 0) {   // pre-split: (column maxima + digit planes + sketch) per chunk
+  if (tc_sketch && p->sk.kind < kSketchSparse && p->sk.tc && m > 0) {   // pre-split: (column maxima + digit planes + sketch) per chunk
     const size_t cap = gauss_tcp_chunk_workspace(m, p->d.n, p->d.dtype, p->sk.tc_splits);
     int64_t chunk = m;
     while (chunk > 32 && gauss_tcp_workspace(chunk, p->d.n, p->d.dtype, p->sk.tc_splits) > cap) chunk = (chunk + 1) / 2;

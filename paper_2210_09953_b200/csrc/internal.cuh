@@ -39,7 +39,13 @@ struct SketchLaunch {
   size_t smem;
   // Gaussian: tcgen05 digit sketch (sketch_gtc.cu) in front of the DMMA kernel described above
   int tc = 0, tc_tiles_k = 0, tc_tiles_n = 0, tc_splits = 0;
-  int max_splits() const { return tc && tc_splits > splits ? tc_splits : splits; }
+  // Rademacher Theta (reading A22): the DMMA kernel above draws +-1 instead of N(0,1); rad_tc: the
+  // tcgen05 int8 kernel of sketch_tc.cu with a dense E tile in front of it (n <= 64, k <= 512)
+  int rad = 0, rad_tc = 0, rad_splits = 0;
+  int max_splits() const {
+    int s = tc && tc_splits > splits ? tc_splits : splits;
+    return rad_tc && rad_splits > s ? rad_splits : s;
+  }
 };
 int gauss_tc_kt(int dtype);   // Theta rows per tcgen05 Gaussian-sketch tile (X columns per tile: 128)
 bool gauss_tc_aligned(const void* X, int dtype, int n, int64_t ldx);

@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
 sketch_gauss_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                     uint64_t seed, int tiles_k, int tiles_n, int64_t rows_per_split,
                     double* __restrict__ part, double* __restrict__ partc, const WarpPlan plan, int seg_chunks,
-                    const int* __restrict__ guard) {
+                    const int* __restrict__ guard, int rad) {
   // guard != null: recompute only if the tensor-core sketch (sketch_gtc.cu) flagged a headroom overflow
   if (guard && *guard == 0) return;
   using C = GCfg<TX, MS, NS>;
@@ -142,7 +142,9 @@ sketch_gauss_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int
             const int qq = cc / KC, ii = cc % KC;
             const int rb = r0 + 4 * qq;
             float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (i0 + ii < i_end && rb < k) z = gauss4_x2(seed, (uint64_t)(row_offset + i0 + ii), (uint32_t)(rb >> 2));
+            if (i0 + ii < i_end && rb < k)
+              z = rad ? rademacher4(seed, (uint64_t)(row_offset + i0 + ii), (uint32_t)rb)
+                      : gauss4_x2(seed, (uint64_t)(row_offset + i0 + ii), (uint32_t)(rb >> 2));
             double* Tc = T + (4 * qq) * C::TS_LD + ii;
             Tc[0 * C::TS_LD] = (rb + 0 < k) ? (double)z.x : 0.0;
             Tc[1 * C::TS_LD] = (rb + 1 < k) ? (double)z.y : 0.0;
@@ -441,6 +443,17 @@ __global__ void sketch_reduce_kernel(const double* __restrict__ part, const doub
 
 // ---------------------------------------------------------------------------------------------
 // Test export of Theta.
+__global__ void theta_rademacher_export_kernel(uint64_t seed, int k, int64_t row_offset, int64_t m, float* Z) {
+  const int nq = (k + 3) / 4;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < m * nq; c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = c % m;
+    const int q = (int)(c / m);
+    const float4 z = rademacher4(seed, (uint64_t)(row_offset + i), (uint32_t)(4 * q));
+    const float v[4] = {z.x, z.y, z.z, z.w};
+    for (int t = 0; t < 4 && 4 * q + t < k; ++t) Z[(int64_t)(4 * q + t) * m + i] = v[t];
+  }
+}
+
 __global__ void theta_gauss_export_kernel(uint64_t seed, int k, int64_t row_offset, int64_t m, float* Z) {
   const int nq = (k + 3) / 4;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < m * nq; c += (int64_t)gridDim.x * blockDim.x) {
@@ -600,6 +613,14 @@ SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms,
   L = cand[best];
   L.splits = choose_splits(L.tiles_k * L.tiles_n, sms);
   L.tc = 0;
+  if (sketch == RCHOLQR_RADEMACHER) {   // DMMA kernel drawing +-1, the dense tcgen05 int8 kernel in front of it
+    L.rad = 1;
+    if (sparse_tc_applicable(k, n, 1) && !getenv("RCHOLQR_RADEMACHER_DMMA")) {
+      L.rad_tc = 1;
+      L.rad_splits = sms;
+    }
+    return L;
+  }
   // tcgen05 int8 digit sketch (sketch_gtc.cu), the DMMA kernel above as its guarded fallback
   if (!getenv("RCHOLQR_GAUSS_DMMA")) {
     const int kt = gauss_tc_kt(dtype);
@@ -624,7 +645,7 @@ static cudaError_t launch_g(const SketchLaunch& L, const void* X, int64_t m, int
     if (plan.cnt[w] > GCfg<TX, MS, NS>::UMAX) return cudaErrorInvalidConfiguration;
   kern<<<L.tiles_k * L.tiles_n * L.splits, SK_THREADS, L.smem, st>>>((const TX*)X, m, n, ldx, ro, k, seed,
                                                                      L.tiles_k, L.tiles_n, rps, part, partc, plan,
-                                                                     seg_chunks(), guard);
+                                                                     seg_chunks(), guard, L.rad);
   return cudaGetLastError();
 }
 
@@ -696,7 +717,24 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
     int splits = L.splits;
     const int* guard = nullptr;
     const bool tc = L.tc && gauss_tc_aligned(X, dtype, n, ldx);
-    if (tc) {
+    if (L.rad_tc && sparse_tc_aligned(X, dtype, n, ldx)) {
+      // dense +-1 E tile on the sparse sketch's tcgen05 kernel (zeta = 0); it writes no compensation
+      // partials, so they are zeroed for the fixed-order reduction; the DMMA kernel below reruns
+      // (guarded) on a headroom overflow
+      splits = L.rad_splits;
+      const int64_t tper = (m + splits - 1) / splits;
+      const int64_t trps = std::max<int64_t>(SPR_KC, ((tper + SPR_KC - 1) / SPR_KC) * SPR_KC);
+      if (trps <= kSparseTcMaxRows) {
+        e = cudaMemsetAsync(flag, 0, sizeof(int), st);
+        if (e == cudaSuccess) e = cudaMemsetAsync(partc, 0, sizeof(double) * (size_t)splits * k * n, st);
+        if (e == cudaSuccess)
+          e = launch_sparse_tc(X, dtype, m, n, ldx, row_offset, k, 0, seed, splits, trps, part, flag, st);
+        if (e != cudaSuccess) return e;
+        guard = flag;
+      } else {
+        splits = L.splits;
+      }
+    } else if (tc) {
       splits = L.tc_splits;
       const int64_t tper = (m + splits - 1) / splits;
       const int64_t trps = std::max<int64_t>(KC, ((tper + KC - 1) / KC) * KC);
@@ -752,11 +790,12 @@ cudaError_t launch_reduce(const double* part, int splits, int64_t kn, double sca
 cudaError_t launch_theta_export(uint64_t seed, int k, int sketch, int zeta, int64_t row_offset, int64_t m,
                                 float* Z, int32_t* rows, int8_t* signs, cudaStream_t st) {
   if (m == 0) return cudaSuccess;
-  if (sketch == RCHOLQR_GAUSSIAN) {
+  if (sketch == RCHOLQR_GAUSSIAN || sketch == RCHOLQR_RADEMACHER) {
     if (!Z) return cudaSuccess;
     const int64_t work = m * ((k + 3) / 4);
     const int blocks = (int)std::min<int64_t>((work + 255) / 256, 65535);
-    theta_gauss_export_kernel<<<blocks, 256, 0, st>>>(seed, k, row_offset, m, Z);
+    if (sketch == RCHOLQR_RADEMACHER) theta_rademacher_export_kernel<<<blocks, 256, 0, st>>>(seed, k, row_offset, m, Z);
+    else theta_gauss_export_kernel<<<blocks, 256, 0, st>>>(seed, k, row_offset, m, Z);
   } else {
     const int blocks = (int)std::min<int64_t>((m + 255) / 256, 65535);
     theta_sparse_export_kernel<<<blocks, 256, 0, st>>>(seed, k, zeta, row_offset, m, rows, signs);

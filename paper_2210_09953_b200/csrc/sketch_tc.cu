@@ -166,7 +166,7 @@ sketch_sparse_tc_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx,
   const int64_t i_end = min(m, i_begin + rows_per_split);
   const int nstages = i_end > i_begin ? (int)((i_end - i_begin + STC_KC - 1) / STC_KC) : 0;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int beta = k / zeta;
+  const int beta = zeta > 0 ? k / zeta : 1;            // zeta = 0: dense Rademacher E (no blocks)
 
   if (tid == 0) {
     for (int s = 0; s < F::DIG; ++s) {
@@ -325,14 +325,56 @@ sketch_sparse_tc_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx,
     const int ii = half * 32 + lane;
     const int zoff = half * 2 * STC_M * 16;               // k-blocks 2half, 2half+1 of the E tile
     const bool full_tile = (zeta == 8 && k <= STC_M);     // common case: 8 nonzeros, one Theta row tile
+    const bool dense = zeta == 0;                         // Rademacher (reading A22): every entry +-1
     for (int c = grp; c < nstages; c += 2) {
       const int s = c % F::DIG;
       const int64_t i0 = i_begin + (int64_t)c * STC_KC;
       const int rows = (int)min((int64_t)STC_KC, i_end - i0);
       const uint64_t gi = (uint64_t)(row_offset + i0 + ii);
-      const uint4 w = philox_at(seed, gi, 0u, kDomainSparse);
+      const uint4 w = philox_at(seed, gi, dense ? (uint32_t)tk : 0u, dense ? kDomainRademacher : kDomainSparse);
       if (c >= F::DIG) tc::mbar_wait(&dempty[s], (uint32_t)(((c / F::DIG) - 1) & 1));
       unsigned char* st = dig_base + (size_t)s * C::DIG_STAGE;
+      if (dense) {
+        // Transpose the warp's 32 X rows x 128 sign bits with ballots: mask (Theta row r) holds bit L =
+        // sign of X row half*32 + L; lane r & 31 keeps the masks of rows r = lane + 32 q.  Each mask is
+        // expanded to two 16-byte K-runs (k-blocks 2 half, 2 half + 1) of +-1 bytes (0 beyond `rows`).
+        const uint32_t valid = __ballot_sync(0xffffffffu, ii < rows);
+        const uint32_t wd[4] = {w.x, w.y, w.z, w.w};
+        uint32_t mine[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t keep = 0u;
+#pragma unroll
+          for (int b = 0; b < 32; ++b) {
+            const uint32_t msk = __ballot_sync(0xffffffffu, (wd[q] >> b) & 1u);
+            keep = lane == b ? msk : keep;
+          }
+          mine[q] = keep;
+        }
+        if (!(dbg & 4)) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int r = 32 * q + lane;
+#pragma unroll
+            for (int hb = 0; hb < 2; ++hb) {
+              uint32_t out[4];
+#pragma unroll
+              for (int nb = 0; nb < 4; ++nb) {
+                const uint32_t sh = 16 * hb + 4 * nb;
+                const uint32_t sg = (((mine[q] >> sh) & 0xFu) * 0x00204081u) & 0x01010101u;
+                const uint32_t vb = (((valid >> sh) & 0xFu) * 0x00204081u) & 0x01010101u;
+                out[nb] = (0x01010101u + sg * 0xFEu) & (vb * 0xFFu);
+              }
+              *reinterpret_cast<uint4*>(st + (2 * half + hb) * STC_M * 16 + r * 16) =
+                  make_uint4(out[0], out[1], out[2], out[3]);
+            }
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&dfull[s]);
+        continue;
+      }
       uint4* zb = reinterpret_cast<uint4*>(st + zoff);
 #pragma unroll
       for (int u = 0; u < 2 * STC_M * 16 / 16 / 32; ++u) zb[u * 32 + lane] = make_uint4(0, 0, 0, 0);
@@ -407,7 +449,7 @@ sketch_sparse_tc_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx,
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
-bool sparse_tc_applicable(int k, int n, int zeta) { return n <= STC_N && k % zeta == 0 && k <= 4 * STC_M; }
+bool sparse_tc_applicable(int k, int n, int zeta) { return n <= STC_N && zeta >= 1 && k % zeta == 0 && k <= 4 * STC_M; }
 
 template <typename TX>
 static cudaError_t launch_stc(const TX* X, int64_t m, int n, int64_t ldx, int64_t ro, int k, int zeta, uint64_t seed,

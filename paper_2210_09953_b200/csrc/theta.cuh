@@ -24,7 +24,7 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
 }
 
 // Counter layout (A2): ctr = (lo32(i), hi32(i), q, domain), key = (lo32(seed), hi32(seed)).
-enum : uint32_t { kDomainGauss = 1u, kDomainSparse = 2u };
+enum : uint32_t { kDomainGauss = 1u, kDomainSparse = 2u, kDomainRademacher = 5u };
 
 __device__ __forceinline__ uint4 philox_at(uint64_t seed, uint64_t i, uint32_t q, uint32_t domain) {
   return philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), q, domain), (uint32_t)seed,
@@ -181,6 +181,16 @@ __device__ __forceinline__ uint32_t sparse_halfword(const uint4& w, int t) {
 }
 __device__ __forceinline__ int sparse_row(uint32_t h, int t, int beta) {
   return t * beta + (int)(((h & 0x7FFFu) * (uint32_t)beta) >> 15);
+}
+
+// Rademacher signs (reading A22) of sketch rows rb..rb+3 (rb % 4 == 0) at global X-row i:
+// bit (r mod 32) of word ((r mod 128) / 32) of Philox(i, r / 128, domain 5); 0 -> +1, 1 -> -1.
+__device__ __forceinline__ float4 rademacher4(uint64_t seed, uint64_t i, uint32_t rb) {
+  const uint4 w = philox_at(seed, i, rb >> 7, kDomainRademacher);
+  const uint32_t q = (rb >> 5) & 3u;
+  const uint32_t word = q == 0 ? w.x : (q == 1 ? w.y : (q == 2 ? w.z : w.w));
+  const uint32_t b = word >> (rb & 31u);
+  return make_float4((b & 1u) ? -1.f : 1.f, (b & 2u) ? -1.f : 1.f, (b & 4u) ? -1.f : 1.f, (b & 8u) ? -1.f : 1.f);
 }
 
 }  // namespace rcq
