@@ -111,7 +111,7 @@ def _workload(cfg_name: str, ws: int, rank: int):
 def _cpu_sample_rate(X_dev, cfg, target_s: float, algo: str = "rcholqr", l: int = 0, tau: float = 0.0):
     """Time the oracle (as it stands, all host cores) on a bounded leading sample of X."""
     import oracle
-    so = oracle.GAUSSIAN if cfg["sketch"] == "gaussian" else oracle.SPARSE_SIGN
+    so = {"gaussian": oracle.GAUSSIAN, "sparse": oracle.SPARSE_SIGN, "rademacher": oracle.RADEMACHER}[cfg["sketch"]]
     if algo == "rcholqr2":
         run = lambda A: oracle.factor2(A, cfg["k"], sketch=so, zeta=cfg["nnz"])  # noqa: E731
     elif algo == "rcholqr_rr":
@@ -140,7 +140,9 @@ def run_reference(args):
     import numpy as np
     import oracle
     cfg = synth.config(args.config)
-    so = oracle.GAUSSIAN if cfg["sketch"] == "gaussian" else oracle.SPARSE_SIGN
+    if args.sketch:
+        cfg["sketch"] = args.sketch
+    so = {"gaussian": oracle.GAUSSIAN, "sparse": oracle.SPARSE_SIGN, "rademacher": oracle.RADEMACHER}[cfg["sketch"]]
     s_x = 8 if cfg["dtype"] == "f64" else 4
     per_step_s = max(1.0, 150.0 / (args.steps + args.warmup))
     # calibrate a sample size on the leading rows of the workload's X
@@ -195,6 +197,8 @@ def run(args):
         comm = rcq.comm_create(obj[0], ws, rank, local)
 
     cfg, m_local, m_global, ro, scaling = _workload(args.config, ws, rank)
+    if args.sketch:                          # experiments: another Theta on the same workload shape
+        cfg["sketch"] = args.sketch
     n, k, dt = cfg["n"], cfg["k"], cfg["dtype"]
     s_x = 8 if dt == "f64" else 4
     # each rank generates exactly its own rows of the global X (reproducible per row range)
@@ -301,8 +305,8 @@ def run(args):
         # fp64 flops, so it is measured against the FP64 tensor (DMMA) peak it replaces.
         flops = 2.0 * k_sk * m_local * n
         ach = flops / (per_ms["sketch"] * 1e-3) / 1e12
-        roofs["sketch"] = {"kernel": "sketch_gauss_tc_kernel", "bound": "tensor", "achieved": ach,
-                           "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
+        roofs["sketch"] = {"kernel": "xdig_split_kernel + sketch_gauss_tcp_kernel", "bound": "tensor",
+                           "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
                            "peak_source": "FP64 DMMA peak 37.2 TF (148 SM x 64 FMA/clk x 2 x 1.965 GHz; "
                                           "microbenchmark 37.0, profiles/peaks_r1.jsonl): fp64-equivalent view "
                                           "of the exact int8 digit emulation",
@@ -313,12 +317,19 @@ def run(args):
         # one; the Gaussian extract's 2 l m n fp64-equivalent flops dominate both passes' time
         flops = 2.0 * l_red * m_local * n
         ach = flops / (per_ms["sketch"] * 1e-3) / 1e12
-        roofs["sketch"] = {"kernel": "sketch_gauss_tc_kernel", "bound": "tensor", "achieved": ach,
+        roofs["sketch"] = {"kernel": "xdig_split_kernel + sketch_gauss_tcp_kernel", "bound": "tensor", "achieved": ach,
                            "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
                            "peak_source": "FP64 DMMA peak 37.2 TF (fp64-equivalent view of the exact int8 digits)",
                            "algorithmic": f"2*l*m*n = {flops:.4g} flop (Gaussian extract; the time includes "
                                           "the sparse sketch pass)", "traffic": None}
-    else:
+    elif cfg["sketch"] == "rademacher" and n > 64:
+        flops = 2.0 * k * m_local * n
+        ach = flops / (per_ms["sketch"] * 1e-3) / 1e12
+        roofs["sketch"] = {"kernel": "sketch_gauss_kernel (Rademacher draws)", "bound": "tensor", "achieved": ach,
+                           "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
+                           "peak_source": "FP64 DMMA peak 37.2 TF", "algorithmic": f"2*k*m*n = {flops:.4g} flop",
+                           "traffic": None}
+    else:   # sparse-sign, or Rademacher on the dense-E tcgen05 kernel: one read of X per Theta tile
         byts = m_local * n * s_x
         ach = byts / (per_ms["sketch"] * 1e-3) / 1e9
         roofs["sketch"] = {"kernel": "sketch_sparse_tc_kernel", "bound": "hbm", "achieved": ach, "peak": hbm,
@@ -366,7 +377,8 @@ def run(args):
     except OSError:
         tr = {}
     for r_ in roofs.values():
-        tb = tr.get(r_["kernel"])
+        names = [x.strip() for x in r_["kernel"].split("+")]
+        tb = sum(tr[x] for x in names) if all(x in tr for x in names) else None
         if tb is not None and ws == 1:
             r_["traffic"] = tb
             r_["traffic_source"] = "ncu --set full: dram__bytes_read.sum + dram__bytes_write.sum per launch"
@@ -394,6 +406,36 @@ def run(args):
             "clocks": clk.summary(), "e2e": e2e}
 
     if args.algo == "rcholqr2":
+        # split Alg. 3's own steps by differences of device-timed calls on the same stream:
+        # factor (Alg. 2) | factor2(implicit) (+ Gram, Cholesky, R'R1) | factor2 (+ the second solve)
+        def _avg(fn, reps):
+            fn()
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _ in range(reps):
+                fn()
+            a1.record(stream)
+            torch.cuda.synchronize()
+            return a0.elapsed_time(a1) / reps
+        reps = max(3, min(args.steps, 10))
+        t2 = _avg(lambda: plan.factor(X, row_offset=ro, Q=Q, R=R, stream=stream), reps)
+        ti = _avg(lambda: plan.factor2(X, row_offset=ro, Q=Q, R=R, Rprime=Rp, implicit=True, stream=stream), reps)
+        te = _avg(lambda: plan.factor2(X, row_offset=ro, Q=Q, R=R, Rprime=Rp, stream=stream), reps)
+        per_ms.update({"gram_cholesky": ti - t2, "second_solve": te - ti})
+        line["per_kernel_ms"] = per_ms
+        flops = float(m_local) * n * (n + 1)          # upper triangle of Q1^T Q1 (incl. the diagonal)
+        ach = flops / ((ti - t2) * 1e-3) / 1e12
+        roofs["gram"] = {"kernel": "gram_kernel + sketch_reduce_kernel + cholesky_kernel", "bound": "tensor",
+                         "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
+                         "peak_source": "FP64 DMMA peak 37.2 TF",
+                         "algorithmic": f"m*n*(n+1) = {flops:.4g} flop (time: factor2(implicit) - factor)",
+                         "traffic": None}
+        dom = max(roofs, key=lambda kk: {"gram": ti - t2}.get(kk, per_ms.get(kk, 0.0)))
+        roof = dict(roofs[dom])
+        roof["share_of_step"] = (ti - t2 if dom == "gram" else per_ms.get(dom, 0.0)) / ms
+        line["roofline"] = roof
+        line["kernel_rooflines"] = roofs
         # Alg. 3 = Alg. 2 + Gram (reads Q1) + Cholesky + second solve (reads Q1, writes Q): 6 passes
         # over an m x n matrix and 2 m n^2 (solves) + m n^2 (Gram, both triangles) fp64 flops
         t_hbm2 = 6.0 * m_local * n * s_x / (hbm * 1e9)
@@ -469,6 +511,8 @@ def main():
                     help="Alg. 2 (default, the north star), Alg. 3 RCholeskyQR2 (orthonormal Q) or Alg. 5 "
                          "reduced RCholeskyQR (Z = L Q)")
     ap.add_argument("--l", type=int, default=0, help="Alg. 5: rows of the extractor L (default k)")
+    ap.add_argument("--sketch", default="", choices=["", "gaussian", "sparse", "rademacher"],
+                    help="override the config's Theta (the BASELINE metric is quoted on the config's own)")
     ap.add_argument("--tau", type=float, default=0.0,
                     help="Alg. 7: truncation tolerance (default: the paper's 4e-15 fp64 / 2e-7 fp32)")
     args = ap.parse_args()

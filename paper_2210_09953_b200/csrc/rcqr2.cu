@@ -82,13 +82,111 @@ gram_kernel(const TX* __restrict__ Q, int64_t m, int n, int64_t ldq, int tb, int
       }
 }
 
+// ---------------------------------------------------------------------------------------------
+// n <= 128: one CTA per row split computes EVERY upper 32 x 32 sub-tile of the Gram from one shared
+// row chunk (KC rows x NPAD columns, cp.async, GS_STAGES-deep ring, zero-filled outside Q), one
+// warp per sub-tile (2 m16 x 4 n8 DMMA accumulators), so Q1 is read once and each staged element
+// feeds every sub-tile it belongs to.
+constexpr int GS_KC = 32;
+constexpr int GS_STAGES = 3;
+
+__device__ __forceinline__ void gs_cp4(void* s, const void* g, bool v) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(g), "r"(v ? 4 : 0));
+}
+__device__ __forceinline__ void gs_cp8(void* s, const void* g, bool v) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(s);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(v ? 8 : 0));
+}
+
+template <typename TX>
+__global__ void gram_small_kernel(const TX* __restrict__ Q, int64_t m, int n, int64_t ldq, int nb,
+                                  int64_t rows_per_split, double* __restrict__ part, const int* status) {
+  if (*status) return;
+  extern __shared__ __align__(16) unsigned char gs_sm[];
+  const int npad = nb * 32, LD = npad + 4;
+  TX* S = reinterpret_cast<TX*>(gs_sm);                 // [GS_STAGES][GS_KC][LD]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  // warp -> upper sub-tile (bi <= bj) in row-major order of the upper triangle
+  int bi = 0, t = warp;
+  while (t >= nb - bi) { t -= nb - bi; ++bi; }
+  const int bj = bi + t;
+  const int64_t r_begin = (int64_t)blockIdx.x * rows_per_split, r_end = min(m, r_begin + rows_per_split);
+  const int nchunks = r_end > r_begin ? (int)((r_end - r_begin + GS_KC - 1) / GS_KC) : 0;
+  const int nthr = blockDim.x;
+  auto issue = [&](int ch) {
+    TX* dst = S + (size_t)(ch % GS_STAGES) * GS_KC * LD;
+    const int64_t r0 = r_begin + (int64_t)ch * GS_KC;
+    for (int c = threadIdx.x; c < GS_KC * npad; c += nthr) {
+      const int rr = c / npad, cc = c % npad;
+      const bool ok = r0 + rr < r_end && cc < n;
+      const TX* src = ok ? Q + (r0 + rr) * ldq + cc : Q;
+      if (sizeof(TX) == 4) gs_cp4(dst + rr * LD + cc, src, ok);
+      else gs_cp8(dst + rr * LD + cc, src, ok);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  double acc[2][4][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[a][b][e] = 0.0;
+  for (int ch = 0; ch < GS_STAGES - 1; ++ch) {
+    if (ch < nchunks) issue(ch);
+    else asm volatile("cp.async.commit_group;\n" ::);
+  }
+  const int i0 = bi * 32, j0 = bj * 32;
+  for (int ch = 0; ch < nchunks; ++ch) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(GS_STAGES - 2) : "memory");
+    __syncthreads();                                    // chunk ch visible; chunk ch-1's slot free
+    if (ch + GS_STAGES - 1 < nchunks) issue(ch + GS_STAGES - 1);
+    else asm volatile("cp.async.commit_group;\n" ::);
+    const TX* C = S + (size_t)(ch % GS_STAGES) * GS_KC * LD;
+#pragma unroll
+    for (int ks = 0; ks < GS_KC / 4; ++ks) {
+      const TX* row = C + (4 * ks + t4) * LD;
+      double a0[2], a1[2], bv[4];
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {                    // A[i][k] = Q[k][i]
+        a0[a] = (double)row[i0 + a * 16 + g];
+        a1[a] = (double)row[i0 + a * 16 + g + 8];
+      }
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = (double)row[j0 + b * 8 + g];   // B[k][j] = Q[k][j]
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int a = 0; a < 2; ++a) dmma_16x8x4(acc[a][b], a0[a], a1[a], bv[b]);
+    }
+  }
+  double* P = part + (size_t)blockIdx.x * n * n;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int i = i0 + a * 16 + g + (e >= 2 ? 8 : 0);
+        const int j = j0 + b * 8 + 2 * t4 + (e & 1);
+        if (i < n && j < n && (bi != bj || i <= j)) {
+          P[(size_t)i * n + j] = acc[a][b][e];
+          P[(size_t)j * n + i] = acc[a][b][e];
+        }
+      }
+}
+
 // R' (upper, row-major) with A = R'^T R'; reads the upper triangle of A.  One CTA; A is copied to
 // the work buffer W (n x n), updated in place (right-looking), R' written as rows are finished.
 __global__ void __launch_bounds__(1024)
-cholesky_kernel(const double* __restrict__ A, int n, double* __restrict__ W, double* __restrict__ Rp, int* status) {
+cholesky_kernel(const double* __restrict__ A, int n, double* __restrict__ Wg, double* __restrict__ Rp, int* status,
+                int stage) {
   if (*status) return;
+  extern __shared__ double ch_s[];
   __shared__ int bad;
   __shared__ double sh_r;
+  double* W = stage ? ch_s : Wg;                      // the working copy in shared memory when it fits
   const int tid = threadIdx.x;
   if (tid == 0) bad = 0;
   for (int c = tid; c < n * n; c += blockDim.x) { W[c] = A[c]; Rp[c] = 0.0; }
@@ -129,6 +227,7 @@ __global__ void trmm_upper_kernel(const double* __restrict__ U, const double* __
 }
 
 int gram_splits(int n, int sms) {
+  if (n <= 128) return 4 * sms;                       // gram_small_kernel: one CTA per split
   const int tb = (n + GR_T - 1) / GR_T, ntiles = tb * (tb + 1) / 2;
   return std::max(1, (2 * sms + ntiles - 1) / ntiles);
 }
@@ -138,6 +237,25 @@ cudaError_t launch_gram(const void* Q, int dtype, int64_t m, int n, int64_t ldq,
   const int tb = (n + GR_T - 1) / GR_T, ntiles = tb * (tb + 1) / 2;
   const int64_t per = (m + splits - 1) / splits;
   const int64_t rps = std::max<int64_t>(GR_KC, (per + GR_KC - 1) / GR_KC * GR_KC);
+  if (n <= 128) {
+    const int nb = (n + 31) / 32, nt = nb * (nb + 1) / 2;
+    const size_t es = dtype == RCHOLQR_F64 ? 8 : 4;
+    const size_t smem = (size_t)GS_STAGES * GS_KC * (nb * 32 + 4) * es;
+    cudaError_t e2;
+    if (dtype == RCHOLQR_F64) {
+      e2 = cudaFuncSetAttribute(gram_small_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e2 == cudaSuccess)
+        gram_small_kernel<double><<<splits, 32 * nt, smem, st>>>((const double*)Q, m, n, ldq, nb, rps, part, status);
+    } else {
+      e2 = cudaFuncSetAttribute(gram_small_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e2 == cudaSuccess)
+        gram_small_kernel<float><<<splits, 32 * nt, smem, st>>>((const float*)Q, m, n, ldq, nb, rps, part, status);
+    }
+    if (e2 != cudaSuccess) return e2;
+    e2 = cudaGetLastError();
+    if (e2 != cudaSuccess) return e2;
+    return launch_reduce(part, splits, (int64_t)n * n, 1.0, A, status, st);
+  }
   if (dtype == RCHOLQR_F64)
     gram_kernel<double><<<ntiles * splits, GR_THREADS, 0, st>>>((const double*)Q, m, n, ldq, tb, ntiles, rps, part,
                                                                  status);
@@ -150,7 +268,12 @@ cudaError_t launch_gram(const void* Q, int dtype, int64_t m, int n, int64_t ldq,
 }
 
 cudaError_t launch_cholesky(const double* A, int n, double* W, double* Rp, int* status, cudaStream_t st) {
-  cholesky_kernel<<<1, 1024, 0, st>>>(A, n, W, Rp, status);
+  const size_t need = sizeof(double) * (size_t)n * n;
+  const int stage = need <= 200 * 1024;
+  cudaError_t e = cudaFuncSetAttribute(cholesky_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       stage ? (int)need : 0);
+  if (e != cudaSuccess) return e;
+  cholesky_kernel<<<1, 1024, stage ? need : 0, st>>>(A, n, W, Rp, status, stage);
   return cudaGetLastError();
 }
 
