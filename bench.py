@@ -426,7 +426,8 @@ def run(args):
         line["per_kernel_ms"] = per_ms
         flops = float(m_local) * n * (n + 1)          # upper triangle of Q1^T Q1 (incl. the diagonal)
         ach = flops / ((ti - t2) * 1e-3) / 1e12
-        roofs["gram"] = {"kernel": "gram_kernel + sketch_reduce_kernel + cholesky_kernel", "bound": "tensor",
+        roofs["gram"] = {"kernel": ("gram_small_kernel" if n <= 128 else "gram_kernel") +
+                                   " + sketch_reduce_kernel + cholesky_kernel", "bound": "tensor",
                          "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
                          "peak_source": "FP64 DMMA peak 37.2 TF",
                          "algorithmic": f"m*n*(n+1) = {flops:.4g} flop (time: factor2(implicit) - factor)",
