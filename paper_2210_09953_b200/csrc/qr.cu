@@ -345,6 +345,7 @@ form_s_kernel(const double* __restrict__ A, const double* __restrict__ tau, cons
 
 int plan_qr(int k, int n, size_t smem_optin) {
   const size_t need = sizeof(double) * (size_t)k * n;
+  if (getenv("RCHOLQR_QR_BLOCKED")) return kQrBlocked;   // experiments: blocked QR at any size
   if (need + 1024 <= std::min<size_t>(smem_optin, 220 * 1024)) return kQrSmem;
   return getenv("RCHOLQR_QR_UNBLOCKED") ? kQrGlobal : kQrBlocked;
 }

@@ -432,6 +432,16 @@ constexpr int GP_THREADS = 32 * (2 + GP_TWARPS);
 constexpr int GP_GROUPS = 4;
 static_assert(GT_DRAIN % GP_GROUPS == 0, "drain stages belong to group 0");
 
+// Levels the pre-split kernel keeps: L <= LK - 1.  A dropped level L >= LK holds at most 4 digit products
+// of weight 256^(LEV-1-L), i.e. <= 2^-53 (fp32 X, LK = 8) / 2^-61 (fp64 X, LK = 9) of a typical
+// |F_z F_x| term -- at or below the fp64 rounding of P (reading A17) -- so X digit b multiplies only
+// the Theta digits a < LK - b, a PREFIX of the stacked B tile (its MMA N shrinks accordingly).
+template <typename TX> struct GpLevels;
+template <> struct GpLevels<float> { static constexpr int LK = 8; };
+template <> struct GpLevels<double> { static constexpr int LK = 9; };
+__host__ __device__ constexpr int gp_nd(int b, int lk) { return (lk - b) < GT_DZ ? (lk - b) : GT_DZ; }
+__host__ __device__ constexpr int gp_n(int b, int lk, int kt) { return (gp_nd(b, lk) * kt + 15) / 16 * 16; }
+
 template <typename TX>
 struct GpCfg {
   using G = GtCfg<TX>;
@@ -555,7 +565,8 @@ sketch_gauss_tcp_kernel(const unsigned char* __restrict__ dig, const uint32_t* _
 
   if (warp == 0) {
     // ---------------------------------------------------------------- MMA issuer (lane 0)
-    constexpr uint32_t idesc = tc::idesc_i8(GT_M, C::NB, true, true);
+    constexpr int LK = GpLevels<TX>::LK;
+    static_assert(gp_n(0, LK, KT) == C::NB && LK > DX - 1, "level truncation shape");
     for (int c = 0; c < nstages; ++c) {
       const int s = c % S;
       if (c > 0 && c % GT_DRAIN == 0) tc::mbar_wait(drained, (uint32_t)((c / GT_DRAIN - 1) & 1));
@@ -565,8 +576,9 @@ sketch_gauss_tcp_kernel(const unsigned char* __restrict__ dig, const uint32_t* _
         const uint32_t sa = tc::smem_u32(sm + (size_t)s * P::DIG_STAGE);
         const uint64_t db = tc::desc(sa + P::A_BYTES, C::B_LBO, GT_BSBO);
 #pragma unroll
-        for (int b = 0; b < DX; ++b)
-          tc::mma_i8(tmem + b * KT, tc::desc(sa + b * 4096, (GT_M / 8) * 128, 128), db, idesc, 1u);
+        for (int b = 0; b < DX; ++b)   // X digit b x Theta digits a < LK - b (levels b .. LK - 1)
+          tc::mma_i8(tmem + b * KT, tc::desc(sa + b * 4096, (GT_M / 8) * 128, 128), db,
+                     tc::idesc_i8(GT_M, gp_n(b, LK, KT), true, true), 1u);
         tc::commit(&dempty[s]);
         if ((c + 1) % GT_DRAIN == 0 || c == nstages - 1) tc::commit(drainbar);
       }
@@ -607,7 +619,7 @@ sketch_gauss_tcp_kernel(const unsigned char* __restrict__ dig, const uint32_t* _
 #pragma unroll
         for (int rr = 0; rr < 8; ++rr) v[rr] = 0.0;
 #pragma unroll
-        for (int L = LEV - 1; L >= 0; --L) {
+        for (int L = GpLevels<TX>::LK - 1; L >= 0; --L) {      // levels >= LK are not computed
           uint32_t a8[8];
           tc::ld8(lb + L * KT + r8 * 8, a8);
           tc::wait_ld();
