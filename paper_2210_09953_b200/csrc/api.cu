@@ -53,6 +53,7 @@ struct SolvePlan {
   TrsmLaunch tr{};
   int res_tm = 0, warp_solve = 0, stream_tb = 0;
   bool solve_tc = false;
+  bool mstream = false;   // 128 < n <= 256: warp-pair substitution with M streamed per column block
 };
 
 struct rcholqr_plan_s {
@@ -217,7 +218,8 @@ SolvePlan plan_solve(int n, int dtype, size_t smem_optin) {
   s.tr = plan_trsm(n, dtype, smem_optin);
   s.res_tm = trsm_resident_tm(n, dtype, smem_optin);
   s.warp_solve = trsm_warp_count(n, smem_optin);
-  if (s.warp_solve == 0 && s.res_tm == 0 && dtype == RCHOLQR_F64) s.stream_tb = n < 512 ? 64 : 128;
+  s.mstream = s.warp_solve == 0 && s.res_tm == 0 && trsm_mstream_applicable(n, smem_optin);
+  if (s.warp_solve == 0 && s.res_tm == 0 && !s.mstream && dtype == RCHOLQR_F64) s.stream_tb = n < 512 ? 64 : 128;
   if (const char* f = getenv("RCHOLQR_SOLVE")) {  // experiments: 0 = inverse GEMM, 1 = CTA-resident, 2 = warp
     const int v = atoi(f);
     if (v != 2) s.warp_solve = 0;
@@ -243,7 +245,11 @@ rcholqr_status solve(rcholqr_plan p, const void* X, int64_t m, int64_t ldx, cons
     if (e == cudaSuccess) return RCHOLQR_OK;
     if (e != cudaErrorNotSupported) return cuda_status(e);
   }
-  if (sp.stream_tb > 0) {
+  if (sp.mstream) {
+    CU(launch_tri_prep_blocked(R, n, p->W, p->status_d, st));
+    if (timed && p->timing) cudaEventRecord(p->ev[5], st);
+    if (m > 0) CU(launch_trsm_mstream(X, p->d.dtype, m, n, ldx, p->W, Q, ldq, p->status_d, p->sms, st));
+  } else if (sp.stream_tb > 0) {
     // blocked substitution by column blocks of width tb, each = 2 fp64 DMMA GEMM launches
     const int tb = sp.stream_tb, npad = (n + 7) / 8 * 8;
     CU(launch_tri_prep_blocked(R, n, p->W, p->status_d, st, tb, npad));

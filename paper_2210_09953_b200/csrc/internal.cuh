@@ -92,6 +92,10 @@ int trsm_resident_tm(int n, int dtype, size_t smem_optin);   // 0 = not applicab
 int trsm_warp_count(int n, size_t smem_optin);                 // 0 = not applicable
 cudaError_t launch_trsm_warp(int warps, const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M,
                              void* Q, int64_t ldq, const int* status, int sms, cudaStream_t st);
+// 128 < n <= 256: warp-pair blocked substitution with M streamed per column block (trsm.cu)
+bool trsm_mstream_applicable(int n, size_t smem_optin);
+cudaError_t launch_trsm_mstream(const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M, void* Q,
+                                int64_t ldq, const int* status, int sms, cudaStream_t st);
 cudaError_t launch_tri_prep_blocked(const double* R, int n, double* M, int* status, cudaStream_t st, int tb = 32,
                                     int npad = 0);
 // fp64 DMMA GEMM C = C0 + A B (gemm.cu), used by the streamed blocked solve (n > 128, fp64 X)

@@ -644,6 +644,164 @@ trsm_pair_kernel(const TX* __restrict__ X, int64_t m, int n, int NPAD, int64_t l
   }
 }
 
+// 128 < n <= 256: the warp-pair blocked substitution with M STREAMED instead of resident (npad^2
+// doubles no longer fit next to the Q slabs).  All pairs of the CTA advance through the column blocks J
+// together; before each J the CTA stages M(0 : c0 + TB, c0 : c0 + TB) -- the only part of M block J
+// reads -- from L2 into one [NPAD][TB + 4] buffer.  That costs (c0 + TB) TB doubles per J per CTA,
+// ~5% of the block's DMMA time.  The fp64 Q history (NPAD columns) stays in the pair's [16][LD] slab.
+constexpr int MS_PAIRS = 4;
+constexpr int MS_MLD = TB + 4;                    // = 4 (mod 16) doubles: fragment loads conflict-free
+
+static size_t mstream_smem(int npad) {
+  return sizeof(double) * ((size_t)npad * MS_MLD + (size_t)MS_PAIRS * 16 * (npad + 4));
+}
+
+template <typename TX>
+__global__ void __launch_bounds__(64 * MS_PAIRS, 1)
+trsm_mstream_kernel(const TX* __restrict__ X, int64_t m, int n, int NPAD, int64_t ldx, const double* __restrict__ Mg,
+                    TX* __restrict__ Q, int64_t ldq, const int* status) {
+  if (*status) return;
+  extern __shared__ __align__(16) double smem_w[];
+  const int LD = NPAD + 4;
+  double* Mb = smem_w;                                              // [NPAD][MS_MLD]: column block J of M
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
+  const int pair = warp >> 1, h = warp & 1;
+  double* Aw = smem_w + (size_t)NPAD * MS_MLD + (size_t)pair * 16 * LD;   // the pair's [16][LD] slab
+  const int NBLK = (NPAD + TB - 1) / TB;
+  const int64_t ntiles = (m + 15) / 16;
+  constexpr int HU = TB / 16;
+  TX xn[HU][4];
+  auto prefetch = [&](int64_t tile, int J) {
+#pragma unroll
+    for (int v = 0; v < HU; ++v)
+      load_x_frag(X, m, n, ldx, tile * 16, J * TB + 8 * (HU * h + v) + 2 * t4, g, xn[v]);
+  };
+  const int64_t step = (int64_t)gridDim.x * MS_PAIRS;
+  const int64_t first = (int64_t)blockIdx.x * MS_PAIRS + pair;
+  if (first < ntiles) prefetch(first, 0);
+  const double* arow = Aw + g * LD + t4;
+  for (int64_t base = (int64_t)blockIdx.x * MS_PAIRS; base < ntiles; base += step) {
+    const int64_t tile = base + pair;
+    const bool active = tile < ntiles;
+    const int64_t r0 = tile * 16;
+    for (int J = 0; J < NBLK; ++J) {
+      const int c0 = J * TB;
+      const int nt8 = min(TB, NPAD - c0) / 8;
+      const int rows = min(NPAD, c0 + TB);
+      __syncthreads();                                              // everyone done with block J-1's Mb
+      for (int c = threadIdx.x; c < rows * (TB / 2); c += 64 * MS_PAIRS) {   // 16-byte cp.async, all in flight
+        const int rr = c / (TB / 2), cc = 2 * (c % (TB / 2));
+        const bool ok = c0 + cc < NPAD;
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(Mb + rr * MS_MLD + cc);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa),
+                     "l"(ok ? Mg + (size_t)rr * NPAD + c0 + cc : Mg), "r"(ok ? 16 : 0));
+      }
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+      __syncthreads();
+      if (!active) continue;
+      double acc[HU][4];
+#pragma unroll
+      for (int v = 0; v < HU; ++v)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[v][e] = (double)xn[v][e];
+      if (J + 1 < NBLK) prefetch(tile, J + 1);
+      else if (tile + step < ntiles) prefetch(tile + step, 0);
+      const int u0 = HU * h;
+      const bool full = nt8 == TB / 8;
+      // phase 1: T_J = X_J + Q_{<J} (-R_{<J,J})
+      if (full) {
+#pragma unroll 4
+        for (int ks = 0; ks < c0 / 4; ++ks) {
+          const double a0 = arow[4 * ks], a1 = arow[8 * LD + 4 * ks];
+          const double* mrow = Mb + (4 * ks + t4) * MS_MLD + 8 * u0 + g;
+          dmma_16x8x4(acc[0], a0, a1, mrow[0]);
+          dmma_16x8x4(acc[1], a0, a1, mrow[8]);
+        }
+      } else {
+        for (int ks = 0; ks < c0 / 4; ++ks) {
+          const double a0 = arow[4 * ks], a1 = arow[8 * LD + 4 * ks];
+          const double* mrow = Mb + (4 * ks + t4) * MS_MLD + g;
+#pragma unroll
+          for (int v = 0; v < HU; ++v)
+            if (u0 + v < nt8) dmma_16x8x4(acc[v], a0, a1, mrow[8 * (u0 + v)]);
+        }
+      }
+#pragma unroll
+      for (int v = 0; v < HU; ++v) {
+        if (u0 + v < nt8) {
+          double* tp = Aw + g * LD + c0 + 8 * (u0 + v) + 2 * t4;
+          tp[0] = acc[v][0]; tp[1] = acc[v][1]; tp[8 * LD] = acc[v][2]; tp[8 * LD + 1] = acc[v][3];
+        }
+      }
+      pair_sync(1 + pair);
+      // phase 2: Q_J = T_J Winv_JJ
+#pragma unroll
+      for (int v = 0; v < HU; ++v)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[v][e] = 0.0;
+#pragma unroll
+      for (int ks = 0; ks < TB / 4; ++ks) {
+        if (4 * ks < 8 * nt8 && 4 * ks <= 8 * (u0 + HU - 1) + 7) {
+          const double a0 = arow[c0 + 4 * ks], a1 = arow[8 * LD + c0 + 4 * ks];
+          const double* mrow = Mb + (c0 + 4 * ks + t4) * MS_MLD + g;
+#pragma unroll
+          for (int v = 0; v < HU; ++v) {
+            const int u = u0 + v;
+            if (u < nt8 && 4 * ks <= 8 * u + 7) dmma_16x8x4(acc[v], a0, a1, mrow[8 * u]);
+          }
+        }
+      }
+      pair_sync(1 + pair);
+#pragma unroll
+      for (int v = 0; v < HU; ++v) {
+        const int u = u0 + v;
+        if (u < nt8) {
+          const int col = c0 + 8 * u + 2 * t4;
+          double* tp = Aw + g * LD + col;
+          tp[0] = acc[v][0]; tp[1] = acc[v][1]; tp[8 * LD] = acc[v][2]; tp[8 * LD + 1] = acc[v][3];
+          const int64_t ra = r0 + g, rb = r0 + g + 8;
+          if (ra < m) {
+            if (col < n) Q[ra * ldq + col] = to_out<TX>(acc[v][0]);
+            if (col + 1 < n) Q[ra * ldq + col + 1] = to_out<TX>(acc[v][1]);
+          }
+          if (rb < m) {
+            if (col < n) Q[rb * ldq + col] = to_out<TX>(acc[v][2]);
+            if (col + 1 < n) Q[rb * ldq + col + 1] = to_out<TX>(acc[v][3]);
+          }
+        }
+      }
+      pair_sync(1 + pair);
+    }
+  }
+}
+
+bool trsm_mstream_applicable(int n, size_t smem_optin) {
+  if (n <= 128 || n > 256 || getenv("RCHOLQR_NO_MSTREAM")) return false;
+  return mstream_smem((n + 7) / 8 * 8) <= smem_optin;
+}
+
+cudaError_t launch_trsm_mstream(const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M, void* Q,
+                                int64_t ldq, const int* status, int sms, cudaStream_t st) {
+  const int npad = (n + 7) / 8 * 8;
+  const size_t smem = mstream_smem(npad);
+  const int64_t ntiles = (m + 15) / 16;
+  const int grid = (int)std::min<int64_t>((ntiles + MS_PAIRS - 1) / MS_PAIRS, sms);
+  if (grid == 0) return cudaSuccess;
+  cudaError_t e;
+  if (dtype == RCHOLQR_F64) {
+    e = cudaFuncSetAttribute(trsm_mstream_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    trsm_mstream_kernel<double><<<grid, 64 * MS_PAIRS, smem, st>>>((const double*)X, m, n, npad, ldx, M, (double*)Q,
+                                                                  ldq, status);
+  } else {
+    e = cudaFuncSetAttribute(trsm_mstream_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    trsm_mstream_kernel<float><<<grid, 64 * MS_PAIRS, smem, st>>>((const float*)X, m, n, npad, ldx, M, (float*)Q,
+                                                                 ldq, status);
+  }
+  return cudaGetLastError();
+}
+
 // M = [-R_{<J,J}; Winv_JJ] packed (npad x npad, zero padded), diagonal blocks of width tb
 // (32 for the resident solves, 64/128 for the streamed one; tb <= 128).  One warp per row i of M:
 // the row of Winv_JJ solves w R_JJ = e_i by forward substitution, lane l holding w[Jb + l + 32 t].
