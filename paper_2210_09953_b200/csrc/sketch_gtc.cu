@@ -57,10 +57,10 @@ template <> struct GtFmt<double> {
   static constexpr int DX = 8, FB = 63, KT = 32, DIG = 3, RAW = 3;
 };
 
-template <typename TX>
+template <typename TX, int KT_ = GtFmt<TX>::KT>
 struct GtCfg {
   using Fm = GtFmt<TX>;
-  static constexpr int DX = Fm::DX, KT = Fm::KT;
+  static constexpr int DX = Fm::DX, KT = KT_;
   static constexpr int NB = GT_DZ * KT;                               // stacked Theta digit planes (MMA N)
   static constexpr int LEV = DX + GT_DZ - 1;                          // digit-product levels
   static constexpr int A_TILE = GT_M * GT_KC;                         // one X digit plane (128 x 32 B)
@@ -70,14 +70,13 @@ struct GtCfg {
   static constexpr int RAW_STAGE = GT_KC * GT_RAWLD * (int)sizeof(TX);
   static constexpr int TASKS_Z = (KT / 4) * (GT_KC / 4);              // Theta tasks per stage (quad x 4 rows)
   static constexpr size_t SMEM = (size_t)Fm::DIG * DIG_STAGE + (size_t)Fm::RAW * RAW_STAGE + 2048;   // + barriers, scales
-  static_assert(NB <= 256 && NB % 16 == 0 && LEV * KT <= 512 && KT % 8 == 0, "MMA / TMEM shape");
-  static_assert(TASKS_Z <= 32 * GT_TWARPS / 2, "one Theta task per group thread");
+  static_assert(KT % 8 == 0, "TMEM / core-matrix shape");
 };
 
 // offset of Theta-digit byte (row R of the stack, k) in the padded B tile
-template <typename TX>
+template <typename TX, int KT_ = GtFmt<TX>::KT>
 __device__ __forceinline__ int b_off(int R, int k) {
-  return (k >> 4) * GtCfg<TX>::B_LBO + (R >> 3) * GT_BSBO + (R & 7) * 16 + (k & 15);
+  return (k >> 4) * GtCfg<TX, KT_>::B_LBO + (R >> 3) * GT_BSBO + (R & 7) * 16 + (k & 15);
 }
 
 struct GtCol {
@@ -153,6 +152,8 @@ sketch_gauss_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int 
                        uint64_t seed, int tiles_k, int tiles_n, int64_t rows_per_split, double* __restrict__ part,
                        double* __restrict__ partc, int* overflow, int dbg) {
   using C = GtCfg<TX>;
+  static_assert(C::NB <= 256 && C::NB % 16 == 0 && C::LEV * C::KT <= 512, "MMA / TMEM shape");
+  static_assert(C::TASKS_Z <= 32 * GT_TWARPS / 2, "one Theta task per group thread");
   using F = GtFmt<TX>;
   constexpr int DX = C::DX, KT = C::KT, LEV = C::LEV;
   extern __shared__ __align__(1024) unsigned char sm[];
@@ -437,14 +438,16 @@ static_assert(GT_DRAIN % GP_GROUPS == 0, "drain stages belong to group 0");
 // |F_z F_x| term -- at or below the fp64 rounding of P (reading A17) -- so X digit b multiplies only
 // the Theta digits a < LK - b, a PREFIX of the stacked B tile (its MMA N shrinks accordingly).
 template <typename TX> struct GpLevels;
-template <> struct GpLevels<float> { static constexpr int LK = 8; };
-template <> struct GpLevels<double> { static constexpr int LK = 9; };
+template <> struct GpLevels<float> { static constexpr int LK = 8, KT = 40; };    // 80 Theta tasks: 10 quads x 8
+template <> struct GpLevels<double> { static constexpr int LK = 9, KT = 48; };   // 96 tasks fill a 3-warp group
+//   (fp64 can take KT = 48 because only LK levels live in TMEM: max_b (b KT + N_b) = 432 <= 512 columns;
+//    a B stack of 6 KT = 288 rows is issued as two MMAs of N = 256 and 32)
 __host__ __device__ constexpr int gp_nd(int b, int lk) { return (lk - b) < GT_DZ ? (lk - b) : GT_DZ; }
 __host__ __device__ constexpr int gp_n(int b, int lk, int kt) { return (gp_nd(b, lk) * kt + 15) / 16 * 16; }
 
 template <typename TX>
 struct GpCfg {
-  using G = GtCfg<TX>;
+  using G = GtCfg<TX, GpLevels<TX>::KT>;
   static constexpr int A_BYTES = G::DX * 4096;                        // DX planes of 128 x 32 B
   static constexpr int DIG_STAGE = A_BYTES + G::B_BYTES;
   static constexpr int STAGES = (232448 - 2048) / DIG_STAGE < 6 ? (232448 - 2048) / DIG_STAGE : 6;
@@ -515,7 +518,7 @@ __global__ void __launch_bounds__(GP_THREADS, 1)
 sketch_gauss_tcp_kernel(const unsigned char* __restrict__ dig, const uint32_t* __restrict__ maxbits, int64_t m, int n,
                         int64_t row_offset, int k, uint64_t seed, int tiles_k, int tiles_n, int64_t rows_per_split,
                         int stages_per_split, double* __restrict__ part, double* __restrict__ partc, int accumulate) {
-  using C = GtCfg<TX>;
+  using C = typename GpCfg<TX>::G;
   using P = GpCfg<TX>;
   using F = GtFmt<TX>;
   constexpr int DX = C::DX, KT = C::KT, LEV = C::LEV, S = P::STAGES;
@@ -556,7 +559,7 @@ sketch_gauss_tcp_kernel(const unsigned char* __restrict__ dig, const uint32_t* _
   const uint32_t tmem = *tmem_slot;
   if (warp < 4) {
     const uint32_t lb = tmem + ((uint32_t)(warp * 32) << 16);
-    for (int c8 = 0; c8 < LEV * KT / 8; ++c8) tc::st8_zero(lb + c8 * 8);
+    for (int c8 = 0; c8 < GpLevels<TX>::LK * KT / 8; ++c8) tc::st8_zero(lb + c8 * 8);
     tc::wait_st();
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -567,6 +570,7 @@ sketch_gauss_tcp_kernel(const unsigned char* __restrict__ dig, const uint32_t* _
     // ---------------------------------------------------------------- MMA issuer (lane 0)
     constexpr int LK = GpLevels<TX>::LK;
     static_assert(gp_n(0, LK, KT) == C::NB && LK > DX - 1, "level truncation shape");
+    static_assert((DX - 1) * KT + gp_n(DX - 1, LK, KT) <= 512 && LK * KT <= 512, "TMEM columns");
     for (int c = 0; c < nstages; ++c) {
       const int s = c % S;
       if (c > 0 && c % GT_DRAIN == 0) tc::mbar_wait(drained, (uint32_t)((c / GT_DRAIN - 1) & 1));
@@ -576,9 +580,15 @@ sketch_gauss_tcp_kernel(const unsigned char* __restrict__ dig, const uint32_t* _
         const uint32_t sa = tc::smem_u32(sm + (size_t)s * P::DIG_STAGE);
         const uint64_t db = tc::desc(sa + P::A_BYTES, C::B_LBO, GT_BSBO);
 #pragma unroll
-        for (int b = 0; b < DX; ++b)   // X digit b x Theta digits a < LK - b (levels b .. LK - 1)
-          tc::mma_i8(tmem + b * KT, tc::desc(sa + b * 4096, (GT_M / 8) * 128, 128), db,
-                     tc::idesc_i8(GT_M, gp_n(b, LK, KT), true, true), 1u);
+        for (int b = 0; b < DX; ++b) {   // X digit b x Theta digits a < LK - b (levels b .. LK - 1)
+          constexpr int NMAX = 256;      // MMA N limit: a longer prefix is issued as two MMAs
+          const int nb = gp_n(b, LK, KT);
+          const uint64_t da = tc::desc(sa + b * 4096, (GT_M / 8) * 128, 128);
+          tc::mma_i8(tmem + b * KT, da, db, tc::idesc_i8(GT_M, nb < NMAX ? nb : NMAX, true, true), 1u);
+          if (nb > NMAX)
+            tc::mma_i8(tmem + b * KT + NMAX, da, tc::desc(sa + P::A_BYTES + (NMAX / 8) * GT_BSBO, C::B_LBO, GT_BSBO),
+                       tc::idesc_i8(GT_M, nb - NMAX, true, true), 1u);
+        }
         tc::commit(&dempty[s]);
         if ((c + 1) % GT_DRAIN == 0 || c == nstages - 1) tc::commit(drainbar);
       }
@@ -645,7 +655,7 @@ sketch_gauss_tcp_kernel(const unsigned char* __restrict__ dig, const uint32_t* _
         }
       }
       if (d + 1 < ndrains) {
-        for (int c8 = 0; c8 < LEV * KT / 8; ++c8) tc::st8_zero(lb + c8 * 8);
+        for (int c8 = 0; c8 < GpLevels<TX>::LK * KT / 8; ++c8) tc::st8_zero(lb + c8 * 8);
         tc::wait_st();
       }
       asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -654,7 +664,7 @@ sketch_gauss_tcp_kernel(const unsigned char* __restrict__ dig, const uint32_t* _
     };
     int boff[4];
 #pragma unroll
-    for (int rr = 0; rr < 4; ++rr) boff[rr] = b_off<TX>(4 * q + rr, 4 * kq);
+    for (int rr = 0; rr < 4; ++rr) boff[rr] = b_off<TX, KT>(4 * q + rr, 4 * kq);
     int next_drain = 1;                                   // drain d is due before stage (d + 1) * GT_DRAIN
     for (int c = grp; c < nstages; c += GP_GROUPS) {
       const int s = c % S;
@@ -770,7 +780,7 @@ size_t gauss_tcp_chunk_workspace(int64_t m, int n, int dtype, int splits) {
   return gauss_tcp_workspace(chunk, n, dtype, splits);
 }
 
-int gauss_tc_kt(int dtype) { return dtype == RCHOLQR_F64 ? GtFmt<double>::KT : GtFmt<float>::KT; }
+int gauss_tc_kt(int dtype) { return dtype == RCHOLQR_F64 ? GpLevels<double>::KT : GpLevels<float>::KT; }
 
 bool gauss_tc_aligned(const void* X, int dtype, int n, int64_t ldx) {
   // TMA: 16-byte aligned base and row pitch
@@ -799,6 +809,7 @@ template <typename TX>
 static cudaError_t launch_gtc(const TX* X, int64_t m, int n, int64_t ldx, int64_t ro, int k, uint64_t seed,
                               int tiles_k, int tiles_n, int splits, int64_t rps, double* part, double* partc,
                               int* overflow, cudaStream_t st) {
+  tiles_k = (k + GtFmt<TX>::KT - 1) / GtFmt<TX>::KT;   // this variant's own Theta tile (the plan's is the pre-split's)
   EncodeTiledFn enc = encode_tiled();
   if (!enc) return cudaErrorNotSupported;
   CUtensorMap map;
