@@ -517,7 +517,8 @@ template <typename TX>
 __global__ void __launch_bounds__(GP_THREADS, 1)
 sketch_gauss_tcp_kernel(const unsigned char* __restrict__ dig, const uint32_t* __restrict__ maxbits, int64_t m, int n,
                         int64_t row_offset, int k, uint64_t seed, int tiles_k, int tiles_n, int64_t rows_per_split,
-                        int stages_per_split, double* __restrict__ part, double* __restrict__ partc, int accumulate) {
+                        int stages_per_split, double* __restrict__ part, double* __restrict__ partc, int accumulate,
+                        int dbg) {
   using C = typename GpCfg<TX>::G;
   using P = GpCfg<TX>;
   using F = GtFmt<TX>;
@@ -601,8 +602,9 @@ sketch_gauss_tcp_kernel(const unsigned char* __restrict__ dig, const uint32_t* _
       if (c >= S) tc::mbar_wait(&dempty[s], (uint32_t)(((c / S) - 1) & 1));
       if (lane == 0) {
         const size_t u = ((size_t)split * stages_per_split + c) * tiles_n + tn;
-        tc::mbar_arrive_tx(&dfull[s], (uint32_t)P::A_BYTES);
-        tc::bulk_g2s(sm + (size_t)s * P::DIG_STAGE, dig + u * P::A_BYTES, (uint32_t)P::A_BYTES, &dfull[s]);
+        const uint32_t bytes = (dbg & 1) ? 16u : (uint32_t)P::A_BYTES;   // ablation: no digit traffic
+        tc::mbar_arrive_tx(&dfull[s], bytes);
+        tc::bulk_g2s(sm + (size_t)s * P::DIG_STAGE, dig + u * P::A_BYTES, bytes, &dfull[s]);
       }
       __syncwarp();
     }
@@ -742,8 +744,10 @@ static cudaError_t launch_gtcp(const TX* X, int64_t m, int n, int64_t ldx, int64
   auto kern = sketch_gauss_tcp_kernel<TX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GpCfg<TX>::SMEM);
   if (e != cudaSuccess) return e;
+  static const int dbg = getenv("RCHOLQR_GTP_DEBUG") ? atoi(getenv("RCHOLQR_GTP_DEBUG")) : 0;   // ablations only
   kern<<<tiles_k * tiles_n * splits, GP_THREADS, GpCfg<TX>::SMEM, st>>>(dig, maxbits, m, n, ro, k, seed, tiles_k,
-                                                                         tiles_n, rps, stages, part, partc, accumulate);
+                                                                         tiles_n, rps, stages, part, partc, accumulate,
+                                                                         dbg);
   return cudaGetLastError();
 }
 
