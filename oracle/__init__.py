@@ -36,7 +36,7 @@ _lock = threading.Lock()
 _lib = None
 
 OK, E_INVALID, E_SHAPE, E_NONFINITE, E_SINGULAR, E_NOMEM = 0, 1, 2, 3, 4, 7
-GAUSSIAN, SPARSE_SIGN, RADEMACHER = 0, 1, 2
+GAUSSIAN, SPARSE_SIGN, RADEMACHER, SRHT = 0, 1, 2, 3
 F64, F32 = 0, 1
 
 
@@ -69,6 +69,10 @@ def _L():
             lib.oracle_theta_gauss_z.argtypes = [U64, I32, I64, I64, P]
             lib.oracle_theta_sparse.argtypes = [U64, I32, I32, I64, I64, P, P]
             lib.oracle_theta_rademacher.argtypes = [U64, I32, I64, I64, P]
+            lib.oracle_theta_srht.argtypes = [U64, I32, I64, I64, P]
+            lib.oracle_srht_rows.argtypes = [U64, I32, P]
+            lib.oracle_srht_sign.argtypes = [U64, U64, U64]
+            lib.oracle_srht_sign.restype = I32
             lib.oracle_rademacher_sign.argtypes = [U64, U64, I32]
             lib.oracle_rademacher_sign.restype = I32
             lib.oracle_sketch.argtypes = [P, I32, I64, I32, I64, I64, I32, I32, I32, U64, P]
@@ -179,6 +183,20 @@ def theta_rademacher(seed: int, k: int, m: int, row_offset: int = 0) -> np.ndarr
     return S
 
 
+def srht_rows(seed: int, k: int) -> np.ndarray:
+    """The k sampled Hadamard rows s_r (uint64, < 2^48) of the SRHT Theta (reading A23)."""
+    s = np.empty(k, dtype=np.uint64)
+    _L().oracle_srht_rows(seed, k, _ptr(s))
+    return s
+
+
+def theta_srht(seed: int, k: int, m: int, row_offset: int = 0) -> np.ndarray:
+    """SRHT signs (k, m) int8 (unscaled; Theta = signs / sqrt(k), reading A23)."""
+    S = np.empty((k, m), dtype=np.int8)
+    _L().oracle_theta_srht(seed, k, row_offset, m, _ptr(S))
+    return S
+
+
 def theta_dense(seed: int, k: int, m: int, sketch: int = GAUSSIAN, zeta: int = 8,
                 row_offset: int = 0) -> np.ndarray:
     """Explicit fp64 Theta (k x m) -- for tiny test inputs only."""
@@ -187,6 +205,8 @@ def theta_dense(seed: int, k: int, m: int, sketch: int = GAUSSIAN, zeta: int = 8
         return Z * (1.0 / np.sqrt(np.float64(k)))
     if sketch == RADEMACHER:
         return theta_rademacher(seed, k, m, row_offset).astype(np.float64) * (1.0 / np.sqrt(np.float64(k)))
+    if sketch == SRHT:
+        return theta_srht(seed, k, m, row_offset).astype(np.float64) * (1.0 / np.sqrt(np.float64(k)))
     rows, signs = theta_sparse(seed, k, zeta, m, row_offset)
     T = np.zeros((k, m), dtype=np.float64)
     v = 1.0 / np.sqrt(np.float64(zeta))

@@ -46,7 +46,8 @@
 
 enum { OR_OK = 0, OR_E_INVALID = 1, OR_E_SHAPE = 2, OR_E_NONFINITE = 3, OR_E_SINGULAR = 4,
        OR_E_NOMEM = 7 };
-enum { OR_GAUSSIAN = 0, OR_SPARSE_SIGN = 1, OR_RADEMACHER = 2 };
+enum { OR_GAUSSIAN = 0, OR_SPARSE_SIGN = 1, OR_RADEMACHER = 2, OR_SRHT = 3 };
+#define OR_SRHT_LOG2M 48   /* the SRHT's Hadamard order m' = 2^48 (reading A23) */
 #define OR_SKETCH_BLOCK 65536
 
 /* ------------------------------------------------------------------------------------------
@@ -195,6 +196,34 @@ int oracle_rademacher_sign(uint64_t seed, uint64_t i, int r) {
     return ((word >> (r % 32)) & 1u) ? -1 : 1;
 }
 
+/* SRHT (reading A23; "SRHT", used in all of the paper's experiments):
+ * Theta = sqrt(m'/k) R H D with m' = 2^48 (X zero-padded), D = diag(d_i) random signs, H the
+ * normalised Walsh-Hadamard matrix, H_si = (-1)^popcount(s & i) / sqrt(m'), R the k sampled rows
+ * s_0..s_{k-1}.  Hence Theta_ri = (-1)^popcount(s_r & i) d_i / sqrt(k) -- a dense +-1/sqrt(k) matrix
+ * evaluated entry by entry (no transform over m rows, so any row partition just sums).
+ *   d_i = +1 if bit 0 of word 0 of Philox(ctr = (i, 0, 6)) is 0, else -1;
+ *   s_r = 48-bit value (w1 << 32 | w0) & (2^48 - 1) of Philox(ctr = (r, a, 7)), the attempt a = 0, 1, ...
+ *         advancing until s_r differs from s_0..s_{r-1} (sampling without replacement). */
+void oracle_srht_rows(uint64_t seed, int k, uint64_t* s) {
+    for (int r = 0; r < k; ++r) {
+        for (uint32_t a = 0;; ++a) {
+            uint32_t w[4];
+            philox_for(seed, (uint64_t)r, a, 7u, w);
+            uint64_t v = (((uint64_t)w[1] << 32) | w[0]) & ((1ull << OR_SRHT_LOG2M) - 1);
+            int dup = 0;
+            for (int q = 0; q < r && !dup; ++q) dup = s[q] == v;
+            if (!dup) { s[r] = v; break; }
+        }
+    }
+}
+int oracle_srht_sign(uint64_t seed, uint64_t s_r, uint64_t i) {
+    uint32_t w[4];
+    philox_for(seed, i, 0u, 6u, w);
+    int d = (w[0] & 1u) ? -1 : 1;
+    int h = (__builtin_popcountll(s_r & i) & 1) ? -1 : 1;
+    return h * d;
+}
+
 /* ---------------- batch helpers for the tests ---------------- */
 void oracle_ln32_batch(const float* a, float* out, int64_t n) {
     for (int64_t t = 0; t < n; ++t) out[t] = oracle_ln32(a[t]);
@@ -219,6 +248,16 @@ void oracle_theta_rademacher(uint64_t seed, int k, int64_t row_offset, int64_t m
     for (int64_t ii = 0; ii < m; ++ii)
         for (int r = 0; r < k; ++r)
             S[(int64_t)r * m + ii] = (int8_t)oracle_rademacher_sign(seed, (uint64_t)(row_offset + ii), r);
+}
+/* S: k x m row-major int8 signs of the SRHT Theta (unscaled). */
+void oracle_theta_srht(uint64_t seed, int k, int64_t row_offset, int64_t m, int8_t* S) {
+    uint64_t* sr = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)(k > 0 ? k : 1));
+    oracle_srht_rows(seed, k, sr);
+    #pragma omp parallel for schedule(static)
+    for (int64_t ii = 0; ii < m; ++ii)
+        for (int r = 0; r < k; ++r)
+            S[(int64_t)r * m + ii] = (int8_t)oracle_srht_sign(seed, sr[r], (uint64_t)(row_offset + ii));
+    free(sr);
 }
 /* rows/signs: m x zeta row-major. */
 void oracle_theta_sparse(uint64_t seed, int k, int zeta, int64_t row_offset, int64_t m,
@@ -266,7 +305,9 @@ int oracle_sketch(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64
     size_t kn = (size_t)k * n;
     double* part = (double*)calloc((size_t)(nb > 0 ? nb : 1) * kn, sizeof(double));
     double* comp = (double*)calloc((size_t)(nb > 0 ? nb : 1) * kn, sizeof(double));
-    if (!part || !comp) { free(part); free(comp); return OR_E_NOMEM; }
+    uint64_t* srows = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)k);
+    if (!part || !comp || !srows) { free(part); free(comp); free(srows); return OR_E_NOMEM; }
+    if (sketch == OR_SRHT) oracle_srht_rows(seed, k, srows);
     #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t b = 0; b < nb; ++b) {
         double* Pb = part + (size_t)b * kn;
@@ -279,8 +320,10 @@ int oracle_sketch(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64
         int64_t i0 = b * OR_SKETCH_BLOCK, i1 = i0 + OR_SKETCH_BLOCK < m ? i0 + OR_SKETCH_BLOCK : m;
         for (int64_t i = i0; i < i1; ++i) {
             uint64_t gi = (uint64_t)(row_offset + i);
-            if (sketch == OR_GAUSSIAN || sketch == OR_RADEMACHER) {
-                if (sketch == OR_GAUSSIAN) {
+            if (sketch == OR_GAUSSIAN || sketch == OR_RADEMACHER || sketch == OR_SRHT) {
+                if (sketch == OR_SRHT) {
+                    for (int r = 0; r < k; ++r) th[r] = oracle_srht_sign(seed, srows[r], gi) > 0 ? sk : -sk;
+                } else if (sketch == OR_GAUSSIAN) {
                     float z[4];
                     for (int q = 0; q < (k + 3) / 4; ++q) {
                         oracle_gauss4(seed, gi, (uint32_t)q, z);
@@ -316,6 +359,7 @@ int oracle_sketch(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64
     }
     free(part);
     free(comp);
+    free(srows);
     for (size_t t = 0; t < kn; ++t)
         if (!isfinite(P[t])) return OR_E_NONFINITE;
     return OR_OK;
@@ -873,6 +917,14 @@ int oracle_factor_rr(const void* X, int dtype, int64_t m, int n, int64_t ldx, in
 double oracle_sketch_entry(const double* x, int64_t m, int64_t row_offset, int k, int sketch, int zeta,
                            uint64_t seed, int r) {
     int64_t nb = (m + OR_SKETCH_BLOCK - 1) / OR_SKETCH_BLOCK;
+    uint64_t sr_r = 0;
+    if (sketch == OR_SRHT) {
+        uint64_t* sr = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)k);
+        if (!sr) return NAN;
+        oracle_srht_rows(seed, k, sr);
+        sr_r = sr[r];
+        free(sr);
+    }
     double* part = (double*)calloc((size_t)(nb > 0 ? 2 * nb : 2), sizeof(double));
     if (!part) return NAN;
     #pragma omp parallel for schedule(dynamic, 1)
@@ -890,6 +942,8 @@ double oracle_sketch_entry(const double* x, int64_t m, int64_t row_offset, int k
                 dot2_add(&acc, &cmp, (double)z[r % 4] * sk, x[i]);
             } else if (sketch == OR_RADEMACHER) {
                 dot2_add(&acc, &cmp, oracle_rademacher_sign(seed, gi, r) > 0 ? sk : -sk, x[i]);
+            } else if (sketch == OR_SRHT) {
+                dot2_add(&acc, &cmp, oracle_srht_sign(seed, sr_r, gi) > 0 ? sk : -sk, x[i]);
             } else {
                 oracle_sparse_col(seed, k, zeta, gi, rows, sg);
                 for (int t = 0; t < zeta && t < 64; ++t)
