@@ -111,7 +111,8 @@ def _workload(cfg_name: str, ws: int, rank: int):
 def _cpu_sample_rate(X_dev, cfg, target_s: float, algo: str = "rcholqr", l: int = 0, tau: float = 0.0):
     """Time the oracle (as it stands, all host cores) on a bounded leading sample of X."""
     import oracle
-    so = {"gaussian": oracle.GAUSSIAN, "sparse": oracle.SPARSE_SIGN, "rademacher": oracle.RADEMACHER}[cfg["sketch"]]
+    so = {"gaussian": oracle.GAUSSIAN, "sparse": oracle.SPARSE_SIGN, "rademacher": oracle.RADEMACHER,
+          "srht": oracle.SRHT}[cfg["sketch"]]
     if algo == "rcholqr2":
         run = lambda A: oracle.factor2(A, cfg["k"], sketch=so, zeta=cfg["nnz"])  # noqa: E731
     elif algo == "rcholqr_rr":
@@ -142,7 +143,8 @@ def run_reference(args):
     cfg = synth.config(args.config)
     if args.sketch:
         cfg["sketch"] = args.sketch
-    so = {"gaussian": oracle.GAUSSIAN, "sparse": oracle.SPARSE_SIGN, "rademacher": oracle.RADEMACHER}[cfg["sketch"]]
+    so = {"gaussian": oracle.GAUSSIAN, "sparse": oracle.SPARSE_SIGN, "rademacher": oracle.RADEMACHER,
+          "srht": oracle.SRHT}[cfg["sketch"]]
     s_x = 8 if cfg["dtype"] == "f64" else 4
     per_step_s = max(1.0, 150.0 / (args.steps + args.warmup))
     # calibrate a sample size on the leading rows of the workload's X
@@ -322,10 +324,10 @@ def run(args):
                            "peak_source": "FP64 DMMA peak 37.2 TF (fp64-equivalent view of the exact int8 digits)",
                            "algorithmic": f"2*l*m*n = {flops:.4g} flop (Gaussian extract; the time includes "
                                           "the sparse sketch pass)", "traffic": None}
-    elif cfg["sketch"] == "rademacher" and n > 64:
+    elif cfg["sketch"] in ("rademacher", "srht") and n > 64:
         flops = 2.0 * k * m_local * n
         ach = flops / (per_ms["sketch"] * 1e-3) / 1e12
-        roofs["sketch"] = {"kernel": "sketch_gauss_kernel (Rademacher draws)", "bound": "tensor", "achieved": ach,
+        roofs["sketch"] = {"kernel": f"sketch_gauss_kernel ({cfg['sketch']} draws)", "bound": "tensor", "achieved": ach,
                            "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
                            "peak_source": "FP64 DMMA peak 37.2 TF", "algorithmic": f"2*k*m*n = {flops:.4g} flop",
                            "traffic": None}
@@ -512,7 +514,7 @@ def main():
                     help="Alg. 2 (default, the north star), Alg. 3 RCholeskyQR2 (orthonormal Q) or Alg. 5 "
                          "reduced RCholeskyQR (Z = L Q)")
     ap.add_argument("--l", type=int, default=0, help="Alg. 5: rows of the extractor L (default k)")
-    ap.add_argument("--sketch", default="", choices=["", "gaussian", "sparse", "rademacher"],
+    ap.add_argument("--sketch", default="", choices=["", "gaussian", "sparse", "rademacher", "srht"],
                     help="override the config's Theta (the BASELINE metric is quoted on the config's own)")
     ap.add_argument("--tau", type=float, default=0.0,
                     help="Alg. 7: truncation tolerance (default: the paper's 4e-15 fp64 / 2e-7 fp32)")

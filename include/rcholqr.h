@@ -32,7 +32,9 @@
  * scaled by sqrt(1/k)").  Sparse-sign: nnz_per_col nonzeros +-1/sqrt(nnz_per_col) per column,
  * one per block of k/nnz_per_col rows (BASELINE.json config 4; OSNAP block construction).
  * Rademacher (reading A22): +-1/sqrt(k), sign = bit (r mod 32) of word ((r mod 128)/32) of the
- * Philox call (i, r/128, domain 5).
+ * Philox call (i, r/128, domain 5).  SRHT (reading A23): sqrt(m'/k) R H D with m' = 2^48, i.e.
+ * (-1)^popcount(s_r & i) d_i / sqrt(k); d_i from Philox(i, 0, domain 6), the k distinct rows s_r from
+ * Philox(r, attempt, domain 7) (computed on the host when the plan is created).
  */
 #ifndef RCHOLQR_H
 #define RCHOLQR_H
@@ -47,7 +49,9 @@ extern "C" {
 typedef struct rcholqr_plan_s* rcholqr_plan;
 
 typedef enum { RCHOLQR_F64 = 0, RCHOLQR_F32 = 1 } rcholqr_dtype;          /* dtype of X and Q */
-typedef enum { RCHOLQR_GAUSSIAN = 0, RCHOLQR_SPARSE_SIGN = 1, RCHOLQR_RADEMACHER = 2 } rcholqr_sketch_kind;
+typedef enum {
+  RCHOLQR_GAUSSIAN = 0, RCHOLQR_SPARSE_SIGN = 1, RCHOLQR_RADEMACHER = 2, RCHOLQR_SRHT = 3
+} rcholqr_sketch_kind;
 
 typedef enum {
   RCHOLQR_OK = 0,

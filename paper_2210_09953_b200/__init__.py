@@ -18,7 +18,7 @@ from typing import Optional, Tuple
 __all__ = ["RCholQR", "RCholQRError", "load_library", "library_path", "theta_export",
            "comm_unique_id", "comm_create", "comm_destroy", "strerror", "version",
            "OK", "E_INVALID", "E_SHAPE", "E_NONFINITE", "E_SINGULAR", "E_CUDA", "E_NCCL", "E_NOMEM",
-           "GAUSSIAN", "SPARSE_SIGN", "RADEMACHER"]
+           "GAUSSIAN", "SPARSE_SIGN", "RADEMACHER", "SRHT"]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_PKG, "lib", "librcholqr.so")
@@ -26,7 +26,7 @@ _lock = threading.Lock()
 _lib = None
 
 OK, E_INVALID, E_SHAPE, E_NONFINITE, E_SINGULAR, E_CUDA, E_NCCL, E_NOMEM = range(8)
-GAUSSIAN, SPARSE_SIGN, RADEMACHER = 0, 1, 2
+GAUSSIAN, SPARSE_SIGN, RADEMACHER, SRHT = 0, 1, 2, 3
 F64, F32 = 0, 1
 
 # exported symbols (checked by tests/test_abi.py against include/rcholqr.h)
@@ -141,7 +141,7 @@ class RCholQR:
             raise TypeError("dtype must be torch.float64 or torch.float32")
         self.n, self.k, self.dtype, self.seed, self.device = int(n), int(k), dtype, int(seed), int(device)
         self.sketch_kind = {"gaussian": GAUSSIAN, "sparse": SPARSE_SIGN, "sparse_sign": SPARSE_SIGN,
-                            "rademacher": RADEMACHER}[sketch]
+                            "rademacher": RADEMACHER, "srht": SRHT}[sketch]
         self.nnz_per_col = int(nnz_per_col)
         self._lib = load_library()
         d = _Desc(self.n, self.k, F64 if dtype == torch.float64 else F32, self.sketch_kind, self.nnz_per_col,
@@ -319,9 +319,9 @@ def theta_export(seed: int, k: int, m: int, sketch: str = "gaussian", nnz_per_co
     torch = _torch()
     lib = load_library()
     dev = torch.device("cuda", device)
-    if sketch in ("gaussian", "rademacher"):
+    if sketch in ("gaussian", "rademacher", "srht"):
         Z = torch.empty((k, m), dtype=torch.float32, device=dev)
-        kind = GAUSSIAN if sketch == "gaussian" else RADEMACHER
+        kind = {"gaussian": GAUSSIAN, "rademacher": RADEMACHER, "srht": SRHT}[sketch]
         _check(lib.rcholqr_theta_export(seed, k, kind, 0, row_offset, m, _ptr(Z), None, None,
                                         _stream_ptr(stream)), "rcholqr_theta_export")
         return Z

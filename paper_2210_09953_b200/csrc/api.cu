@@ -9,6 +9,7 @@
 #include <cmath>
 #include <cstring>
 #include <mutex>
+#include <unordered_set>
 #include <vector>
 #include "internal.cuh"
 #include "rcholqr.h"
@@ -48,6 +49,35 @@ bool nccl_load() {
 }  // namespace
 
 // ---------------------------------------------------------------------------------------------
+// SRHT sampled rows (reading A23), computed on the host at plan creation: a host
+// Philox4x32-10 (Salmon et al. SC'11; the device generator is theta.cuh's philox_at).
+namespace {
+void host_philox(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint64_t seed, uint32_t out[4]) {
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+  uint32_t c[4] = {c0, c1, c2, c3};
+  for (int round = 0; round < 10; ++round) {
+    if (round) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    const uint64_t p0 = (uint64_t)0xD2511F53u * c[0], p1 = (uint64_t)0xCD9E8D57u * c[2];
+    const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c[1] ^ k0, n2 = (uint32_t)(p0 >> 32) ^ c[3] ^ k1;
+    c[0] = n0; c[1] = (uint32_t)p1; c[2] = n2; c[3] = (uint32_t)p0;
+  }
+  for (int t = 0; t < 4; ++t) out[t] = c[t];
+}
+// s_r = (w1 << 32 | w0) mod 2^48 of Philox(ctr = (r, 0, a, 7)), a advancing past duplicates
+std::vector<uint64_t> srht_rows_host(uint64_t seed, int k) {
+  std::vector<uint64_t> s((size_t)k);
+  std::unordered_set<uint64_t> seen;
+  for (int r = 0; r < k; ++r)
+    for (uint32_t a = 0;; ++a) {
+      uint32_t w[4];
+      host_philox((uint32_t)r, 0u, a, 7u, seed, w);
+      const uint64_t v = (((uint64_t)w[1] << 32) | w[0]) & ((1ull << 48) - 1);
+      if (seen.insert(v).second) { s[(size_t)r] = v; break; }
+    }
+  return s;
+}
+}  // namespace
+
 // Which tall-solve kernels serve n columns of dtype (the plan's n, or Alg. 7's rank r).
 struct SolvePlan {
   TrsmLaunch tr{};
@@ -78,6 +108,7 @@ struct rcholqr_plan_s {
   // rank-revealing RCholeskyQR (Alg. 7), allocated on first use: [P; colsq] (k + 1) x n, P D^{-1},
   // the pivoting workspace, P(:, perm), R, R11^{-1}, the compact R11, d, column partials, scalars
   double* rr_buf = nullptr; double* rr_Pn = nullptr; double* rr_A = nullptr; double* rr_Pg = nullptr;
+  uint64_t* srht_d = nullptr;   // SRHT: the k sampled Hadamard rows
   double* rr_R = nullptr; double* rr_W = nullptr; double* rr_R11 = nullptr; double* rr_d = nullptr;
   double* rr_cpart = nullptr; double* rr_sd = nullptr; int* rr_si = nullptr; int* rr_perm = nullptr;
   int* rr_qst = nullptr; int rr_splits = 0;
@@ -139,7 +170,8 @@ rcholqr_status cuda_status(cudaError_t e) {
 rcholqr_status validate_desc(const rcholqr_desc* d) {
   if (!d) return RCHOLQR_E_INVALID;
   if (d->dtype != RCHOLQR_F64 && d->dtype != RCHOLQR_F32) return RCHOLQR_E_INVALID;
-  if (d->sketch != RCHOLQR_GAUSSIAN && d->sketch != RCHOLQR_SPARSE_SIGN && d->sketch != RCHOLQR_RADEMACHER)
+  if (d->sketch != RCHOLQR_GAUSSIAN && d->sketch != RCHOLQR_SPARSE_SIGN && d->sketch != RCHOLQR_RADEMACHER &&
+      d->sketch != RCHOLQR_SRHT)
     return RCHOLQR_E_INVALID;
   if (d->n < 1 || d->k < d->n) return RCHOLQR_E_SHAPE;
   if (d->sketch == RCHOLQR_SPARSE_SIGN &&
@@ -367,6 +399,16 @@ rcholqr_status rcholqr_create(const rcholqr_desc* desc, rcholqr_plan* out) {
     rcholqr_destroy(p);
     return RCHOLQR_E_NOMEM;
   }
+  if (desc->sketch == RCHOLQR_SRHT) {
+    const std::vector<uint64_t> rows = srht_rows_host(desc->seed, k);
+    if (cudaMalloc(&p->srht_d, sizeof(uint64_t) * (size_t)k) != cudaSuccess ||
+        cudaMemcpy(p->srht_d, rows.data(), sizeof(uint64_t) * (size_t)k, cudaMemcpyHostToDevice) != cudaSuccess) {
+      cudaGetLastError();
+      rcholqr_destroy(p);
+      return RCHOLQR_E_NOMEM;
+    }
+    p->sk.srht_s = p->srht_d;
+  }
   cudaMemset(p->status_d, 0, sizeof(int));
   *p->status_h = 0;
   *out = p;
@@ -382,7 +424,7 @@ rcholqr_status rcholqr_destroy(rcholqr_plan p) {
   cudaFree(p->red_part); cudaFree(p->red_partc); cudaFree(p->red_P);
   cudaFree(p->rr_buf); cudaFree(p->rr_Pn); cudaFree(p->rr_A); cudaFree(p->rr_Pg); cudaFree(p->rr_R); cudaFree(p->rr_W);
   cudaFree(p->rr_R11); cudaFree(p->rr_d); cudaFree(p->rr_cpart); cudaFree(p->rr_sd); cudaFree(p->rr_si);
-  cudaFree(p->rr_perm); cudaFree(p->rr_qst); cudaFree(p->rr_xr);
+  cudaFree(p->rr_perm); cudaFree(p->rr_qst); cudaFree(p->rr_xr); cudaFree(p->srht_d);
   if (p->status_h) cudaFreeHost(p->status_h);
   cudaFree(p->xbuf); cudaFree(p->qbuf); cudaFree(p->rbuf); cudaFree(p->sbuf); cudaFree(p->tbuf);
   for (int t = 0; t < 7; ++t)
@@ -476,9 +518,6 @@ rcholqr_status rcholqr_factor_reduced(rcholqr_plan p, const void* X, int64_t m, 
   cudaStream_t st = (cudaStream_t)stream;
   if (p->red_l != l) {   // the (k + l)-row launch (Gaussian Theta) or the l-row extractor launch (sparse Theta)
     cudaFree(p->red_part); cudaFree(p->red_partc); cudaFree(p->red_P);
-  cudaFree(p->rr_buf); cudaFree(p->rr_Pn); cudaFree(p->rr_A); cudaFree(p->rr_Pg); cudaFree(p->rr_R); cudaFree(p->rr_W);
-  cudaFree(p->rr_R11); cudaFree(p->rr_d); cudaFree(p->rr_cpart); cudaFree(p->rr_sd); cudaFree(p->rr_si);
-  cudaFree(p->rr_perm); cudaFree(p->rr_qst); cudaFree(p->rr_xr);
     p->red_part = p->red_partc = p->red_P = nullptr;
     p->red_l = 0;
     p->red_sk = plan_sketch(gauss ? k + l : l, n, p->d.dtype, RCHOLQR_GAUSSIAN, p->d.nnz_per_col, p->sms, p->smem_optin);
@@ -736,12 +775,21 @@ rcholqr_status rcholqr_tri_solve(rcholqr_plan p, const void* X, int64_t m, int64
 rcholqr_status rcholqr_theta_export(uint64_t seed, int32_t k, int32_t sketch, int32_t zeta, int64_t ro, int64_t m,
                                     float* Z, int32_t* rows, int8_t* signs, void* stream) {
   if (k < 1 || m < 0 || ro < 0) return RCHOLQR_E_INVALID;
-  if (sketch != RCHOLQR_GAUSSIAN && sketch != RCHOLQR_SPARSE_SIGN && sketch != RCHOLQR_RADEMACHER)
+  if (sketch != RCHOLQR_GAUSSIAN && sketch != RCHOLQR_SPARSE_SIGN && sketch != RCHOLQR_RADEMACHER &&
+      sketch != RCHOLQR_SRHT)
     return RCHOLQR_E_INVALID;
   if (sketch == RCHOLQR_SPARSE_SIGN && (zeta < 1 || zeta > k || k % zeta != 0)) return RCHOLQR_E_SHAPE;
   cudaStream_t st = (cudaStream_t)stream;
-  CU(launch_theta_export(seed, k, sketch, zeta, ro, m, Z, rows, signs, st));
-  CU(cudaStreamSynchronize(st));
+  uint64_t* sd = nullptr;
+  if (sketch == RCHOLQR_SRHT) {
+    const std::vector<uint64_t> rows_h = srht_rows_host(seed, k);
+    CU(cudaMalloc(&sd, sizeof(uint64_t) * (size_t)k));
+    CU(cudaMemcpy(sd, rows_h.data(), sizeof(uint64_t) * (size_t)k, cudaMemcpyHostToDevice));
+  }
+  cudaError_t e = launch_theta_export(seed, k, sketch, zeta, ro, m, Z, rows, signs, st, sd);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  cudaFree(sd);
+  CU(e);
   return RCHOLQR_OK;
 }
 

@@ -28,7 +28,7 @@ bool sparse_tc_applicable(int k, int n, int zeta);
 bool sparse_tc_aligned(const void* X, int dtype, int n, int64_t ldx);
 cudaError_t launch_sparse_tc(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                              int zeta, uint64_t seed, int splits, int64_t rows_per_split, double* part, int* overflow,
-                             cudaStream_t st);
+                             cudaStream_t st, const uint64_t* srht_s = nullptr);
 enum TrsmKind : int { kTrsm64x24 = 0, kTrsm128x64 = 1, kTrsm128x112 = 2, kTrsm128x128 = 3 };
 enum QrKind : int { kQrSmem = 0, kQrGlobal = 1, kQrBlocked = 2 };
 
@@ -41,7 +41,8 @@ struct SketchLaunch {
   int tc = 0, tc_tiles_k = 0, tc_tiles_n = 0, tc_splits = 0;
   // Rademacher Theta (reading A22): the DMMA kernel above draws +-1 instead of N(0,1); rad_tc: the
   // tcgen05 int8 kernel of sketch_tc.cu with a dense E tile in front of it (n <= 64, k <= 512)
-  int rad = 0, rad_tc = 0, rad_splits = 0;
+  int rad = 0, rad_tc = 0, rad_splits = 0;   // rad: 1 = Rademacher, 2 = SRHT (reading A23)
+  const uint64_t* srht_s = nullptr;          // SRHT: the k sampled Hadamard rows (plan-owned device array)
   int max_splits() const {
     int s = tc && tc_splits > splits ? tc_splits : splits;
     return rad_tc && rad_splits > s ? rad_splits : s;
@@ -85,7 +86,8 @@ cudaError_t launch_qr_blocked(const double* P, int k, int n, double* R, double* 
 cudaError_t launch_form_s(const double* Awork, const double* tau, const double* diag, int k, int n,
                           double* S, const int* status, cudaStream_t st);
 cudaError_t launch_theta_export(uint64_t seed, int k, int sketch, int zeta, int64_t row_offset, int64_t m,
-                                float* Z, int32_t* rows, int8_t* signs, cudaStream_t st);
+                                float* Z, int32_t* rows, int8_t* signs, cudaStream_t st,
+                                const uint64_t* srht_s = nullptr);
 cudaError_t launch_check_diag(const double* R, int n, int* status, cudaStream_t st);
 // blocked substitution (default tall solve for n <= 128): M = [-R_{<J,J}; Winv_JJ] packed
 int trsm_resident_tm(int n, int dtype, size_t smem_optin);   // 0 = not applicable

@@ -87,7 +87,7 @@ __global__ void __launch_bounds__(SK_THREADS, 1)
 sketch_gauss_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                     uint64_t seed, int tiles_k, int tiles_n, int64_t rows_per_split,
                     double* __restrict__ part, double* __restrict__ partc, const WarpPlan plan, int seg_chunks,
-                    const int* __restrict__ guard, int rad) {
+                    const int* __restrict__ guard, int rad, const uint64_t* __restrict__ srht_s) {
   // guard != null: recompute only if the tensor-core sketch (sketch_gtc.cu) flagged a headroom overflow
   if (guard && *guard == 0) return;
   using C = GCfg<TX, MS, NS>;
@@ -143,8 +143,9 @@ sketch_gauss_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int
             const int rb = r0 + 4 * qq;
             float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
             if (i0 + ii < i_end && rb < k)
-              z = rad ? rademacher4(seed, (uint64_t)(row_offset + i0 + ii), (uint32_t)rb)
-                      : gauss4_x2(seed, (uint64_t)(row_offset + i0 + ii), (uint32_t)(rb >> 2));
+              z = rad == 2 ? srht4(srht_s, k, seed, (uint64_t)(row_offset + i0 + ii), (uint32_t)rb)
+                  : rad ? rademacher4(seed, (uint64_t)(row_offset + i0 + ii), (uint32_t)rb)
+                        : gauss4_x2(seed, (uint64_t)(row_offset + i0 + ii), (uint32_t)(rb >> 2));
             double* Tc = T + (4 * qq) * C::TS_LD + ii;
             Tc[0 * C::TS_LD] = (rb + 0 < k) ? (double)z.x : 0.0;
             Tc[1 * C::TS_LD] = (rb + 1 < k) ? (double)z.y : 0.0;
@@ -454,6 +455,18 @@ __global__ void theta_rademacher_export_kernel(uint64_t seed, int k, int64_t row
   }
 }
 
+__global__ void theta_srht_export_kernel(const uint64_t* s, uint64_t seed, int k, int64_t row_offset, int64_t m,
+                                         float* Z) {
+  const int nq = (k + 3) / 4;
+  for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < m * nq; c += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = c % m;
+    const int q = (int)(c / m);
+    const float4 z = srht4(s, k, seed, (uint64_t)(row_offset + i), (uint32_t)(4 * q));
+    const float v[4] = {z.x, z.y, z.z, z.w};
+    for (int t = 0; t < 4 && 4 * q + t < k; ++t) Z[(int64_t)(4 * q + t) * m + i] = v[t];
+  }
+}
+
 __global__ void theta_gauss_export_kernel(uint64_t seed, int k, int64_t row_offset, int64_t m, float* Z) {
   const int nq = (k + 3) / 4;
   for (int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c < m * nq; c += (int64_t)gridDim.x * blockDim.x) {
@@ -613,8 +626,8 @@ SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms,
   L = cand[best];
   L.splits = choose_splits(L.tiles_k * L.tiles_n, sms);
   L.tc = 0;
-  if (sketch == RCHOLQR_RADEMACHER) {   // DMMA kernel drawing +-1, the dense tcgen05 int8 kernel in front of it
-    L.rad = 1;
+  if (sketch == RCHOLQR_RADEMACHER || sketch == RCHOLQR_SRHT) {   // DMMA kernel drawing +-1, dense tcgen05 in front
+    L.rad = sketch == RCHOLQR_SRHT ? 2 : 1;
     if (sparse_tc_applicable(k, n, 1) && !getenv("RCHOLQR_RADEMACHER_DMMA")) {
       L.rad_tc = 1;
       L.rad_splits = sms;
@@ -645,7 +658,7 @@ static cudaError_t launch_g(const SketchLaunch& L, const void* X, int64_t m, int
     if (plan.cnt[w] > GCfg<TX, MS, NS>::UMAX) return cudaErrorInvalidConfiguration;
   kern<<<L.tiles_k * L.tiles_n * L.splits, SK_THREADS, L.smem, st>>>((const TX*)X, m, n, ldx, ro, k, seed,
                                                                      L.tiles_k, L.tiles_n, rps, part, partc, plan,
-                                                                     seg_chunks(), guard, L.rad);
+                                                                     seg_chunks(), guard, L.rad, L.srht_s);
   return cudaGetLastError();
 }
 
@@ -717,7 +730,8 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
     int splits = L.splits;
     const int* guard = nullptr;
     const bool tc = L.tc && gauss_tc_aligned(X, dtype, n, ldx);
-    if (L.rad_tc && sparse_tc_aligned(X, dtype, n, ldx)) {
+    // (SRHT: the tcgen05 E tile splits the global row as (multiple of 32) + lane, so row_offset % 32 == 0)
+    if (L.rad_tc && sparse_tc_aligned(X, dtype, n, ldx) && (L.rad != 2 || row_offset % 32 == 0)) {
       // dense +-1 E tile on the sparse sketch's tcgen05 kernel (zeta = 0); it writes no compensation
       // partials, so they are zeroed for the fixed-order reduction; the DMMA kernel below reruns
       // (guarded) on a headroom overflow
@@ -728,7 +742,8 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
         e = cudaMemsetAsync(flag, 0, sizeof(int), st);
         if (e == cudaSuccess) e = cudaMemsetAsync(partc, 0, sizeof(double) * (size_t)splits * k * n, st);
         if (e == cudaSuccess)
-          e = launch_sparse_tc(X, dtype, m, n, ldx, row_offset, k, 0, seed, splits, trps, part, flag, st);
+          e = launch_sparse_tc(X, dtype, m, n, ldx, row_offset, k, L.rad == 2 ? -1 : 0, seed, splits, trps, part,
+                               flag, st, L.srht_s);
         if (e != cudaSuccess) return e;
         guard = flag;
       } else {
@@ -788,13 +803,14 @@ cudaError_t launch_reduce(const double* part, int splits, int64_t kn, double sca
 }
 
 cudaError_t launch_theta_export(uint64_t seed, int k, int sketch, int zeta, int64_t row_offset, int64_t m,
-                                float* Z, int32_t* rows, int8_t* signs, cudaStream_t st) {
+                                float* Z, int32_t* rows, int8_t* signs, cudaStream_t st, const uint64_t* srht_s) {
   if (m == 0) return cudaSuccess;
-  if (sketch == RCHOLQR_GAUSSIAN || sketch == RCHOLQR_RADEMACHER) {
+  if (sketch == RCHOLQR_GAUSSIAN || sketch == RCHOLQR_RADEMACHER || sketch == RCHOLQR_SRHT) {
     if (!Z) return cudaSuccess;
     const int64_t work = m * ((k + 3) / 4);
     const int blocks = (int)std::min<int64_t>((work + 255) / 256, 65535);
-    if (sketch == RCHOLQR_RADEMACHER) theta_rademacher_export_kernel<<<blocks, 256, 0, st>>>(seed, k, row_offset, m, Z);
+    if (sketch == RCHOLQR_SRHT) theta_srht_export_kernel<<<blocks, 256, 0, st>>>(srht_s, seed, k, row_offset, m, Z);
+    else if (sketch == RCHOLQR_RADEMACHER) theta_rademacher_export_kernel<<<blocks, 256, 0, st>>>(seed, k, row_offset, m, Z);
     else theta_gauss_export_kernel<<<blocks, 256, 0, st>>>(seed, k, row_offset, m, Z);
   } else {
     const int blocks = (int)std::min<int64_t>((m + 255) / 256, 65535);

@@ -144,7 +144,8 @@ __device__ __forceinline__ void split_words(double x, const ColParam& p, uint32_
 template <typename TX>
 __global__ void __launch_bounds__(STC_THREADS, 1)
 sketch_sparse_tc_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64_t row_offset, int k, int zeta,
-                        uint64_t seed, int tiles_k, int64_t rows_per_split, double* __restrict__ part, int* overflow, int dbg) {
+                        uint64_t seed, int tiles_k, int64_t rows_per_split, double* __restrict__ part, int* overflow, int dbg,
+                        const uint64_t* __restrict__ srht_s) {
   using C = StcCfg<TX>;
   using F = Fmt<TX>;
   constexpr int D = C::D;
@@ -325,13 +326,15 @@ sketch_sparse_tc_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx,
     const int ii = half * 32 + lane;
     const int zoff = half * 2 * STC_M * 16;               // k-blocks 2half, 2half+1 of the E tile
     const bool full_tile = (zeta == 8 && k <= STC_M);     // common case: 8 nonzeros, one Theta row tile
-    const bool dense = zeta == 0;                         // Rademacher (reading A22): every entry +-1
+    const bool dense = zeta <= 0;                         // Rademacher (0, reading A22) / SRHT (-1, A23): all +-1
+    const bool srht = zeta < 0;
     for (int c = grp; c < nstages; c += 2) {
       const int s = c % F::DIG;
       const int64_t i0 = i_begin + (int64_t)c * STC_KC;
       const int rows = (int)min((int64_t)STC_KC, i_end - i0);
       const uint64_t gi = (uint64_t)(row_offset + i0 + ii);
-      const uint4 w = philox_at(seed, gi, dense ? (uint32_t)tk : 0u, dense ? kDomainRademacher : kDomainSparse);
+      const uint4 w = philox_at(seed, gi, srht ? 0u : (dense ? (uint32_t)tk : 0u),
+                                srht ? kDomainSrhtD : (dense ? kDomainRademacher : kDomainSparse));
       if (c >= F::DIG) tc::mbar_wait(&dempty[s], (uint32_t)(((c / F::DIG) - 1) & 1));
       unsigned char* st = dig_base + (size_t)s * C::DIG_STAGE;
       if (dense) {
@@ -339,17 +342,39 @@ sketch_sparse_tc_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx,
         // sign of X row half*32 + L; lane r & 31 keeps the masks of rows r = lane + 32 q.  Each mask is
         // expanded to two 16-byte K-runs (k-blocks 2 half, 2 half + 1) of +-1 bytes (0 beyond `rows`).
         const uint32_t valid = __ballot_sync(0xffffffffu, ii < rows);
-        const uint32_t wd[4] = {w.x, w.y, w.z, w.w};
         uint32_t mine[4];
+        if (srht) {
+          // lane L takes Theta rows r = r0 + L + 32 q.  The warp's global rows are B + lane' with
+          // B = gi - lane a multiple of 32 (row_offset % 32 == 0), so popcount(s & (B + lane')) splits
+          // as popcount(s & B) + popcount(s & lane'): the mask over lane' is the Walsh mask of s & 31,
+          // flipped when popcount(s & B) is odd, XOR the ballot of the d_i signs.
+          const uint32_t dmask = __ballot_sync(0xffffffffu, w.x & 1u);
+          const uint64_t B = gi - (uint64_t)lane;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint32_t keep = 0u;
-#pragma unroll
-          for (int b = 0; b < 32; ++b) {
-            const uint32_t msk = __ballot_sync(0xffffffffu, (wd[q] >> b) & 1u);
-            keep = lane == b ? msk : keep;
+          for (int q = 0; q < 4; ++q) {
+            const int r = r0 + lane + 32 * q;
+            const uint64_t sr = r < k ? srht_s[r] : 0ull;
+            const uint32_t t = (uint32_t)sr & 31u;
+            uint32_t wm = 0u;
+            wm ^= (t & 1u) ? 0xAAAAAAAAu : 0u;
+            wm ^= (t & 2u) ? 0xCCCCCCCCu : 0u;
+            wm ^= (t & 4u) ? 0xF0F0F0F0u : 0u;
+            wm ^= (t & 8u) ? 0xFF00FF00u : 0u;
+            wm ^= (t & 16u) ? 0xFFFF0000u : 0u;
+            mine[q] = wm ^ ((__popcll(sr & B) & 1) ? 0xFFFFFFFFu : 0u) ^ dmask;
           }
-          mine[q] = keep;
+        } else {
+          const uint32_t wd[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            uint32_t keep = 0u;
+#pragma unroll
+            for (int b = 0; b < 32; ++b) {
+              const uint32_t msk = __ballot_sync(0xffffffffu, (wd[q] >> b) & 1u);
+              keep = lane == b ? msk : keep;
+            }
+            mine[q] = keep;
+          }
         }
         if (!(dbg & 4)) {
 #pragma unroll
@@ -453,25 +478,26 @@ bool sparse_tc_applicable(int k, int n, int zeta) { return n <= STC_N && zeta >=
 
 template <typename TX>
 static cudaError_t launch_stc(const TX* X, int64_t m, int n, int64_t ldx, int64_t ro, int k, int zeta, uint64_t seed,
-                              int tiles_k, int splits, int64_t rps, double* part, int* overflow, cudaStream_t st) {
+                              int tiles_k, int splits, int64_t rps, double* part, int* overflow, cudaStream_t st,
+                              const uint64_t* srht_s) {
   auto kern = sketch_sparse_tc_kernel<TX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)StcCfg<TX>::SMEM);
   if (e != cudaSuccess) return e;
   static const int dbg = getenv("RCHOLQR_STC_DEBUG") ? atoi(getenv("RCHOLQR_STC_DEBUG")) : 0;   // ablations only
   kern<<<tiles_k * splits, STC_THREADS, StcCfg<TX>::SMEM, st>>>(X, m, n, ldx, ro, k, zeta, seed, tiles_k, rps, part,
-                                                                 overflow, dbg);
+                                                                 overflow, dbg, srht_s);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sparse_tc(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                              int zeta, uint64_t seed, int splits, int64_t rows_per_split, double* part, int* overflow,
-                             cudaStream_t st) {
+                             cudaStream_t st, const uint64_t* srht_s) {
   const int tiles_k = (k + STC_M - 1) / STC_M;
   if (dtype == RCHOLQR_F64)
     return launch_stc((const double*)X, m, n, ldx, row_offset, k, zeta, seed, tiles_k, splits, rows_per_split, part,
-                      overflow, st);
+                      overflow, st, srht_s);
   return launch_stc((const float*)X, m, n, ldx, row_offset, k, zeta, seed, tiles_k, splits, rows_per_split, part,
-                    overflow, st);
+                    overflow, st, srht_s);
 }
 
 bool sparse_tc_aligned(const void* X, int dtype, int n, int64_t ldx) {

@@ -24,7 +24,8 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
 }
 
 // Counter layout (A2): ctr = (lo32(i), hi32(i), q, domain), key = (lo32(seed), hi32(seed)).
-enum : uint32_t { kDomainGauss = 1u, kDomainSparse = 2u, kDomainRademacher = 5u };
+enum : uint32_t { kDomainGauss = 1u, kDomainSparse = 2u, kDomainRademacher = 5u, kDomainSrhtD = 6u,
+                  kDomainSrhtRows = 7u };
 
 __device__ __forceinline__ uint4 philox_at(uint64_t seed, uint64_t i, uint32_t q, uint32_t domain) {
   return philox4x32_10(make_uint4((uint32_t)i, (uint32_t)(i >> 32), q, domain), (uint32_t)seed,
@@ -191,6 +192,22 @@ __device__ __forceinline__ float4 rademacher4(uint64_t seed, uint64_t i, uint32_
   const uint32_t word = q == 0 ? w.x : (q == 1 ? w.y : (q == 2 ? w.z : w.w));
   const uint32_t b = word >> (rb & 31u);
   return make_float4((b & 1u) ? -1.f : 1.f, (b & 2u) ? -1.f : 1.f, (b & 4u) ? -1.f : 1.f, (b & 8u) ? -1.f : 1.f);
+}
+
+// SRHT (reading A23): Theta_ri = (-1)^popcount(s_r & i) d_i / sqrt(k); the sign of rows
+// rb..rb+3 at global X-row i given the sampled Hadamard rows s (k of them, device array).
+__device__ __forceinline__ float srht_d(uint64_t seed, uint64_t i) {
+  return (philox_at(seed, i, 0u, kDomainSrhtD).x & 1u) ? -1.f : 1.f;
+}
+__device__ __forceinline__ float4 srht4(const uint64_t* __restrict__ s, int k, uint64_t seed, uint64_t i, uint32_t rb) {
+  const float d = srht_d(seed, i);
+  float v[4];
+#pragma unroll
+  for (int t = 0; t < 4; ++t) {
+    const uint64_t sr = (int)rb + t < k ? s[rb + t] : 0ull;
+    v[t] = (__popcll(sr & i) & 1) ? -d : d;
+  }
+  return make_float4(v[0], v[1], v[2], v[3]);
 }
 
 }  // namespace rcq
