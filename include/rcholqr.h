@@ -110,6 +110,15 @@ rcholqr_status rcholqr_factor_host(rcholqr_plan plan, const void* X_host, int64_
                                    int64_t row_offset, int64_t ldx, void* Q_host, int64_t ldq,
                                    double* R_host, double* S_host, void* stream);
 
+/* Alg. 2 for COLUMN-MAJOR X and Q (element (i, j) at X[j * ldx + i], ldx >= m_local; the storage the
+ * paper notes favours sketching).  Layout adapter: X is transposed on the GPU into a
+ * plan-owned row-major buffer, factored by the row-major path (bitwise the same R, S and Q values), and
+ * Q transposed back -- two extra passes over m_local x n (native column-major kernels: DESIGN.md NEXT).
+ *   X [device] n columns of m_local rows, leading dim ldx;  Q [device] likewise, leading dim ldq;
+ *   R, S, row_offset, stream: as for rcholqr_factor.  Q must not overlap X.  SYNCHRONOUS. */
+rcholqr_status rcholqr_factor_colmajor(rcholqr_plan plan, const void* X, int64_t m_local, int64_t row_offset,
+                                       int64_t ldx, void* Q, int64_t ldq, double* R, double* S, void* stream);
+
 /* RCholeskyQR2 (Alg. 3, alg:RCQR2): RCholeskyQR (Alg. 2) followed by one
  * CholeskyQR pass, A = Q1^T Q1 (all-reduced over the communicator), R' = chol(A), R = R' R1,
  * Q = Q1 R'^{-1} -- an orthonormal Q factor (to O(n u)) and the QR factor R of X.

@@ -35,7 +35,7 @@ SYMBOLS = ["rcholqr_create", "rcholqr_destroy", "rcholqr_factor", "rcholqr_facto
            "rcholqr_tri_solve", "rcholqr_theta_export", "rcholqr_comm_unique_id",
            "rcholqr_comm_create", "rcholqr_comm_destroy", "rcholqr_strerror", "rcholqr_version",
            "rcholqr_launches_per_factor", "rcholqr_set_timing", "rcholqr_last_timings", "rcholqr_factor2",
-           "rcholqr_factor_reduced", "rcholqr_factor_rr"]
+           "rcholqr_factor_reduced", "rcholqr_factor_rr", "rcholqr_factor_colmajor"]
 
 
 class _Desc(ctypes.Structure):
@@ -74,6 +74,7 @@ def load_library():
             "rcholqr_factor_host": ([V, V, I64, I64, I64, V, I64, V, V, V], I32),
             "rcholqr_factor2": ([V, V, I64, I64, I64, V, I64, V, V, I32, V], I32),
             "rcholqr_factor_reduced": ([V, V, I64, I64, I64, I32, V, V, V, V, V], I32),
+            "rcholqr_factor_colmajor": ([V, V, I64, I64, I64, V, I64, V, V, V], I32),
             "rcholqr_factor_rr": ([V, V, I64, I64, I64, ctypes.c_double, ctypes.c_double, I32, V, I64, V, V, V, V,
                                    ctypes.POINTER(I32), ctypes.POINTER(I32), V], I32),
             "rcholqr_sketch": ([V, V, I64, I64, I64, V, V], I32),
@@ -195,6 +196,23 @@ class RCholQR:
                 _ptr(S), _stream_ptr(stream))
         _check(st, "rcholqr_factor")
         return Q, R, S
+
+    def factor_colmajor(self, Xt, row_offset: int = 0, want_S: bool = False, Qt=None, R=None, S=None, stream=None):
+        """Alg. 2 on column-major X given as its transpose Xt (n, m) row-major CUDA tensor -- i.e. the
+        column-major buffer itself; returns (Qt (n, m), R, S) with Qt the column-major Q."""
+        torch = _torch()
+        if not (Xt.is_cuda and Xt.dtype == self.dtype and Xt.dim() == 2 and Xt.shape[0] == self.n and Xt.stride(1) == 1):
+            raise ValueError(f"Xt must be a CUDA {self.dtype} tensor of shape ({self.n}, m), stride(1) == 1")
+        m = Xt.shape[1]
+        ldx = max(Xt.stride(0), m, 1)
+        Qt = torch.empty((self.n, m), dtype=self.dtype, device=Xt.device) if Qt is None else Qt
+        R = torch.empty((self.n, self.n), dtype=torch.float64, device=Xt.device) if R is None else R
+        if want_S and S is None:
+            S = torch.empty((self.k, self.n), dtype=torch.float64, device=Xt.device)
+        st = self._lib.rcholqr_factor_colmajor(self._h, _ptr(Xt), m, row_offset, ldx, _ptr(Qt), max(Qt.stride(0), m, 1),
+                                               _ptr(R), _ptr(S), _stream_ptr(stream))
+        _check(st, "rcholqr_factor_colmajor")
+        return Qt, R, S
 
     def factor2(self, X, row_offset: int = 0, Q=None, R=None, Rprime=None, implicit: bool = False,
                 stream=None) -> Tuple:

@@ -681,6 +681,32 @@ rcholqr_status rcholqr_factor_rr(rcholqr_plan p, const void* X, int64_t m, int64
   return read_status(p, st);
 }
 
+rcholqr_status rcholqr_factor_colmajor(rcholqr_plan p, const void* X, int64_t m, int64_t ro, int64_t ldx, void* Q,
+                                       int64_t ldq, double* R, double* S, void* stream) {
+  if (!p || m < 0 || ro < 0 || ldx < std::max<int64_t>(m, 1) || ldq < std::max<int64_t>(m, 1) ||
+      (m > 0 && (!X || !Q)))
+    return RCHOLQR_E_INVALID;
+  const int n = p->d.n;
+  const size_t es = esize(p->d.dtype);
+  if (m > 0 && overlaps(X, span_bytes(n, ldx, (int)m, es), Q, span_bytes(n, ldq, (int)m, es))) return RCHOLQR_E_INVALID;
+  DeviceGuard dg(p->d.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t need = (size_t)std::max<int64_t>(m, 1) * n * es;   // row-major staging of X and Q
+  if (need > p->xq_bytes) {
+    cudaFree(p->xbuf); cudaFree(p->qbuf);
+    p->xbuf = p->qbuf = nullptr; p->xq_bytes = 0;
+    CU(cudaMalloc(&p->xbuf, need));
+    CU(cudaMalloc(&p->qbuf, need));
+    p->xq_bytes = need;
+  }
+  // X (n columns of length m, ld ldx) -> row-major m x n; the row-major path; Q back to column-major
+  CU(launch_transpose(X, n, m, ldx, p->xbuf, n, es, st));
+  rcholqr_status s = rcholqr_factor_async(p, p->xbuf, m, ro, n, p->qbuf, n, R, S, stream);
+  if (s != RCHOLQR_OK) return s;
+  CU(launch_transpose(p->qbuf, m, n, n, Q, ldq, es, st));
+  return rcholqr_query_status(p, stream);
+}
+
 rcholqr_status rcholqr_query_status(rcholqr_plan p, void* stream) {
   if (!p) return RCHOLQR_E_INVALID;
   DeviceGuard dg(p->d.device);

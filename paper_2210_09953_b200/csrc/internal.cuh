@@ -135,6 +135,9 @@ cudaError_t launch_rr_finalize(const double* Rf, int n, int r, const double* d, 
                                double* R11, cudaStream_t st);
 cudaError_t launch_gather_x(const void* X, int dtype, int64_t m, int64_t ldx, const int* perm, int r, void* Xr,
                             int sms, cudaStream_t st);
+// out (cols x rows, ld ldo) = in^T (rows x cols, ld ldi), element size es (reduced.cu)
+cudaError_t launch_transpose(const void* in, int64_t rows, int64_t cols, int64_t ldi, void* out, int64_t ldo,
+                             size_t es, cudaStream_t st);
 cudaError_t launch_trsm_resident(int tm, const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M,
                                  void* Q, int64_t ldq, const int* status, int sms, cudaStream_t st);
 

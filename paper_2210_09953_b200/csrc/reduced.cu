@@ -44,4 +44,42 @@ cudaError_t launch_rowsub(const double* Y, int64_t l, int n, const double* R, do
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------------
+// Column-major layout adapter (rcholqr_factor_colmajor): out(r, c) = in(c, r) through 32 x 33 shared
+// tiles -- coalesced reads of the source's rows and writes of the destination's rows.
+template <typename T>
+__global__ void transpose_kernel(const T* __restrict__ in, int64_t rows, int64_t cols, int64_t ldi, T* __restrict__ out,
+                                 int64_t ldo) {
+  __shared__ T tile[32][33];
+  const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;   // tile of `in` (rows x cols)
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t r = r0 + y, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[y][threadIdx.x] = in[r * ldi + c];
+  }
+  __syncthreads();
+  for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+    const int64_t c = c0 + y, r = r0 + threadIdx.x;                               // out is cols x rows
+    if (r < rows && c < cols) out[c * ldo + r] = tile[threadIdx.x][y];
+  }
+}
+
+cudaError_t launch_transpose(const void* in, int64_t rows, int64_t cols, int64_t ldi, void* out, int64_t ldo,
+                             size_t es, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  const dim3 block(32, 8), grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
+  if (grid.y > 65535u) {                                         // very tall: chunk the rows
+    const int64_t chunk = (int64_t)65535 * 32;
+    for (int64_t r = 0; r < rows; r += chunk) {
+      const int64_t rr = std::min(chunk, rows - r);
+      cudaError_t e = launch_transpose((const char*)in + (size_t)r * ldi * es, rr, cols, ldi,
+                                       (char*)out + (size_t)r * es, ldo, es, st);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
+  if (es == 8) transpose_kernel<double><<<grid, block, 0, st>>>((const double*)in, rows, cols, ldi, (double*)out, ldo);
+  else transpose_kernel<float><<<grid, block, 0, st>>>((const float*)in, rows, cols, ldi, (float*)out, ldo);
+  return cudaGetLastError();
+}
+
 }  // namespace rcq
