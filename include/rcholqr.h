@@ -168,7 +168,7 @@ rcholqr_status rcholqr_factor_reduced(rcholqr_plan plan, const void* X, int64_t 
  *   perm  [device] n int32: Pi as perm[j] = original column in position j.
  *   D     [device] n fp64 column norms or NULL;  S [device] k x n fp64 or NULL (columns 0..r-1 = S).
  *   rank_out, swaps_out [host] int32: r and the number of Gu-Eisenstat swaps (swaps_out may be NULL).
- * Status: E_INVALID (arguments, f <= 1, tau < 0), E_NONFINITE, E_SINGULAR if r = 0 (X = 0).
+ * Status: E_INVALID (arguments, f <= 1, tau < 0), E_SHAPE (n > 1024), E_NONFINITE, E_SINGULAR if r = 0 (X = 0).
  * Memory: the plan allocates an O(k n) workspace on first use and an m_local x r gather buffer.
  * SYNCHRONOUS (the rank and each swap decision are read on the host).  With a communicator every
  * rank must call this (one all-reduce); Pi, r and R are identical on every rank. */

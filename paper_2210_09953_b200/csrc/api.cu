@@ -577,6 +577,7 @@ rcholqr_status rcholqr_factor_rr(rcholqr_plan p, const void* X, int64_t m, int64
   if (!R || !perm || !rank_out || !(f > 1.0) || !(tau >= 0.0) || !std::isfinite(tau) || rank_fixed < 0)
     return RCHOLQR_E_INVALID;
   const int k = p->d.k, n = p->d.n;
+  if (n > 1024) return RCHOLQR_E_SHAPE;                      // the pivoting kernel's norm arrays
   const size_t kn = (size_t)k * n, nn = (size_t)n * n, es = esize(p->d.dtype);
   DeviceGuard dg(p->d.device);
   cudaStream_t st = (cudaStream_t)stream;

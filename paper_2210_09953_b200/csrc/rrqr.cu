@@ -103,12 +103,16 @@ __device__ double rr_block_sum(double v, double* red) {
 }
 
 // Column pivoting on the k x n row-major Pn (A: k x n column-major workspace, in shared memory when
-// `stage` -- the loops below are L2-latency bound otherwise); writes perm only.
+// `stage` -- the loops below are L2-latency bound otherwise); writes perm only.  The trailing column
+// norms are DOWNDATED after each step (nrm2_l -= A(j, l)^2, as LAPACK's dgeqp3 / dlaqp2) and recomputed
+// exactly when cancellation makes the downdate unreliable (remaining < 1e-4 of the last exact value) --
+// the pivots equal the oracle's recomputed-norm choices except at rounding-level ties.
 __global__ void __launch_bounds__(1024) qrcp_kernel(const double* __restrict__ Pn, int k, int n, double* __restrict__ Ag,
                                                     int* __restrict__ perm, int stage) {
   extern __shared__ double qp_s[];
   __shared__ double sv[32], s_bv;
   __shared__ int si[32], s_bi;
+  __shared__ double nrm[1024], nref[1024];          // current (downdated) and last exact squared norms (n <= 1024)
   double* A = stage ? qp_s : Ag;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   for (int64_t t = tid; t < (int64_t)k * n; t += blockDim.x) {
@@ -117,29 +121,25 @@ __global__ void __launch_bounds__(1024) qrcp_kernel(const double* __restrict__ P
   }
   for (int j = tid; j < n; j += blockDim.x) perm[j] = j;
   __syncthreads();
+  auto exact_norm = [&](int l, int j0) {            // warp-wide sum of squares of column l, rows j0..k-1
+    const double* c = A + (size_t)l * k;
+    double ss = 0.0;
+    for (int i = j0 + lane; i < k; i += 32) ss = fma(c[i], c[i], ss);
+    return rr_warp_sum(ss);
+  };
+  for (int l = warp; l < n; l += nw) {
+    const double v = exact_norm(l, 0);
+    if (lane == 0) { nrm[l] = v; nref[l] = v; }
+  }
+  __syncthreads();
   for (int j = 0; j < n; ++j) {
-    // trailing column norms (rows j..k-1): warp w owns columns j + w + q nw, four at a time for ILP;
-    // block argmax (first index on ties)
+    // argmax of the trailing norms (first index on ties)
     double best = -1.0;
     int bidx = n;
-    for (int l0 = j + warp; l0 < n; l0 += 4 * nw) {
-      double ss[4] = {0.0, 0.0, 0.0, 0.0};
-      for (int i = j + lane; i < k; i += 32)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int l = l0 + q * nw;
-          if (l < n) { const double v = A[(size_t)l * k + i]; ss[q] = fma(v, v, ss[q]); }
-        }
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const double t = rr_warp_sum(ss[q]);
-        const int l = l0 + q * nw;
-        if (l < n && t > best) { best = t; bidx = l; }   // l ascending within the warp
-      }
-    }
+    for (int l = j + tid; l < n; l += blockDim.x)
+      if (nrm[l] > best) { best = nrm[l]; bidx = l; }
     rr_block_argmax(best, bidx, sv, si, &s_bv, &s_bi);
     const int p = s_bi;
-    const double alpha = sqrt(s_bv);
     if (p >= n) break;                         // no comparable norm (non-finite P: the status word reports it)
     if (p != j) {
       for (int i = tid; i < k; i += blockDim.x) {
@@ -147,9 +147,20 @@ __global__ void __launch_bounds__(1024) qrcp_kernel(const double* __restrict__ P
         A[(size_t)j * k + i] = A[(size_t)p * k + i];
         A[(size_t)p * k + i] = t;
       }
-      if (tid == 0) { const int t = perm[j]; perm[j] = perm[p]; perm[p] = t; }
+      if (tid == 0) {
+        const int t = perm[j]; perm[j] = perm[p]; perm[p] = t;
+        const double a = nrm[j]; nrm[j] = nrm[p]; nrm[p] = a;
+        const double b = nref[j]; nref[j] = nref[p]; nref[p] = b;
+      }
     }
     __syncthreads();
+    // the pivot column's norm exactly (its reflector needs it)
+    if (warp == 0) {
+      const double v = exact_norm(j, j);
+      if (lane == 0) s_bv = v;
+    }
+    __syncthreads();
+    const double alpha = sqrt(s_bv);
     if (!(alpha > 0.0)) break;                 // the trailing columns are all zero
     const double* a = A + (size_t)j * k;
     const double aj = a[j];
@@ -170,13 +181,34 @@ __global__ void __launch_bounds__(1024) qrcp_kernel(const double* __restrict__ P
 #pragma unroll
       for (int q = 0; q < 4; ++q) t[q] = (rr_warp_sum(dot[q]) + v0 * cj[q]) * scale;
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (lane == 0 && l0 + q * nw < n) A[(size_t)(l0 + q * nw) * k + j] = cj[q] - t[q] * v0;
+      for (int q = 0; q < 4; ++q) {
+        const int l = l0 + q * nw;
+        if (l < n) {
+          const double rjl = cj[q] - t[q] * v0;           // the new A(j, l) = R(j, l)
+          if (lane == 0) {
+            A[(size_t)l * k + j] = rjl;
+            const double left = nrm[l] - rjl * rjl;       // downdate
+            nrm[l] = left;
+          }
+        }
+      }
       for (int i = j + 1 + lane; i < k; i += 32) {
         const double ai = a[i];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
           if (l0 + q * nw < n) A[(size_t)(l0 + q * nw) * k + i] -= t[q] * ai;
+      }
+      __syncwarp();                                       // lane 0's downdates and every lane's axpys visible
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {                       // cancellation: recompute rows j+1.. exactly
+        const int l = l0 + q * nw;
+        if (l < n) {
+          const bool redo = !(nrm[l] > 1e-4 * nref[l]);
+          if (redo) {
+            const double v = exact_norm(l, j + 1);
+            if (lane == 0) { nrm[l] = v; nref[l] = v; }
+          }
+        }
       }
     }
     __syncthreads();
