@@ -406,6 +406,23 @@ def factor_rr(X: np.ndarray, k: int, tau: float, f: float = 1.5, rank_fixed: int
             "S": None if S is None else S[:, :r].copy(), "swaps": swaps.value}
 
 
+def factor_rr2(X: np.ndarray, k: int, tau: float, f: float = 1.5, rank_fixed: int = 0, sketch: int = GAUSSIAN,
+               zeta: int = 8, seed: int = 0, row_offset: int = 0) -> dict:
+    """RRRCholeskyQR2 (RRRCholeskyQR "augmented with the classical CholeskyQR in exactly the
+    same way as done in RCholeskyQR2"): Alg. 7 gives (Q1, R1, perm, r); then A = Q1^T Q1, R' = chol(A),
+    R = R' R1 (r x n, upper trapezoidal), Q = Q1 R'^{-1}.  Returns dict(Q, R, Rp, Q1, perm, rank, swaps)."""
+    rr = factor_rr(X, k, tau, f=f, rank_fixed=rank_fixed, sketch=sketch, zeta=zeta, seed=seed,
+                   row_offset=row_offset)
+    Q1 = np.ascontiguousarray(rr["Q"])
+    A = gram(Q1)
+    Rp, st = cholesky(A)
+    if st != OK:
+        raise OracleError(st, "factor_rr2 cholesky")
+    R = np.triu(Rp @ rr["R"])          # (r x r upper) (r x n upper trapezoidal); exact zeros kept below
+    Q = forward_subst(Q1, Rp)
+    return {"Q": Q, "R": R, "Rp": Rp, "Q1": Q1, "perm": rr["perm"], "rank": rr["rank"], "swaps": rr["swaps"]}
+
+
 # ---------------------------------------------------------------- metrics (PAPER.md:773, 797)
 def orth_defect(S: np.ndarray) -> float:
     """||I - S^T S||_2 (fp64)."""

@@ -142,3 +142,21 @@ def test_metamorphic_power_of_two_scalings():
     c = oracle.factor_rr(X * E, 20, tau=1e-9)               # P D^{-1} is bitwise unchanged
     assert np.array_equal(a["perm"], c["perm"]) and np.array_equal(a["Q"], c["Q"])
     assert np.array_equal(a["R"] * E[a["perm"]][None, :], c["R"])
+
+
+def test_rr2_orthonormal_and_consistent():
+    # RRRCholeskyQR2: same rank and pivots as Alg. 7, Q orthonormal to O(r u) even for a
+    # rank-deficient X, X[:, perm] = Q R to the tau bound, R = R' R1 with R' = chol(Q1^T Q1)
+    m, n, rank, tau = 30_000, 14, 9, 1e-9
+    X = synth.make_X_lowrank(m, n, rank, 2.0, 1e-13)
+    out = oracle.factor_rr2(X, 28, tau)
+    rr = oracle.factor_rr(X, 28, tau)
+    assert out["rank"] == rr["rank"] == rank and np.array_equal(out["perm"], rr["perm"])
+    Q, R, p = out["Q"], out["R"], out["perm"]
+    assert np.linalg.norm(Q.T @ Q - np.eye(rank), 2) <= 10 * rank * U64
+    assert np.linalg.cond(out["Rp"]) <= 8.0
+    D = rr["D"][p]
+    E = (X[:, p] - Q @ R) / D[None, :]
+    assert np.linalg.norm(E) <= np.sqrt(2) * (U64 * n * 10 + 1.02 * np.sqrt(1.5) * tau) * np.sqrt(n)
+    assert np.allclose(R, out["Rp"] @ rr["R"], rtol=0, atol=1e-13 * np.abs(R).max())
+    assert np.all(np.tril(R[:, :rank], -1) == 0) and np.all(np.diag(R) > 0)
