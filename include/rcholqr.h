@@ -177,6 +177,18 @@ rcholqr_status rcholqr_factor_rr(rcholqr_plan plan, const void* X, int64_t m_loc
                                  double* R, int32_t* perm, double* D, double* S, int32_t* rank_out,
                                  int32_t* swaps_out, void* stream);
 
+/* RRRCholeskyQR2 (RRRCholeskyQR "augmented with the classical CholeskyQR in exactly the same
+ * way as done in RCholeskyQR2"): rcholqr_factor_rr gives (Q1, R1, Pi, r); then A = Q1^T Q1 (r x r,
+ * all-reduced), R' = chol(A), R = R' R1, Q = Q1 R'^{-1} -- an ORTHONORMAL m x r Q with X Pi ~= Q R.
+ *   Arguments as rcholqr_factor_rr (tau, f, rank_fixed, perm, D, rank_out, swaps_out); Rprime [device]
+ *   r x r (ld r, n x n buffer) or NULL: R'.  R: rows 0..r-1 = R' R1 (permuted column order), the rest 0.
+ * Status: as rcholqr_factor_rr; E_SINGULAR also if Q1^T Q1 is not numerically positive definite.
+ * Memory: a plan-owned m_local x n buffer for Q1.  SYNCHRONOUS; collective with a communicator. */
+rcholqr_status rcholqr_factor_rr2(rcholqr_plan plan, const void* X, int64_t m_local, int64_t row_offset,
+                                  int64_t ldx, double tau, double f, int32_t rank_fixed, void* Q, int64_t ldq,
+                                  double* R, double* Rprime, int32_t* perm, double* D, int32_t* rank_out,
+                                  int32_t* swaps_out, void* stream);
+
 /* ---- step-level entry points (same kernels as rcholqr_factor; used by the parity tests) ---- */
 
 /* Step 1 (+ the all-reduce when the plan has a communicator): P = Theta X, k x n fp64 row-major

@@ -35,7 +35,8 @@ SYMBOLS = ["rcholqr_create", "rcholqr_destroy", "rcholqr_factor", "rcholqr_facto
            "rcholqr_tri_solve", "rcholqr_theta_export", "rcholqr_comm_unique_id",
            "rcholqr_comm_create", "rcholqr_comm_destroy", "rcholqr_strerror", "rcholqr_version",
            "rcholqr_launches_per_factor", "rcholqr_set_timing", "rcholqr_last_timings", "rcholqr_factor2",
-           "rcholqr_factor_reduced", "rcholqr_factor_rr", "rcholqr_factor_colmajor"]
+           "rcholqr_factor_reduced", "rcholqr_factor_rr", "rcholqr_factor_colmajor",
+           "rcholqr_factor_rr2"]
 
 
 class _Desc(ctypes.Structure):
@@ -75,6 +76,8 @@ def load_library():
             "rcholqr_factor2": ([V, V, I64, I64, I64, V, I64, V, V, I32, V], I32),
             "rcholqr_factor_reduced": ([V, V, I64, I64, I64, I32, V, V, V, V, V], I32),
             "rcholqr_factor_colmajor": ([V, V, I64, I64, I64, V, I64, V, V, V], I32),
+            "rcholqr_factor_rr2": ([V, V, I64, I64, I64, ctypes.c_double, ctypes.c_double, I32, V, I64, V, V, V, V,
+                                    ctypes.POINTER(I32), ctypes.POINTER(I32), V], I32),
             "rcholqr_factor_rr": ([V, V, I64, I64, I64, ctypes.c_double, ctypes.c_double, I32, V, I64, V, V, V, V,
                                    ctypes.POINTER(I32), ctypes.POINTER(I32), V], I32),
             "rcholqr_sketch": ([V, V, I64, I64, I64, V, V], I32),
@@ -265,6 +268,26 @@ class RCholQR:
         r = rank.value
         return {"Q": Q[:, :r], "R": R[:r], "perm": perm, "rank": r, "D": D,
                 "S": None if S is None else S[:, :r], "swaps": swaps.value}
+
+    def factor_rr2(self, X, tau: float, f: float = 1.5, rank_fixed: int = 0, row_offset: int = 0, Q=None,
+                   stream=None) -> dict:
+        """RRRCholeskyQR2: dict(Q (m x r, orthonormal), R (r x n), Rp (r x r), perm, rank, D, swaps)."""
+        torch = _torch()
+        m, ldx = self._check_x(X)
+        Q = torch.empty((m, self.n), dtype=self.dtype, device=X.device) if Q is None else Q
+        f64 = dict(dtype=torch.float64, device=X.device)
+        R = torch.empty((self.n, self.n), **f64)
+        Rp = torch.empty((self.n * self.n,), **f64)
+        perm = torch.empty(self.n, dtype=torch.int32, device=X.device)
+        D = torch.empty(self.n, **f64)
+        rank, swaps = ctypes.c_int32(0), ctypes.c_int32(0)
+        st = self._lib.rcholqr_factor_rr2(self._h, _ptr(X), m, row_offset, ldx, float(tau), float(f), int(rank_fixed),
+                                          _ptr(Q), Q.stride(0) if m > 1 else self.n, _ptr(R), _ptr(Rp), _ptr(perm),
+                                          _ptr(D), ctypes.byref(rank), ctypes.byref(swaps), _stream_ptr(stream))
+        _check(st, "rcholqr_factor_rr2")
+        r = rank.value
+        return {"Q": Q[:, :r], "R": R[:r], "Rp": Rp[: r * r].view(r, r), "perm": perm, "rank": r, "D": D,
+                "swaps": swaps.value}
 
     def query_status(self, stream=None) -> int:
         return int(self._lib.rcholqr_query_status(self._h, _stream_ptr(stream)))

@@ -453,6 +453,25 @@ rcholqr_status rcholqr_factor_async(rcholqr_plan p, const void* X, int64_t m, in
   return RCHOLQR_OK;
 }
 
+// Gram / Cholesky workspace of Alg. 3 and RRRCholeskyQR2 (n x n each; the partials hold the most
+// splits any column count <= n uses), allocated on first use.
+static bool ensure_gram(rcholqr_plan p) {
+  if (p->gA) return true;
+  const int n = p->d.n;
+  const size_t nn = (size_t)n * n;
+  p->gram_splits = gram_splits(n, p->sms);
+  size_t part_elems = nn * (size_t)p->gram_splits;
+  for (int r = 1; r <= n; r = r < 128 ? 128 : n + 1)     // n <= 128 uses the most splits (4 per SM)
+    part_elems = std::max(part_elems, (size_t)r * r * (size_t)gram_splits(std::min(r, n), p->sms));
+  bool ok = cudaMalloc(&p->gpart, sizeof(double) * part_elems) == cudaSuccess &&
+            cudaMalloc(&p->gA, sizeof(double) * nn) == cudaSuccess &&
+            cudaMalloc(&p->gW, sizeof(double) * nn) == cudaSuccess &&
+            cudaMalloc(&p->gRp, sizeof(double) * nn) == cudaSuccess &&
+            cudaMalloc(&p->gR1, sizeof(double) * nn) == cudaSuccess;
+  if (!ok) { cudaGetLastError(); return false; }
+  return true;
+}
+
 rcholqr_status rcholqr_factor2(rcholqr_plan p, const void* X, int64_t m, int64_t ro, int64_t ldx, void* Q,
                                int64_t ldq, double* R, double* Rprime, int32_t implicit, void* stream) {
   rcholqr_status a = check_factor_args(p, X, m, ro, ldx, Q, ldq);
@@ -462,15 +481,7 @@ rcholqr_status rcholqr_factor2(rcholqr_plan p, const void* X, int64_t m, int64_t
   cudaStream_t st = (cudaStream_t)stream;
   const int n = p->d.n;
   const size_t nn = (size_t)n * n, es = esize(p->d.dtype);
-  if (!p->gA) {   // Gram workspace, allocated on first use
-    p->gram_splits = gram_splits(n, p->sms);
-    bool ok = cudaMalloc(&p->gpart, sizeof(double) * nn * p->gram_splits) == cudaSuccess &&
-              cudaMalloc(&p->gA, sizeof(double) * nn) == cudaSuccess &&
-              cudaMalloc(&p->gW, sizeof(double) * nn) == cudaSuccess &&
-              cudaMalloc(&p->gRp, sizeof(double) * nn) == cudaSuccess &&
-              cudaMalloc(&p->gR1, sizeof(double) * nn) == cudaSuccess;
-    if (!ok) { cudaGetLastError(); return RCHOLQR_E_NOMEM; }
-  }
+  if (!ensure_gram(p)) return RCHOLQR_E_NOMEM;
   // Q1: the caller's Q (implicit form) or a plan-owned buffer (explicit form; Q must not alias it)
   void* Q1 = Q;
   int64_t ldq1 = ldq;
@@ -680,6 +691,56 @@ rcholqr_status rcholqr_factor_rr(rcholqr_plan p, const void* X, int64_t m, int64
   if (t) cudaEventRecord(p->ev[6], st);
   p->timing = t;
   return read_status(p, st);
+}
+
+rcholqr_status rcholqr_factor_rr2(rcholqr_plan p, const void* X, int64_t m, int64_t ro, int64_t ldx, double tau,
+                                  double f, int32_t rank_fixed, void* Q, int64_t ldq, double* R, double* Rprime,
+                                  int32_t* perm, double* D, int32_t* rank_out, int32_t* swaps_out, void* stream) {
+  rcholqr_status a = check_factor_args(p, X, m, ro, ldx, Q, ldq);
+  if (a != RCHOLQR_OK) return a;
+  if (!R || !perm || !rank_out) return RCHOLQR_E_INVALID;
+  const int n = p->d.n;
+  const size_t es = esize(p->d.dtype);
+  DeviceGuard dg(p->d.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!ensure_gram(p)) return RCHOLQR_E_NOMEM;
+  if (m > 0) {                                                 // Q1: plan-owned m x n (first r columns used)
+    const size_t need = (size_t)m * n * es;
+    if (need > p->q1_bytes) {
+      cudaFree(p->q1buf);
+      p->q1buf = nullptr; p->q1_bytes = 0;
+      CU(cudaMalloc(&p->q1buf, need));
+      p->q1_bytes = need;
+    }
+  }
+  // 1. Alg. 7: Q1 (m x r), R1 (r x n), perm, r
+  int32_t r = 0;
+  rcholqr_status s = rcholqr_factor_rr(p, X, m, ro, ldx, tau, f, rank_fixed, m > 0 ? p->q1buf : Q, n, p->gR1, perm, D,
+                                       nullptr, &r, swaps_out, stream);
+  *rank_out = r;
+  if (s != RCHOLQR_OK) return s;
+  // 2. A = Q1^T Q1 (r x r, + all-reduce); 3. R' = chol(A), R = R' R1; 4. Q = Q1 R'^{-1}
+  CU(cudaMemsetAsync(p->status_d, 0, sizeof(int), st));
+  if (m > 0) CU(launch_gram(p->q1buf, p->d.dtype, m, r, n, gram_splits(r, p->sms), p->gpart, p->gA, p->status_d, st));
+  else CU(cudaMemsetAsync(p->gA, 0, sizeof(double) * (size_t)r * r, st));
+  if (p->d.nccl_comm) {
+    if (!nccl_load()) return RCHOLQR_E_NCCL;
+    if (g_nccl.AllReduce(p->gA, p->gA, (size_t)r * r, ncclFloat64, ncclSum, (ncclComm_t)p->d.nccl_comm, st) !=
+        ncclSuccess)
+      return RCHOLQR_E_NCCL;
+  }
+  double* Rp = Rprime ? Rprime : p->gRp;
+  CU(launch_cholesky(p->gA, r, p->gW, Rp, p->status_d, st));
+  CU(launch_trmm_trap(Rp, r, p->gR1, n, R, p->status_d, st));
+  if (m > 0) {
+    s = solve(p, p->q1buf, m, n, Rp, Q, ldq, st, false, r);
+    if (s != RCHOLQR_OK) return s;
+  }
+  const bool t = p->timing;
+  p->timing = false;
+  rcholqr_status rs = read_status(p, st);
+  p->timing = t;
+  return rs;
 }
 
 rcholqr_status rcholqr_factor_colmajor(rcholqr_plan p, const void* X, int64_t m, int64_t ro, int64_t ldx, void* Q,

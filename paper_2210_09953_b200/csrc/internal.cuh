@@ -119,6 +119,8 @@ cudaError_t launch_gram(const void* Q, int dtype, int64_t m, int n, int64_t ldq,
 cudaError_t launch_cholesky(const double* A, int n, double* W, double* Rp, int* status, cudaStream_t st);
 cudaError_t launch_trmm_upper(const double* U, const double* V, int n, double* out, const int* status,
                               cudaStream_t st);
+cudaError_t launch_trmm_trap(const double* U, int r, const double* V, int n, double* out, const int* status,
+                             cudaStream_t st);
 // reduced RCholeskyQR (reduced.cu): Z = Y R^{-1} for the small l x n extract Y, row-wise substitution
 cudaError_t launch_rowsub(const double* Y, int64_t l, int n, const double* R, double* Z, const int* status,
                           cudaStream_t st);

@@ -277,6 +277,27 @@ cudaError_t launch_cholesky(const double* A, int n, double* W, double* Rp, int* 
   return cudaGetLastError();
 }
 
+// out (n x n, rows >= r zero) = U V for U r x r upper (ld r) and V r x n upper trapezoidal (ld n):
+// RRRCholeskyQR2's R = R' R1.
+__global__ void trmm_trap_kernel(const double* __restrict__ U, int r, const double* __restrict__ V, int n,
+                                 double* __restrict__ out, const int* status) {
+  if (*status) return;
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c >= (int64_t)n * n) return;
+  const int i = (int)(c / n), j = (int)(c % n);
+  double s = 0.0;
+  if (i < r && j >= i)
+    for (int l = i; l <= min(j, r - 1); ++l) s += U[(size_t)i * r + l] * V[(size_t)l * n + j];
+  out[c] = s;
+}
+
+cudaError_t launch_trmm_trap(const double* U, int r, const double* V, int n, double* out, const int* status,
+                             cudaStream_t st) {
+  const int64_t nn = (int64_t)n * n;
+  trmm_trap_kernel<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(U, r, V, n, out, status);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_trmm_upper(const double* U, const double* V, int n, double* out, const int* status,
                               cudaStream_t st) {
   const int64_t nn = (int64_t)n * n;

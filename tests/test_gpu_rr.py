@@ -140,3 +140,27 @@ def test_rr_nccl_single_rank(cuda):
         pb.close()
     finally:
         rcq.comm_destroy(comm)
+
+
+@pytest.mark.parametrize("m,n,k,rank,dt,sk,tau", [
+    (100_000, 48, 96, 30, "f64", "gaussian", 1e-9),
+    (262_144, 64, 128, 40, "f32", "sparse", 1e-5),
+    (40_000, 256, 512, 180, "f64", "gaussian", 1e-9),
+])
+def test_factor_rr2_parity(cuda, m, n, k, rank, dt, sk, tau):
+    # RRRCholeskyQR2: Alg. 7's rank and pivots, then an orthonormal Q
+    X = synth.make_X_lowrank(m, n, rank, 2.0, 1e-13, dt)
+    so = oracle.GAUSSIAN if sk == "gaussian" else oracle.SPARSE_SIGN
+    ref = oracle.factor_rr2(X, k, tau, sketch=so, zeta=8)
+    plan = rcq.RCholQR(n=n, k=k, dtype=torch.float64 if dt == "f64" else torch.float32, sketch=sk, nnz_per_col=8)
+    g = plan.factor_rr2(_t(X), tau)
+    r = g["rank"]
+    perm = _np(g["perm"]).astype(np.int64)
+    assert r == ref["rank"] == rank and np.array_equal(perm[:r], ref["perm"][:r])
+    Rg = _np(g["R"])
+    assert _rel(_by_original_column(Rg, perm, n), _by_original_column(ref["R"], ref["perm"], n)) <= \
+        (1e-10 if dt == "f64" else 1e-4)
+    Q = _np(g["Q"]).astype(np.float64)
+    assert np.linalg.norm(Q.T @ Q - np.eye(r), 2) <= (1e-12 if dt == "f64" else 1e-5)
+    assert _rel(Q, ref["Q"]) <= (1e-10 if dt == "f64" else 1e-5)
+    assert np.linalg.cond(_np(g["Rp"])) <= 8.0
