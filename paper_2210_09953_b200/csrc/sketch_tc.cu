@@ -364,16 +364,21 @@ sketch_sparse_tc_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx,
             mine[q] = wm ^ ((__popcll(sr & B) & 1) ? 0xFFFFFFFFu : 0u) ^ dmask;
           }
         } else {
+          // 32 x 32 bit-matrix transpose per word (row = lane's X row, column = Theta row 32 q + b): a
+          // butterfly of 5 shuffle levels; at level j, lanes with bit j clear keep their bit positions
+          // with bit j clear and take the partner's into the others, and vice versa.
           const uint32_t wd[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
-            uint32_t keep = 0u;
+            uint32_t x = wd[q];
 #pragma unroll
-            for (int b = 0; b < 32; ++b) {
-              const uint32_t msk = __ballot_sync(0xffffffffu, (wd[q] >> b) & 1u);
-              keep = lane == b ? msk : keep;
+            for (int j = 16; j >= 1; j >>= 1) {
+              const uint32_t m = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
+                                 : j == 2 ? 0x33333333u : 0x55555555u;   // bit positions with bit j clear
+              const uint32_t y = __shfl_xor_sync(0xffffffffu, x, j);
+              x = (lane & j) ? ((x & ~m) | ((y & ~m) >> j)) : ((x & m) | ((y & m) << j));
             }
-            mine[q] = keep;
+            mine[q] = x;                          // bit L = sign bit of X row L for Theta row 32 q + lane
           }
         }
         if (!(dbg & 4)) {
