@@ -117,6 +117,8 @@ def _cpu_sample_rate(X_dev, cfg, target_s: float, algo: str = "rcholqr", l: int 
         run = lambda A: oracle.factor2(A, cfg["k"], sketch=so, zeta=cfg["nnz"])  # noqa: E731
     elif algo == "rcholqr_rr":
         run = lambda A: oracle.factor_rr(A, cfg["k"], tau, sketch=so, zeta=cfg["nnz"])  # noqa: E731
+    elif algo == "rcholqr_rr2":
+        run = lambda A: oracle.factor_rr2(A, cfg["k"], tau, sketch=so, zeta=cfg["nnz"])  # noqa: E731
     elif algo == "rcholqr_reduced":
         run = lambda A: oracle.factor_reduced(A, cfg["k"], l, sketch=so, zeta=cfg["nnz"], want_S=False)  # noqa: E731
     else:
@@ -222,6 +224,8 @@ def run(args):
     def step():
         if args.algo == "rcholqr_rr":   # Alg. 7: synchronous (rank and swap decisions on the host)
             rr_last.update(plan.factor_rr(X, tau_rr, row_offset=ro, Q=Q, R=R, stream=stream))
+        elif args.algo == "rcholqr_rr2":   # RRRCholeskyQR2: Alg. 7 + one CholeskyQR pass
+            rr_last.update(plan.factor_rr2(X, tau_rr, row_offset=ro, Q=Q, stream=stream))
         elif args.algo == "rcholqr2":   # Alg. 3: synchronous (status read inside the call)
             plan.factor2(X, row_offset=ro, Q=Q, R=R, Rprime=Rp, stream=stream)
         elif args.algo == "rcholqr_reduced":   # Alg. 5: synchronous
@@ -299,7 +303,7 @@ def run(args):
     hbm = peaks.get("hbm_gbs", 6545.0)
     roofs = {}
     reduced = args.algo == "rcholqr_reduced"
-    rr = args.algo == "rcholqr_rr"
+    rr = args.algo in ("rcholqr_rr", "rcholqr_rr2")
     r_rr = rr_last.get("rank", n)
     k_sk = k + l_red if reduced else k      # Alg. 5 with a Gaussian Theta: one (k + l)-row sketch
     if cfg["sketch"] == "gaussian":
@@ -468,24 +472,28 @@ def run(args):
         line["gpu_launches"] = (plan.launches_per_factor(m_local) - 1) * args.steps
         line["e2e"] = None
     if rr:
-        # Alg. 7 passes: sketch + column norms (2 reads of X), gather (r/n read + write), solve (r/n read + write)
-        t_hbm7 = (2.0 + 4.0 * r_rr / n) * m_local * n * s_x / (hbm * 1e9)
-        t_flop7 = float(m_local) * r_rr * r_rr / (DMMA_PEAK_TFLOPS * 1e12)
-        line["metric"] = "RRRCholQR factor throughput (GB/s of X)"
-        line["config"]["algo"] = f"rcholqr_rr (Alg. 7, tau = {tau_rr:g}, f = 1.5)"
+        # Alg. 7 passes: sketch + column norms (2 reads of X), gather (r/n read + write), solve (r/n read + write);
+        # RRRCholeskyQR2 adds the Gram (r/n read) and a second solve (r/n read + write) and 2 m r^2 flops
+        two = args.algo == "rcholqr_rr2"
+        t_hbm7 = (2.0 + (7.0 if two else 4.0) * r_rr / n) * m_local * n * s_x / (hbm * 1e9)
+        t_flop7 = (3.0 if two else 1.0) * float(m_local) * r_rr * r_rr / (DMMA_PEAK_TFLOPS * 1e12)
+        line["metric"] = ("RRRCholQR2" if two else "RRRCholQR") + " factor throughput (GB/s of X)"
+        line["config"]["algo"] = f"{args.algo} ({'PAPER.md:397' if two else 'Alg. 7'}, tau = {tau_rr:g}, f = 1.5)"
         line["config"]["rank"] = r_rr
         line["config"]["swaps"] = rr_last.get("swaps")
         line["northstar_roofline"] = {"t_hbm_ms": t_hbm7 * 1e3, "t_fp64_ms": t_flop7 * 1e3,
                                       "roofline_ms": max(t_hbm7, t_flop7) * 1e3,
                                       "frac": max(t_hbm7, t_flop7) * 1e3 / ms,
-                                      "note": "Alg. 7 accounting: (2 + 4 r/n) passes over m x n, m r^2 fp64 flops"}
+                                      "note": "Alg. 7 accounting: (2 + 4 r/n) passes over m x n, m r^2 fp64 flops"
+                                              + ("; RRRCholeskyQR2: + 3 r/n passes, + 2 m r^2 flops" if two else "")}
         # sketch launches + colsq (2) + normalize + qrcp + gather + QR + rank + strong + finalize + gather_x
         # + check_diag + solve
         line["gpu_launches"] = (plan.launches_per_factor(m_local) + 10) * args.steps
         line["e2e"] = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         rows, dt_s, cores = _cpu_sample_rate(X, cfg, args.cpu_seconds, args.algo, l_red, tau_rr)
-        fn = {"rcholqr2": "factor2", "rcholqr_reduced": "factor_reduced", "rcholqr_rr": "factor_rr"}.get(args.algo,
+        fn = {"rcholqr2": "factor2", "rcholqr_reduced": "factor_reduced", "rcholqr_rr": "factor_rr",
+              "rcholqr_rr2": "factor_rr2"}.get(args.algo,
                                                                                                        "factor")
         line["cpu_baseline"] = {"value": rows * n * s_x / dt_s / 1e9, "unit": "GB/s", "cores": cores,
                                 "kind": "oracle", "seconds": dt_s,
@@ -510,7 +518,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
-    ap.add_argument("--algo", default="rcholqr", choices=["rcholqr", "rcholqr2", "rcholqr_reduced", "rcholqr_rr"],
+    ap.add_argument("--algo", default="rcholqr",
+                    choices=["rcholqr", "rcholqr2", "rcholqr_reduced", "rcholqr_rr", "rcholqr_rr2"],
                     help="Alg. 2 (default, the north star), Alg. 3 RCholeskyQR2 (orthonormal Q) or Alg. 5 "
                          "reduced RCholeskyQR (Z = L Q)")
     ap.add_argument("--l", type=int, default=0, help="Alg. 5: rows of the extractor L (default k)")
