@@ -428,6 +428,11 @@ sketch_gauss_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int 
 // DX x 4 KB block per (split, 32-row stage, 128-column tile)), so the sketch kernel receives each
 // stage with a single bulk copy and all of its producer warps generate Theta.  Column scales are
 // per (split, column), from the split's first 32 rows (the same heuristic and overflow guard).
+// Two differences from the in-kernel variant above: (1) only the digit-product levels L < LK are
+// computed (GpLevels: X digit b multiplies a prefix of the Theta digit stack; the dropped levels are
+// below the fp64 rounding of P, A17), so TMEM holds LK * KT columns; (2) fp64 tiles take
+// KT = 48 Theta rows (96 Theta tasks per stage fill a 3-warp group), an N = 288 prefix being issued as
+// two MMAs (N = 256 + 32).  RCHOLQR_GTP_DEBUG=1 (ablation) copies 16 B per stage instead of the digits.
 constexpr int GP_TWARPS = 12;                     // Theta warps 2..13: four groups of three
 constexpr int GP_THREADS = 32 * (2 + GP_TWARPS);
 constexpr int GP_GROUPS = 4;
