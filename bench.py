@@ -382,8 +382,16 @@ def run(args):
             tr = json.load(f).get(args.config) or {}
     except OSError:
         tr = {}
+    try:   # issue / SM / tensor-pipe utilisation of the same capture (the kernels' native bound, e.g. the
+        #   Gaussian sketch's instruction issue behind its fp64-equivalent tensor view)
+        with open(os.path.join(ROOT, "profiles", "issue.json")) as f:
+            iss = json.load(f).get(args.config) or {}
+    except OSError:
+        iss = {}
     for r_ in roofs.values():
         names = [x.strip() for x in r_["kernel"].split("+")]
+        if ws == 1 and any(x in iss for x in names):
+            r_["ncu_utilisation"] = {x: iss[x] for x in names if x in iss}
         tb = sum(tr[x] for x in names) if all(x in tr for x in names) else None
         if tb is not None and ws == 1:
             r_["traffic"] = tb
