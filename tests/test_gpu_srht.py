@@ -138,3 +138,27 @@ def test_one_plan_all_entry_points_interleaved(cuda):
     assert torch.equal(q2[1], _plan(24, 48, "f64").factor2(X)[1])
     plan.close()
     rcq.theta_export(0, 8, 16, sketch="rademacher")    # raises if an error was left pending
+
+
+def test_edge_cases_new_entry_points(cuda):
+    X = synth.make_X(30_000, 20, 3.0)
+    Xt = _t(X)
+    # SRHT with k > 512 (beyond the tcgen05 tile limit): DMMA path, still the oracle's sketch
+    Pg = _np(_plan(20, 600, "f64").sketch(Xt))
+    assert _rel(Pg, oracle.sketch(X, 600, sketch=oracle.SRHT)) <= 1e-12
+    # Alg. 5 with more extractor rows than sketch rows, sparse Theta
+    plan = rcq.RCholQR(n=20, k=40, dtype=torch.float64, sketch="sparse", nnz_per_col=8)
+    Z, R, _, Y = plan.factor_reduced(Xt, 90, want_Y=True)
+    ref = oracle.factor_reduced(X, 40, 90, sketch=oracle.SPARSE_SIGN, zeta=8)
+    assert _rel(_np(Y), ref["Y"]) <= 1e-12 and _rel(_np(Z), ref["Z"]) <= 1e-11
+    # Alg. 7 with tau = 0 on a full-rank X: rank n, Q equals Alg. 2 on the permuted columns
+    g = _plan(20, 40, "f64").factor_rr(Xt, 0.0)
+    assert g["rank"] == 20
+    perm = _np(g["perm"]).astype(np.int64)
+    Qp, _, _ = _plan(20, 40, "f64").factor(_t(np.ascontiguousarray(X[:, perm])))
+    assert _rel(_np(g["Q"]), _np(Qp)) <= 1e-12
+    # RRRCholeskyQR2 at a fixed rank: orthonormal m x r Q
+    g2 = _plan(20, 40, "f64").factor_rr2(Xt, 0.0, rank_fixed=7)
+    Q = _np(g2["Q"])
+    assert g2["rank"] == 7 and Q.shape == (30_000, 7)
+    assert np.linalg.norm(Q.T @ Q - np.eye(7), 2) <= 1e-13
