@@ -15,6 +15,8 @@
 //   i.e. A_t <- (I - V T^T V^T) A_t = Q_panel^T A_t.
 #include <cuda_runtime.h>
 #include <algorithm>
+#include <cooperative_groups.h>
+#include <cstdlib>
 #include "internal.cuh"
 
 namespace rcq {
@@ -133,6 +135,192 @@ qr_panel_kernel(double* __restrict__ A, int k, int n, int j0, int nb, double* __
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// The same panel factorization on a thread-block CLUSTER (K = k - j0 <= QC_ROWS * QC_MAXCL rows): CTA c
+// owns rows j0 + c QC_ROWS .. + QC_ROWS - 1, one row per thread, the row's nb panel values in REGISTERS.
+// Per column p: the partial column norm (rows >= j) and the nb - p - 1 partial dot products of each CTA
+// are exchanged through distributed shared memory around cluster barriers and summed in a fixed CTA
+// order (every CTA computes bit-identical alpha, beta, w_q).  The pivot row j0 + p always lies in CTA 0
+// (p < nb <= QC_ROWS).  Outputs exactly as qr_panel_kernel: the updated panel in A (v0 on the diagonal),
+// diag / tau, Vt / Vr, and -T from G = V^T V (partial G per CTA from a shared V tile, summed in CTA 0).
+constexpr int QC_ROWS = 256;
+constexpr int QC_MAXCL = 8;
+
+// warp all-reduce of 32 per-lane vectors by a transpose-reduce butterfly: on return lane L holds the
+// warp sum of component L (31 shuffles instead of 32 x 5)
+__device__ __forceinline__ double qc_transpose_reduce(double (&v)[32], int lane) {
+#pragma unroll
+  for (int j = 16; j >= 1; j >>= 1) {
+    const bool lo = !(lane & j);
+#pragma unroll
+    for (int i = 0; i < j; ++i) {
+      const double send = lo ? v[i + j] : v[i];
+      const double keep = lo ? v[i] : v[i + j];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, j);
+    }
+  }
+  return v[0];
+}
+
+__global__ void __launch_bounds__(QC_ROWS, 1)
+qr_panel_cluster_kernel(double* __restrict__ A, int k, int n, int j0, int nb, double* __restrict__ diag,
+                        double* __restrict__ tau, double* __restrict__ Vt, double* __restrict__ Vr,
+                        double* __restrict__ Tneg, const int* status) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cluster = cg::this_cluster();
+  const int crank = (int)cluster.block_rank(), csize = (int)cluster.num_blocks();
+  if (*status) return;                                     // uniform over the cluster
+  __shared__ double sh_norm[2];                            // this CTA's partial norm^2, by step parity
+  __shared__ double sh_x0[2];                              // CTA 0: the next pivot entry
+  __shared__ double sh_dot[2][QB_NB];                      // this CTA's partial dots, by step parity
+  __shared__ double sh_wred[QC_ROWS / 32][QB_NB];          // per-warp partials
+  __shared__ double sh_nred[QC_ROWS / 32];
+  __shared__ double sh_G[QB_NB][QB_NB + 1];                // partial G (upper), then (CTA 0) the sum
+  __shared__ double sh_beta[QB_NB], sh_v0[QB_NB];
+  __shared__ double sh_w[QB_NB], sh_gath[2];              // gathered (cluster-summed) dots / norm^2, x0
+  extern __shared__ double qc_dyn[];
+  double (*Vs)[QB_NB + 1] = reinterpret_cast<double (*)[QB_NB + 1]>(qc_dyn);   // [QC_ROWS][QB_NB + 1]
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int K = k - j0;
+  const int lr = tid, gi = j0 + crank * QC_ROWS + lr;      // this thread's global row
+  const bool live = gi < k;
+  double x[QB_NB];
+#pragma unroll
+  for (int q = 0; q < QB_NB; ++q) x[q] = (live && q < nb) ? A[(size_t)(j0 + q) * k + gi] : 0.0;
+  auto block_sum = [&](double v) {                         // CTA sum (all threads get it)
+    v = qb_warp_sum(v);
+    if (lane == 0) sh_nred[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+#pragma unroll
+    for (int w = 0; w < QC_ROWS / 32; ++w) t += sh_nred[w];
+    __syncthreads();
+    return t;
+  };
+  {   // partial ||A[j0:, j0]||^2 and the first pivot entry
+    const double t = block_sum(x[0] * x[0]);
+    if (tid == 0) sh_norm[0] = t;
+    if (crank == 0 && tid == 0) sh_x0[0] = x[0];
+  }
+  for (int p = 0; p < nb; ++p) {
+    const int j = j0 + p, par = p & 1;
+    cluster.sync();                                        // exchange 1: norm partials and x0 of step p
+    if (tid == 0) {                                        // one gather per CTA, fixed CTA order
+      double t = 0.0;
+      for (int c = 0; c < csize; ++c) t += *cluster.map_shared_rank(&sh_norm[par], c);
+      sh_gath[0] = t;
+      sh_gath[1] = *cluster.map_shared_rank(&sh_x0[par], 0);
+    }
+    __syncthreads();
+    const double norm2 = sh_gath[0], x0 = sh_gath[1];
+    const double alpha = sqrt(norm2);
+    const double sgn = x0 >= 0.0 ? 1.0 : -1.0;
+    const double v0 = x0 + sgn * alpha;
+    const double beta = alpha == 0.0 ? 0.0 : 1.0 / (alpha * fabs(v0));
+    if (crank == 0 && tid == 0) {
+      tau[j] = beta;
+      diag[j] = alpha == 0.0 ? 0.0 : -sgn * alpha;
+      diag[n + j] = v0;
+    }
+    if (tid == 0) { sh_beta[p] = beta; sh_v0[p] = v0; }
+    // this thread's reflector entry: v0 on row j, the column below it, 0 above
+    double vt = 0.0;
+#pragma unroll
+    for (int q = 0; q < QB_NB; ++q)
+      if (q == p) vt = (live && gi > j) ? x[q] : (gi == j ? v0 : 0.0);
+    // partial dots of the trailing panel columns q > p
+    double prod[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) prod[q] = (q > p && q < nb) ? vt * x[q < QB_NB ? q : 0] : 0.0;
+    const double wsum = qc_transpose_reduce(prod, lane);   // lane q: warp partial of column q
+    sh_wred[warp][lane] = wsum;
+    __syncthreads();
+    if (warp == 0) {
+      double t = 0.0;
+#pragma unroll
+      for (int w = 0; w < QC_ROWS / 32; ++w) t += sh_wred[w][lane];
+      sh_dot[par][lane] = t;
+    }
+    cluster.sync();                                        // exchange 2: dot partials of step p
+    if (warp == 0) {                                       // lane q gathers column q, fixed CTA order
+      double t = 0.0;
+      if (lane > p && lane < nb)
+        for (int c = 0; c < csize; ++c) t += cluster.map_shared_rank(&sh_dot[par][0], c)[lane];
+      sh_w[lane] = t * beta;
+    }
+    __syncthreads();
+    if (beta != 0.0) {
+#pragma unroll
+      for (int q = 0; q < QB_NB; ++q)
+        if (q > p && q < nb && live && gi >= j) x[q] -= vt * sh_w[q];   // row j: v0 * w
+    }
+    // look-ahead: partial norm^2 of column p + 1 over rows >= j + 1, and its pivot entry
+    if (p + 1 < nb) {
+      double xn = 0.0;
+#pragma unroll
+      for (int q = 0; q < QB_NB; ++q)
+        if (q == p + 1) xn = x[q];
+      const double t = block_sum((live && gi > j) ? xn * xn : 0.0);
+      if (tid == 0) sh_norm[par ^ 1] = t;
+      if (crank == 0 && lr == p + 1) sh_x0[par ^ 1] = xn;
+    }
+  }
+  // write back the panel (v0 on the diagonal), V in both layouts, the partial G from the V tile
+#pragma unroll
+  for (int q = 0; q < QB_NB; ++q) {
+    if (q >= nb) break;
+    const int col = j0 + q;
+    double v;
+    if (!live) v = 0.0;
+    else if (gi < col) v = 0.0;
+    else if (gi == col) v = sh_v0[q];
+    else v = x[q];
+    Vs[lr][q] = v;
+    if (live) {
+      A[(size_t)col * k + gi] = gi == col ? sh_v0[q] : x[q];
+      Vt[(size_t)(gi - j0) * nb + q] = v;
+      Vr[(size_t)q * K + (gi - j0)] = v;
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < nb * nb; e += QC_ROWS) {           // partial G(a, b), a <= b
+    const int a = e / nb, b = e % nb;
+    if (a > b) continue;
+    double t = 0.0;
+    for (int r = 0; r < QC_ROWS; ++r) t += Vs[r][a] * Vs[r][b];
+    sh_G[a][b] = t;
+  }
+  cluster.sync();
+  if (crank == 0) {
+    for (int e = tid; e < nb * nb; e += QC_ROWS) {
+      const int a = e / nb, b = e % nb;
+      if (a > b) continue;
+      double t = 0.0;
+      for (int c = 0; c < csize; ++c) t += cluster.map_shared_rank(&sh_G[0][0], c)[a * (QB_NB + 1) + b];
+      Tneg[a * nb + b] = t;                                // scratch: the summed G (upper), read below
+    }
+  }
+  cluster.sync();                                          // remote reads of sh_G finished
+  if (crank == 0) {
+    __threadfence_block();
+    if (warp == 0) {
+      __shared__ double Tsh[QB_NB][QB_NB + 1];
+      for (int jj = 0; jj < nb; ++jj) {
+        double y = 0.0;
+        if (lane < jj)
+          for (int q = lane; q < jj; ++q) y += Tsh[lane][q] * Tneg[q * nb + jj];
+        __syncwarp();
+        if (lane < jj) Tsh[lane][jj] = -sh_beta[jj] * y;
+        if (lane == jj) Tsh[jj][jj] = sh_beta[jj];
+        if (lane > jj) Tsh[lane][jj] = 0.0;
+        __syncwarp();
+      }
+      __syncwarp();
+      for (int c = lane; c < nb * nb; c += 32) Tneg[c] = -Tsh[c / nb][c % nb];
+    }
+  }
+}
+
 // R (row-major, zeros below the diagonal, rows with a negative pivot negated) + singular flag.
 __global__ void qr_finalize_kernel(const double* __restrict__ A, int k, int n, const double* __restrict__ diag,
                                    double* __restrict__ R, int* status) {
@@ -171,7 +359,31 @@ cudaError_t launch_qr_blocked(const double* P, int k, int n, double* R, double* 
   for (int j0 = 0; j0 < n; j0 += QB_NB) {
     const int nb = std::min(QB_NB, n - j0);
     const int K = k - j0;
-    qr_panel_kernel<<<1, QB_THREADS, 0, st>>>(A, k, n, j0, nb, diag, tau, Vt, Vr, Tneg, status);
+    static const bool old_panel = getenv("RCHOLQR_QR_PANEL_OLD") != nullptr;   // experiments
+    const int cl = (K + QC_ROWS - 1) / QC_ROWS;
+    bool done = false;
+    if (!old_panel && cl >= 3 && cl <= QC_MAXCL) {      // panel held on-chip by a cluster of cl CTAs (K > 512)
+      constexpr size_t qc_smem = sizeof(double) * QC_ROWS * (QB_NB + 1);
+      static const bool attr_ok = cudaFuncSetAttribute(qr_panel_cluster_kernel,
+                                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                       (int)qc_smem) == cudaSuccess;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(cl);
+      cfg.blockDim = dim3(QC_ROWS);
+      cfg.dynamicSmemBytes = qc_smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = cl;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      done = attr_ok && cudaLaunchKernelEx(&cfg, qr_panel_cluster_kernel, A, k, n, j0, nb, diag, tau, Vt, Vr, Tneg,
+                                (const int*)status) == cudaSuccess;
+      if (!done) cudaGetLastError();                       // no cluster launch: the single-CTA kernel
+    }
+    if (!done) qr_panel_kernel<<<1, QB_THREADS, 0, st>>>(A, k, n, j0, nb, diag, tau, Vt, Vr, Tneg, status);
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     const int nt = n - j0 - nb;
     if (nt <= 0) continue;
