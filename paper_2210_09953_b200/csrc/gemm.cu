@@ -278,6 +278,9 @@ cudaError_t launch_gemm_f64(const double* A, int64_t lda, const double* B, int64
   static const bool no_cp = getenv("RCHOLQR_GEMM_NO_CP") != nullptr;               // experiments
   if (wide && N > 64) return launch_g64<2, 4, 4, 4>(A, lda, B, ldb, C0, ldc0, C, ldc, m, N, K, tri_b, status, st);
   if (!no_cp && K >= 128 && N >= 64) return launch_gcp<4, 2, 2, 4>(A, lda, B, ldb, C0, ldc0, C, ldc, m, N, K, tri_b, status, st);
+  // narrow products (the blocked QR's N = 32 panel updates): 128 x 32 tiles, 8 warps of 16 x 32
+  static const bool no_narrow = getenv("RCHOLQR_GEMM_NO_NARROW") != nullptr;      // experiments
+  if (!no_narrow && N <= 32) return launch_g64<8, 1, 1, 4>(A, lda, B, ldb, C0, ldc0, C, ldc, m, N, K, tri_b, status, st);
   auto kern = gemm_f64_kernel<4, 2, 2, 4>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GemmC::SMEM);
   if (e != cudaSuccess) return e;
