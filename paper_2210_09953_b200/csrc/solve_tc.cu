@@ -26,8 +26,9 @@
 // digits (cp.async.bulk) and, for n <= 64, the X tiles (one 2D TMA box of 128 rows x K+4 columns
 // per tile, two-stage ring); warps 2..9 drain TMEM in two sets of four (set d drains level buffer d,
 // one lane quadrant per warp) and write Q through swizzled shared memory with TMA stores; warps
-// 10..17 split X into digit planes (for 64 < n <= 128 they read X with plain loads: there is room
-// for only one digit stage and no raw ring).
+// 10..17 split X into digit planes (for 64 < n <= 128 they read X with plain loads into registers
+// and write the digits as two K-halves into a ring of three half slots: there is no room for a raw
+// ring or a second full digit stage).
 #include <cuda_runtime.h>
 #include <cmath>
 #include <cstdint>
@@ -64,40 +65,52 @@ struct QCfg {
   static constexpr int RS = KMAX + 4;             // raw X row pitch (floats): K + 4 -> conflict-free LDS.128
   static constexpr int RAW_STAGE = QT_M * RS * 4;
   static constexpr int W_BYTES = qt_woff(KMAX / 32);
+  // 64 < n <= 128: the X digits of a tile are kept as two K-halves (columns 0..63, 64..127) in a
+  // ring of three half slots, so the first half of tile t + 1 is written while the MMAs of tile t
+  // still read both halves of tile t; Q is stored from registers (no staging tile: no room)
+  static constexpr bool HALF = !TMA_RAW;
+  static constexpr int NSLOT = HALF ? 3 : DIG;
+  static constexpr int H_TILE = QT_M * 64;        // one digit plane of one K-half
+  static constexpr int SLOT_BYTES = HALF ? QT_DA * H_TILE : QT_DA * A_TILE;
+  static constexpr int QS = HALF ? QT_RWARPS * 32 * 8 * 4 : QT_QS_BYTES;   // HALF: one 32-row x 8-column tile per drain warp
   static constexpr size_t SMEM =
-      (size_t)W_BYTES + (size_t)DIG * QT_DA * A_TILE + (size_t)RAW * RAW_STAGE + QT_QS_BYTES + 2048;
+      (size_t)W_BYTES + (size_t)NSLOT * SLOT_BYTES + (size_t)RAW * RAW_STAGE + QS + 4096;
   static_assert(SMEM <= 232448, "shared memory");
 };
 
 // ---------------------------------------------------------------------------------------------
 // W digit prep: column scales e_j and the signed digit planes, laid out per group g as the B
 // operand tile [6 * 32 rows (row = b * 32 + jj) x K bytes], K-major SWIZZLE_NONE core matrices.
-__global__ void solve_tc_prep_kernel(const double* __restrict__ W, int n, int kpad, int8_t* __restrict__ wdig,
-                                     int* __restrict__ wexp, const int* status) {
+__global__ void __launch_bounds__(QT_KMAX_ALL)
+solve_tc_prep_kernel(const double* __restrict__ W, int n, int kpad, int8_t* __restrict__ wdig,
+                     int* __restrict__ wexp, const int* status) {
+  // one CTA per column j, one thread per row l of W (the serial per-column loops of a single CTA
+  // cost ~0.1 ms at n = 100: two dependent global-load chains of n steps)
   if (*status) return;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  const int groups = (n + QT_G - 1) / QT_G;
-  if (j >= groups * QT_G) return;
-  const int g = j / QT_G, jj = j % QT_G;
+  __shared__ double wmax[QT_KMAX_ALL / 32];
+  const int j = blockIdx.x, l = threadIdx.x, g = j / QT_G, jj = j % QT_G;
   const int kg = min(QT_G * (g + 1), kpad);          // rows l < kg of W (upper triangular)
-  int8_t* tile = wdig + qt_woff(g);
-  double mx = 0.0;
-  if (j < n)
-    for (int l = 0; l < n; ++l) mx = fmax(mx, fabs(W[(size_t)l * n + j]));
+  const double w = (j < n && l < n) ? W[(size_t)l * n + j] : 0.0;
+  double mx = fabs(w);
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((l & 31) == 0) wmax[l >> 5] = mx;
+  __syncthreads();
+  mx = 0.0;
+  for (int q = 0; q < (int)(blockDim.x >> 5); ++q) mx = fmax(mx, wmax[q]);
   int e = 0;
   if (mx > 0.0) { frexp(mx, &e); }                     // mx < 2^e
-  wexp[j] = e;
-  for (int l = 0; l < kg; ++l) {
-    long long F = (j < n && l < n) ? llrint(ldexp(W[(size_t)l * n + j], 54 - e)) : 0;   // |F| <= 2^54
-    int d[QT_DB];
-    for (int b = QT_DB - 1; b >= 1; --b) {             // balanced base-256 digits, exact
-      const long long r = ((F + 128) & 255) - 128;
-      d[b] = (int)r;
-      F = (F - r) >> 8;
-    }
-    d[0] = (int)F;                                     // |d0| <= 65
-    for (int b = 0; b < QT_DB; ++b) tile[(l >> 4) * QT_NB * 16 + (b * QT_G + jj) * 16 + (l & 15)] = (int8_t)d[b];
+  if (l == 0) wexp[j] = e;
+  if (l >= kg) return;
+  long long F = llrint(ldexp(w, 54 - e));               // |F| <= 2^54
+  int d[QT_DB];
+  for (int b = QT_DB - 1; b >= 1; --b) {               // balanced base-256 digits, exact
+    const long long r = ((F + 128) & 255) - 128;
+    d[b] = (int)r;
+    F = (F - r) >> 8;
   }
+  d[0] = (int)F;                                       // |d0| <= 65
+  int8_t* tile = wdig + qt_woff(g);
+  for (int b = 0; b < QT_DB; ++b) tile[(l >> 4) * QT_NB * 16 + (b * QT_G + jj) * 16 + (l & 15)] = (int8_t)d[b];
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -109,24 +122,28 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
                 int dbg) {
   using Cf = QCfg<KMAX>;
   constexpr int QT_DIG = Cf::DIG, QT_RAW = Cf::RAW > 0 ? Cf::RAW : 1, QT_A_TILE = Cf::A_TILE;
+  constexpr int NSLOT = Cf::NSLOT, SLOT = Cf::SLOT_BYTES, H_TILE = Cf::H_TILE;
   constexpr int QT_RS_MAX = Cf::RS, QT_RAW_STAGE = Cf::RAW_STAGE;
   if (*status) return;                                 // singular R: Q is not written
   extern __shared__ __align__(1024) unsigned char sm[];
   unsigned char* wsm = sm;                                                   // W digits, all groups
-  unsigned char* abase = sm + Cf::W_BYTES;                                    // [DIG][DA][A_TILE]
-  float* raw_base = reinterpret_cast<float*>(abase + (size_t)QT_DIG * QT_DA * QT_A_TILE);   // [RAW][128][RS]
+  unsigned char* abase = sm + Cf::W_BYTES;                                    // [NSLOT][DA][A_TILE or H_TILE]
+  float* raw_base = reinterpret_cast<float*>(abase + (size_t)NSLOT * SLOT);  // [RAW][128][RS]
   unsigned char* qstage = reinterpret_cast<unsigned char*>(raw_base) + (size_t)Cf::RAW * QT_RAW_STAGE;   // [8][32 rows][128 B]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(qstage + QT_QS_BYTES);
-  uint64_t* dfull = bars;                   // [DIG] X digits of a tile ready
-  uint64_t* dempty = dfull + QT_DIG;        // [DIG] tile fully drained (slot + row scales free)
-  uint64_t* rfull = dempty + QT_DIG;        // [RAW]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(qstage + Cf::QS);
+  uint64_t* dfull = bars;                   // [NSLOT] X digits of a tile (or K-half) ready
+  uint64_t* dempty = dfull + NSLOT;         // [NSLOT] MMAs reading the slot complete (tcgen05.commit)
+  uint64_t* rfull = dempty + NSLOT;         // [RAW]
   uint64_t* rempty = rfull + QT_RAW;        // [RAW]
   uint64_t* tready = rempty + QT_RAW;       // [2] level buffer written (commit)
   uint64_t* tfree = tready + 2;             // [2] level buffer drained
   uint64_t* wbar = tfree + 2;               // W digits staged
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wbar + 1);
-  int* rexp = reinterpret_cast<int*>(tmem_slot + 4);                          // [DIG][128]
-  double* wsc = reinterpret_cast<double*>(rexp + QT_DIG * QT_M);             // [64] 2^(e_j - 60): column scale x 2^-(46+54-40)
+  // row scales: a ring of 4 tiles, so the digit slot can be refilled while the drain of the tile
+  // before still reads its scales (a slot is free once the MMAs of tile t complete, and those
+  // follow every drain of tile t - 2; see the TMEM buffer waits below)
+  int* rexp = reinterpret_cast<int*>(tmem_slot + 4);                          // [4][128]
+  double* wsc = reinterpret_cast<double*>(rexp + 4 * QT_M);             // [64] 2^(e_j - 60): column scale x 2^-(46+54-40)
 
   const int groups = (n + QT_G - 1) / QT_G;
   const int64_t ntiles = (m + QT_M - 1) / QT_M;
@@ -135,7 +152,7 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
   const int lg_n = kpad / 16;                                                 // 16-column groups per row
 
   if (tid == 0) {
-    for (int s = 0; s < QT_DIG; ++s) { tc::mbar_init(&dfull[s], QT_DWARPS); tc::mbar_init(&dempty[s], QT_RWARPS); }
+    for (int s = 0; s < NSLOT; ++s) { tc::mbar_init(&dfull[s], QT_DWARPS); tc::mbar_init(&dempty[s], 1); }
     for (int s = 0; s < QT_RAW; ++s) { tc::mbar_init(&rfull[s], 1); tc::mbar_init(&rempty[s], QT_DWARPS); }
     for (int b = 0; b < 2; ++b) { tc::mbar_init(&tready[b], 1); tc::mbar_init(&tfree[b], 4); }
     tc::mbar_init(wbar, 1);
@@ -155,21 +172,29 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
     // ---------------------------------------------------------------- MMA issuer (lane 0)
     tc::mbar_wait(wbar, 0u);
     for (int tt = 0; tt < my_tiles; ++tt) {
-      const int s = tt % QT_DIG;
-      tc::mbar_wait(&dfull[s], (uint32_t)((tt / QT_DIG) & 1));
+      // full-tile slot s (n <= 64), or the two K-half slots s, s1 (uses 2 tt and 2 tt + 1 of the ring)
+      const int s = Cf::HALF ? (2 * tt) % NSLOT : tt % NSLOT, s1 = (2 * tt + 1) % NSLOT;
+      tc::mbar_wait(&dfull[s], (uint32_t)(((Cf::HALF ? 2 * tt : tt) / NSLOT) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;\n");
+      bool have1 = !Cf::HALF;
       for (int g = 0; g < groups; ++g) {
         const int use = tt * groups + g, buf = use & 1, u = use >> 1;
         if (u > 0) tc::mbar_wait(&tfree[buf], (uint32_t)((u - 1) & 1));
+        const int ksteps = min(g + 1, kpad / 32);             // W rows l < 32 (g + 1): upper triangular
+        if (!have1 && ksteps > 2) {                           // second K-half needed from here on
+          tc::mbar_wait(&dfull[s1], (uint32_t)(((2 * tt + 1) / NSLOT) & 1));
+          have1 = true;
+        }
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         if (lane == 0 && !(dbg & 1)) {
-          const uint32_t sa = tc::smem_u32(abase + (size_t)s * QT_DA * QT_A_TILE);
           const uint32_t sb = tc::smem_u32(wsm + qt_woff(g));
-          const int ksteps = min(g + 1, kpad / 32);           // W rows l < 32 (g + 1): upper triangular
           for (int ks = 0; ks < ksteps; ++ks) {
+            const uint32_t sa = Cf::HALF ? tc::smem_u32(abase + (size_t)(ks < 2 ? s : s1) * SLOT) + (ks & 1) * 2 * (QT_M * 16)
+                                         : tc::smem_u32(abase + (size_t)s * SLOT) + ks * 2 * (QT_M * 16);
+            constexpr int PLANE = Cf::HALF ? H_TILE : QT_A_TILE;
 #pragma unroll
             for (int a = 0; a < QT_DA; ++a) {
-              const uint64_t da = tc::desc(sa + a * QT_A_TILE + ks * 2 * (QT_M * 16), QT_M * 16, 128);
+              const uint64_t da = tc::desc(sa + a * PLANE, QT_M * 16, 128);
               const uint64_t db = tc::desc(sb + ks * 2 * (QT_NB * 16), QT_NB * 16, 128);
               const uint32_t idesc = tc::idesc_i8(QT_M, (QT_DB - a) * QT_G, true, true);
               tc::mma_i8(tmem + buf * (QT_LEV * QT_G) + a * QT_G, da, db, idesc, (ks > 0 || a > 0) ? 1u : 0u);
@@ -179,6 +204,11 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
         if (lane == 0) tc::commit(&tready[buf]);
         __syncwarp();
       }
+      if (lane == 0) {                                    // digit slot(s) free once these MMAs complete
+        tc::commit(&dempty[s]);
+        if (Cf::HALF) tc::commit(&dempty[s1]);
+      }
+      __syncwarp();
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- loader (lane 0)
@@ -207,7 +237,6 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
     const int dset = (warp - 2) >> 2, dq = warp & 3, row_l = dq * 32 + lane;
     const uint32_t lb = tmem + ((uint32_t)(dq * 32) << 16);
     for (int tt = 0; tt < my_tiles; ++tt) {
-      const int s = tt % QT_DIG;
       for (int g = 0; g < groups; ++g) {
         const int use = tt * groups + g, buf = use & 1, u = use >> 1;
         if (buf != dset) continue;
@@ -218,6 +247,56 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
         // each converted to fp64 by the 2^52 magic constant (LOP3 + DADD, no I2F), then combined
         // by three DFMAs -- the fewest issue slots per output of the variants tried.
         static_assert(QT_LEV == 7, "pairing below assumes 7 levels");
+        if constexpr (Cf::HALF) {
+          // 8 columns at a time: all 7 level loads in flight before one wait; each 32-row x 8-column
+          // fp32 chunk is staged in a 1 KB tile (all the room the K-half ring leaves) and written
+          // by a 2D TMA store; the TMEM buffer is released right after the last chunk's loads
+          const double si = __hiloint2double((rexp[(tt & 3) * QT_M + row_l] + 1023) << 20, 0);   // 2^e_i
+          const uint32_t lv = lb + buf * (QT_LEV * QT_G);
+          unsigned char* qs = qstage + (warp - 2) * (32 * 8 * 4);
+#pragma unroll
+          for (int h = 0; h < QT_G / 8; ++h) {
+            uint32_t lvl[QT_LEV][8];
+#pragma unroll
+            for (int L = 0; L < QT_LEV; ++L) {
+              if (dbg & 4) {
+#pragma unroll
+                for (int c = 0; c < 8; ++c) lvl[L][c] = 0u;
+              } else {
+                tc::ld8(lv + L * QT_G + h * 8, lvl[L]);
+              }
+            }
+            tc::wait_ld();
+            if (h == QT_G / 8 - 1) {
+              asm volatile("tcgen05.fence::before_thread_sync;\n");
+              __syncwarp();
+              if (lane == 0) tc::mbar_arrive(&tfree[buf]);
+            }
+            float o[8];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              double f[4];
+#pragma unroll
+              for (int pp = 0; pp < 4; ++pp) {
+                const uint32_t pv = pp < 3 ? lvl[2 * pp][c] * 256u + lvl[2 * pp + 1][c] : lvl[6][c];
+                f[pp] = __hiloint2double(0x43300000, (int)(pv ^ 0x80000000u)) - 4503601774854144.0;   // 2^52 + 2^31
+              }
+              const double v = fma(f[0], 0x1p40, fma(f[1], 0x1p24, fma(f[2], 256.0, f[3])));
+              o[c] = __double2float_rn(v * si * wsc[g * QT_G + h * 8 + c]);
+            }
+            if (lane == 0) tc::bulk_wait_read0();            // previous chunk's store has read the tile
+            __syncwarp();
+            *reinterpret_cast<float4*>(qs + lane * 32) = make_float4(o[0], o[1], o[2], o[3]);
+            *reinterpret_cast<float4*>(qs + lane * 32 + 16) = make_float4(o[4], o[5], o[6], o[7]);
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {                                 // TMA clips rows >= m and columns >= n
+              tc::tma_store_2d(&qmap, qs, g * QT_G + h * 8, (int)((blockIdx.x + (int64_t)tt * gridDim.x) * QT_M + dq * 32));
+              tc::bulk_commit();
+            }
+          }
+          continue;
+        }
         double v[QT_G];
         const uint32_t lv = lb + buf * (QT_LEV * QT_G);
         if (dbg & 4) {
@@ -247,6 +326,9 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
             v[h * 8 + c] = fma(f[0], 0x1p40, fma(f[1], 0x1p24, fma(f[2], 256.0, f[3])));
           }
         }
+        // row scale read before the buffer is released: the rexp ring slot is reused only after
+        // later MMAs, which wait on this release
+        const double si = __hiloint2double((rexp[(tt & 3) * QT_M + row_l] + 1023) << 20, 0);   // 2^e_i
         asm volatile("tcgen05.fence::before_thread_sync;\n");
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(&tfree[buf]);       // TMEM buffer free; the stores below need no TMEM
@@ -254,7 +336,6 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
           // stage this warp's 32 rows x 32 columns (fp32) in shared memory with the 128-byte swizzle
           // (16-byte chunk c of row r at chunk c ^ (r & 7): conflict-free STS.128), then one 2D TMA
           // store writes them; TMA clips rows >= m and columns >= n.
-          const double si = __hiloint2double((rexp[s * QT_M + row_l] + 1023) << 20, 0);   // 2^e_i
           unsigned char* qs = qstage + (warp - 2) * (32 * QT_G * 4);
           if (lane == 0) tc::bulk_wait_read0();              // previous store finished reading the tile
           __syncwarp();
@@ -275,83 +356,152 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
           }
         }
       }
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&dempty[s]);          // slot (X digits + row scales) free
     }
   } else {
     // ---------------------------------------------------------------- X digit planes
+    // lane -> (column group lg, row): consecutive lanes take consecutive rows of one column group,
+    // so with the (K + 4)-float pitch every 8-lane phase of an LDS.128 hits 8 distinct 16-byte
+    // bank groups, and the digit STS.128 of a phase are contiguous.  The column groups per row are
+    // rounded up to a power of two (lg_map) for the shuffle max; groups >= lg_n read zeros.
+    // Plain-load producers (64 < n <= 128) issue the loads of all their tasks of a tile before
+    // waiting for the digit slot, so the HBM latency overlaps the MMAs of the tile before.
     const int dt = tid - 32 * (2 + QT_RWARPS);
+    const int lg_map = lg_n <= 2 ? lg_n : (lg_n <= 4 ? 4 : 8), rpw = 32 / lg_map;
+    const int ntask = (dbg & 2) ? 0 : QT_M * lg_map;
+    auto task_pos = [&](int task, int& lg, int& i) {
+      const int w = task >> 5, l = task & 31;
+      lg = l / rpw; i = w * rpw + (l % rpw);
+    };
+    // the six signed base-256 digits of round(x 2^(46 - e)), packed 4 columns per word, for 16 x
+    auto digit_words = [&](const float* x, int e, uint32_t (&W)[QT_DA][4]) {
+      const double sx = ldexp(1.0, 128 + 46 - e);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t hw[4], lw[4];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint32_t ub = __float_as_uint(x[q * 4 + kk]);
+          const uint32_t h = ((uint32_t)((int32_t)ub >> 3) & 0x8FFFFFFFu) | 0x30000000u;   // x 2^-128
+          const double t = fma(__hiloint2double((int)h, (int)(ub << 29)), sx, kMagic + (double)0x8080808080ull);
+          hw[kk] = (uint32_t)__double2hiint(t);                                              // F + C, 48 bits
+          lw[kk] = (uint32_t)__double2loint(t);
+        }
+        uint32_t H[4], L[4];
+        transpose4(hw[0], hw[1], hw[2], hw[3], H);
+        transpose4(lw[0], lw[1], lw[2], lw[3], L);
+        W[0][q] = H[1]; W[1][q] = H[0] ^ 0x80808080u;
+        W[2][q] = L[3] ^ 0x80808080u; W[3][q] = L[2] ^ 0x80808080u;
+        W[4][q] = L[1] ^ 0x80808080u; W[5][q] = L[0] ^ 0x80808080u;
+      }
+    };
+    auto digits = [&](int task, int tt, unsigned char* at, const float* x) {
+      int lg, i;
+      task_pos(task, lg, i);
+      uint32_t mx = 0u;
+#pragma unroll
+      for (int c = 0; c < 16; ++c) mx = max(mx, __float_as_uint(x[c]) & 0x7FFFFFFFu);
+      for (int o = rpw; o < 32; o <<= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      // e_i: smallest e with max |x| < 2^e (finite input assumed: the sketch rejected NaN/Inf)
+      const int e = mx == 0u ? 0 : (mx < 0x00800000u ? -126 : (int)(mx >> 23) - 126);
+      if (lg == 0) rexp[(tt & 3) * QT_M + i] = e;
+      uint32_t W[QT_DA][4];
+      digit_words(x, e, W);
+#pragma unroll
+      for (int a = 0; a < QT_DA; ++a)
+        *reinterpret_cast<uint4*>(at + a * QT_A_TILE + lg * (QT_M * 16) + i * 16) =
+            make_uint4(W[a][0], W[a][1], W[a][2], W[a][3]);
+    };
+    float xh0[2][16], xh1[2][16];                          // HALF producers: [task][16] per K-half
     for (int tt = 0; tt < my_tiles; ++tt) {
       const int s = tt % QT_DIG, sr = tt % QT_RAW;
-      if (tt >= QT_DIG) tc::mbar_wait(&dempty[s], (uint32_t)(((tt / QT_DIG) - 1) & 1));
-      if (Cf::TMA_RAW) tc::mbar_wait(&rfull[sr], (uint32_t)((tt / QT_RAW) & 1));
-      const float* raw = raw_base + (size_t)sr * QT_M * QT_RS_MAX;
-      const int64_t trow0 = (blockIdx.x + (int64_t)tt * gridDim.x) * QT_M;
       unsigned char* at = abase + (size_t)s * QT_DA * QT_A_TILE;
-      const int rs = kpad + 4, rpw = 32 / lg_n;            // raw row pitch; rows per warp pass
-      for (int task = dt; task < ((dbg & 2) ? 0 : QT_M * lg_n); task += 32 * QT_DWARPS) {
-        // lane -> (column group lg, row): consecutive lanes take consecutive rows of one column
-        // group, so with the (K + 4)-float pitch every 8-lane phase of an LDS.128 hits 8 distinct
-        // 16-byte bank groups, and the digit STS.128 of a phase are contiguous.
-        const int w = task >> 5, l = task & 31;
-        const int lg = l / rpw, i = w * rpw + (l % rpw);
-        float x[16];
-        if constexpr (Cf::TMA_RAW) {
+      if constexpr (Cf::TMA_RAW) {
+        if (tt >= QT_DIG) tc::mbar_wait(&dempty[s], (uint32_t)(((tt / QT_DIG) - 1) & 1));
+        tc::mbar_wait(&rfull[sr], (uint32_t)((tt / QT_RAW) & 1));
+        const float* raw = raw_base + (size_t)sr * QT_M * QT_RS_MAX;
+        const int rs = kpad + 4;                                         // raw row pitch
+        for (int task = dt; task < ntask; task += 32 * QT_DWARPS) {
+          int lg, i;
+          task_pos(task, lg, i);
+          float x[16];
 #pragma unroll
           for (int c = 0; c < 16; c += 4) {
             const float4 f = *reinterpret_cast<const float4*>(raw + i * rs + lg * 16 + c);
             x[c] = f.x; x[c + 1] = f.y; x[c + 2] = f.z; x[c + 3] = f.w;
           }
-        } else {                                           // plain loads, zero outside X
-          const int64_t row = trow0 + i;
-          const float* xr = X + row * ldx + lg * 16;
-          const bool rok = row < m, full = rok && lg * 16 + 16 <= n;
-          if (full) {
+          digits(task, tt, at, x);
+        }
+      } else {
+        // K-half producers: lane -> (row i = 8 w + (lane & 7), 16-column group lg' = lane >> 3 of
+        // each half); each task holds its row's columns 16 lg' .. + 15 of both halves, so the row
+        // exponent (max over the row: lanes xor 8, 16) is known before either half is written.
+        // Software-pipelined: the loads of a half of tile t + 1 are issued as soon as the digits of
+        // that half of tile t are written, so HBM latency overlaps the waits for free half slots.
+        const int dw = warp - (2 + QT_RWARPS), lgp = lane >> 3;
+        auto load_half = [&](int t2, int h, float (&xo)[2][16]) {
+          const int64_t r0 = (blockIdx.x + (int64_t)t2 * gridDim.x) * QT_M;
 #pragma unroll
-            for (int c = 0; c < 16; c += 4) {
-              const float4 f = *reinterpret_cast<const float4*>(xr + c);
-              x[c] = f.x; x[c + 1] = f.y; x[c + 2] = f.z; x[c + 3] = f.w;
+          for (int b = 0; b < 2; ++b) {
+            const int64_t row = r0 + (dw + QT_DWARPS * b) * 8 + (lane & 7);
+            const int c0 = 64 * h + 16 * lgp;
+            const float* xr = X + row * ldx + c0;
+            if (row < m && c0 + 16 <= n) {
+#pragma unroll
+              for (int c = 0; c < 16; c += 4) {
+                const float4 f = __ldg(reinterpret_cast<const float4*>(xr + c));
+                xo[b][c] = f.x; xo[b][c + 1] = f.y; xo[b][c + 2] = f.z; xo[b][c + 3] = f.w;
+              }
+            } else {
+#pragma unroll
+              for (int c = 0; c < 16; ++c) xo[b][c] = (row < m && c0 + c < n) ? xr[c] : 0.0f;
             }
-          } else {
+          }
+        };
+        if (tt == 0) { load_half(0, 0, xh0); load_half(0, 1, xh1); }
+        int ee[2];
 #pragma unroll
-            for (int c = 0; c < 16; ++c) x[c] = (rok && lg * 16 + c < n) ? xr[c] : 0.0f;
+        for (int h = 0; h < 2; ++h) {
+          const int u = 2 * tt + h, sh = u % NSLOT;
+          if (u >= NSLOT) tc::mbar_wait(&dempty[sh], (uint32_t)(((u / NSLOT) - 1) & 1));
+          float (&xc)[2][16] = h == 0 ? xh0 : xh1;
+          if (h == 0) {
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+              uint32_t mx = 0u;
+#pragma unroll
+              for (int c = 0; c < 16; ++c)
+                mx = max(mx, max(__float_as_uint(xh0[b][c]) & 0x7FFFFFFFu, __float_as_uint(xh1[b][c]) & 0x7FFFFFFFu));
+              mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+              mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+              ee[b] = mx == 0u ? 0 : (mx < 0x00800000u ? -126 : (int)(mx >> 23) - 126);
+              if (lgp == 0) rexp[(tt & 3) * QT_M + (dw + QT_DWARPS * b) * 8 + (lane & 7)] = ee[b];
+            }
+          }
+          unsigned char* ah = abase + (size_t)sh * SLOT;
+          if (!(dbg & 2)) {
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {
+              uint32_t W[QT_DA][4];
+              digit_words(xc[b], ee[b], W);
+              const int i = (dw + QT_DWARPS * b) * 8 + (lane & 7);
+#pragma unroll
+              for (int a = 0; a < QT_DA; ++a)
+                *reinterpret_cast<uint4*>(ah + a * H_TILE + lgp * (QT_M * 16) + i * 16) =
+                    make_uint4(W[a][0], W[a][1], W[a][2], W[a][3]);
+            }
+          }
+          if (tt + 1 < my_tiles) load_half(tt + 1, h, xc);      // next tile's half, in flight early
+          if (h == 0) {                                  // the second half is published below
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&dfull[sh]);
           }
         }
-        uint32_t mx = 0u;
-#pragma unroll
-        for (int c = 0; c < 16; ++c) mx = max(mx, __float_as_uint(x[c]) & 0x7FFFFFFFu);
-        for (int o = rpw; o < 32; o <<= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        // e_i: smallest e with max |x| < 2^e (finite input assumed: the sketch rejected NaN/Inf)
-        const int e = mx == 0u ? 0 : (mx < 0x00800000u ? -126 : (int)(mx >> 23) - 126);
-        const double sx = ldexp(1.0, 128 + 46 - e);
-        if (lg == 0) rexp[s * QT_M + i] = e;
-        uint32_t W[QT_DA][4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint32_t hw[4], lw[4];
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint32_t ub = __float_as_uint(x[q * 4 + kk]);
-            const uint32_t h = ((uint32_t)((int32_t)ub >> 3) & 0x8FFFFFFFu) | 0x30000000u;   // x 2^-128
-            const double t = fma(__hiloint2double((int)h, (int)(ub << 29)), sx, kMagic + (double)0x8080808080ull);
-            hw[kk] = (uint32_t)__double2hiint(t);                                              // F + C, 48 bits
-            lw[kk] = (uint32_t)__double2loint(t);
-          }
-          uint32_t H[4], L[4];
-          transpose4(hw[0], hw[1], hw[2], hw[3], H);
-          transpose4(lw[0], lw[1], lw[2], lw[3], L);
-          W[0][q] = H[1]; W[1][q] = H[0] ^ 0x80808080u;
-          W[2][q] = L[3] ^ 0x80808080u; W[3][q] = L[2] ^ 0x80808080u;
-          W[4][q] = L[1] ^ 0x80808080u; W[5][q] = L[0] ^ 0x80808080u;
-        }
-#pragma unroll
-        for (int a = 0; a < QT_DA; ++a)
-          *reinterpret_cast<uint4*>(at + a * QT_A_TILE + lg * (QT_M * 16) + i * 16) =
-              make_uint4(W[a][0], W[a][1], W[a][2], W[a][3]);
       }
+      const int sdone = Cf::HALF ? (2 * tt + 1) % NSLOT : s;
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       __syncwarp();
-      if (lane == 0) { tc::mbar_arrive(&dfull[s]); if (Cf::TMA_RAW) tc::mbar_arrive(&rempty[sr]); }
+      if (lane == 0) { tc::mbar_arrive(&dfull[sdone]); if (Cf::TMA_RAW) tc::mbar_arrive(&rempty[sr]); }
     }
   }
   if (warp >= 2 && warp < 2 + QT_RWARPS && lane == 0) tc::bulk_wait0();   // Q stores complete before exit
@@ -360,11 +510,11 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
-// n <= 64 by default; 64 < n <= 128 (plain-load producers, one digit stage) is correct but not yet
-// faster than the DMMA substitution on B200 (C2: 0.80 vs 0.69 ms), so it is opt-in.
+// fp32 X, n <= 128 (RCHOLQR_SOLVE_DMMA=1 selects the DMMA substitution instead).  At C2 (n = 100)
+// the digit solve with its prep takes 0.54 ms against the DMMA kernel's 0.70 ms.
 bool solve_tc_applicable(int dtype, int n) {
   if (dtype != RCHOLQR_F32 || n < 1 || getenv("RCHOLQR_SOLVE_DMMA")) return false;
-  return n <= 64 || (n <= QT_KMAX_ALL && getenv("RCHOLQR_SOLVE_TC128"));
+  return n <= QT_KMAX_ALL;
 }
 
 bool solve_tc_supported(const void* X, int64_t m, int64_t ldx, const void* Q, int64_t ldq) {
@@ -396,7 +546,7 @@ cudaError_t launch_solve_tc(const double* Winv, int n, const float* X, int64_t m
   const int groups = (n + QT_G - 1) / QT_G;
   int8_t* wdig = reinterpret_cast<int8_t*>(ws);
   int* wexp = reinterpret_cast<int*>(wdig + qt_woff(QT_KMAX_ALL / QT_G));
-  solve_tc_prep_kernel<<<1, groups * QT_G, 0, st>>>(Winv, n, kpad, wdig, wexp, status);
+  solve_tc_prep_kernel<<<groups * QT_G, kpad, 0, st>>>(Winv, n, kpad, wdig, wexp, status);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   CUtensorMap map;
@@ -410,9 +560,10 @@ cudaError_t launch_solve_tc(const double* Winv, int n, const float* X, int64_t m
   CUtensorMap qmapd;
   const cuuint64_t qdims[2] = {(cuuint64_t)n, (cuuint64_t)m};
   const cuuint64_t qstrides[1] = {(cuuint64_t)ldq * 4};
-  const cuuint32_t qbox[2] = {QT_G, 32};
+  const bool half = kpad > 64;                       // QCfg<128>::HALF: 8-column store boxes
+  const cuuint32_t qbox[2] = {half ? 8u : (cuuint32_t)QT_G, 32};
   if (enc(&qmapd, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Q, qdims, qstrides, qbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-          CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+          half ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   const int64_t ntiles = (m + QT_M - 1) / QT_M;
   const int grid = (int)std::min<int64_t>(ntiles, sms);

@@ -49,6 +49,48 @@ tri_inverse_kernel(const double* __restrict__ R, int n, double* __restrict__ W, 
   for (int j = lane; j < n; j += 32) W[(size_t)i * n + j] = w[j];
 }
 
+// Same W for n <= 128 (the tcgen05 digit solve's prep): R staged once per CTA in shared memory and
+// the substitution done right-looking -- lane c keeps the residual s_c of w_i R = e_i for columns
+// c = lane + 32 q; at step j the owner lane's s_j is final, w_ij = s_j / R_jj is broadcast and every
+// lane updates s_c -= w_ij R_jc (c > j).  One shuffle + one division per step instead of a global
+// load chain and a 5-step shuffle reduction; the diagonal reciprocals are taken once, so a step is
+// a shuffle, a multiply and the lane's FMAs (0.074 ms -> a few us at n = 100).
+constexpr int INVS_WARPS = 8;
+__global__ void __launch_bounds__(32 * INVS_WARPS)
+tri_inverse_small_kernel(const double* __restrict__ R, int n, double* __restrict__ W, const int* status) {
+  if (*status) return;
+  extern __shared__ __align__(16) double rsm[];        // R, n x n; then 1 / R_jj
+  double* dinv = rsm + (size_t)n * n;
+#pragma unroll 8
+  for (int t = threadIdx.x; t < n * n; t += blockDim.x) rsm[t] = R[t];     // unrolled: loads batched
+  for (int t = threadIdx.x; t < n; t += blockDim.x) dinv[t] = 1.0 / R[(size_t)t * n + t];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * INVS_WARPS + warp;
+  if (i >= n) return;
+  double s[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) s[q] = (lane + 32 * q == i) ? 1.0 : 0.0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    for (int jj = 0; jj < 32; ++jj) {
+      const int j = 32 * q + jj;
+      if (j >= n) break;
+      if (j < i) continue;                               // w_ij = 0 below the diagonal
+      const double z = __shfl_sync(0xffffffffu, s[q], jj) * dinv[j];   // w_ij (reciprocal: W is fp64 to ~1 ulp)
+      if (lane == jj) s[q] = z;
+#pragma unroll
+      for (int q2 = q; q2 < 4; ++q2) {
+        const int c = lane + 32 * q2;
+        if (c > j && c < n) s[q2] = fma(-z, rsm[(size_t)j * n + c], s[q2]);
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+    if (lane + 32 * q < n) W[(size_t)i * n + lane + 32 * q] = s[q];
+}
+
 // --------------------------------------------------------------------------------------------
 constexpr int KCT = 16;  // K rows of W per pipeline chunk
 
@@ -233,6 +275,13 @@ cudaError_t launch_trsm(const TrsmLaunch& L, const void* X, int dtype, int64_t m
 }
 
 cudaError_t launch_tri_inverse(const double* R, int n, double* W, int* status, cudaStream_t st) {
+  if (n <= 128 && !getenv("RCHOLQR_TRI_INVERSE_OLD")) {
+    const size_t sm = sizeof(double) * (size_t)n * (n + 1);
+    cudaError_t e = cudaFuncSetAttribute(tri_inverse_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    tri_inverse_small_kernel<<<(n + INVS_WARPS - 1) / INVS_WARPS, 32 * INVS_WARPS, sm, st>>>(R, n, W, status);
+    return cudaGetLastError();
+  }
   const size_t smem = sizeof(double) * (size_t)n * INV_WARPS;
   cudaError_t e = cudaFuncSetAttribute(tri_inverse_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

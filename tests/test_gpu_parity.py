@@ -233,13 +233,14 @@ SOLVE_TC_CASES = [
     (5_000, 128, 3, None),       # four full groups
     (3_001, 97, 4, 104),         # strided, ragged last group
     (1, 100, 1, None),           # single row
+    (50_001, 80, 4, None),       # K padded to 96: 6 column groups of 16 per row (not a power of two)
+    (777, 65, 2, None),          # n just above 64
+    (12_345, 96, 3, None),       # three full groups
 ]
 
 
 @pytest.mark.parametrize("m,n,c,ldx", SOLVE_TC_CASES)
 def test_tri_solve_tc_parity(cuda, monkeypatch, m, n, c, ldx):
-    if n > 64:
-        monkeypatch.setenv("RCHOLQR_SOLVE_TC128", "1")   # opt-in path for 64 < n <= 128
     X = synth.make_X(max(m, n), n, c, "f32")
     Ro, _, _ = oracle.householder(oracle.sketch(X, 2 * n))
     X = X[:m]
@@ -257,12 +258,13 @@ def test_tri_solve_tc_parity(cuda, monkeypatch, m, n, c, ldx):
     assert np.all(err <= 4 * U32 * np.abs(Qo.astype(np.float64)).max(axis=1) + 1e-30)
 
 
-def test_tri_solve_tc_matches_dmma(cuda, monkeypatch):
-    X = synth.make_X(200_000, 64, 4.0, "f32")
-    Ro, _, _ = oracle.householder(oracle.sketch(X[:20_000], 128))
-    a = _np(_plan(64, 128, "f32").tri_solve(_t(X), _t(Ro)))
+@pytest.mark.parametrize("n", [64, 100])
+def test_tri_solve_tc_matches_dmma(cuda, monkeypatch, n):
+    X = synth.make_X(200_000, n, 4.0, "f32")
+    Ro, _, _ = oracle.householder(oracle.sketch(X[:20_000], 2 * n))
+    a = _np(_plan(n, 2 * n, "f32").tri_solve(_t(X), _t(Ro)))
     monkeypatch.setenv("RCHOLQR_SOLVE_DMMA", "1")
-    b = _np(_plan(64, 128, "f32").tri_solve(_t(X), _t(Ro)))
+    b = _np(_plan(n, 2 * n, "f32").tri_solve(_t(X), _t(Ro)))
     assert _rel(a, b) <= 4 * U32, _rel(a, b)
 
 
