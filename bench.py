@@ -356,15 +356,23 @@ def run(args):
                            "frac": ach / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
                            "algorithmic": f"2*m*r*s_x = {byts:.4g} B (read r columns, write them packed)",
                            "traffic": None}
-        flops = float(m_local) * r_rr * r_rr
-        ach = flops / (per_ms["solve"] * 1e-3) / 1e12
-        roofs["solve"] = {"kernel": "blocked substitution (fp64 DMMA), r columns", "bound": "tensor", "achieved": ach,
-                          "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
-                          "peak_source": "FP64 DMMA peak 37.2 TF", "algorithmic": f"m*r^2 = {flops:.4g} flop",
-                          "traffic": None}
+        if dt == "f32" and r_rr <= 128 and not os.environ.get("RCHOLQR_SOLVE_DMMA"):
+            byts = 2.0 * m_local * r_rr * s_x
+            ach = byts / (per_ms["solve"] * 1e-3) / 1e9
+            roofs["solve"] = {"kernel": "solve_tc_kernel, r columns", "bound": "hbm", "achieved": ach, "peak": hbm,
+                              "unit": "GB/s", "frac": ach / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                              "algorithmic": f"2*m*r*s_x = {byts:.4g} B (read the packed columns, write Q)",
+                              "traffic": None}
+        else:
+            flops = float(m_local) * r_rr * r_rr
+            ach = flops / (per_ms["solve"] * 1e-3) / 1e12
+            roofs["solve"] = {"kernel": "blocked substitution (fp64 DMMA), r columns", "bound": "tensor",
+                              "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                              "frac": ach / DMMA_PEAK_TFLOPS, "peak_source": "FP64 DMMA peak 37.2 TF",
+                              "algorithmic": f"m*r^2 = {flops:.4g} flop", "traffic": None}
         per_ms = {"sketch": per_ms["sketch"], "colnorms": per_ms["reduce"], "allreduce": per_ms["allreduce"],
                   "rrqr": per_ms["small_qr"], "gather": per_ms["tri_prep"], "solve": per_ms["solve"]}
-    elif dt == "f32" and n <= 64:
+    elif dt == "f32" and n <= 128 and not os.environ.get("RCHOLQR_SOLVE_DMMA"):   # tcgen05 digit solve
         byts = 2.0 * m_local * n * s_x
         ach = byts / (per_ms["solve"] * 1e-3) / 1e9
         roofs["solve"] = {"kernel": "solve_tc_kernel", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
