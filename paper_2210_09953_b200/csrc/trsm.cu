@@ -61,8 +61,20 @@ tri_inverse_small_kernel(const double* __restrict__ R, int n, double* __restrict
   if (*status) return;
   extern __shared__ __align__(16) double rsm[];        // R, n x n; then 1 / R_jj
   double* dinv = rsm + (size_t)n * n;
-#pragma unroll 8
-  for (int t = threadIdx.x; t < n * n; t += blockDim.x) rsm[t] = R[t];     // unrolled: loads batched
+  const int nn = n * n;
+  for (int t0 = 0; t0 < nn; t0 += 8 * (int)blockDim.x) {                 // 8 loads in flight per thread
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int t = t0 + u * (int)blockDim.x + (int)threadIdx.x;
+      v[u] = t < nn ? R[t] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int t = t0 + u * (int)blockDim.x + (int)threadIdx.x;
+      if (t < nn) rsm[t] = v[u];
+    }
+  }
   for (int t = threadIdx.x; t < n; t += blockDim.x) dinv[t] = 1.0 / R[(size_t)t * n + t];
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
