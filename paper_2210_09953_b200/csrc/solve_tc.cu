@@ -22,11 +22,12 @@
 // W = R^{-1} is upper triangular, so column group g only needs rows l < 32 (g + 1): its digit
 // tile and its MMAs stop there (K_g = 32 (g + 1)).
 //
-// Roles (persistent CTAs, 18 warps): warp 0 lane 0 issues tcgen05.mma; warp 1 lane 0 stages the W
-// digits (cp.async.bulk) and, for n <= 64, the X tiles (one 2D TMA box of 128 rows x K+4 columns
-// per tile, two-stage ring); warps 2..9 drain TMEM in two sets of four (set d drains level buffer d,
-// one lane quadrant per warp) and write Q through swizzled shared memory with TMA stores; warps
-// 10..17 split X into digit planes (for 64 < n <= 128 they read X with plain loads into registers
+// Roles (persistent CTAs; 26 warps for n <= 64, 18 above): warp 0 lane 0 issues tcgen05.mma; warp 1
+// lane 0 stages the W digits (cp.async.bulk) and, for n <= 64, the X tiles (one 2D TMA box of 128
+// rows x K+4 columns per tile, two-stage ring); the next RW warps drain TMEM -- two sets (set d
+// drains level buffer d, one lane quadrant per warp), and for n <= 64 each set twice over (16 columns
+// per warp: the drain is bound by TMEM read concurrency, C4 solve 11.05 -> 10.02 ms) -- and write Q
+// through shared memory with TMA stores; the last 8 warps split X into digit planes (for 64 < n <= 128 they read X with plain loads into registers
 // and write the digits as two K-halves into a ring of three half slots: there is no room for a raw
 // ring or a second full digit stage).
 #include <cuda_runtime.h>
@@ -48,8 +49,6 @@ constexpr int QT_LEV = 7;       // levels kept (a + b <= 6)
 constexpr int QT_NB = QT_DB * QT_G;             // stacked W digit rows of one group (224)
 constexpr int QT_DWARPS = 8;    // digit warps 10..17
 constexpr int QT_RWARPS = 8;    // drain warps 2..9: two sets of four (one per TMEM level buffer)
-constexpr int QT_THREADS = 32 * (2 + QT_RWARPS + QT_DWARPS);
-constexpr int QT_QS_BYTES = QT_RWARPS * 32 * QT_G * 4;  // Q staging: one 32-row x 32-col fp32 tile per drain warp (128B-swizzled)
 constexpr int QT_KMAX_ALL = 128;
 static_assert(2 * QT_LEV * QT_G <= 512, "two TMEM level buffers");
 
@@ -72,7 +71,12 @@ struct QCfg {
   static constexpr int NSLOT = HALF ? 3 : DIG;
   static constexpr int H_TILE = QT_M * 64;        // one digit plane of one K-half
   static constexpr int SLOT_BYTES = HALF ? QT_DA * H_TILE : QT_DA * A_TILE;
-  static constexpr int QS = HALF ? QT_RWARPS * 32 * 8 * 4 : QT_QS_BYTES;   // HALF: one 32-row x 8-column tile per drain warp
+  // n <= 64: 16 drain warps (two per lane quadrant per TMEM buffer, 16 columns each) -- the drain
+  // is bound by TMEM read concurrency; 64 < n <= 128: 8 (registers: the K-half producers need 96)
+  static constexpr int RW = TMA_RAW ? 16 : QT_RWARPS;
+  static constexpr int THREADS = 32 * (2 + RW + QT_DWARPS);
+  static constexpr int DCOLS = QT_G * 8 / RW;     // columns of a group per drain warp (16 or 32)
+  static constexpr int QS = HALF ? QT_RWARPS * 32 * 8 * 4 : RW * 32 * DCOLS * 4;   // HALF: 32 x 8 tile per drain warp
   static constexpr size_t SMEM =
       (size_t)W_BYTES + (size_t)NSLOT * SLOT_BYTES + (size_t)RAW * RAW_STAGE + QS + 4096;
   static_assert(SMEM <= 232448, "shared memory");
@@ -115,7 +119,7 @@ solve_tc_prep_kernel(const double* __restrict__ W, int n, int kpad, int8_t* __re
 
 // ---------------------------------------------------------------------------------------------
 template <int KMAX>
-__global__ void __launch_bounds__(QT_THREADS, 1)
+__global__ void __launch_bounds__(QCfg<KMAX>::THREADS, 1)
 solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap qmap,
                 const int8_t* __restrict__ wdig, const int* __restrict__ wexp, const float* __restrict__ X,
                 int64_t ldx, int64_t m, int n, int kpad, float* __restrict__ Q, int64_t ldq, const int* status,
@@ -154,7 +158,7 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
   if (tid == 0) {
     for (int s = 0; s < NSLOT; ++s) { tc::mbar_init(&dfull[s], QT_DWARPS); tc::mbar_init(&dempty[s], 1); }
     for (int s = 0; s < QT_RAW; ++s) { tc::mbar_init(&rfull[s], 1); tc::mbar_init(&rempty[s], QT_DWARPS); }
-    for (int b = 0; b < 2; ++b) { tc::mbar_init(&tready[b], 1); tc::mbar_init(&tfree[b], 4); }
+    for (int b = 0; b < 2; ++b) { tc::mbar_init(&tready[b], 1); tc::mbar_init(&tfree[b], Cf::RW / 2); }
     tc::mbar_init(wbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -232,9 +236,11 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
       }
       __syncwarp();
     }
-  } else if (warp < 2 + QT_RWARPS) {
+  } else if (warp < 2 + Cf::RW) {
     // ---------------------------------------------------------------- drain (set = buffer, lane quadrant)
-    const int dset = (warp - 2) >> 2, dq = warp & 3, row_l = dq * 32 + lane;
+    // set = buffer (warps 2..5, 6..9, then again for the second column half when RW = 16)
+    const int dset = ((warp - 2) >> 2) & 1, dq = warp & 3, row_l = dq * 32 + lane;
+    const int dc0 = ((warp - 2) >> 3) * Cf::DCOLS;     // first column of the group this warp drains
     const uint32_t lb = tmem + ((uint32_t)(dq * 32) << 16);
     for (int tt = 0; tt < my_tiles; ++tt) {
       for (int g = 0; g < groups; ++g) {
@@ -297,14 +303,15 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
           }
           continue;
         }
-        double v[QT_G];
-        const uint32_t lv = lb + buf * (QT_LEV * QT_G);
+        constexpr int DC = Cf::DCOLS;
+        double v[DC];
+        const uint32_t lv = lb + buf * (QT_LEV * QT_G) + dc0;
         if (dbg & 4) {
 #pragma unroll
-          for (int c = 0; c < QT_G; ++c) v[c] = 0.0;
+          for (int c = 0; c < DC; ++c) v[c] = 0.0;
         } else
 #pragma unroll
-        for (int h = 0; h < QT_G / 8; ++h) {
+        for (int h = 0; h < DC / 8; ++h) {
           uint32_t p[4][8];
 #pragma unroll
           for (int pp = 0; pp < 3; ++pp) {
@@ -336,22 +343,24 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
           // stage this warp's 32 rows x 32 columns (fp32) in shared memory with the 128-byte swizzle
           // (16-byte chunk c of row r at chunk c ^ (r & 7): conflict-free STS.128), then one 2D TMA
           // store writes them; TMA clips rows >= m and columns >= n.
-          unsigned char* qs = qstage + (warp - 2) * (32 * QT_G * 4);
+          unsigned char* qs = qstage + (warp - 2) * (32 * DC * 4);
           if (lane == 0) tc::bulk_wait_read0();              // previous store finished reading the tile
           __syncwarp();
 #pragma unroll
-          for (int c = 0; c < QT_G; c += 4) {
+          for (int c = 0; c < DC; c += 4) {
             float o4[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {   // exact power-of-two scale 2^(e_i - 46 + e_j - 54 + 40)
-              o4[q] = __double2float_rn(v[c + q] * si * wsc[g * QT_G + c + q]);   // v carries 256^(6-L)
+              o4[q] = __double2float_rn(v[c + q] * si * wsc[g * QT_G + dc0 + c + q]);   // v carries 256^(6-L)
             }
-            *reinterpret_cast<float4*>(qs + lane * 128 + (((c >> 2) ^ (lane & 7)) << 4)) = make_float4(o4[0], o4[1], o4[2], o4[3]);
+            // 32-column rows: 128-byte swizzle (conflict-free); 16-column rows: plain 64-byte rows
+            const int off = DC == 32 ? lane * 128 + (((c >> 2) ^ (lane & 7)) << 4) : lane * (DC * 4) + c * 4;
+            *reinterpret_cast<float4*>(qs + off) = make_float4(o4[0], o4[1], o4[2], o4[3]);
           }
           asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
           __syncwarp();
           if (lane == 0) {
-            tc::tma_store_2d(&qmap, qs, g * QT_G, (int)((blockIdx.x + (int64_t)tt * gridDim.x) * QT_M + dq * 32));
+            tc::tma_store_2d(&qmap, qs, g * QT_G + dc0, (int)((blockIdx.x + (int64_t)tt * gridDim.x) * QT_M + dq * 32));
             tc::bulk_commit();
           }
         }
@@ -365,7 +374,7 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
     // rounded up to a power of two (lg_map) for the shuffle max; groups >= lg_n read zeros.
     // Plain-load producers (64 < n <= 128) issue the loads of all their tasks of a tile before
     // waiting for the digit slot, so the HBM latency overlaps the MMAs of the tile before.
-    const int dt = tid - 32 * (2 + QT_RWARPS);
+    const int dt = tid - 32 * (2 + Cf::RW);
     const int lg_map = lg_n <= 2 ? lg_n : (lg_n <= 4 ? 4 : 8), rpw = 32 / lg_map;
     const int ntask = (dbg & 2) ? 0 : QT_M * lg_map;
     auto task_pos = [&](int task, int& lg, int& i) {
@@ -437,7 +446,7 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
         // exponent (max over the row: lanes xor 8, 16) is known before either half is written.
         // Software-pipelined: the loads of a half of tile t + 1 are issued as soon as the digits of
         // that half of tile t are written, so HBM latency overlaps the waits for free half slots.
-        const int dw = warp - (2 + QT_RWARPS), lgp = lane >> 3;
+        const int dw = warp - (2 + Cf::RW), lgp = lane >> 3;
         auto load_half = [&](int t2, int h, float (&xo)[2][16]) {
           const int64_t r0 = (blockIdx.x + (int64_t)t2 * gridDim.x) * QT_M;
 #pragma unroll
@@ -504,7 +513,7 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
       if (lane == 0) { tc::mbar_arrive(&dfull[sdone]); if (Cf::TMA_RAW) tc::mbar_arrive(&rempty[sr]); }
     }
   }
-  if (warp >= 2 && warp < 2 + QT_RWARPS && lane == 0) tc::bulk_wait0();   // Q stores complete before exit
+  if (warp >= 2 && warp < 2 + Cf::RW && lane == 0) tc::bulk_wait0();   // Q stores complete before exit
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
@@ -561,20 +570,22 @@ cudaError_t launch_solve_tc(const double* Winv, int n, const float* X, int64_t m
   const cuuint64_t qdims[2] = {(cuuint64_t)n, (cuuint64_t)m};
   const cuuint64_t qstrides[1] = {(cuuint64_t)ldq * 4};
   const bool half = kpad > 64;                       // QCfg<128>::HALF: 8-column store boxes
-  const cuuint32_t qbox[2] = {half ? 8u : (cuuint32_t)QT_G, 32};
+  const int dcols = QCfg<64>::DCOLS;                 // n <= 64: columns per drain warp
+  const cuuint32_t qbox[2] = {half ? 8u : (cuuint32_t)dcols, 32};
   if (enc(&qmapd, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Q, qdims, qstrides, qbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-          half ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+          (half || dcols != 32) ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   const int64_t ntiles = (m + QT_M - 1) / QT_M;
   const int grid = (int)std::min<int64_t>(ntiles, sms);
   static const int dbg = getenv("RCHOLQR_QTC_DEBUG") ? atoi(getenv("RCHOLQR_QTC_DEBUG")) : 0;   // ablations only
-  auto go = [&](auto kern, size_t smem) -> cudaError_t {
+  auto go = [&](auto kern, size_t smem, int threads) -> cudaError_t {
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e2 != cudaSuccess) return e2;
-    kern<<<grid, QT_THREADS, smem, st>>>(map, qmapd, wdig, wexp, X, ldx, m, n, kpad, Q, ldq, status, dbg);
+    kern<<<grid, threads, smem, st>>>(map, qmapd, wdig, wexp, X, ldx, m, n, kpad, Q, ldq, status, dbg);
     return cudaGetLastError();
   };
-  return kpad <= 64 ? go(solve_tc_kernel<64>, QCfg<64>::SMEM) : go(solve_tc_kernel<128>, QCfg<128>::SMEM);
+  return kpad <= 64 ? go(solve_tc_kernel<64>, QCfg<64>::SMEM, QCfg<64>::THREADS)
+                    : go(solve_tc_kernel<128>, QCfg<128>::SMEM, QCfg<128>::THREADS);
 }
 
 }  // namespace rcq
