@@ -916,6 +916,10 @@ int oracle_factor_rr(const void* X, int dtype, int64_t m, int n, int64_t ldx, in
  * fixed-block order as oracle_sketch -- used to check sampled entries of full-size sketches. */
 double oracle_sketch_entry(const double* x, int64_t m, int64_t row_offset, int k, int sketch, int zeta,
                            uint64_t seed, int r) {
+    /* invalid arguments give NaN (the same rules as oracle_sketch: 0 <= r < k, sparse 1 <= zeta <= k, k % zeta == 0) */
+    if (k < 1 || r < 0 || r >= k || m < 0 || (m > 0 && !x)) return NAN;
+    if (sketch < OR_GAUSSIAN || sketch > OR_SRHT) return NAN;
+    if (sketch == OR_SPARSE_SIGN && (zeta < 1 || zeta > k || k % zeta != 0)) return NAN;
     int64_t nb = (m + OR_SKETCH_BLOCK - 1) / OR_SKETCH_BLOCK;
     uint64_t sr_r = 0;
     if (sketch == OR_SRHT) {
@@ -929,9 +933,10 @@ double oracle_sketch_entry(const double* x, int64_t m, int64_t row_offset, int k
     if (!part) return NAN;
     #pragma omp parallel for schedule(dynamic, 1)
     for (int64_t b = 0; b < nb; ++b) {
-        int32_t rows[64];
-        int8_t sg[64];
-        double acc = 0.0, cmp = 0.0;
+        int zc = sketch == OR_SPARSE_SIGN ? zeta : 1;
+        int32_t* rows = (int32_t*)malloc(sizeof(int32_t) * (size_t)zc);
+        int8_t* sg = (int8_t*)malloc((size_t)zc);
+        double acc = (rows && sg) ? 0.0 : NAN, cmp = 0.0;
         double sk = 1.0 / sqrt((double)k), sz = zeta > 0 ? 1.0 / sqrt((double)zeta) : 0.0;
         int64_t i0 = b * OR_SKETCH_BLOCK, i1 = i0 + OR_SKETCH_BLOCK < m ? i0 + OR_SKETCH_BLOCK : m;
         for (int64_t i = i0; i < i1; ++i) {
@@ -946,10 +951,12 @@ double oracle_sketch_entry(const double* x, int64_t m, int64_t row_offset, int k
                 dot2_add(&acc, &cmp, oracle_srht_sign(seed, sr_r, gi) > 0 ? sk : -sk, x[i]);
             } else {
                 oracle_sparse_col(seed, k, zeta, gi, rows, sg);
-                for (int t = 0; t < zeta && t < 64; ++t)
+                for (int t = 0; t < zeta; ++t)
                     if (rows[t] == r) dot2_add(&acc, &cmp, sg[t] > 0 ? sz : -sz, x[i]);
             }
         }
+        free(rows);
+        free(sg);
         part[2 * b] = acc;
         part[2 * b + 1] = cmp;
     }

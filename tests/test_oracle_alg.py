@@ -242,3 +242,45 @@ def test_factor_orthogonality_defect_scales_with_kappa():
     ob = oracle.factor(Xb, 40, seed=0)
     db = oracle.orth_defect(oracle.sketch(ob["Q"], 40, seed=0))
     assert 1e3 * da < db < 2 * 6.1 * U64 * 20**1.5 * 1e10
+
+
+# ------------------------------------------------------------------ sketch_entry (sampled checker)
+@pytest.mark.parametrize("sk,zeta", [(oracle.GAUSSIAN, 8), (oracle.SPARSE_SIGN, 8), (oracle.SPARSE_SIGN, 96)])
+def test_sketch_entry_exact_rational(sk, zeta):
+    # oracle_sketch_entry is the checker of the full-size GPU sketches (tests/test_gpu_parity.py).  Pin it
+    # to exact rational sums of the KAT-pinned Theta (theta_dense -> oracle_theta_gauss_z /
+    # oracle_theta_sparse) with a 64-bit row offset, inside the Dot2 bound (~2u |sum| + u^2 sum|terms|,
+    # PAPER.md:422 with u_f ~ u^2).  zeta = 96 > 64 exercises the heap buffers (no fixed rows[64]).
+    rng = np.random.default_rng(11)
+    m, k, off = 45, (192 if zeta == 96 else 24), 2**35 + 3
+    x = rng.standard_normal(m)
+    T = oracle.theta_dense(4, k, m, sketch=sk, zeta=zeta, row_offset=off)
+    for r in range(k):
+        got = oracle.sketch_entry(x, r, k, sketch=sk, zeta=zeta, seed=4, row_offset=off)
+        exact = sum(Fraction(float(T[r, i])) * Fraction(float(x[i])) for i in range(m))
+        mag = sum(abs(Fraction(float(T[r, i])) * Fraction(float(x[i]))) for i in range(m))
+        assert abs(Fraction(got) - exact) <= Fraction(2.0**-52) * abs(exact) + Fraction(2.0**-100) * mag \
+            + Fraction(1, 2**1074)
+
+
+@pytest.mark.parametrize("sk", [oracle.GAUSSIAN, oracle.SPARSE_SIGN, oracle.RADEMACHER])
+def test_sketch_entry_equals_sketch_across_blocks(sk):
+    # Same fixed 65,536-row blocks, same Dot2 order => the sampled checker reproduces the pinned
+    # oracle_sketch bitwise, over several blocks and with a row offset that is not a multiple of 32.
+    X = synth.make_X(2 * 65536 + 777, 5, 3.0, "f32")
+    k, off = 32, 1_000_003
+    P = oracle.sketch(X, k, sketch=sk, seed=7, row_offset=off)
+    for r in (0, 3, 17, 31):
+        for j in (0, 4):
+            x = np.ascontiguousarray(X[:, j], dtype=np.float64)
+            assert oracle.sketch_entry(x, r, k, sketch=sk, seed=7, row_offset=off) == P[r, j]
+
+
+def test_sketch_entry_rejects_bad_arguments():
+    x = np.ones(10)
+    for kw in [dict(r=-1, k=8), dict(r=8, k=8), dict(r=0, k=0),
+               dict(r=0, k=8, sketch=oracle.SPARSE_SIGN, zeta=0),
+               dict(r=0, k=10, sketch=oracle.SPARSE_SIGN, zeta=4),
+               dict(r=0, k=8, sketch=oracle.SPARSE_SIGN, zeta=9),
+               dict(r=0, k=8, sketch=7)]:
+        assert np.isnan(oracle.sketch_entry(x, **kw))
