@@ -233,6 +233,26 @@ int32_t rcholqr_launches_per_factor(rcholqr_plan plan, int64_t m_local);
 rcholqr_status rcholqr_set_timing(rcholqr_plan plan, int32_t enable);
 rcholqr_status rcholqr_last_timings(rcholqr_plan plan, float out_ms[6]);
 
+/* Which kernels served the last sketch / factor / solve call on this plan (a bit set; the parity
+ * tests assert with it that the tcgen05 kernels, not the guarded CUDA-core fallbacks, computed a
+ * result).  Bits accumulate over the steps of one call and are cleared when the next call starts:
+ *   SKETCH_TC        a tcgen05 sketch kernel ran (Gaussian digit, sparse-sign or dense +-1 E tile)
+ *   SKETCH_PRESPLIT  the Gaussian sketch took X from pre-split digit planes (xdig_split_kernel)
+ *   SKETCH_CUDA_CORE the sketch was computed by a CUDA-core / DMMA kernel alone (no tcgen05 kernel)
+ *   SKETCH_FALLBACK  a tcgen05 sketch raised its headroom-overflow flag and the guarded DMMA /
+ *                    CUDA-core kernel recomputed the partials (PAPER.md:423's u_f is kept either way)
+ *   SOLVE_TC         the tall solve ran on tcgen05 (fp32 X, n <= 128; solve_tc.cu)
+ *   SOLVE_DMMA       the tall solve ran on a blocked fp64 DMMA substitution kernel
+ * *out receives the bits.  SYNCHRONIZES on `stream` (reads the device overflow word).  Errors:
+ * E_INVALID for a NULL plan or out. */
+#define RCHOLQR_PATH_SKETCH_TC 1u
+#define RCHOLQR_PATH_SKETCH_PRESPLIT 2u
+#define RCHOLQR_PATH_SKETCH_CUDA_CORE 4u
+#define RCHOLQR_PATH_SKETCH_FALLBACK 8u
+#define RCHOLQR_PATH_SOLVE_TC 16u
+#define RCHOLQR_PATH_SOLVE_DMMA 32u
+rcholqr_status rcholqr_last_path(rcholqr_plan plan, uint32_t* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -36,7 +36,11 @@ SYMBOLS = ["rcholqr_create", "rcholqr_destroy", "rcholqr_factor", "rcholqr_facto
            "rcholqr_comm_create", "rcholqr_comm_destroy", "rcholqr_strerror", "rcholqr_version",
            "rcholqr_launches_per_factor", "rcholqr_set_timing", "rcholqr_last_timings", "rcholqr_factor2",
            "rcholqr_factor_reduced", "rcholqr_factor_rr", "rcholqr_factor_colmajor",
-           "rcholqr_factor_rr2"]
+           "rcholqr_factor_rr2", "rcholqr_last_path"]
+
+# rcholqr_last_path bits (include/rcholqr.h)
+PATH_SKETCH_TC, PATH_SKETCH_PRESPLIT, PATH_SKETCH_CUDA_CORE, PATH_SKETCH_FALLBACK = 1, 2, 4, 8
+PATH_SOLVE_TC, PATH_SOLVE_DMMA = 16, 32
 
 
 class _Desc(ctypes.Structure):
@@ -92,6 +96,7 @@ def load_library():
             "rcholqr_launches_per_factor": ([V, I64], I32),
             "rcholqr_set_timing": ([V, I32], I32),
             "rcholqr_last_timings": ([V, V], I32),
+            "rcholqr_last_path": ([V, ctypes.POINTER(ctypes.c_uint32), V], I32),
         }
         for name, (argt, rest) in sig.items():
             f = getattr(lib, name)
@@ -176,10 +181,30 @@ class RCholQR:
     def _dev(self):
         return _torch().device("cuda", self.device)
 
+    def _check_out(self, t, name, rows, cols, dtype, cuda=True, exact=False):
+        """Validate a caller-supplied output buffer before its raw pointer reaches the C ABI: device
+        (the plan's CUDA device, or CPU for the host entry point), dtype, 2-D, at least rows x cols,
+        stride(1) == 1 (exact=True: exactly rows x cols and contiguous -- buffers without a leading
+        dimension in the ABI).  Returns its leading dimension."""
+        if t is None:
+            return cols
+        ok_dev = (t.is_cuda and t.device.index == self.device) if cuda else (not t.is_cuda)
+        if not ok_dev or t.dtype != dtype or t.dim() != 2:
+            where = f"cuda:{self.device}" if cuda else "cpu"
+            raise ValueError(f"{name} must be a 2-D {dtype} tensor on {where}")
+        if exact:
+            if tuple(t.shape) != (rows, cols) or not t.is_contiguous():
+                raise ValueError(f"{name} must be a contiguous ({rows}, {cols}) tensor")
+            return cols
+        if t.shape[0] < rows or t.shape[1] < cols or (rows > 0 and t.stride(1) != 1):
+            raise ValueError(f"{name} must have shape >= ({rows}, {cols}) with stride(1) == 1")
+        return max(t.stride(0), cols) if rows > 1 else cols
+
     def _check_x(self, X):
         torch = _torch()
-        if not (X.is_cuda and X.dtype == self.dtype and X.dim() == 2 and X.shape[1] == self.n):
-            raise ValueError(f"X must be a CUDA {self.dtype} tensor of shape (m, {self.n})")
+        if not (X.is_cuda and X.device.index == self.device and X.dtype == self.dtype and X.dim() == 2
+                and X.shape[1] == self.n):
+            raise ValueError(f"X must be a cuda:{self.device} {self.dtype} tensor of shape (m, {self.n})")
         if X.stride(1) != 1:
             raise ValueError("X must be row-major (stride(1) == 1)")
         return X.shape[0], max(X.stride(0), self.n) if X.shape[0] > 1 else self.n
@@ -194,9 +219,11 @@ class RCholQR:
         R = torch.empty((self.n, self.n), dtype=torch.float64, device=X.device) if R is None else R
         if want_S and S is None:
             S = torch.empty((self.k, self.n), dtype=torch.float64, device=X.device)
+        ldq = self._check_out(Q, "Q", m, self.n, self.dtype)
+        self._check_out(R, "R", self.n, self.n, torch.float64, exact=True)
+        self._check_out(S, "S", self.k, self.n, torch.float64, exact=True)
         fn = self._lib.rcholqr_factor if sync else self._lib.rcholqr_factor_async
-        st = fn(self._h, _ptr(X), m, row_offset, ldx, _ptr(Q), Q.stride(0) if m > 1 else self.n, _ptr(R),
-                _ptr(S), _stream_ptr(stream))
+        st = fn(self._h, _ptr(X), m, row_offset, ldx, _ptr(Q), ldq, _ptr(R), _ptr(S), _stream_ptr(stream))
         _check(st, "rcholqr_factor")
         return Q, R, S
 
@@ -226,9 +253,11 @@ class RCholQR:
         R = torch.empty((self.n, self.n), dtype=torch.float64, device=X.device) if R is None else R
         if Rprime is None:
             Rprime = torch.empty((self.n, self.n), dtype=torch.float64, device=X.device)
-        st = self._lib.rcholqr_factor2(self._h, _ptr(X), m, row_offset, ldx, _ptr(Q),
-                                       Q.stride(0) if m > 1 else self.n, _ptr(R), _ptr(Rprime), int(bool(implicit)),
-                                       _stream_ptr(stream))
+        ldq = self._check_out(Q, "Q", m, self.n, self.dtype)
+        self._check_out(R, "R", self.n, self.n, torch.float64, exact=True)
+        self._check_out(Rprime, "Rprime", self.n, self.n, torch.float64, exact=True)
+        st = self._lib.rcholqr_factor2(self._h, _ptr(X), m, row_offset, ldx, _ptr(Q), ldq, _ptr(R), _ptr(Rprime),
+                                       int(bool(implicit)), _stream_ptr(stream))
         _check(st, "rcholqr_factor2")
         return Q, R, Rprime
 
@@ -244,6 +273,8 @@ class RCholQR:
             S = torch.empty((self.k, self.n), **f64)
         if want_Y and Y is None:
             Y = torch.empty((l, self.n), **f64)
+        for t, name, rows in ((Z, "Z", l), (R, "R", self.n), (S, "S", self.k), (Y, "Y", l)):
+            self._check_out(t, name, rows, self.n, torch.float64, exact=True)
         st = self._lib.rcholqr_factor_reduced(self._h, _ptr(X), m, row_offset, ldx, int(l), _ptr(Z), _ptr(R),
                                               _ptr(S), _ptr(Y), _stream_ptr(stream))
         _check(st, "rcholqr_factor_reduced")
@@ -260,9 +291,11 @@ class RCholQR:
         perm = torch.empty(self.n, dtype=torch.int32, device=X.device)
         D = torch.empty(self.n, dtype=torch.float64, device=X.device)
         S = torch.empty((self.k, self.n), dtype=torch.float64, device=X.device) if want_S else None
+        ldq = self._check_out(Q, "Q", m, self.n, self.dtype)
+        self._check_out(R, "R", self.n, self.n, torch.float64, exact=True)
         rank, swaps = ctypes.c_int32(0), ctypes.c_int32(0)
         st = self._lib.rcholqr_factor_rr(self._h, _ptr(X), m, row_offset, ldx, float(tau), float(f), int(rank_fixed),
-                                         _ptr(Q), Q.stride(0) if m > 1 else self.n, _ptr(R), _ptr(perm), _ptr(D),
+                                         _ptr(Q), ldq, _ptr(R), _ptr(perm), _ptr(D),
                                          _ptr(S), ctypes.byref(rank), ctypes.byref(swaps), _stream_ptr(stream))
         _check(st, "rcholqr_factor_rr")
         r = rank.value
@@ -281,8 +314,9 @@ class RCholQR:
         perm = torch.empty(self.n, dtype=torch.int32, device=X.device)
         D = torch.empty(self.n, **f64)
         rank, swaps = ctypes.c_int32(0), ctypes.c_int32(0)
+        ldq = self._check_out(Q, "Q", m, self.n, self.dtype)
         st = self._lib.rcholqr_factor_rr2(self._h, _ptr(X), m, row_offset, ldx, float(tau), float(f), int(rank_fixed),
-                                          _ptr(Q), Q.stride(0) if m > 1 else self.n, _ptr(R), _ptr(Rp), _ptr(perm),
+                                          _ptr(Q), ldq, _ptr(R), _ptr(Rp), _ptr(perm),
                                           _ptr(D), ctypes.byref(rank), ctypes.byref(swaps), _stream_ptr(stream))
         _check(st, "rcholqr_factor_rr2")
         r = rank.value
@@ -303,8 +337,11 @@ class RCholQR:
         R_host = torch.empty((self.n, self.n), dtype=torch.float64, pin_memory=True) if R_host is None else R_host
         if want_S and S_host is None:
             S_host = torch.empty((self.k, self.n), dtype=torch.float64, pin_memory=True)
+        ldq = self._check_out(Q_host, "Q_host", m, self.n, self.dtype, cuda=False)
+        self._check_out(R_host, "R_host", self.n, self.n, torch.float64, cuda=False, exact=True)
+        self._check_out(S_host, "S_host", self.k, self.n, torch.float64, cuda=False, exact=True)
         st = self._lib.rcholqr_factor_host(self._h, _ptr(X_host), m, row_offset, max(X_host.stride(0), self.n),
-                                           _ptr(Q_host), self.n, _ptr(R_host), _ptr(S_host), _stream_ptr(stream))
+                                           _ptr(Q_host), ldq, _ptr(R_host), _ptr(S_host), _stream_ptr(stream))
         _check(st, "rcholqr_factor_host")
         return Q_host, R_host, S_host
 
@@ -313,6 +350,7 @@ class RCholQR:
         torch = _torch()
         m, ldx = self._check_x(X)
         P = torch.empty((self.k, self.n), dtype=torch.float64, device=X.device) if P is None else P
+        self._check_out(P, "P", self.k, self.n, torch.float64, exact=True)
         _check(self._lib.rcholqr_sketch(self._h, _ptr(X), m, row_offset, ldx, _ptr(P), _stream_ptr(stream)),
                "rcholqr_sketch")
         return P
@@ -333,13 +371,21 @@ class RCholQR:
         m, ldx = self._check_x(X)
         R = R.contiguous()
         Q = torch.empty((m, self.n), dtype=self.dtype, device=X.device) if Q is None else Q
-        _check(self._lib.rcholqr_tri_solve(self._h, _ptr(X), m, ldx, _ptr(R), _ptr(Q), self.n,
+        ldq = self._check_out(Q, "Q", m, self.n, self.dtype)
+        self._check_out(R, "R", self.n, self.n, torch.float64, exact=True)
+        _check(self._lib.rcholqr_tri_solve(self._h, _ptr(X), m, ldx, _ptr(R), _ptr(Q), ldq,
                                            _stream_ptr(stream)), "rcholqr_tri_solve")
         return Q
 
     # -- introspection
     def launches_per_factor(self, m: int) -> int:
         return int(self._lib.rcholqr_launches_per_factor(self._h, m))
+
+    def last_path(self, stream=None) -> int:
+        """RCHOLQR_PATH_* bits of the kernels that served the last call (rcholqr_last_path)."""
+        out = ctypes.c_uint32(0)
+        _check(self._lib.rcholqr_last_path(self._h, ctypes.byref(out), _stream_ptr(stream)), "rcholqr_last_path")
+        return int(out.value)
 
     def set_timing(self, enable: bool = True):
         _check(self._lib.rcholqr_set_timing(self._h, int(enable)), "rcholqr_set_timing")

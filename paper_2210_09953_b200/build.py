@@ -1,17 +1,31 @@
-"""Build the in-tree CUDA library ``lib/librcholqr.so`` for sm_100a (nvcc, no JIT cache)."""
+"""Build the in-tree CUDA library ``lib/librcholqr.so`` for sm_100a (nvcc, no JIT cache).
+
+Staleness is decided by CONTENT, not mtimes: a SHA-256 over the sources, headers and the nvcc command
+is written next to the library (``lib/librcholqr.so.sha256``) and the library is rebuilt whenever it
+differs -- so a prebuilt .so shipped with a snapshot is reused only if it was built from exactly these
+sources.  ``build()`` returns the path; ``last_build_info()`` says whether this process rebuilt it.
+Translation units compile in parallel (one nvcc per .cu) and are linked once.
+"""
 from __future__ import annotations
 
+import concurrent.futures as cf
 import glob
+import hashlib
 import os
+import shutil
 import subprocess
 import sys
+import tempfile
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "lib", "librcholqr.so")
+STAMP = LIB + ".sha256"
 SRCS = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")))
 HDRS = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cuh"))) + [os.path.join(ROOT, "include", "rcholqr.h")]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+FLAGS = ["-O3", "-std=c++20", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC"]
+_info = {"rebuilt": False, "hash": None}
 
 
 def _nccl_include() -> str:
@@ -27,28 +41,54 @@ def _nccl_include() -> str:
     raise RuntimeError("nccl.h not found (needed for the multi-GPU all-reduce types)")
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def source_hash() -> str:
+    h = hashlib.sha256()
+    h.update(" ".join(FLAGS).encode())
+    for f in SRCS + HDRS:
+        h.update(os.path.basename(f).encode())
+        with open(f, "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()
+
+
+def _stale(digest: str) -> bool:
+    if not os.path.exists(LIB) or not os.path.exists(STAMP):
         return True
-    t = os.path.getmtime(LIB)
-    return any(os.path.getmtime(f) > t for f in SRCS + HDRS)
+    with open(STAMP) as f:
+        return f.read().strip() != digest
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+    digest = source_hash()
+    _info["hash"] = digest
+    if not force and not _stale(digest):
         return LIB
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     nvcc = os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "bin", "nvcc")
-    tmp = LIB + ".tmp%d" % os.getpid()
-    cmd = [nvcc, "-O3", "-std=c++20", *ARCH, "-lineinfo", "-Xcompiler", "-fPIC", "-shared",
-           "-I" + os.path.join(ROOT, "include"), "-I" + _nccl_include(),
-           "-o", tmp, *SRCS, "-ldl"]
-    if verbose:
-        cmd.insert(1, "-Xptxas=-v")
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
-    os.replace(tmp, LIB)
+    inc = ["-I" + os.path.join(ROOT, "include"), "-I" + _nccl_include()]
+    extra = ["-Xptxas=-v"] if verbose else []
+    tmpdir = tempfile.mkdtemp(prefix="rcholqr_build_")
+    try:
+        def obj(src):
+            o = os.path.join(tmpdir, os.path.basename(src) + ".o")
+            subprocess.check_call([nvcc, *FLAGS, *extra, *inc, "-c", "-o", o, src])
+            return o
+        with cf.ThreadPoolExecutor(max_workers=min(len(SRCS), os.cpu_count() or 4)) as ex:
+            objs = list(ex.map(obj, SRCS))
+        tmp = LIB + ".tmp%d" % os.getpid()
+        subprocess.check_call([nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-ldl"])
+        os.replace(tmp, LIB)
+        with open(STAMP, "w") as f:
+            f.write(digest + "\n")
+    finally:
+        shutil.rmtree(tmpdir, ignore_errors=True)
+    _info["rebuilt"] = True
     return LIB
+
+
+def last_build_info() -> dict:
+    """{"rebuilt": did this process compile the library, "hash": the source hash it matches}."""
+    return dict(_info)
 
 
 if __name__ == "__main__":

@@ -129,6 +129,8 @@ struct rcholqr_plan_s {
   double* Rtmp = nullptr;   // [n][n] R when the caller does not want one
   int* status_d = nullptr;
   int* flag_d = nullptr;    // tensor-core sketch overflow flag (selects the guarded fallback kernel)
+  int* flag_seen_d = nullptr;   // set by the reduction when that flag was raised (rcholqr_last_path)
+  unsigned path = 0;        // RCHOLQR_PATH_* bits of the current / last call
   int* status_h = nullptr;  // pinned
   // factor_host staging
   void* xbuf = nullptr; void* qbuf = nullptr; size_t xq_bytes = 0;
@@ -230,7 +232,7 @@ rcholqr_status do_sketch(rcholqr_plan p, const void* X, int64_t m, int64_t ro, i
       }
     }
     CU(launch_sketch(L, X, d.dtype, m, d.n, ldx, ro, k, d.nnz_per_col, d.seed, part, partc, P, p->status_d, p->flag_d,
-                     p->xdig, p->xdig_bytes, st, timed ? p->ev[1] : nullptr, k_first));
+                     p->xdig, p->xdig_bytes, st, timed ? p->ev[1] : nullptr, k_first, &p->path, p->flag_seen_d));
   } else {
     if (timed) { cudaEventRecord(p->ev[0], st); cudaEventRecord(p->ev[1], st); }
     CU(cudaMemsetAsync(P, 0, sizeof(double) * (size_t)k * d.n, st));
@@ -274,9 +276,10 @@ rcholqr_status solve(rcholqr_plan p, const void* X, int64_t m, int64_t ldx, cons
     if (timed && p->timing) cudaEventRecord(p->ev[5], st);
     const cudaError_t e = launch_solve_tc(p->W, n, (const float*)X, m, ldx, (float*)Q, ldq, p->qws, p->status_d,
                                           p->sms, st);
-    if (e == cudaSuccess) return RCHOLQR_OK;
+    if (e == cudaSuccess) { p->path |= kPathSolveTC; return RCHOLQR_OK; }
     if (e != cudaErrorNotSupported) return cuda_status(e);
   }
+  if (m > 0) p->path |= kPathSolveDmma;
   if (sp.mstream) {
     CU(launch_tri_prep_blocked(R, n, p->W, p->status_d, st));
     if (timed && p->timing) cudaEventRecord(p->ev[5], st);
@@ -389,9 +392,10 @@ rcholqr_status rcholqr_create(const rcholqr_desc* desc, rcholqr_plan* out) {
                  cudaMalloc(&p->diag, sizeof(double) * 2 * n) == cudaSuccess &&
                  cudaMalloc(&p->tau, sizeof(double) * n) == cudaSuccess &&
                  cudaMalloc(&p->Rtmp, sizeof(double) * nn) == cudaSuccess &&
-                 cudaMalloc(&p->status_d, sizeof(int)) == cudaSuccess &&
+                 cudaMalloc(&p->status_d, 2 * sizeof(int)) == cudaSuccess &&   // [status, flag_seen]
                  cudaMallocHost(&p->status_h, sizeof(int)) == cudaSuccess;
   if (okalloc) {
+    p->flag_seen_d = p->status_d + 1;
     for (int t = 0; t < 7 && okalloc; ++t) okalloc = cudaEventCreate(&p->ev[t]) == cudaSuccess;
   }
   if (!okalloc) {
@@ -409,7 +413,7 @@ rcholqr_status rcholqr_create(const rcholqr_desc* desc, rcholqr_plan* out) {
     }
     p->sk.srht_s = p->srht_d;
   }
-  cudaMemset(p->status_d, 0, sizeof(int));
+  cudaMemset(p->status_d, 0, 2 * sizeof(int));
   *p->status_h = 0;
   *out = p;
   return RCHOLQR_OK;
@@ -441,7 +445,8 @@ rcholqr_status rcholqr_factor_async(rcholqr_plan p, const void* X, int64_t m, in
   cudaStream_t st = (cudaStream_t)stream;
   const int k = p->d.k, n = p->d.n;
   double* Rout = R ? R : p->Rtmp;
-  CU(cudaMemsetAsync(p->status_d, 0, sizeof(int), st));
+  p->path = 0;   // a new call: clear the path bits and the device status / overflow-seen words
+  CU(cudaMemsetAsync(p->status_d, 0, 2 * sizeof(int), st));
   rcholqr_status s = do_sketch(p, X, m, ro, ldx, p->P, st);
   if (s != RCHOLQR_OK) return s;
   CU(launch_qr(p->qr_kind, p->P, k, n, Rout, p->Awork, p->diag, p->tau, p->qr_ws, p->status_d, st));
@@ -543,7 +548,8 @@ rcholqr_status rcholqr_factor_reduced(rcholqr_plan p, const void* X, int64_t m, 
   double* P = p->red_P;
   double* Yd = p->red_P + (size_t)k * n;
   double* Rout = R ? R : p->Rtmp;
-  CU(cudaMemsetAsync(p->status_d, 0, sizeof(int), st));
+  p->path = 0;   // a new call: clear the path bits and the device status / overflow-seen words
+  CU(cudaMemsetAsync(p->status_d, 0, 2 * sizeof(int), st));
   // 1. P = Theta X, Y = L X: one (k + l)-row pass for a Gaussian Theta, else the sparse sketch and the
   //    l-row Gaussian extract; one all-reduce of [P; Y] either way
   rcholqr_status s;
@@ -612,7 +618,8 @@ rcholqr_status rcholqr_factor_rr(rcholqr_plan p, const void* X, int64_t m, int64
   const bool t = p->timing;
   p->timing = false;
   struct Restore { rcholqr_plan p; bool t; ~Restore() { p->timing = t; } } restore{p, t};
-  CU(cudaMemsetAsync(p->status_d, 0, sizeof(int), st));
+  p->path = 0;   // a new call: clear the path bits and the device status / overflow-seen words
+  CU(cudaMemsetAsync(p->status_d, 0, 2 * sizeof(int), st));
   // library events: sketch | column norms | all-reduce | RRQR (incl. host decisions) | gather | solve
   if (t) cudaEventRecord(p->ev[0], st);
   // 1. P = Theta X and the column sums of squares, all-reduced together as [P; colsq]
@@ -816,7 +823,8 @@ rcholqr_status rcholqr_sketch(rcholqr_plan p, const void* X, int64_t m, int64_t 
   if (!p || !P || m < 0 || ro < 0 || ldx < p->d.n || (m > 0 && !X)) return RCHOLQR_E_INVALID;
   DeviceGuard dg(p->d.device);
   cudaStream_t st = (cudaStream_t)stream;
-  CU(cudaMemsetAsync(p->status_d, 0, sizeof(int), st));
+  p->path = 0;   // a new call: clear the path bits and the device status / overflow-seen words
+  CU(cudaMemsetAsync(p->status_d, 0, 2 * sizeof(int), st));
   rcholqr_status s = do_sketch(p, X, m, ro, ldx, P, st);
   if (s != RCHOLQR_OK) return s;
   const bool t = p->timing;
@@ -831,7 +839,8 @@ rcholqr_status rcholqr_small_qr(rcholqr_plan p, const double* P, double* R, doub
   DeviceGuard dg(p->d.device);
   cudaStream_t st = (cudaStream_t)stream;
   const int k = p->d.k, n = p->d.n;
-  CU(cudaMemsetAsync(p->status_d, 0, sizeof(int), st));
+  p->path = 0;   // a new call: clear the path bits and the device status / overflow-seen words
+  CU(cudaMemsetAsync(p->status_d, 0, 2 * sizeof(int), st));
   CU(launch_qr(p->qr_kind, P, k, n, R, p->Awork, p->diag, p->tau, p->qr_ws, p->status_d, st));
   if (S) CU(launch_form_s(p->Awork, p->tau, p->diag, k, n, S, p->status_d, st));
   const bool t = p->timing;
@@ -849,7 +858,8 @@ rcholqr_status rcholqr_tri_solve(rcholqr_plan p, const void* X, int64_t m, int64
   DeviceGuard dg(p->d.device);
   cudaStream_t st = (cudaStream_t)stream;
   const int n = p->d.n;
-  CU(cudaMemsetAsync(p->status_d, 0, sizeof(int), st));
+  p->path = 0;   // a new call: clear the path bits and the device status / overflow-seen words
+  CU(cudaMemsetAsync(p->status_d, 0, 2 * sizeof(int), st));
   CU(launch_check_diag(R, n, p->status_d, st));
   rcholqr_status s2 = solve(p, X, m, ldx, R, Q, ldq, st, false);
   if (s2 != RCHOLQR_OK) return s2;
@@ -935,6 +945,16 @@ int32_t rcholqr_launches_per_factor(rcholqr_plan p, int64_t m) {
     qr_launches = 2 + panels + 3 * (panels - 1);
   }
   return (m > 0 ? sketch_launches : 0) + qr_launches + 1 + (m > 0 ? solve_launches : 0);
+}
+
+rcholqr_status rcholqr_last_path(rcholqr_plan p, uint32_t* out, void* stream) {
+  if (!p || !out) return RCHOLQR_E_INVALID;
+  DeviceGuard dg(p->d.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  CU(cudaMemcpyAsync(p->status_h, p->flag_seen_d, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  *out = p->path | (*p->status_h ? kPathSketchFallback : 0u);
+  return RCHOLQR_OK;
 }
 
 rcholqr_status rcholqr_set_timing(rcholqr_plan p, int32_t enable) {

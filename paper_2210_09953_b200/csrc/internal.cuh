@@ -9,6 +9,10 @@ namespace rcq {
 
 // Status bits written by kernels into the plan's device status word (0 = OK).
 enum : int { kStNonfinite = 1, kStSingular = 2 };
+// Which kernels served the last call (rcholqr_last_path; the bits are RCHOLQR_PATH_* of rcholqr.h).
+enum : unsigned { kPathSketchTC = RCHOLQR_PATH_SKETCH_TC, kPathSketchPresplit = RCHOLQR_PATH_SKETCH_PRESPLIT,
+                  kPathSketchCudaCore = RCHOLQR_PATH_SKETCH_CUDA_CORE, kPathSketchFallback = RCHOLQR_PATH_SKETCH_FALLBACK,
+                  kPathSolveTC = RCHOLQR_PATH_SOLVE_TC, kPathSolveDmma = RCHOLQR_PATH_SOLVE_DMMA };
 
 // One FP64 tensor-core MMA: D(16x8) += A(16x4) B(4x8)  (DMMA on sm_100a; tcgen05 has no f64 kind).
 // Fragments (PTX ISA, mma.m16n8k4 .f64): g = lane/4, t = lane%4;
@@ -71,7 +75,7 @@ SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms,
 cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
                           int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* partc, double* P,
                           int* status, int* flag, void* xdig, size_t xdig_bytes, cudaStream_t st, cudaEvent_t ev_mid,
-                          int k_first = 0);
+                          int k_first = 0, unsigned* path = nullptr, int* flag_seen = nullptr);
 TrsmLaunch plan_trsm(int n, int dtype, size_t smem_optin);
 cudaError_t launch_tri_inverse(const double* R, int n, double* W, int* status, cudaStream_t st);
 cudaError_t launch_trsm(const TrsmLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
@@ -109,7 +113,7 @@ bool solve_tc_applicable(int dtype, int n);
 bool solve_tc_supported(const void* X, int64_t m, int64_t ldx, const void* Q, int64_t ldq);
 size_t solve_tc_workspace();
 cudaError_t launch_solve_tc(const double* Winv, int n, const float* X, int64_t m, int64_t ldx, float* Q, int64_t ldq,
-                            void* ws, const int* status, int sms, cudaStream_t st);
+                            void* ws, int* status, int sms, cudaStream_t st);
 // RCholeskyQR2 (rcqr2.cu): Gram A = Q^T Q, Cholesky R', R' R
 cudaError_t launch_reduce(const double* part, int splits, int64_t kn, double scale, double* P, int* status,
                           cudaStream_t st);

@@ -424,7 +424,10 @@ sketch_sparse_reg_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx
 // Theta rows by 1/sqrt(k), extractor rows by 1/sqrt(l)).
 __global__ void sketch_reduce_kernel(const double* __restrict__ part, const double* __restrict__ partc, int splits,
                                      int64_t kn, double scale, int64_t kn_first, double scale2,
-                                     double* __restrict__ P, int* status) {
+                                     double* __restrict__ P, int* status, const int* flag, int* flag_seen) {
+  // record (for rcholqr_last_path) that a tensor-core sketch raised its overflow flag and the guarded
+  // CUDA-core kernel recomputed the partials
+  if (flag_seen && blockIdx.x == 0 && threadIdx.x == 0 && *flag) atomicOr(flag_seen, 1);
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < kn;
        idx += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0, c = 0.0;                    // compensated (TwoSum) sum over the splits
@@ -677,8 +680,9 @@ static cudaError_t launch_gauss_typed(const SketchLaunch& L, const void* X, int6
 cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
                           int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* partc, double* P,
                           int* status, int* flag, void* xdig, size_t xdig_bytes, cudaStream_t st, cudaEvent_t ev_mid,
-                          int k_first) {
+                          int k_first, unsigned* path, int* flag_seen) {
   cudaError_t e;
+  unsigned pb = 0;
   const int64_t per = (m + L.splits - 1) / L.splits;
   double scale;
   int reduce_splits = L.splits;
@@ -694,7 +698,9 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
       e = launch_sparse_tc(X, dtype, m, n, ldx, row_offset, k, zeta, seed, L.splits, rps, part, flag, st);
       if (e != cudaSuccess) return e;
       guard = flag;
+      pb |= kPathSketchTC;
     }
+    pb |= kPathSketchCudaCore;
     auto launch = [&](auto* tag) -> cudaError_t {
       using TX = std::remove_pointer_t<decltype(tag)>;
       auto go = [&](auto kern, int cpl) -> cudaError_t {
@@ -726,6 +732,7 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
     };
     e = dtype == RCHOLQR_F64 ? launch((double*)nullptr) : launch((float*)nullptr);
     scale = 1.0 / std::sqrt((double)zeta);
+    pb |= kPathSketchCudaCore;
   } else {
     int splits = L.splits;
     const int* guard = nullptr;
@@ -746,6 +753,7 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
                                flag, st, L.srht_s);
         if (e != cudaSuccess) return e;
         guard = flag;
+        pb |= kPathSketchTC;
       } else {
         splits = L.splits;
       }
@@ -756,13 +764,15 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
       e = cudaMemsetAsync(flag, 0, sizeof(int), st);
       if (e != cudaSuccess) return e;
       e = cudaErrorNotSupported;
-      if (xdig && !getenv("RCHOLQR_GAUSS_NO_PRESPLIT"))    // pre-split digits (row chunks that fit the workspace)
+      if (xdig && !getenv("RCHOLQR_GAUSS_NO_PRESPLIT")) {   // pre-split digits (row chunks that fit the workspace)
         e = launch_gauss_tcp(X, dtype, m, n, ldx, row_offset, k, seed, L.tc_tiles_k, L.tc_tiles_n, splits, part,
                              partc, flag, xdig, xdig_bytes, st);
+        if (e == cudaSuccess) pb |= kPathSketchPresplit;
+      }
       if (e == cudaErrorNotSupported)
         e = launch_gauss_tc(X, dtype, m, n, ldx, row_offset, k, seed, L.tc_tiles_k, L.tc_tiles_n, splits, trps, part,
                             partc, flag, st);
-      if (e == cudaSuccess) guard = flag;                     // else: the DMMA kernel computes the sketch
+      if (e == cudaSuccess) { guard = flag; pb |= kPathSketchTC; }   // else: the DMMA kernel computes the sketch
       else if (e != cudaErrorNotSupported) return e;
     }
     // DMMA kernel: the path itself, or the overflow fallback of the tensor-core kernel (same splits)
@@ -775,6 +785,7 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
             : launch_gauss_typed<float>(Lg, X, m, n, ldx, row_offset, k, seed, rps, part, partc, st, guard);
     scale = 1.0 / std::sqrt((double)k);
     reduce_splits = splits;
+    if (!guard) pb |= kPathSketchCudaCore;
   }
   if (e != cudaSuccess) return e;
   if (ev_mid) cudaEventRecord(ev_mid, st);
@@ -789,7 +800,9 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
     scale2 = 1.0 / std::sqrt((double)(k - k_first));
   }
   sketch_reduce_kernel<<<blocks, threads, 0, st>>>(part, sparse ? nullptr : partc, reduce_splits, kn, scale,
-                                                   (int64_t)std::min(std::max(k_first, 0), k) * n, scale2, P, status);
+                                                   (int64_t)std::min(std::max(k_first, 0), k) * n, scale2, P, status,
+                                                   (pb & kPathSketchTC) ? flag : nullptr, flag_seen);
+  if (path) *path |= pb;
   return cudaGetLastError();
 }
 
@@ -798,7 +811,8 @@ cudaError_t launch_reduce(const double* part, int splits, int64_t kn, double sca
                           cudaStream_t st) {
   const int threads = 256;
   const int blocks = (int)std::min<int64_t>((kn + threads - 1) / threads, 4096);
-  sketch_reduce_kernel<<<blocks, threads, 0, st>>>(part, nullptr, splits, kn, scale, kn, scale, P, status);
+  sketch_reduce_kernel<<<blocks, threads, 0, st>>>(part, nullptr, splits, kn, scale, kn, scale, P, status, nullptr,
+                                                   nullptr);
   return cudaGetLastError();
 }
 

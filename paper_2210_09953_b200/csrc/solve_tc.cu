@@ -122,7 +122,7 @@ template <int KMAX>
 __global__ void __launch_bounds__(QCfg<KMAX>::THREADS, 1)
 solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap qmap,
                 const int8_t* __restrict__ wdig, const int* __restrict__ wexp, const float* __restrict__ X,
-                int64_t ldx, int64_t m, int n, int kpad, float* __restrict__ Q, int64_t ldq, const int* status,
+                int64_t ldx, int64_t m, int n, int kpad, float* __restrict__ Q, int64_t ldq, int* status,
                 int dbg) {
   using Cf = QCfg<KMAX>;
   constexpr int QT_DIG = Cf::DIG, QT_RAW = Cf::RAW > 0 ? Cf::RAW : 1, QT_A_TILE = Cf::A_TILE;
@@ -410,7 +410,9 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
 #pragma unroll
       for (int c = 0; c < 16; ++c) mx = max(mx, __float_as_uint(x[c]) & 0x7FFFFFFFu);
       for (int o = rpw; o < 32; o <<= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-      // e_i: smallest e with max |x| < 2^e (finite input assumed: the sketch rejected NaN/Inf)
+      // e_i: smallest e with max |x| < 2^e.  Inside rcholqr_factor the sketch has already rejected
+      // NaN/Inf; a direct tri_solve call reports them here (Q is then not meaningful)
+      if (mx >= 0x7F800000u) atomicOr(status, kStNonfinite);
       const int e = mx == 0u ? 0 : (mx < 0x00800000u ? -126 : (int)(mx >> 23) - 126);
       if (lg == 0) rexp[(tt & 3) * QT_M + i] = e;
       uint32_t W[QT_DA][4];
@@ -482,6 +484,7 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
                 mx = max(mx, max(__float_as_uint(xh0[b][c]) & 0x7FFFFFFFu, __float_as_uint(xh1[b][c]) & 0x7FFFFFFFu));
               mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
               mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+              if (mx >= 0x7F800000u) atomicOr(status, kStNonfinite);   // tri_solve on NaN/Inf X
               ee[b] = mx == 0u ? 0 : (mx < 0x00800000u ? -126 : (int)(mx >> 23) - 126);
               if (lgp == 0) rexp[(tt & 3) * QT_M + (dw + QT_DWARPS * b) * 8 + (lane & 7)] = ee[b];
             }
@@ -539,7 +542,7 @@ using EncodeTiledFn2 = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_
 
 // W = R^{-1} already in Winv (n x n fp64).  ws: workspace of solve_tc_workspace(n) bytes.
 cudaError_t launch_solve_tc(const double* Winv, int n, const float* X, int64_t m, int64_t ldx, float* Q, int64_t ldq,
-                            void* ws, const int* status, int sms, cudaStream_t st) {
+                            void* ws, int* status, int sms, cudaStream_t st) {
   if (m == 0) return cudaSuccess;
   if (!solve_tc_supported(X, m, ldx, Q, ldq)) return cudaErrorNotSupported;
   static EncodeTiledFn2 enc = [] {

@@ -144,6 +144,36 @@ def test_sketch_gauss_chunked_presplit(cuda, monkeypatch, dt, n, k):
     assert _rel(full, Po) <= 1e-12, _rel(full, Po)
 
 
+@pytest.mark.parametrize("chunked", [False, True])
+@pytest.mark.parametrize("dt,case", [("f32", "spike"), ("f64", "spike"), ("f32", "zero_head"), ("f64", "zero_head")])
+def test_sketch_gauss_tc_headroom_overflow(cuda, monkeypatch, dt, case, chunked):
+    # The Gaussian tcgen05 sketch's digit scales come from the first rows of each split (sketch_gtc.cu):
+    # rows far above that scale, or a column that is zero there, must raise the overflow flag; the
+    # guarded DMMA kernel then recomputes the partials and P still matches the oracle.  Unchunked and
+    # with a tiny digit-workspace cap (many pre-split row chunks adding into the same partials).
+    if chunked:
+        monkeypatch.setenv("RCHOLQR_XDIG_CAP_MB", "2")
+    m, n, k = 200_000, 100, 200
+    X = synth.make_X(m, n, 3.0, dt)
+    if case == "spike":
+        X[1000::4099, :] *= 1e6
+    else:
+        # column 7 is zero but for two rows 43 apart: whatever the split boundaries, one of them lies
+        # outside its split's leading 32 rows with a zero (or 1e6-times smaller) column scale there
+        X[:, 7] = 0.0
+        X[123_457, 7] = 1.0
+        X[123_500, 7] = 1e6
+    plan = _plan(n, k, dt)
+    Pg = _np(plan.sketch(_t(X)))
+    path = plan.last_path()
+    assert path & rcq.PATH_SKETCH_TC and path & rcq.PATH_SKETCH_FALLBACK, path
+    Po = oracle.sketch(X, k)
+    assert _rel(Pg, Po) <= 1e-12, _rel(Pg, Po)
+    # a clean X on the same plan: no fallback
+    plan.sketch(_t(synth.make_X(50_000, n, 3.0, dt)))
+    assert not plan.last_path() & rcq.PATH_SKETCH_FALLBACK
+
+
 def test_sketch_ld_and_row_offset(cuda):
     X = synth.make_X(5000, 40, 3.0)
     wide = np.zeros((5000, 57))
@@ -296,6 +326,16 @@ E2E = [
 ]
 
 
+def _assert_tc_path(plan, dt, n):
+    """The tcgen05 kernels (not the guarded CUDA-core fallbacks) computed the sketch, and the tall solve
+    ran on tcgen05 for fp32 X with n <= 128, else on the DMMA substitution (rcholqr_last_path)."""
+    path = plan.last_path()
+    assert path & rcq.PATH_SKETCH_TC, path
+    assert not path & (rcq.PATH_SKETCH_FALLBACK | rcq.PATH_SKETCH_CUDA_CORE), path
+    want = rcq.PATH_SOLVE_TC if (dt == "f32" and n <= 128) else rcq.PATH_SOLVE_DMMA
+    assert path & want, path
+
+
 def _check_e2e(X, k, sk, c, Qg, Rg, plan, dt):
     n = X.shape[1]
     so = oracle.GAUSSIAN if sk == "gaussian" else oracle.SPARSE_SIGN
@@ -321,6 +361,7 @@ def test_factor_parity(cuda, name, m, n, k, dt, sk, c):
     X = synth.make_X(m, n, c, dt)
     plan = _plan(n, k, dt, sk)
     Q, R, S = plan.factor(_t(X), want_S=True)
+    _assert_tc_path(plan, dt, n)
     Qg, Rg, Sg = _np(Q), _np(R), _np(S)
     _check_e2e(X, k, sk, c, Qg, Rg, plan, dt)
     assert np.linalg.norm(Sg.T @ Sg - np.eye(n)) <= 50 * n * U64
@@ -334,6 +375,8 @@ def test_factor_C2_full_size(cuda):
     X = synth.make_X(cfg["m"], cfg["n"], cfg["log10_cond"], cfg["dtype"])
     plan = _plan(cfg["n"], cfg["k"], cfg["dtype"])
     Q, R, _ = plan.factor(_t(X))
+    _assert_tc_path(plan, "f32", cfg["n"])
+    assert plan.last_path() & rcq.PATH_SKETCH_PRESPLIT
     _check_e2e(X, cfg["k"], "gaussian", cfg["log10_cond"], _np(Q), _np(R), plan, "f32")
 
 
@@ -346,20 +389,50 @@ def test_factor_host_matches_device(cuda):
     assert np.array_equal(_np(Qd), Qh.numpy()) and np.array_equal(_np(Rd), Rh.numpy())
 
 
-def test_factor_nccl_single_rank_comm(cuda):
-    # the collective path with a 1-rank NCCL communicator (all-reduce = identity) is bit-identical
-    X = _t(synth.make_X(30_000, 20, 3.0))
+@pytest.mark.parametrize("dt,n,k,sk,c", [("f64", 20, 40, "gaussian", 3), ("f32", 64, 128, "sparse", 4),
+                                         ("f32", 100, 200, "gaussian", 5)])
+def test_factor_nccl_single_rank_comm(cuda, dt, n, k, sk, c):
+    # S3: the collective path -- ncclAllReduce of P on the library stream -- with a
+    # 1-rank communicator is checked against the ORACLE (north-star bars), and is bit-identical to the
+    # non-collective plan (the all-reduce of one rank is the identity)
+    Xh = synth.make_X(30_000, n, c, dt)
+    X = _t(Xh)
     uid = rcq.comm_unique_id()
     comm = rcq.comm_create(uid, 1, 0, 0)
     try:
-        a = rcq.RCholQR(n=20, k=40, comm=comm)
-        b = rcq.RCholQR(n=20, k=40)
+        a = _plan_comm(n, k, dt, sk, comm)
+        b = _plan(n, k, dt, sk)
         Qa, Ra, _ = a.factor(X)
+        _check_e2e(Xh, k, sk, c, _np(Qa), _np(Ra), a, dt)
         Qb, Rb, _ = b.factor(X)
         assert torch.equal(Qa, Qb) and torch.equal(Ra, Rb)
         a.close()
     finally:
         rcq.comm_destroy(comm)
+
+
+def _plan_comm(n, k, dt, sk, comm):
+    return rcq.RCholQR(n=n, k=k, dtype=torch.float64 if dt == "f64" else torch.float32, sketch=sk, comm=comm)
+
+
+@pytest.mark.parametrize("sk", ["gaussian", "sparse", "rademacher", "srht"])
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+def test_rank_partition_sum_vs_oracle(cuda, sk, dt):
+    # What every rank computes before the all-reduce: the sketch of its own row block with Theta keyed by
+    # the GLOBAL row.  Three blocks at offsets that are not multiples of 32 (and one that
+    # is, so SRHT's tcgen05 path runs too) summed on the host == the oracle's sketch of the whole X.
+    n, k = 48, 96
+    X = synth.make_X(90_011, n, 4.0, dt)
+    so = {"gaussian": oracle.GAUSSIAN, "sparse": oracle.SPARSE_SIGN, "rademacher": oracle.RADEMACHER,
+          "srht": oracle.SRHT}[sk]
+    base = 1_000_000   # a multiple of 32: the first block of each split takes SRHT's tcgen05 path
+    Po = oracle.sketch(X, k, sketch=so, zeta=8, seed=3, row_offset=base)
+    plan = _plan(n, k, dt, sk, seed=3)
+    Xt = _t(X)
+    for bounds in ([0, 12_345, 50_007, 90_011], [0, 29, 45_061, 90_011]):
+        parts = [_np(plan.sketch(Xt[a:b], row_offset=base + a)) for a, b in zip(bounds[:-1], bounds[1:])]
+        tot = parts[0] + parts[1] + parts[2]
+        assert _rel(tot, Po) <= 1e-13, (bounds, _rel(tot, Po))
 
 
 # ---------------------------------------------------------------------------------- edge cases
@@ -405,6 +478,46 @@ def test_factor_ragged_m(cuda, m):
     assert _rel(_np(R), out["R"]) <= 1e-12 and _rel(_np(Q), out["Q"]) <= 1e-12
 
 
+# ---------------------------------------------------------------------------------- full size, end to end
+@pytest.mark.slow
+def test_full_size_C4_end_to_end(cuda):
+    """BASELINE C4 (m = 2^26, n = 64, k = 128, sparse-sign, fp32 X, cond 1e4) at full size, in the bench's
+    launch configuration, against oracle.factor on the SAME X end to end (the oracle's own sketch,
+    Householder and substitution): R at the north-star bar (and at fp64 level), Q whole-matrix relative
+    Frobenius, the sketched orthonormality (A12) and cond(Q) (A11)."""
+    cfg = synth.config("C4")
+    m, n, k = cfg["m"], cfg["n"], cfg["k"]
+    Xd = synth.make_X_torch(m, n, cfg["log10_cond"], "f32")
+    plan = _plan(n, k, "f32", "sparse")
+    Q, R, _ = plan.factor(Xd)
+    _assert_tc_path(plan, "f32", n)
+    X = _np(Xd)
+    del Xd
+    out = oracle.factor(X, k, sketch=oracle.SPARSE_SIGN, zeta=8, want_S=False)
+    Qo, Ro = out["Q"], out["R"]
+    rel_r = _rel(_np(R), Ro)
+    assert rel_r <= 1e-4 and rel_r <= 1e-10, rel_r      # north-star bar (fp32 X) and the fp64-level agreement
+    num = den = 0.0
+    for a in range(0, m, 1 << 24):                        # Q compared chunk by chunk (17 GB each)
+        qg = _np(Q[a:a + (1 << 24)]).astype(np.float64)
+        qo = Qo[a:a + (1 << 24)].astype(np.float64)
+        num += float(np.sum((qg - qo) ** 2))
+        den += float(np.sum(qo ** 2))
+    rel_q = (num / den) ** 0.5
+    assert rel_q <= 10 * U64 * 10**cfg["log10_cond"] + 2 * U32, rel_q
+    dg = oracle.orth_defect(_np(plan.sketch(Q)))
+    do = oracle.orth_defect(oracle.sketch(Qo, k, sketch=oracle.SPARSE_SIGN, zeta=8))
+    assert dg <= max(1e-5, 10 * do), (dg, do)
+    Qd = Q.double()
+    cg = oracle.cond_from_gram(_np(Qd.T @ Qd))
+    del Qd
+    Gq = np.zeros((n, n))
+    for a in range(0, m, 1 << 24):
+        qo = Qo[a:a + (1 << 24)].astype(np.float64)
+        Gq += qo.T @ qo
+    assert cg <= 8.0 and abs(cg / oracle.cond_from_gram(Gq) - 1) <= 1e-5, cg
+
+
 # ---------------------------------------------------------------------------------- full size, sampled
 @pytest.mark.slow
 @pytest.mark.parametrize("name", ["C3", "C4", "C5"])
@@ -423,13 +536,20 @@ def test_full_size_sampled(cuda, name):
     assert st == rcq.OK and torch.equal(R2, R)
     Pn, Rn = _np(P), _np(R)
     rng = np.random.default_rng(0)
-    cols = rng.choice(n, 3, replace=False)
-    for j in cols:
-        xj = _np(X[:, j].double())
-        for r in rng.choice(k, 2, replace=False):
-            ref = oracle.sketch_entry(xj, int(r), k, sketch=so, zeta=8)
-            assert abs(Pn[r, j] - ref) <= 1e-12 * np.linalg.norm(Pn[:, j]), (r, j, Pn[r, j], ref)
-        del xj
+    cols = np.sort(rng.choice(n, 3, replace=False))
+    # three WHOLE columns of P (all k rows) from the oracle's sketch of those columns of X -- the
+    # oracle's Theta generation and compensated sums, on the same bytes
+    Xc = _np(X[:, torch.from_numpy(cols).cuda()].double())
+    Pc = oracle.sketch(Xc, k, sketch=so, zeta=8)
+    del Xc
+    for t, j in enumerate(cols):
+        assert np.linalg.norm(Pn[:, j] - Pc[:, t]) <= 1e-12 * np.linalg.norm(Pc[:, t]), j
+    # plus sampled single entries through oracle_sketch_entry (its own pinned code path)
+    xj = _np(X[:, int(cols[0])].double())
+    for r in rng.choice(k, 2, replace=False):
+        ref = oracle.sketch_entry(xj, int(r), k, sketch=so, zeta=8)
+        assert abs(Pn[r, cols[0]] - ref) <= 1e-12 * np.linalg.norm(Pn[:, cols[0]]), (r, Pn[r, cols[0]], ref)
+    del xj
     Ro, _, _ = oracle.householder(Pn, want_S=False)
     assert _rel(Rn, Ro) <= 1e-13
     rows = np.concatenate([[0, m - 1], rng.choice(m, 62, replace=False)])
