@@ -2,13 +2,13 @@
 """Benchmark: RandCholQR factor throughput (GB/s of X, rows/s) on B200 (BASELINE.json metric).
 
 One step = one whole Algorithm 2 factorization (sketch + reduce [+ all-reduce] + Householder QR +
-R^-1 + tall solve) of the workload's X, inputs resident in HBM.  Default workload at N=1 is
-BASELINE.json configs[1] (C2: m=2^20, n=100, k=200, Gaussian, fp32 X, cond 1e5).  With N GPUs
-(torchrun, one process per GPU) each rank factors its own C2-sized row block of a (N*2^20) x 100
-X with one NCCL all-reduce of the 200 x 100 sketch ("weak" scaling); --config C3/C4/C5 instead
-row-partitions the full BASELINE matrix ("strong").
+R^-1 + tall solve) of the workload's X, inputs resident in HBM.  The default workload is BASELINE.json
+C4 (m = 2^26, n = 64, k = 128, sparse-sign Theta, fp32 X, cond 1e4), one of the metric's 1/2/4/8-GPU
+configs: with N GPUs (torchrun, one process per GPU) the full C4 matrix is row-partitioned across the
+ranks with one NCCL all-reduce of the 128 x 64 sketch ("strong" scaling; C3 / C5 likewise).  C1 / C2
+(single-GPU configs) stay available with --config; at N > 1 they give each rank its own block ("weak").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
 """
 from __future__ import annotations
 
@@ -25,8 +25,9 @@ sys.path.insert(0, ROOT)
 
 import synth  # noqa: E402
 
-DMMA_PEAK_TFLOPS = 37.2   # derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz
+DMMA_PEAK_DERIVED = 37.2   # 148 SMs x 64 FP64 FMA/clk x 2 x 1.965 GHz (fallback only)
 L2_BYTES = 126 * 2**20
+DEFAULT_CONFIG = "C4"
 
 
 def _peaks():
@@ -35,6 +36,29 @@ def _peaks():
             return json.load(f)
     except OSError:
         return {}
+
+
+def _unit_peaks():
+    """Measured FP64 (DMMA) and tcgen05 kind::i8 peaks of this pool's B200s from
+    profiles/peaks_r2.jsonl (tools/measure_peaks.sh: tools/micro/peaks.cu and tc_rate.cu on all SMs,
+    with the SM clock sampled under load).  Falls back to the derived DMMA figure when absent."""
+    out = {"dmma_tflops": DMMA_PEAK_DERIVED, "dmma_source": "derived 148 SM x 64 FMA/clk x 2 x 1.965 GHz",
+           "i8_tops": None, "i8_source": None}
+    try:
+        rows = [json.loads(x) for x in open(os.path.join(ROOT, "profiles", "peaks_r2.jsonl")) if x.strip()]
+    except OSError:
+        return out
+    dm = [r["tflops"] for r in rows if str(r.get("kernel", "")).startswith("dmma")]
+    if dm:
+        out["dmma_tflops"] = max(dm)
+        out["dmma_source"] = "measured: max DMMA (mma.sync f64) rate, profiles/peaks_r2.jsonl"
+    i8 = [r for r in rows if r.get("kind") == "i8" and "tops_chip" in r]
+    if i8:
+        best = max(i8, key=lambda r: r["tops_chip"])
+        out["i8_tops"] = best["tops_chip"]
+        out["i8_source"] = (f"measured: tcgen05.mma kind::i8 M=128 N={best['N']}, {best['mac_per_cyc']:.0f} MAC/clk/SM "
+                            f"x 148 SM x 2 x {best['sm_mhz']} MHz, profiles/peaks_r2.jsonl")
+    return out
 
 
 class ClockSampler:
@@ -98,7 +122,7 @@ def _dist():
 def _workload(cfg_name: str, ws: int, rank: int):
     from paper_2210_09953_b200.partition import row_block, weak_block
     cfg = synth.config(cfg_name)
-    if cfg_name in ("C1", "C2"):           # single-GPU configs: weak scaling, one C2 block per rank
+    if cfg_name in ("C1", "C2"):           # single-GPU configs: weak scaling, one block per rank
         ro, m_local, m_global = weak_block(cfg["m"], ws, rank)
         scaling = "weak"
     else:                                  # BASELINE multi-GPU configs: row-partition the full X
@@ -135,12 +159,30 @@ def _cpu_sample_rate(X_dev, cfg, target_s: float, algo: str = "rcholqr", l: int 
         rows = min(m, int(rows * max(2.0, 0.8 * target_s / max(dt, 1e-3))))
 
 
+def _host_X(cfg: dict, rows: int):
+    """The workload's X (its leading `rows` rows) on the host: generated on the GPU when one is present
+    (the same bytes bench.py's own arm factors, synth.make_X_torch), else by the host generator."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            Xd = synth.make_X_torch(rows, cfg["n"], cfg["log10_cond"], cfg["dtype"], seed=synth.X_SEED)
+            X = Xd.cpu().numpy()
+            del Xd
+            torch.cuda.empty_cache()
+            return X
+    except Exception:  # noqa: BLE001 - fall back to the host generator
+        pass
+    return synth.make_X(rows, cfg["n"], cfg["log10_cond"], cfg["dtype"])
+
+
 def run_reference(args):
-    """--impl reference: the CPU fp64 oracle timed as it stands (this tier's reference arm)."""
+    """--impl reference: the CPU fp64 oracle timed as it stands (this tier's reference arm) on the host
+    cores.  The sample is the WHOLE workload when the --steps/--warmup run fits the time budget
+    (then the line's config equals our arm's), else the leading rows -- never fewer than
+    cores x 65,536, so every OpenMP thread has one of the oracle's fixed 65,536-row blocks."""
     ws, rank, _ = _dist()
     if rank != 0:
         return 0
-    import numpy as np
     import oracle
     cfg = synth.config(args.config)
     if args.sketch:
@@ -148,38 +190,67 @@ def run_reference(args):
     so = {"gaussian": oracle.GAUSSIAN, "sparse": oracle.SPARSE_SIGN, "rademacher": oracle.RADEMACHER,
           "srht": oracle.SRHT}[cfg["sketch"]]
     s_x = 8 if cfg["dtype"] == "f64" else 4
-    per_step_s = max(1.0, 150.0 / (args.steps + args.warmup))
-    # calibrate a sample size on the leading rows of the workload's X
-    rows = 4096
-    while True:
-        X = synth.make_X(rows, cfg["n"], cfg["log10_cond"], cfg["dtype"])
-        t0 = time.perf_counter()
-        oracle.factor(X, cfg["k"], sketch=so, zeta=cfg["nnz"], want_S=False)
-        dt = time.perf_counter() - t0
-        if dt >= 0.5 * per_step_s or rows >= cfg["m"]:
-            break
-        rows = min(cfg["m"], int(rows * max(2.0, 0.8 * per_step_s / max(dt, 1e-3))))
-    X = synth.make_X(rows, cfg["n"], cfg["log10_cond"], cfg["dtype"])
-    for _ in range(args.warmup):
-        oracle.factor(X, cfg["k"], sketch=so, zeta=cfg["nnz"], want_S=False)
+    cores = oracle.num_threads()
+    m = cfg["m"]
+    run = lambda A: oracle.factor(A, cfg["k"], sketch=so, zeta=cfg["nnz"], want_S=False)  # noqa: E731
+    budget_s = args.ref_budget_s                       # whole warm-up + timed run
+    per_step_s = budget_s / (args.steps + args.warmup)
+    rows = min(m, cores * 65536)
+    X = _host_X(cfg, rows)                             # leading rows of the workload's X
+    t0 = time.perf_counter()
+    run(X)                                             # calibration (also the first warm-up step)
+    dt = time.perf_counter() - t0
+    if rows < m:
+        rate = rows / max(dt, 1e-6)                    # rows per second of this oracle on these cores
+        want = max(rows, min(m, int(rate * per_step_s)))
+        want = m if want >= 0.98 * m else want // 65536 * 65536 or want
+        if want > rows:
+            rows = want
+            del X
+            X = _host_X(cfg, rows)
+    Xs = X
+    for _ in range(max(0, args.warmup - 1)):
+        run(Xs)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.factor(X, cfg["k"], sketch=so, zeta=cfg["nnz"], want_S=False)
+        run(Xs)
     el = time.perf_counter() - t0
     ms = el / args.steps * 1e3
     gbs = rows * cfg["n"] * s_x / (ms * 1e-3) / 1e9
-    cores = oracle.num_threads()
-    sample = f"{rows} leading rows of {args.config} (m={cfg['m']}) per step, oracle.factor fp64 C/OpenMP"
+    whole = rows == m
+    sample = (f"the whole {args.config} X ({m} rows)" if whole else
+              f"{rows} leading rows of {args.config} (m={m}; the whole X does not fit the {budget_s:.0f} s budget)") + \
+        f" per step, oracle.factor (fp64 C, OpenMP over fixed 65,536-row blocks, {cores} threads)"
     line = {"metric": "RandCholQR factor throughput (GB/s of X)", "value": gbs, "unit": "GB/s",
             "impl": "reference", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "rows_per_s": rows / (ms * 1e-3), "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.config, "m": rows, "n": cfg["n"], "k": cfg["k"], "sketch": cfg["sketch"],
-                       "x_dtype": cfg["dtype"]},
+            "rows_per_s": rows / (ms * 1e-3), "higher_is_better": True, "scaling": "strong" if whole else "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": _config_dict(args.config, cfg, rows, s_x),
             "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def _config_dict(name: str, cfg: dict, m_global: int, s_x: int) -> dict:
+    """The workload description both arms print (identical keys and values for the same workload, so
+    the driver can match the reference arm's line to ours)."""
+    return {"workload": name, "m": m_global, "n": cfg["n"], "k": cfg["k"], "sketch": cfg["sketch"],
+            "x_dtype": cfg["dtype"], "cond": 10.0 ** cfg["log10_cond"],
+            "l2": "inputs larger than L2 (per-rank X > 126 MiB), no flush" if m_global * cfg["n"] * s_x > 8 * L2_BYTES
+                  else "X fits in L2 on some ranks: NOT flushed (small config)"}
+
+
+def _i8_macs(cfg: dict, m: int, k: int) -> float:
+    """int8 MACs the pre-split tcgen05 Gaussian sketch issues for m rows (sketch_gtc.cu): X digit b (DX of
+    them) times the Theta digit prefix of min(LK - b, 6) digits, over the padded tile (k up to KT rows,
+    n up to 128 columns)."""
+    f32 = cfg["dtype"] == "f32"
+    dx, lk, kt = (6, 8, 40) if f32 else (8, 9, 48)
+    pairs = sum(min(lk - b, 6) for b in range(dx))
+    kpad = -(-k // kt) * kt
+    npad = -(-cfg["n"] // 128) * 128
+    return float(pairs) * kpad * npad * m
 
 
 def run(args):
@@ -187,6 +258,9 @@ def run(args):
     import torch.distributed as dist
 
     import paper_2210_09953_b200 as rcq
+
+    up = _unit_peaks()
+    DMMA_PEAK_TFLOPS = up["dmma_tflops"]
 
     ws, rank, local = _dist()
     if ws != args.gpus and "WORLD_SIZE" in os.environ:
@@ -313,11 +387,14 @@ def run(args):
         ach = flops / (per_ms["sketch"] * 1e-3) / 1e12
         roofs["sketch"] = {"kernel": "xdig_split_kernel + sketch_gauss_tcp_kernel", "bound": "tensor",
                            "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
-                           "peak_source": "FP64 DMMA peak 37.2 TF (148 SM x 64 FMA/clk x 2 x 1.965 GHz; "
-                                          "microbenchmark 37.0, profiles/peaks_r1.jsonl): fp64-equivalent view "
-                                          "of the exact int8 digit emulation",
+                           "peak_source": up["dmma_source"] + ": fp64-equivalent view of the exact int8 digit emulation",
                            "algorithmic": f"2*{'(k+l)' if reduced else 'k'}*m*n = {flops:.4g} flop per launch",
                            "traffic": None}
+        if up["i8_tops"]:    # the unit that actually does the work: executed int8 MACs vs the tcgen05 i8 rate
+            i8 = 2.0 * _i8_macs(cfg, m_local, k_sk) / (per_ms["sketch"] * 1e-3) / 1e12
+            roofs["sketch"]["int8_view"] = {"achieved": i8, "peak": up["i8_tops"], "unit": "TOP/s",
+                                            "frac": i8 / up["i8_tops"], "peak_source": up["i8_source"],
+                                            "executed": "2 x int8 MACs issued incl. tile padding (sketch_gtc.cu)"}
     elif reduced:
         # sparse Theta: P by the sparse tcgen05 sketch (one HBM pass), then Y = L X by the Gaussian
         # one; the Gaussian extract's 2 l m n fp64-equivalent flops dominate both passes' time
@@ -325,7 +402,7 @@ def run(args):
         ach = flops / (per_ms["sketch"] * 1e-3) / 1e12
         roofs["sketch"] = {"kernel": "xdig_split_kernel + sketch_gauss_tcp_kernel", "bound": "tensor", "achieved": ach,
                            "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
-                           "peak_source": "FP64 DMMA peak 37.2 TF (fp64-equivalent view of the exact int8 digits)",
+                           "peak_source": up["dmma_source"] + " (fp64-equivalent view of the exact int8 digits)",
                            "algorithmic": f"2*l*m*n = {flops:.4g} flop (Gaussian extract; the time includes "
                                           "the sparse sketch pass)", "traffic": None}
     elif cfg["sketch"] in ("rademacher", "srht") and n > 64:
@@ -333,7 +410,7 @@ def run(args):
         ach = flops / (per_ms["sketch"] * 1e-3) / 1e12
         roofs["sketch"] = {"kernel": f"sketch_gauss_kernel ({cfg['sketch']} draws)", "bound": "tensor", "achieved": ach,
                            "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
-                           "peak_source": "FP64 DMMA peak 37.2 TF", "algorithmic": f"2*k*m*n = {flops:.4g} flop",
+                           "peak_source": up["dmma_source"], "algorithmic": f"2*k*m*n = {flops:.4g} flop",
                            "traffic": None}
     else:   # sparse-sign, or Rademacher on the dense-E tcgen05 kernel: one read of X per Theta tile
         byts = m_local * n * s_x
@@ -368,7 +445,7 @@ def run(args):
             ach = flops / (per_ms["solve"] * 1e-3) / 1e12
             roofs["solve"] = {"kernel": "blocked substitution (fp64 DMMA), r columns", "bound": "tensor",
                               "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                              "frac": ach / DMMA_PEAK_TFLOPS, "peak_source": "FP64 DMMA peak 37.2 TF",
+                              "frac": ach / DMMA_PEAK_TFLOPS, "peak_source": up["dmma_source"],
                               "algorithmic": f"m*r^2 = {flops:.4g} flop", "traffic": None}
         per_ms = {"sketch": per_ms["sketch"], "colnorms": per_ms["reduce"], "allreduce": per_ms["allreduce"],
                   "rrqr": per_ms["small_qr"], "gather": per_ms["tri_prep"], "solve": per_ms["solve"]}
@@ -383,7 +460,7 @@ def run(args):
         ach = flops / (per_ms["solve"] * 1e-3) / 1e12
         roofs["solve"] = {"kernel": "blocked substitution (fp64 DMMA)", "bound": "tensor", "achieved": ach,
                           "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
-                          "peak_source": "FP64 DMMA peak 37.2 TF", "algorithmic": f"m*n^2 = {flops:.4g} flop per solve",
+                          "peak_source": up["dmma_source"], "algorithmic": f"m*n^2 = {flops:.4g} flop per solve",
                           "traffic": None}
     try:   # DRAM bytes per launch from one `ncu --set full` capture of the same workload (tools/ncu_traffic.py)
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
@@ -419,10 +496,8 @@ def run(args):
             "rows_per_s": m_global / (ms * 1e-3), "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
-            "config": {"workload": args.config, "m_global": m_global, "m_local": m_local, "n": n, "k": k,
-                       "sketch": cfg["sketch"], "x_dtype": dt, "cond": 10.0 ** cfg["log10_cond"],
-                       "parallelism": f"row-partition x{ws}, 1 all-reduce",
-                       "l2": f"inputs larger than L2 (X = {m_local * n * s_x / 2**20:.0f} MiB > 126 MiB), no flush"},
+            "config": _config_dict(args.config, cfg, m_global, s_x),
+            "partition": {"m_local": m_local, "row_offset": ro, "parallelism": f"row-partition x{ws}, 1 all-reduce"},
             "per_kernel_ms": per_ms, "roofline": roof, "kernel_rooflines": roofs, "northstar_roofline": ns,
             "gpu_launches": plan.launches_per_factor(m_local) * args.steps,
             "clocks": clk.summary(), "e2e": e2e}
@@ -451,7 +526,7 @@ def run(args):
         roofs["gram"] = {"kernel": ("gram_small_kernel" if n <= 128 else "gram_kernel") +
                                    " + sketch_reduce_kernel + cholesky_kernel", "bound": "tensor",
                          "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s", "frac": ach / DMMA_PEAK_TFLOPS,
-                         "peak_source": "FP64 DMMA peak 37.2 TF",
+                         "peak_source": up["dmma_source"],
                          "algorithmic": f"m*n*(n+1) = {flops:.4g} flop (time: factor2(implicit) - factor)",
                          "traffic": None}
         dom = max(roofs, key=lambda kk: {"gram": ti - t2}.get(kk, per_ms.get(kk, 0.0)))
@@ -506,16 +581,19 @@ def run(args):
         # + check_diag + solve
         line["gpu_launches"] = (plan.launches_per_factor(m_local) + 10) * args.steps
         line["e2e"] = None
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and not args.no_cpu_baseline:   # rank 0's host cores (the other ranks wait below)
         rows, dt_s, cores = _cpu_sample_rate(X, cfg, args.cpu_seconds, args.algo, l_red, tau_rr)
         fn = {"rcholqr2": "factor2", "rcholqr_reduced": "factor_reduced", "rcholqr_rr": "factor_rr",
               "rcholqr_rr2": "factor_rr2"}.get(args.algo,
                                                                                                        "factor")
         line["cpu_baseline"] = {"value": rows * n * s_x / dt_s / 1e9, "unit": "GB/s", "cores": cores,
                                 "kind": "oracle", "seconds": dt_s,
-                                "sample": f"oracle.{fn} on the leading {rows} rows of the same X"}
+                                "sample": f"oracle.{fn} on the leading {rows} rows of rank 0's block of the same X "
+                                          f"(measured after the timed region)"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
     plan.close()
     if comm is not None:
         rcq.comm_destroy(comm)
@@ -529,11 +607,13 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-budget-s", type=float, default=240.0,
+                    help="--impl reference: wall-clock budget of the whole warm-up + timed oracle run")
     ap.add_argument("--algo", default="rcholqr",
                     choices=["rcholqr", "rcholqr2", "rcholqr_reduced", "rcholqr_rr", "rcholqr_rr2"],
                     help="Alg. 2 (default, the north star), Alg. 3 RCholeskyQR2 (orthonormal Q) or Alg. 5 "

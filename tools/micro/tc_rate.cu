@@ -75,16 +75,25 @@ void run(int G, int sbo_b = 128, int nreg = 4, int shift = N) {
   const int iters = 2000;
   rate<KIND, N><<<148, 128>>>(iters, G, out, sbo_b, nreg, shift);
   cudaDeviceSynchronize();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0); cudaEventCreate(&e1);
+  cudaEventRecord(e0);
   rate<KIND, N><<<148, 128>>>(iters, G, out, sbo_b, nreg, shift);
+  cudaEventRecord(e1);
   cudaError_t e = cudaDeviceSynchronize();
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
   if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return; }
   double s = 0;
   for (int i = 0; i < 148; ++i) s += out[i];
   s /= 148;
   const double per = s / ((double)iters * G);
   const double macs = 128.0 * N * (KIND == 0 ? 32 : 16);
-  printf("{\"nreg\":%d,\"shift\":%d,\"sbo_b\":%d,\"kind\":\"%s\",\"N\":%d,\"G\":%d,\"cyc_per_mma\":%.1f,\"mac_per_cyc\":%.0f}\n", nreg, shift, sbo_b, KIND == 0 ? "i8" : "f16", N, G,
-         per, macs / per);
+  // chip-level rate from device events (all 148 SMs issue concurrently) and the SM clock it implies
+  const double tops = 2.0 * macs * iters * G * 148 / (ms * 1e-3) / 1e12;
+  const double mhz = s / (ms * 1e-3) / 1e6;
+  printf("{\"nreg\":%d,\"shift\":%d,\"sbo_b\":%d,\"kind\":\"%s\",\"N\":%d,\"G\":%d,\"cyc_per_mma\":%.1f,\"mac_per_cyc\":%.0f,"
+         "\"tops_chip\":%.1f,\"sm_mhz\":%.0f}\n", nreg, shift, sbo_b, KIND == 0 ? "i8" : "f16", N, G, per, macs / per, tops, mhz);
   cudaFree(out);
 }
 
