@@ -427,7 +427,7 @@ __global__ void sketch_reduce_kernel(const double* __restrict__ part, const doub
                                      double* __restrict__ P, int* status, const int* flag, int* flag_seen) {
   // record (for rcholqr_last_path) that a tensor-core sketch raised its overflow flag and the guarded
   // CUDA-core kernel recomputed the partials
-  if (flag_seen && blockIdx.x == 0 && threadIdx.x == 0 && *flag) atomicOr(flag_seen, 1);
+  if (flag && flag_seen && blockIdx.x == 0 && threadIdx.x == 0 && *flag) atomicOr(flag_seen, 1);
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < kn;
        idx += (int64_t)gridDim.x * blockDim.x) {
     double s = 0.0, c = 0.0;                    // compensated (TwoSum) sum over the splits
