@@ -700,7 +700,7 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
       guard = flag;
       pb |= kPathSketchTC;
     }
-    pb |= kPathSketchCudaCore;
+    if (!guard) pb |= kPathSketchCudaCore;
     auto launch = [&](auto* tag) -> cudaError_t {
       using TX = std::remove_pointer_t<decltype(tag)>;
       auto go = [&](auto kern, int cpl) -> cudaError_t {

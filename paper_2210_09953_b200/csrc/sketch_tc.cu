@@ -15,11 +15,13 @@
 // flag and the register sparse kernel (sketch.cu) recomputes the whole sketch, so the result never
 // depends on that heuristic.
 //
-// Roles (1 CTA per SM, 12 warps): warp 0 lane 0 issues tcgen05.mma and commits to mbarriers;
+// Roles (1 CTA per SM, 22 warps): warp 0 lane 0 issues tcgen05.mma and commits to mbarriers;
 // warp 1 lane 0 streams X rows into a raw shared-memory ring with cp.async.bulk (mbarrier
-// complete_tx); warps 2..11 build each stage's operands -- the E tile from Philox (theta.cuh) and
-// the D digit planes -- in the canonical K-major SWIZZLE_NONE core-matrix layout.  At the end
-// warps 0..3 drain TMEM (tcgen05.ld, lane = Theta row) and write the fp64 partial sums.
+// complete_tx); warps 2..21 build each stage's operands -- the D digit planes (two groups of 8 warps
+// taking alternate stages) and the E tile from Philox (theta.cuh; two groups of 2 warps) -- in the
+// canonical K-major SWIZZLE_NONE core-matrix layout.  At the end warps 0..3 drain TMEM (tcgen05.ld,
+// lane = Theta row) and write the fp64 partial sums.  (Round 1 had one digit group of 8 warps: the
+// digit warps were latency-bound at 44% issue with 3.5 warps per scheduler; C4 sketch 5.45 ms.)
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdlib>
@@ -34,9 +36,10 @@ namespace rcq {
 constexpr int STC_M = 128;        // Theta rows per CTA (MMA M = TMEM lanes)
 constexpr int STC_N = 64;         // X columns per CTA (MMA N)
 constexpr int STC_KC = 64;        // X rows per stage (2 MMA k-steps of 32)
-constexpr int STC_DWARPS = 8;     // digit-plane warps (2..9): one (column, 16-row group) task per thread
-constexpr int STC_EWARPS = 4;     // E-tile warps (10..13): two groups alternating stages, one X row per lane
-constexpr int STC_THREADS = 32 * (2 + STC_DWARPS + STC_EWARPS);
+constexpr int STC_DWARPS = 8;     // digit-plane warps per stage group: one (column, 16-row group) task per thread
+constexpr int STC_DGROUPS = 2;    // digit groups (warps 2..9, 10..17) alternating stages, like the E groups
+constexpr int STC_EWARPS = 4;     // E-tile warps (18..21): two groups alternating stages, one X row per lane
+constexpr int STC_THREADS = 32 * (2 + STC_DGROUPS * STC_DWARPS + STC_EWARPS);
 static_assert(32 * STC_DWARPS == STC_N * (STC_KC / 16), "one digit task per thread");
 static_assert(16 * STC_EWARPS == STC_KC, "one X row per E-warp lane, two warp groups");
 
@@ -243,26 +246,27 @@ sketch_sparse_tc_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx,
       }
       __syncwarp();
     }
-  } else if (warp < 2 + STC_DWARPS) {
+  } else if (warp < 2 + STC_DGROUPS * STC_DWARPS) {
     // ---------------------------------------------------------------- digit planes
-    const int dt = tid - 64;
+    const int dgrp = (warp - 2) / STC_DWARPS;            // stages c = dgrp (mod 2)
+    const int dt = tid - 64 - dgrp * 32 * STC_DWARPS;
     const int j = dt % STC_N, kg = dt / STC_N;           // fixed task: column j, rows kg*16 .. +15
     ColParam cp{};
-    if (nstages > 0) {                                   // column scales from the first stage
+    if (nstages > 0) {                                   // column scales from the first stage (both groups)
       tc::mbar_wait(&rfull[0], 0u);
       const int rows0 = (int)min((int64_t)STC_KC, i_end - i_begin);
       const TX* raw = raw_base;
-      for (int u = dt; u < rows0 * n; u += 32 * STC_DWARPS) atomicMax(&col_max[u % n], hi_abs(raw[u]));
-      tc::named_bar(1, 32 * STC_DWARPS);
+      for (int u = tid - 64; u < rows0 * n; u += 32 * STC_DGROUPS * STC_DWARPS) atomicMax(&col_max[u % n], hi_abs(raw[u]));
+      tc::named_bar(1, 32 * STC_DGROUPS * STC_DWARPS);
       cp = col_param<TX>(col_max[j < n ? j : 0]);
-      if (kg == 0 && j < n) col_exp[j] = cp.e;
+      if (dgrp == 0 && kg == 0 && j < n) col_exp[j] = cp.e;
     }
     int dst_off[D];
 #pragma unroll
     for (int t = 0; t < D; ++t)
       dst_off[t] = C::E_BYTES + C::grp(t) * C::G0_BYTES + cm_off(C::brow(t) + j, kg * 16, C::grp(t) ? C::N1 : C::N0);
     uint32_t acc_or = 0u, acc_and = 0xFFFFFFFFu, amax = 0u;   // overflow detection
-    for (int c = 0; c < nstages; ++c) {
+    for (int c = dgrp; c < nstages; c += STC_DGROUPS) {
       const int s = c % F::DIG, sr = c % F::RAW;
       const int64_t i0 = i_begin + (int64_t)c * STC_KC;
       const int rows = (int)min((int64_t)STC_KC, i_end - i0);
@@ -321,7 +325,7 @@ sketch_sparse_tc_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx,
     // Two groups of two warps take alternate stages (group g: stages c = g mod 2), each lane one X
     // row; the Philox draw of a row is computed before its slot is awaited, so the generator
     // latency overlaps the MMAs still reading that slot.
-    const int ew = warp - 2 - STC_DWARPS;
+    const int ew = warp - 2 - STC_DGROUPS * STC_DWARPS;
     const int grp = ew >> 1, half = ew & 1;               // rows half*32 + lane of stages c = grp (mod 2)
     const int ii = half * 32 + lane;
     const int zoff = half * 2 * STC_M * 16;               // k-blocks 2half, 2half+1 of the E tile

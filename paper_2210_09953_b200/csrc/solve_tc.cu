@@ -47,7 +47,7 @@ constexpr int QT_DA = 6;        // X digits
 constexpr int QT_DB = 7;        // W digits
 constexpr int QT_LEV = 7;       // levels kept (a + b <= 6)
 constexpr int QT_NB = QT_DB * QT_G;             // stacked W digit rows of one group (224)
-constexpr int QT_DWARPS = 8;    // digit warps 10..17
+constexpr int QT_DWARPS = 8;    // digit warps of the K-half producers (64 < n <= 128)
 constexpr int QT_RWARPS = 8;    // drain warps 2..9: two sets of four (one per TMEM level buffer)
 constexpr int QT_KMAX_ALL = 128;
 static_assert(2 * QT_LEV * QT_G <= 512, "two TMEM level buffers");
@@ -74,7 +74,10 @@ struct QCfg {
   // n <= 64: 16 drain warps (two per lane quadrant per TMEM buffer, 16 columns each) -- the drain
   // is bound by TMEM read concurrency; 64 < n <= 128: 8 (registers: the K-half producers need 96)
   static constexpr int RW = TMA_RAW ? 16 : QT_RWARPS;
-  static constexpr int THREADS = 32 * (2 + RW + QT_DWARPS);
+  // digit warps: 6 for the TMA ring (a strided task loop; fewer warps leave the drain more registers),
+  // 8 for the K-half producers (their row mapping assumes 8)
+  static constexpr int DW = TMA_RAW ? 6 : QT_DWARPS;
+  static constexpr int THREADS = 32 * (2 + RW + DW);
   static constexpr int DCOLS = QT_G * 8 / RW;     // columns of a group per drain warp (16 or 32)
   static constexpr int QS = HALF ? QT_RWARPS * 32 * 8 * 4 : RW * 32 * DCOLS * 4;   // HALF: 32 x 8 tile per drain warp
   static constexpr size_t SMEM =
@@ -118,6 +121,35 @@ solve_tc_prep_kernel(const double* __restrict__ W, int n, int kpad, int8_t* __re
 }
 
 // ---------------------------------------------------------------------------------------------
+// Epilogue arithmetic.  The levels are exact int32 (|acc_L| < 2^23: <= 6 pairs x 64 terms x 2^14, and
+// |acc_0|, |acc_1| < 2^18, 2^21 from the small leading digits), and
+//     Q_ij = 2^(e_i - 46 + e_j - 54) sum_L acc_L 256^(11 - L) = v 2^(e_i + e_j - 60),
+//     v    = sum_L acc_L 256^(6 - L)  (up to ~2^66: not an int64).
+// The epilogue forms T = acc_0 2^40 + acc_1 2^32 + acc_2 2^24 + acc_3 2^16 + acc_4 2^8 + acc_5 +
+// floor(acc_6 / 2^8) EXACTLY in int64 (|T| < 2^60; T 2^8 differs from v by acc_6 mod 2^8 < 2^8, i.e.
+// 2^-37 of a typical |v| -- far below the fp32 rounding of Q, the same order as the dropped levels),
+// converts it once with round-to-nearest (I2F.F32.S64) and scales by 2^(e_i + e_j - 52) with one FMUL
+// whose factor is built from the two exponents by one integer add: Q_ij = RN(T) 2^(e_i + e_j - 52).
+// Round 1 combined the levels in fp64 (four magic-constant conversions, three DFMAs and two DMULs per
+// output); this form needs ~10 integer-pipe instructions, one conversion and one FMUL.
+__device__ __forceinline__ long long qt_combine(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t a4,
+                                                uint32_t a5, uint32_t a6) {
+  long long t = (long long)((int)a6 >> 8);
+  t += (long long)(int)a5;
+  t += (long long)(int)a4 * 256;
+  t += (long long)(int)a3 * 65536;
+  t += (long long)(int)a2 * 16777216;
+  t += (long long)(int)(a0 * 256u + a1) << 32;
+  return t;
+}
+// fast: every 2^(e_i + e_j - 52) of this warp is a normal fp32 (row_bits = (e_i + 75) << 23,
+// col_bits = e_j << 23); else the exact fp64 route (any exponent range)
+__device__ __noinline__ float qt_scale_slow(long long t, int ei, int ej) { return (float)ldexp((double)t, ei + ej - 52); }
+__device__ __forceinline__ float qt_scale(long long t, bool fast, int row_bits, int col_bits, int ei, int ej) {
+  if (fast) return __ll2float_rn(t) * __int_as_float(row_bits + col_bits);
+  return qt_scale_slow(t, ei, ej);
+}
+
 template <int KMAX>
 __global__ void __launch_bounds__(QCfg<KMAX>::THREADS, 1)
 solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap qmap,
@@ -147,7 +179,8 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
   // before still reads its scales (a slot is free once the MMAs of tile t complete, and those
   // follow every drain of tile t - 2; see the TMEM buffer waits below)
   int* rexp = reinterpret_cast<int*>(tmem_slot + 4);                          // [4][128]
-  double* wsc = reinterpret_cast<double*>(rexp + 4 * QT_M);             // [64] 2^(e_j - 60): column scale x 2^-(46+54-40)
+  int* cexp = rexp + 4 * QT_M;                                                // [KMAX] e_j (W column exponents)
+  int* crange = cexp + QT_KMAX_ALL;                                           // [2] min, max e_j
 
   const int groups = (n + QT_G - 1) / QT_G;
   const int64_t ntiles = (m + QT_M - 1) / QT_M;
@@ -156,13 +189,19 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
   const int lg_n = kpad / 16;                                                 // 16-column groups per row
 
   if (tid == 0) {
-    for (int s = 0; s < NSLOT; ++s) { tc::mbar_init(&dfull[s], QT_DWARPS); tc::mbar_init(&dempty[s], 1); }
-    for (int s = 0; s < QT_RAW; ++s) { tc::mbar_init(&rfull[s], 1); tc::mbar_init(&rempty[s], QT_DWARPS); }
+    for (int s = 0; s < NSLOT; ++s) { tc::mbar_init(&dfull[s], Cf::DW); tc::mbar_init(&dempty[s], 1); }
+    for (int s = 0; s < QT_RAW; ++s) { tc::mbar_init(&rfull[s], 1); tc::mbar_init(&rempty[s], Cf::DW); }
     for (int b = 0; b < 2; ++b) { tc::mbar_init(&tready[b], 1); tc::mbar_init(&tfree[b], Cf::RW / 2); }
     tc::mbar_init(wbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (tid < groups * QT_G) wsc[tid] = ldexp(1.0, wexp[tid] - 60);
+  if (tid < 2) crange[tid] = tid == 0 ? INT32_MAX : INT32_MIN;
+  __syncthreads();
+  if (tid < groups * QT_G) {
+    const int ej = wexp[tid];
+    cexp[tid] = ej;
+    if (tid < n) { atomicMin(&crange[0], ej); atomicMax(&crange[1], ej); }
+  }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(tc::smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -248,30 +287,23 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
         if (buf != dset) continue;
         tc::mbar_wait(&tready[buf], (uint32_t)(u & 1));
         asm volatile("tcgen05.fence::after_thread_sync;\n");
-        // Levels are exact int32 with |acc_L| < 2^23 (<= 6 pairs x 64 terms x 2^14), so adjacent
-        // levels pair exactly in int32 (acc_L 256 + acc_{L+1} < 2^31): four values per output,
-        // each converted to fp64 by the 2^52 magic constant (LOP3 + DADD, no I2F), then combined
-        // by three DFMAs -- the fewest issue slots per output of the variants tried.
-        static_assert(QT_LEV == 7, "pairing below assumes 7 levels");
+        // the seven exact int32 levels of an output combine into one int64 (qt_combine); the warp
+        // takes the fp32 scaling route unless some 2^(e_i + e_j - 52) of its rows leaves the normal range
+        static_assert(QT_LEV == 7, "qt_combine assumes 7 levels");
         if constexpr (Cf::HALF) {
           // 8 columns at a time: all 7 level loads in flight before one wait; each 32-row x 8-column
           // fp32 chunk is staged in a 1 KB tile (all the room the K-half ring leaves) and written
           // by a 2D TMA store; the TMEM buffer is released right after the last chunk's loads
-          const double si = __hiloint2double((rexp[(tt & 3) * QT_M + row_l] + 1023) << 20, 0);   // 2^e_i
+          const int ei = rexp[(tt & 3) * QT_M + row_l];
+          const int rbits = (ei + 75) << 23;
+          const bool fast = __all_sync(0xffffffffu, ei + crange[0] + 75 >= 1 && ei + crange[1] + 75 <= 254);
           const uint32_t lv = lb + buf * (QT_LEV * QT_G);
           unsigned char* qs = qstage + (warp - 2) * (32 * 8 * 4);
 #pragma unroll
           for (int h = 0; h < QT_G / 8; ++h) {
             uint32_t lvl[QT_LEV][8];
 #pragma unroll
-            for (int L = 0; L < QT_LEV; ++L) {
-              if (dbg & 4) {
-#pragma unroll
-                for (int c = 0; c < 8; ++c) lvl[L][c] = 0u;
-              } else {
-                tc::ld8(lv + L * QT_G + h * 8, lvl[L]);
-              }
-            }
+            for (int L = 0; L < QT_LEV; ++L) tc::ld8(lv + L * QT_G + h * 8, lvl[L]);
             tc::wait_ld();
             if (h == QT_G / 8 - 1) {
               asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -281,14 +313,9 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
             float o[8];
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-              double f[4];
-#pragma unroll
-              for (int pp = 0; pp < 4; ++pp) {
-                const uint32_t pv = pp < 3 ? lvl[2 * pp][c] * 256u + lvl[2 * pp + 1][c] : lvl[6][c];
-                f[pp] = __hiloint2double(0x43300000, (int)(pv ^ 0x80000000u)) - 4503601774854144.0;   // 2^52 + 2^31
-              }
-              const double v = fma(f[0], 0x1p40, fma(f[1], 0x1p24, fma(f[2], 256.0, f[3])));
-              o[c] = __double2float_rn(v * si * wsc[g * QT_G + h * 8 + c]);
+              const int ej = cexp[g * QT_G + h * 8 + c];
+              o[c] = qt_scale(qt_combine(lvl[0][c], lvl[1][c], lvl[2][c], lvl[3][c], lvl[4][c], lvl[5][c], lvl[6][c]),
+                              fast, rbits, ej << 23, ei, ej);
             }
             if (lane == 0) tc::bulk_wait_read0();            // previous chunk's store has read the tile
             __syncwarp();
@@ -304,43 +331,33 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
           continue;
         }
         constexpr int DC = Cf::DCOLS;
-        double v[DC];
+        float o[DC];
         const uint32_t lv = lb + buf * (QT_LEV * QT_G) + dc0;
-        if (dbg & 4) {
-#pragma unroll
-          for (int c = 0; c < DC; ++c) v[c] = 0.0;
-        } else
-#pragma unroll
-        for (int h = 0; h < DC / 8; ++h) {
-          uint32_t p[4][8];
-#pragma unroll
-          for (int pp = 0; pp < 3; ++pp) {
-            uint32_t hi8[8], lo8[8];
-            tc::ld8(lv + (2 * pp) * QT_G + h * 8, hi8);
-            tc::ld8(lv + (2 * pp + 1) * QT_G + h * 8, lo8);
-            tc::wait_ld();
-#pragma unroll
-            for (int c = 0; c < 8; ++c) p[pp][c] = hi8[c] * 256u + lo8[c];
-          }
-          tc::ld8(lv + 6 * QT_G + h * 8, p[3]);
-          tc::wait_ld();
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            double f[4];
-#pragma unroll
-            for (int pp = 0; pp < 4; ++pp)
-              f[pp] = __hiloint2double(0x43300000, (int)(p[pp][c] ^ 0x80000000u)) - 4503601774854144.0;   // 2^52 + 2^31
-            v[h * 8 + c] = fma(f[0], 0x1p40, fma(f[1], 0x1p24, fma(f[2], 256.0, f[3])));
-          }
-        }
         // row scale read before the buffer is released: the rexp ring slot is reused only after
         // later MMAs, which wait on this release
-        const double si = __hiloint2double((rexp[(tt & 3) * QT_M + row_l] + 1023) << 20, 0);   // 2^e_i
-        asm volatile("tcgen05.fence::before_thread_sync;\n");
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&tfree[buf]);       // TMEM buffer free; the stores below need no TMEM
+        const int ei = rexp[(tt & 3) * QT_M + row_l];
+        const int rbits = (ei + 75) << 23;
+        const bool fast = __all_sync(0xffffffffu, ei + crange[0] + 75 >= 1 && ei + crange[1] + 75 <= 254);
+#pragma unroll
+        for (int h = 0; h < DC / 8; ++h) {
+          uint32_t lvl[QT_LEV][8];                           // all seven levels in flight before one wait
+#pragma unroll
+          for (int L = 0; L < QT_LEV; ++L) tc::ld8(lv + L * QT_G + h * 8, lvl[L]);
+          tc::wait_ld();
+          if (h == DC / 8 - 1) {                             // TMEM buffer free; the stores below need no TMEM
+            asm volatile("tcgen05.fence::before_thread_sync;\n");
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tfree[buf]);
+          }
+#pragma unroll
+          for (int c = 0; c < 8; ++c) {
+            const int ej = cexp[g * QT_G + dc0 + h * 8 + c];
+            o[h * 8 + c] = qt_scale(qt_combine(lvl[0][c], lvl[1][c], lvl[2][c], lvl[3][c], lvl[4][c], lvl[5][c],
+                                               lvl[6][c]), fast, rbits, ej << 23, ei, ej);
+          }
+        }
         {
-          // stage this warp's 32 rows x 32 columns (fp32) in shared memory with the 128-byte swizzle
+          // stage this warp's 32 rows x DC columns (fp32) in shared memory with the 128-byte swizzle
           // (16-byte chunk c of row r at chunk c ^ (r & 7): conflict-free STS.128), then one 2D TMA
           // store writes them; TMA clips rows >= m and columns >= n.
           unsigned char* qs = qstage + (warp - 2) * (32 * DC * 4);
@@ -348,11 +365,7 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
           __syncwarp();
 #pragma unroll
           for (int c = 0; c < DC; c += 4) {
-            float o4[4];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {   // exact power-of-two scale 2^(e_i - 46 + e_j - 54 + 40)
-              o4[q] = __double2float_rn(v[c + q] * si * wsc[g * QT_G + dc0 + c + q]);   // v carries 256^(6-L)
-            }
+            const float o4[4] = {o[c], o[c + 1], o[c + 2], o[c + 3]};
             // 32-column rows: 128-byte swizzle (conflict-free); 16-column rows: plain 64-byte rows
             const int off = DC == 32 ? lane * 128 + (((c >> 2) ^ (lane & 7)) << 4) : lane * (DC * 4) + c * 4;
             *reinterpret_cast<float4*>(qs + off) = make_float4(o4[0], o4[1], o4[2], o4[3]);
@@ -431,7 +444,7 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
         tc::mbar_wait(&rfull[sr], (uint32_t)((tt / QT_RAW) & 1));
         const float* raw = raw_base + (size_t)sr * QT_M * QT_RS_MAX;
         const int rs = kpad + 4;                                         // raw row pitch
-        for (int task = dt; task < ntask; task += 32 * QT_DWARPS) {
+        for (int task = dt; task < ntask; task += 32 * Cf::DW) {
           int lg, i;
           task_pos(task, lg, i);
           float x[16];

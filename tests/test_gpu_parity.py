@@ -158,11 +158,11 @@ def test_sketch_gauss_tc_headroom_overflow(cuda, monkeypatch, dt, case, chunked)
     if case == "spike":
         X[1000::4099, :] *= 1e6
     else:
-        # column 7 is zero but for two rows 43 apart: whatever the split boundaries, one of them lies
-        # outside its split's leading 32 rows with a zero (or 1e6-times smaller) column scale there
+        # column 7 is zero but for a 100-row ramp x = 2^t: whatever the split (and row-chunk) boundaries,
+        # a split that reaches 5+ rows past its leading 32 rows inside the ramp sees |x| >= 32x its head
+        # maximum (or a zero head), above the 16x headroom
         X[:, 7] = 0.0
-        X[123_457, 7] = 1.0
-        X[123_500, 7] = 1e6
+        X[150_000:150_100, 7] = 2.0 ** np.arange(100)
     plan = _plan(n, k, dt)
     Pg = _np(plan.sketch(_t(X)))
     path = plan.last_path()
