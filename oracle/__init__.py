@@ -15,6 +15,8 @@ Parity status of each oracle function ("Oracle pins"):
   sparse_col         pinned: structural invariants (one row per block, +-1/sqrt(zeta)), chi^2
   sketch             pinned: exact rational Theta X on tiny inputs, n=1 closed form, linearity,
                      partition invariance
+  sketch_entry       pinned: exact rational sums (Gaussian, sparse-sign incl. zeta > 64, Rademacher,
+                     SRHT), bitwise equal to sketch across 65,536-row blocks, NaN on bad arguments
   householder        pinned: SPEC examples, LAPACK QR (sign-normalised), mpmath 50-digit QR
   forward_subst      pinned: SPEC examples, R = I, scipy solve_triangular, Higham Thm 8.5 bound
   factor             pinned: cond(Q) = cond(Theta U) identity, eq:main1 residual, metamorphic

@@ -81,7 +81,7 @@ std::vector<uint64_t> srht_rows_host(uint64_t seed, int k) {
 // Which tall-solve kernels serve n columns of dtype (the plan's n, or Alg. 7's rank r).
 struct SolvePlan {
   TrsmLaunch tr{};
-  int res_tm = 0, warp_solve = 0, stream_tb = 0;
+  int pairs = 0, stream_tb = 0;
   bool solve_tc = false;
   bool mstream = false;   // 128 < n <= 256: warp-pair substitution with M streamed per column block
 };
@@ -91,10 +91,9 @@ struct rcholqr_plan_s {
   int sms = 0;
   size_t smem_optin = 0;
   SketchLaunch sk{};
-  // tall-solve kernels for n columns: TrsmLaunch tr (R^{-1} GEMM); res_tm > 0: blocked-substitution
-  // resident solve with this row tile; warp_solve > 0: warp-independent blocked substitution with this
-  // many warps/CTA; stream_tb > 0: streamed blocked substitution (fp64, n > 128) with this block width;
-  // solve_tc: fp32 X, n <= 64, tcgen05 digit solve Q = X R^{-1} (solve_tc.cu)
+  // tall-solve kernels for n columns: TrsmLaunch tr (R^{-1} GEMM); pairs > 0: warp-pair blocked
+  // substitution with this many pairs per CTA; stream_tb > 0: streamed blocked substitution (fp64,
+  // n > 256) with this block width; solve_tc: fp32 X, n <= 128, tcgen05 digit solve (solve_tc.cu)
   SolvePlan sp{};
   void* xdig = nullptr;     // pre-split X digit planes of the tcgen05 Gaussian sketch (grown on demand)
   // RCholeskyQR2 (rcqr2.cu): Gram partials, A, Cholesky work, R', R1, and Q1 (grown on demand)
@@ -247,23 +246,19 @@ rcholqr_status do_sketch(rcholqr_plan p, const void* X, int64_t m, int64_t ro, i
   return RCHOLQR_OK;
 }
 
+// n <= 128: warp-pair blocked substitution (or the tcgen05 digit solve for fp32 X); 128 < n <= 256:
+// streamed-M substitution; fp64 n > 256: column-block GEMMs; fp32 n > 256: the R^{-1} GEMM kernel.
 SolvePlan plan_solve(int n, int dtype, size_t smem_optin) {
   SolvePlan s;
   s.tr = plan_trsm(n, dtype, smem_optin);
-  s.res_tm = trsm_resident_tm(n, dtype, smem_optin);
-  s.warp_solve = trsm_warp_count(n, smem_optin);
-  s.mstream = s.warp_solve == 0 && s.res_tm == 0 && trsm_mstream_applicable(n, smem_optin);
-  if (s.warp_solve == 0 && s.res_tm == 0 && !s.mstream && dtype == RCHOLQR_F64) s.stream_tb = n < 512 ? 64 : 128;
-  if (const char* f = getenv("RCHOLQR_SOLVE")) {  // experiments: 0 = inverse GEMM, 1 = CTA-resident, 2 = warp
-    const int v = atoi(f);
-    if (v != 2) s.warp_solve = 0;
-    if (v == 0) { s.res_tm = 0; s.stream_tb = 0; }
-  }
+  s.pairs = trsm_pair_count(n, smem_optin);
+  s.mstream = s.pairs == 0 && trsm_mstream_applicable(n, smem_optin);
+  if (s.pairs == 0 && !s.mstream && dtype == RCHOLQR_F64) s.stream_tb = n < 512 ? 64 : 128;
   s.solve_tc = solve_tc_applicable(dtype, n);
   return s;
 }
 
-// Step 3: triangular prep + tall solve (blocked substitution when resident, else R^{-1} GEMM).  `n_cols`
+// Step 3: triangular prep + tall solve (the kernels plan_solve picked).  `n_cols`
 // > 0 solves with that many columns (R n_cols x n_cols) instead of the plan's n.
 rcholqr_status solve(rcholqr_plan p, const void* X, int64_t m, int64_t ldx, const double* R, void* Q, int64_t ldq,
                      cudaStream_t st, bool timed, int n_cols = 0) {
@@ -308,14 +303,10 @@ rcholqr_status solve(rcholqr_plan p, const void* X, int64_t m, int64_t ldx, cons
                            p->status_d, st));
       }
     }
-  } else if (sp.warp_solve > 0) {
+  } else if (sp.pairs > 0) {
     CU(launch_tri_prep_blocked(R, n, p->W, p->status_d, st));
     if (timed && p->timing) cudaEventRecord(p->ev[5], st);
-    if (m > 0) CU(launch_trsm_warp(sp.warp_solve, X, p->d.dtype, m, n, ldx, p->W, Q, ldq, p->status_d, p->sms, st));
-  } else if (sp.res_tm > 0) {
-    CU(launch_tri_prep_blocked(R, n, p->W, p->status_d, st));
-    if (timed && p->timing) cudaEventRecord(p->ev[5], st);
-    if (m > 0) CU(launch_trsm_resident(sp.res_tm, X, p->d.dtype, m, n, ldx, p->W, Q, ldq, p->status_d, p->sms, st));
+    if (m > 0) CU(launch_trsm_pairs(sp.pairs, X, p->d.dtype, m, n, ldx, p->W, Q, ldq, p->status_d, p->sms, st));
   } else {
     CU(launch_tri_inverse(R, n, p->W, p->status_d, st));
     if (timed && p->timing) cudaEventRecord(p->ev[5], st);

@@ -7,6 +7,14 @@
 
 namespace rcq {
 
+// Ablation switches of the tensor-core kernels (role work switched off, RCHOLQR_*_DEBUG): compiled in only
+// with -DRCHOLQR_ABLATION (tools/ experiments); production builds fold them to 0 and drop the branches.
+#ifdef RCHOLQR_ABLATION
+constexpr bool kAblation = true;
+#else
+constexpr bool kAblation = false;
+#endif
+
 // Status bits written by kernels into the plan's device status word (0 = OK).
 enum : int { kStNonfinite = 1, kStSingular = 2 };
 // Which kernels served the last call (rcholqr_last_path; the bits are RCHOLQR_PATH_* of rcholqr.h).
@@ -94,10 +102,9 @@ cudaError_t launch_theta_export(uint64_t seed, int k, int sketch, int zeta, int6
                                 const uint64_t* srht_s = nullptr);
 cudaError_t launch_check_diag(const double* R, int n, int* status, cudaStream_t st);
 // blocked substitution (default tall solve for n <= 128): M = [-R_{<J,J}; Winv_JJ] packed
-int trsm_resident_tm(int n, int dtype, size_t smem_optin);   // 0 = not applicable
-int trsm_warp_count(int n, size_t smem_optin);                 // 0 = not applicable
-cudaError_t launch_trsm_warp(int warps, const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M,
-                             void* Q, int64_t ldq, const int* status, int sms, cudaStream_t st);
+int trsm_pair_count(int n, size_t smem_optin);                 // warp pairs per CTA; 0 = not applicable
+cudaError_t launch_trsm_pairs(int pairs, const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M,
+                              void* Q, int64_t ldq, const int* status, int sms, cudaStream_t st);
 // 128 < n <= 256: warp-pair blocked substitution with M streamed per column block (trsm.cu)
 bool trsm_mstream_applicable(int n, size_t smem_optin);
 cudaError_t launch_trsm_mstream(const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M, void* Q,
@@ -144,7 +151,5 @@ cudaError_t launch_gather_x(const void* X, int dtype, int64_t m, int64_t ldx, co
 // out (cols x rows, ld ldo) = in^T (rows x cols, ld ldi), element size es (reduced.cu)
 cudaError_t launch_transpose(const void* in, int64_t rows, int64_t cols, int64_t ldi, void* out, int64_t ldo,
                              size_t es, cudaStream_t st);
-cudaError_t launch_trsm_resident(int tm, const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M,
-                                 void* Q, int64_t ldq, const int* status, int sms, cudaStream_t st);
 
 }  // namespace rcq

@@ -150,7 +150,8 @@ template <typename TX>
 __global__ void __launch_bounds__(GT_THREADS, 1)
 sketch_gauss_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int n, int64_t row_offset, int k,
                        uint64_t seed, int tiles_k, int tiles_n, int64_t rows_per_split, double* __restrict__ part,
-                       double* __restrict__ partc, int* overflow, int dbg) {
+                       double* __restrict__ partc, int* overflow, int dbg_in) {
+  const int dbg = kAblation ? dbg_in : 0;   // ablation switches (see internal.cuh)
   using C = GtCfg<TX>;
   static_assert(C::NB <= 256 && C::NB % 16 == 0 && C::LEV * C::KT <= 512, "MMA / TMEM shape");
   static_assert(C::TASKS_Z <= 32 * GT_TWARPS / 2, "one Theta task per group thread");
@@ -523,7 +524,8 @@ __global__ void __launch_bounds__(GP_THREADS, 1)
 sketch_gauss_tcp_kernel(const unsigned char* __restrict__ dig, const uint32_t* __restrict__ maxbits, int64_t m, int n,
                         int64_t row_offset, int k, uint64_t seed, int tiles_k, int tiles_n, int64_t rows_per_split,
                         int stages_per_split, double* __restrict__ part, double* __restrict__ partc, int accumulate,
-                        int dbg) {
+                        int dbg_in) {
+  const int dbg = kAblation ? dbg_in : 0;   // ablation switches (see internal.cuh)
   using C = typename GpCfg<TX>::G;
   using P = GpCfg<TX>;
   using F = GtFmt<TX>;
@@ -749,7 +751,7 @@ static cudaError_t launch_gtcp(const TX* X, int64_t m, int n, int64_t ldx, int64
   auto kern = sketch_gauss_tcp_kernel<TX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GpCfg<TX>::SMEM);
   if (e != cudaSuccess) return e;
-  static const int dbg = getenv("RCHOLQR_GTP_DEBUG") ? atoi(getenv("RCHOLQR_GTP_DEBUG")) : 0;   // ablations only
+  static const int dbg = !kAblation ? 0 : getenv("RCHOLQR_GTP_DEBUG") ? atoi(getenv("RCHOLQR_GTP_DEBUG")) : 0;   // ablations only
   kern<<<tiles_k * tiles_n * splits, GP_THREADS, GpCfg<TX>::SMEM, st>>>(dig, maxbits, m, n, ro, k, seed, tiles_k,
                                                                          tiles_n, rps, stages, part, partc, accumulate,
                                                                          dbg);
@@ -832,7 +834,7 @@ static cudaError_t launch_gtc(const TX* X, int64_t m, int n, int64_t ldx, int64_
   auto kern = sketch_gauss_tc_kernel<TX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GtCfg<TX>::SMEM);
   if (e != cudaSuccess) return e;
-  static const int dbg = getenv("RCHOLQR_GTC_DEBUG") ? atoi(getenv("RCHOLQR_GTC_DEBUG")) : 0;   // ablations only
+  static const int dbg = !kAblation ? 0 : getenv("RCHOLQR_GTC_DEBUG") ? atoi(getenv("RCHOLQR_GTC_DEBUG")) : 0;   // ablations only
   kern<<<tiles_k * tiles_n * splits, GT_THREADS, GtCfg<TX>::SMEM, st>>>(map, m, n, ro, k, seed, tiles_k, tiles_n, rps,
                                                                          part, partc, overflow, dbg);
   return cudaGetLastError();

@@ -147,8 +147,9 @@ __device__ __forceinline__ void split_words(double x, const ColParam& p, uint32_
 template <typename TX>
 __global__ void __launch_bounds__(STC_THREADS, 1)
 sketch_sparse_tc_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64_t row_offset, int k, int zeta,
-                        uint64_t seed, int tiles_k, int64_t rows_per_split, double* __restrict__ part, int* overflow, int dbg,
+                        uint64_t seed, int tiles_k, int64_t rows_per_split, double* __restrict__ part, int* overflow, int dbg_in,
                         const uint64_t* __restrict__ srht_s) {
+  const int dbg = kAblation ? dbg_in : 0;   // ablation switches (see internal.cuh)
   using C = StcCfg<TX>;
   using F = Fmt<TX>;
   constexpr int D = C::D;
@@ -492,7 +493,7 @@ static cudaError_t launch_stc(const TX* X, int64_t m, int n, int64_t ldx, int64_
   auto kern = sketch_sparse_tc_kernel<TX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)StcCfg<TX>::SMEM);
   if (e != cudaSuccess) return e;
-  static const int dbg = getenv("RCHOLQR_STC_DEBUG") ? atoi(getenv("RCHOLQR_STC_DEBUG")) : 0;   // ablations only
+  static const int dbg = !kAblation ? 0 : getenv("RCHOLQR_STC_DEBUG") ? atoi(getenv("RCHOLQR_STC_DEBUG")) : 0;   // ablations only
   kern<<<tiles_k * splits, STC_THREADS, StcCfg<TX>::SMEM, st>>>(X, m, n, ldx, ro, k, zeta, seed, tiles_k, rps, part,
                                                                  overflow, dbg, srht_s);
   return cudaGetLastError();

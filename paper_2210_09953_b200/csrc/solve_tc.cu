@@ -155,7 +155,8 @@ __global__ void __launch_bounds__(QCfg<KMAX>::THREADS, 1)
 solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap qmap,
                 const int8_t* __restrict__ wdig, const int* __restrict__ wexp, const float* __restrict__ X,
                 int64_t ldx, int64_t m, int n, int kpad, float* __restrict__ Q, int64_t ldq, int* status,
-                int dbg) {
+                int dbg_in) {
+  const int dbg = kAblation ? dbg_in : 0;   // ablation switches (see internal.cuh)
   using Cf = QCfg<KMAX>;
   constexpr int QT_DIG = Cf::DIG, QT_RAW = Cf::RAW > 0 ? Cf::RAW : 1, QT_A_TILE = Cf::A_TILE;
   constexpr int NSLOT = Cf::NSLOT, SLOT = Cf::SLOT_BYTES, H_TILE = Cf::H_TILE;
@@ -593,7 +594,7 @@ cudaError_t launch_solve_tc(const double* Winv, int n, const float* X, int64_t m
     return cudaErrorInvalidValue;
   const int64_t ntiles = (m + QT_M - 1) / QT_M;
   const int grid = (int)std::min<int64_t>(ntiles, sms);
-  static const int dbg = getenv("RCHOLQR_QTC_DEBUG") ? atoi(getenv("RCHOLQR_QTC_DEBUG")) : 0;   // ablations only
+  static const int dbg = !kAblation ? 0 : getenv("RCHOLQR_QTC_DEBUG") ? atoi(getenv("RCHOLQR_QTC_DEBUG")) : 0;   // ablations only
   auto go = [&](auto kern, size_t smem, int threads) -> cudaError_t {
     cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e2 != cudaSuccess) return e2;

@@ -315,171 +315,12 @@ cudaError_t launch_check_diag(const double* R, int n, int* status, cudaStream_t 
 // blocks inverted, which keeps the row-wise backward stability of substitution (an explicit full
 // R^{-1} lost 4x in ||I - (Theta Q)^T Theta Q|| at n=1024, kappa=1e12 -- DESIGN.md "Tall solve").
 // M (npad x npad) packs both operands: M[L,J] = -R_{L,J} (L < J), M[J,J] = Winv_JJ, 0 below.
-//
-// Resident variant (n <= 128): a persistent CTA keeps M in shared memory for its whole life and a
-// TM-row tile of X (widened to fp64, overwritten in place by Q) so the fp64 history Q_{<J} never
-// leaves the SM; the next tile's X is prefetched with cp.async while the current tile is solved.
 constexpr int TB = 32;           // diagonal block width
-constexpr int RES_THREADS = 256;
 
-__device__ __forceinline__ void cp_async4(void* s, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"((unsigned)__cvta_generic_to_shared(s)), "l"(g));
-}
-__device__ __forceinline__ void cp_async8(void* s, const void* g) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"((unsigned)__cvta_generic_to_shared(s)), "l"(g));
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
-struct ResLayout {
-  int ld, tld;
-  size_t m_bytes, a_bytes, t_bytes, raw_bytes;
-  __host__ __device__ ResLayout(int npad, int tm, int xs) {
-    ld = npad + 4;                       // (npad+4) = 4 or 12 (mod 16): fragment loads conflict-free
-    tld = TB + 4;
-    m_bytes = sizeof(double) * (size_t)npad * ld;
-    a_bytes = sizeof(double) * (size_t)tm * ld;
-    t_bytes = sizeof(double) * (size_t)tm * tld;
-    raw_bytes = (size_t)xs * tm * npad;
-  }
-  __host__ __device__ size_t total() const { return m_bytes + a_bytes + t_bytes + raw_bytes; }
-};
 
-template <typename TX, int TM>
-__global__ void __launch_bounds__(RES_THREADS, 1)
-trsm_resident_kernel(const TX* __restrict__ X, int64_t m, int n, int NPAD, int64_t ldx,
-                     const double* __restrict__ Mg, TX* __restrict__ Q, int64_t ldq, const int* status) {
-  if (*status) return;
-  const ResLayout C(NPAD, TM, (int)sizeof(TX));
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* Ms = reinterpret_cast<double*>(smem_raw);
-  double* As = reinterpret_cast<double*>(smem_raw + C.m_bytes);
-  double* Ts = reinterpret_cast<double*>(smem_raw + C.m_bytes + C.a_bytes);
-  TX* raw = reinterpret_cast<TX*>(smem_raw + C.m_bytes + C.a_bytes + C.t_bytes);
-  constexpr int STRIPS = TM / 16;
-  constexpr int NWARP = RES_THREADS / 32;
-  constexpr int WPS = NWARP / STRIPS;          // warps sharing one m16 strip
-  const int NBLK = (NPAD + TB - 1) / TB;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
-  const int strip = warp % STRIPS, wsub = warp / STRIPS;
-  const int64_t ntiles = (m + TM - 1) / TM;
-
-  for (int c = tid; c < NPAD * NPAD; c += RES_THREADS) Ms[(c / NPAD) * C.ld + (c % NPAD)] = Mg[c];
-
-  auto prefetch = [&](int64_t tile) {
-    if (tile >= ntiles) return;
-    const int64_t r0 = tile * TM;
-    for (int c = tid; c < TM * n; c += RES_THREADS) {
-      const int ii = c / n, jj = c % n;
-      if (r0 + ii < m) {
-        if (sizeof(TX) == 4) cp_async4(raw + ii * NPAD + jj, X + (r0 + ii) * ldx + jj);
-        else cp_async8(raw + ii * NPAD + jj, X + (r0 + ii) * ldx + jj);
-      }
-    }
-    cp_async_commit();
-  };
-
-  int64_t tile = blockIdx.x;
-  prefetch(tile);
-  for (; tile < ntiles; tile += gridDim.x) {
-    const int64_t r0 = tile * TM;
-    const int rows = (int)min((int64_t)TM, m - r0);
-    cp_async_wait_all();
-    __syncthreads();  // raw landed; previous tile fully consumed (As, Ts free)
-    for (int c = tid; c < TM * NPAD; c += RES_THREADS) {
-      const int ii = c / NPAD, jj = c % NPAD;
-      As[ii * C.ld + jj] = (ii < rows && jj < n) ? (double)raw[ii * NPAD + jj] : 0.0;
-    }
-    __syncthreads();
-    prefetch(tile + gridDim.x);   // overlaps with the solve of this tile
-
-    for (int J = 0; J < NBLK; ++J) {
-      const int c0 = J * TB;
-      const int bw = min(TB, NPAD - c0);       // block width (multiple of 8)
-      const int nt8 = bw / 8;
-      // n8 tiles of this block owned by this warp: t = wsub, wsub + WPS, ...
-      constexpr int MAXT = (TB / 8 + WPS - 1) / WPS;
-      double acc[MAXT][4];
-      const int arow = strip * 16 + g;
-#pragma unroll
-      for (int u = 0; u < MAXT; ++u) {
-        const int t = wsub + WPS * u;
-        if (t < nt8) {
-          const int col = c0 + 8 * t + 2 * t4;
-          acc[u][0] = As[arow * C.ld + col];
-          acc[u][1] = As[arow * C.ld + col + 1];
-          acc[u][2] = As[(arow + 8) * C.ld + col];
-          acc[u][3] = As[(arow + 8) * C.ld + col + 1];
-        }
-      }
-      // phase 1: T = X_J + Q_{<J} (-R_{<J,J})
-      for (int ks = 0; ks < c0 / 4; ++ks) {
-        const double a0 = As[arow * C.ld + 4 * ks + t4];
-        const double a1 = As[(arow + 8) * C.ld + 4 * ks + t4];
-#pragma unroll
-        for (int u = 0; u < MAXT; ++u) {
-          const int t = wsub + WPS * u;
-          if (t < nt8) dmma_16x8x4(acc[u], a0, a1, Ms[(4 * ks + t4) * C.ld + c0 + 8 * t + g]);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < MAXT; ++u) {
-        const int t = wsub + WPS * u;
-        if (t < nt8) {
-          const int col = 8 * t + 2 * t4;
-          Ts[arow * C.tld + col] = acc[u][0];
-          Ts[arow * C.tld + col + 1] = acc[u][1];
-          Ts[(arow + 8) * C.tld + col] = acc[u][2];
-          Ts[(arow + 8) * C.tld + col + 1] = acc[u][3];
-        }
-      }
-      __syncthreads();
-      // phase 2: Q_J = T_J Winv_JJ (Winv upper triangular: skip k-steps past the tile's columns)
-#pragma unroll
-      for (int u = 0; u < MAXT; ++u)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[u][e] = 0.0;
-      for (int ks = 0; ks < bw / 4; ++ks) {
-        const double a0 = Ts[arow * C.tld + 4 * ks + t4];
-        const double a1 = Ts[(arow + 8) * C.tld + 4 * ks + t4];
-#pragma unroll
-        for (int u = 0; u < MAXT; ++u) {
-          const int t = wsub + WPS * u;
-          if (t < nt8 && 4 * ks <= 8 * t + 7)
-            dmma_16x8x4(acc[u], a0, a1, Ms[(c0 + 4 * ks + t4) * C.ld + c0 + 8 * t + g]);
-        }
-      }
-      // Q_J -> shared history (fp64) and global (rounded once to TX)
-#pragma unroll
-      for (int u = 0; u < MAXT; ++u) {
-        const int t = wsub + WPS * u;
-        if (t < nt8) {
-          const int col = c0 + 8 * t + 2 * t4;
-          As[arow * C.ld + col] = acc[u][0];
-          As[arow * C.ld + col + 1] = acc[u][1];
-          As[(arow + 8) * C.ld + col] = acc[u][2];
-          As[(arow + 8) * C.ld + col + 1] = acc[u][3];
-          const int64_t gr = r0 + arow;
-          if (arow < rows) {
-            if (col < n) Q[gr * ldq + col] = to_out<TX>(acc[u][0]);
-            if (col + 1 < n) Q[gr * ldq + col + 1] = to_out<TX>(acc[u][1]);
-          }
-          if (arow + 8 < rows) {
-            if (col < n) Q[(gr + 8) * ldq + col] = to_out<TX>(acc[u][2]);
-            if (col + 1 < n) Q[(gr + 8) * ldq + col + 1] = to_out<TX>(acc[u][3]);
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  cp_async_wait_all();
-}
-
-// Warp-independent variant (default for n <= 128): every warp owns whole 16-row tiles and runs the
-// blocked substitution on them alone -- no CTA barrier after the one-time load of M -- with its
-// fp64 Q history in a private 16-row shared-memory slab.  The X values of block J+1 are
-// prefetched into registers while block J is solved.
+// X fragment loads of the warp-pair kernel below (the X values of block J+1 are prefetched into
+// registers while block J is solved).
 template <typename TX>
 __device__ __forceinline__ void load_x_frag(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64_t r0, int c,
                                             int g, TX (&v)[4]) {
@@ -490,108 +331,6 @@ __device__ __forceinline__ void load_x_frag(const TX* __restrict__ X, int64_t m,
   v[3] = (rb < m && c + 1 < n) ? __ldcs(X + rb * ldx + c + 1) : TX(0);
 }
 
-template <typename TX, int WARPS>
-__global__ void __launch_bounds__(32 * WARPS, 1)
-trsm_warp_kernel(const TX* __restrict__ X, int64_t m, int n, int NPAD, int64_t ldx, const double* __restrict__ Mg,
-                 TX* __restrict__ Q, int64_t ldq, const int* status) {
-  if (*status) return;
-  extern __shared__ __align__(16) double smem_w[];
-  const int LD = NPAD + 4;                       // = 4 or 12 (mod 16) doubles: fragment loads conflict-free
-  double* Ms = smem_w;                            // [NPAD][LD]
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t4 = lane & 3;
-  double* Aw = smem_w + (size_t)NPAD * LD + (size_t)warp * 16 * LD;   // this warp's [16][LD] slab
-  for (int c = threadIdx.x; c < NPAD * NPAD; c += 32 * WARPS) Ms[(c / NPAD) * LD + (c % NPAD)] = Mg[c];
-  __syncthreads();
-  const int NBLK = (NPAD + TB - 1) / TB;
-  const int64_t ntiles = (m + 15) / 16;
-  const int64_t gw = (int64_t)blockIdx.x * WARPS + warp, nw = (int64_t)gridDim.x * WARPS;
-  TX xn[TB / 8][4];                               // prefetched X fragments of the next block
-  auto prefetch = [&](int64_t tile, int J) {
-    const int c0 = J * TB;
-#pragma unroll
-    for (int u = 0; u < TB / 8; ++u) load_x_frag(X, m, n, ldx, tile * 16, c0 + 8 * u + 2 * t4, g, xn[u]);
-  };
-  if (gw < ntiles) prefetch(gw, 0);
-  for (int64_t tile = gw; tile < ntiles; tile += nw) {
-    const int64_t r0 = tile * 16;
-    for (int J = 0; J < NBLK; ++J) {
-      const int c0 = J * TB;
-      const int nt8 = min(TB, NPAD - c0) / 8;
-      double acc[TB / 8][4];
-#pragma unroll
-      for (int u = 0; u < TB / 8; ++u)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[u][e] = (double)xn[u][e];
-      // prefetch the next block (or the next tile's first block)
-      if (J + 1 < NBLK) prefetch(tile, J + 1);
-      else if (tile + nw < ntiles) prefetch(tile + nw, 0);
-      // phase 1: T_J = X_J + Q_{<J} (-R_{<J,J})
-      const double* arow = Aw + g * LD + t4;
-      if (nt8 == TB / 8) {             // full-width block: no per-MMA predicates (no WARPSYNC)
-#pragma unroll 4
-        for (int ks = 0; ks < c0 / 4; ++ks) {
-          const double a0 = arow[4 * ks], a1 = arow[8 * LD + 4 * ks];
-          const double* mrow = Ms + (4 * ks + t4) * LD + c0 + g;
-          double b[TB / 8];
-#pragma unroll
-          for (int u = 0; u < TB / 8; ++u) b[u] = mrow[8 * u];
-#pragma unroll
-          for (int u = 0; u < TB / 8; ++u) dmma_16x8x4(acc[u], a0, a1, b[u]);
-        }
-      } else {
-        for (int ks = 0; ks < c0 / 4; ++ks) {
-          const double a0 = arow[4 * ks], a1 = arow[8 * LD + 4 * ks];
-          const double* mrow = Ms + (4 * ks + t4) * LD + c0 + g;
-#pragma unroll
-          for (int u = 0; u < TB / 8; ++u)
-            if (u < nt8) dmma_16x8x4(acc[u], a0, a1, mrow[8 * u]);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < TB / 8; ++u) {
-        if (u < nt8) {
-          double* tp = Aw + g * LD + c0 + 8 * u + 2 * t4;
-          tp[0] = acc[u][0]; tp[1] = acc[u][1]; tp[8 * LD] = acc[u][2]; tp[8 * LD + 1] = acc[u][3];
-        }
-      }
-      __syncwarp();
-      // phase 2: Q_J = T_J Winv_JJ (upper triangular: skip k-steps past each 8-column tile)
-#pragma unroll
-      for (int u = 0; u < TB / 8; ++u)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[u][e] = 0.0;
-#pragma unroll
-      for (int ks = 0; ks < TB / 4; ++ks) {
-        if (4 * ks < 8 * nt8) {
-          const double a0 = arow[c0 + 4 * ks], a1 = arow[8 * LD + c0 + 4 * ks];
-          const double* mrow = Ms + (c0 + 4 * ks + t4) * LD + c0 + g;
-#pragma unroll
-          for (int u = 0; u < TB / 8; ++u)
-            if (u < nt8 && 4 * ks <= 8 * u + 7) dmma_16x8x4(acc[u], a0, a1, mrow[8 * u]);
-        }
-      }
-      __syncwarp();
-#pragma unroll
-      for (int u = 0; u < TB / 8; ++u) {
-        if (u < nt8) {
-          const int col = c0 + 8 * u + 2 * t4;
-          double* tp = Aw + g * LD + col;
-          tp[0] = acc[u][0]; tp[1] = acc[u][1]; tp[8 * LD] = acc[u][2]; tp[8 * LD + 1] = acc[u][3];
-          const int64_t ra = r0 + g, rb = r0 + g + 8;
-          if (ra < m) {
-            if (col < n) Q[ra * ldq + col] = to_out<TX>(acc[u][0]);
-            if (col + 1 < n) Q[ra * ldq + col + 1] = to_out<TX>(acc[u][1]);
-          }
-          if (rb < m) {
-            if (col < n) Q[rb * ldq + col] = to_out<TX>(acc[u][2]);
-            if (col + 1 < n) Q[rb * ldq + col + 1] = to_out<TX>(acc[u][3]);
-          }
-        }
-      }
-      __syncwarp();
-    }
-  }
-}
 
 // Warp-pair variant: two warps share one 16-row tile (each owns half of the 8-column MMA tiles of a
 // block), so 16 warps run with the same shared-memory slabs as 8 -- twice the warps per SMSP to
@@ -919,29 +658,14 @@ __global__ void tri_prep_blocked_kernel(const double* __restrict__ R, int n, int
 // ---------------------------------------------------------------------------------------------
 static size_t warp_smem(int npad, int warps) { return sizeof(double) * (size_t)(npad + 4) * (npad + 16 * warps); }
 
-int trsm_warp_count(int n, size_t smem_optin) {
+// Warp pairs per CTA of the blocked substitution for n <= 128 (fp64 X, or fp32 X off the tcgen05 path):
+// 8 when their Q-history slabs and M fit in shared memory (n <= 112), else 4 (n <= 128).
+int trsm_pair_count(int n, size_t smem_optin) {
   const int npad = (n + 7) / 8 * 8;
   if (n > 128) return 0;
-  const char* f = getenv("RCHOLQR_SOLVE_WARPS");  // experiments: 8 = one warp per tile
-  if (!(f && atoi(f) == 8) && warp_smem(npad, 8) <= smem_optin) return 16;   // 8 warp pairs
   if (warp_smem(npad, 8) <= smem_optin) return 8;
   if (warp_smem(npad, 4) <= smem_optin) return 4;
   return 0;
-}
-
-template <typename TX, int WARPS>
-static cudaError_t launch_w(const void* X, int64_t m, int n, int64_t ldx, const double* M, void* Q, int64_t ldq,
-                            const int* status, int sms, cudaStream_t st) {
-  const int npad = (n + 7) / 8 * 8;
-  const size_t smem = warp_smem(npad, WARPS);
-  auto kern = trsm_warp_kernel<TX, WARPS>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const int64_t ntiles = (m + 15) / 16;
-  const int grid = (int)std::min<int64_t>((ntiles + WARPS - 1) / WARPS, sms);
-  if (grid == 0) return cudaSuccess;
-  kern<<<grid, 32 * WARPS, smem, st>>>((const TX*)X, m, n, npad, ldx, M, (TX*)Q, ldq, status);
-  return cudaGetLastError();
 }
 
 template <typename TX, int PAIRS>
@@ -959,25 +683,13 @@ static cudaError_t launch_p(const void* X, int64_t m, int n, int64_t ldx, const 
   return cudaGetLastError();
 }
 
-cudaError_t launch_trsm_warp(int warps, const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M,
-                             void* Q, int64_t ldq, const int* status, int sms, cudaStream_t st) {
-  if (warps == 16)
-    return dtype == RCHOLQR_F64 ? launch_p<double, 8>(X, m, n, ldx, M, Q, ldq, status, sms, st)
-                                : launch_p<float, 8>(X, m, n, ldx, M, Q, ldq, status, sms, st);
+cudaError_t launch_trsm_pairs(int pairs, const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M,
+                              void* Q, int64_t ldq, const int* status, int sms, cudaStream_t st) {
   if (dtype == RCHOLQR_F64)
-    return warps == 8 ? launch_w<double, 8>(X, m, n, ldx, M, Q, ldq, status, sms, st)
-                      : launch_w<double, 4>(X, m, n, ldx, M, Q, ldq, status, sms, st);
-  return warps == 8 ? launch_w<float, 8>(X, m, n, ldx, M, Q, ldq, status, sms, st)
-                    : launch_w<float, 4>(X, m, n, ldx, M, Q, ldq, status, sms, st);
-}
-
-int trsm_resident_tm(int n, int dtype, size_t smem_optin) {
-  const int npad = (n + 7) / 8 * 8;
-  const int xs = dtype == RCHOLQR_F64 ? 8 : 4;
-  if (n > 128) return 0;
-  if (ResLayout(npad, 64, xs).total() <= smem_optin) return 64;
-  if (ResLayout(npad, 32, xs).total() <= smem_optin) return 32;
-  return 0;
+    return pairs == 8 ? launch_p<double, 8>(X, m, n, ldx, M, Q, ldq, status, sms, st)
+                      : launch_p<double, 4>(X, m, n, ldx, M, Q, ldq, status, sms, st);
+  return pairs == 8 ? launch_p<float, 8>(X, m, n, ldx, M, Q, ldq, status, sms, st)
+                    : launch_p<float, 4>(X, m, n, ldx, M, Q, ldq, status, sms, st);
 }
 
 cudaError_t launch_tri_prep_blocked(const double* R, int n, double* M, int* status, cudaStream_t st, int tb,
@@ -987,30 +699,6 @@ cudaError_t launch_tri_prep_blocked(const double* R, int n, double* M, int* stat
   tri_prep_blocked_kernel<<<(npad + warps_per_block - 1) / warps_per_block, 32 * warps_per_block, 0, st>>>(
       R, n, npad, tb, M, status);
   return cudaGetLastError();
-}
-
-template <typename TX, int TM>
-static cudaError_t launch_res(const void* X, int64_t m, int n, int64_t ldx, const double* M, void* Q, int64_t ldq,
-                              const int* status, int sms, cudaStream_t st) {
-  const int npad = (n + 7) / 8 * 8;
-  const size_t smem = ResLayout(npad, TM, (int)sizeof(TX)).total();
-  auto kern = trsm_resident_kernel<TX, TM>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const int64_t ntiles = (m + TM - 1) / TM;
-  const int grid = (int)std::min<int64_t>(ntiles, sms);
-  if (grid == 0) return cudaSuccess;
-  kern<<<grid, RES_THREADS, smem, st>>>((const TX*)X, m, n, npad, ldx, M, (TX*)Q, ldq, status);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_trsm_resident(int tm, const void* X, int dtype, int64_t m, int n, int64_t ldx, const double* M,
-                                 void* Q, int64_t ldq, const int* status, int sms, cudaStream_t st) {
-  if (dtype == RCHOLQR_F64)
-    return tm == 64 ? launch_res<double, 64>(X, m, n, ldx, M, Q, ldq, status, sms, st)
-                    : launch_res<double, 32>(X, m, n, ldx, M, Q, ldq, status, sms, st);
-  return tm == 64 ? launch_res<float, 64>(X, m, n, ldx, M, Q, ldq, status, sms, st)
-                  : launch_res<float, 32>(X, m, n, ldx, M, Q, ldq, status, sms, st);
 }
 
 }  // namespace rcq
