@@ -36,6 +36,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <algorithm>
+#include <type_traits>
 #include "internal.cuh"
 #include "tcgen05.cuh"
 
@@ -142,13 +143,9 @@ __device__ __forceinline__ long long qt_combine(uint32_t a0, uint32_t a1, uint32
   t += (long long)(int)(a0 * 256u + a1) << 32;
   return t;
 }
-// fast: every 2^(e_i + e_j - 52) of this warp is a normal fp32 (row_bits = (e_i + 75) << 23,
-// col_bits = e_j << 23); else the exact fp64 route (any exponent range)
+// fast route (warp-uniform): every 2^(e_i + e_j - 52) of the warp's rows is a normal fp32, built as the bits
+// (e_i + 75) << 23 plus e_j << 23; else this exact fp64 route (any exponent range)
 __device__ __noinline__ float qt_scale_slow(long long t, int ei, int ej) { return (float)ldexp((double)t, ei + ej - 52); }
-__device__ __forceinline__ float qt_scale(long long t, bool fast, int row_bits, int col_bits, int ei, int ej) {
-  if (fast) return __ll2float_rn(t) * __int_as_float(row_bits + col_bits);
-  return qt_scale_slow(t, ei, ej);
-}
 
 template <int KMAX>
 __global__ void __launch_bounds__(QCfg<KMAX>::THREADS, 1)
@@ -300,13 +297,70 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
           const bool fast = __all_sync(0xffffffffu, ei + crange[0] + 75 >= 1 && ei + crange[1] + 75 <= 254);
           const uint32_t lv = lb + buf * (QT_LEV * QT_G);
           unsigned char* qs = qstage + (warp - 2) * (32 * 8 * 4);
+          auto drain = [&](auto fast_tag) {
+            constexpr bool FAST = decltype(fast_tag)::value;
 #pragma unroll
-          for (int h = 0; h < QT_G / 8; ++h) {
-            uint32_t lvl[QT_LEV][8];
+            for (int h = 0; h < QT_G / 8; ++h) {
+              uint32_t lvl[QT_LEV][8];
+#pragma unroll
+              for (int L = 0; L < QT_LEV; ++L) tc::ld8(lv + L * QT_G + h * 8, lvl[L]);
+              const int4 c0 = *reinterpret_cast<const int4*>(cexp + g * QT_G + h * 8);
+              const int4 c1 = *reinterpret_cast<const int4*>(cexp + g * QT_G + h * 8 + 4);
+              const int cb[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+              tc::wait_ld();
+              if (h == QT_G / 8 - 1) {
+                asm volatile("tcgen05.fence::before_thread_sync;\n");
+                __syncwarp();
+                if (lane == 0) tc::mbar_arrive(&tfree[buf]);
+              }
+              float o[8];
+#pragma unroll
+              for (int c = 0; c < 8; ++c) {
+                const long long t = qt_combine(lvl[0][c], lvl[1][c], lvl[2][c], lvl[3][c], lvl[4][c], lvl[5][c], lvl[6][c]);
+                if constexpr (FAST) o[c] = __ll2float_rn(t) * __int_as_float(rbits + (cb[c] << 23));
+                else o[c] = qt_scale_slow(t, ei, cb[c]);
+              }
+              if (lane == 0) tc::bulk_wait_read0();          // previous chunk's store has read the tile
+              __syncwarp();
+              *reinterpret_cast<float4*>(qs + lane * 32) = make_float4(o[0], o[1], o[2], o[3]);
+              *reinterpret_cast<float4*>(qs + lane * 32 + 16) = make_float4(o[4], o[5], o[6], o[7]);
+              asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+              __syncwarp();
+              if (lane == 0) {                               // TMA clips rows >= m and columns >= n
+                tc::tma_store_2d(&qmap, qs, g * QT_G + h * 8, (int)((blockIdx.x + (int64_t)tt * gridDim.x) * QT_M + dq * 32));
+                tc::bulk_commit();
+              }
+            }
+          };
+          if (fast) drain(std::true_type{});
+          else drain(std::false_type{});
+        } else {
+        constexpr int DC = Cf::DCOLS;
+        const uint32_t lv = lb + buf * (QT_LEV * QT_G) + dc0;
+        // row scale read before the buffer is released: the rexp ring slot is reused only after
+        // later MMAs, which wait on this release
+        const int ei = rexp[(tt & 3) * QT_M + row_l];
+        const int rbits = (ei + 75) << 23;
+        const bool fast = __all_sync(0xffffffffu, ei + crange[0] + 75 >= 1 && ei + crange[1] + 75 <= 254);
+        // this warp's 32 rows x DC columns (fp32) are staged in shared memory (16-column rows: plain
+        // 64-byte rows; 32-column rows: 128-byte swizzle, chunk c of row r at c ^ (r & 7) -- conflict-free
+        // STS.128) as they are computed, then one 2D TMA store writes them (rows >= m, columns >= n clipped)
+        unsigned char* qs = qstage + (warp - 2) * (32 * DC * 4);
+        if (lane == 0) tc::bulk_wait_read0();                // the previous store has read the tile
+        __syncwarp();
+        // the fast / exact-range choice is warp-uniform, so it is taken once per drained group
+        auto drain = [&](auto fast_tag) {
+          constexpr bool FAST = decltype(fast_tag)::value;
+#pragma unroll
+          for (int h = 0; h < DC / 8; ++h) {
+            uint32_t lvl[QT_LEV][8];                         // all seven levels in flight before one wait
 #pragma unroll
             for (int L = 0; L < QT_LEV; ++L) tc::ld8(lv + L * QT_G + h * 8, lvl[L]);
+            const int4 c0 = *reinterpret_cast<const int4*>(cexp + g * QT_G + dc0 + h * 8);
+            const int4 c1 = *reinterpret_cast<const int4*>(cexp + g * QT_G + dc0 + h * 8 + 4);
+            const int cb[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
             tc::wait_ld();
-            if (h == QT_G / 8 - 1) {
+            if (h == DC / 8 - 1) {                           // TMEM buffer free; the stores below need no TMEM
               asm volatile("tcgen05.fence::before_thread_sync;\n");
               __syncwarp();
               if (lane == 0) tc::mbar_arrive(&tfree[buf]);
@@ -314,70 +368,27 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
             float o[8];
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-              const int ej = cexp[g * QT_G + h * 8 + c];
-              o[c] = qt_scale(qt_combine(lvl[0][c], lvl[1][c], lvl[2][c], lvl[3][c], lvl[4][c], lvl[5][c], lvl[6][c]),
-                              fast, rbits, ej << 23, ei, ej);
+              const long long t = qt_combine(lvl[0][c], lvl[1][c], lvl[2][c], lvl[3][c], lvl[4][c], lvl[5][c], lvl[6][c]);
+              if constexpr (FAST) o[c] = __ll2float_rn(t) * __int_as_float(rbits + (cb[c] << 23));
+              else o[c] = qt_scale_slow(t, ei, cb[c]);
             }
-            if (lane == 0) tc::bulk_wait_read0();            // previous chunk's store has read the tile
-            __syncwarp();
-            *reinterpret_cast<float4*>(qs + lane * 32) = make_float4(o[0], o[1], o[2], o[3]);
-            *reinterpret_cast<float4*>(qs + lane * 32 + 16) = make_float4(o[4], o[5], o[6], o[7]);
-            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            __syncwarp();
-            if (lane == 0) {                                 // TMA clips rows >= m and columns >= n
-              tc::tma_store_2d(&qmap, qs, g * QT_G + h * 8, (int)((blockIdx.x + (int64_t)tt * gridDim.x) * QT_M + dq * 32));
-              tc::bulk_commit();
+#pragma unroll
+            for (int c = 0; c < 8; c += 4) {
+              const int ch = h * 2 + (c >> 2);                // 16-byte chunk of the row
+              const int off = DC == 32 ? lane * 128 + ((ch ^ (lane & 7)) << 4) : lane * (DC * 4) + ch * 16;
+              *reinterpret_cast<float4*>(qs + off) = make_float4(o[c], o[c + 1], o[c + 2], o[c + 3]);
             }
           }
-          continue;
+        };
+        if (fast) drain(std::true_type{});
+        else drain(std::false_type{});
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+          tc::tma_store_2d(&qmap, qs, g * QT_G + dc0, (int)((blockIdx.x + (int64_t)tt * gridDim.x) * QT_M + dq * 32));
+          tc::bulk_commit();
         }
-        constexpr int DC = Cf::DCOLS;
-        float o[DC];
-        const uint32_t lv = lb + buf * (QT_LEV * QT_G) + dc0;
-        // row scale read before the buffer is released: the rexp ring slot is reused only after
-        // later MMAs, which wait on this release
-        const int ei = rexp[(tt & 3) * QT_M + row_l];
-        const int rbits = (ei + 75) << 23;
-        const bool fast = __all_sync(0xffffffffu, ei + crange[0] + 75 >= 1 && ei + crange[1] + 75 <= 254);
-#pragma unroll
-        for (int h = 0; h < DC / 8; ++h) {
-          uint32_t lvl[QT_LEV][8];                           // all seven levels in flight before one wait
-#pragma unroll
-          for (int L = 0; L < QT_LEV; ++L) tc::ld8(lv + L * QT_G + h * 8, lvl[L]);
-          tc::wait_ld();
-          if (h == DC / 8 - 1) {                             // TMEM buffer free; the stores below need no TMEM
-            asm volatile("tcgen05.fence::before_thread_sync;\n");
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&tfree[buf]);
-          }
-#pragma unroll
-          for (int c = 0; c < 8; ++c) {
-            const int ej = cexp[g * QT_G + dc0 + h * 8 + c];
-            o[h * 8 + c] = qt_scale(qt_combine(lvl[0][c], lvl[1][c], lvl[2][c], lvl[3][c], lvl[4][c], lvl[5][c],
-                                               lvl[6][c]), fast, rbits, ej << 23, ei, ej);
-          }
-        }
-        {
-          // stage this warp's 32 rows x DC columns (fp32) in shared memory with the 128-byte swizzle
-          // (16-byte chunk c of row r at chunk c ^ (r & 7): conflict-free STS.128), then one 2D TMA
-          // store writes them; TMA clips rows >= m and columns >= n.
-          unsigned char* qs = qstage + (warp - 2) * (32 * DC * 4);
-          if (lane == 0) tc::bulk_wait_read0();              // previous store finished reading the tile
-          __syncwarp();
-#pragma unroll
-          for (int c = 0; c < DC; c += 4) {
-            const float o4[4] = {o[c], o[c + 1], o[c + 2], o[c + 3]};
-            // 32-column rows: 128-byte swizzle (conflict-free); 16-column rows: plain 64-byte rows
-            const int off = DC == 32 ? lane * 128 + (((c >> 2) ^ (lane & 7)) << 4) : lane * (DC * 4) + c * 4;
-            *reinterpret_cast<float4*>(qs + off) = make_float4(o4[0], o4[1], o4[2], o4[3]);
-          }
-          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-          __syncwarp();
-          if (lane == 0) {
-            tc::tma_store_2d(&qmap, qs, g * QT_G + dc0, (int)((blockIdx.x + (int64_t)tt * gridDim.x) * QT_M + dq * 32));
-            tc::bulk_commit();
-          }
-        }
+        }   // TMA_RAW drain
       }
     }
   } else {
