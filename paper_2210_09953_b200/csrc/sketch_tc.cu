@@ -36,6 +36,7 @@ namespace rcq {
 constexpr int STC_M = 128;        // Theta rows per CTA (MMA M = TMEM lanes)
 constexpr int STC_N = 64;         // X columns per CTA (MMA N)
 constexpr int STC_KC = 64;        // X rows per stage (2 MMA k-steps of 32)
+constexpr int STC_PF = 8;         // stages prefetched into L2 ahead of the raw ring (contiguous X)
 constexpr int STC_DWARPS = 8;     // digit-plane warps per stage group: one (column, 16-row group) task per thread
 constexpr int STC_DGROUPS = 2;    // digit groups (warps 2..9, 10..17) alternating stages, like the E groups
 constexpr int STC_EWARPS = 4;     // E-tile warps (18..21): two groups alternating stages, one X row per lane
@@ -231,10 +232,20 @@ sketch_sparse_tc_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx,
     // ---------------------------------------------------------------- X loader (bulk copies, lane 0)
     const bool contiguous = ldx == n;
     const uint32_t row_bytes = (uint32_t)(n * sizeof(TX));
+    // contiguous X: stages up to STC_PF ahead are prefetched into L2 (no shared memory), so that more
+    // HBM bytes are in flight per SM than the raw ring holds; the ring's bulk copies then hit L2
+    auto prefetch = [&](int c) {
+      const int64_t i0 = i_begin + (int64_t)c * STC_KC;
+      const int rows = (int)min((int64_t)STC_KC, i_end - i0);
+      tc::bulk_prefetch_l2(X + i0 * ldx, row_bytes * rows);
+    };
+    if (contiguous && lane == 0)
+      for (int c = 1; c < STC_PF && c < nstages; ++c) prefetch(c);
     for (int c = 0; c < nstages; ++c) {
       const int s = c % F::RAW;
       if (c >= F::RAW) tc::mbar_wait(&rempty[s], (uint32_t)(((c / F::RAW) - 1) & 1));
       if (lane == 0) {
+        if (contiguous && c + STC_PF < nstages) prefetch(c + STC_PF);
         const int64_t i0 = i_begin + (int64_t)c * STC_KC;
         const int rows = (int)min((int64_t)STC_KC, i_end - i0);
         TX* dst = raw_base + (size_t)s * STC_KC * n;

@@ -51,6 +51,7 @@ constexpr int QT_NB = QT_DB * QT_G;             // stacked W digit rows of one g
 constexpr int QT_DWARPS = 8;    // digit warps of the K-half producers (64 < n <= 128)
 constexpr int QT_RWARPS = 8;    // drain warps 2..9: two sets of four (one per TMEM level buffer)
 constexpr int QT_KMAX_ALL = 128;
+constexpr int QT_PF = 4;        // X tiles prefetched into L2 ahead of the raw ring (n <= 64)
 static_assert(2 * QT_LEV * QT_G <= 512, "two TMEM level buffers");
 
 // byte offset of column group g's W digit tile (triangular: K_h = 32 (h + 1) rows of W per group)
@@ -260,10 +261,17 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
       tc::bulk_g2s(wsm, wdig, wbytes, wbar);
     }
     __syncwarp();
+    // the raw ring holds two tiles; tiles up to QT_PF ahead are prefetched into L2 so that enough HBM
+    // bytes are in flight per SM (~QT_PF x 34 KB) -- the ring loads then hit L2
+    if (Cf::TMA_RAW && lane == 0)
+      for (int tp = 1; tp < QT_PF && tp < my_tiles; ++tp)
+        tc::tma_prefetch_2d(&xmap, 0, (int)((blockIdx.x + (int64_t)tp * gridDim.x) * QT_M));
     for (int tt = 0; tt < (Cf::TMA_RAW ? my_tiles : 0); ++tt) {
       const int s = tt % QT_RAW;
       if (tt >= QT_RAW) tc::mbar_wait(&rempty[s], (uint32_t)(((tt / QT_RAW) - 1) & 1));
       if (lane == 0) {
+        if (tt + QT_PF < my_tiles)
+          tc::tma_prefetch_2d(&xmap, 0, (int)((blockIdx.x + (int64_t)(tt + QT_PF) * gridDim.x) * QT_M));
         const int64_t row0 = (blockIdx.x + (int64_t)tt * gridDim.x) * QT_M;
         if (dbg & 8) tc::mbar_arrive(&rfull[s]);
         else {
