@@ -177,7 +177,8 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
   // row scales: a ring of 4 tiles, so the digit slot can be refilled while the drain of the tile
   // before still reads its scales (a slot is free once the MMAs of tile t complete, and those
   // follow every drain of tile t - 2; see the TMEM buffer waits below)
-  int* rexp = reinterpret_cast<int*>(tmem_slot + 4);                          // [4][128]
+  // 16-byte aligned: the drain reads the column exponents cexp with LDS.128
+  int* rexp = reinterpret_cast<int*>((reinterpret_cast<uintptr_t>(tmem_slot + 4) + 15) & ~uintptr_t(15));   // [4][128]
   int* cexp = rexp + 4 * QT_M;                                                // [KMAX] e_j (W column exponents)
   int* crange = cexp + QT_KMAX_ALL;                                           // [2] min, max e_j
 
