@@ -21,7 +21,9 @@ __all__ = ["RCholQR", "RCholQRError", "load_library", "library_path", "theta_exp
            "GAUSSIAN", "SPARSE_SIGN", "RADEMACHER", "SRHT"]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-_LIB_PATH = os.path.join(_PKG, "lib", "librcholqr.so")
+# RCHOLQR_ABLATION_LIB=1 (kernel experiments under tools/ only) loads the build with the role ablation switches
+# compiled in (python -m paper_2210_09953_b200.build --ablation); the product path always loads librcholqr.so
+_LIB_PATH = os.path.join(_PKG, "lib", "librcholqr_ablation.so" if os.environ.get("RCHOLQR_ABLATION_LIB") else "librcholqr.so")
 _lock = threading.Lock()
 _lib = None
 

@@ -41,9 +41,13 @@ def _nccl_include() -> str:
     raise RuntimeError("nccl.h not found (needed for the multi-GPU all-reduce types)")
 
 
-def source_hash() -> str:
+def _lib(ablation: bool) -> str:
+    return LIB.replace("librcholqr.so", "librcholqr_ablation.so") if ablation else LIB
+
+
+def source_hash(ablation: bool = False) -> str:
     h = hashlib.sha256()
-    h.update(" ".join(FLAGS).encode())
+    h.update(" ".join(FLAGS + (["-DRCHOLQR_ABLATION"] if ablation else [])).encode())
     for f in SRCS + HDRS:
         h.update(os.path.basename(f).encode())
         with open(f, "rb") as fh:
@@ -51,17 +55,23 @@ def source_hash() -> str:
     return h.hexdigest()
 
 
-def _stale(digest: str) -> bool:
-    if not os.path.exists(LIB) or not os.path.exists(STAMP):
+def _stale(digest: str, lib: str) -> bool:
+    stamp = lib + ".sha256"
+    if not os.path.exists(lib) or not os.path.exists(stamp):
         return True
-    with open(STAMP) as f:
+    with open(stamp) as f:
         return f.read().strip() != digest
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    digest = source_hash()
-    _info["hash"] = digest
-    if not force and not _stale(digest):
+def build(force: bool = False, verbose: bool = False, ablation: bool = False) -> str:
+    """ablation=True: a separate library (lib/librcholqr_ablation.so) with the kernels' role-ablation switches
+    (RCHOLQR_*_DEBUG) compiled in, for the experiments under tools/; never loaded by the product path."""
+    LIB = _lib(ablation)
+    STAMP = LIB + ".sha256"
+    digest = source_hash(ablation)
+    if not ablation:
+        _info["hash"] = digest
+    if not force and not _stale(digest, LIB):
         return LIB
     os.makedirs(os.path.dirname(LIB), exist_ok=True)
     nvcc = os.path.join(os.environ.get("CUDA_HOME", "/usr/local/cuda"), "bin", "nvcc")
@@ -71,7 +81,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     try:
         def obj(src):
             o = os.path.join(tmpdir, os.path.basename(src) + ".o")
-            subprocess.check_call([nvcc, *FLAGS, *extra, *inc, "-c", "-o", o, src])
+            subprocess.check_call([nvcc, *FLAGS, *extra, *(["-DRCHOLQR_ABLATION"] if ablation else []), *inc, "-c", "-o", o, src])
             return o
         with cf.ThreadPoolExecutor(max_workers=min(len(SRCS), os.cpu_count() or 4)) as ex:
             objs = list(ex.map(obj, SRCS))
@@ -82,7 +92,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             f.write(digest + "\n")
     finally:
         shutil.rmtree(tmpdir, ignore_errors=True)
-    _info["rebuilt"] = True
+    if not ablation:
+        _info["rebuilt"] = True
     return LIB
 
 
@@ -92,4 +103,4 @@ def last_build_info() -> dict:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, ablation="--ablation" in sys.argv))

@@ -918,7 +918,7 @@ int32_t rcholqr_launches_per_factor(rcholqr_plan p, int64_t m) {
   //   sketch: [tcgen05 sketch +] the CUDA-core kernel (its guarded fallback, exits at once) + reduce
   //   QR: 1 | triangular prep (blocked prep or R^{-1}): 1 | solve: tcgen05 (W-digit prep + solve) = 2,
   //   streamed fp64 GEMMs = 2 per column block, else 1.
-  const bool tc_sketch = p->sk.kind == kSketchSparseTC || (p->sk.kind < kSketchSparse && (p->sk.tc || p->sk.rad_tc));
+  const bool tc_sketch = p->sk.sp_tc || (p->sk.kind < kSketchSparse && (p->sk.tc || p->sk.rad_tc));
   int sketch_launches = (tc_sketch ? 2 : 1) + 1;
   if (tc_sketch && p->sk.kind < kSketchSparse && p->sk.tc && m > 0) {   // pre-split: (column maxima + digit planes + sketch) per chunk
     const size_t cap = gauss_tcp_chunk_workspace(m, p->d.n, p->d.dtype, p->sk.tc_splits);

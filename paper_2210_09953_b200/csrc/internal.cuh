@@ -33,11 +33,11 @@ __device__ __forceinline__ void dmma_16x8x4(double (&d)[4], double a0, double a1
 
 // ---- launch configurations chosen at plan creation ----
 enum SketchKind : int { kSketchG48x24 = 0, kSketchG128x64 = 1, kSketchG112x104 = 2, kSketchG64x64 = 3,
-                        kSketchSparse = 10, kSketchSparseReg = 11, kSketchSparseTC = 12 };
+                        kSketchSparse = 10, kSketchSparseReg = 11 };
 // tcgen05 int8 sparse sketch (sketch_tc.cu): exact int32 accumulation bound on rows per CTA
 constexpr int64_t kSparseTcMaxRows = 8 * 1024 * 1024;
 bool sparse_tc_applicable(int k, int n, int zeta);
-bool sparse_tc_aligned(const void* X, int dtype, int n, int64_t ldx);
+bool sparse_tc_aligned(const void* X, int dtype, int64_t m, int64_t ldx);
 cudaError_t launch_sparse_tc(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                              int zeta, uint64_t seed, int splits, int64_t rows_per_split, double* part, int* overflow,
                              cudaStream_t st, const uint64_t* srht_s = nullptr);
@@ -54,6 +54,8 @@ struct SketchLaunch {
   // Rademacher Theta (reading A22): the DMMA kernel above draws +-1 instead of N(0,1); rad_tc: the
   // tcgen05 int8 kernel of sketch_tc.cu with a dense E tile in front of it (n <= 64, k <= 512)
   int rad = 0, rad_tc = 0, rad_splits = 0;   // rad: 1 = Rademacher, 2 = SRHT (reading A23)
+  // sparse-sign: the tcgen05 kernel of sketch_tc.cu in front of the CUDA-core kind above (its guarded fallback)
+  int sp_tc = 0;
   const uint64_t* srht_s = nullptr;          // SRHT: the k sampled Hadamard rows (plan-owned device array)
   int max_splits() const {
     int s = tc && tc_splits > splits ? tc_splits : splits;

@@ -251,7 +251,9 @@ template <typename TX>
 __global__ void __launch_bounds__(SPARSE_THREADS)
 sketch_sparse_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                      int zeta, uint64_t seed, int tiles_n, int nts, int64_t rows_per_split,
-                     double* __restrict__ part) {
+                     double* __restrict__ part, const int* __restrict__ guard) {
+  // guard != null: recompute only if the tensor-core sketch (sketch_tc.cu) flagged a headroom overflow
+  if (guard && *guard == 0) return;
   extern __shared__ __align__(16) double smem[];
   double* Ps = smem;                              // [k][nts]
   double* Xs = Ps + (size_t)k * nts;              // [KCS][nts]
@@ -580,32 +582,32 @@ static int choose_splits(int tiles, int sms) {
 
 SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms, size_t smem_optin) {
   SketchLaunch L{};
-  if (sketch == RCHOLQR_SPARSE_SIGN && zeta <= 8 && k / zeta <= 16 && n <= 64 && !getenv("RCHOLQR_SPARSE_SMEM")) {
-    L.kind = kSketchSparseReg;
-    L.threads = SPR_THREADS;
-    L.KT = k; L.NT = n; L.tiles_k = 1; L.tiles_n = 1; L.smem = 0;
-    L.splits = choose_splits(1, 2 * sms);
-    // tcgen05 int8 path (sketch_tc.cu) with the register kernel as its guarded fallback
+  if (sketch == RCHOLQR_SPARSE_SIGN) {
+    if (zeta <= 8 && k / zeta <= 16 && n <= 64 && !getenv("RCHOLQR_SPARSE_SMEM")) {
+      L.kind = kSketchSparseReg;
+      L.threads = SPR_THREADS;
+      L.KT = k; L.NT = n; L.tiles_k = 1; L.tiles_n = 1; L.smem = 0;
+      L.splits = choose_splits(1, 2 * sms);
+    } else {
+      L.kind = kSketchSparse;
+      L.threads = SPARSE_THREADS;
+      L.KT = k;
+      // columns per CTA so that Ps + Xs + sel fit comfortably (<= ~110 KB -> 2 CTAs / SM)
+      size_t budget = std::min<size_t>(110 * 1024, smem_optin);
+      int nts = n;
+      while (nts > 8 && sizeof(double) * ((size_t)k * nts + (size_t)KCS * nts) + sizeof(int) * KCS * zeta > budget)
+        nts = (nts + 1) / 2;
+      L.NT = nts;
+      L.tiles_k = 1;
+      L.tiles_n = (n + nts - 1) / nts;
+      L.smem = sizeof(double) * ((size_t)k * nts + (size_t)KCS * nts) + sizeof(int) * KCS * zeta;
+      L.splits = choose_splits(L.tiles_n, 2 * sms);
+    }
+    // tcgen05 int8 path (sketch_tc.cu, any n by 64-column tiles) with the kernel above as its guarded fallback
     if (sparse_tc_applicable(k, n, zeta) && !getenv("RCHOLQR_SPARSE_CUDA_CORE")) {
-      L.kind = kSketchSparseTC;
+      L.sp_tc = 1;
       L.splits = sms;
     }
-    return L;
-  }
-  if (sketch == RCHOLQR_SPARSE_SIGN) {
-    L.kind = kSketchSparse;
-    L.threads = SPARSE_THREADS;
-    L.KT = k;
-    // columns per CTA so that Ps + Xs + sel fit comfortably (<= ~110 KB -> 2 CTAs / SM)
-    size_t budget = std::min<size_t>(110 * 1024, smem_optin);
-    int nts = n;
-    while (nts > 8 && sizeof(double) * ((size_t)k * nts + (size_t)KCS * nts) + sizeof(int) * KCS * zeta > budget)
-      nts = (nts + 1) / 2;
-    L.NT = nts;
-    L.tiles_k = 1;
-    L.tiles_n = (n + nts - 1) / nts;
-    L.smem = sizeof(double) * ((size_t)k * nts + (size_t)KCS * nts) + sizeof(int) * KCS * zeta;
-    L.splits = choose_splits(L.tiles_n, 2 * sms);
     return L;
   }
   // Gaussian: pick the tile minimising padded work (tiles * KT * NT), ties -> larger tile.
@@ -686,23 +688,31 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
   const int64_t per = (m + L.splits - 1) / L.splits;
   double scale;
   int reduce_splits = L.splits;
-  if (L.kind == kSketchSparseReg || L.kind == kSketchSparseTC) {
-    const int64_t rps = std::max<int64_t>(SPR_KC, ((per + SPR_KC - 1) / SPR_KC) * SPR_KC);
+  if (L.kind == kSketchSparseReg || L.kind == kSketchSparse) {
+    static_assert(KCS % SPR_KC == 0, "row chunks");
+    const int64_t rps = std::max<int64_t>(KCS, ((per + KCS - 1) / KCS) * KCS);   // whole chunks of both kernels
     const int beta = k / zeta;
-    // tensor-core path first; the register kernel below then runs only if it raised the overflow
+    // tensor-core path first; the CUDA-core kernel below then runs only if it raised the overflow
     // flag.  int32 accumulators are exact while rows_per_split * 255 < 2^31.
     const int* guard = nullptr;
-    if (L.kind == kSketchSparseTC && rps <= kSparseTcMaxRows && sparse_tc_aligned(X, dtype, n, ldx)) {
+    if (L.sp_tc && rps <= kSparseTcMaxRows && sparse_tc_aligned(X, dtype, m, ldx)) {
       e = cudaMemsetAsync(flag, 0, sizeof(int), st);
       if (e != cudaSuccess) return e;
       e = launch_sparse_tc(X, dtype, m, n, ldx, row_offset, k, zeta, seed, L.splits, rps, part, flag, st);
-      if (e != cudaSuccess) return e;
-      guard = flag;
-      pb |= kPathSketchTC;
+      if (e == cudaSuccess) { guard = flag; pb |= kPathSketchTC; }
+      else if (e != cudaErrorNotSupported) return e;
     }
     if (!guard) pb |= kPathSketchCudaCore;
     auto launch = [&](auto* tag) -> cudaError_t {
       using TX = std::remove_pointer_t<decltype(tag)>;
+      if (L.kind == kSketchSparse) {
+        auto kern = sketch_sparse_kernel<TX>;
+        cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
+        if (e2 != cudaSuccess) return e2;
+        kern<<<L.tiles_n * L.splits, SPARSE_THREADS, L.smem, st>>>((const TX*)X, m, n, ldx, row_offset, k, zeta,
+                                                                   seed, L.tiles_n, L.NT, rps, part, guard);
+        return cudaGetLastError();
+      }
       auto go = [&](auto kern, int cpl) -> cudaError_t {
         const size_t sm = (sizeof(double) + sizeof(TX) * SPR_STAGES) * SPR_KC * 32 * cpl + SPR_STAGES * SPR_KC * 8;
         cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -719,26 +729,12 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
     };
     e = dtype == RCHOLQR_F64 ? launch((double*)nullptr) : launch((float*)nullptr);
     scale = 1.0 / std::sqrt((double)zeta);
-  } else if (L.kind == kSketchSparse) {
-    const int64_t rps = std::max<int64_t>(KCS, ((per + KCS - 1) / KCS) * KCS);
-    auto launch = [&](auto* tag) -> cudaError_t {
-      using TX = std::remove_pointer_t<decltype(tag)>;
-      auto kern = sketch_sparse_kernel<TX>;
-      cudaError_t e2 = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem);
-      if (e2 != cudaSuccess) return e2;
-      kern<<<L.tiles_n * L.splits, SPARSE_THREADS, L.smem, st>>>((const TX*)X, m, n, ldx, row_offset, k, zeta,
-                                                                 seed, L.tiles_n, L.NT, rps, part);
-      return cudaGetLastError();
-    };
-    e = dtype == RCHOLQR_F64 ? launch((double*)nullptr) : launch((float*)nullptr);
-    scale = 1.0 / std::sqrt((double)zeta);
-    pb |= kPathSketchCudaCore;
   } else {
     int splits = L.splits;
     const int* guard = nullptr;
     const bool tc = L.tc && gauss_tc_aligned(X, dtype, n, ldx);
     // (SRHT: the tcgen05 E tile splits the global row as (multiple of 32) + lane, so row_offset % 32 == 0)
-    if (L.rad_tc && sparse_tc_aligned(X, dtype, n, ldx) && (L.rad != 2 || row_offset % 32 == 0)) {
+    if (L.rad_tc && sparse_tc_aligned(X, dtype, m, ldx) && (L.rad != 2 || row_offset % 32 == 0)) {
       // dense +-1 E tile on the sparse sketch's tcgen05 kernel (zeta = 0); it writes no compensation
       // partials, so they are zeroed for the fixed-order reduction; the DMMA kernel below reruns
       // (guarded) on a headroom overflow
@@ -792,7 +788,7 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
   const int64_t kn = (int64_t)k * n;
   const int threads = 256;
   const int blocks = (int)std::min<int64_t>((kn + threads - 1) / threads, 4096);
-  const bool sparse = L.kind == kSketchSparse || L.kind == kSketchSparseReg || L.kind == kSketchSparseTC;
+  const bool sparse = L.kind == kSketchSparse || L.kind == kSketchSparseReg;
   // Gaussian rows >= k_first (Alg. 5's extractor rows) take 1/sqrt(k - k_first) instead of 1/sqrt(k)
   double scale2 = scale;
   if (!sparse && k_first > 0 && k_first < k) {

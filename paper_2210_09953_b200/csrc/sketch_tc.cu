@@ -1,30 +1,41 @@
-// sketch_tc.cu -- sparse-sign sketch on the 5th-generation tensor core (tcgen05.mma kind::i8).
+// sketch_tc.cu -- sparse-sign (and dense +-1) sketch on the 5th-generation tensor core (tcgen05.mma kind::i8).
 //
-// P = E X / sqrt(zeta) (Alg. 2 step 1 with the sparse-sign Theta of reading A3):
-// E (k x m) has entries in {-1, 0, +1}, i.e. it is EXACT in int8.  X is written exactly as a
-// fixed-point integer against a per-(CTA, column) power-of-two scale 2^e_j,
-//     F(x) = trunc(x 2^(FB - e_j)),  FB = 7 + 8 (D-1),  |F| < 2^FB,
-// and F is split into D two's-complement bytes (d_0 signed, d_1.. unsigned):
-//     F = d_0 2^(8(D-1)) + d_1 2^(8(D-2)) + ... + d_{D-1}.
-// D = 6 (fp32 X, FB = 47) or 8 (fp64 X, FB = 63).  Each digit plane is one int8 GEMM into its own
-// int32 TMEM accumulator, which is exact while rows * 255 < 2^31 (kSparseTcMaxRows), so the only
-// approximation is the truncation of x below 2^(e_j - FB): relative 2^-43 (fp32) / 2^-59 (fp64)
-// of the column scale -- the "random projection in higher precision" of PAPER.md:83, 423.
-// e_j = (exponent of the column maximum over the CTA's FIRST stage) + 4 bits of headroom.  If a
-// later element of the CTA does not fit (|x| >= 2^e_j, or Inf/NaN) the kernel raises an overflow
-// flag and the register sparse kernel (sketch.cu) recomputes the whole sketch, so the result never
-// depends on that heuristic.
+// P = E X / sqrt(zeta) (Alg. 2 step 1 with the sparse-sign Theta of reading A3; the dense
+// Rademacher / SRHT Theta of readings A22 / A23 use the same kernel with a dense E tile).  E (k x m) has entries
+// in {-1, 0, +1}: EXACT in int8.  X is written exactly as a fixed-point integer against a per-(CTA, column)
+// power-of-two scale 2^e_j, F(x) = round(x 2^(FB - e_j)), and the int8 MMA sums E times the base-256 digits of F
+// exactly in int32 TMEM (rows * 255 < 2^31: kSparseTcMaxRows) -- the "random projection in higher precision" of
+// PAPER.md:83, 423; the only approximation is the rounding of x at 2^(e_j - FB) (relative 2^-44 / 2^-60 of the
+// column scale).
 //
-// Roles (1 CTA per SM, 22 warps): warp 0 lane 0 issues tcgen05.mma and commits to mbarriers;
-// warp 1 lane 0 streams X rows into a raw shared-memory ring with cp.async.bulk (mbarrier
-// complete_tx); warps 2..21 build each stage's operands -- the D digit planes (two groups of 8 warps
-// taking alternate stages) and the E tile from Philox (theta.cuh; two groups of 2 warps) -- in the
-// canonical K-major SWIZZLE_NONE core-matrix layout.  At the end warps 0..3 drain TMEM (tcgen05.ld,
-// lane = Theta row) and write the fp64 partial sums.  (Round 1 had one digit group of 8 warps: the
-// digit warps were latency-bound at 44% issue with 3.5 warps per scheduler; C4 sketch 5.45 ms.)
+// Operand layout (round 2).  The B operand is the 8 BYTES of each X element's magic-constant double, MN-major:
+//     B[k = X row i][n = 8 j + b] = byte b of W(x_ij),
+// so an element's digits are contiguous along N and come straight out of ONE DFMA -- no digit planes, no byte
+// transposes (round 1 wrote six K-major digit planes with 8 PRMTs per 4 values and was bound by that work):
+//   * fp32 X: W = RN(x 2^(47-e) + 2^47 + 1.5 2^52), one DFMA on x 2^-128 built from the float's bits; bytes 0..5
+//     are the unsigned digits of F + 2^47 (weight 256^b), bytes 6, 7 the constant exponent bytes 0x38, 0x43.  TMEM
+//     column 8 j + 6 therefore holds 0x38 S_r, S_r = sum_i E_ri, which removes the 2^47 bias exactly.  The high
+//     word is 0x4338xxxx iff F + 2^47 fits in 48 bits: one LOP3 per element accumulates the overflow / Inf / NaN
+//     test.
+//   * fp64 X: (hi, lo) = F + C by two magic-constant floors, F = floor(x 2^(63-e)); stored as signed digits
+//     (bytes XOR 0x80 except the top one), byte b of weight 256^b.
+// P_rj = 2^(e_j - FB) sum_b acc_b 256^b with acc_b = TMEM column 8 j + b.  One stage (64 X rows, 64 columns)
+// is two k-steps x two MMAs of M = 128, N = 256, K = 32 (all 512 TMEM columns); the tensor core reads B
+// MN-major (idesc bit 16; probe tools/micro/tc_i8_mn_test.cu).  Columns beyond 64 are further CTAs (column tiles:
+// X is read through a 2D TMA box of 64 columns x 64 rows, zero-filled outside X).
+//
+// e_j = (exponent of the column maximum over the CTA's FIRST stage) + 4 bits of headroom.  If a later element
+// does not fit (|x| >= 2^e_j, or Inf/NaN) the kernel raises an overflow flag and a CUDA-core kernel recomputes
+// the whole sketch (sketch.cu), so the result never depends on that heuristic.
+//
+// Roles (1 CTA per SM, 22 warps): warp 0 lane 0 issues tcgen05.mma; warp 1 lane 0 loads the raw X ring by 2D TMA
+// (and prefetches STC_PF stages ahead into L2); warps 2..17 write the B bytes (two groups of 8 taking alternate
+// stages); warps 18..21 build the E tile from Philox (theta.cuh; two groups of 2).  At the end warps 0..3 drain
+// TMEM (tcgen05.ld, lane = Theta row) and write the fp64 partial sums.
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdlib>
+#include <algorithm>
 #include <type_traits>
 #include "internal.cuh"
 #include "tcgen05.cuh"
@@ -32,65 +43,44 @@
 
 namespace rcq {
 
-
 constexpr int STC_M = 128;        // Theta rows per CTA (MMA M = TMEM lanes)
-constexpr int STC_N = 64;         // X columns per CTA (MMA N)
+constexpr int STC_N = 64;         // X columns per CTA
+constexpr int STC_BN = 8 * STC_N; // B columns: 8 bytes per X column (two MMAs of N = 256)
 constexpr int STC_KC = 64;        // X rows per stage (2 MMA k-steps of 32)
-constexpr int STC_PF = 8;         // stages prefetched into L2 ahead of the raw ring (contiguous X)
-constexpr int STC_DWARPS = 8;     // digit-plane warps per stage group: one (column, 16-row group) task per thread
-constexpr int STC_DGROUPS = 2;    // digit groups (warps 2..9, 10..17) alternating stages, like the E groups
+constexpr int STC_PF = 8;         // stages prefetched into L2 ahead of the raw ring
+constexpr int STC_DWARPS = 8;     // B-byte warps per stage group
+constexpr int STC_DGROUPS = 2;    // B-byte groups (warps 2..9, 10..17) alternating stages, like the E groups
 constexpr int STC_EWARPS = 4;     // E-tile warps (18..21): two groups alternating stages, one X row per lane
 constexpr int STC_THREADS = 32 * (2 + STC_DGROUPS * STC_DWARPS + STC_EWARPS);
-static_assert(32 * STC_DWARPS == STC_N * (STC_KC / 16), "one digit task per thread");
+constexpr int STC_E_BYTES = STC_M * STC_KC;              // E tile (int8, K-major)
+constexpr int STC_B_BYTES = STC_KC * STC_BN;             // B tile (int8, MN-major)
+constexpr int STC_LBO = (STC_BN / 16) * 128;             // B: byte stride between 8-row K groups
 static_assert(16 * STC_EWARPS == STC_KC, "one X row per E-warp lane, two warp groups");
 
-// Digit split of one element.  F(x) = round(x 2^(FB-e)) is
-// written in base 256 with D digits, each digit plane one int8 operand; several planes are stacked
-// along N so one MMA covers them (N = 192..256).
-//   fp32 X (D = 6, FB = 47, the C4 hot path): x 2^-128 is built exactly from the float's bits (one
-//     shift, one LOP3: exponent 0x300 | exp_f), and ONE round-to-nearest DFMA by 2^(175-e) onto
-//     1.5 2^52 + 2^47 leaves F + 2^47 in the low 48 mantissa bits: six UNSIGNED digits, hi word
-//     bytes 1,0 = d0,d1, lo word bytes 3..0 = d2..d5.  The bias 2^47 = 128 * 256^5 is removed
-//     exactly in the epilogue with S_r = sum_i E_ri, which a constant ones-block in the first
-//     MMA group accumulates (acc_0 - 128 S).  The high word is 0x4338xxxx iff F + 2^47 fits in
-//     48 bits, so OR/AND accumulators of it detect overflow, Inf and NaN.
-//   fp64 X (D = 8, FB = 63): H = floor(x 2^(31-e)) + C_hi, L = floor(frac 2^32) + C_lo by magic-
-//     constant floors; SIGNED digits via the offset C (0x80 in all bytes but the top one; digit
-//     bytes XOR 0x80), carry of L into H -> hi word bytes 3..0 = d0..d3, lo = d4..d7.
-// All steps are exact (power-of-two scalings, magic-constant roundings of integers < 2^51).
 template <typename TX> struct Fmt;
 template <> struct Fmt<float> {
-  static constexpr int D = 6, FB = 47;
-  static constexpr int RAW = 4, DIG = 4;   // raw X ring / operand ring depths
-  static constexpr int ONES = 16;          // ones-block rows in group 0 (bias correction)
+  static constexpr int FB = 47;
+  static constexpr int RAW = 4, DIG = 3;   // raw X ring / operand ring depths
   static constexpr bool SIGNED = false;
 };
 template <> struct Fmt<double> {
-  static constexpr int D = 8, FB = 63;
+  static constexpr int FB = 63;
   static constexpr int RAW = 3, DIG = 3;
-  static constexpr int ONES = 0;
   static constexpr bool SIGNED = true;
 };
 
 template <typename TX>
 struct StcCfg {
   using Fm = Fmt<TX>;
-  static constexpr int D = Fm::D;
-  static constexpr int PG = D / 2;                                  // digit planes per MMA group
-  static constexpr int N0 = Fm::ONES + PG * STC_N;                  // group 0: [ones | planes 0..PG-1]
-  static constexpr int N1 = (D - PG) * STC_N;                       // group 1: planes PG..D-1
-  static constexpr int TBASE1 = 256;                                // TMEM column of group 1
-  static constexpr int E_BYTES = STC_M * STC_KC;                    // E tile (int8)
-  static constexpr int G0_BYTES = N0 * STC_KC, G1_BYTES = N1 * STC_KC;
-  static constexpr int DIG_STAGE = E_BYTES + G0_BYTES + G1_BYTES;
+  static constexpr int DIG_STAGE = STC_E_BYTES + STC_B_BYTES;
   static constexpr int RAW_STAGE = STC_KC * STC_N * (int)sizeof(TX);
+  static constexpr int CE = 16 / (int)sizeof(TX);            // elements per 16-byte raw chunk (4 / 2)
+  static constexpr int CHUNKS = STC_N / CE;                   // raw chunks per row (16 / 32)
+  static constexpr int CB = CHUNKS / 8;                       // blocks of 8 chunks (2 / 4)
+  static constexpr int TASKS = STC_KC * CHUNKS / (32 * STC_DWARPS);   // chunks per thread per stage (4 / 8)
   static constexpr size_t SMEM = (size_t)Fm::DIG * DIG_STAGE + (size_t)Fm::RAW * RAW_STAGE + 1024;
-  static_assert(N0 <= 256 && N0 % 16 == 0 && N1 <= 256 && N1 % 16 == 0, "MMA N");
-  static_assert(N0 <= TBASE1 && TBASE1 + N1 <= 512, "TMEM columns");
-  // plane t: group, row inside the group's B tile, TMEM column
-  static __device__ __forceinline__ int grp(int t) { return t < PG ? 0 : 1; }
-  static __device__ __forceinline__ int brow(int t) { return t < PG ? Fm::ONES + t * STC_N : (t - PG) * STC_N; }
-  static __device__ __forceinline__ int tcol(int t) { return t < PG ? Fm::ONES + t * STC_N : TBASE1 + (t - PG) * STC_N; }
+  static_assert(SMEM <= 232448, "shared memory");
+  static_assert(TASKS * (4 / CB) == 8 || CB == 4, "task mapping covers the 8 row blocks");
 };
 
 // Per-(CTA, column) scale: e = (exponent bound of the first stage's max |x|) + 4 bits of headroom.
@@ -126,37 +116,38 @@ __device__ __forceinline__ ColParam col_param(uint32_t maxbits) {
   return p;
 }
 
-// fp32: (hi, lo) words of t = RN(x 2^(47-e) + 1.5 2^52 + 2^47)
-__device__ __forceinline__ void split_words(float x, const ColParam& p, uint32_t& hi, uint32_t& lo) {
+// fp32: the magic double t = RN(x 2^(47-e) + 1.5 2^52 + 2^47) as (lo, hi) words: lo, hi bytes 0, 1 = the
+// unsigned digits of F + 2^47, hi bytes 2, 3 = 0x38, 0x43 unless F overflowed.  x 2^-128 is built exactly from
+// the float's bits (normal x; one shift, one LOP3), so the scaling is one DFMA.
+__device__ __forceinline__ uint2 magic_word(float x, double s) {
   const uint32_t u = __float_as_uint(x);
-  const uint32_t h = ((uint32_t)((int32_t)u >> 3) & 0x8FFFFFFFu) | 0x30000000u;   // x 2^-128 (normal x)
-  const double y = __hiloint2double((int)h, (int)(u << 29));
-  const double t = fma(y, p.s, kMagic + 140737488355328.0);                       // + 2^47
-  hi = (uint32_t)__double2hiint(t);
-  lo = (uint32_t)__double2loint(t);
+  const uint32_t h = ((uint32_t)((int32_t)u >> 3) & 0x8FFFFFFFu) | 0x30000000u;   // x 2^-128
+  const double t = fma(__hiloint2double((int)h, (int)(u << 29)), s, kMagic + 140737488355328.0);
+  return make_uint2((uint32_t)__double2loint(t), (uint32_t)__double2hiint(t));
 }
-// fp64: (hi, lo) words holding F(x) + C (signed digits, see above)
-__device__ __forceinline__ void split_words(double x, const ColParam& p, uint32_t& hi, uint32_t& lo) {
-  const double t1 = __fma_rd(x, p.s, kMagic + (double)0x808080u);
+// fp64: F + C (C = 0x80 in bytes 0..6) by two magic-constant floors, returned as the signed digits (bytes XOR
+// 0x80 but the top one): byte b has weight 256^b
+__device__ __forceinline__ uint2 magic_word(double x, double s) {
+  const double t1 = __fma_rd(x, s, kMagic + (double)0x808080u);
   const double H = t1 - (kMagic + (double)0x808080u);       // floor(x 2^(31-e)), exact
-  const double r = fma(x, p.s, -H);                          // in [0, 1), exact
+  const double r = fma(x, s, -H);                          // in [0, 1), exact
   const double t2 = __fma_rd(r, 4294967296.0, kMagic + (double)0x80808080u);
-  lo = (uint32_t)__double2loint(t2);
-  hi = (uint32_t)__double2loint(t1) + ((uint32_t)__double2hiint(t2) & 1u);   // carry of L + C_lo
+  const uint32_t lo = (uint32_t)__double2loint(t2);
+  const uint32_t hi = (uint32_t)__double2loint(t1) + ((uint32_t)__double2hiint(t2) & 1u);   // carry of L + C_lo
+  return make_uint2(lo ^ 0x80808080u, hi ^ 0x00808080u);
 }
 
 template <typename TX>
 __global__ void __launch_bounds__(STC_THREADS, 1)
-sketch_sparse_tc_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64_t row_offset, int k, int zeta,
-                        uint64_t seed, int tiles_k, int64_t rows_per_split, double* __restrict__ part, int* overflow, int dbg_in,
-                        const uint64_t* __restrict__ srht_s) {
+sketch_sparse_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int n, int64_t row_offset, int k,
+                        int zeta, uint64_t seed, int tiles_k, int tiles_n, int64_t rows_per_split,
+                        double* __restrict__ part, int* overflow, int dbg_in, const uint64_t* __restrict__ srht_s) {
   const int dbg = kAblation ? dbg_in : 0;   // ablation switches (see internal.cuh)
   using C = StcCfg<TX>;
   using F = Fmt<TX>;
-  constexpr int D = C::D;
   extern __shared__ __align__(1024) unsigned char sm[];
-  unsigned char* dig_base = sm;                                                 // [DIG][DIG_STAGE]
-  TX* raw_base = reinterpret_cast<TX*>(sm + (size_t)F::DIG * C::DIG_STAGE);    // [RAW][KC][n]
+  unsigned char* dig_base = sm;                                                 // [DIG][E | B]
+  TX* raw_base = reinterpret_cast<TX*>(sm + (size_t)F::DIG * C::DIG_STAGE);    // [RAW][KC][64]
   uint64_t* dfull = reinterpret_cast<uint64_t*>(sm + (size_t)F::DIG * C::DIG_STAGE + (size_t)F::RAW * C::RAW_STAGE);
   uint64_t* dempty = dfull + F::DIG;
   uint64_t* rfull = dempty + F::DIG;
@@ -166,13 +157,13 @@ sketch_sparse_tc_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx,
   uint32_t* col_max = tmem_slot + 1;                                            // [STC_N] high |x| bits
   int* col_exp = reinterpret_cast<int*>(col_max + STC_N);                      // [STC_N]
 
-  const int tk = blockIdx.x % tiles_k, split = blockIdx.x / tiles_k;
-  const int r0 = tk * STC_M;
+  const int tk = blockIdx.x % tiles_k, tn = (blockIdx.x / tiles_k) % tiles_n, split = blockIdx.x / (tiles_k * tiles_n);
+  const int r0 = tk * STC_M, n0 = tn * STC_N;
   const int64_t i_begin = (int64_t)split * rows_per_split;
   const int64_t i_end = min(m, i_begin + rows_per_split);
   const int nstages = i_end > i_begin ? (int)((i_end - i_begin + STC_KC - 1) / STC_KC) : 0;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int beta = zeta > 0 ? k / zeta : 1;            // zeta = 0: dense Rademacher E (no blocks)
+  const int beta = zeta > 0 ? k / zeta : 1;            // zeta <= 0: dense Rademacher / SRHT E (no blocks)
 
   if (tid == 0) {
     for (int s = 0; s < F::DIG; ++s) {
@@ -184,15 +175,6 @@ sketch_sparse_tc_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx,
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (tid < STC_N) { col_max[tid] = 0u; col_exp[tid] = 0; }
-  if constexpr (F::ONES > 0) {   // constant ones-block (rows 0..15 of group 0) in every operand slot
-    for (int u = tid; u < F::DIG * F::ONES * STC_KC / 16; u += STC_THREADS) {
-      const int s = u / (F::ONES * STC_KC / 16), v = u % (F::ONES * STC_KC / 16);
-      const int r = v % F::ONES, kb = v / F::ONES;
-      *reinterpret_cast<uint4*>(dig_base + (size_t)s * C::DIG_STAGE + C::E_BYTES + cm_off(r, kb * 16, C::N0)) =
-          make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
-    }
-    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-  }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(tc::smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -204,8 +186,7 @@ sketch_sparse_tc_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx,
 
   if (warp == 0) {
     // ---------------------------------------------------------------- MMA issuer (lane 0)
-    constexpr uint32_t id0 = tc::idesc_i8(STC_M, C::N0, true, F::SIGNED);   // E (s8) x digit group
-    constexpr uint32_t id1 = tc::idesc_i8(STC_M, C::N1, true, F::SIGNED);
+    constexpr uint32_t idesc = tc::idesc_i8(STC_M, STC_BN / 2, true, F::SIGNED) | (1u << 16);   // B MN-major
     for (int c = 0; c < nstages; ++c) {
       const int s = c % F::DIG;
       tc::mbar_wait(&dfull[s], (uint32_t)((c / F::DIG) & 1));
@@ -217,10 +198,11 @@ sketch_sparse_tc_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx,
           for (int ks = 0; ks < STC_KC / 32; ++ks) {
             const uint64_t da = tc::desc(sa + ks * 2 * (STC_M / 8) * 128, (STC_M / 8) * 128, 128);
             const uint32_t accum = (c > 0 || ks > 0) ? 1u : 0u;
-            const uint32_t sb0 = sa + C::E_BYTES + ks * 2 * (C::N0 / 8) * 128;
-            const uint32_t sb1 = sa + C::E_BYTES + C::G0_BYTES + ks * 2 * (C::N1 / 8) * 128;
-            tc::mma_i8(tmem, da, tc::desc(sb0, (C::N0 / 8) * 128, 128), id0, accum);
-            tc::mma_i8(tmem + C::TBASE1, da, tc::desc(sb1, (C::N1 / 8) * 128, 128), id1, accum);
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const uint32_t sb = sa + STC_E_BYTES + h * (STC_BN / 32) * 128 + ks * 4 * STC_LBO;
+              tc::mma_i8(tmem + h * (STC_BN / 2), da, tc::desc(sb, STC_LBO, 128), idesc, accum);
+            }
           }
         }
         tc::commit(&dempty[s]);          // stage reusable once these MMAs have consumed it
@@ -229,109 +211,99 @@ sketch_sparse_tc_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx,
       __syncwarp();
     }
   } else if (warp == 1) {
-    // ---------------------------------------------------------------- X loader (bulk copies, lane 0)
-    const bool contiguous = ldx == n;
-    const uint32_t row_bytes = (uint32_t)(n * sizeof(TX));
-    // contiguous X: stages up to STC_PF ahead are prefetched into L2 (no shared memory), so that more
-    // HBM bytes are in flight per SM than the raw ring holds; the ring's bulk copies then hit L2
-    auto prefetch = [&](int c) {
-      const int64_t i0 = i_begin + (int64_t)c * STC_KC;
-      const int rows = (int)min((int64_t)STC_KC, i_end - i0);
-      tc::bulk_prefetch_l2(X + i0 * ldx, row_bytes * rows);
-    };
-    if (contiguous && lane == 0)
-      for (int c = 1; c < STC_PF && c < nstages; ++c) prefetch(c);
+    // ---------------------------------------------------------------- X loader (2D TMA, lane 0)
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];\n" ::"l"(&xmap) : "memory");
+      for (int c = 1; c < STC_PF && c < nstages; ++c) tc::tma_prefetch_2d(&xmap, n0, (int)(i_begin + (int64_t)c * STC_KC));
+    }
     for (int c = 0; c < nstages; ++c) {
       const int s = c % F::RAW;
       if (c >= F::RAW) tc::mbar_wait(&rempty[s], (uint32_t)(((c / F::RAW) - 1) & 1));
       if (lane == 0) {
-        if (contiguous && c + STC_PF < nstages) prefetch(c + STC_PF);
-        const int64_t i0 = i_begin + (int64_t)c * STC_KC;
-        const int rows = (int)min((int64_t)STC_KC, i_end - i0);
-        TX* dst = raw_base + (size_t)s * STC_KC * n;
-        tc::mbar_arrive_tx(&rfull[s], row_bytes * rows);
-        if (contiguous) {
-          tc::bulk_g2s(dst, X + i0 * ldx, row_bytes * rows, &rfull[s]);
-        } else {
-          for (int ii = 0; ii < rows; ++ii) tc::bulk_g2s(dst + (size_t)ii * n, X + (i0 + ii) * ldx, row_bytes, &rfull[s]);
-        }
+        if (c + STC_PF < nstages) tc::tma_prefetch_2d(&xmap, n0, (int)(i_begin + (int64_t)(c + STC_PF) * STC_KC));
+        tc::mbar_arrive_tx(&rfull[s], (uint32_t)C::RAW_STAGE);
+        tc::tma_load_2d(raw_base + (size_t)s * STC_KC * STC_N, &xmap, n0, (int)(i_begin + (int64_t)c * STC_KC), &rfull[s]);
       }
       __syncwarp();
     }
   } else if (warp < 2 + STC_DGROUPS * STC_DWARPS) {
-    // ---------------------------------------------------------------- digit planes
+    // ---------------------------------------------------------------- B bytes
+    // Thread -> (fixed 16-byte raw chunk c of a row, rows 8 rb + q): lane = 8 p + q, chunk
+    // c = 8 cb + ((q + p + rot) & 7).  Every 8-lane phase of an LDS.128 then reads 8 distinct bank groups
+    // (c mod 8) and every phase of the STS.128 into B writes 8 distinct ones (row mod 8).
     const int dgrp = (warp - 2) / STC_DWARPS;            // stages c = dgrp (mod 2)
-    const int dt = tid - 64 - dgrp * 32 * STC_DWARPS;
-    const int j = dt % STC_N, kg = dt / STC_N;           // fixed task: column j, rows kg*16 .. +15
-    ColParam cp{};
+    const int w = (warp - 2) % STC_DWARPS, p = lane >> 3, q = lane & 7;
+    const int wi = w & 3, rot = 4 * (w >> 2);
+    const int cb = wi % C::CB, rbase = (wi / C::CB) * C::TASKS;
+    const int ch = 8 * cb + ((q + p + rot) & 7);         // this thread's raw chunk (columns ch * CE .. + CE - 1)
+    double sc[C::CE];
+    uint32_t lim[C::CE];
+    bool bad = false;
     if (nstages > 0) {                                   // column scales from the first stage (both groups)
       tc::mbar_wait(&rfull[0], 0u);
       const int rows0 = (int)min((int64_t)STC_KC, i_end - i_begin);
-      const TX* raw = raw_base;
-      for (int u = tid - 64; u < rows0 * n; u += 32 * STC_DGROUPS * STC_DWARPS) atomicMax(&col_max[u % n], hi_abs(raw[u]));
+      const int dt = tid - 64, j = dt & (STC_N - 1);
+      uint32_t mx = 0u;
+      for (int r = dt >> 6; r < rows0; r += 32 * STC_DGROUPS * STC_DWARPS / STC_N) mx = max(mx, hi_abs(raw_base[r * STC_N + j]));
+      atomicMax(&col_max[j], mx);
       tc::named_bar(1, 32 * STC_DGROUPS * STC_DWARPS);
-      cp = col_param<TX>(col_max[j < n ? j : 0]);
-      if (dgrp == 0 && kg == 0 && j < n) col_exp[j] = cp.e;
-    }
-    int dst_off[D];
 #pragma unroll
-    for (int t = 0; t < D; ++t)
-      dst_off[t] = C::E_BYTES + C::grp(t) * C::G0_BYTES + cm_off(C::brow(t) + j, kg * 16, C::grp(t) ? C::N1 : C::N0);
-    uint32_t acc_or = 0u, acc_and = 0xFFFFFFFFu, amax = 0u;   // overflow detection
+      for (int e = 0; e < C::CE; ++e) {
+        const ColParam cp = col_param<TX>(col_max[ch * C::CE + e]);
+        sc[e] = cp.s; lim[e] = cp.lim;
+        bad |= cp.bad && n0 + ch * C::CE + e < n;
+      }
+      if (dgrp == 0 && dt < STC_N) col_exp[dt] = col_param<TX>(col_max[dt]).e;
+    }
+    uint32_t acc = 0u;                                   // overflow detection
     for (int c = dgrp; c < nstages; c += STC_DGROUPS) {
       const int s = c % F::DIG, sr = c % F::RAW;
       const int64_t i0 = i_begin + (int64_t)c * STC_KC;
       const int rows = (int)min((int64_t)STC_KC, i_end - i0);
-      const TX* raw = raw_base + (size_t)sr * STC_KC * n;
+      const TX* raw = raw_base + (size_t)sr * STC_KC * STC_N;
       if (c >= F::DIG) tc::mbar_wait(&dempty[s], (uint32_t)(((c / F::DIG) - 1) & 1));
       tc::mbar_wait(&rfull[sr], (uint32_t)((c / F::RAW) & 1));
-      unsigned char* st = dig_base + (size_t)s * C::DIG_STAGE;
-      auto build = [&](auto full) {
-        constexpr bool FULL = decltype(full)::value;
-        uint32_t W[D][4];
-        const TX* src = FULL ? raw + (kg * 16) * STC_N + j : raw + (kg * 16) * n + j;
+      unsigned char* bt = dig_base + (size_t)s * C::DIG_STAGE + STC_E_BYTES;
+      if (!(dbg & 2)) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          uint32_t hw[4], lw[4];
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const int ii = q * 4 + kk;
-            TX x;
-            if constexpr (FULL) x = src[ii * STC_N];
-            else x = (kg * 16 + ii < rows && j < n) ? src[ii * n] : (TX)0;
-            split_words(x, cp, hw[kk], lw[kk]);
-            if constexpr (sizeof(TX) == 4) { acc_or |= hw[kk]; acc_and &= hw[kk]; }
-            else amax = max(amax, hi_abs(x));
+        for (int t = 0; t < C::TASKS; ++t) {
+          const int i = 8 * (rbase + t) + q;
+          TX x[C::CE];
+          if constexpr (sizeof(TX) == 4) {
+            const float4 f = *reinterpret_cast<const float4*>(raw + i * STC_N + ch * 4);
+            x[0] = f.x; x[1] = f.y; x[2] = f.z; x[3] = f.w;
+          } else {
+            const double2 f = *reinterpret_cast<const double2*>(raw + i * STC_N + ch * 2);
+            x[0] = f.x; x[1] = f.y;
           }
-          uint32_t H[4], L[4];
-          transpose4(hw[0], hw[1], hw[2], hw[3], H);
-          transpose4(lw[0], lw[1], lw[2], lw[3], L);
-          if constexpr (D == 6) {      // unsigned digits of F + 2^47
-            W[0][q] = H[1]; W[1][q] = H[0];
-            W[2][q] = L[3]; W[3][q] = L[2]; W[4][q] = L[1]; W[5][q] = L[0];
-          } else {                     // signed digits of F + C
-            W[0][q] = H[3]; W[1][q] = H[2] ^ 0x80808080u; W[2][q] = H[1] ^ 0x80808080u;
-            W[3][q] = H[0] ^ 0x80808080u;
-            W[4][q] = L[3] ^ 0x80808080u; W[5][q] = L[2] ^ 0x80808080u;
-            W[6][q] = L[1] ^ 0x80808080u; W[7][q] = L[0] ^ 0x80808080u;
+          if (i >= rows) {                                 // rows of the next split (or past m): E is zero there
+#pragma unroll
+            for (int e = 0; e < C::CE; ++e) x[e] = (TX)0;
+          }
+          uint2 wv[C::CE];
+#pragma unroll
+          for (int e = 0; e < C::CE; ++e) {
+            wv[e] = magic_word(x[e], sc[e]);
+            if constexpr (sizeof(TX) == 4) acc |= wv[e].y ^ 0x43380000u;
+            else acc |= hi_abs(x[e]) >= lim[e] ? 1u : 0u;
+          }
+          // element pair (2 g, 2 g + 1) of the tile's columns -> MN group g (16 bytes), row i
+#pragma unroll
+          for (int e = 0; e < C::CE; e += 2) {
+            const int g = (ch * C::CE + e) >> 1;
+            *reinterpret_cast<uint4*>(bt + (i & 7) * 16 + g * 128 + (i >> 3) * STC_LBO) =
+                make_uint4(wv[e].x, wv[e].y, wv[e + 1].x, wv[e + 1].y);
           }
         }
-#pragma unroll
-        for (int t = 0; t < D; ++t)
-          *reinterpret_cast<uint4*>(st + dst_off[t]) = make_uint4(W[t][0], W[t][1], W[t][2], W[t][3]);
-      };
-      if (!(dbg & 2)) {
-        if (rows == STC_KC && n == STC_N) build(std::true_type{});
-        else build(std::false_type{});
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic smem writes -> tensor core
       __syncwarp();
       if (lane == 0) { tc::mbar_arrive(&dfull[s]); tc::mbar_arrive(&rempty[sr]); }
     }
     bool ovf;
-    if constexpr (sizeof(TX) == 4) ovf = (acc_or >> 16) != 0x4338u || (acc_and >> 16) != 0x4338u;
-    else ovf = amax >= cp.lim;
-    if (nstages > 0 && (ovf || cp.bad)) atomicOr(overflow, 1);        // headroom exceeded / Inf / NaN
+    if constexpr (sizeof(TX) == 4) ovf = (acc >> 16) != 0u;
+    else ovf = acc != 0u;
+    if (nstages > 0 && (ovf || bad)) atomicOr(overflow, 1);        // headroom exceeded / Inf / NaN
   } else {
     // ---------------------------------------------------------------- E tile (Philox, theta.cuh)
     // Two groups of two warps take alternate stages (group g: stages c = g mod 2), each lane one X
@@ -456,38 +428,41 @@ sketch_sparse_tc_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx,
     double* Pp = part + (size_t)split * (size_t)k * n;
     const int row = r0 + warp * 32 + lane;             // TMEM lane = Theta row
     const uint32_t lbase = tmem + ((uint32_t)(warp * 32) << 16);
+    const int ncols = min(STC_N, n - n0);
     if (nstages > 0) {
       tc::mbar_wait(done, 0u);
       asm volatile("tcgen05.fence::after_thread_sync;\n");
-      int32_t bias = 0;                                  // 128 S_r (fp32 digits are of F + 2^47)
-      if constexpr (F::ONES > 0) {
-        uint32_t a[16];
-        tc::ld16(lbase, a);
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n");
-        bias = 128 * (int32_t)a[0];
+      int32_t bias = 0;                                  // fp32: 2^47 S_r = 128 S_r at weight 256^5
+      if constexpr (!F::SIGNED) {
+        uint32_t a[8];
+        tc::ld8(lbase, a);
+        tc::wait_ld();
+        bias = 128 * ((int32_t)a[6] / 0x38);             // column 6: 0x38 S_r exactly
       }
 #pragma unroll 1
-      for (int c0 = 0; c0 < STC_N; c0 += 16) {
-        double v[16];
+      for (int j0 = 0; j0 < STC_N; j0 += 2) {
+        uint32_t a[16];                                  // the 8 byte accumulators of columns j0, j0 + 1
+        tc::ld16(lbase + 8 * j0, a);
+        tc::wait_ld();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0.0;
+        for (int u = 0; u < 2; ++u) {
+          const int j = j0 + u;
+          const uint32_t* b = a + 8 * u;
+          double v;
+          if constexpr (F::SIGNED) {
+            v = (double)(int32_t)b[7];
 #pragma unroll
-        for (int t = D - 1; t >= 0; --t) {             // least significant plane first
-          uint32_t a[16];
-          tc::ld16(lbase + C::tcol(t) + c0, a);
-          asm volatile("tcgen05.wait::ld.sync.aligned;\n");
-          const double w = (double)(1ull << (8 * (D - 1 - t)));
+            for (int t = 6; t >= 0; --t) v = fma(v, 256.0, (double)(int32_t)b[t]);
+          } else {
+            v = (double)((int32_t)b[5] - bias);
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = fma((double)((int32_t)a[j] - (t == 0 ? bias : 0)), w, v[j]);
-        }
-        if (row < k) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (c0 + j < n) Pp[(size_t)row * n + c0 + j] = ldexp(v[j], col_exp[c0 + j] - F::FB);
+            for (int t = 4; t >= 0; --t) v = fma(v, 256.0, (double)(int32_t)b[t]);
+          }
+          if (row < k && j < ncols) Pp[(size_t)row * n + n0 + j] = ldexp(v, col_exp[j] - F::FB);
         }
       }
     } else if (row < k) {
-      for (int j = 0; j < n; ++j) Pp[(size_t)row * n + j] = 0.0;
+      for (int j = 0; j < ncols; ++j) Pp[(size_t)row * n + n0 + j] = 0.0;
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -495,18 +470,41 @@ sketch_sparse_tc_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx,
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem));
 }
 
-bool sparse_tc_applicable(int k, int n, int zeta) { return n <= STC_N && zeta >= 1 && k % zeta == 0 && k <= 4 * STC_M; }
+// tcgen05 path: any n (64-column tiles), k <= 4 * 128 Theta rows
+bool sparse_tc_applicable(int k, int n, int zeta) { return n >= 1 && zeta >= 1 && k % zeta == 0 && k <= 4 * STC_M; }
+
+using EncodeTiledFnS = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 template <typename TX>
 static cudaError_t launch_stc(const TX* X, int64_t m, int n, int64_t ldx, int64_t ro, int k, int zeta, uint64_t seed,
                               int tiles_k, int splits, int64_t rps, double* part, int* overflow, cudaStream_t st,
                               const uint64_t* srht_s) {
+  static EncodeTiledFnS enc = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFnS>(p);
+  }();
+  if (!enc) return cudaErrorNotSupported;
+  CUtensorMap map;
+  const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)m};
+  const cuuint64_t strides[1] = {(cuuint64_t)ldx * sizeof(TX)};
+  const cuuint32_t box[2] = {(cuuint32_t)STC_N, (cuuint32_t)STC_KC}, estr[2] = {1, 1};
+  if (enc(&map, sizeof(TX) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+          const_cast<TX*>(X), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorNotSupported;
   auto kern = sketch_sparse_tc_kernel<TX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)StcCfg<TX>::SMEM);
   if (e != cudaSuccess) return e;
   static const int dbg = !kAblation ? 0 : getenv("RCHOLQR_STC_DEBUG") ? atoi(getenv("RCHOLQR_STC_DEBUG")) : 0;   // ablations only
-  kern<<<tiles_k * splits, STC_THREADS, StcCfg<TX>::SMEM, st>>>(X, m, n, ldx, ro, k, zeta, seed, tiles_k, rps, part,
-                                                                 overflow, dbg, srht_s);
+  const int tiles_n = (n + STC_N - 1) / STC_N;
+  kern<<<tiles_k * tiles_n * splits, STC_THREADS, StcCfg<TX>::SMEM, st>>>(map, m, n, ro, k, zeta, seed, tiles_k, tiles_n,
+                                                                           rps, part, overflow, dbg, srht_s);
   return cudaGetLastError();
 }
 
@@ -521,9 +519,10 @@ cudaError_t launch_sparse_tc(const void* X, int dtype, int64_t m, int n, int64_t
                     overflow, st, srht_s);
 }
 
-bool sparse_tc_aligned(const void* X, int dtype, int n, int64_t ldx) {
-  const size_t es = dtype == RCHOLQR_F64 ? 8 : 4;   // cp.async.bulk: 16-byte aligned addresses and sizes
-  return ((uintptr_t)X % 16) == 0 && ((size_t)n * es) % 16 == 0 && ((size_t)ldx * es) % 16 == 0;
+// 2D TMA of X: 16-byte aligned base and row pitch, row coordinates < 2^31
+bool sparse_tc_aligned(const void* X, int dtype, int64_t m, int64_t ldx) {
+  const size_t es = dtype == RCHOLQR_F64 ? 8 : 4;
+  return ((uintptr_t)X % 16) == 0 && ((size_t)ldx * es) % 16 == 0 && m < ((int64_t)1 << 31);
 }
 
 }  // namespace rcq

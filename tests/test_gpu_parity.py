@@ -87,9 +87,12 @@ SPARSE_TC_CASES = [
     (100_003, 64, 128, "f64", 8, None),          # C4 shape, fp64 X: 8 digit planes
     (50_001, 20, 40, "f32", 4, None),            # n < 64, k < 128
     (30_000, 50, 256, "f64", 8, None),           # two Theta row tiles
-    (20_000, 60, 120, "f32", 8, 68),             # strided rows (one bulk copy per row)
+    (20_000, 60, 120, "f32", 8, 68),             # strided rows (2D TMA box with a 68-float pitch)
     (20_000, 61, 122, "f32", 2, 63),             # unaligned rows -> CUDA-core kernel
     (65, 64, 128, "f32", 8, None),               # fewer rows than CTAs, one ragged stage
+    (40_000, 100, 200, "f32", 8, None),          # two 64-column tiles (C2 width), ragged last tile
+    (30_000, 130, 256, "f64", 8, 136),           # three column tiles x two Theta row tiles, strided
+    (70_001, 33, 64, "f32", 8, None),            # n*4 not a multiple of 16 B: TMA box clips the row
 ]
 
 
@@ -105,6 +108,12 @@ def test_sketch_sparse_tc_parity(cuda, m, n, k, dt, nnz, ldx):
     Pg = _np(plan.sketch(Xt, row_offset=977))
     Po = oracle.sketch(X, k, sketch=oracle.SPARSE_SIGN, zeta=nnz, seed=11, row_offset=977)
     assert _rel(Pg, Po) <= 1e-12, _rel(Pg, Po)
+    aligned = (Xt.stride(0) * Xt.element_size()) % 16 == 0
+    path = plan.last_path()
+    if aligned:   # the tcgen05 kernel served the call, without the overflow fallback
+        assert path & rcq.PATH_SKETCH_TC and not path & rcq.PATH_SKETCH_FALLBACK, path
+    else:
+        assert path & rcq.PATH_SKETCH_CUDA_CORE and not path & rcq.PATH_SKETCH_TC, path
 
 
 @pytest.mark.parametrize("dt,case", [("f32", "spike"), ("f64", "spike"), ("f32", "zero_head")])
@@ -121,6 +130,8 @@ def test_sketch_sparse_tc_headroom_overflow(cuda, dt, case):
     Pg = _np(plan.sketch(_t(X)))
     Po = oracle.sketch(X, k, sketch=oracle.SPARSE_SIGN, zeta=8)
     assert _rel(Pg, Po) <= 1e-12, _rel(Pg, Po)
+    path = plan.last_path()
+    assert path & rcq.PATH_SKETCH_TC and path & rcq.PATH_SKETCH_FALLBACK, path
 
 
 def test_sketch_sparse_tc_matches_cuda_core(cuda, monkeypatch):
