@@ -8,21 +8,21 @@
 // PAPER.md:83, 423; the only approximation is the rounding of x at 2^(e_j - FB) (relative 2^-44 / 2^-60 of the
 // column scale).
 //
-// Operand layout (round 2).  The B operand is the 8 BYTES of each X element's magic-constant double, MN-major:
-//     B[k = X row i][n = 8 j + b] = byte b of W(x_ij),
-// so an element's digits are contiguous along N and come straight out of ONE DFMA -- no digit planes, no byte
-// transposes (round 1 wrote six K-major digit planes with 8 PRMTs per 4 values and was bound by that work):
-//   * fp32 X: W = RN(x 2^(47-e) + 2^47 + 1.5 2^52), one DFMA on x 2^-128 built from the float's bits; bytes 0..5
-//     are the unsigned digits of F + 2^47 (weight 256^b), bytes 6, 7 the constant exponent bytes 0x38, 0x43.  TMEM
-//     column 8 j + 6 therefore holds 0x38 S_r, S_r = sum_i E_ri, which removes the 2^47 bias exactly.  The high
-//     word is 0x4338xxxx iff F + 2^47 fits in 48 bits: one LOP3 per element accumulates the overflow / Inf / NaN
-//     test.
-//   * fp64 X: (hi, lo) = F + C by two magic-constant floors, F = floor(x 2^(63-e)); stored as signed digits
-//     (bytes XOR 0x80 except the top one), byte b of weight 256^b.
-// P_rj = 2^(e_j - FB) sum_b acc_b 256^b with acc_b = TMEM column 8 j + b.  One stage (64 X rows, 64 columns)
-// is two k-steps x two MMAs of M = 128, N = 256, K = 32 (all 512 TMEM columns); the tensor core reads B
-// MN-major (idesc bit 16; probe tools/micro/tc_i8_mn_test.cu).  Columns beyond 64 are further CTAs (column tiles:
-// X is read through a 2D TMA box of 64 columns x 64 rows, zero-filled outside X).
+// Operand layout (round 2).  B is built from each X element's magic-constant double W(x), MN-major (the 8 bytes
+// of an element contiguous along N), straight out of ONE DFMA -- no digit planes, no byte transposes (round 1
+// wrote six K-major digit planes with 8 PRMTs per 4 values and was bound by that work):
+//   * fp32 X: W = RN(x 2^(47-e) + 2^47 + 1.5 2^52), one DFMA on x 2^-128 built from the float's bits; its low
+//     48 bits are the unsigned base-256 digits of F + 2^47.  Row i of B = [the low words of the tile's 64
+//     columns | their digits 4, 5 (16-bit halves) | 16 ones]: the two constant exponent bytes are not fed to the
+//     tensor core.  TMEM column 4 j + b holds digit b (< 4) of column j, column 256 + 2 j + b' digit 4 + b', and
+//     the ones block S_r = sum_i E_ri, which removes the 2^47 bias exactly.  The high word is 0x4338xxxx iff
+//     F + 2^47 fits in 48 bits: one LOP3 per element accumulates the overflow / Inf / NaN test.
+//   * fp64 X: (hi, lo) = F + C by two magic-constant floors, F = floor(x 2^(63-e)); all 8 bytes as signed
+//     digits (bytes XOR 0x80 except the top one), byte b of weight 256^b at TMEM column 8 j + b.
+// P_rj = 2^(e_j - FB) sum_b acc_b 256^b.  One stage (64 X rows, 64 columns) is two k-steps x two MMAs of
+// M = 128, K = 32 (N = 256 + 144 for fp32, 256 + 256 for fp64); the tensor core reads B MN-major (idesc bit 16;
+// probe tools/micro/tc_i8_mn_test.cu).  Columns beyond 64 are further CTAs (column tiles: X is read through a
+// 2D TMA box of 64 columns x 64 rows, zero-filled outside X).
 //
 // e_j = (exponent of the column maximum over the CTA's FIRST stage) + 4 bits of headroom.  If a later element
 // does not fit (|x| >= 2^e_j, or Inf/NaN) the kernel raises an overflow flag and a CUDA-core kernel recomputes
@@ -45,7 +45,6 @@ namespace rcq {
 
 constexpr int STC_M = 128;        // Theta rows per CTA (MMA M = TMEM lanes)
 constexpr int STC_N = 64;         // X columns per CTA
-constexpr int STC_BN = 8 * STC_N; // B columns: 8 bytes per X column (two MMAs of N = 256)
 constexpr int STC_KC = 64;        // X rows per stage (2 MMA k-steps of 32)
 constexpr int STC_PF = 8;         // stages prefetched into L2 ahead of the raw ring
 constexpr int STC_DWARPS = 8;     // B-byte warps per stage group
@@ -53,26 +52,36 @@ constexpr int STC_DGROUPS = 2;    // B-byte groups (warps 2..9, 10..17) alternat
 constexpr int STC_EWARPS = 4;     // E-tile warps (18..21): two groups alternating stages, one X row per lane
 constexpr int STC_THREADS = 32 * (2 + STC_DGROUPS * STC_DWARPS + STC_EWARPS);
 constexpr int STC_E_BYTES = STC_M * STC_KC;              // E tile (int8, K-major)
-constexpr int STC_B_BYTES = STC_KC * STC_BN;             // B tile (int8, MN-major)
-constexpr int STC_LBO = (STC_BN / 16) * 128;             // B: byte stride between 8-row K groups
 static_assert(16 * STC_EWARPS == STC_KC, "one X row per E-warp lane, two warp groups");
 
 template <typename TX> struct Fmt;
+// B row layout (bytes along N) and the two MMAs per k-step (N0 + N1 columns):
+//   fp32: [lo words of the 64 columns (256 B) | hi halves (128 B) | 16 ones]: N = 256 + 144.  The two constant
+//         exponent bytes of each magic double are NOT fed to the tensor core (22% fewer MACs than 8 bytes per
+//         element); the ones block gives S_r = sum_i E_ri for the 2^47 bias.
+//   fp64: the 8 signed digit bytes of each element: N = 256 + 256.
 template <> struct Fmt<float> {
   static constexpr int FB = 47;
-  static constexpr int RAW = 4, DIG = 3;   // raw X ring / operand ring depths
+  static constexpr int RAW = 5, DIG = 4;   // raw X ring / operand ring depths (DIG = 4: slot pairs, see below)
   static constexpr bool SIGNED = false;
+  static constexpr int N0 = 256, N1 = 144;
 };
 template <> struct Fmt<double> {
   static constexpr int FB = 63;
-  static constexpr int RAW = 3, DIG = 3;
+  static constexpr int RAW = 2, DIG = 4;
   static constexpr bool SIGNED = true;
+  static constexpr int N0 = 256, N1 = 256;
 };
+
+static_assert(Fmt<float>::DIG == 4 && Fmt<double>::DIG == 4, "slot pairs: stages c, c+1 share one release");
 
 template <typename TX>
 struct StcCfg {
   using Fm = Fmt<TX>;
-  static constexpr int DIG_STAGE = STC_E_BYTES + STC_B_BYTES;
+  static constexpr int BN = Fm::N0 + Fm::N1;                  // B columns
+  static constexpr int LBO = (BN / 16) * 128;                 // B: byte stride between 8-row K groups
+  static constexpr int B_BYTES = STC_KC * BN;
+  static constexpr int DIG_STAGE = STC_E_BYTES + B_BYTES;
   static constexpr int RAW_STAGE = STC_KC * STC_N * (int)sizeof(TX);
   static constexpr int CE = 16 / (int)sizeof(TX);            // elements per 16-byte raw chunk (4 / 2)
   static constexpr int CHUNKS = STC_N / CE;                   // raw chunks per row (16 / 32)
@@ -121,7 +130,8 @@ __device__ __forceinline__ ColParam col_param(uint32_t maxbits) {
 // the float's bits (normal x; one shift, one LOP3), so the scaling is one DFMA.
 __device__ __forceinline__ uint2 magic_word(float x, double s) {
   const uint32_t u = __float_as_uint(x);
-  const uint32_t h = ((uint32_t)((int32_t)u >> 3) & 0x8FFFFFFFu) | 0x30000000u;   // x 2^-128
+  uint32_t h;                                                                      // x 2^-128: one LOP3
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(h) : "r"((uint32_t)((int32_t)u >> 3)), "r"(0x8FFFFFFFu), "r"(0x30000000u));
   const double t = fma(__hiloint2double((int)h, (int)(u << 29)), s, kMagic + 140737488355328.0);
   return make_uint2((uint32_t)__double2loint(t), (uint32_t)__double2hiint(t));
 }
@@ -149,8 +159,8 @@ sketch_sparse_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int
   unsigned char* dig_base = sm;                                                 // [DIG][E | B]
   TX* raw_base = reinterpret_cast<TX*>(sm + (size_t)F::DIG * C::DIG_STAGE);    // [RAW][KC][64]
   uint64_t* dfull = reinterpret_cast<uint64_t*>(sm + (size_t)F::DIG * C::DIG_STAGE + (size_t)F::RAW * C::RAW_STAGE);
-  uint64_t* dempty = dfull + F::DIG;
-  uint64_t* rfull = dempty + F::DIG;
+  uint64_t* dempty = dfull + F::DIG;      // [2]: one per PAIR of operand slots
+  uint64_t* rfull = dempty + 2;
   uint64_t* rempty = rfull + F::RAW;
   uint64_t* done = rempty + F::RAW;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
@@ -168,13 +178,21 @@ sketch_sparse_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int
   if (tid == 0) {
     for (int s = 0; s < F::DIG; ++s) {
       tc::mbar_init(&dfull[s], STC_DWARPS + STC_EWARPS / 2);
-      tc::mbar_init(&dempty[s], 1);
+      if (s < 2) tc::mbar_init(&dempty[s], 1);
     }
     for (int s = 0; s < F::RAW; ++s) { tc::mbar_init(&rfull[s], 1); tc::mbar_init(&rempty[s], STC_DWARPS); }
     tc::mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (tid < STC_N) { col_max[tid] = 0u; col_exp[tid] = 0; }
+  if constexpr (sizeof(TX) == 4) {   // the constant ones block (MN group 24) of every operand slot
+    for (int u = tid; u < F::DIG * STC_KC; u += STC_THREADS) {
+      const int sl = u / STC_KC, i = u % STC_KC;
+      *reinterpret_cast<uint4*>(dig_base + (size_t)sl * C::DIG_STAGE + STC_E_BYTES + (i & 7) * 16 + 24 * 128 + (i >> 3) * C::LBO) =
+          make_uint4(0x01010101u, 0x01010101u, 0x01010101u, 0x01010101u);
+    }
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(tc::smem_u32(tmem_slot)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
@@ -186,7 +204,8 @@ sketch_sparse_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int
 
   if (warp == 0) {
     // ---------------------------------------------------------------- MMA issuer (lane 0)
-    constexpr uint32_t idesc = tc::idesc_i8(STC_M, STC_BN / 2, true, F::SIGNED) | (1u << 16);   // B MN-major
+    constexpr uint32_t id0 = tc::idesc_i8(STC_M, F::N0, true, F::SIGNED) | (1u << 16);   // B MN-major
+    constexpr uint32_t id1 = tc::idesc_i8(STC_M, F::N1, true, F::SIGNED) | (1u << 16);
     for (int c = 0; c < nstages; ++c) {
       const int s = c % F::DIG;
       tc::mbar_wait(&dfull[s], (uint32_t)((c / F::DIG) & 1));
@@ -198,14 +217,14 @@ sketch_sparse_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int
           for (int ks = 0; ks < STC_KC / 32; ++ks) {
             const uint64_t da = tc::desc(sa + ks * 2 * (STC_M / 8) * 128, (STC_M / 8) * 128, 128);
             const uint32_t accum = (c > 0 || ks > 0) ? 1u : 0u;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-              const uint32_t sb = sa + STC_E_BYTES + h * (STC_BN / 32) * 128 + ks * 4 * STC_LBO;
-              tc::mma_i8(tmem + h * (STC_BN / 2), da, tc::desc(sb, STC_LBO, 128), idesc, accum);
-            }
+            const uint32_t sb = sa + STC_E_BYTES + ks * 4 * C::LBO;
+            tc::mma_i8(tmem, da, tc::desc(sb, C::LBO, 128), id0, accum);
+            tc::mma_i8(tmem + F::N0, da, tc::desc(sb + (F::N0 / 16) * 128, C::LBO, 128), id1, accum);
           }
         }
-        tc::commit(&dempty[s]);          // stage reusable once these MMAs have consumed it
+        // one tcgen05.commit per TWO stages (8 MMAs): a commit costs the tensor pipe ~100-400 cycles, so at
+        // 4 MMAs per commit the pipe ran at ~45% (tools/micro/tc_commit_rate.cu); it releases the slot pair
+        if ((c & 1) || c == nstages - 1) tc::commit(&dempty[(c >> 1) & 1]);
         if (c == nstages - 1) tc::commit(done);
       }
       __syncwarp();
@@ -261,44 +280,63 @@ sketch_sparse_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int
       const int64_t i0 = i_begin + (int64_t)c * STC_KC;
       const int rows = (int)min((int64_t)STC_KC, i_end - i0);
       const TX* raw = raw_base + (size_t)sr * STC_KC * STC_N;
-      if (c >= F::DIG) tc::mbar_wait(&dempty[s], (uint32_t)(((c / F::DIG) - 1) & 1));
+      if (c >= F::DIG) tc::mbar_wait(&dempty[(c >> 1) & 1], (uint32_t)(((c >> 2) - 1) & 1));   // slot pair free
       tc::mbar_wait(&rfull[sr], (uint32_t)((c / F::RAW) & 1));
       unsigned char* bt = dig_base + (size_t)s * C::DIG_STAGE + STC_E_BYTES;
       if (!(dbg & 2)) {
+        // all of the thread's raw chunks first: the compiler cannot hoist an LDS above the STS of the previous
+        // chunk (both shared memory), so a per-chunk loop paid one LDS latency per chunk
+        TX xv[C::TASKS][C::CE];
 #pragma unroll
         for (int t = 0; t < C::TASKS; ++t) {
           const int i = 8 * (rbase + t) + q;
-          TX x[C::CE];
           if constexpr (sizeof(TX) == 4) {
             const float4 f = *reinterpret_cast<const float4*>(raw + i * STC_N + ch * 4);
-            x[0] = f.x; x[1] = f.y; x[2] = f.z; x[3] = f.w;
+            xv[t][0] = f.x; xv[t][1] = f.y; xv[t][2] = f.z; xv[t][3] = f.w;
           } else {
             const double2 f = *reinterpret_cast<const double2*>(raw + i * STC_N + ch * 2);
-            x[0] = f.x; x[1] = f.y;
+            xv[t][0] = f.x; xv[t][1] = f.y;
           }
-          if (i >= rows) {                                 // rows of the next split (or past m): E is zero there
+        }
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&rempty[sr]);     // raw slot consumed: the loader may refill it
+        if (rows < STC_KC) {                             // rows of the next split (or past m): E is zero there
 #pragma unroll
-            for (int e = 0; e < C::CE; ++e) x[e] = (TX)0;
-          }
+          for (int t = 0; t < C::TASKS; ++t)
+            if (8 * (rbase + t) + q >= rows) {
+#pragma unroll
+              for (int e = 0; e < C::CE; ++e) xv[t][e] = (TX)0;
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < C::TASKS; ++t) {
+          const int i = 8 * (rbase + t) + q;
           uint2 wv[C::CE];
 #pragma unroll
           for (int e = 0; e < C::CE; ++e) {
-            wv[e] = magic_word(x[e], sc[e]);
+            wv[e] = magic_word(xv[t][e], sc[e]);
             if constexpr (sizeof(TX) == 4) acc |= wv[e].y ^ 0x43380000u;
-            else acc |= hi_abs(x[e]) >= lim[e] ? 1u : 0u;
+            else acc |= hi_abs(xv[t][e]) >= lim[e] ? 1u : 0u;
           }
-          // element pair (2 g, 2 g + 1) of the tile's columns -> MN group g (16 bytes), row i
-#pragma unroll
-          for (int e = 0; e < C::CE; e += 2) {
-            const int g = (ch * C::CE + e) >> 1;
-            *reinterpret_cast<uint4*>(bt + (i & 7) * 16 + g * 128 + (i >> 3) * STC_LBO) =
-                make_uint4(wv[e].x, wv[e].y, wv[e + 1].x, wv[e + 1].y);
+          unsigned char* brow = bt + (i & 7) * 16 + (i >> 3) * C::LBO;   // row i, MN group 0
+          if constexpr (sizeof(TX) == 4) {
+            // lo words of columns 4 ch .. + 3 -> MN group ch; their hi halves (digits 4, 5) -> 8 bytes of group
+            // 16 + ch / 2
+            *reinterpret_cast<uint4*>(brow + ch * 128) = make_uint4(wv[0].x, wv[1].x, wv[2].x, wv[3].x);
+            *reinterpret_cast<uint2*>(brow + (16 + (ch >> 1)) * 128 + (ch & 1) * 8) =
+                make_uint2(__byte_perm(wv[0].y, wv[1].y, 0x5410), __byte_perm(wv[2].y, wv[3].y, 0x5410));
+          } else {
+            // element pair (2 ch, 2 ch + 1): the 8 digit bytes of each -> MN group ch
+            *reinterpret_cast<uint4*>(brow + ch * 128) = make_uint4(wv[0].x, wv[0].y, wv[1].x, wv[1].y);
           }
         }
+      } else {
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&rempty[sr]);
       }
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic smem writes -> tensor core
       __syncwarp();
-      if (lane == 0) { tc::mbar_arrive(&dfull[s]); tc::mbar_arrive(&rempty[sr]); }
+      if (lane == 0) tc::mbar_arrive(&dfull[s]);
     }
     bool ovf;
     if constexpr (sizeof(TX) == 4) ovf = (acc >> 16) != 0u;
@@ -323,7 +361,7 @@ sketch_sparse_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int
       const uint64_t gi = (uint64_t)(row_offset + i0 + ii);
       const uint4 w = philox_at(seed, gi, srht ? 0u : (dense ? (uint32_t)tk : 0u),
                                 srht ? kDomainSrhtD : (dense ? kDomainRademacher : kDomainSparse));
-      if (c >= F::DIG) tc::mbar_wait(&dempty[s], (uint32_t)(((c / F::DIG) - 1) & 1));
+      if (c >= F::DIG) tc::mbar_wait(&dempty[(c >> 1) & 1], (uint32_t)(((c >> 2) - 1) & 1));   // slot pair free
       unsigned char* st = dig_base + (size_t)s * C::DIG_STAGE;
       if (dense) {
         // Transpose the warp's 32 X rows x 128 sign bits with ballots: mask (Theta row r) holds bit L =
@@ -432,33 +470,42 @@ sketch_sparse_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int
     if (nstages > 0) {
       tc::mbar_wait(done, 0u);
       asm volatile("tcgen05.fence::after_thread_sync;\n");
-      int32_t bias = 0;                                  // fp32: 2^47 S_r = 128 S_r at weight 256^5
       if constexpr (!F::SIGNED) {
-        uint32_t a[8];
-        tc::ld8(lbase, a);
+        // fp32: F + 2^47 = sum_b lo_b 256^b + hi_0 256^4 + hi_1 256^5; the bias 2^47 S_r = 128 S_r at 256^5
+        uint32_t o[8];
+        tc::ld8(lbase + 384, o);                         // ones block: S_r
         tc::wait_ld();
-        bias = 128 * ((int32_t)a[6] / 0x38);             // column 6: 0x38 S_r exactly
-      }
+        const int32_t bias = 128 * (int32_t)o[0];
 #pragma unroll 1
-      for (int j0 = 0; j0 < STC_N; j0 += 2) {
-        uint32_t a[16];                                  // the 8 byte accumulators of columns j0, j0 + 1
-        tc::ld16(lbase + 8 * j0, a);
-        tc::wait_ld();
+        for (int j0 = 0; j0 < STC_N; j0 += 4) {
+          uint32_t lo[16], hi[8];                        // columns j0 .. j0 + 3
+          tc::ld16(lbase + 4 * j0, lo);
+          tc::ld8(lbase + F::N0 + 2 * j0, hi);
+          tc::wait_ld();
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int j = j0 + u;
-          const uint32_t* b = a + 8 * u;
-          double v;
-          if constexpr (F::SIGNED) {
-            v = (double)(int32_t)b[7];
+          for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u;
+            double v = (double)((int32_t)hi[2 * u + 1] - bias);
+            v = fma(v, 256.0, (double)(int32_t)hi[2 * u]);
 #pragma unroll
-            for (int t = 6; t >= 0; --t) v = fma(v, 256.0, (double)(int32_t)b[t]);
-          } else {
-            v = (double)((int32_t)b[5] - bias);
-#pragma unroll
-            for (int t = 4; t >= 0; --t) v = fma(v, 256.0, (double)(int32_t)b[t]);
+            for (int t = 3; t >= 0; --t) v = fma(v, 256.0, (double)(int32_t)lo[4 * u + t]);
+            if (row < k && j < ncols) Pp[(size_t)row * n + n0 + j] = ldexp(v, col_exp[j] - F::FB);
           }
-          if (row < k && j < ncols) Pp[(size_t)row * n + n0 + j] = ldexp(v, col_exp[j] - F::FB);
+        }
+      } else {
+#pragma unroll 1
+        for (int j0 = 0; j0 < STC_N; j0 += 2) {
+          uint32_t a[16];                                // the 8 digit accumulators of columns j0, j0 + 1
+          tc::ld16(lbase + 8 * j0, a);
+          tc::wait_ld();
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int j = j0 + u;
+            double v = (double)(int32_t)a[8 * u + 7];
+#pragma unroll
+            for (int t = 6; t >= 0; --t) v = fma(v, 256.0, (double)(int32_t)a[8 * u + t]);
+            if (row < k && j < ncols) Pp[(size_t)row * n + n0 + j] = ldexp(v, col_exp[j] - F::FB);
+          }
         }
       }
     } else if (row < k) {
