@@ -134,15 +134,21 @@ solve_tc_prep_kernel(const double* __restrict__ W, int n, int kpad, int8_t* __re
 // whose factor is built from the two exponents by one integer add: Q_ij = RN(T) 2^(e_i + e_j - 52).
 // Round 1 combined the levels in fp64 (four magic-constant conversions, three DFMAs and two DMULs per
 // output); this form needs ~10 integer-pipe instructions, one conversion and one FMUL.
+template <bool K64>
 __device__ __forceinline__ long long qt_combine(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t a4,
                                                 uint32_t a5, uint32_t a6) {
-  long long t = (long long)((int)a6 >> 8);
-  t += (long long)(int)a5;
-  t += (long long)(int)a4 * 256;
-  t += (long long)(int)a3 * 65536;
-  t += (long long)(int)a2 * 16777216;
-  t += (long long)(int)(a0 * 256u + a1) << 32;
-  return t;
+  // adjacent levels pair exactly in int32: |acc_0 256 + acc_1| < 2^28, |acc_2 256 + acc_3| < 2^31 for K <= 128,
+  // and for K <= 64 also |acc_4 256 + acc_5 + (acc_6 >> 8)| < 2^31 (the digit bounds above); then
+  // T = p0 2^32 + p1 2^16 + p2 is one IMAD.WIDE and one add into the high word
+  const int p0 = (int)a0 * 256 + (int)a1;
+  const int p1 = (int)a2 * 256 + (int)a3;
+  long long t;
+  if constexpr (K64) {
+    t = (long long)p1 * 65536 + (long long)((int)a4 * 256 + (int)a5 + ((int)a6 >> 8));
+  } else {
+    t = (long long)p1 * 65536 + (long long)(int)a4 * 256 + (long long)((int)a5 + ((int)a6 >> 8));
+  }
+  return t + ((long long)p0 << 32);
 }
 // fast route (warp-uniform): every 2^(e_i + e_j - 52) of the warp's rows is a normal fp32, built as the bits
 // (e_i + 75) << 23 plus e_j << 23; else this exact fp64 route (any exponent range)
@@ -177,8 +183,10 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
   // row scales: a ring of 4 tiles, so the digit slot can be refilled while the drain of the tile
   // before still reads its scales (a slot is free once the MMAs of tile t complete, and those
   // follow every drain of tile t - 2; see the TMEM buffer waits below)
-  // 16-byte aligned: the drain reads the column exponents cexp with LDS.128
-  int* rexp = reinterpret_cast<int*>((reinterpret_cast<uintptr_t>(tmem_slot + 4) + 15) & ~uintptr_t(15));   // [4][128]
+  // 16-byte aligned (the drain reads the column exponents cexp with LDS.128); offset from sm, so the compiler
+  // keeps these accesses in the shared window (LDS/STS, not generic LD/ST)
+  const size_t rexp_off = ((size_t)(reinterpret_cast<unsigned char*>(tmem_slot + 4) - sm) + 15) & ~(size_t)15;
+  int* rexp = reinterpret_cast<int*>(sm + rexp_off);                          // [4][128]
   int* cexp = rexp + 4 * QT_M;                                                // [KMAX] e_j (W column exponents)
   int* crange = cexp + QT_KMAX_ALL;                                           // [2] min, max e_j
 
@@ -325,14 +333,16 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
               float o[8];
 #pragma unroll
               for (int c = 0; c < 8; ++c) {
-                const long long t = qt_combine(lvl[0][c], lvl[1][c], lvl[2][c], lvl[3][c], lvl[4][c], lvl[5][c], lvl[6][c]);
+                const long long t = qt_combine<KMAX <= 64>(lvl[0][c], lvl[1][c], lvl[2][c], lvl[3][c], lvl[4][c], lvl[5][c], lvl[6][c]);
                 if constexpr (FAST) o[c] = __ll2float_rn(t) * __int_as_float(rbits + (cb[c] << 23));
                 else o[c] = qt_scale_slow(t, ei, cb[c]);
               }
               if (lane == 0) tc::bulk_wait_read0();          // previous chunk's store has read the tile
               __syncwarp();
-              *reinterpret_cast<float4*>(qs + lane * 32) = make_float4(o[0], o[1], o[2], o[3]);
-              *reinterpret_cast<float4*>(qs + lane * 32 + 16) = make_float4(o[4], o[5], o[6], o[7]);
+              // 32-byte rows, TMA SWIZZLE_32B (16-byte chunk c of row r at c ^ ((r >> 2) & 1)): conflict-free STS.128
+              const int sw = (lane >> 2) & 1;
+              *reinterpret_cast<float4*>(qs + lane * 32 + (sw << 4)) = make_float4(o[0], o[1], o[2], o[3]);
+              *reinterpret_cast<float4*>(qs + lane * 32 + ((sw ^ 1) << 4)) = make_float4(o[4], o[5], o[6], o[7]);
               asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
               __syncwarp();
               if (lane == 0) {                               // TMA clips rows >= m and columns >= n
@@ -377,14 +387,16 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
             float o[8];
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
-              const long long t = qt_combine(lvl[0][c], lvl[1][c], lvl[2][c], lvl[3][c], lvl[4][c], lvl[5][c], lvl[6][c]);
+              const long long t = qt_combine<KMAX <= 64>(lvl[0][c], lvl[1][c], lvl[2][c], lvl[3][c], lvl[4][c], lvl[5][c], lvl[6][c]);
               if constexpr (FAST) o[c] = __ll2float_rn(t) * __int_as_float(rbits + (cb[c] << 23));
               else o[c] = qt_scale_slow(t, ei, cb[c]);
             }
 #pragma unroll
             for (int c = 0; c < 8; c += 4) {
               const int ch = h * 2 + (c >> 2);                // 16-byte chunk of the row
-              const int off = DC == 32 ? lane * 128 + ((ch ^ (lane & 7)) << 4) : lane * (DC * 4) + ch * 16;
+              // 128-byte rows (DC = 32): TMA SWIZZLE_128B, chunk ch at ch ^ (r & 7); 64-byte rows (DC = 16): SWIZZLE_64B,
+              // chunk ch at ch ^ ((r >> 1) & 3) -- each 8-lane phase of the STS.128 hits 8 distinct bank groups
+              const int off = DC == 32 ? lane * 128 + ((ch ^ (lane & 7)) << 4) : lane * 64 + ((ch ^ ((lane >> 1) & 3)) << 4);
               *reinterpret_cast<float4*>(qs + off) = make_float4(o[c], o[c + 1], o[c + 2], o[c + 3]);
             }
           }
@@ -424,7 +436,8 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
           const uint32_t ub = __float_as_uint(x[q * 4 + kk]);
-          const uint32_t h = ((uint32_t)((int32_t)ub >> 3) & 0x8FFFFFFFu) | 0x30000000u;   // x 2^-128
+          uint32_t h;                                                                        // x 2^-128: one LOP3
+          asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(h) : "r"((uint32_t)((int32_t)ub >> 3)), "r"(0x8FFFFFFFu), "r"(0x30000000u));
           const double t = fma(__hiloint2double((int)h, (int)(ub << 29)), sx, kMagic + (double)0x8080808080ull);
           hw[kk] = (uint32_t)__double2hiint(t);                                              // F + C, 48 bits
           lw[kk] = (uint32_t)__double2loint(t);
@@ -610,7 +623,8 @@ cudaError_t launch_solve_tc(const double* Winv, int n, const float* X, int64_t m
   const int dcols = QCfg<64>::DCOLS;                 // n <= 64: columns per drain warp
   const cuuint32_t qbox[2] = {half ? 8u : (cuuint32_t)dcols, 32};
   if (enc(&qmapd, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Q, qdims, qstrides, qbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-          (half || dcols != 32) ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+          half ? CU_TENSOR_MAP_SWIZZLE_32B : (dcols == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B),
+          CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   const int64_t ntiles = (m + QT_M - 1) / QT_M;
   const int grid = (int)std::min<int64_t>(ntiles, sms);
