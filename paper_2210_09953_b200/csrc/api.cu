@@ -334,6 +334,15 @@ rcholqr_status read_status(rcholqr_plan p, cudaStream_t st) {
 // ---------------------------------------------------------------------------------------------
 extern "C" {
 
+#ifdef RCHOLQR_ABLATION
+// ablation builds only (not declared in include/rcholqr.h): copy CTA 0's event timeline of the last traced
+// kernel (which = 0: tcgen05 solve, 1: sparse tcgen05 sketch) to the host and clear it
+int32_t rcholqr_trace_read(int32_t which, void* host, size_t bytes) {
+  if (bytes < sizeof(long long) * rcq::kTraceRoles * rcq::kTraceTiles * rcq::kTraceEvents) return -1;
+  return which == 0 ? rcq::trace_read_solve(host) : rcq::trace_read_sketch(host);
+}
+#endif
+
 int32_t rcholqr_version(void) { return RCHOLQR_VERSION; }
 
 const char* rcholqr_strerror(rcholqr_status s) {

@@ -15,6 +15,30 @@ constexpr bool kAblation = true;
 constexpr bool kAblation = false;
 #endif
 
+// Per-role event timeline of CTA 0 (clock64), ablation builds only: trace(role, tile, event) for the first
+// kTraceTiles tiles; read back with rcholqr_trace_read (tools/trace_*.py).  Compiled out of production.
+constexpr int kTraceRoles = 8, kTraceTiles = 64, kTraceEvents = 8;
+#ifdef RCHOLQR_ABLATION
+// one buffer per translation unit (no relocatable device code); each traced TU defines a reader below
+static __device__ long long g_trace[kTraceRoles * kTraceTiles * kTraceEvents];
+#define RCQ_TRACE_READER(name)                                                                                \
+  int name(void* host) {                                                                                        \
+    static long long zero[kTraceRoles * kTraceTiles * kTraceEvents];                                            \
+    if (cudaDeviceSynchronize() != cudaSuccess || cudaMemcpyFromSymbol(host, g_trace, sizeof(zero)) != cudaSuccess) \
+      return -2;                                                                                                \
+    return cudaMemcpyToSymbol(g_trace, zero, sizeof(zero)) == cudaSuccess ? 0 : -3;                             \
+  }
+int trace_read_solve(void* host);
+int trace_read_sketch(void* host);
+#endif
+__device__ __forceinline__ void trace(int role, int tile, int ev) {
+#ifdef RCHOLQR_ABLATION
+  if (blockIdx.x == 0 && tile < kTraceTiles) g_trace[(role * kTraceTiles + tile) * kTraceEvents + ev] = clock64();
+#else
+  (void)role; (void)tile; (void)ev;
+#endif
+}
+
 // Status bits written by kernels into the plan's device status word (0 = OK).
 enum : int { kStNonfinite = 1, kStSingular = 2 };
 // Which kernels served the last call (rcholqr_last_path; the bits are RCHOLQR_PATH_* of rcholqr.h).

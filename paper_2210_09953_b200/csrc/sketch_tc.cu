@@ -572,4 +572,8 @@ bool sparse_tc_aligned(const void* X, int dtype, int64_t m, int64_t ldx) {
   return ((uintptr_t)X % 16) == 0 && ((size_t)ldx * es) % 16 == 0 && m < ((int64_t)1 << 31);
 }
 
+#ifdef RCHOLQR_ABLATION
+RCQ_TRACE_READER(trace_read_sketch)
+#endif
+
 }  // namespace rcq

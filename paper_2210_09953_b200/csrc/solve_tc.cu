@@ -225,12 +225,15 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
     for (int tt = 0; tt < my_tiles; ++tt) {
       // full-tile slot s (n <= 64), or the two K-half slots s, s1 (uses 2 tt and 2 tt + 1 of the ring)
       const int s = Cf::HALF ? (2 * tt) % NSLOT : tt % NSLOT, s1 = (2 * tt + 1) % NSLOT;
+      if (lane == 0) trace(0, tt, 0);
       tc::mbar_wait(&dfull[s], (uint32_t)(((Cf::HALF ? 2 * tt : tt) / NSLOT) & 1));
+      if (lane == 0) trace(0, tt, 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n");
       bool have1 = !Cf::HALF;
       for (int g = 0; g < groups; ++g) {
         const int use = tt * groups + g, buf = use & 1, u = use >> 1;
         if (u > 0) tc::mbar_wait(&tfree[buf], (uint32_t)((u - 1) & 1));
+        if (lane == 0 && g < 2) trace(0, tt, 2 + 2 * g);
         const int ksteps = min(g + 1, kpad / 32);             // W rows l < 32 (g + 1): upper triangular
         if (!have1 && ksteps > 2) {                           // second K-half needed from here on
           tc::mbar_wait(&dfull[s1], (uint32_t)(((2 * tt + 1) / NSLOT) & 1));
@@ -252,7 +255,7 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
             }
           }
         }
-        if (lane == 0) tc::commit(&tready[buf]);
+        if (lane == 0) { tc::commit(&tready[buf]); if (g < 2) trace(0, tt, 3 + 2 * g); }
         __syncwarp();
       }
       if (lane == 0) {                                    // digit slot(s) free once these MMAs complete
@@ -277,8 +280,10 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
         tc::tma_prefetch_2d(&xmap, 0, (int)((blockIdx.x + (int64_t)tp * gridDim.x) * QT_M));
     for (int tt = 0; tt < (Cf::TMA_RAW ? my_tiles : 0); ++tt) {
       const int s = tt % QT_RAW;
+      if (lane == 0) trace(1, tt, 0);
       if (tt >= QT_RAW) tc::mbar_wait(&rempty[s], (uint32_t)(((tt / QT_RAW) - 1) & 1));
       if (lane == 0) {
+        trace(1, tt, 1);
         if (tt + QT_PF < my_tiles)
           tc::tma_prefetch_2d(&xmap, 0, (int)((blockIdx.x + (int64_t)(tt + QT_PF) * gridDim.x) * QT_M));
         const int64_t row0 = (blockIdx.x + (int64_t)tt * gridDim.x) * QT_M;
@@ -300,7 +305,10 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
       for (int g = 0; g < groups; ++g) {
         const int use = tt * groups + g, buf = use & 1, u = use >> 1;
         if (buf != dset) continue;
+        const int trole = (warp == 2 || warp == 6) ? 2 + dset : -1;
+        if (lane == 0 && trole >= 0) trace(trole, tt, 0);
         tc::mbar_wait(&tready[buf], (uint32_t)(u & 1));
+        if (lane == 0 && trole >= 0) trace(trole, tt, 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n");
         // the seven exact int32 levels of an output combine into one int64 (qt_combine); the warp
         // takes the fp32 scaling route unless some 2^(e_i + e_j - 52) of its rows leaves the normal range
@@ -382,7 +390,7 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
             if (h == DC / 8 - 1) {                           // TMEM buffer free; the stores below need no TMEM
               asm volatile("tcgen05.fence::before_thread_sync;\n");
               __syncwarp();
-              if (lane == 0) tc::mbar_arrive(&tfree[buf]);
+              if (lane == 0) { tc::mbar_arrive(&tfree[buf]); if (trole >= 0) trace(trole, tt, 2); }
             }
             float o[8];
 #pragma unroll
@@ -408,6 +416,7 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
         if (lane == 0) {
           tc::tma_store_2d(&qmap, qs, g * QT_G + dc0, (int)((blockIdx.x + (int64_t)tt * gridDim.x) * QT_M + dq * 32));
           tc::bulk_commit();
+          if (trole >= 0) trace(trole, tt, 3);
         }
         }   // TMA_RAW drain
       }
@@ -474,8 +483,11 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
       const int s = tt % QT_DIG, sr = tt % QT_RAW;
       unsigned char* at = abase + (size_t)s * QT_DA * QT_A_TILE;
       if constexpr (Cf::TMA_RAW) {
+        if (dt == 0) trace(4, tt, 0);
         if (tt >= QT_DIG) tc::mbar_wait(&dempty[s], (uint32_t)(((tt / QT_DIG) - 1) & 1));
+        if (dt == 0) trace(4, tt, 1);
         tc::mbar_wait(&rfull[sr], (uint32_t)((tt / QT_RAW) & 1));
+        if (dt == 0) trace(4, tt, 2);
         const float* raw = raw_base + (size_t)sr * QT_M * QT_RS_MAX;
         const int rs = kpad + 4;                                         // raw row pitch
         for (int task = dt; task < ntask; task += 32 * Cf::DW) {
@@ -561,6 +573,7 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
       asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
       __syncwarp();
       if (lane == 0) { tc::mbar_arrive(&dfull[sdone]); if (Cf::TMA_RAW) tc::mbar_arrive(&rempty[sr]); }
+      if (dt == 0) trace(4, tt, 3);
     }
   }
   if (warp >= 2 && warp < 2 + Cf::RW && lane == 0) tc::bulk_wait0();   // Q stores complete before exit
@@ -638,5 +651,9 @@ cudaError_t launch_solve_tc(const double* Winv, int n, const float* X, int64_t m
   return kpad <= 64 ? go(solve_tc_kernel<64>, QCfg<64>::SMEM, QCfg<64>::THREADS)
                     : go(solve_tc_kernel<128>, QCfg<128>::SMEM, QCfg<128>::THREADS);
 }
+
+#ifdef RCHOLQR_ABLATION
+RCQ_TRACE_READER(trace_read_solve)
+#endif
 
 }  // namespace rcq
