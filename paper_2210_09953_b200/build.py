@@ -45,9 +45,14 @@ def _lib(ablation: bool) -> str:
     return LIB.replace("librcholqr.so", "librcholqr_ablation.so") if ablation else LIB
 
 
+def _ablation_flags() -> list:
+    # kernel experiments (tools/ only): extra -D switches for the ablation library, never for the product build
+    return ["-DRCHOLQR_ABLATION"] + os.environ.get("RCHOLQR_EXTRA_NVCC_FLAGS", "").split()
+
+
 def source_hash(ablation: bool = False) -> str:
     h = hashlib.sha256()
-    h.update(" ".join(FLAGS + (["-DRCHOLQR_ABLATION"] if ablation else [])).encode())
+    h.update(" ".join(FLAGS + (_ablation_flags() if ablation else [])).encode())
     for f in SRCS + HDRS:
         h.update(os.path.basename(f).encode())
         with open(f, "rb") as fh:
@@ -81,7 +86,7 @@ def build(force: bool = False, verbose: bool = False, ablation: bool = False) ->
     try:
         def obj(src):
             o = os.path.join(tmpdir, os.path.basename(src) + ".o")
-            subprocess.check_call([nvcc, *FLAGS, *extra, *(["-DRCHOLQR_ABLATION"] if ablation else []), *inc, "-c", "-o", o, src])
+            subprocess.check_call([nvcc, *FLAGS, *extra, *(_ablation_flags() if ablation else []), *inc, "-c", "-o", o, src])
             return o
         with cf.ThreadPoolExecutor(max_workers=min(len(SRCS), os.cpu_count() or 4)) as ex:
             objs = list(ex.map(obj, SRCS))

@@ -22,12 +22,11 @@
 // W = R^{-1} is upper triangular, so column group g only needs rows l < 32 (g + 1): its digit
 // tile and its MMAs stop there (K_g = 32 (g + 1)).
 //
-// Roles (persistent CTAs; 26 warps for n <= 64, 18 above): warp 0 lane 0 issues tcgen05.mma; warp 1
+// Roles (persistent CTAs; 20 warps for n <= 64, 18 above): warp 0 lane 0 issues tcgen05.mma; warp 1
 // lane 0 stages the W digits (cp.async.bulk) and, for n <= 64, the X tiles (one 2D TMA box of 128
-// rows x K+4 columns per tile, two-stage ring); the next RW warps drain TMEM -- two sets (set d
-// drains level buffer d, one lane quadrant per warp), and for n <= 64 each set twice over (16 columns
-// per warp: the drain is bound by TMEM read concurrency, C4 solve 11.05 -> 10.02 ms) -- and write Q
-// through shared memory with TMA stores; the last 8 warps split X into digit planes (for 64 < n <= 128 they read X with plain loads into registers
+// rows x K+4 columns per tile, two-stage ring); the next RW = 8 warps drain TMEM -- two sets (set d
+// drains level buffer d, one lane quadrant per warp, 32 columns) -- and write Q
+// through shared memory with TMA stores; the last warps (10 for n <= 64, 8 above) split X into digit planes (for 64 < n <= 128 they read X with plain loads into registers
 // and write the digits as two K-halves into a ring of three half slots: there is no room for a raw
 // ring or a second full digit stage).
 #include <cuda_runtime.h>
@@ -57,6 +56,12 @@ static_assert(2 * QT_LEV * QT_G <= 512, "two TMEM level buffers");
 // byte offset of column group g's W digit tile (triangular: K_h = 32 (h + 1) rows of W per group)
 __host__ __device__ constexpr int qt_woff(int g) { return QT_NB * 32 * g * (g + 1) / 2; }
 
+#ifndef RCQ_SOLVE_RW
+#define RCQ_SOLVE_RW 8
+#endif
+#ifndef RCQ_SOLVE_DW
+#define RCQ_SOLVE_DW 10
+#endif
 template <int KMAX>
 struct QCfg {
   static constexpr bool TMA_RAW = KMAX <= 64;     // raw X ring via TMA (else plain loads)
@@ -73,12 +78,13 @@ struct QCfg {
   static constexpr int NSLOT = HALF ? 3 : DIG;
   static constexpr int H_TILE = QT_M * 64;        // one digit plane of one K-half
   static constexpr int SLOT_BYTES = HALF ? QT_DA * H_TILE : QT_DA * A_TILE;
-  // n <= 64: 16 drain warps (two per lane quadrant per TMEM buffer, 16 columns each) -- the drain
-  // is bound by TMEM read concurrency; 64 < n <= 128: 8 (registers: the K-half producers need 96)
-  static constexpr int RW = TMA_RAW ? 16 : QT_RWARPS;
-  // digit warps: 6 for the TMA ring (a strided task loop; fewer warps leave the drain more registers),
-  // 8 for the K-half producers (their row mapping assumes 8)
-  static constexpr int DW = TMA_RAW ? 6 : QT_DWARPS;
+  // n <= 64: 8 drain warps (one per lane quadrant per TMEM buffer, 32 columns each) and 10 digit warps.
+  // Measured splits (C4, ms): 16 drain / 6 digit 8.5 (spills at 80 registers), 8 / 6 8.1, 8 / 14 8.1
+  // (spills), 8 / 10 7.6 (96 registers, no spill): the digit production is the critical path
+  // (tools/trace_solve.py: ~3.2 K of a ~3.7 K-cycle tile), not the TMEM read concurrency.
+  // 64 < n <= 128: 8 drain warps and 8 K-half digit producers (their row mapping assumes 8)
+  static constexpr int RW = TMA_RAW ? RCQ_SOLVE_RW : QT_RWARPS;
+  static constexpr int DW = TMA_RAW ? RCQ_SOLVE_DW : QT_DWARPS;
   static constexpr int THREADS = 32 * (2 + RW + DW);
   static constexpr int DCOLS = QT_G * 8 / RW;     // columns of a group per drain warp (16 or 32)
   static constexpr int QS = HALF ? QT_RWARPS * 32 * 8 * 4 : RW * 32 * DCOLS * 4;   // HALF: 32 x 8 tile per drain warp
@@ -409,11 +415,14 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
             }
           }
         };
-        if (fast) drain(std::true_type{});
+        if (dbg & 4) {                                     // ablation: no TMEM loads, combine or Q stores
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&tfree[buf]);
+        } else if (fast) drain(std::true_type{});
         else drain(std::false_type{});
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncwarp();
-        if (lane == 0) {
+        if (lane == 0 && !(dbg & 4)) {
           tc::tma_store_2d(&qmap, qs, g * QT_G + dc0, (int)((blockIdx.x + (int64_t)tt * gridDim.x) * QT_M + dq * 32));
           tc::bulk_commit();
           if (trole >= 0) trace(trole, tt, 3);
