@@ -243,6 +243,8 @@ rcholqr_status rcholqr_last_timings(rcholqr_plan plan, float out_ms[6]);
  *                    CUDA-core kernel recomputed the partials (PAPER.md:423's u_f is kept either way)
  *   SOLVE_TC         the tall solve ran on tcgen05 (fp32 X, n <= 128; solve_tc.cu)
  *   SOLVE_DMMA       the tall solve ran on a blocked fp64 DMMA substitution kernel
+ *   COLSQ_FUSED      (rcholqr_factor_rr / _rr2) D = diag ||X(:,j)|| came out of the sketch's own pass over X
+ *                    (the pre-split Gaussian digit split), no separate column-norm pass
  * *out receives the bits.  SYNCHRONIZES on `stream` (reads the device overflow word).  Errors:
  * E_INVALID for a NULL plan or out. */
 #define RCHOLQR_PATH_SKETCH_TC 1u
@@ -251,6 +253,7 @@ rcholqr_status rcholqr_last_timings(rcholqr_plan plan, float out_ms[6]);
 #define RCHOLQR_PATH_SKETCH_FALLBACK 8u
 #define RCHOLQR_PATH_SOLVE_TC 16u
 #define RCHOLQR_PATH_SOLVE_DMMA 32u
+#define RCHOLQR_PATH_COLSQ_FUSED 64u
 rcholqr_status rcholqr_last_path(rcholqr_plan plan, uint32_t* out, void* stream);
 
 #ifdef __cplusplus

@@ -109,7 +109,7 @@ struct rcholqr_plan_s {
   double* rr_buf = nullptr; double* rr_Pn = nullptr; double* rr_A = nullptr; double* rr_Pg = nullptr;
   uint64_t* srht_d = nullptr;   // SRHT: the k sampled Hadamard rows
   double* rr_R = nullptr; double* rr_W = nullptr; double* rr_R11 = nullptr; double* rr_d = nullptr;
-  double* rr_cpart = nullptr; double* rr_sd = nullptr; int* rr_si = nullptr; int* rr_perm = nullptr;
+  double* rr_cpart = nullptr; double* rr_cspart = nullptr; double* rr_sd = nullptr; int* rr_si = nullptr; int* rr_perm = nullptr;
   int* rr_qst = nullptr; int rr_splits = 0;
   void* rr_xr = nullptr; size_t rr_xr_bytes = 0;
   size_t xdig_bytes = 0;
@@ -214,7 +214,9 @@ rcholqr_status check_factor_args(rcholqr_plan p, const void* X, int64_t m, int64
 // all-reduce (allreduce = false) to sum [P; Y] at once.
 rcholqr_status do_sketch(rcholqr_plan p, const void* X, int64_t m, int64_t ro, int64_t ldx, double* P,
                          cudaStream_t st, const SketchLaunch* Lp = nullptr, int k = 0, double* part = nullptr,
-                         double* partc = nullptr, int k_first = 0, bool allreduce = true) {
+                         double* partc = nullptr, int k_first = 0, bool allreduce = true, double* cs_part = nullptr,
+                         double* cs_out = nullptr, bool* cs_done = nullptr) {
+  if (cs_done) *cs_done = false;
   const auto& d = p->d;
   const SketchLaunch& L = Lp ? *Lp : p->sk;
   if (!Lp) { k = d.k; part = p->part; partc = p->partc; }
@@ -231,7 +233,8 @@ rcholqr_status do_sketch(rcholqr_plan p, const void* X, int64_t m, int64_t ro, i
       }
     }
     CU(launch_sketch(L, X, d.dtype, m, d.n, ldx, ro, k, d.nnz_per_col, d.seed, part, partc, P, p->status_d, p->flag_d,
-                     p->xdig, p->xdig_bytes, st, timed ? p->ev[1] : nullptr, k_first, &p->path, p->flag_seen_d));
+                     p->xdig, p->xdig_bytes, st, timed ? p->ev[1] : nullptr, k_first, &p->path, p->flag_seen_d,
+                     cs_part, cs_out, cs_done));
   } else {
     if (timed) { cudaEventRecord(p->ev[0], st); cudaEventRecord(p->ev[1], st); }
     CU(cudaMemsetAsync(P, 0, sizeof(double) * (size_t)k * d.n, st));
@@ -427,7 +430,7 @@ rcholqr_status rcholqr_destroy(rcholqr_plan p) {
   cudaFree(p->gpart); cudaFree(p->gA); cudaFree(p->gW); cudaFree(p->gRp); cudaFree(p->gR1); cudaFree(p->q1buf);
   cudaFree(p->red_part); cudaFree(p->red_partc); cudaFree(p->red_P);
   cudaFree(p->rr_buf); cudaFree(p->rr_Pn); cudaFree(p->rr_A); cudaFree(p->rr_Pg); cudaFree(p->rr_R); cudaFree(p->rr_W);
-  cudaFree(p->rr_R11); cudaFree(p->rr_d); cudaFree(p->rr_cpart); cudaFree(p->rr_sd); cudaFree(p->rr_si);
+  cudaFree(p->rr_R11); cudaFree(p->rr_d); cudaFree(p->rr_cpart); cudaFree(p->rr_cspart); cudaFree(p->rr_sd); cudaFree(p->rr_si);
   cudaFree(p->rr_perm); cudaFree(p->rr_qst); cudaFree(p->rr_xr); cudaFree(p->srht_d);
   if (p->status_h) cudaFreeHost(p->status_h);
   cudaFree(p->xbuf); cudaFree(p->qbuf); cudaFree(p->rbuf); cudaFree(p->sbuf); cudaFree(p->tbuf);
@@ -609,6 +612,7 @@ rcholqr_status rcholqr_factor_rr(rcholqr_plan p, const void* X, int64_t m, int64
               cudaMalloc(&p->rr_R11, sizeof(double) * nn) == cudaSuccess &&
               cudaMalloc(&p->rr_d, sizeof(double) * n) == cudaSuccess &&
               cudaMalloc(&p->rr_cpart, sizeof(double) * n * p->rr_splits) == cudaSuccess &&
+              cudaMalloc(&p->rr_cspart, sizeof(double) * n * kXdigSplitBlocks) == cudaSuccess &&
               cudaMalloc(&p->rr_sd, sizeof(double) * 2) == cudaSuccess &&
               cudaMalloc(&p->rr_si, sizeof(int) * 2) == cudaSuccess &&
               cudaMalloc(&p->rr_perm, sizeof(int) * n) == cudaSuccess &&
@@ -623,10 +627,15 @@ rcholqr_status rcholqr_factor_rr(rcholqr_plan p, const void* X, int64_t m, int64
   // library events: sketch | column norms | all-reduce | RRQR (incl. host decisions) | gather | solve
   if (t) cudaEventRecord(p->ev[0], st);
   // 1. P = Theta X and the column sums of squares, all-reduced together as [P; colsq]
-  rcholqr_status s = do_sketch(p, X, m, ro, ldx, p->rr_buf, st, nullptr, 0, nullptr, nullptr, 0, false);
+  //    (D "along with P <- Theta X in step 1 during the same pass": the pre-split Gaussian path sums
+  //    the squares in its digit-split kernel; the other sketch paths fall back to one colsq pass over X)
+  bool cs_fused = false;
+  rcholqr_status s = do_sketch(p, X, m, ro, ldx, p->rr_buf, st, nullptr, 0, nullptr, nullptr, 0, false, p->rr_cspart,
+                               p->rr_buf + kn, &cs_fused);
   if (s != RCHOLQR_OK) return s;
   if (t) cudaEventRecord(p->ev[1], st);
-  if (m > 0) CU(launch_colsq(X, p->d.dtype, m, n, ldx, p->rr_splits, p->rr_cpart, p->rr_buf + kn, p->status_d, st));
+  if (cs_fused) p->path |= RCHOLQR_PATH_COLSQ_FUSED;
+  else if (m > 0) CU(launch_colsq(X, p->d.dtype, m, n, ldx, p->rr_splits, p->rr_cpart, p->rr_buf + kn, p->status_d, st));
   else CU(cudaMemsetAsync(p->rr_buf + kn, 0, sizeof(double) * n, st));
   if (t) cudaEventRecord(p->ev[2], st);
   if (p->d.nccl_comm) {
@@ -671,10 +680,10 @@ rcholqr_status rcholqr_factor_rr(rcholqr_plan p, const void* X, int64_t m, int64
   CU(cudaMemcpyAsync(perm, p->rr_perm, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
   if (D) CU(cudaMemcpyAsync(D, p->rr_d, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   if (S) CU(launch_form_s(p->Awork, p->tau, p->diag, k, n, S, p->rr_qst, st));
-  if (r == 0) {
+  if (r == 0) {   // rank 0: E_SINGULAR, unless the sketch (or D) was non-finite -- then that is the diagnosis
     CU(cudaMemsetAsync(R, 0, sizeof(double) * nn, st));
-    CU(cudaStreamSynchronize(st));
-    return RCHOLQR_E_SINGULAR;
+    const rcholqr_status s0 = read_status(p, st);
+    return s0 == RCHOLQR_E_NONFINITE ? s0 : RCHOLQR_E_SINGULAR;
   }
   // R <- R(1:r, :) Pi^T D Pi;  4. Q = (X Pi(:, 1:r)) R11^{-1}
   CU(launch_rr_finalize(p->rr_R, n, r, p->rr_d, p->rr_perm, R, p->rr_R11, st));

@@ -94,9 +94,13 @@ cudaError_t launch_gauss_tc(const void* X, int dtype, int64_t m, int n, int64_t 
 // pre-split variant: X digit planes written once to a workspace of gauss_tcp_workspace() bytes
 size_t gauss_tcp_workspace(int64_t m, int n, int dtype, int splits);
 size_t gauss_tcp_chunk_workspace(int64_t m, int n, int dtype, int splits);   // capped at kXdigCapBytes
+// cs_part (optional, kXdigSplitBlocks x n doubles): per-CTA column sums of squares of X from the
+// digit-split pass (Alg. 7's D), reduced by the caller with launch_reduce(.., kXdigSplitBlocks, ..)
+constexpr int kXdigSplitBlocks = 148 * 8;
+cudaError_t launch_colsum_reduce(const double* part, int n, double* out, int* status, cudaStream_t st);
 cudaError_t launch_gauss_tcp(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                              uint64_t seed, int tiles_k, int tiles_n, int splits, double* part, double* partc,
-                             int* overflow, void* ws, size_t ws_bytes, cudaStream_t st);
+                             int* overflow, void* ws, size_t ws_bytes, cudaStream_t st, double* cs_part = nullptr);
 constexpr size_t kXdigCapBytes = (size_t)4 << 30;   // largest pre-split digit workspace a plan allocates
 struct TrsmLaunch {
   int kind;
@@ -109,7 +113,8 @@ SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms,
 cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
                           int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* partc, double* P,
                           int* status, int* flag, void* xdig, size_t xdig_bytes, cudaStream_t st, cudaEvent_t ev_mid,
-                          int k_first = 0, unsigned* path = nullptr, int* flag_seen = nullptr);
+                          int k_first = 0, unsigned* path = nullptr, int* flag_seen = nullptr,
+                          double* cs_part = nullptr, double* cs_out = nullptr, bool* cs_done = nullptr);
 TrsmLaunch plan_trsm(int n, int dtype, size_t smem_optin);
 cudaError_t launch_tri_inverse(const double* R, int n, double* W, int* status, cudaStream_t st);
 cudaError_t launch_trsm(const TrsmLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,

@@ -682,7 +682,8 @@ static cudaError_t launch_gauss_typed(const SketchLaunch& L, const void* X, int6
 cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
                           int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* partc, double* P,
                           int* status, int* flag, void* xdig, size_t xdig_bytes, cudaStream_t st, cudaEvent_t ev_mid,
-                          int k_first, unsigned* path, int* flag_seen) {
+                          int k_first, unsigned* path, int* flag_seen, double* cs_part, double* cs_out, bool* cs_done) {
+  if (cs_done) *cs_done = false;
   cudaError_t e;
   unsigned pb = 0;
   const int64_t per = (m + L.splits - 1) / L.splits;
@@ -762,8 +763,15 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
       e = cudaErrorNotSupported;
       if (xdig && !getenv("RCHOLQR_GAUSS_NO_PRESPLIT")) {   // pre-split digits (row chunks that fit the workspace)
         e = launch_gauss_tcp(X, dtype, m, n, ldx, row_offset, k, seed, L.tc_tiles_k, L.tc_tiles_n, splits, part,
-                             partc, flag, xdig, xdig_bytes, st);
-        if (e == cudaSuccess) pb |= kPathSketchPresplit;
+                             partc, flag, xdig, xdig_bytes, st, cs_out ? cs_part : nullptr);
+        if (e == cudaSuccess) {
+          pb |= kPathSketchPresplit;
+          if (cs_out) {                                    // D of Alg. 7 came with this pass
+            e = launch_colsum_reduce(cs_part, n, cs_out, status, st);
+            if (e != cudaSuccess) return e;
+            if (cs_done) *cs_done = true;
+          }
+        }
       }
       if (e == cudaErrorNotSupported)
         e = launch_gauss_tc(X, dtype, m, n, ldx, row_offset, k, seed, L.tc_tiles_k, L.tc_tiles_n, splits, trps, part,

@@ -481,12 +481,16 @@ template <typename TX>
 __global__ void __launch_bounds__(256)
 xdig_split_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64_t rows_per_split, int stages,
                   int tiles_n, int64_t units, const uint32_t* __restrict__ maxbits, unsigned char* __restrict__ dig,
-                  int* overflow) {
+                  int* overflow, double* __restrict__ cs_part) {
   constexpr int DX = GtFmt<TX>::DX;
   const int j = threadIdx.x & (GT_M - 1), kg = threadIdx.x >> 7;
   const int npad = tiles_n * GT_M;
   uint32_t amax = 0u;
   bool bad = false;
+  // cs_part != null (Alg. 7, "computing this matrix along with P <- Theta X in step 1 during the
+  // same pass"): the column sums of squares of X in the pass that already reads every element.  gridDim.x is a
+  // multiple of tiles_n, so a block's column tile tn = blockIdx.x % tiles_n is fixed.
+  double cs = 0.0;
   for (int64_t u = blockIdx.x; u < units; u += gridDim.x) {
     const int tn = (int)(u % tiles_n);
     const int64_t st_g = u / tiles_n;
@@ -504,6 +508,7 @@ xdig_split_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64
         const int64_t i = i0 + kg * 16 + qq * 4 + kk;
         const TX x = (col < n && i < i_end) ? X[i * ldx + col] : (TX)0;
         if (col < n) { amax = max(amax, gt_habs(x) >= cp.lim ? 0xFFFFFFFFu : 0u); bad |= cp.bad; }
+        if (cs_part) cs = fma((double)x, (double)x, cs);
         gt_split(x, cp.s, hw[kk], lw[kk]);
       }
       uint32_t W[DX];
@@ -517,6 +522,13 @@ xdig_split_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64
       *reinterpret_cast<uint4*>(blk + b * 4096 + cm_off(j, kg * 16, GT_M)) = make_uint4(Wd[b][0], Wd[b][1], Wd[b][2], Wd[b][3]);
   }
   if (amax || bad) atomicOr(overflow, 1);
+  if (cs_part) {                                       // the two row halves of each column, fixed order
+    __shared__ double csh[GT_M];
+    if (kg == 1) csh[j] = cs;
+    __syncthreads();
+    const int col = (int)(blockIdx.x % tiles_n) * GT_M + j;
+    if (kg == 0 && col < n) cs_part[(size_t)blockIdx.x * n + col] += cs + csh[j];
+  }
 }
 
 template <typename TX>
@@ -736,18 +748,43 @@ size_t gauss_tcp_workspace(int64_t m, int n, int dtype, int splits) {
   return (size_t)splits * stages * tiles_n * dx * 4096 + (size_t)splits * tiles_n * GT_M * 4;
 }
 
+// column j of out = sum over the kXdigSplitBlocks partial rows: one warp per column, lanes take rows lane, lane + 32,
+// ... in order, then a fixed shuffle tree (deterministic; the 1184-long column sums of a 256-thread reduce were
+// ~0.1 ms of serial adds)
+__global__ void __launch_bounds__(32) colsum_reduce_kernel(const double* __restrict__ part, int rows, int n,
+                                                             double* __restrict__ out, int* status) {
+  const int j = blockIdx.x, lane = threadIdx.x;
+  double s = 0.0;
+  for (int r = lane; r < rows; r += 32) s += part[(size_t)r * n + j];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) {
+    out[j] = s;
+    if (!isfinite(s)) atomicOr(status, kStNonfinite);
+  }
+}
+cudaError_t launch_colsum_reduce(const double* part, int n, double* out, int* status, cudaStream_t st) {
+  colsum_reduce_kernel<<<n, 32, 0, st>>>(part, kXdigSplitBlocks, n, out, status);
+  return cudaGetLastError();
+}
+
+// split grid: at most kXdigSplitBlocks CTAs, a multiple of tiles_n (each CTA keeps one column tile)
+static int xdig_split_grid(int64_t units, int tiles_n) {
+  const int64_t g = std::min<int64_t>(units, kXdigSplitBlocks);
+  return (int)std::max<int64_t>(tiles_n, g / tiles_n * tiles_n);
+}
+
 template <typename TX>
 static cudaError_t launch_gtcp(const TX* X, int64_t m, int n, int64_t ldx, int64_t ro, int k, uint64_t seed,
                                int tiles_k, int tiles_n, int splits, int64_t rps, double* part, double* partc,
-                               int* overflow, void* ws, int accumulate, cudaStream_t st) {
+                               int* overflow, void* ws, int accumulate, double* cs_part, cudaStream_t st) {
   constexpr int DX = GtFmt<TX>::DX;
   const int stages = (int)(rps / GT_KC);
   const int64_t units = (int64_t)splits * stages * tiles_n;
   unsigned char* dig = reinterpret_cast<unsigned char*>(ws);
   uint32_t* maxbits = reinterpret_cast<uint32_t*>(dig + (size_t)units * DX * 4096);
   xdig_maxbits_kernel<TX><<<splits, 256, 0, st>>>(X, m, n, ldx, rps, tiles_n * GT_M, maxbits);
-  xdig_split_kernel<TX><<<(int)std::min<int64_t>(units, 148 * 8), 256, 0, st>>>(X, m, n, ldx, rps, stages, tiles_n,
-                                                                                 units, maxbits, dig, overflow);
+  xdig_split_kernel<TX><<<xdig_split_grid(units, tiles_n), 256, 0, st>>>(X, m, n, ldx, rps, stages, tiles_n, units,
+                                                                          maxbits, dig, overflow, cs_part);
   auto kern = sketch_gauss_tcp_kernel<TX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GpCfg<TX>::SMEM);
   if (e != cudaSuccess) return e;
@@ -762,11 +799,15 @@ static cudaError_t launch_gtcp(const TX* X, int64_t m, int n, int64_t ldx, int64
 // into the per-split partials (TwoSum), so the result is the sketch of all m rows.
 cudaError_t launch_gauss_tcp(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                              uint64_t seed, int tiles_k, int tiles_n, int splits, double* part, double* partc,
-                             int* overflow, void* ws, size_t ws_bytes, cudaStream_t st) {
+                             int* overflow, void* ws, size_t ws_bytes, cudaStream_t st, double* cs_part) {
   const size_t es = dtype == RCHOLQR_F64 ? 8 : 4;
   int64_t chunk = m;
   while (chunk > GT_KC && gauss_tcp_workspace(chunk, n, dtype, splits) > ws_bytes) chunk = (chunk + 1) / 2;
   if (gauss_tcp_workspace(chunk, n, dtype, splits) > ws_bytes) return cudaErrorNotSupported;
+  if (cs_part) {                                       // every chunk's split kernel adds into these partials
+    cudaError_t e = cudaMemsetAsync(cs_part, 0, sizeof(double) * kXdigSplitBlocks * n, st);
+    if (e != cudaSuccess) return e;
+  }
   for (int64_t c0 = 0; c0 < m; c0 += chunk) {
     const int64_t mc = std::min(chunk, m - c0);
     const int64_t per = (mc + splits - 1) / splits;
@@ -774,9 +815,9 @@ cudaError_t launch_gauss_tcp(const void* X, int dtype, int64_t m, int n, int64_t
     const char* Xc = reinterpret_cast<const char*>(X) + (size_t)c0 * ldx * es;
     cudaError_t e = dtype == RCHOLQR_F64
                         ? launch_gtcp((const double*)Xc, mc, n, ldx, row_offset + c0, k, seed, tiles_k, tiles_n, splits,
-                                      rps, part, partc, overflow, ws, c0 > 0, st)
+                                      rps, part, partc, overflow, ws, c0 > 0, cs_part, st)
                         : launch_gtcp((const float*)Xc, mc, n, ldx, row_offset + c0, k, seed, tiles_k, tiles_n, splits,
-                                      rps, part, partc, overflow, ws, c0 > 0, st);
+                                      rps, part, partc, overflow, ws, c0 > 0, cs_part, st);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
