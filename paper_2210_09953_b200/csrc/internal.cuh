@@ -64,7 +64,7 @@ bool sparse_tc_applicable(int k, int n, int zeta);
 bool sparse_tc_aligned(const void* X, int dtype, int64_t m, int64_t ldx);
 cudaError_t launch_sparse_tc(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                              int zeta, uint64_t seed, int splits, int64_t rows_per_split, double* part, int* overflow,
-                             cudaStream_t st, const uint64_t* srht_s = nullptr);
+                             cudaStream_t st, const uint64_t* srht_s = nullptr, double* cs_part = nullptr);
 enum TrsmKind : int { kTrsm64x24 = 0, kTrsm128x64 = 1, kTrsm128x112 = 2, kTrsm128x128 = 3 };
 enum QrKind : int { kQrSmem = 0, kQrGlobal = 1, kQrBlocked = 2 };
 
@@ -97,7 +97,7 @@ size_t gauss_tcp_chunk_workspace(int64_t m, int n, int dtype, int splits);   // 
 // cs_part (optional, kXdigSplitBlocks x n doubles): per-CTA column sums of squares of X from the
 // digit-split pass (Alg. 7's D), reduced by the caller with launch_reduce(.., kXdigSplitBlocks, ..)
 constexpr int kXdigSplitBlocks = 148 * 8;
-cudaError_t launch_colsum_reduce(const double* part, int n, double* out, int* status, cudaStream_t st);
+cudaError_t launch_colsum_reduce(const double* part, int rows, int n, double* out, int* status, cudaStream_t st);
 cudaError_t launch_gauss_tcp(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                              uint64_t seed, int tiles_k, int tiles_n, int splits, double* part, double* partc,
                              int* overflow, void* ws, size_t ws_bytes, cudaStream_t st, double* cs_part = nullptr);

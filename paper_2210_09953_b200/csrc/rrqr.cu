@@ -3,7 +3,7 @@
 // to the sketch of Alg. 2's kernels) and the gather of the r selected columns for step 4's solve.
 // Everything between is the small k x n / n x n work of steps 2-3 ("negligible"),
 // run by single-CTA kernels in fp64:
-//   colsq_kernel         per-split column sums of squares (reduced by sketch_reduce_kernel)
+//   colsq_kernel         per-split column sums of squares (only when the sketch pass could not carry D)
 //   rr_normalize_kernel  d_j = sqrt(sum), P <- P D^{-1} (zero columns stay zero)
 //   qrcp_kernel          Businger-Golub column pivoting: the permutation only (norms recomputed)
 //   rr_gather_kernel     P(:, perm) for the unpivoted Householder of qr.cu / qr_blocked.cu

@@ -699,9 +699,16 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
     if (L.sp_tc && rps <= kSparseTcMaxRows && sparse_tc_aligned(X, dtype, m, ldx)) {
       e = cudaMemsetAsync(flag, 0, sizeof(int), st);
       if (e != cudaSuccess) return e;
-      e = launch_sparse_tc(X, dtype, m, n, ldx, row_offset, k, zeta, seed, L.splits, rps, part, flag, st);
-      if (e == cudaSuccess) { guard = flag; pb |= kPathSketchTC; }
-      else if (e != cudaErrorNotSupported) return e;
+      e = launch_sparse_tc(X, dtype, m, n, ldx, row_offset, k, zeta, seed, L.splits, rps, part, flag, st, nullptr,
+                           cs_out ? cs_part : nullptr);
+      if (e == cudaSuccess) {
+        guard = flag; pb |= kPathSketchTC;
+        if (cs_out) {                                      // D of Alg. 7 came with this pass
+          e = launch_colsum_reduce(cs_part, L.splits, n, cs_out, status, st);
+          if (e != cudaSuccess) return e;
+          if (cs_done) *cs_done = true;
+        }
+      } else if (e != cudaErrorNotSupported) return e;
     }
     if (!guard) pb |= kPathSketchCudaCore;
     auto launch = [&](auto* tag) -> cudaError_t {
@@ -767,7 +774,7 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
         if (e == cudaSuccess) {
           pb |= kPathSketchPresplit;
           if (cs_out) {                                    // D of Alg. 7 came with this pass
-            e = launch_colsum_reduce(cs_part, n, cs_out, status, st);
+            e = launch_colsum_reduce(cs_part, kXdigSplitBlocks, n, cs_out, status, st);
             if (e != cudaSuccess) return e;
             if (cs_done) *cs_done = true;
           }

@@ -762,8 +762,8 @@ __global__ void __launch_bounds__(32) colsum_reduce_kernel(const double* __restr
     if (!isfinite(s)) atomicOr(status, kStNonfinite);
   }
 }
-cudaError_t launch_colsum_reduce(const double* part, int n, double* out, int* status, cudaStream_t st) {
-  colsum_reduce_kernel<<<n, 32, 0, st>>>(part, kXdigSplitBlocks, n, out, status);
+cudaError_t launch_colsum_reduce(const double* part, int rows, int n, double* out, int* status, cudaStream_t st) {
+  colsum_reduce_kernel<<<n, 32, 0, st>>>(part, rows, n, out, status);
   return cudaGetLastError();
 }
 

@@ -151,7 +151,8 @@ template <typename TX>
 __global__ void __launch_bounds__(STC_THREADS, 1)
 sketch_sparse_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int n, int64_t row_offset, int k,
                         int zeta, uint64_t seed, int tiles_k, int tiles_n, int64_t rows_per_split,
-                        double* __restrict__ part, int* overflow, int dbg_in, const uint64_t* __restrict__ srht_s) {
+                        double* __restrict__ part, int* overflow, int dbg_in, const uint64_t* __restrict__ srht_s,
+                        double* __restrict__ cs_part) {
   const int dbg = kAblation ? dbg_in : 0;   // ablation switches (see internal.cuh)
   using C = StcCfg<TX>;
   using F = Fmt<TX>;
@@ -275,6 +276,10 @@ sketch_sparse_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int
       if (dgrp == 0 && dt < STC_N) col_exp[dt] = col_param<TX>(col_max[dt]).e;
     }
     uint32_t acc = 0u;                                   // overflow detection
+    // cs_part != null (Alg. 7): column sums of squares of X in this same pass over X
+    double cs[C::CE];
+#pragma unroll
+    for (int e = 0; e < C::CE; ++e) cs[e] = 0.0;
     for (int c = dgrp; c < nstages; c += STC_DGROUPS) {
       const int s = c % F::DIG, sr = c % F::RAW;
       const int64_t i0 = i_begin + (int64_t)c * STC_KC;
@@ -314,6 +319,7 @@ sketch_sparse_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int
           uint2 wv[C::CE];
 #pragma unroll
           for (int e = 0; e < C::CE; ++e) {
+            if (cs_part) cs[e] = fma((double)xv[t][e], (double)xv[t][e], cs[e]);
             wv[e] = magic_word(xv[t][e], sc[e]);
             if constexpr (sizeof(TX) == 4) acc |= wv[e].y ^ 0x43380000u;
             else acc |= hi_abs(xv[t][e]) >= lim[e] ? 1u : 0u;
@@ -342,6 +348,25 @@ sketch_sparse_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int
     if constexpr (sizeof(TX) == 4) ovf = (acc >> 16) != 0u;
     else ovf = acc != 0u;
     if (nstages > 0 && (ovf || bad)) atomicOr(overflow, 1);        // headroom exceeded / Inf / NaN
+    if (cs_part) {
+      // per-thread sums -> per-CTA column sums in a fixed order (thread index), through the raw ring (all B
+      // warps are past their last raw read once the named barrier below completes)
+      constexpr int NB = 32 * STC_DGROUPS * STC_DWARPS;
+      const int bt = tid - 64;
+      tc::named_bar(1, NB);
+      double* scr = reinterpret_cast<double*>(raw_base);              // [NB][CE]
+      int* sch = reinterpret_cast<int*>(scr + NB * C::CE);             // [NB] chunk of each thread
+#pragma unroll
+      for (int e = 0; e < C::CE; ++e) scr[bt * C::CE + e] = cs[e];
+      sch[bt] = ch;
+      tc::named_bar(1, NB);
+      if (bt < STC_N && tk == 0 && n0 + bt < n) {
+        double sum = 0.0;
+        for (int t2 = 0; t2 < NB; ++t2)
+          if (sch[t2] == bt / C::CE) sum += scr[t2 * C::CE + bt % C::CE];
+        cs_part[(size_t)split * n + n0 + bt] = sum;
+      }
+    }
   } else {
     // ---------------------------------------------------------------- E tile (Philox, theta.cuh)
     // Two groups of two warps take alternate stages (group g: stages c = g mod 2), each lane one X
@@ -518,6 +543,8 @@ sketch_sparse_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int
 }
 
 // tcgen05 path: any n (64-column tiles), k <= 4 * 128 Theta rows
+static_assert(sizeof(double) * 32 * STC_DGROUPS * STC_DWARPS * 4 + sizeof(int) * 32 * STC_DGROUPS * STC_DWARPS <=
+              (size_t)Fmt<double>::RAW * STC_KC * STC_N * sizeof(double), "column-sum scratch fits the raw ring");
 bool sparse_tc_applicable(int k, int n, int zeta) { return n >= 1 && zeta >= 1 && k % zeta == 0 && k <= 4 * STC_M; }
 
 using EncodeTiledFnS = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -527,7 +554,7 @@ using EncodeTiledFnS = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_
 template <typename TX>
 static cudaError_t launch_stc(const TX* X, int64_t m, int n, int64_t ldx, int64_t ro, int k, int zeta, uint64_t seed,
                               int tiles_k, int splits, int64_t rps, double* part, int* overflow, cudaStream_t st,
-                              const uint64_t* srht_s) {
+                              const uint64_t* srht_s, double* cs_part) {
   static EncodeTiledFnS enc = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -551,19 +578,19 @@ static cudaError_t launch_stc(const TX* X, int64_t m, int n, int64_t ldx, int64_
   static const int dbg = !kAblation ? 0 : getenv("RCHOLQR_STC_DEBUG") ? atoi(getenv("RCHOLQR_STC_DEBUG")) : 0;   // ablations only
   const int tiles_n = (n + STC_N - 1) / STC_N;
   kern<<<tiles_k * tiles_n * splits, STC_THREADS, StcCfg<TX>::SMEM, st>>>(map, m, n, ro, k, zeta, seed, tiles_k, tiles_n,
-                                                                           rps, part, overflow, dbg, srht_s);
+                                                                           rps, part, overflow, dbg, srht_s, cs_part);
   return cudaGetLastError();
 }
 
 cudaError_t launch_sparse_tc(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                              int zeta, uint64_t seed, int splits, int64_t rows_per_split, double* part, int* overflow,
-                             cudaStream_t st, const uint64_t* srht_s) {
+                             cudaStream_t st, const uint64_t* srht_s, double* cs_part) {
   const int tiles_k = (k + STC_M - 1) / STC_M;
   if (dtype == RCHOLQR_F64)
     return launch_stc((const double*)X, m, n, ldx, row_offset, k, zeta, seed, tiles_k, splits, rows_per_split, part,
-                      overflow, st, srht_s);
+                      overflow, st, srht_s, cs_part);
   return launch_stc((const float*)X, m, n, ldx, row_offset, k, zeta, seed, tiles_k, splits, rows_per_split, part,
-                    overflow, st, srht_s);
+                    overflow, st, srht_s, cs_part);
 }
 
 // 2D TMA of X: 16-byte aligned base and row pitch, row coordinates < 2^31

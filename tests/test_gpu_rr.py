@@ -59,7 +59,9 @@ def test_factor_rr_parity(cuda, name, kind, m, n, k, rank, dt, sk, tau, f, rf):
     ref = oracle.factor_rr(X, k, tau, f=f, rank_fixed=rf, sketch=so, zeta=8)
     plan = rcq.RCholQR(n=n, k=k, dtype=torch.float64 if dt == "f64" else torch.float32, sketch=sk, nnz_per_col=8)
     g = plan.factor_rr(_t(X), tau, f=f, rank_fixed=rf)
-    if sk == "gaussian":   # D came out of the sketch's own pass over X, not a second read
+    # D came out of the sketch's own pass over X, not a second read: the pre-split Gaussian digit
+    # split or the sparse tcgen05 sketch
+    if sk in ("gaussian", "sparse"):
         assert plan.last_path() & rcq.PATH_COLSQ_FUSED, plan.last_path()
     r = g["rank"]
     perm = _np(g["perm"]).astype(np.int64)
