@@ -111,9 +111,15 @@ rcholqr_status rcholqr_factor_host(rcholqr_plan plan, const void* X_host, int64_
                                    double* R_host, double* S_host, void* stream);
 
 /* Alg. 2 for COLUMN-MAJOR X and Q (element (i, j) at X[j * ldx + i], ldx >= m_local; the storage the
- * paper notes favours sketching).  Layout adapter: X is transposed on the GPU into a
- * plan-owned row-major buffer, factored by the row-major path (bitwise the same R, S and Q values), and
- * Q transposed back -- two extra passes over m_local x n (native column-major kernels: DESIGN.md NEXT).
+ * paper notes favours sketching).
+ * NATIVE kernels (no transposes; the same two reads of X and one write of Q as the row-major path) serve
+ * fp32 X with n <= 128 when X, Q and their column pitches are 16-byte aligned: the tcgen05 sketch kernels
+ * (sparse-sign, Rademacher, SRHT, pre-split Gaussian) and the tcgen05 digit solve take column-major tiles
+ * through their TMA tensor maps; rcholqr_last_path then reports RCHOLQR_PATH_COLMAJOR_NATIVE.  R, S and Q
+ * are bitwise those of the row-major path on the transposed input.
+ * Otherwise (fp64 X, n > 128, misaligned buffers, or a sketch kernel's headroom-overflow flag) a layout
+ * ADAPTER runs: X is transposed on the GPU into a plan-owned row-major buffer, factored by the row-major
+ * path and Q transposed back -- two extra passes over m_local x n.
  *   X [device] n columns of m_local rows, leading dim ldx;  Q [device] likewise, leading dim ldq;
  *   R, S, row_offset, stream: as for rcholqr_factor.  Q must not overlap X.  SYNCHRONOUS. */
 rcholqr_status rcholqr_factor_colmajor(rcholqr_plan plan, const void* X, int64_t m_local, int64_t row_offset,
@@ -245,6 +251,7 @@ rcholqr_status rcholqr_last_timings(rcholqr_plan plan, float out_ms[6]);
  *   SOLVE_DMMA       the tall solve ran on a blocked fp64 DMMA substitution kernel
  *   COLSQ_FUSED      (rcholqr_factor_rr / _rr2) D = diag ||X(:,j)|| came out of the sketch's own pass over X
  *                    (the pre-split Gaussian digit split), no separate column-norm pass
+ *   COLMAJOR_NATIVE  (rcholqr_factor_colmajor) the native column-major kernels served the call (no transposes)
  * *out receives the bits.  SYNCHRONIZES on `stream` (reads the device overflow word).  Errors:
  * E_INVALID for a NULL plan or out. */
 #define RCHOLQR_PATH_SKETCH_TC 1u
@@ -254,6 +261,7 @@ rcholqr_status rcholqr_last_timings(rcholqr_plan plan, float out_ms[6]);
 #define RCHOLQR_PATH_SOLVE_TC 16u
 #define RCHOLQR_PATH_SOLVE_DMMA 32u
 #define RCHOLQR_PATH_COLSQ_FUSED 64u
+#define RCHOLQR_PATH_COLMAJOR_NATIVE 128u /* rcholqr_factor_colmajor: native column-major kernels, no layout adapter */
 rcholqr_status rcholqr_last_path(rcholqr_plan plan, uint32_t* out, void* stream);
 
 #ifdef __cplusplus

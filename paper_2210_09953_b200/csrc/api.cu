@@ -156,6 +156,9 @@ struct DeviceGuard {
   }
 };
 
+// internal: no native column-major kernel for this plan / alignment (rcholqr_factor_colmajor then takes the adapter)
+constexpr rcholqr_status RCHOLQR_E_UNSUPPORTED_INTERNAL = (rcholqr_status)100;
+
 rcholqr_status cuda_status(cudaError_t e) {
   if (e == cudaSuccess) return RCHOLQR_OK;
   if (getenv("RCHOLQR_DEBUG")) fprintf(stderr, "rcholqr: CUDA error: %s\n", cudaGetErrorString(e));
@@ -215,7 +218,7 @@ rcholqr_status check_factor_args(rcholqr_plan p, const void* X, int64_t m, int64
 rcholqr_status do_sketch(rcholqr_plan p, const void* X, int64_t m, int64_t ro, int64_t ldx, double* P,
                          cudaStream_t st, const SketchLaunch* Lp = nullptr, int k = 0, double* part = nullptr,
                          double* partc = nullptr, int k_first = 0, bool allreduce = true, double* cs_part = nullptr,
-                         double* cs_out = nullptr, bool* cs_done = nullptr) {
+                         double* cs_out = nullptr, bool* cs_done = nullptr, bool colmajor = false) {
   if (cs_done) *cs_done = false;
   const auto& d = p->d;
   const SketchLaunch& L = Lp ? *Lp : p->sk;
@@ -232,9 +235,11 @@ rcholqr_status do_sketch(rcholqr_plan p, const void* X, int64_t m, int64_t ro, i
         else cudaGetLastError();   // not enough memory: the in-kernel split is used instead
       }
     }
-    CU(launch_sketch(L, X, d.dtype, m, d.n, ldx, ro, k, d.nnz_per_col, d.seed, part, partc, P, p->status_d, p->flag_d,
-                     p->xdig, p->xdig_bytes, st, timed ? p->ev[1] : nullptr, k_first, &p->path, p->flag_seen_d,
-                     cs_part, cs_out, cs_done));
+    const cudaError_t se = launch_sketch(L, X, d.dtype, m, d.n, ldx, ro, k, d.nnz_per_col, d.seed, part, partc, P,
+                                         p->status_d, p->flag_d, p->xdig, p->xdig_bytes, st, timed ? p->ev[1] : nullptr,
+                                         k_first, &p->path, p->flag_seen_d, cs_part, cs_out, cs_done, colmajor);
+    if (colmajor && se == cudaErrorNotSupported) return RCHOLQR_E_UNSUPPORTED_INTERNAL;
+    CU(se);
   } else {
     if (timed) { cudaEventRecord(p->ev[0], st); cudaEventRecord(p->ev[1], st); }
     CU(cudaMemsetAsync(P, 0, sizeof(double) * (size_t)k * d.n, st));
@@ -263,8 +268,10 @@ SolvePlan plan_solve(int n, int dtype, size_t smem_optin) {
 
 // Step 3: triangular prep + tall solve (the kernels plan_solve picked).  `n_cols`
 // > 0 solves with that many columns (R n_cols x n_cols) instead of the plan's n.
+// colmajor: X and Q column-major -- only the tcgen05 digit solve reads and writes that layout (else
+// RCHOLQR_E_UNSUPPORTED_INTERNAL: the caller takes the layout adapter).
 rcholqr_status solve(rcholqr_plan p, const void* X, int64_t m, int64_t ldx, const double* R, void* Q, int64_t ldq,
-                     cudaStream_t st, bool timed, int n_cols = 0) {
+                     cudaStream_t st, bool timed, int n_cols = 0, bool colmajor = false) {
   const int n = n_cols > 0 ? n_cols : p->d.n;
   SolvePlan sp_own;
   if (n_cols > 0) sp_own = plan_solve(n, p->d.dtype, p->smem_optin);
@@ -273,10 +280,11 @@ rcholqr_status solve(rcholqr_plan p, const void* X, int64_t m, int64_t ldx, cons
     CU(launch_tri_inverse(R, n, p->W, p->status_d, st));
     if (timed && p->timing) cudaEventRecord(p->ev[5], st);
     const cudaError_t e = launch_solve_tc(p->W, n, (const float*)X, m, ldx, (float*)Q, ldq, p->qws, p->status_d,
-                                          p->sms, st);
+                                          p->sms, st, colmajor);
     if (e == cudaSuccess) { p->path |= kPathSolveTC; return RCHOLQR_OK; }
     if (e != cudaErrorNotSupported) return cuda_status(e);
   }
+  if (colmajor) return RCHOLQR_E_UNSUPPORTED_INTERNAL;
   if (m > 0) p->path |= kPathSolveDmma;
   if (sp.mstream) {
     CU(launch_tri_prep_blocked(R, n, p->W, p->status_d, st));
@@ -769,6 +777,37 @@ rcholqr_status rcholqr_factor_colmajor(rcholqr_plan p, const void* X, int64_t m,
   if (m > 0 && overlaps(X, span_bytes(n, ldx, (int)m, es), Q, span_bytes(n, ldq, (int)m, es))) return RCHOLQR_E_INVALID;
   DeviceGuard dg(p->d.device);
   cudaStream_t st = (cudaStream_t)stream;
+  // Native path (column-wise storage keeps the sketch a single pass): the tcgen05 sketch (sparse-sign /
+  // Rademacher / SRHT E tile, or the pre-split Gaussian) and the tcgen05 digit solve read X and write Q column-major
+  // through their tensor maps -- no transposes, the same two reads of X and one write of Q as the row-major
+  // path.  It needs fp32 X with n <= 128 (the digit solve) and 16-byte aligned bases and column pitches; if a
+  // sketch kernel raises its headroom-overflow flag (the guarded fallbacks are row-major kernels) or a kernel
+  // is not applicable, the call is redone through the layout adapter below.
+  if (m > 0 && p->sp.solve_tc && solve_tc_supported(X, m, ldx, Q, ldq) && !getenv("RCHOLQR_COLMAJOR_ADAPTER")) {
+    const int k = p->d.k;
+    double* Rout = R ? R : p->Rtmp;
+    p->path = 0;
+    CU(cudaMemsetAsync(p->status_d, 0, 2 * sizeof(int), st));
+    rcholqr_status s = do_sketch(p, X, m, ro, ldx, p->P, st, nullptr, 0, nullptr, nullptr, 0, true, nullptr, nullptr,
+                                 nullptr, true);
+    if (s == RCHOLQR_OK) {
+      CU(launch_qr(p->qr_kind, p->P, k, n, Rout, p->Awork, p->diag, p->tau, p->qr_ws, p->status_d, st));
+      if (S) CU(launch_form_s(p->Awork, p->tau, p->diag, k, n, S, p->status_d, st));
+      if (p->timing) cudaEventRecord(p->ev[4], st);
+      s = solve(p, X, m, ldx, Rout, Q, ldq, st, true, 0, true);
+      if (s == RCHOLQR_OK) {
+        if (p->timing) cudaEventRecord(p->ev[6], st);
+        int words[2] = {0, 0};                                       // [status, sketch overflow seen]
+        CU(cudaMemcpyAsync(words, p->status_d, sizeof(words), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        if (!words[1]) {
+          p->path |= kPathColmajorNative;
+          return read_status(p, st);
+        }
+      }
+    }
+    if (s != RCHOLQR_OK && s != RCHOLQR_E_UNSUPPORTED_INTERNAL) return s;
+  }
   const size_t need = (size_t)std::max<int64_t>(m, 1) * n * es;   // row-major staging of X and Q
   if (need > p->xq_bytes) {
     cudaFree(p->xbuf); cudaFree(p->qbuf);

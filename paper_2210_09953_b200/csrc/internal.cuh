@@ -44,7 +44,8 @@ enum : int { kStNonfinite = 1, kStSingular = 2 };
 // Which kernels served the last call (rcholqr_last_path; the bits are RCHOLQR_PATH_* of rcholqr.h).
 enum : unsigned { kPathSketchTC = RCHOLQR_PATH_SKETCH_TC, kPathSketchPresplit = RCHOLQR_PATH_SKETCH_PRESPLIT,
                   kPathSketchCudaCore = RCHOLQR_PATH_SKETCH_CUDA_CORE, kPathSketchFallback = RCHOLQR_PATH_SKETCH_FALLBACK,
-                  kPathSolveTC = RCHOLQR_PATH_SOLVE_TC, kPathSolveDmma = RCHOLQR_PATH_SOLVE_DMMA };
+                  kPathSolveTC = RCHOLQR_PATH_SOLVE_TC, kPathSolveDmma = RCHOLQR_PATH_SOLVE_DMMA,
+                  kPathColmajorNative = RCHOLQR_PATH_COLMAJOR_NATIVE };
 
 // One FP64 tensor-core MMA: D(16x8) += A(16x4) B(4x8)  (DMMA on sm_100a; tcgen05 has no f64 kind).
 // Fragments (PTX ISA, mma.m16n8k4 .f64): g = lane/4, t = lane%4;
@@ -64,7 +65,8 @@ bool sparse_tc_applicable(int k, int n, int zeta);
 bool sparse_tc_aligned(const void* X, int dtype, int64_t m, int64_t ldx);
 cudaError_t launch_sparse_tc(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                              int zeta, uint64_t seed, int splits, int64_t rows_per_split, double* part, int* overflow,
-                             cudaStream_t st, const uint64_t* srht_s = nullptr, double* cs_part = nullptr);
+                             cudaStream_t st, const uint64_t* srht_s = nullptr, double* cs_part = nullptr,
+                             bool colmajor = false);
 enum TrsmKind : int { kTrsm64x24 = 0, kTrsm128x64 = 1, kTrsm128x112 = 2, kTrsm128x128 = 3 };
 enum QrKind : int { kQrSmem = 0, kQrGlobal = 1, kQrBlocked = 2 };
 
@@ -100,7 +102,8 @@ constexpr int kXdigSplitBlocks = 148 * 8;
 cudaError_t launch_colsum_reduce(const double* part, int rows, int n, double* out, int* status, cudaStream_t st);
 cudaError_t launch_gauss_tcp(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                              uint64_t seed, int tiles_k, int tiles_n, int splits, double* part, double* partc,
-                             int* overflow, void* ws, size_t ws_bytes, cudaStream_t st, double* cs_part = nullptr);
+                             int* overflow, void* ws, size_t ws_bytes, cudaStream_t st, double* cs_part = nullptr,
+                             bool colmajor = false);
 constexpr size_t kXdigCapBytes = (size_t)4 << 30;   // largest pre-split digit workspace a plan allocates
 struct TrsmLaunch {
   int kind;
@@ -114,7 +117,8 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
                           int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* partc, double* P,
                           int* status, int* flag, void* xdig, size_t xdig_bytes, cudaStream_t st, cudaEvent_t ev_mid,
                           int k_first = 0, unsigned* path = nullptr, int* flag_seen = nullptr,
-                          double* cs_part = nullptr, double* cs_out = nullptr, bool* cs_done = nullptr);
+                          double* cs_part = nullptr, double* cs_out = nullptr, bool* cs_done = nullptr,
+                          bool colmajor = false);
 TrsmLaunch plan_trsm(int n, int dtype, size_t smem_optin);
 cudaError_t launch_tri_inverse(const double* R, int n, double* W, int* status, cudaStream_t st);
 cudaError_t launch_trsm(const TrsmLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
@@ -151,7 +155,7 @@ bool solve_tc_applicable(int dtype, int n);
 bool solve_tc_supported(const void* X, int64_t m, int64_t ldx, const void* Q, int64_t ldq);
 size_t solve_tc_workspace();
 cudaError_t launch_solve_tc(const double* Winv, int n, const float* X, int64_t m, int64_t ldx, float* Q, int64_t ldq,
-                            void* ws, int* status, int sms, cudaStream_t st);
+                            void* ws, int* status, int sms, cudaStream_t st, bool colmajor = false);
 // RCholeskyQR2 (rcqr2.cu): Gram A = Q^T Q, Cholesky R', R' R
 cudaError_t launch_reduce(const double* part, int splits, int64_t kn, double scale, double* P, int* status,
                           cudaStream_t st);

@@ -682,7 +682,12 @@ static cudaError_t launch_gauss_typed(const SketchLaunch& L, const void* X, int6
 cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
                           int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* partc, double* P,
                           int* status, int* flag, void* xdig, size_t xdig_bytes, cudaStream_t st, cudaEvent_t ev_mid,
-                          int k_first, unsigned* path, int* flag_seen, double* cs_part, double* cs_out, bool* cs_done) {
+                          int k_first, unsigned* path, int* flag_seen, double* cs_part, double* cs_out, bool* cs_done,
+                          bool colmajor) {
+  // colmajor: X column-major (ldx >= m is the column pitch).  Only the tcgen05 kernels read that layout (sparse /
+  // dense-E kernel, pre-split Gaussian); the guarded CUDA-core / DMMA fallbacks are not launched, so a raised
+  // overflow flag (reported through flag_seen) means the caller must redo the call through the layout adapter.
+  // cudaErrorNotSupported: no native kernel for this plan / alignment.
   if (cs_done) *cs_done = false;
   cudaError_t e;
   unsigned pb = 0;
@@ -700,7 +705,7 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
       e = cudaMemsetAsync(flag, 0, sizeof(int), st);
       if (e != cudaSuccess) return e;
       e = launch_sparse_tc(X, dtype, m, n, ldx, row_offset, k, zeta, seed, L.splits, rps, part, flag, st, nullptr,
-                           cs_out ? cs_part : nullptr);
+                           cs_out ? cs_part : nullptr, colmajor);
       if (e == cudaSuccess) {
         guard = flag; pb |= kPathSketchTC;
         if (cs_out) {                                      // D of Alg. 7 came with this pass
@@ -710,6 +715,7 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
         }
       } else if (e != cudaErrorNotSupported) return e;
     }
+    if (colmajor && !guard) return cudaErrorNotSupported;
     if (!guard) pb |= kPathSketchCudaCore;
     auto launch = [&](auto* tag) -> cudaError_t {
       using TX = std::remove_pointer_t<decltype(tag)>;
@@ -735,7 +741,7 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
       if (e2 != cudaSuccess) return e2;
       return cudaGetLastError();
     };
-    e = dtype == RCHOLQR_F64 ? launch((double*)nullptr) : launch((float*)nullptr);
+    e = colmajor ? cudaSuccess : (dtype == RCHOLQR_F64 ? launch((double*)nullptr) : launch((float*)nullptr));
     scale = 1.0 / std::sqrt((double)zeta);
   } else {
     int splits = L.splits;
@@ -754,7 +760,7 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
         if (e == cudaSuccess) e = cudaMemsetAsync(partc, 0, sizeof(double) * (size_t)splits * k * n, st);
         if (e == cudaSuccess)
           e = launch_sparse_tc(X, dtype, m, n, ldx, row_offset, k, L.rad == 2 ? -1 : 0, seed, splits, trps, part,
-                               flag, st, L.srht_s);
+                               flag, st, L.srht_s, nullptr, colmajor);
         if (e != cudaSuccess) return e;
         guard = flag;
         pb |= kPathSketchTC;
@@ -770,7 +776,7 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
       e = cudaErrorNotSupported;
       if (xdig && !getenv("RCHOLQR_GAUSS_NO_PRESPLIT")) {   // pre-split digits (row chunks that fit the workspace)
         e = launch_gauss_tcp(X, dtype, m, n, ldx, row_offset, k, seed, L.tc_tiles_k, L.tc_tiles_n, splits, part,
-                             partc, flag, xdig, xdig_bytes, st, cs_out ? cs_part : nullptr);
+                             partc, flag, xdig, xdig_bytes, st, cs_out ? cs_part : nullptr, colmajor);
         if (e == cudaSuccess) {
           pb |= kPathSketchPresplit;
           if (cs_out) {                                    // D of Alg. 7 came with this pass
@@ -780,18 +786,20 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
           }
         }
       }
-      if (e == cudaErrorNotSupported)
+      if (e == cudaErrorNotSupported && !colmajor)
         e = launch_gauss_tc(X, dtype, m, n, ldx, row_offset, k, seed, L.tc_tiles_k, L.tc_tiles_n, splits, trps, part,
                             partc, flag, st);
       if (e == cudaSuccess) { guard = flag; pb |= kPathSketchTC; }   // else: the DMMA kernel computes the sketch
       else if (e != cudaErrorNotSupported) return e;
     }
+    if (colmajor && !guard) return cudaErrorNotSupported;
     // DMMA kernel: the path itself, or the overflow fallback of the tensor-core kernel (same splits)
     SketchLaunch Lg = L;
     Lg.splits = splits;
     const int64_t gper = (m + splits - 1) / splits;
     const int64_t rps = std::max<int64_t>(KC, ((gper + KC - 1) / KC) * KC);
-    e = dtype == RCHOLQR_F64
+    e = colmajor ? cudaSuccess
+        : dtype == RCHOLQR_F64
             ? launch_gauss_typed<double>(Lg, X, m, n, ldx, row_offset, k, seed, rps, part, partc, st, guard)
             : launch_gauss_typed<float>(Lg, X, m, n, ldx, row_offset, k, seed, rps, part, partc, st, guard);
     scale = 1.0 / std::sqrt((double)k);

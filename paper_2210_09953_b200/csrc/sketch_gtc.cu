@@ -463,15 +463,16 @@ struct GpCfg {
 
 // per (split, column): max |x| high bits over the split's first 32 rows (tile-padded columns)
 template <typename TX>
-__global__ void xdig_maxbits_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64_t rows_per_split,
-                                    int npad, uint32_t* __restrict__ maxbits) {
+__global__ void xdig_maxbits_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t sr, int64_t sc,
+                                    int64_t rows_per_split, int npad, uint32_t* __restrict__ maxbits) {
+  // element (i, j) at X[i sr + j sc]: (ldx, 1) row-major, (1, ldx) column-major
   const int split = blockIdx.x;
   const int64_t i0 = (int64_t)split * rows_per_split;
   const int rows = (int)max((int64_t)0, min((int64_t)GT_KC, min(m, i0 + rows_per_split) - i0));
   for (int j = threadIdx.x; j < npad; j += blockDim.x) {
     uint32_t mx = 0u;
     if (j < n)
-      for (int ii = 0; ii < rows; ++ii) mx = max(mx, gt_habs(X[(i0 + ii) * ldx + j]));
+      for (int ii = 0; ii < rows; ++ii) mx = max(mx, gt_habs(X[(i0 + ii) * sr + j * sc]));
     maxbits[(size_t)split * npad + j] = mx;
   }
 }
@@ -479,7 +480,7 @@ __global__ void xdig_maxbits_kernel(const TX* __restrict__ X, int64_t m, int n, 
 // unit u = ((split * stages + stage) * tiles_n + tn): DX digit planes of 128 columns x 32 rows
 template <typename TX>
 __global__ void __launch_bounds__(256)
-xdig_split_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64_t rows_per_split, int stages,
+xdig_split_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t sr, int64_t sc, int64_t rows_per_split, int stages,
                   int tiles_n, int64_t units, const uint32_t* __restrict__ maxbits, unsigned char* __restrict__ dig,
                   int* overflow, double* __restrict__ cs_part) {
   constexpr int DX = GtFmt<TX>::DX;
@@ -503,10 +504,27 @@ xdig_split_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx, int64
 #pragma unroll
     for (int qq = 0; qq < 4; ++qq) {
       uint32_t hw[4], lw[4];
+      // column-major X (sr == 1): the thread's 4 consecutive rows of its column are one 16 / 32-byte
+      // vector when aligned (i0 is a multiple of 32 rows, so the base and sc decide)
+      TX xq[4];
+      const int64_t iq = i0 + kg * 16 + qq * 4;
+      const bool vec = sr == 1 && col < n && iq + 4 <= i_end && ((uintptr_t)(X + iq + (int64_t)col * sc) % 16) == 0;
+      if (vec) {
+        if constexpr (sizeof(TX) == 4) {
+          const float4 f = __ldg(reinterpret_cast<const float4*>(X + iq + (int64_t)col * sc));
+          xq[0] = f.x; xq[1] = f.y; xq[2] = f.z; xq[3] = f.w;
+        } else {
+          const double2 f0 = __ldg(reinterpret_cast<const double2*>(X + iq + (int64_t)col * sc));
+          const double2 f1 = __ldg(reinterpret_cast<const double2*>(X + iq + (int64_t)col * sc) + 1);
+          xq[0] = f0.x; xq[1] = f0.y; xq[2] = f1.x; xq[3] = f1.y;
+        }
+      } else {
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) xq[kk] = (col < n && iq + kk < i_end) ? X[(iq + kk) * sr + (int64_t)col * sc] : (TX)0;
+      }
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
-        const int64_t i = i0 + kg * 16 + qq * 4 + kk;
-        const TX x = (col < n && i < i_end) ? X[i * ldx + col] : (TX)0;
+        const TX x = xq[kk];
         if (col < n) { amax = max(amax, gt_habs(x) >= cp.lim ? 0xFFFFFFFFu : 0u); bad |= cp.bad; }
         if (cs_part) cs = fma((double)x, (double)x, cs);
         gt_split(x, cp.s, hw[kk], lw[kk]);
@@ -776,14 +794,15 @@ static int xdig_split_grid(int64_t units, int tiles_n) {
 template <typename TX>
 static cudaError_t launch_gtcp(const TX* X, int64_t m, int n, int64_t ldx, int64_t ro, int k, uint64_t seed,
                                int tiles_k, int tiles_n, int splits, int64_t rps, double* part, double* partc,
-                               int* overflow, void* ws, int accumulate, double* cs_part, cudaStream_t st) {
+                               int* overflow, void* ws, int accumulate, double* cs_part, cudaStream_t st, bool colmajor) {
   constexpr int DX = GtFmt<TX>::DX;
+  const int64_t sr = colmajor ? 1 : ldx, sc = colmajor ? ldx : 1;   // element (i, j) at X[i sr + j sc]
   const int stages = (int)(rps / GT_KC);
   const int64_t units = (int64_t)splits * stages * tiles_n;
   unsigned char* dig = reinterpret_cast<unsigned char*>(ws);
   uint32_t* maxbits = reinterpret_cast<uint32_t*>(dig + (size_t)units * DX * 4096);
-  xdig_maxbits_kernel<TX><<<splits, 256, 0, st>>>(X, m, n, ldx, rps, tiles_n * GT_M, maxbits);
-  xdig_split_kernel<TX><<<xdig_split_grid(units, tiles_n), 256, 0, st>>>(X, m, n, ldx, rps, stages, tiles_n, units,
+  xdig_maxbits_kernel<TX><<<splits, 256, 0, st>>>(X, m, n, sr, sc, rps, tiles_n * GT_M, maxbits);
+  xdig_split_kernel<TX><<<xdig_split_grid(units, tiles_n), 256, 0, st>>>(X, m, n, sr, sc, rps, stages, tiles_n, units,
                                                                           maxbits, dig, overflow, cs_part);
   auto kern = sketch_gauss_tcp_kernel<TX>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GpCfg<TX>::SMEM);
@@ -799,7 +818,7 @@ static cudaError_t launch_gtcp(const TX* X, int64_t m, int n, int64_t ldx, int64
 // into the per-split partials (TwoSum), so the result is the sketch of all m rows.
 cudaError_t launch_gauss_tcp(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                              uint64_t seed, int tiles_k, int tiles_n, int splits, double* part, double* partc,
-                             int* overflow, void* ws, size_t ws_bytes, cudaStream_t st, double* cs_part) {
+                             int* overflow, void* ws, size_t ws_bytes, cudaStream_t st, double* cs_part, bool colmajor) {
   const size_t es = dtype == RCHOLQR_F64 ? 8 : 4;
   int64_t chunk = m;
   while (chunk > GT_KC && gauss_tcp_workspace(chunk, n, dtype, splits) > ws_bytes) chunk = (chunk + 1) / 2;
@@ -812,12 +831,12 @@ cudaError_t launch_gauss_tcp(const void* X, int dtype, int64_t m, int n, int64_t
     const int64_t mc = std::min(chunk, m - c0);
     const int64_t per = (mc + splits - 1) / splits;
     const int64_t rps = std::max<int64_t>(GT_KC, ((per + GT_KC - 1) / GT_KC) * GT_KC);
-    const char* Xc = reinterpret_cast<const char*>(X) + (size_t)c0 * ldx * es;
+    const char* Xc = reinterpret_cast<const char*>(X) + (size_t)c0 * (colmajor ? 1 : ldx) * es;   // row c0
     cudaError_t e = dtype == RCHOLQR_F64
                         ? launch_gtcp((const double*)Xc, mc, n, ldx, row_offset + c0, k, seed, tiles_k, tiles_n, splits,
-                                      rps, part, partc, overflow, ws, c0 > 0, cs_part, st)
+                                      rps, part, partc, overflow, ws, c0 > 0, cs_part, st, colmajor)
                         : launch_gtcp((const float*)Xc, mc, n, ldx, row_offset + c0, k, seed, tiles_k, tiles_n, splits,
-                                      rps, part, partc, overflow, ws, c0 > 0, cs_part, st);
+                                      rps, part, partc, overflow, ws, c0 > 0, cs_part, st, colmajor);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -54,6 +54,9 @@ constexpr int STC_THREADS = 32 * (2 + STC_DGROUPS * STC_DWARPS + STC_EWARPS);
 constexpr int STC_E_BYTES = STC_M * STC_KC;              // E tile (int8, K-major)
 static_assert(16 * STC_EWARPS == STC_KC, "one X row per E-warp lane, two warp groups");
 
+#ifndef RCQ_STC_F2F
+#define RCQ_STC_F2F 1             // fp32 X -> double by F2F.F64.F32 (0: built from the float's bits, x 2^-128)
+#endif
 template <typename TX> struct Fmt;
 // B row layout (bytes along N) and the two MMAs per k-step (N0 + N1 columns):
 //   fp32: [lo words of the 64 columns (256 B) | hi halves (128 B) | 16 ones]: N = 256 + 144.  The two constant
@@ -94,7 +97,7 @@ struct StcCfg {
 
 // Per-(CTA, column) scale: e = (exponent bound of the first stage's max |x|) + 4 bits of headroom.
 struct ColParam {
-  double s;          // fp32: 2^(175 - e) (applied to x 2^-128); fp64: 2^(31 - e)
+  double s;          // fp32: 2^(47 - e) (RCQ_STC_F2F = 0: 2^(175 - e), applied to x 2^-128); fp64: 2^(31 - e)
   uint32_t lim;      // fp64: |x| high word must be < lim (high word of 2^e)
   bool bad;          // scale outside the exact construction range: fall back
   int e;
@@ -111,7 +114,7 @@ __device__ __forceinline__ ColParam col_param(uint32_t maxbits) {
     emax = maxbits < 0x00800000u ? -126 : (int)(maxbits >> 23) - 126;
     if (maxbits == 0u) emax = -44;       // all-zero first stage: later |x| >= 2^-40 overflows -> fallback
     p.e = emax + 4;
-    p.s = ldexp(1.0, 128 + Fmt<float>::FB - p.e);
+    p.s = ldexp(1.0, (RCQ_STC_F2F ? 0 : 128) + Fmt<float>::FB - p.e);
     p.bad = p.e < -70;                   // subnormal inputs could then round to nonzero digits
   } else {
     emax = maxbits < 0x00100000u ? -1022 : (int)(maxbits >> 20) - 1022;
@@ -129,6 +132,11 @@ __device__ __forceinline__ ColParam col_param(uint32_t maxbits) {
 // unsigned digits of F + 2^47, hi bytes 2, 3 = 0x38, 0x43 unless F overflowed.  x 2^-128 is built exactly from
 // the float's bits (normal x; one shift, one LOP3), so the scaling is one DFMA.
 __device__ __forceinline__ uint2 magic_word(float x, double s) {
+#if RCQ_STC_F2F
+  // one exact F2F.F64.F32 on the conversion pipe instead of three integer-pipe instructions (s = 2^(47-e))
+  const double tf = fma((double)x, s, kMagic + 140737488355328.0);
+  return make_uint2((uint32_t)__double2loint(tf), (uint32_t)__double2hiint(tf));
+#endif
   const uint32_t u = __float_as_uint(x);
   uint32_t h;                                                                      // x 2^-128: one LOP3
   asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(h) : "r"((uint32_t)((int32_t)u >> 3)), "r"(0x8FFFFFFFu), "r"(0x30000000u));
@@ -147,7 +155,10 @@ __device__ __forceinline__ uint2 magic_word(double x, double s) {
   return make_uint2(lo ^ 0x80808080u, hi ^ 0x00808080u);
 }
 
-template <typename TX>
+// CM: X column-major (element (i, j) at X[j * ldx + i]): the tensor map's contiguous dimension is
+// the row, a raw stage is [64 columns][64 rows], and the B-byte warps take their elements with conflict-free
+// scalar LDS (thread -> fixed chunk, 8-row blocks rotated per lane octet); E, B, the MMAs and TMEM are the same.
+template <typename TX, bool CM>
 __global__ void __launch_bounds__(STC_THREADS, 1)
 sketch_sparse_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int n, int64_t row_offset, int k,
                         int zeta, uint64_t seed, int tiles_k, int tiles_n, int64_t rows_per_split,
@@ -234,15 +245,23 @@ sketch_sparse_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int
     // ---------------------------------------------------------------- X loader (2D TMA, lane 0)
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];\n" ::"l"(&xmap) : "memory");
-      for (int c = 1; c < STC_PF && c < nstages; ++c) tc::tma_prefetch_2d(&xmap, n0, (int)(i_begin + (int64_t)c * STC_KC));
+      for (int c = 1; c < STC_PF && c < nstages; ++c) {
+        const int pr = (int)(i_begin + (int64_t)c * STC_KC);
+        if (CM) tc::tma_prefetch_2d(&xmap, pr, n0); else tc::tma_prefetch_2d(&xmap, n0, pr);
+      }
     }
     for (int c = 0; c < nstages; ++c) {
       const int s = c % F::RAW;
       if (c >= F::RAW) tc::mbar_wait(&rempty[s], (uint32_t)(((c / F::RAW) - 1) & 1));
       if (lane == 0) {
-        if (c + STC_PF < nstages) tc::tma_prefetch_2d(&xmap, n0, (int)(i_begin + (int64_t)(c + STC_PF) * STC_KC));
+        if (c + STC_PF < nstages) {
+          const int pr = (int)(i_begin + (int64_t)(c + STC_PF) * STC_KC);
+          if (CM) tc::tma_prefetch_2d(&xmap, pr, n0); else tc::tma_prefetch_2d(&xmap, n0, pr);
+        }
         tc::mbar_arrive_tx(&rfull[s], (uint32_t)C::RAW_STAGE);
-        tc::tma_load_2d(raw_base + (size_t)s * STC_KC * STC_N, &xmap, n0, (int)(i_begin + (int64_t)c * STC_KC), &rfull[s]);
+        const int lr = (int)(i_begin + (int64_t)c * STC_KC);
+        if (CM) tc::tma_load_2d(raw_base + (size_t)s * STC_KC * STC_N, &xmap, lr, n0, &rfull[s]);
+        else tc::tma_load_2d(raw_base + (size_t)s * STC_KC * STC_N, &xmap, n0, lr, &rfull[s]);
       }
       __syncwarp();
     }
@@ -255,7 +274,17 @@ sketch_sparse_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int
     const int w = (warp - 2) % STC_DWARPS, p = lane >> 3, q = lane & 7;
     const int wi = w & 3, rot = 4 * (w >> 2);
     const int cb = wi % C::CB, rbase = (wi / C::CB) * C::TASKS;
-    const int ch = 8 * cb + ((q + p + rot) & 7);         // this thread's raw chunk (columns ch * CE .. + CE - 1)
+    // column-major: lane octet o = p takes 8 consecutive rows of one chunk; fp32: chunks 2 w + (o & 1), 8-row
+    // blocks (2 t + (o >> 1) + 2 (o & 1)) mod 8; fp64: chunks 4 w + o, blocks (t + o) mod 8 -- the four octets of an
+    // LDS read four distinct bank groups, the STS.128 of an octet is 128 contiguous bytes and the two octets of
+    // an STS.64 phase write different 8-byte halves
+    const int ch = !CM ? 8 * cb + ((q + p + rot) & 7)     // this thread's raw chunk (columns ch * CE .. + CE - 1)
+                       : (sizeof(TX) == 4 ? 2 * w + (p & 1) : 4 * w + p);
+    auto row_of = [&](int t) {                           // row (within the stage) of the thread's task t
+      if constexpr (!CM) return 8 * (rbase + t) + q;
+      else if constexpr (sizeof(TX) == 4) return 8 * ((2 * t + (p >> 1) + 2 * (p & 1)) & 7) + q;
+      else return 8 * ((t + p) & 7) + q;
+    };
     double sc[C::CE];
     uint32_t lim[C::CE];
     bool bad = false;
@@ -264,7 +293,8 @@ sketch_sparse_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int
       const int rows0 = (int)min((int64_t)STC_KC, i_end - i_begin);
       const int dt = tid - 64, j = dt & (STC_N - 1);
       uint32_t mx = 0u;
-      for (int r = dt >> 6; r < rows0; r += 32 * STC_DGROUPS * STC_DWARPS / STC_N) mx = max(mx, hi_abs(raw_base[r * STC_N + j]));
+      for (int r = dt >> 6; r < rows0; r += 32 * STC_DGROUPS * STC_DWARPS / STC_N)
+        mx = max(mx, hi_abs(raw_base[CM ? j * STC_KC + r : r * STC_N + j]));
       atomicMax(&col_max[j], mx);
       tc::named_bar(1, 32 * STC_DGROUPS * STC_DWARPS);
 #pragma unroll
@@ -294,8 +324,11 @@ sketch_sparse_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int
         TX xv[C::TASKS][C::CE];
 #pragma unroll
         for (int t = 0; t < C::TASKS; ++t) {
-          const int i = 8 * (rbase + t) + q;
-          if constexpr (sizeof(TX) == 4) {
+          const int i = row_of(t);
+          if constexpr (CM) {
+#pragma unroll
+            for (int e = 0; e < C::CE; ++e) xv[t][e] = raw[(ch * C::CE + e) * STC_KC + i];
+          } else if constexpr (sizeof(TX) == 4) {
             const float4 f = *reinterpret_cast<const float4*>(raw + i * STC_N + ch * 4);
             xv[t][0] = f.x; xv[t][1] = f.y; xv[t][2] = f.z; xv[t][3] = f.w;
           } else {
@@ -308,14 +341,14 @@ sketch_sparse_tc_kernel(const __grid_constant__ CUtensorMap xmap, int64_t m, int
         if (rows < STC_KC) {                             // rows of the next split (or past m): E is zero there
 #pragma unroll
           for (int t = 0; t < C::TASKS; ++t)
-            if (8 * (rbase + t) + q >= rows) {
+            if (row_of(t) >= rows) {
 #pragma unroll
               for (int e = 0; e < C::CE; ++e) xv[t][e] = (TX)0;
             }
         }
 #pragma unroll
         for (int t = 0; t < C::TASKS; ++t) {
-          const int i = 8 * (rbase + t) + q;
+          const int i = row_of(t);
           uint2 wv[C::CE];
 #pragma unroll
           for (int e = 0; e < C::CE; ++e) {
@@ -554,7 +587,7 @@ using EncodeTiledFnS = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_
 template <typename TX>
 static cudaError_t launch_stc(const TX* X, int64_t m, int n, int64_t ldx, int64_t ro, int k, int zeta, uint64_t seed,
                               int tiles_k, int splits, int64_t rps, double* part, int* overflow, cudaStream_t st,
-                              const uint64_t* srht_s, double* cs_part) {
+                              const uint64_t* srht_s, double* cs_part, bool colmajor) {
   static EncodeTiledFnS enc = [] {
     void* p = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -565,14 +598,15 @@ static cudaError_t launch_stc(const TX* X, int64_t m, int n, int64_t ldx, int64_
   }();
   if (!enc) return cudaErrorNotSupported;
   CUtensorMap map;
-  const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)m};
+  // row-major: dims (columns, rows), box (64 columns, 64 rows); column-major: dims (rows, columns), box (64 rows, 64 columns)
+  const cuuint64_t dims[2] = {(cuuint64_t)(colmajor ? m : n), (cuuint64_t)(colmajor ? n : m)};
   const cuuint64_t strides[1] = {(cuuint64_t)ldx * sizeof(TX)};
-  const cuuint32_t box[2] = {(cuuint32_t)STC_N, (cuuint32_t)STC_KC}, estr[2] = {1, 1};
+  const cuuint32_t box[2] = {(cuuint32_t)(colmajor ? STC_KC : STC_N), (cuuint32_t)(colmajor ? STC_N : STC_KC)}, estr[2] = {1, 1};
   if (enc(&map, sizeof(TX) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
           const_cast<TX*>(X), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorNotSupported;
-  auto kern = sketch_sparse_tc_kernel<TX>;
+  auto kern = colmajor ? sketch_sparse_tc_kernel<TX, true> : sketch_sparse_tc_kernel<TX, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)StcCfg<TX>::SMEM);
   if (e != cudaSuccess) return e;
   static const int dbg = !kAblation ? 0 : getenv("RCHOLQR_STC_DEBUG") ? atoi(getenv("RCHOLQR_STC_DEBUG")) : 0;   // ablations only
@@ -584,13 +618,13 @@ static cudaError_t launch_stc(const TX* X, int64_t m, int n, int64_t ldx, int64_
 
 cudaError_t launch_sparse_tc(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
                              int zeta, uint64_t seed, int splits, int64_t rows_per_split, double* part, int* overflow,
-                             cudaStream_t st, const uint64_t* srht_s, double* cs_part) {
+                             cudaStream_t st, const uint64_t* srht_s, double* cs_part, bool colmajor) {
   const int tiles_k = (k + STC_M - 1) / STC_M;
   if (dtype == RCHOLQR_F64)
     return launch_stc((const double*)X, m, n, ldx, row_offset, k, zeta, seed, tiles_k, splits, rows_per_split, part,
-                      overflow, st, srht_s, cs_part);
+                      overflow, st, srht_s, cs_part, colmajor);
   return launch_stc((const float*)X, m, n, ldx, row_offset, k, zeta, seed, tiles_k, splits, rows_per_split, part,
-                    overflow, st, srht_s, cs_part);
+                    overflow, st, srht_s, cs_part, colmajor);
 }
 
 // 2D TMA of X: 16-byte aligned base and row pitch, row coordinates < 2^31

@@ -62,6 +62,13 @@ __host__ __device__ constexpr int qt_woff(int g) { return QT_NB * 32 * g * (g + 
 #ifndef RCQ_SOLVE_DW
 #define RCQ_SOLVE_DW 10
 #endif
+// kernel-experiment switches (ablation library only; the defaults are the production kernel)
+#ifndef RCQ_SOLVE_F2F
+#define RCQ_SOLVE_F2F 1      // X -> double by F2F.F64.F32 (0: three integer-pipe instructions)
+#endif
+#ifndef RCQ_SOLVE_ROT
+#define RCQ_SOLVE_ROT 1      // rotate the first digit warp with the tile
+#endif
 template <int KMAX>
 struct QCfg {
   static constexpr bool TMA_RAW = KMAX <= 64;     // raw X ring via TMA (else plain loads)
@@ -88,8 +95,11 @@ struct QCfg {
   static constexpr int THREADS = 32 * (2 + RW + DW);
   static constexpr int DCOLS = QT_G * 8 / RW;     // columns of a group per drain warp (16 or 32)
   static constexpr int QS = HALF ? QT_RWARPS * 32 * 8 * 4 : RW * 32 * DCOLS * 4;   // HALF: 32 x 8 tile per drain warp
+  // row-scale ring depth (tiles): 8 for the raw-ring kernel (column-major X: the loader warp writes the scales of
+  // tile t as soon as its raw stage lands, up to 5 tiles ahead of the last drain that reads the ring), else 4
+  static constexpr int RXD = TMA_RAW ? 8 : 4;
   static constexpr size_t SMEM =
-      (size_t)W_BYTES + (size_t)NSLOT * SLOT_BYTES + (size_t)RAW * RAW_STAGE + QS + 4096;
+      (size_t)W_BYTES + (size_t)NSLOT * SLOT_BYTES + (size_t)RAW * RAW_STAGE + QS + 2048 + (size_t)RXD * QT_M * 4;
   static_assert(SMEM <= 232448, "shared memory");
 };
 
@@ -148,19 +158,40 @@ __device__ __forceinline__ long long qt_combine(uint32_t a0, uint32_t a1, uint32
   // T = p0 2^32 + p1 2^16 + p2 is one IMAD.WIDE and one add into the high word
   const int p0 = (int)a0 * 256 + (int)a1;
   const int p1 = (int)a2 * 256 + (int)a3;
-  long long t;
   if constexpr (K64) {
-    t = (long long)p1 * 65536 + (long long)((int)a4 * 256 + (int)a5 + ((int)a6 >> 8));
+    // p0 2^32 + p2 as one register pair: low word p2 (as unsigned), high word p0 - [p2 < 0]; then one IMAD.WIDE
+    const int p2 = (int)a4 * 256 + (int)a5 + ((int)a6 >> 8);
+    long long c;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(c) : "r"(p2), "r"(p0 + (p2 >> 31)));
+    return (long long)p1 * 65536 + c;
   } else {
-    t = (long long)p1 * 65536 + (long long)(int)a4 * 256 + (long long)((int)a5 + ((int)a6 >> 8));
+    const long long t = (long long)p1 * 65536 + (long long)(int)a4 * 256 + (long long)((int)a5 + ((int)a6 >> 8));
+    return t + ((long long)p0 << 32);
   }
-  return t + ((long long)p0 << 32);
+}
+// column scales of 8 consecutive outputs: fast route 2^(e_j - min e_j) as floats, exact route e_j
+template <bool FAST>
+__device__ __forceinline__ void qt_col_scales(const int* cexp, const float* csf, int j0, int (&cb)[8], float (&sc)[8]) {
+  if constexpr (FAST) {
+    const float4 s0 = *reinterpret_cast<const float4*>(csf + j0), s1 = *reinterpret_cast<const float4*>(csf + j0 + 4);
+    sc[0] = s0.x; sc[1] = s0.y; sc[2] = s0.z; sc[3] = s0.w; sc[4] = s1.x; sc[5] = s1.y; sc[6] = s1.z; sc[7] = s1.w;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) cb[c] = 0;
+  } else {
+    const int4 c0 = *reinterpret_cast<const int4*>(cexp + j0), c1 = *reinterpret_cast<const int4*>(cexp + j0 + 4);
+    cb[0] = c0.x; cb[1] = c0.y; cb[2] = c0.z; cb[3] = c0.w; cb[4] = c1.x; cb[5] = c1.y; cb[6] = c1.z; cb[7] = c1.w;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) sc[c] = 0.0f;
+  }
 }
 // fast route (warp-uniform): every 2^(e_i + e_j - 52) of the warp's rows is a normal fp32, built as the bits
 // (e_i + 75) << 23 plus e_j << 23; else this exact fp64 route (any exponent range)
 __device__ __noinline__ float qt_scale_slow(long long t, int ei, int ej) { return (float)ldexp((double)t, ei + ej - 52); }
 
-template <int KMAX>
+// CM: X and Q column-major (element (i, j) at [j * ld + i]), else row-major.  The tensor maps
+// then have the row as their contiguous dimension: a raw X stage is [column][128 rows], a Q staging tile
+// [column][32 rows]; the digit tiles, the MMAs and TMEM are the same.
+template <int KMAX, bool CM>
 __global__ void __launch_bounds__(QCfg<KMAX>::THREADS, 1)
 solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant__ CUtensorMap qmap,
                 const int8_t* __restrict__ wdig, const int* __restrict__ wexp, const float* __restrict__ X,
@@ -185,16 +216,19 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
   uint64_t* tready = rempty + QT_RAW;       // [2] level buffer written (commit)
   uint64_t* tfree = tready + 2;             // [2] level buffer drained
   uint64_t* wbar = tfree + 2;               // W digits staged
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(wbar + 1);
+  uint64_t* sfull = wbar + 1;               // [RAW] column-major: raw stage landed AND its row scales written
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sfull + QT_RAW);
   // row scales: a ring of 4 tiles, so the digit slot can be refilled while the drain of the tile
   // before still reads its scales (a slot is free once the MMAs of tile t complete, and those
   // follow every drain of tile t - 2; see the TMEM buffer waits below)
   // 16-byte aligned (the drain reads the column exponents cexp with LDS.128); offset from sm, so the compiler
   // keeps these accesses in the shared window (LDS/STS, not generic LD/ST)
   const size_t rexp_off = ((size_t)(reinterpret_cast<unsigned char*>(tmem_slot + 4) - sm) + 15) & ~(size_t)15;
-  int* rexp = reinterpret_cast<int*>(sm + rexp_off);                          // [4][128]
-  int* cexp = rexp + 4 * QT_M;                                                // [KMAX] e_j (W column exponents)
+  int* rexp = reinterpret_cast<int*>(sm + rexp_off);                          // [RXD][128]
+  constexpr int RXD = Cf::RXD;
+  int* cexp = rexp + RXD * QT_M;                                                // [KMAX] e_j (W column exponents)
   int* crange = cexp + QT_KMAX_ALL;                                           // [2] min, max e_j
+  float* csf = reinterpret_cast<float*>(crange + 4);                          // [KMAX] 2^(e_j - min e_j) (fast scaling route)
 
   const int groups = (n + QT_G - 1) / QT_G;
   const int64_t ntiles = (m + QT_M - 1) / QT_M;
@@ -204,7 +238,7 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
 
   if (tid == 0) {
     for (int s = 0; s < NSLOT; ++s) { tc::mbar_init(&dfull[s], Cf::DW); tc::mbar_init(&dempty[s], 1); }
-    for (int s = 0; s < QT_RAW; ++s) { tc::mbar_init(&rfull[s], 1); tc::mbar_init(&rempty[s], Cf::DW); }
+    for (int s = 0; s < QT_RAW; ++s) { tc::mbar_init(&rfull[s], 1); tc::mbar_init(&rempty[s], Cf::DW); tc::mbar_init(&sfull[s], 1); }
     for (int b = 0; b < 2; ++b) { tc::mbar_init(&tready[b], 1); tc::mbar_init(&tfree[b], Cf::RW / 2); }
     tc::mbar_init(wbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -224,6 +258,8 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;\n");
   const uint32_t tmem = *tmem_slot;
+  if (tid < groups * QT_G) csf[tid] = __int_as_float(min(max(cexp[tid] - crange[0], 0), 127) + 127 << 23);
+  __syncthreads();
 
   if (warp == 0) {
     // ---------------------------------------------------------------- MMA issuer (lane 0)
@@ -281,32 +317,70 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
     __syncwarp();
     // the raw ring holds two tiles; tiles up to QT_PF ahead are prefetched into L2 so that enough HBM
     // bytes are in flight per SM (~QT_PF x 34 KB) -- the ring loads then hit L2
+    // raw-stage coordinates: (column 0, row r) row-major, (row r, column 0) column-major
+    auto pf_tile = [&](int64_t row) { if (CM) tc::tma_prefetch_2d(&xmap, (int)row, 0); else tc::tma_prefetch_2d(&xmap, 0, (int)row); };
+    // column-major: this warp also computes the row scales e_i of a landed stage (lane = row; the stage is
+    // [column][128 rows], so a row's columns are 512 B apart and a 16-column digit task cannot see the whole
+    // row) and publishes stage + scales on sfull; row-major: the digit warps do it with a shuffle max
+    auto row_scales = [&](int t2) {
+      const int s2 = t2 % QT_RAW;
+      tc::mbar_wait(&rfull[s2], (uint32_t)((t2 / QT_RAW) & 1));
+      const float* raw = raw_base + (size_t)s2 * QT_M * QT_RS_MAX;
+#pragma unroll 1
+      for (int rb = 0; rb < QT_M / 32; ++rb) {
+        float mf = 0.0f;
+#pragma unroll 8
+        for (int c = 0; c < kpad; c += 2)
+          asm("max.NaN.f32 %0, %0, %1, %2;" : "+f"(mf) : "f"(fabsf(raw[c * QT_M + rb * 32 + lane])),
+              "f"(fabsf(raw[(c + 1) * QT_M + rb * 32 + lane])));
+        const uint32_t mx = __float_as_uint(mf);
+        if (mx >= 0x7F800000u) atomicOr(status, kStNonfinite);
+        rexp[(t2 % RXD) * QT_M + rb * 32 + lane] = mx == 0u ? 0 : (mx < 0x00800000u ? -126 : (int)(mx >> 23) - 126);
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&sfull[s2]);           // release: the scales above are visible to the waiters
+    };
     if (Cf::TMA_RAW && lane == 0)
-      for (int tp = 1; tp < QT_PF && tp < my_tiles; ++tp)
-        tc::tma_prefetch_2d(&xmap, 0, (int)((blockIdx.x + (int64_t)tp * gridDim.x) * QT_M));
+      for (int tp = 1; tp < QT_PF && tp < my_tiles; ++tp) pf_tile((blockIdx.x + (int64_t)tp * gridDim.x) * QT_M);
     for (int tt = 0; tt < (Cf::TMA_RAW ? my_tiles : 0); ++tt) {
       const int s = tt % QT_RAW;
       if (lane == 0) trace(1, tt, 0);
+      // scales of the stage before (landed while the digit warps worked on tile tt - 2), so the digits of tile
+      // tt - 1 can start the moment those warps are free; only then wait for the slot of tile tt
+      if (CM && tt > 0) row_scales(tt - 1);
       if (tt >= QT_RAW) tc::mbar_wait(&rempty[s], (uint32_t)(((tt / QT_RAW) - 1) & 1));
       if (lane == 0) {
         trace(1, tt, 1);
-        if (tt + QT_PF < my_tiles)
-          tc::tma_prefetch_2d(&xmap, 0, (int)((blockIdx.x + (int64_t)(tt + QT_PF) * gridDim.x) * QT_M));
+        if (tt + QT_PF < my_tiles) pf_tile((blockIdx.x + (int64_t)(tt + QT_PF) * gridDim.x) * QT_M);
         const int64_t row0 = (blockIdx.x + (int64_t)tt * gridDim.x) * QT_M;
         if (dbg & 8) tc::mbar_arrive(&rfull[s]);
-        else {
+        else if (CM) {
+          tc::mbar_arrive_tx(&rfull[s], (uint32_t)(QT_M * kpad * 4));
+          tc::tma_load_2d(raw_base + (size_t)s * QT_M * QT_RS_MAX, &xmap, (int)row0, 0, &rfull[s]);
+        } else {
           tc::mbar_arrive_tx(&rfull[s], (uint32_t)(QT_M * (kpad + 4) * 4));
           tc::tma_load_2d(raw_base + (size_t)s * QT_M * QT_RS_MAX, &xmap, 0, (int)row0, &rfull[s]);
         }
       }
       __syncwarp();
     }
+    if (CM && Cf::TMA_RAW && my_tiles > 0) row_scales(my_tiles - 1);
   } else if (warp < 2 + Cf::RW) {
     // ---------------------------------------------------------------- drain (set = buffer, lane quadrant)
     // set = buffer (warps 2..5, 6..9, then again for the second column half when RW = 16)
     const int dset = ((warp - 2) >> 2) & 1, dq = warp & 3, row_l = dq * 32 + lane;
     const int dc0 = ((warp - 2) >> 3) * Cf::DCOLS;     // first column of the group this warp drains
     const uint32_t lb = tmem + ((uint32_t)(dq * 32) << 16);
+    // Column-major Q: a TMA store clips its contiguous (row) dimension in 16-byte units, not by element (measured:
+    // tools/micro/tma_clip_test.cu), so the Q tensor map ends at row m & ~3 and the last m % 4 rows are written by
+    // these plain stores -- the pitch padding of Q is never touched.
+    auto cm_tail = [&](const float (&o)[8], int col0, int64_t row) {
+      if (CM && row >= (m & ~(int64_t)3) && row < m) {
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          if (col0 + c < n) Q[(size_t)(col0 + c) * ldq + row] = o[c];
+      }
+    };
     for (int tt = 0; tt < my_tiles; ++tt) {
       for (int g = 0; g < groups; ++g) {
         const int use = tt * groups + g, buf = use & 1, u = use >> 1;
@@ -323,9 +397,10 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
           // 8 columns at a time: all 7 level loads in flight before one wait; each 32-row x 8-column
           // fp32 chunk is staged in a 1 KB tile (all the room the K-half ring leaves) and written
           // by a 2D TMA store; the TMEM buffer is released right after the last chunk's loads
-          const int ei = rexp[(tt & 3) * QT_M + row_l];
-          const int rbits = (ei + 75) << 23;
-          const bool fast = __all_sync(0xffffffffu, ei + crange[0] + 75 >= 1 && ei + crange[1] + 75 <= 254);
+          const int ei = rexp[(tt % RXD) * QT_M + row_l];
+          const float rs = __int_as_float((ei + crange[0] + 75) << 23);   // 2^(e_i + min e_j - 52), used if fast
+          const bool fast = __all_sync(0xffffffffu, ei + crange[0] + 75 >= 1 && ei + crange[1] + 75 <= 254 &&
+                                                        crange[1] - crange[0] <= 127);
           const uint32_t lv = lb + buf * (QT_LEV * QT_G);
           unsigned char* qs = qstage + (warp - 2) * (32 * 8 * 4);
           auto drain = [&](auto fast_tag) {
@@ -335,9 +410,9 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
               uint32_t lvl[QT_LEV][8];
 #pragma unroll
               for (int L = 0; L < QT_LEV; ++L) tc::ld8(lv + L * QT_G + h * 8, lvl[L]);
-              const int4 c0 = *reinterpret_cast<const int4*>(cexp + g * QT_G + h * 8);
-              const int4 c1 = *reinterpret_cast<const int4*>(cexp + g * QT_G + h * 8 + 4);
-              const int cb[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+              int cb[8];
+              float sc[8];
+              qt_col_scales<FAST>(cexp, csf, g * QT_G + h * 8, cb, sc);
               tc::wait_ld();
               if (h == QT_G / 8 - 1) {
                 asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -348,19 +423,27 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
 #pragma unroll
               for (int c = 0; c < 8; ++c) {
                 const long long t = qt_combine<KMAX <= 64>(lvl[0][c], lvl[1][c], lvl[2][c], lvl[3][c], lvl[4][c], lvl[5][c], lvl[6][c]);
-                if constexpr (FAST) o[c] = __ll2float_rn(t) * __int_as_float(rbits + (cb[c] << 23));
+                if constexpr (FAST) o[c] = __ll2float_rn(t) * (rs * sc[c]);   // exact power-of-two factor (normal: fast)
                 else o[c] = qt_scale_slow(t, ei, cb[c]);
               }
               if (lane == 0) tc::bulk_wait_read0();          // previous chunk's store has read the tile
               __syncwarp();
               // 32-byte rows, TMA SWIZZLE_32B (16-byte chunk c of row r at c ^ ((r >> 2) & 1)): conflict-free STS.128
-              const int sw = (lane >> 2) & 1;
-              *reinterpret_cast<float4*>(qs + lane * 32 + (sw << 4)) = make_float4(o[0], o[1], o[2], o[3]);
-              *reinterpret_cast<float4*>(qs + lane * 32 + ((sw ^ 1) << 4)) = make_float4(o[4], o[5], o[6], o[7]);
+              if constexpr (CM) {                            // [8 columns][32 rows]: conflict-free STS.32
+#pragma unroll
+                for (int c = 0; c < 8; ++c) reinterpret_cast<float*>(qs)[c * 32 + lane] = o[c];
+                cm_tail(o, g * QT_G + h * 8, (blockIdx.x + (int64_t)tt * gridDim.x) * QT_M + row_l);
+              } else {
+                const int sw = (lane >> 2) & 1;
+                *reinterpret_cast<float4*>(qs + lane * 32 + (sw << 4)) = make_float4(o[0], o[1], o[2], o[3]);
+                *reinterpret_cast<float4*>(qs + lane * 32 + ((sw ^ 1) << 4)) = make_float4(o[4], o[5], o[6], o[7]);
+              }
               asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
               __syncwarp();
               if (lane == 0) {                               // TMA clips rows >= m and columns >= n
-                tc::tma_store_2d(&qmap, qs, g * QT_G + h * 8, (int)((blockIdx.x + (int64_t)tt * gridDim.x) * QT_M + dq * 32));
+                const int qrow = (int)((blockIdx.x + (int64_t)tt * gridDim.x) * QT_M + dq * 32);
+                if (CM) tc::tma_store_2d(&qmap, qs, qrow, g * QT_G + h * 8);
+                else tc::tma_store_2d(&qmap, qs, g * QT_G + h * 8, qrow);
                 tc::bulk_commit();
               }
             }
@@ -372,9 +455,10 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
         const uint32_t lv = lb + buf * (QT_LEV * QT_G) + dc0;
         // row scale read before the buffer is released: the rexp ring slot is reused only after
         // later MMAs, which wait on this release
-        const int ei = rexp[(tt & 3) * QT_M + row_l];
-        const int rbits = (ei + 75) << 23;
-        const bool fast = __all_sync(0xffffffffu, ei + crange[0] + 75 >= 1 && ei + crange[1] + 75 <= 254);
+        const int ei = rexp[(tt % RXD) * QT_M + row_l];
+        const float rs = __int_as_float((ei + crange[0] + 75) << 23);     // 2^(e_i + min e_j - 52), used if fast
+        const bool fast = __all_sync(0xffffffffu, ei + crange[0] + 75 >= 1 && ei + crange[1] + 75 <= 254 &&
+                                                      crange[1] - crange[0] <= 127);
         // this warp's 32 rows x DC columns (fp32) are staged in shared memory (16-column rows: plain
         // 64-byte rows; 32-column rows: 128-byte swizzle, chunk c of row r at c ^ (r & 7) -- conflict-free
         // STS.128) as they are computed, then one 2D TMA store writes them (rows >= m, columns >= n clipped)
@@ -389,9 +473,9 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
             uint32_t lvl[QT_LEV][8];                         // all seven levels in flight before one wait
 #pragma unroll
             for (int L = 0; L < QT_LEV; ++L) tc::ld8(lv + L * QT_G + h * 8, lvl[L]);
-            const int4 c0 = *reinterpret_cast<const int4*>(cexp + g * QT_G + dc0 + h * 8);
-            const int4 c1 = *reinterpret_cast<const int4*>(cexp + g * QT_G + dc0 + h * 8 + 4);
-            const int cb[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+            int cb[8];
+            float sc[8];
+            qt_col_scales<FAST>(cexp, csf, g * QT_G + dc0 + h * 8, cb, sc);
             tc::wait_ld();
             if (h == DC / 8 - 1) {                           // TMEM buffer free; the stores below need no TMEM
               asm volatile("tcgen05.fence::before_thread_sync;\n");
@@ -402,16 +486,22 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
               const long long t = qt_combine<KMAX <= 64>(lvl[0][c], lvl[1][c], lvl[2][c], lvl[3][c], lvl[4][c], lvl[5][c], lvl[6][c]);
-              if constexpr (FAST) o[c] = __ll2float_rn(t) * __int_as_float(rbits + (cb[c] << 23));
+              if constexpr (FAST) o[c] = __ll2float_rn(t) * (rs * sc[c]);   // exact power-of-two factor (normal: fast)
               else o[c] = qt_scale_slow(t, ei, cb[c]);
             }
+            if constexpr (CM) {                              // [DC columns][32 rows]: conflict-free STS.32
 #pragma unroll
-            for (int c = 0; c < 8; c += 4) {
-              const int ch = h * 2 + (c >> 2);                // 16-byte chunk of the row
-              // 128-byte rows (DC = 32): TMA SWIZZLE_128B, chunk ch at ch ^ (r & 7); 64-byte rows (DC = 16): SWIZZLE_64B,
-              // chunk ch at ch ^ ((r >> 1) & 3) -- each 8-lane phase of the STS.128 hits 8 distinct bank groups
-              const int off = DC == 32 ? lane * 128 + ((ch ^ (lane & 7)) << 4) : lane * 64 + ((ch ^ ((lane >> 1) & 3)) << 4);
-              *reinterpret_cast<float4*>(qs + off) = make_float4(o[c], o[c + 1], o[c + 2], o[c + 3]);
+              for (int c = 0; c < 8; ++c) reinterpret_cast<float*>(qs)[(h * 8 + c) * 32 + lane] = o[c];
+              cm_tail(o, g * QT_G + dc0 + h * 8, (blockIdx.x + (int64_t)tt * gridDim.x) * QT_M + row_l);
+            } else {
+#pragma unroll
+              for (int c = 0; c < 8; c += 4) {
+                const int ch = h * 2 + (c >> 2);                // 16-byte chunk of the row
+                // 128-byte rows (DC = 32): TMA SWIZZLE_128B, chunk ch at ch ^ (r & 7); 64-byte rows (DC = 16): SWIZZLE_64B,
+                // chunk ch at ch ^ ((r >> 1) & 3) -- each 8-lane phase of the STS.128 hits 8 distinct bank groups
+                const int off = DC == 32 ? lane * 128 + ((ch ^ (lane & 7)) << 4) : lane * 64 + ((ch ^ ((lane >> 1) & 3)) << 4);
+                *reinterpret_cast<float4*>(qs + off) = make_float4(o[c], o[c + 1], o[c + 2], o[c + 3]);
+              }
             }
           }
         };
@@ -423,7 +513,9 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
         __syncwarp();
         if (lane == 0 && !(dbg & 4)) {
-          tc::tma_store_2d(&qmap, qs, g * QT_G + dc0, (int)((blockIdx.x + (int64_t)tt * gridDim.x) * QT_M + dq * 32));
+          const int qrow = (int)((blockIdx.x + (int64_t)tt * gridDim.x) * QT_M + dq * 32);
+          if (CM) tc::tma_store_2d(&qmap, qs, qrow, g * QT_G + dc0);
+          else tc::tma_store_2d(&qmap, qs, g * QT_G + dc0, qrow);
           tc::bulk_commit();
           if (trole >= 0) trace(trole, tt, 3);
         }
@@ -440,23 +532,30 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
     // waiting for the digit slot, so the HBM latency overlaps the MMAs of the tile before.
     const int dt = tid - 32 * (2 + Cf::RW);
     const int lg_map = lg_n <= 2 ? lg_n : (lg_n <= 4 ? 4 : 8), rpw = 32 / lg_map;
+    const int lsh = 31 - __clz(rpw);
     const int ntask = (dbg & 2) ? 0 : QT_M * lg_map;
     auto task_pos = [&](int task, int& lg, int& i) {
       const int w = task >> 5, l = task & 31;
-      lg = l / rpw; i = w * rpw + (l % rpw);
+      lg = l >> lsh; i = (w << lsh) + (l & (rpw - 1));           // rpw = 2^lsh
     };
     // the six signed base-256 digits of round(x 2^(46 - e)), packed 4 columns per word, for 16 x
     auto digit_words = [&](const float* x, int e, uint32_t (&W)[QT_DA][4]) {
-      const double sx = ldexp(1.0, 128 + 46 - e);
+      // 2^(46 - e) built from its exponent field (e in [-126, 128]: always a normal double)
+      const double sx = __hiloint2double((1023 + 46 - e + (RCQ_SOLVE_F2F ? 0 : 128)) << 20, 0);
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         uint32_t hw[4], lw[4];
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
+          // one exact F2F.F64.F32 (conversion pipe) instead of three integer-pipe instructions building the double
+#if RCQ_SOLVE_F2F
+          const double t = fma((double)x[q * 4 + kk], sx, kMagic + (double)0x8080808080ull);
+#else
           const uint32_t ub = __float_as_uint(x[q * 4 + kk]);
           uint32_t h;                                                                        // x 2^-128: one LOP3
           asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(h) : "r"((uint32_t)((int32_t)ub >> 3)), "r"(0x8FFFFFFFu), "r"(0x30000000u));
           const double t = fma(__hiloint2double((int)h, (int)(ub << 29)), sx, kMagic + (double)0x8080808080ull);
+#endif
           hw[kk] = (uint32_t)__double2hiint(t);                                              // F + C, 48 bits
           lw[kk] = (uint32_t)__double2loint(t);
         }
@@ -471,15 +570,32 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
     auto digits = [&](int task, int tt, unsigned char* at, const float* x) {
       int lg, i;
       task_pos(task, lg, i);
-      uint32_t mx = 0u;
+      float mf = 0.0f;                                     // max |x|, NaN-propagating: 8 FMNMX3.NAN with |.| operands
 #pragma unroll
-      for (int c = 0; c < 16; ++c) mx = max(mx, __float_as_uint(x[c]) & 0x7FFFFFFFu);
+      for (int c = 0; c < 16; c += 2)
+        asm("max.NaN.f32 %0, %0, %1, %2;" : "+f"(mf) : "f"(fabsf(x[c])), "f"(fabsf(x[c + 1])));
+      uint32_t mx = __float_as_uint(mf);                   // NaN -> 0x7FFFFFFF
       for (int o = rpw; o < 32; o <<= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       // e_i: smallest e with max |x| < 2^e.  Inside rcholqr_factor the sketch has already rejected
       // NaN/Inf; a direct tri_solve call reports them here (Q is then not meaningful)
       if (mx >= 0x7F800000u) atomicOr(status, kStNonfinite);
       const int e = mx == 0u ? 0 : (mx < 0x00800000u ? -126 : (int)(mx >> 23) - 126);
-      if (lg == 0) rexp[(tt & 3) * QT_M + i] = e;
+      if (lg == 0) rexp[(tt % RXD) * QT_M + i] = e;
+      uint32_t W[QT_DA][4];
+      digit_words(x, e, W);
+#pragma unroll
+      for (int a = 0; a < QT_DA; ++a)
+        *reinterpret_cast<uint4*>(at + a * QT_A_TILE + lg * (QT_M * 16) + i * 16) =
+            make_uint4(W[a][0], W[a][1], W[a][2], W[a][3]);
+    };
+    // column-major raw stage [column][128 rows]: warp-task w = (32-row block, 16-column group), lane = row, so
+    // the 16 LDS.32 of a task and its digit STS.128 are conflict-free; the row scale comes from the loader warp
+    auto digits_cm = [&](int w, int tt, unsigned char* at, const float* raw) {
+      const int lg = w % lg_n, i = (w / lg_n) * 32 + lane;
+      float x[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) x[c] = raw[(lg * 16 + c) * QT_M + i];
+      const int e = rexp[(tt % RXD) * QT_M + i];
       uint32_t W[QT_DA][4];
       digit_words(x, e, W);
 #pragma unroll
@@ -495,11 +611,19 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
         if (dt == 0) trace(4, tt, 0);
         if (tt >= QT_DIG) tc::mbar_wait(&dempty[s], (uint32_t)(((tt / QT_DIG) - 1) & 1));
         if (dt == 0) trace(4, tt, 1);
-        tc::mbar_wait(&rfull[sr], (uint32_t)((tt / QT_RAW) & 1));
+        tc::mbar_wait(CM ? &sfull[sr] : &rfull[sr], (uint32_t)((tt / QT_RAW) & 1));
         if (dt == 0) trace(4, tt, 2);
         const float* raw = raw_base + (size_t)sr * QT_M * QT_RS_MAX;
         const int rs = kpad + 4;                                         // raw row pitch
-        for (int task = dt; task < ntask; task += 32 * Cf::DW) {
+        // the tile's NW = 4 lg_map warp-tasks (32 lanes x 16 columns each) are dealt round-robin to the DW
+        // digit warps starting at a warp that rotates with the tile: NW is not a multiple of DW (16 over 10),
+        // so a fixed start would leave the same warps with the extra task on every tile (the digit stages
+        // let a lightly loaded warp run ahead into the next tile, which evens the load out)
+        const int nw = ntask >> 5, dw = dt >> 5;
+        const int off = RCQ_SOLVE_ROT ? (int)(((unsigned)tt * (unsigned)(nw % Cf::DW)) % Cf::DW) : 0;
+        for (int w = (dw + Cf::DW - off) % Cf::DW; w < nw; w += Cf::DW) {
+          if constexpr (CM) { digits_cm(w, tt, at, raw); continue; }
+          const int task = w * 32 + lane;
           int lg, i;
           task_pos(task, lg, i);
           float x[16];
@@ -524,7 +648,10 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
             const int64_t row = r0 + (dw + QT_DWARPS * b) * 8 + (lane & 7);
             const int c0 = 64 * h + 16 * lgp;
             const float* xr = X + row * ldx + c0;
-            if (row < m && c0 + 16 <= n) {
+            if constexpr (CM) {                              // column-major: element (row, c0 + c) at X[(c0 + c) ldx + row]
+#pragma unroll
+              for (int c = 0; c < 16; ++c) xo[b][c] = (row < m && c0 + c < n) ? __ldg(X + (int64_t)(c0 + c) * ldx + row) : 0.0f;
+            } else if (row < m && c0 + 16 <= n) {
 #pragma unroll
               for (int c = 0; c < 16; c += 4) {
                 const float4 f = __ldg(reinterpret_cast<const float4*>(xr + c));
@@ -546,15 +673,16 @@ solve_tc_kernel(const __grid_constant__ CUtensorMap xmap, const __grid_constant_
           if (h == 0) {
 #pragma unroll
             for (int b = 0; b < 2; ++b) {
-              uint32_t mx = 0u;
+              float mf = 0.0f;                             // NaN-propagating max |x| (FMNMX3.NAN)
 #pragma unroll
               for (int c = 0; c < 16; ++c)
-                mx = max(mx, max(__float_as_uint(xh0[b][c]) & 0x7FFFFFFFu, __float_as_uint(xh1[b][c]) & 0x7FFFFFFFu));
+                asm("max.NaN.f32 %0, %0, %1, %2;" : "+f"(mf) : "f"(fabsf(xh0[b][c])), "f"(fabsf(xh1[b][c])));
+              uint32_t mx = __float_as_uint(mf);
               mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
               mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
               if (mx >= 0x7F800000u) atomicOr(status, kStNonfinite);   // tri_solve on NaN/Inf X
               ee[b] = mx == 0u ? 0 : (mx < 0x00800000u ? -126 : (int)(mx >> 23) - 126);
-              if (lgp == 0) rexp[(tt & 3) * QT_M + (dw + QT_DWARPS * b) * 8 + (lane & 7)] = ee[b];
+              if (lgp == 0) rexp[(tt % RXD) * QT_M + (dw + QT_DWARPS * b) * 8 + (lane & 7)] = ee[b];
             }
           }
           unsigned char* ah = abase + (size_t)sh * SLOT;
@@ -610,8 +738,9 @@ using EncodeTiledFn2 = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 // W = R^{-1} already in Winv (n x n fp64).  ws: workspace of solve_tc_workspace(n) bytes.
+// colmajor: X and Q column-major with leading dimensions ldx, ldq >= m (native kernels, no transposes).
 cudaError_t launch_solve_tc(const double* Winv, int n, const float* X, int64_t m, int64_t ldx, float* Q, int64_t ldq,
-                            void* ws, int* status, int sms, cudaStream_t st) {
+                            void* ws, int* status, int sms, cudaStream_t st, bool colmajor) {
   if (m == 0) return cudaSuccess;
   if (!solve_tc_supported(X, m, ldx, Q, ldq)) return cudaErrorNotSupported;
   static EncodeTiledFn2 enc = [] {
@@ -631,21 +760,29 @@ cudaError_t launch_solve_tc(const double* Winv, int n, const float* X, int64_t m
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   CUtensorMap map;
-  const cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)m};
+  // row-major: dims (columns, rows), box (K + 4 zero-padded columns, 128 rows); column-major: dims (rows, columns),
+  // box (128 rows, K columns)
+  const cuuint64_t dims[2] = {(cuuint64_t)(colmajor ? m : n), (cuuint64_t)(colmajor ? n : m)};
   const cuuint64_t strides[1] = {(cuuint64_t)ldx * 4};
-  const cuuint32_t box[2] = {(cuuint32_t)std::min(kpad, 64) + 4, QT_M}, estr[2] = {1, 1};   // + 4 zero-filled pad columns
+  const cuuint32_t estr[2] = {1, 1};
+  const cuuint32_t box[2] = {colmajor ? (cuuint32_t)QT_M : (cuuint32_t)std::min(kpad, 64) + 4,
+                             colmajor ? (cuuint32_t)std::min(kpad, 64) : (cuuint32_t)QT_M};
   if (enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(X), dims, strides, box, estr,
           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   CUtensorMap qmapd;
-  const cuuint64_t qdims[2] = {(cuuint64_t)n, (cuuint64_t)m};
+  // column-major: rows m & ~3 .. m - 1 are written by plain stores (cm_tail), see there
+  if (colmajor && m < 4) return cudaErrorNotSupported;
+  const cuuint64_t qdims[2] = {(cuuint64_t)(colmajor ? (m & ~(int64_t)3) : n), (cuuint64_t)(colmajor ? n : m)};
   const cuuint64_t qstrides[1] = {(cuuint64_t)ldq * 4};
   const bool half = kpad > 64;                       // QCfg<128>::HALF: 8-column store boxes
   const int dcols = QCfg<64>::DCOLS;                 // n <= 64: columns per drain warp
-  const cuuint32_t qbox[2] = {half ? 8u : (cuuint32_t)dcols, 32};
+  const cuuint32_t qcols = half ? 8u : (cuuint32_t)dcols;
+  const cuuint32_t qbox[2] = {colmajor ? 32u : qcols, colmajor ? qcols : 32u};   // column-major: [columns][32 rows], no swizzle
   if (enc(&qmapd, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Q, qdims, qstrides, qbox, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-          half ? CU_TENSOR_MAP_SWIZZLE_32B : (dcols == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B),
+          colmajor ? CU_TENSOR_MAP_SWIZZLE_NONE
+                   : (half ? CU_TENSOR_MAP_SWIZZLE_32B : (dcols == 32 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B)),
           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
     return cudaErrorInvalidValue;
   const int64_t ntiles = (m + QT_M - 1) / QT_M;
@@ -657,8 +794,11 @@ cudaError_t launch_solve_tc(const double* Winv, int n, const float* X, int64_t m
     kern<<<grid, threads, smem, st>>>(map, qmapd, wdig, wexp, X, ldx, m, n, kpad, Q, ldq, status, dbg);
     return cudaGetLastError();
   };
-  return kpad <= 64 ? go(solve_tc_kernel<64>, QCfg<64>::SMEM, QCfg<64>::THREADS)
-                    : go(solve_tc_kernel<128>, QCfg<128>::SMEM, QCfg<128>::THREADS);
+  if (colmajor)
+    return kpad <= 64 ? go(solve_tc_kernel<64, true>, QCfg<64>::SMEM, QCfg<64>::THREADS)
+                      : go(solve_tc_kernel<128, true>, QCfg<128>::SMEM, QCfg<128>::THREADS);
+  return kpad <= 64 ? go(solve_tc_kernel<64, false>, QCfg<64>::SMEM, QCfg<64>::THREADS)
+                    : go(solve_tc_kernel<128, false>, QCfg<128>::SMEM, QCfg<128>::THREADS);
 }
 
 #ifdef RCHOLQR_ABLATION
