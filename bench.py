@@ -238,7 +238,7 @@ def _config_dict(name: str, cfg: dict, m_global: int, s_x: int) -> dict:
     return {"workload": name, "m": m_global, "n": cfg["n"], "k": cfg["k"], "sketch": cfg["sketch"],
             "x_dtype": cfg["dtype"], "cond": 10.0 ** cfg["log10_cond"],
             "l2": "inputs larger than L2 (per-rank X > 126 MiB), no flush" if m_global * cfg["n"] * s_x > 8 * L2_BYTES
-                  else "X fits in L2 on some ranks: NOT flushed (small config)"}
+                  else "flushed: 4 x L2 written between timed steps, each step its own device event pair"}
 
 
 def _i8_macs(cfg: dict, m: int, k: int) -> float:
@@ -295,6 +295,12 @@ def run(args):
     tau_rr = args.tau if args.tau > 0 else (4e-15 if dt == "f64" else 2e-7)
     rr_last = {}
 
+    # launch-bound configs (X fits in L2: C1): the chain is replayed from a CUDA graph (rcholqr_factor_graph) and
+    # L2 is flushed between timed steps, each step timed by its own event pair
+    small = m_local * n * s_x <= 8 * L2_BYTES
+    use_graph = args.algo == "rcholqr" and ws == 1 and (args.graph == "on" or (args.graph == "auto" and small))
+    flush = torch.empty(4 * L2_BYTES, dtype=torch.uint8, device=dev) if small else None
+
     def step():
         if args.algo == "rcholqr_rr":   # Alg. 7: synchronous (rank and swap decisions on the host)
             rr_last.update(plan.factor_rr(X, tau_rr, row_offset=ro, Q=Q, R=R, stream=stream))
@@ -305,7 +311,7 @@ def run(args):
         elif args.algo == "rcholqr_reduced":   # Alg. 5: synchronous
             plan.factor_reduced(X, l_red, row_offset=ro, Z=Z, R=R, stream=stream)
         else:
-            plan.factor(X, row_offset=ro, Q=Q, R=R, stream=stream, sync=False)
+            plan.factor(X, row_offset=ro, Q=Q, R=R, stream=stream, sync=False, graph=use_graph)
 
     def barrier():
         if ws > 1:
@@ -322,12 +328,22 @@ def run(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         barrier()
-        e0.record(stream)
-        for _ in range(args.steps):
-            step()
-        e1.record(stream)
-        barrier()
-    ms_local = e0.elapsed_time(e1) / args.steps
+        if small:      # per-step event pairs; a write of 4 x L2 between steps evicts X, Q and the workspaces
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+            for a, b in evs:
+                flush.fill_(1)
+                a.record(stream)
+                step()
+                b.record(stream)
+            barrier()
+            ms_local = sum(a.elapsed_time(b) for a, b in evs) / args.steps
+        else:
+            e0.record(stream)
+            for _ in range(args.steps):
+                step()
+            e1.record(stream)
+            barrier()
+            ms_local = e0.elapsed_time(e1) / args.steps
     st = plan.query_status()
     if st != rcq.OK:
         raise rcq.RCholQRError(st, "timed factor")
@@ -390,7 +406,10 @@ def run(args):
                            "peak_source": up["dmma_source"] + ": fp64-equivalent view of the exact int8 digit emulation",
                            "algorithmic": f"2*{'(k+l)' if reduced else 'k'}*m*n = {flops:.4g} flop per launch",
                            "traffic": None}
-        if up["i8_tops"]:    # the unit that actually does the work: executed int8 MACs vs the tcgen05 i8 rate
+        if flops < 2e7:      # launch-bound sizes (C1) run the single DMMA kernel (sketch.cu, gauss_tc_min_work)
+            roofs["sketch"]["kernel"] = "sketch_gauss_kernel"
+            roofs["sketch"]["peak_source"] = up["dmma_source"]
+        elif up["i8_tops"]:    # the unit that actually does the work: executed int8 MACs vs the tcgen05 i8 rate
             i8 = 2.0 * _i8_macs(cfg, m_local, k_sk) / (per_ms["sketch"] * 1e-3) / 1e12
             roofs["sketch"]["int8_view"] = {"achieved": i8, "peak": up["i8_tops"], "unit": "TOP/s",
                                             "frac": i8 / up["i8_tops"], "peak_source": up["i8_source"],
@@ -500,7 +519,7 @@ def run(args):
             "partition": {"m_local": m_local, "row_offset": ro, "parallelism": f"row-partition x{ws}, 1 all-reduce"},
             "per_kernel_ms": per_ms, "roofline": roof, "kernel_rooflines": roofs, "northstar_roofline": ns,
             "gpu_launches": plan.launches_per_factor(m_local) * args.steps,
-            "clocks": clk.summary(), "e2e": e2e}
+            "clocks": clk.summary(), "e2e": e2e, "cuda_graph": use_graph}
 
     if args.algo == "rcholqr2":
         # split Alg. 3's own steps by differences of device-timed calls on the same stream:
@@ -609,6 +628,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default=DEFAULT_CONFIG, choices=sorted(synth.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
+                    help="Alg. 2 through rcholqr_factor_graph (auto: configs whose X fits in L2, i.e. C1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)

@@ -110,6 +110,17 @@ rcholqr_status rcholqr_factor_host(rcholqr_plan plan, const void* X_host, int64_
                                    int64_t row_offset, int64_t ldx, void* Q_host, int64_t ldq,
                                    double* R_host, double* S_host, void* stream);
 
+/* rcholqr_factor_async replayed from a CUDA GRAPH: for launch-bound problems (BASELINE config C1, 10^4 x 20:
+ * every kernel of the chain runs a few microseconds, so the ~8 launches are the cost; PAPER.md:163 expects
+ * the small QR and the other small steps to "not have much impact").  The first call with a given argument
+ * tuple (X, m_local, row_offset, ldx, Q, ldq, R, S) runs the chain directly and captures it; every later call
+ * with the SAME tuple replays the captured graph with one launch on `stream`.  A different tuple re-captures
+ * (one graph is cached per plan).  The buffers' CONTENTS may change between calls, their addresses may not.
+ * Plans with an NCCL communicator, and plans with event timing enabled, launch directly (same results).
+ * ASYNCHRONOUS like rcholqr_factor_async: numerical status through rcholqr_query_status. */
+rcholqr_status rcholqr_factor_graph(rcholqr_plan plan, const void* X, int64_t m_local, int64_t row_offset,
+                                    int64_t ldx, void* Q, int64_t ldq, double* R, double* S, void* stream);
+
 /* Alg. 2 for COLUMN-MAJOR X and Q (element (i, j) at X[j * ldx + i], ldx >= m_local; the storage the
  * paper notes favours sketching).
  * NATIVE kernels (no transposes; the same two reads of X and one write of Q as the row-major path) serve

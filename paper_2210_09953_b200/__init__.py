@@ -32,7 +32,7 @@ GAUSSIAN, SPARSE_SIGN, RADEMACHER, SRHT = 0, 1, 2, 3
 F64, F32 = 0, 1
 
 # exported symbols (checked by tests/test_abi.py against include/rcholqr.h)
-SYMBOLS = ["rcholqr_create", "rcholqr_destroy", "rcholqr_factor", "rcholqr_factor_async",
+SYMBOLS = ["rcholqr_create", "rcholqr_destroy", "rcholqr_factor", "rcholqr_factor_async", "rcholqr_factor_graph",
            "rcholqr_query_status", "rcholqr_factor_host", "rcholqr_sketch", "rcholqr_small_qr",
            "rcholqr_tri_solve", "rcholqr_theta_export", "rcholqr_comm_unique_id",
            "rcholqr_comm_create", "rcholqr_comm_destroy", "rcholqr_strerror", "rcholqr_version",
@@ -77,6 +77,7 @@ def load_library():
             "rcholqr_destroy": ([V], I32),
             "rcholqr_factor": ([V, V, I64, I64, I64, V, I64, V, V, V], I32),
             "rcholqr_factor_async": ([V, V, I64, I64, I64, V, I64, V, V, V], I32),
+            "rcholqr_factor_graph": ([V, V, I64, I64, I64, V, I64, V, V, V], I32),
             "rcholqr_query_status": ([V, V], I32),
             "rcholqr_factor_host": ([V, V, I64, I64, I64, V, I64, V, V, V], I32),
             "rcholqr_factor2": ([V, V, I64, I64, I64, V, I64, V, V, I32, V], I32),
@@ -213,8 +214,10 @@ class RCholQR:
 
     # -- Algorithm 2
     def factor(self, X, row_offset: int = 0, want_S: bool = False, Q=None, R=None, S=None,
-               stream=None, sync: bool = True) -> Tuple:
-        """Q, R (and S) of X.  ``sync=False`` uses rcholqr_factor_async (status via query_status)."""
+               stream=None, sync: bool = True, graph: bool = False) -> Tuple:
+        """Q, R (and S) of X.  ``sync=False`` uses rcholqr_factor_async (status via query_status);
+        ``graph=True`` uses rcholqr_factor_graph (the chain replayed from a CUDA graph when X, Q, R, S
+        are the same buffers as in the previous call)."""
         torch = _torch()
         m, ldx = self._check_x(X)
         Q = torch.empty((m, self.n), dtype=self.dtype, device=X.device) if Q is None else Q
@@ -224,9 +227,11 @@ class RCholQR:
         ldq = self._check_out(Q, "Q", m, self.n, self.dtype)
         self._check_out(R, "R", self.n, self.n, torch.float64, exact=True)
         self._check_out(S, "S", self.k, self.n, torch.float64, exact=True)
-        fn = self._lib.rcholqr_factor if sync else self._lib.rcholqr_factor_async
+        fn = self._lib.rcholqr_factor_graph if graph else (self._lib.rcholqr_factor if sync else self._lib.rcholqr_factor_async)
         st = fn(self._h, _ptr(X), m, row_offset, ldx, _ptr(Q), ldq, _ptr(R), _ptr(S), _stream_ptr(stream))
         _check(st, "rcholqr_factor")
+        if graph and sync:
+            _check(self.query_status(stream), "rcholqr_factor_graph")
         return Q, R, S
 
     def factor_colmajor(self, Xt, row_offset: int = 0, want_S: bool = False, Qt=None, R=None, S=None, stream=None):

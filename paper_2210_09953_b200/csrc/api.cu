@@ -134,6 +134,17 @@ struct rcholqr_plan_s {
   // factor_host staging
   void* xbuf = nullptr; void* qbuf = nullptr; size_t xq_bytes = 0;
   double* rbuf = nullptr; double* sbuf = nullptr;
+  // rcholqr_factor_graph: the captured kernel chain of one argument tuple
+  struct GraphKey {
+    const void* X = nullptr; int64_t m = -1, ro = 0, ldx = 0; void* Q = nullptr; int64_t ldq = 0;
+    double* R = nullptr; double* S = nullptr;
+    bool operator==(const GraphKey& o) const {
+      return X == o.X && m == o.m && ro == o.ro && ldx == o.ldx && Q == o.Q && ldq == o.ldq && R == o.R && S == o.S;
+    }
+  } gkey;
+  cudaGraphExec_t gexec = nullptr;
+  cudaStream_t gstream = nullptr;   // capture stream (capture on the legacy default stream is not allowed)
+  unsigned gpath = 0;               // path bits of the captured chain
   bool timing = false;
   cudaEvent_t ev[7] = {};
   float last_ms[6] = {0, 0, 0, 0, 0, 0};
@@ -441,6 +452,8 @@ rcholqr_status rcholqr_destroy(rcholqr_plan p) {
   cudaFree(p->rr_R11); cudaFree(p->rr_d); cudaFree(p->rr_cpart); cudaFree(p->rr_cspart); cudaFree(p->rr_sd); cudaFree(p->rr_si);
   cudaFree(p->rr_perm); cudaFree(p->rr_qst); cudaFree(p->rr_xr); cudaFree(p->srht_d);
   if (p->status_h) cudaFreeHost(p->status_h);
+  if (p->gexec) cudaGraphExecDestroy(p->gexec);
+  if (p->gstream) cudaStreamDestroy(p->gstream);
   cudaFree(p->xbuf); cudaFree(p->qbuf); cudaFree(p->rbuf); cudaFree(p->sbuf); cudaFree(p->tbuf);
   for (int t = 0; t < 7; ++t)
     if (p->ev[t]) cudaEventDestroy(p->ev[t]);
@@ -466,6 +479,48 @@ rcholqr_status rcholqr_factor_async(rcholqr_plan p, const void* X, int64_t m, in
   rcholqr_status s2 = solve(p, X, m, ldx, Rout, Q, ldq, st, true);
   if (s2 != RCHOLQR_OK) return s2;
   if (p->timing) cudaEventRecord(p->ev[6], st);
+  return RCHOLQR_OK;
+}
+
+// Launch-bound problems (C1: 10^4 x 20, a few microseconds of work per kernel; PAPER.md:163 expects the small
+// steps to "not have much impact"): the whole chain -- status memset, sketch, reduction, small QR, triangular
+// prep, solve -- is captured once per argument tuple into a CUDA graph and replayed with ONE launch.
+rcholqr_status rcholqr_factor_graph(rcholqr_plan p, const void* X, int64_t m, int64_t ro, int64_t ldx, void* Q,
+                                    int64_t ldq, double* R, double* S, void* stream) {
+  rcholqr_status a = check_factor_args(p, X, m, ro, ldx, Q, ldq);
+  if (a != RCHOLQR_OK) return a;
+  if (p->d.nccl_comm || p->timing)   // collective / event-timed chains are launched directly
+    return rcholqr_factor_async(p, X, m, ro, ldx, Q, ldq, R, S, stream);
+  DeviceGuard dg(p->d.device);
+  cudaStream_t st = (cudaStream_t)stream;
+  rcholqr_plan_s::GraphKey key;
+  key.X = X; key.m = m; key.ro = ro; key.ldx = ldx; key.Q = Q; key.ldq = ldq; key.R = R; key.S = S;
+  if (p->gexec && key == p->gkey) {
+    p->path = p->gpath;
+    CU(cudaGraphLaunch(p->gexec, st));
+    return RCHOLQR_OK;
+  }
+  // new arguments: this call runs directly (it also sizes every lazily grown workspace, so the capture
+  // below allocates nothing), then the same chain is captured for the calls that follow
+  if (p->gexec) { cudaGraphExecDestroy(p->gexec); p->gexec = nullptr; }
+  rcholqr_status s = rcholqr_factor_async(p, X, m, ro, ldx, Q, ldq, R, S, stream);
+  if (s != RCHOLQR_OK) return s;
+  const unsigned path = p->path;
+  if (!p->gstream) CU(cudaStreamCreateWithFlags(&p->gstream, cudaStreamNonBlocking));
+  CU(cudaStreamSynchronize(st));   // the capture pass re-issues (does not run) the chain; keep it off the live buffers' timeline
+  if (cudaStreamBeginCapture(p->gstream, cudaStreamCaptureModeThreadLocal) != cudaSuccess) { cudaGetLastError(); return RCHOLQR_OK; }
+  const rcholqr_status cs = rcholqr_factor_async(p, X, m, ro, ldx, Q, ldq, R, S, p->gstream);
+  cudaGraph_t g = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(p->gstream, &g);
+  p->path = path;
+  if (cs == RCHOLQR_OK && ce == cudaSuccess && g && cudaGraphInstantiate(&p->gexec, g, 0) == cudaSuccess) {
+    p->gkey = key;
+    p->gpath = path;
+  } else {
+    cudaGetLastError();          // not capturable here: later calls keep launching directly
+    p->gexec = nullptr;
+  }
+  if (g) cudaGraphDestroy(g);
   return RCHOLQR_OK;
 }
 
@@ -975,9 +1030,10 @@ int32_t rcholqr_launches_per_factor(rcholqr_plan p, int64_t m) {
   //   sketch: [tcgen05 sketch +] the CUDA-core kernel (its guarded fallback, exits at once) + reduce
   //   QR: 1 | triangular prep (blocked prep or R^{-1}): 1 | solve: tcgen05 (W-digit prep + solve) = 2,
   //   streamed fp64 GEMMs = 2 per column block, else 1.
-  const bool tc_sketch = p->sk.sp_tc || (p->sk.kind < kSketchSparse && (p->sk.tc || p->sk.rad_tc));
+  const bool gauss_tc = p->sk.tc && 2.0 * p->d.k * (double)m * p->d.n >= gauss_tc_min_work();
+  const bool tc_sketch = p->sk.sp_tc || (p->sk.kind < kSketchSparse && (gauss_tc || p->sk.rad_tc));
   int sketch_launches = (tc_sketch ? 2 : 1) + 1;
-  if (tc_sketch && p->sk.kind < kSketchSparse && p->sk.tc && m > 0) {   // pre-split: (column maxima + digit planes + sketch) per chunk
+  if (tc_sketch && p->sk.kind < kSketchSparse && gauss_tc && m > 0) {   // pre-split: (column maxima + digit planes + sketch) per chunk
     const size_t cap = gauss_tcp_chunk_workspace(m, p->d.n, p->d.dtype, p->sk.tc_splits);
     int64_t chunk = m;
     while (chunk > 32 && gauss_tcp_workspace(chunk, p->d.n, p->d.dtype, p->sk.tc_splits) > cap) chunk = (chunk + 1) / 2;

@@ -113,6 +113,7 @@ struct TrsmLaunch {
 
 // Host-side launchers (defined in sketch.cu / qr.cu / trsm.cu).
 SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms, size_t smem_optin);
+double gauss_tc_min_work();   // 2kmn below which the Gaussian sketch takes the single DMMA kernel (launch-bound sizes)
 cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
                           int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* partc, double* P,
                           int* status, int* flag, void* xdig, size_t xdig_bytes, cudaStream_t st, cudaEvent_t ev_mid,

@@ -421,29 +421,49 @@ sketch_sparse_reg_kernel(const TX* __restrict__ X, int64_t m, int n, int64_t ldx
   }
 }
 
-// Fixed-order sum of the per-split partials, one scaling, non-finite detection.
+// Fixed-order compensated sum of the per-split partials, one scaling, non-finite detection.
 // Entries idx < kn_first are scaled by `scale`, the rest by `scale2` (the (k + l)-row sketch of Alg. 5:
 // Theta rows by 1/sqrt(k), extractor rows by 1/sqrt(l)).
+// Each warp sums 4 consecutive entries: lane = 4 * sl + il takes splits sl, sl + 8, ... of entry idx0 + il
+// (a split's 4 entries are one 32-byte sector), then the 8 split lanes combine by an xor butterfly of TwoSums
+// (a fixed tree: deterministic, and every lane ends with the same value).  The serial loop over all
+// splits this replaces was a chain of dependent-latency loads (C1: 29 us for 800 entries).
 __global__ void sketch_reduce_kernel(const double* __restrict__ part, const double* __restrict__ partc, int splits,
                                      int64_t kn, double scale, int64_t kn_first, double scale2,
                                      double* __restrict__ P, int* status, const int* flag, int* flag_seen) {
   // record (for rcholqr_last_path) that a tensor-core sketch raised its overflow flag and the guarded
   // CUDA-core kernel recomputed the partials
   if (flag && flag_seen && blockIdx.x == 0 && threadIdx.x == 0 && *flag) atomicOr(flag_seen, 1);
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < kn;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    double s = 0.0, c = 0.0;                    // compensated (TwoSum) sum over the splits
-    for (int sp = 0; sp < splits; ++sp) {
-      const double v = part[(size_t)sp * kn + idx];
-      const double t = s + v;
-      const double bb = t - s;
-      c += (s - (t - bb)) + (v - bb);
-      s = t;
-      if (partc) c += partc[(size_t)sp * kn + idx];
+  const int lane = threadIdx.x & 31, il = lane & 3, sl = lane >> 2;
+  const int64_t warp0 = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t idx0 = warp0 * 4; idx0 < kn; idx0 += nwarps * 4) {
+    const int64_t idx = idx0 + il;
+    double s = 0.0, c = 0.0;                    // compensated (TwoSum) sum over this lane's splits
+    if (idx < kn) {
+#pragma unroll 4
+      for (int sp = sl; sp < splits; sp += 8) {
+        const double v = part[(size_t)sp * kn + idx];
+        const double t = s + v;
+        const double bb = t - s;
+        c += (s - (t - bb)) + (v - bb);
+        s = t;
+        if (partc) c += partc[(size_t)sp * kn + idx];
+      }
     }
-    s = (s + c) * (idx < kn_first ? scale : scale2);
-    P[idx] = s;
-    if (!isfinite(s)) atomicOr(status, kStNonfinite);
+#pragma unroll
+    for (int off = 4; off < 32; off <<= 1) {
+      const double s2 = __shfl_xor_sync(0xffffffffu, s, off), c2 = __shfl_xor_sync(0xffffffffu, c, off);
+      const double t = s + s2;
+      const double bb = t - s;
+      c = (c + c2) + ((s - (t - bb)) + (s2 - bb));
+      s = t;
+    }
+    if (sl == 0 && idx < kn) {
+      s = (s + c) * (idx < kn_first ? scale : scale2);
+      P[idx] = s;
+      if (!isfinite(s)) atomicOr(status, kStNonfinite);
+    }
   }
 }
 
@@ -679,6 +699,11 @@ static cudaError_t launch_gauss_typed(const SketchLaunch& L, const void* X, int6
   }
 }
 
+double gauss_tc_min_work() {
+  const char* e = getenv("RCHOLQR_GAUSS_TC_MIN_WORK");     // tests: 0 sends the tiniest shapes through tcgen05 too
+  return e ? atof(e) : 2.0e7;
+}
+
 cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
                           int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* partc, double* P,
                           int* status, int* flag, void* xdig, size_t xdig_bytes, cudaStream_t st, cudaEvent_t ev_mid,
@@ -746,7 +771,9 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
   } else {
     int splits = L.splits;
     const int* guard = nullptr;
-    const bool tc = L.tc && gauss_tc_aligned(X, dtype, n, ldx);
+    // launch-bound problems (C1: 2kmn = 1.6e7 flops) take the single DMMA kernel: the pre-split tcgen05 path's three
+    // launches cost more than they save there (C1 sketch: 17 vs 41 us)
+    const bool tc = L.tc && gauss_tc_aligned(X, dtype, n, ldx) && 2.0 * k * (double)m * n >= gauss_tc_min_work();
     // (SRHT: the tcgen05 E tile splits the global row as (multiple of 32) + lane, so row_offset % 32 == 0)
     if (L.rad_tc && sparse_tc_aligned(X, dtype, m, ldx) && (L.rad != 2 || row_offset % 32 == 0)) {
       // dense +-1 E tile on the sparse sketch's tcgen05 kernel (zeta = 0); it writes no compensation
@@ -809,8 +836,8 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
   if (e != cudaSuccess) return e;
   if (ev_mid) cudaEventRecord(ev_mid, st);
   const int64_t kn = (int64_t)k * n;
-  const int threads = 256;
-  const int blocks = (int)std::min<int64_t>((kn + threads - 1) / threads, 4096);
+  const int threads = 256;                                   // 8 warps x 4 entries per block pass
+  const int blocks = (int)std::min<int64_t>((kn + 31) / 32, 4096);
   const bool sparse = L.kind == kSketchSparse || L.kind == kSketchSparseReg;
   // Gaussian rows >= k_first (Alg. 5's extractor rows) take 1/sqrt(k - k_first) instead of 1/sqrt(k)
   double scale2 = scale;
@@ -829,7 +856,7 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
 cudaError_t launch_reduce(const double* part, int splits, int64_t kn, double scale, double* P, int* status,
                           cudaStream_t st) {
   const int threads = 256;
-  const int blocks = (int)std::min<int64_t>((kn + threads - 1) / threads, 4096);
+  const int blocks = (int)std::min<int64_t>((kn + 31) / 32, 4096);
   sketch_reduce_kernel<<<blocks, threads, 0, st>>>(part, nullptr, splits, kn, scale, kn, scale, P, status, nullptr,
                                                    nullptr);
   return cudaGetLastError();

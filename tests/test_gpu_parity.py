@@ -73,11 +73,23 @@ SKETCH_CASES = [
 ]
 
 
+@pytest.mark.parametrize("force_tc", [False, True])
 @pytest.mark.parametrize("m,n,k,dt,sk,c", SKETCH_CASES)
-def test_sketch_parity(cuda, m, n, k, dt, sk, c):
+def test_sketch_parity(cuda, monkeypatch, m, n, k, dt, sk, c, force_tc):
+    # force_tc: Gaussian problems below 2kmn = 2e7 take the DMMA kernel by default (launch-bound sizes); with the
+    # threshold at 0 the tiniest shapes (single row, m < one chunk) go through the tcgen05 pre-split path as well
+    small = sk == "gaussian" and 2.0 * k * m * n < 2e7
+    if force_tc:
+        if not small:
+            pytest.skip("already on the tcgen05 path")
+        monkeypatch.setenv("RCHOLQR_GAUSS_TC_MIN_WORK", "0")
     X = synth.make_X(m, n, c, dt)
     plan = _plan(n, k, dt, sk)
     Pg = _np(plan.sketch(_t(X)))
+    if small and not force_tc:
+        assert not plan.last_path() & rcq.PATH_SKETCH_TC, plan.last_path()
+    elif (m, n, k) == (10_000, 20, 40):
+        assert plan.last_path() & rcq.PATH_SKETCH_TC, plan.last_path()
     Po = oracle.sketch(X, k, sketch=oracle.GAUSSIAN if sk == "gaussian" else oracle.SPARSE_SIGN, zeta=8)
     assert _rel(Pg, Po) <= 1e-12, _rel(Pg, Po)
 
@@ -337,12 +349,15 @@ E2E = [
 ]
 
 
-def _assert_tc_path(plan, dt, n):
+def _assert_tc_path(plan, dt, n, small_gauss=False):
     """The tcgen05 kernels (not the guarded CUDA-core fallbacks) computed the sketch, and the tall solve
     ran on tcgen05 for fp32 X with n <= 128, else on the DMMA substitution (rcholqr_last_path)."""
     path = plan.last_path()
-    assert path & rcq.PATH_SKETCH_TC, path
-    assert not path & (rcq.PATH_SKETCH_FALLBACK | rcq.PATH_SKETCH_CUDA_CORE), path
+    if small_gauss:    # launch-bound Gaussian problems (2kmn < 2e7, i.e. C1) take the single DMMA sketch kernel by design
+        assert path & rcq.PATH_SKETCH_CUDA_CORE and not path & rcq.PATH_SKETCH_TC, path
+    else:
+        assert path & rcq.PATH_SKETCH_TC, path
+        assert not path & (rcq.PATH_SKETCH_FALLBACK | rcq.PATH_SKETCH_CUDA_CORE), path
     want = rcq.PATH_SOLVE_TC if (dt == "f32" and n <= 128) else rcq.PATH_SOLVE_DMMA
     assert path & want, path
 
@@ -372,7 +387,7 @@ def test_factor_parity(cuda, name, m, n, k, dt, sk, c):
     X = synth.make_X(m, n, c, dt)
     plan = _plan(n, k, dt, sk)
     Q, R, S = plan.factor(_t(X), want_S=True)
-    _assert_tc_path(plan, dt, n)
+    _assert_tc_path(plan, dt, n, small_gauss=(sk == "gaussian" and 2.0 * k * m * n < 2e7))
     Qg, Rg, Sg = _np(Q), _np(R), _np(S)
     _check_e2e(X, k, sk, c, Qg, Rg, plan, dt)
     assert np.linalg.norm(Sg.T @ Sg - np.eye(n)) <= 50 * n * U64
