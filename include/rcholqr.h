@@ -263,6 +263,8 @@ rcholqr_status rcholqr_last_timings(rcholqr_plan plan, float out_ms[6]);
  *   COLSQ_FUSED      (rcholqr_factor_rr / _rr2) D = diag ||X(:,j)|| came out of the sketch's own pass over X
  *                    (the pre-split Gaussian digit split), no separate column-norm pass
  *   COLMAJOR_NATIVE  (rcholqr_factor_colmajor) the native column-major kernels served the call (no transposes)
+ *   SKETCH_FWHT      the SRHT sketch ran as a blocked fast Walsh-Hadamard transform (m n log2 m,
+ *                    here 10 + k/1024 adds per element of X) instead of a dense +-1 product
  * *out receives the bits.  SYNCHRONIZES on `stream` (reads the device overflow word).  Errors:
  * E_INVALID for a NULL plan or out. */
 #define RCHOLQR_PATH_SKETCH_TC 1u
@@ -273,6 +275,7 @@ rcholqr_status rcholqr_last_timings(rcholqr_plan plan, float out_ms[6]);
 #define RCHOLQR_PATH_SOLVE_DMMA 32u
 #define RCHOLQR_PATH_COLSQ_FUSED 64u
 #define RCHOLQR_PATH_COLMAJOR_NATIVE 128u /* rcholqr_factor_colmajor: native column-major kernels, no layout adapter */
+#define RCHOLQR_PATH_SKETCH_FWHT 256u /* SRHT sketch computed by the blocked fast Walsh-Hadamard transform (m n log2 1024) */
 rcholqr_status rcholqr_last_path(rcholqr_plan plan, uint32_t* out, void* stream);
 
 #ifdef __cplusplus

@@ -42,7 +42,7 @@ SYMBOLS = ["rcholqr_create", "rcholqr_destroy", "rcholqr_factor", "rcholqr_facto
 
 # rcholqr_last_path bits (include/rcholqr.h)
 PATH_SKETCH_TC, PATH_SKETCH_PRESPLIT, PATH_SKETCH_CUDA_CORE, PATH_SKETCH_FALLBACK = 1, 2, 4, 8
-PATH_SOLVE_TC, PATH_SOLVE_DMMA, PATH_COLSQ_FUSED, PATH_COLMAJOR_NATIVE = 16, 32, 64, 128
+PATH_SOLVE_TC, PATH_SOLVE_DMMA, PATH_COLSQ_FUSED, PATH_COLMAJOR_NATIVE, PATH_SKETCH_FWHT = 16, 32, 64, 128, 256
 
 
 class _Desc(ctypes.Structure):

@@ -45,7 +45,7 @@ enum : int { kStNonfinite = 1, kStSingular = 2 };
 enum : unsigned { kPathSketchTC = RCHOLQR_PATH_SKETCH_TC, kPathSketchPresplit = RCHOLQR_PATH_SKETCH_PRESPLIT,
                   kPathSketchCudaCore = RCHOLQR_PATH_SKETCH_CUDA_CORE, kPathSketchFallback = RCHOLQR_PATH_SKETCH_FALLBACK,
                   kPathSolveTC = RCHOLQR_PATH_SOLVE_TC, kPathSolveDmma = RCHOLQR_PATH_SOLVE_DMMA,
-                  kPathColmajorNative = RCHOLQR_PATH_COLMAJOR_NATIVE };
+                  kPathColmajorNative = RCHOLQR_PATH_COLMAJOR_NATIVE, kPathSketchFwht = RCHOLQR_PATH_SKETCH_FWHT };
 
 // One FP64 tensor-core MMA: D(16x8) += A(16x4) B(4x8)  (DMMA on sm_100a; tcgen05 has no f64 kind).
 // Fragments (PTX ISA, mma.m16n8k4 .f64): g = lane/4, t = lane%4;
@@ -83,9 +83,12 @@ struct SketchLaunch {
   // sparse-sign: the tcgen05 kernel of sketch_tc.cu in front of the CUDA-core kind above (its guarded fallback)
   int sp_tc = 0;
   const uint64_t* srht_s = nullptr;          // SRHT: the k sampled Hadamard rows (plan-owned device array)
+  // SRHT by the blocked fast Walsh-Hadamard transform (srht_fwht.cu; k <= 1024), in front of the dense kernels
+  int fwht = 0, fwht_splits = 0;
   int max_splits() const {
     int s = tc && tc_splits > splits ? tc_splits : splits;
-    return rad_tc && rad_splits > s ? rad_splits : s;
+    s = rad_tc && rad_splits > s ? rad_splits : s;
+    return fwht && fwht_splits > s ? fwht_splits : s;
   }
 };
 int gauss_tc_kt(int dtype);   // Theta rows per tcgen05 Gaussian-sketch tile (X columns per tile: 128)
@@ -113,6 +116,11 @@ struct TrsmLaunch {
 
 // Host-side launchers (defined in sketch.cu / qr.cu / trsm.cu).
 SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms, size_t smem_optin);
+bool srht_fwht_applicable(int k);
+int srht_fwht_splits(int n, int sms);
+cudaError_t launch_srht_fwht(const void* X, int dtype, int64_t m, int n, int64_t ldx, int64_t row_offset, int k,
+                             uint64_t seed, const uint64_t* srht_s, int splits_max, double* part, double* partc,
+                             int* splits_used, cudaStream_t st);
 double gauss_tc_min_work();   // 2kmn below which the Gaussian sketch takes the single DMMA kernel (launch-bound sizes)
 cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64_t m, int n, int64_t ldx,
                           int64_t row_offset, int k, int zeta, uint64_t seed, double* part, double* partc, double* P,

@@ -653,6 +653,10 @@ SketchLaunch plan_sketch(int k, int n, int dtype, int sketch, int zeta, int sms,
   L.tc = 0;
   if (sketch == RCHOLQR_RADEMACHER || sketch == RCHOLQR_SRHT) {   // DMMA kernel drawing +-1, dense tcgen05 in front
     L.rad = sketch == RCHOLQR_SRHT ? 2 : 1;
+    if (L.rad == 2 && srht_fwht_applicable(k)) {           // blocked fast Walsh-Hadamard transform (srht_fwht.cu)
+      L.fwht = 1;
+      L.fwht_splits = srht_fwht_splits(n, sms);
+    }
     if (sparse_tc_applicable(k, n, 1) && !getenv("RCHOLQR_RADEMACHER_DMMA")) {
       L.rad_tc = 1;
       L.rad_splits = sms;
@@ -768,6 +772,14 @@ cudaError_t launch_sketch(const SketchLaunch& L, const void* X, int dtype, int64
     };
     e = colmajor ? cudaSuccess : (dtype == RCHOLQR_F64 ? launch((double*)nullptr) : launch((float*)nullptr));
     scale = 1.0 / std::sqrt((double)zeta);
+  } else if (L.fwht && !colmajor &&
+             (e = launch_srht_fwht(X, dtype, m, n, ldx, row_offset, k, seed, L.srht_s, L.fwht_splits, part, partc,
+                                   &reduce_splits, st)) != cudaErrorNotSupported) {
+    // SRHT by the blocked fast Walsh-Hadamard transform (srht_fwht.cu): fp64 butterflies with
+    // compensated block sums, no digit scales and so no overflow guard / fallback
+    if (e != cudaSuccess) return e;
+    pb |= kPathSketchFwht;
+    scale = 1.0 / std::sqrt((double)k);
   } else {
     int splits = L.splits;
     const int* guard = nullptr;

@@ -52,9 +52,15 @@ def test_theta_export_bit_exact(cuda, k, m, ro, seed):
     (40_000, 100, 200, "f32"),     # n > 64: DMMA path drawing +-1
     (333, 17, 34, "f64"),          # fewer rows than CTAs, ragged
 ])
-def test_sketch_parity(cuda, m, n, k, dt):
+@pytest.mark.parametrize("dense", [True, False])
+def test_sketch_parity(cuda, monkeypatch, m, n, k, dt, dense):
+    # dense: the +-1 kernels at every k (by default k > 128 runs the fast Walsh-Hadamard transform, srht_fwht.cu)
+    if dense:
+        monkeypatch.setenv("RCHOLQR_SRHT_DENSE", "1")
     X = synth.make_X(m, n, 5.0, dt)
-    Pg = _np(_plan(n, k, dt).sketch(_t(X), row_offset=24_864))
+    plan = _plan(n, k, dt)
+    Pg = _np(plan.sketch(_t(X), row_offset=24_864))
+    assert bool(plan.last_path() & rcq.PATH_SKETCH_FWHT) == (not dense and k > 128 and (n * X.itemsize) % 16 == 0)
     Po = oracle.sketch(X, k, sketch=oracle.SRHT, row_offset=24_864)
     assert _rel(Pg, Po) <= 1e-12, _rel(Pg, Po)
 

@@ -21,9 +21,12 @@ ap.add_argument("--iters", type=int, default=40)
 ap.add_argument("--warm", type=int, default=15)
 ap.add_argument("--what", default="solve,sketch")
 ap.add_argument("--tag", default="")
+ap.add_argument("--sketch", default="")
 a = ap.parse_args()
 cfg = synth.config(a.config)
 m = a.m or cfg["m"]
+if a.sketch:
+    cfg["sketch"] = a.sketch
 X = synth.make_X_torch(m, cfg["n"], cfg["log10_cond"], cfg["dtype"])
 plan = rcq.RCholQR(n=cfg["n"], k=cfg["k"], dtype=X.dtype, sketch=cfg["sketch"], nnz_per_col=cfg["nnz"])
 P = plan.sketch(X)
@@ -65,12 +68,13 @@ def timed(fn):
             "power_w_max": round(max(s.pw), 1) if s.pw else None}
 
 
-out = {"tag": a.tag, "config": a.config, "m": m}
+out = {"tag": a.tag, "config": a.config, "m": m, "sketch": cfg["sketch"]}
 for w in a.what.split(","):
     if w == "solve":
         out["solve"] = timed(lambda: plan.tri_solve(X, R, Q=Q))
     elif w == "sketch":
-        out["sketch"] = timed(lambda: plan.sketch(X))
+        out["sketch_ms"] = timed(lambda: plan.sketch(X))
+        out["sketch_ms"]["path"] = plan.last_path()
     elif w == "factor":
         out["factor"] = timed(lambda: plan.factor(X, Q=Q))
     elif w == "factor_cm":                               # column-major X and Q (native kernels when applicable)
