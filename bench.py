@@ -424,6 +424,13 @@ def run(args):
                            "peak_source": up["dmma_source"] + " (fp64-equivalent view of the exact int8 digits)",
                            "algorithmic": f"2*l*m*n = {flops:.4g} flop (Gaussian extract; the time includes "
                                           "the sparse sketch pass)", "traffic": None}
+    elif cfg["sketch"] == "srht" and k > 128:
+        # blocked fast Walsh-Hadamard transform (srht_fwht.cu): one read of X, 10 + k/1024 fp64 adds per element
+        byts = m_local * n * s_x
+        ach = byts / (per_ms["sketch"] * 1e-3) / 1e9
+        roofs["sketch"] = {"kernel": "srht_fwht_kernel", "bound": "hbm", "achieved": ach, "peak": hbm,
+                           "unit": "GB/s", "frac": ach / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                           "algorithmic": f"m*n*s_x = {byts:.4g} B per launch (one read of X)", "traffic": None}
     elif cfg["sketch"] in ("rademacher", "srht") and n > 64:
         flops = 2.0 * k * m_local * n
         ach = flops / (per_ms["sketch"] * 1e-3) / 1e12
@@ -442,10 +449,16 @@ def run(args):
     elif rr:
         # Alg. 7: column norms (one read of X), gather of the r kept columns, solve with r columns
         byts = m_local * n * s_x
-        ach = byts / (per_ms["reduce"] * 1e-3) / 1e9
-        roofs["colnorms"] = {"kernel": "colsq_kernel", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
-                             "frac": ach / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
-                             "algorithmic": f"m*n*s_x = {byts:.4g} B (one read of X)", "traffic": None}
+        if plan.last_path() & rcq.PATH_COLSQ_FUSED:
+            # D came out of the sketch's own pass over X: no separate kernel, nothing to rate
+            roofs["colnorms"] = {"kernel": "fused into the sketch pass (RCHOLQR_PATH_COLSQ_FUSED)", "bound": "hbm",
+                                 "achieved": None, "peak": hbm, "unit": "GB/s", "frac": None,
+                                 "algorithmic": "0 B (no second read of X)", "traffic": None}
+        else:
+            ach = byts / (max(per_ms["reduce"], 1e-6) * 1e-3) / 1e9
+            roofs["colnorms"] = {"kernel": "colsq_kernel", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                                 "frac": ach / hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs",
+                                 "algorithmic": f"m*n*s_x = {byts:.4g} B (one read of X)", "traffic": None}
         byts = 2.0 * m_local * r_rr * s_x
         ach = byts / (per_ms["tri_prep"] * 1e-3) / 1e9
         roofs["gather"] = {"kernel": "gather_x_kernel", "bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",

@@ -1033,6 +1033,7 @@ int32_t rcholqr_launches_per_factor(rcholqr_plan p, int64_t m) {
   const bool gauss_tc = p->sk.tc && 2.0 * p->d.k * (double)m * p->d.n >= gauss_tc_min_work();
   const bool tc_sketch = p->sk.sp_tc || (p->sk.kind < kSketchSparse && (gauss_tc || p->sk.rad_tc));
   int sketch_launches = (tc_sketch ? 2 : 1) + 1;
+  if (p->sk.fwht) sketch_launches = (p->d.k + 1023) / 1024 + 1;   // SRHT transform launches (no guarded fallback) + reduce
   if (tc_sketch && p->sk.kind < kSketchSparse && gauss_tc && m > 0) {   // pre-split: (column maxima + digit planes + sketch) per chunk
     const size_t cap = gauss_tcp_chunk_workspace(m, p->d.n, p->d.dtype, p->sk.tc_splits);
     int64_t chunk = m;

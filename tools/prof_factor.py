@@ -13,8 +13,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="C2")
 ap.add_argument("--iters", type=int, default=3)
 ap.add_argument("--m", type=int, default=0, help="override m (smaller runs)")
+ap.add_argument("--sketch", default="", help="another Theta on the same shape")
 a = ap.parse_args()
 cfg = synth.config(a.config)
+if a.sketch:
+    cfg["sketch"] = a.sketch
 m = a.m or cfg["m"]
 X = synth.make_X_torch(m, cfg["n"], cfg["log10_cond"], cfg["dtype"])
 plan = rcq.RCholQR(n=cfg["n"], k=cfg["k"], dtype=X.dtype, sketch=cfg["sketch"], nnz_per_col=cfg["nnz"])
