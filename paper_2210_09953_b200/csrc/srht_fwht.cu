@@ -15,7 +15,8 @@
 //
 // One CTA (256 threads) owns 8 columns and a contiguous range of blocks (grid = column tiles x row splits):
 //   * 32 TMA boxes (32 rows x 8 columns; out-of-range rows and columns arrive as zeros, also for the negative
-//     start row of a rank's first, partial block) fill a stage of a 2/3-deep ring;
+//     start row of a rank's first, partial block) fill a stage of a 2 (fp64) / 3 (fp32) deep ring, refilled as soon
+//     as pass 1 has read it;
 //   * pass 1: thread (c, L) holds rows 32 q + L, q = 0..31, of column c in registers, applies d and the
 //     radix-32 butterfly over q (row bits 5..9);  pass 2: thread (c, H) holds rows 32 H + q and transforms row
 //     bits 0..4.  Both passes read and write shared memory without bank conflicts (per 32-row group the row
@@ -43,10 +44,10 @@ constexpr int FW_KMAX = 1024;
 template <typename TX>
 struct FwCfg {
   static constexpr bool F64 = sizeof(TX) == 8;
-  static constexpr int GS_IN = F64 ? FW_GS : 32 * FW_CT;                // elements per 32-row group of a stage
-  static constexpr int STAGE_BYTES = 32 * GS_IN * (int)sizeof(TX);      // fp64 69632, fp32 32768
-  static constexpr int NST = 3;
-  static constexpr int Y_BYTES = F64 ? 0 : 32 * FW_GS * 8;              // fp32: separate fp64 work buffer
+  static constexpr int GS_IN = 32 * FW_CT;                              // elements per 32-row group of a stage (one TMA box)
+  static constexpr int STAGE_BYTES = 32 * GS_IN * (int)sizeof(TX);      // fp64 65536, fp32 32768
+  static constexpr int NST = F64 ? 2 : 3;                               // a stage is refilled right after pass 1 has read it
+  static constexpr int Y_BYTES = 32 * FW_GS * 8;                        // the fp64 work buffer of the block being transformed
   static constexpr size_t SMEM = (size_t)NST * STAGE_BYTES + Y_BYTES + FW_KMAX * 8 + 32 * 4 + NST * 8 + 256;
   static_assert(SMEM <= 232448, "shared memory");
 };
@@ -75,7 +76,7 @@ srht_fwht_kernel(const __grid_constant__ CUtensorMap xmap, const uint64_t* __res
   using Cf = FwCfg<TX>;
   extern __shared__ __align__(1024) unsigned char sm[];
   TX* stage = reinterpret_cast<TX*>(sm);                                                 // [NST][32][GS_IN]
-  double* ybuf = Cf::F64 ? nullptr : reinterpret_cast<double*>(sm + (size_t)Cf::NST * Cf::STAGE_BYTES);
+  double* y = reinterpret_cast<double*>(sm + (size_t)Cf::NST * Cf::STAGE_BYTES);
   uint64_t* s_sm = reinterpret_cast<uint64_t*>(sm + (size_t)Cf::NST * Cf::STAGE_BYTES + Cf::Y_BYTES);   // [FW_KMAX]
   uint32_t* dbits = reinterpret_cast<uint32_t*>(s_sm + FW_KMAX);                          // [32] bit q of word g: d of row 32 q + g
   uint64_t* full = reinterpret_cast<uint64_t*>(dbits + 32);                              // [NST]
@@ -86,7 +87,11 @@ srht_fwht_kernel(const __grid_constant__ CUtensorMap xmap, const uint64_t* __res
   const int64_t b_end = min(nblk, b_begin + blocks_per_split);
   const int nb = b_end > b_begin ? (int)(b_end - b_begin) : 0;
 
-  for (int r = tid; r < k; r += FW_T) s_sm[r] = srows[r0 + r];
+  // per sketch row: (sh_r << 16) | (offset of Y[sl_r] in 8-double units)
+  for (int r = tid; r < k; r += FW_T) {
+    const uint64_t sr = srows[r0 + r];
+    s_sm[r] = ((sr >> 10) << 16) | (uint64_t)(fw_phys((int)(sr & (FW_B - 1))) >> 3);
+  }
   if (tid == 0) {
     for (int s = 0; s < Cf::NST; ++s) tc::mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -104,9 +109,14 @@ srht_fwht_kernel(const __grid_constant__ CUtensorMap xmap, const uint64_t* __res
   if (warp == 0)
     for (int b = 0; b < Cf::NST && b < nb; ++b) load_block(b);
 
-  double acc[KU], accc[KU];
+  // fp64 X: TwoSum-compensated block sums (the DMMA sketch's "higher precision", reading A15); fp32 X: a plain
+  // fp64 chain already has u_f ~ 1e-13 << u_32 (same reading), so no compensation registers or adds
+  constexpr int KC_ = Cf::F64 ? KU : 1;
+  double acc[KU], accc[KC_];
 #pragma unroll
-  for (int u = 0; u < KU; ++u) { acc[u] = 0.0; accc[u] = 0.0; }
+  for (int u = 0; u < KU; ++u) acc[u] = 0.0;
+#pragma unroll
+  for (int u = 0; u < KC_; ++u) accc[u] = 0.0;
 
   for (int b = 0; b < nb; ++b) {
     const int s = b % Cf::NST;
@@ -133,12 +143,10 @@ srht_fwht_kernel(const __grid_constant__ CUtensorMap xmap, const uint64_t* __res
       }
     }
     fwht32(v);                                                            // row bits 5..9
-    double* y = Cf::F64 ? reinterpret_cast<double*>(stage + (size_t)s * 32 * Cf::GS_IN) : ybuf;
-    if (Cf::F64) __syncthreads();                                         // in place: every thread has read its inputs
 #pragma unroll
     for (int q = 0; q < 32; ++q) y[q * FW_GS + ((g ^ (q & 1)) << 3) + c] = v[q];   // row 32 q + g, swizzled
     __syncthreads();
-    if (!Cf::F64 && warp == 0 && b + Cf::NST < nb) load_block(b + Cf::NST);        // fp32: the stage is consumed
+    if (warp == 0 && b + Cf::NST < nb) load_block(b + Cf::NST);           // every thread has read the stage: refill it
 #pragma unroll
     for (int q = 0; q < 32; ++q) v[q] = y[g * FW_GS + ((q ^ (g & 1)) << 3) + c];  // row 32 g + q
     fwht32(v);                                                            // row bits 0..4
@@ -151,18 +159,17 @@ srht_fwht_kernel(const __grid_constant__ CUtensorMap xmap, const uint64_t* __res
       const int r = g + 32 * u;
       if (r < k) {
         const uint64_t sr = s_sm[r];
-        double yv = y[fw_phys((int)(sr & (FW_B - 1))) + c];
-        if (__popcll((sr >> 10) & (uint64_t)hb) & 1) yv = -yv;
-        const double t = acc[u] + yv;
-        const double bb = t - acc[u];
-        accc[u] += (acc[u] - (t - bb)) + (yv - bb);
-        acc[u] = t;
+        double yv = y[(((int)sr & 0xFFFF) << 3) + c];
+        if (__popcll((sr >> 16) & (uint64_t)hb) & 1) yv = -yv;
+        if constexpr (Cf::F64) {
+          const double t = acc[u] + yv;
+          const double bb = t - acc[u];
+          accc[u] += (acc[u] - (t - bb)) + (yv - bb);
+          acc[u] = t;
+        } else {
+          acc[u] += yv;
+        }
       }
-    }
-    if (Cf::F64) {
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");       // generic writes of y before the TMA refill
-      __syncthreads();                                                    // fp64: the stage (= y) is free now
-      if (warp == 0 && b + Cf::NST < nb) load_block(b + Cf::NST);
     }
   }
   const size_t kn = (size_t)k_total * n;
@@ -171,14 +178,14 @@ srht_fwht_kernel(const __grid_constant__ CUtensorMap xmap, const uint64_t* __res
     const int r = g + 32 * u;
     if (r < k && col0 + c < n) {
       part[blockIdx.y * kn + (size_t)(r0 + r) * n + col0 + c] = acc[u];
-      partc[blockIdx.y * kn + (size_t)(r0 + r) * n + col0 + c] = accc[u];
+      partc[blockIdx.y * kn + (size_t)(r0 + r) * n + col0 + c] = Cf::F64 ? accc[u % KC_] : 0.0;
     }
   }
 }
 
 // Measured on B200 (tools/ab_time.py --sketch srht, ms per sketch; dense = the +-1 E tile on tcgen05):
-//   C4 shape (fp32, n = 64, k = 128): transform 9.9, dense 5.0      C2 shape (fp32, n = 100, k = 200): 0.37 vs 0.41
-//   C3 shape (fp64, n = 256, k = 512): 17.4 vs 26.3
+//   C4 shape (fp32, n = 64, k = 128): transform 9.1, dense 4.9      C2 shape (fp32, n = 100, k = 200): 0.32 vs 0.41
+//   C3 shape (fp64, n = 256, k = 512): 13.9 vs 26.4                 C5 shape (fp64, n = 1024, k = 2048): 43.3 vs 1070
 // The transform's cost does not grow with k (10 + k / 1024 adds per element), the dense product's does, so the
 // transform serves k > 128 (more than one Theta tile of the dense kernel); RCHOLQR_SRHT_FWHT=1 / RCHOLQR_SRHT_DENSE=1
 // force one or the other.  k > 1024 runs one launch per 1024 sketch rows (the accumulators live in registers).
