@@ -343,9 +343,10 @@ E2E = [
     # name, m, n, k, dtype, sketch, log10 cond
     ("C1", 10_000, 20, 40, "f64", "gaussian", 3),
     ("C2-reduced", 262_144, 100, 200, "f32", "gaussian", 5),
-    ("C3-reduced", 65_536, 256, 512, "f64", "gaussian", 10),
+    ("C3-reduced", 32_768, 256, 512, "f64", "gaussian", 10),   # (the oracle is single-threaded below 65,536 rows: the row
+    # counts of the two fp64 cases keep the whole GPU suite well inside the driver's 20-minute limit)
     ("C4-reduced", 262_144, 64, 128, "f32", "sparse", 4),
-    ("C5-reduced", 12_288, 1024, 2048, "f64", "gaussian", 12),
+    ("C5-reduced", 6_144, 1024, 2048, "f64", "gaussian", 12),
 ]
 
 
