@@ -1,5 +1,6 @@
 #!/bin/bash
-D=gpurun_out/r3o; mkdir -p $D
+# SRHT suites + the transform-vs-dense sketch timings of profiles/srht_fwht_vs_dense_r2.jsonl (run under gpurun)
+D=gpurun_out/srht; mkdir -p $D
 python -c "import __graft_entry__ as g; g.build()" > $D/build.log 2>&1
 timeout 900 python -m pytest tests/test_gpu_srht_fwht.py tests/test_gpu_srht.py -q -p no:cacheprovider > $D/tests.txt 2>&1
 echo "pytest rc=$?" >> $D/tests.txt
