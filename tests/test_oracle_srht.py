@@ -90,3 +90,40 @@ def test_alg2_with_srht():
     TU = oracle.theta_dense(0, 64, X.shape[0], oracle.SRHT) @ U
     assert abs(oracle.cond(out["Q"]) / oracle.cond(TU) - 1) < 1e-3
     assert oracle.cond(out["Q"]) <= 8.0
+
+
+def test_blocked_walsh_hadamard_identity():
+    """The identity behind the GPU's fast transform (csrc/srht_fwht.cu; the SRHT costs
+    m n log2 m): with the global row i = B h + l and s_r = B sh_r + sl_r (B a power of two),
+    popcount(s_r & i) = popcount(sh_r & h) + popcount(sl_r & l), so
+        (Theta X)_r sqrt(k) = sum_h (-1)^popcount(sh_r & h) Y_h[sl_r],   Y_h = H_B (d .* X)[block h],
+    with blocks aligned to GLOBAL multiples of B (rows outside X are zero).  Checked in exact integer
+    arithmetic against the oracle's entry-by-entry signs, with a row offset inside a block, a ragged
+    last block and a Sylvester H_B built by Kronecker products (numpy only: no code of the CUDA path)."""
+    B, k, m, n, ro = 64, 24, 300, 5, 2**35 + 37          # ro mod B = 37: the first block is partial
+    rng = np.random.default_rng(5)
+    X = rng.integers(-1000, 1000, size=(m, n)).astype(np.int64)
+    S = oracle.theta_srht(3, k, m, ro).astype(np.int64)  # signs (-1)^popcount(s_r & i) d_i
+    want = S @ X
+    s = oracle.srht_rows(3, k)
+    H = np.array([[1]], dtype=np.int64)
+    while H.shape[0] < B:
+        H = np.kron(np.array([[1, 1], [1, -1]], dtype=np.int64), H)   # Sylvester: H[t, l] = (-1)^popcount(t & l)
+    # d_i from the oracle's own signs: row r of S is (-1)^popcount(s_r & i) d_i
+    i_glob = ro + np.arange(m, dtype=np.uint64)
+    par0 = np.array([bin(int(s[0] & i)).count("1") & 1 for i in i_glob])
+    d = S[0] * np.where(par0 == 1, -1, 1)
+    got = np.zeros((k, n), dtype=np.int64)
+    h0, h1 = ro // B, (ro + m - 1) // B
+    for h in range(h0, h1 + 1):
+        blk = np.zeros((B, n), dtype=np.int64)
+        for l in range(B):
+            i = h * B + l - ro                           # local row of global row B h + l
+            if 0 <= i < m:
+                blk[l] = d[i] * X[i]
+        Y = H @ blk                                      # the B-point Walsh-Hadamard transform of the block
+        for r in range(k):
+            sl, sh = int(s[r]) % B, int(s[r]) // B
+            sign = -1 if bin(sh & h).count("1") & 1 else 1
+            got[r] += sign * Y[sl]
+    assert np.array_equal(got, want)
