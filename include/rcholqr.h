@@ -115,7 +115,8 @@ rcholqr_status rcholqr_factor_host(rcholqr_plan plan, const void* X_host, int64_
  * the small QR and the other small steps to "not have much impact").  The first call with a given argument
  * tuple (X, m_local, row_offset, ldx, Q, ldq, R, S) runs the chain directly and captures it; every later call
  * with the SAME tuple replays the captured graph with one launch on `stream`.  A different tuple re-captures
- * (one graph is cached per plan).  The buffers' CONTENTS may change between calls, their addresses may not.
+ * (one graph is cached per plan), and so does a call made after another entry point regrew the plan's
+ * workspaces.  The buffers' CONTENTS may change between calls, their addresses may not.
  * Plans with an NCCL communicator, and plans with event timing enabled, launch directly (same results).
  * ASYNCHRONOUS like rcholqr_factor_async: numerical status through rcholqr_query_status. */
 rcholqr_status rcholqr_factor_graph(rcholqr_plan plan, const void* X, int64_t m_local, int64_t row_offset,

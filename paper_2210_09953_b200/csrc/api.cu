@@ -138,8 +138,12 @@ struct rcholqr_plan_s {
   struct GraphKey {
     const void* X = nullptr; int64_t m = -1, ro = 0, ldx = 0; void* Q = nullptr; int64_t ldq = 0;
     double* R = nullptr; double* S = nullptr;
+    // the plan's lazily grown workspaces the chain reads (a later, larger call frees and reallocates them:
+    // a graph captured before that must not be replayed)
+    const void* xdig = nullptr; const void* tbuf = nullptr;
     bool operator==(const GraphKey& o) const {
-      return X == o.X && m == o.m && ro == o.ro && ldx == o.ldx && Q == o.Q && ldq == o.ldq && R == o.R && S == o.S;
+      return X == o.X && m == o.m && ro == o.ro && ldx == o.ldx && Q == o.Q && ldq == o.ldq && R == o.R && S == o.S &&
+             xdig == o.xdig && tbuf == o.tbuf;
     }
   } gkey;
   cudaGraphExec_t gexec = nullptr;
@@ -495,6 +499,7 @@ rcholqr_status rcholqr_factor_graph(rcholqr_plan p, const void* X, int64_t m, in
   cudaStream_t st = (cudaStream_t)stream;
   rcholqr_plan_s::GraphKey key;
   key.X = X; key.m = m; key.ro = ro; key.ldx = ldx; key.Q = Q; key.ldq = ldq; key.R = R; key.S = S;
+  key.xdig = p->xdig; key.tbuf = p->tbuf;
   if (p->gexec && key == p->gkey) {
     p->path = p->gpath;
     CU(cudaGraphLaunch(p->gexec, st));
@@ -514,6 +519,7 @@ rcholqr_status rcholqr_factor_graph(rcholqr_plan p, const void* X, int64_t m, in
   const cudaError_t ce = cudaStreamEndCapture(p->gstream, &g);
   p->path = path;
   if (cs == RCHOLQR_OK && ce == cudaSuccess && g && cudaGraphInstantiate(&p->gexec, g, 0) == cudaSuccess) {
+    key.xdig = p->xdig; key.tbuf = p->tbuf;      // as the direct run above left them
     p->gkey = key;
     p->gpath = path;
   } else {

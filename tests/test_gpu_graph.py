@@ -56,3 +56,25 @@ def test_graph_status(cuda):
     with pytest.raises(rcq.RCholQRError) as e:
         plan.factor(X, Q=Q, R=R, graph=True)
     assert e.value.status == rcq.E_NONFINITE
+
+
+def test_graph_survives_workspace_regrowth(cuda):
+    """A larger plain call regrows the plan's lazily sized workspaces (the pre-split digit buffer, the streamed
+    solve's T buffer): a graph captured before that holds freed pointers and must be re-captured, not replayed."""
+    for n, k, dt in ((100, 200, torch.float32), (300, 600, torch.float64)):
+        f = "f64" if dt == torch.float64 else "f32"
+        Xs = torch.from_numpy(synth.make_X(30_000, n, 3.0, f)).cuda()
+        Xl = torch.from_numpy(synth.make_X(90_000, n, 3.0, f, seed=3)).cuda()
+        plan = rcq.RCholQR(n=n, k=k, dtype=dt)
+        Q0, R0, _ = plan.factor(Xs)
+        Q, R = torch.empty_like(Q0), torch.empty_like(R0)
+        plan.factor(Xs, Q=Q, R=R, graph=True)
+        plan.factor(Xs, Q=Q, R=R, graph=True)                # replay
+        Ql, Rl, _ = plan.factor(Xl)                           # three times the rows: workspaces regrown
+        Q.fill_(0); R.fill_(0)
+        plan.factor(Xs, Q=Q, R=R, graph=True)
+        assert torch.equal(Q, Q0) and torch.equal(R, R0)
+        plan.factor(Xs, Q=Q, R=R, graph=True)
+        assert torch.equal(Q, Q0) and torch.equal(R, R0)
+        Q2, R2, _ = plan.factor(Xl)
+        assert torch.equal(Q2, Ql) and torch.equal(R2, Rl)
