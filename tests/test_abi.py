@@ -93,3 +93,25 @@ def test_binding_fails_loudly_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(RuntimeError):
         rcq.RCholQR(n=4, k=8)
+
+
+def test_header_is_plain_c_and_the_c_example_links(lib, tmp_path):
+    """include/rcholqr.h compiles as C99 with no CUDA or C++ headers, and examples/factor_host.c links against the
+    in-tree library (the program itself needs a GPU: tests/test_gpu_c_example.py runs it)."""
+    probe = tmp_path / "probe.c"
+    probe.write_text('#include "rcholqr.h"\nint main(void) { rcholqr_desc d = {1, 2, RCHOLQR_F64, RCHOLQR_GAUSSIAN, 8, 0, 0, 0}; '
+                     'return (int)sizeof(d) == 0; }\n')
+    subprocess.run(["gcc", "-std=c99", "-pedantic", "-Werror", "-I" + os.path.join(ROOT, "include"), "-fsyntax-only",
+                    str(probe)], check=True)
+    libdir = os.path.dirname(rbuild.LIB)
+    subprocess.run(["gcc", "-O1", "-Wall", "-Werror", "-I" + os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "examples", "factor_host.c"), "-L" + libdir, "-lrcholqr", "-Wl,-rpath," + libdir,
+                    "-lm", "-o", str(tmp_path / "factor_host")], check=True)
+
+
+def test_tcgen05_and_tma_in_sass(lib):
+    """The tensor-core paths are Blackwell-native: tcgen05 MMAs (UTCIMMA), TMEM loads (LDTM) and TMA tensor loads /
+    stores (UTMALDG / UTMASTG) are in the library's SASS."""
+    sass = subprocess.check_output(["cuobjdump", "-sass", rbuild.LIB], text=True)
+    for mnemonic in ("UTCIMMA", "LDTM", "UTMALDG", "UTMASTG"):
+        assert mnemonic in sass, mnemonic
