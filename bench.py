@@ -232,6 +232,16 @@ def run_reference(args):
     return 0
 
 
+def _path_names(rcq, bits: int) -> dict:
+    """rcholqr_last_path of the timed loop's last step, decoded: which kernels served the factorization."""
+    names = [("sketch_tcgen05", rcq.PATH_SKETCH_TC), ("sketch_presplit_digits", rcq.PATH_SKETCH_PRESPLIT),
+             ("sketch_cuda_core_or_dmma", rcq.PATH_SKETCH_CUDA_CORE), ("sketch_overflow_fallback", rcq.PATH_SKETCH_FALLBACK),
+             ("solve_tcgen05", rcq.PATH_SOLVE_TC), ("solve_dmma", rcq.PATH_SOLVE_DMMA),
+             ("colnorms_fused", rcq.PATH_COLSQ_FUSED), ("colmajor_native", rcq.PATH_COLMAJOR_NATIVE),
+             ("sketch_srht_fwht", rcq.PATH_SKETCH_FWHT)]
+    return {"bits": bits, "kernels": [n for n, b in names if bits & b]}
+
+
 def _config_dict(name: str, cfg: dict, m_global: int, s_x: int) -> dict:
     """The workload description both arms print (identical keys and values for the same workload, so
     the driver can match the reference arm's line to ours)."""
@@ -347,6 +357,7 @@ def run(args):
     st = plan.query_status()
     if st != rcq.OK:
         raise rcq.RCholQRError(st, "timed factor")
+    path_bits = plan.last_path()
     t = torch.tensor([ms_local], dtype=torch.float64, device=dev)
     if ws > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -532,7 +543,7 @@ def run(args):
             "partition": {"m_local": m_local, "row_offset": ro, "parallelism": f"row-partition x{ws}, 1 all-reduce"},
             "per_kernel_ms": per_ms, "roofline": roof, "kernel_rooflines": roofs, "northstar_roofline": ns,
             "gpu_launches": plan.launches_per_factor(m_local) * args.steps,
-            "clocks": clk.summary(), "e2e": e2e, "cuda_graph": use_graph}
+            "clocks": clk.summary(), "e2e": e2e, "cuda_graph": use_graph, "path": _path_names(rcq, path_bits)}
 
     if args.algo == "rcholqr2":
         # split Alg. 3's own steps by differences of device-timed calls on the same stream:
